@@ -1,0 +1,132 @@
+"""Generate golden fixtures by running the LIVE reference (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The reference (``/root/reference/pkg/src/polartraces``) is importable here but
+does not exist on the GPU box, so its outputs are committed as small ``.npz``
+fixtures.  Inputs come from ``paper_1510_01831_b200.configs`` so both sides see
+identical problems.  Recorded per case: wavefield (full for the small cases,
+every 4th node for config 1), outer GMRES iteration count and residual
+history, true relative residual, the inner ``TouchCounter`` total, and the
+per-layer-solve inner GMRES iteration counts (via a wrapper around
+``nested.krylov.gmres``).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import polartraces as pt  # noqa: E402
+from polartraces import krylov as ref_krylov  # noqa: E402
+from polartraces import nested as ref_nested  # noqa: E402
+
+from paper_1510_01831_b200.configs import make_config, small_problem  # noqa: E402
+
+_INNER = []
+_orig_gmres = ref_krylov.gmres
+
+
+_STATE = {"in_solve": False, "depth": 0}
+_orig_solve = ref_krylov.solve
+
+
+def _counting_gmres(*a, **kw):
+    # record every gmres call except the outer one (the call krylov.solve
+    # makes at depth 1, sie.py:419); inner calls come from nested.py:147
+    _STATE["depth"] += 1
+    try:
+        res = _orig_gmres(*a, **kw)
+    finally:
+        _STATE["depth"] -= 1
+    if not (_STATE["in_solve"] and _STATE["depth"] == 0):
+        _INNER.append(res.iterations)
+    return res
+
+
+def _outer_solve(*a, **kw):
+    _STATE["in_solve"] = True
+    try:
+        return _orig_solve(*a, **kw)
+    finally:
+        _STATE["in_solve"] = False
+
+
+ref_krylov.gmres = _counting_gmres
+ref_krylov.solve = _outer_solve
+
+
+def ref_solver(prob, nested=True):
+    g = prob.grid
+    grid = pt.Grid(g.nx, g.nz, g.h, g.npml)
+    model = pt.VelocityModel(grid, prob.model.c)
+    pml = pt.PmlProfile(g.npml, g.h, prob.pml.C, prob.pml.omega)
+    part = pt.LayerPartition(tuple(prob.partition.extents))
+    layers = None
+    if nested:
+        layers = pt.build_nested_layers(grid, model, pml, part, Lc=prob.Lc, backend="pt",
+                                        inner_ktol=prob.inner_ktol)
+    return pt.PolarizedTracesSolver(grid, model, pml, part, layers=layers)
+
+
+def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1):
+    t0 = time.time()
+    s = ref_solver(prob, nested)
+    t1 = time.time()
+    f = prob.rhs([src_idx])[0]
+    _INNER.clear()
+    for lay in s.layers:
+        if hasattr(lay, "counter"):
+            lay.counter.reset()
+    res = s.solve(f, pt.KrylovConfig(ktol=ktol, max_iter=200))
+    t2 = time.time()
+    touches = sum(lay.counter.total for lay in s.layers if hasattr(lay, "counter"))
+    u = res.u if full_u else res.u[::decim, ::decim]
+    out = dict(
+        u=u,
+        decim=decim,
+        unorm=np.linalg.norm(res.u),
+        iterations=res.iterations,
+        residuals=np.array(res.residuals),
+        relres=res.relative_residual,
+        touches=touches,
+        inner_iterations=np.array(_INNER, dtype=float),
+        source=np.array(prob.sources[src_idx]),
+        ktol=ktol,
+        nested=nested,
+        offline_s=t1 - t0,
+        online_s=t2 - t1,
+    )
+    print(f"{prob.name} src{src_idx} nested={nested}: its={res.iterations} "
+          f"res={res.residuals} relres={res.relative_residual:.3e} touches={touches} "
+          f"inner={len(_INNER)} offline={t1 - t0:.2f}s online={t2 - t1:.2f}s")
+    return out
+
+
+def main():
+    cases = {
+        "small_a": (small_problem(nx=40, nz=36, npml=6, L=3, Lc=2, omega=14.0, seed=0), 0, True),
+        "small_b": (small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, True),
+        "small_c": (small_problem(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7), 0, True),
+        "small_direct": (small_problem(nx=40, nz=36, npml=6, L=3, Lc=2, omega=14.0, seed=0), 0,
+                         False),
+    }
+    for name, (prob, si, nested) in cases.items():
+        out = run_case(prob, si, nested=nested)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    for name, decim in (("cfg1", 4), ("cfg2", 8)):
+        prob = make_config(name)
+        out = run_case(prob, 0, full_u=False, decim=decim)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+
+
+if __name__ == "__main__":
+    main()
