@@ -1,0 +1,117 @@
+/*
+ * pt_b200.h -- C ABI of the B200-native online stage of the nested
+ * polarized-traces Helmholtz solver (libpt_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types cross this boundary.
+ * Complex numbers are interleaved (re, im) doubles, i.e. numpy complex128 /
+ * C99 double _Complex / CUDA double2.
+ *
+ * What each entry point replaces in the reference
+ * (/root/reference/pkg/src/polartraces):
+ *
+ *   pt_create       build_nested_layers(..., backend="pt") + PolarizedTracesSolver.__init__
+ *                   (nested.py:507-521, sie.py:368-381): the offline factors computed by the
+ *                   host (paper_1510_01831_b200/offline.py) are uploaded once.
+ *   pt_solve        PolarizedTracesSolver.solve (sie.py:392-439) for nrhs sources at once,
+ *                   host buffers in and out (the call a ctypes/cffi binding makes).
+ *   pt_solve_device the same with device-resident f/u (e.g. torch CUDA tensors).
+ *   pt_layer_solve  NestedLayerSolver.solve (nested.py:344-353), one layer, nrhs volumes:
+ *                   the "layer object" protocol of sie.py:112-118 (test/plugin hook).
+ *   pt_cell_solve   LayerWorkspace.solve on one cell (subdomain.py:214-221 -> SuperLU
+ *                   solve): the K1 kernel alone (test hook).
+ *   pt_destroy / pt_last_error / pt_version.
+ *
+ * Return codes (errors map to the reference's exceptions, sie.py:420-425,
+ * nested.py:148-152, krylov.py:101-123, subdomain.py:219-220):
+ *   PT_OK 0, PT_NOT_CONVERGED 1 (KrylovBreakdown: outer did not reach ktol),
+ *   PT_INNER_NOT_CONVERGED 2 (InnerSolveError), PT_BREAKDOWN 3 (KrylovBreakdown:
+ *   zero Hessenberg column / happy breakdown before convergence), PT_BAD_ARGUMENT 4
+ *   (ValueError), PT_CAPACITY 5 (a Krylov basis outgrew its preallocated capacity),
+ *   PT_CUDA_ERROR -1 (see pt_last_error).
+ */
+#ifndef PT_B200_H
+#define PT_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PT_OK 0
+#define PT_NOT_CONVERGED 1
+#define PT_INNER_NOT_CONVERGED 2
+#define PT_BREAKDOWN 3
+#define PT_BAD_ARGUMENT 4
+#define PT_CAPACITY 5
+#define PT_CUDA_ERROR (-1)
+
+typedef struct pt_ctx pt_ctx;
+
+/* Problem geometry and offline factors.  All arrays may be host or device
+ * pointers (copied with cudaMemcpyDefault); the caller keeps ownership. */
+typedef struct {
+  int nx, nz, npml;          /* interior nodes and PML width (Grid, discretization.py:58-71) */
+  int L, Lc;                 /* layers and cells per layer */
+  double h, omega;
+  const int* layer_extents;  /* [L]  partition_layers extents (subdomain.py:93-100) */
+  const int* cell_extents;   /* [Lc] swapped-frame cell extents (nested.py:294-296) */
+  /* global 5-point operator for the true residual (sie.py:441-445) */
+  const double* tx;          /* [3][wx] complex: lower, main, upper of T_x */
+  const double* tz;          /* [3][wz] complex: lower, main, upper of T_z */
+  const double* m;           /* [wz][wx] real squared slowness */
+  /* layer-level slot sources (subdomain.py:157-182): coefficient of v0,v1,vn,vnp */
+  const double* layer_coefs; /* [L][4] complex */
+  /* per cell, layer-major (id = l*Lc + c) */
+  const double* cell_coefs;  /* [L*Lc][4] complex, cell-level slot coefficients */
+  const double* const* lz;   /* [L*Lc] -> [wz_c] complex block sub-diagonal scalars  */
+  const double* const* uz;   /* [L*Lc] -> [wz_c] complex block super-diagonal scalars */
+  const double* const* sinv; /* [L*Lc] -> [wz_c][w][w] complex Schur inverses, column-major blocks */
+  const double* const* green;/* [L*Lc] -> [4 rows][4 slots][w][w] complex, column-major blocks */
+} pt_problem;
+
+typedef struct {
+  double ktol;           /* outer relative preconditioned residual (KrylovConfig.ktol) */
+  int max_iter;          /* KrylovConfig.max_iter */
+  int restart;           /* KrylovConfig.restart (0 = none) */
+  double inner_ktol;     /* NestedLayerSolver inner_ktol (1e-6) */
+  int inner_max_iter;    /* NestedLayerSolver inner_max_iter (200) */
+  int precond;           /* 0 = "gs", 1 = "jac" (sie.py:407) */
+} pt_krylov;
+
+typedef struct {
+  /* all optional (NULL = not requested); sized by the caller */
+  double* iterations;    /* [nrhs] outer GMRES iterations (float, krylov.py:135) */
+  double* residuals;     /* [nrhs][max_iter] residual history (relative preconditioned) */
+  int* n_residuals;      /* [nrhs] entries written per rhs */
+  double* relres;        /* [nrhs] ||H u - f|| / ||f|| */
+  int* converged;        /* [nrhs] */
+  double* traces;        /* [nrhs][nI][2][wx] complex reassembled traces (down + up) */
+  double* polarized;     /* [nrhs][4*nI*wx] complex polarized solution */
+  long long* layer_solves;   /* [1] number of layer-solve instances executed */
+  long long* inner_iters;    /* [1] sum of inner GMRES iterations over all instances */
+  long long* touches;        /* [1] inner Green-block element touches (TouchCounter.total) */
+  int* inner_hist;           /* [inner_hist_len] histogram of inner iteration counts */
+  int inner_hist_len;
+  double* timing_ms;         /* [1] device time of the online solve (CUDA events) */
+} pt_stats;
+
+int pt_create(const pt_problem* prob, int device, pt_ctx** out);
+int pt_destroy(pt_ctx* ctx);
+
+int pt_solve(pt_ctx* ctx, const double* f, int nrhs, const pt_krylov* cfg, double* u,
+             pt_stats* stats);
+int pt_solve_device(pt_ctx* ctx, const double* f_dev, int nrhs, const pt_krylov* cfg,
+                    double* u_dev, pt_stats* stats);
+
+/* layer ell (0-based): u_l = (H_l)^{-1} rhs for nrhs slabs [nrhs][n_l+2npml][wx] (host) */
+int pt_layer_solve(pt_ctx* ctx, int layer, const double* rhs, int nrhs, double inner_ktol,
+                   int inner_max_iter, double* out, pt_stats* stats);
+/* cell (layer, c): x = H_c^{-1} b for nrhs right-hand sides [nrhs][wz_c][w] (host) */
+int pt_cell_solve(pt_ctx* ctx, int layer, int cell, const double* b, int nrhs, double* x);
+
+const char* pt_last_error(void);
+const char* pt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PT_B200_H */

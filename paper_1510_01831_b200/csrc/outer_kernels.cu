@@ -1,0 +1,196 @@
+// Outer-level kernels: equivalent-source panel gather, sample combination,
+// polarized-vector algebra, fused MGS Arnoldi, and the true residual (K5).
+//
+// Outer vectors are RHS-major: element e of RHS r of view V lives at
+// V.p[r * V.stride + e]; panels (segments) are wx long.  Stage kernels run on
+// the compacted list of still-active RHS (rmap), so converged right-hand sides
+// cost nothing and never feed garbage into an inner solve.
+#include "pt_device.cuh"
+
+#include "pt_launch.cuh"
+
+
+__device__ __forceinline__ double2 vref(const VecTab& t, Ref rf, int r, int x, int wx) {
+  return ld_cg(t.v[rf.vec].p + (size_t)r * t.v[rf.vec].stride + (size_t)rf.seg * wx + x);
+}
+
+// P[job][s][q][x] = sum of the slot's refs (sie.py:203-308 panel expressions)
+__global__ void k_gather_panels(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
+                                double2* P) {
+  const long long total = (long long)njobs * 4 * nq * wx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(e % wx);
+    long long rest = e / wx;
+    const int q = (int)(rest % nq);
+    rest /= nq;
+    const int s = (int)(rest % 4);
+    const int j = (int)(rest / 4);
+    const Ref* pr = jobs[j].pan[s];
+    if (pr[0].vec < 0) continue;
+    const int r = rmap[q];
+    double2 v = vref(t, pr[0], r, x, wx);
+    if (pr[1].vec >= 0) v = cadd(v, vref(t, pr[1], r, x, wx));
+    P[e] = v;
+  }
+}
+
+// dst = scoef*sample + add - (sub0 + sub1)
+__global__ void k_combine(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
+                          const double2* smp) {
+  const long long total = (long long)njobs * 4 * nq * wx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(e % wx);
+    long long rest = e / wx;
+    const int q = (int)(rest % nq);
+    rest /= nq;
+    const int o = (int)(rest % 4);
+    const int j = (int)(rest / 4);
+    const OJob& jb = jobs[j];
+    if (o >= jb.nout) continue;
+    const int r = rmap[q];
+    double2 y = cscale(smp[e], jb.scoef[o]);
+    if (jb.add[o].vec >= 0) y = cadd(y, vref(t, jb.add[o], r, x, wx));
+    if (jb.sub[o][0].vec >= 0) {
+      double2 sb = vref(t, jb.sub[o][0], r, x, wx);
+      if (jb.sub[o][1].vec >= 0) sb = cadd(sb, vref(t, jb.sub[o][1], r, x, wx));
+      y = csub(y, sb);
+    }
+    const VecView& dv = t.v[jb.dst[o].vec];
+    dv.p[(size_t)r * dv.stride + (size_t)jb.dst[o].seg * wx + x] = y;
+  }
+}
+
+// dst[seg..] = a*x[seg..] (+ b*y[seg..]) over len elements, for the active RHS
+__global__ void k_lincomb(VecView dst, long long doff, VecView xv, long long xoff, double a, VecView yv,
+                          long long yoff, double b, int use_y, long long len, const int* rmap, int nq) {
+  const long long total = len * nq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / len);
+    const long long i = e - (long long)q * len;
+    const int r = rmap[q];
+    double2 v = cscale(ld_cg(xv.p + r * xv.stride + xoff + i), a);
+    if (use_y) v = cadd(v, cscale(ld_cg(yv.p + r * yv.stride + yoff + i), b));
+    dst.p[r * dst.stride + doff + i] = v;
+  }
+}
+
+// squared norms per active RHS: out[r] = sum |v|^2 (one CTA per RHS)
+__global__ void k_norm2(VecView v, long long len, const int* rmap, double* out) {
+  __shared__ double red[32];
+  const int r = rmap[blockIdx.x];
+  const double2* p = v.p + r * v.stride;
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < len; i += blockDim.x) {
+    const double2 a = p[i];
+    s += a.x * a.x + a.y * a.y;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[r] = s;
+}
+
+// dst = src / scale[r] (scale on device)
+__global__ void k_scale_div(VecView dst, VecView src, long long len, const int* rmap, int nq,
+                            const double* scale) {
+  const long long total = len * nq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / len);
+    const long long i = e - (long long)q * len;
+    const int r = rmap[q];
+    const double s = scale[r];
+    const double2 a = src.p[r * src.stride + i];
+    dst.p[r * dst.stride + i] = make_double2(a.x / s, a.y / s);
+  }
+}
+
+// Fused MGS (krylov.py:89-94) for one RHS per CTA: for i = 0..j
+//   h_i = vdot(V_i, w); w -= h_i V_i;   then hn = ||w||.
+// V: [r][cap+1][n]; w is V_{j+1}.  hout[r][0..j] = h, hout[r][j+1] = hn.
+__global__ void k_arnoldi(double2* V, long long vstride, long long n, int j, const int* rmap, double2* hout,
+                          int hld) {
+  __shared__ double red[32];
+  const int r = rmap[blockIdx.x];
+  double2* base = V + r * vstride;
+  double2* w = base + (long long)(j + 1) * n;
+  for (int i = 0; i <= j; ++i) {
+    const double2* vi = base + (long long)i * n;
+    double sr = 0.0, si = 0.0;
+    for (long long e = threadIdx.x; e < n; e += blockDim.x) {
+      const double2 c = cconjmul(vi[e], w[e]);
+      sr += c.x;
+      si += c.y;
+    }
+    sr = block_sum(sr, red);
+    si = block_sum(si, red);
+    const double2 h = make_double2(sr, si);
+    for (long long e = threadIdx.x; e < n; e += blockDim.x) w[e] = csub(w[e], cmul(h, vi[e]));
+    if (threadIdx.x == 0) hout[(size_t)r * hld + i] = h;
+    __syncthreads();
+  }
+  double s = 0.0;
+  for (long long e = threadIdx.x; e < n; e += blockDim.x) s += w[e].x * w[e].x + w[e].y * w[e].y;
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) hout[(size_t)r * hld + j + 1] = make_double2(sqrt(s), 0.0);
+}
+
+// x[r] += sum_i y[r][i] V[r][i]   (krylov.py:128-131)
+__global__ void k_accum_x(VecView x, const double2* V, long long vstride, long long n, const double2* y,
+                          int yld, int k, const int* rmap, int nq) {
+  const long long total = n * nq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / n);
+    const long long i = e - (long long)q * n;
+    const int r = rmap[q];
+    double2 acc = czero();
+    for (int l = 0; l < k; ++l) cfma(acc, V[r * vstride + (long long)l * n + i], y[(size_t)r * yld + l]);
+    double2* xp = x.p + r * x.stride + i;
+    *xp = cadd(*xp, acc);
+  }
+}
+
+// K5: ||H u - f||^2 and ||f||^2 per RHS (sie.py:441-445), 5-point PML stencil
+__global__ void k_residual(const double2* u, const double2* f, long long stride, int wz, int wx, const double2* tx,
+                           const double2* tz, const double* m, double omega2, const int* rmap, double* out) {
+  __shared__ double red[32];
+  const int r = rmap[blockIdx.y];
+  const double2* ur = u + r * stride;
+  const double2* fr = f + r * stride;
+  double rr = 0.0, ff = 0.0;
+  const long long N = (long long)wz * wx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / wx), pcol = (int)(e % wx);
+    // diag = (Tx_main + Tz_main) - omega^2 m
+    const double2 dg = csub(cadd(tx[wx + pcol], tz[wz + q]), make_double2(omega2 * m[e], 0.0));
+    double2 a = cmul(dg, ur[e]);
+    if (pcol > 0) a = cadd(a, cmul(tx[pcol], ur[e - 1]));
+    if (pcol < wx - 1) a = cadd(a, cmul(tx[2 * wx + pcol], ur[e + 1]));
+    if (q > 0) a = cadd(a, cmul(tz[q], ur[e - wx]));
+    if (q < wz - 1) a = cadd(a, cmul(tz[2 * wz + q], ur[e + wx]));
+    const double2 d = csub(a, fr[e]);
+    rr += d.x * d.x + d.y * d.y;
+    ff += fr[e].x * fr[e].x + fr[e].y * fr[e].y;
+  }
+  rr = block_sum(rr, red);
+  ff = block_sum(ff, red);
+  if (threadIdx.x == 0) {
+    atomicAdd(out + 2 * r, rr);
+    atomicAdd(out + 2 * r + 1, ff);
+  }
+}
+
+// full-volume norms ||f||^2 per RHS (zero-source detection, sie.py:397-399)
+__global__ void k_vol_norm2(const double2* f, long long stride, long long N, double* out) {
+  __shared__ double red[32];
+  const int r = blockIdx.y;
+  double s = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x) {
+    const double2 a = f[r * stride + e];
+    s += a.x * a.x + a.y * a.y;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) atomicAdd(out + r, s);
+}

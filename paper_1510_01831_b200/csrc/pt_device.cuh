@@ -1,0 +1,143 @@
+// Device-side data model and PTX helpers shared by the B200 kernels.
+//
+// Data layout in HBM:
+//   * complex128 everywhere as interleaved double2;
+//   * Schur inverses S_k^{-1} of a cell: [wz_c][w][w], each block COLUMN-major
+//     (element (i,j) at j*w+i) so a CTA streams whole column panels with one
+//     1-D bulk copy (cp.async.bulk -> UBLKCP) and thread i reads row i;
+//   * Green blocks of a cell: [4 rows r0,r1,rn,rnp][4 slots v0,v1,vn,vnp][w][w], column-major;
+//   * outer polarized vectors per RHS: [down(nI,2,wx) | up(nI,2,wx)] exactly like
+//     PolarizedTraceStack.flat (sie.py:102-103), RHS-major with a per-RHS stride;
+//   * inner vectors identical with (Lc-1, 2, w).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PT_MAX_LC 64
+#define PT_THREADS 256
+
+// ---------------------------------------------------------------- geometry
+
+struct LayerInfo {
+  int n, off, w, lo, hi;  // interior rows, interior offset, width (= n + 2 npml), kept rows [lo,hi)
+  int has_top, has_bot;
+  int prow[4];            // layer rows of slot sources v0,v1,vn,vnp: row(1), row(0), row(n+1), row(n)
+  double2 coef[4];        // slot coefficients (subdomain.py:157-182)
+};
+
+struct CellInfo {
+  int layer, cell, w, wzc, nxc, off, lo, hi;  // cell c of layer: block rows [0,wzc), kept [lo,hi)
+  int has_top, has_bot;
+  int krow[4];            // block rows of cell slot sources v0,v1,vn,vnp
+  int srow[4];            // sampled block rows r0,r1,rn,rnp
+  double2 coef[4];        // cell-level slot coefficients
+  long long sinv_off;     // double2 offset into the Schur-inverse pool
+  long long green_off;    // double2 offset into the Green-block pool
+  long long lz_off;       // offset into lz/uz pools
+};
+
+// A reference to one panel (segment) of a vector: vec < 0 = absent.
+struct Ref {
+  int vec, seg;
+};
+
+// One outer layer-solve job (a boundary_samples / newton_samples / reconstruct call).
+struct OJob {
+  int layer;
+  int vol;           // add the split global source f_l (sie.py:134-151)
+  int vfull;         // volume source/output is a full layer slab (no split mask), slab-local rows
+  Ref pan[4][2];     // slot panels v0,v1,vn,vnp, each a sum of up to two refs
+  int nout;          // sampled layer rows (<=4); -1 = full-volume output (reconstruct)
+  int orow[4];       // layer local depths of the sampled rows
+  double scoef[4];   // out = scoef*sample + add - (sub0 + sub1)
+  Ref dst[4], add[4], sub[4][2];
+};
+
+// One inner item: output panel = sum_slot G[cell][row][slot] @ panel_slot + add - (sub0+sub1).
+struct IItem {
+  int cell, row;     // cell < 0: no Green product (pure combination)
+  Ref pan[4][2];
+  Ref dst, add, sub[2];
+};
+
+// K1 task: one cell, a contiguous range of columns (job, rhs) of its layer.
+struct K1Task {
+  int cell;          // global cell id (layer-major)
+  int jb;            // index into the stage's per-layer job list
+  int q0, nq;        // columns [q0, q0+nq) of the layer column space (job-major, R per job)
+  long long zoff;    // double2 offset of this task's forward-sweep scratch
+};
+
+// ---------------------------------------------------------------- complex helpers
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// acc += a*b
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// conj(a)*b
+__device__ __forceinline__ double2 cconjmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+
+// coherent (L2) load for data produced earlier in the same kernel by other CTAs/threads
+__device__ __forceinline__ double2 ld_cg(const double2* p) { return __ldcg(p); }
+
+// ---------------------------------------------------------------- mbarrier + bulk copy (TMA)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared, completion counted on an mbarrier (SASS UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------- reductions
+
+// block-wide sum of one double (all threads get the result); red: >= 32 doubles of smem
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  const int nw = (blockDim.x + 31) >> 5;
+  for (int i = 0; i < nw; ++i) s += red[i];  // fixed order: deterministic
+  return s;
+}

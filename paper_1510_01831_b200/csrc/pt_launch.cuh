@@ -1,0 +1,87 @@
+// Kernel parameter blocks and launchers shared by the kernels and the host
+// orchestration (solver.cu).
+#pragma once
+#include "pt_device.cuh"
+
+#define INNER_NC 8
+#define PT_HIST 64
+
+struct VecView {
+  double2* p;
+  long long stride;
+};
+struct VecTab {
+  VecView v[3];  // 0 IN, 1 OUT, 2 AUX
+};
+
+struct K1Params {
+  const CellInfo* cells;
+  const LayerInfo* layers;
+  const OJob* jobs;
+  const int* ljobs;
+  const K1Task* tasks;
+  const double2* sinv;
+  const double2* lz;
+  const double2* uz;
+  int R, pass, npml, wx, Lc, wmax;
+  int slot_bytes, ns;
+  const double2* f;
+  long long f_stride;
+  const double2* P;   // [job][4][R][wx]
+  const double2* tr;  // [job][R][Lc-1][2][wmax]
+  double2* tables;    // [job][Lc][4][R][wmax]
+  double2* smp;       // [job][4][R][wx]
+  double2* u;
+  long long u_stride;
+  double2* Z;
+  const double2* bd;  // pass 2 (dense test mode): b [q][wzc][w]
+  double2* xd;        // pass 2: x [q][wzc][w]
+};
+
+struct InnerParams {
+  const CellInfo* cells;
+  const LayerInfo* layers;
+  const OJob* jobs;
+  const int* stage_jobs;  // job id per CTA
+  const double2* green;
+  const IItem* items;
+  const int* op_ph;       // phase begin offsets into items (op_nph + 1 entries)
+  int op_nph;
+  const int* pre_ph;
+  int pre_nph;
+  int R, Lc, wmax, cap, max_iter;
+  double ktol;
+  const double2* tables;  // [job][Lc][4][R][wmax]
+  double2* tr;            // [job][R][Lc-1][2][wmax]
+  double2* scratch;       // per (job, r): (cap + 5) vectors of nmax
+  long long inst_stride, nmax;
+  double2* hess;
+  long long hstride;
+  int* iters;             // [job][R] inner iterations (-1 = error)
+  int* err;               // PT_* code (atomicMax)
+  unsigned long long* counters;  // [0] inner iterations, [1] Green touches, [2] instances
+  int* hist;              // [PT_HIST] histogram of inner iteration counts
+  long long op_blocks, pre_blocks;  // block matvecs per inner op / preconditioner application
+};
+
+size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns);
+cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStream_t st);
+size_t inner_smem_bytes(int wmax, int R);
+cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
+
+__global__ void k_gather_panels(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
+                                double2* P);
+__global__ void k_combine(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
+                          const double2* smp);
+__global__ void k_lincomb(VecView dst, long long doff, VecView xv, long long xoff, double a, VecView yv,
+                          long long yoff, double b, int use_y, long long len, const int* rmap, int nq);
+__global__ void k_norm2(VecView v, long long len, const int* rmap, double* out);
+__global__ void k_scale_div(VecView dst, VecView src, long long len, const int* rmap, int nq,
+                            const double* scale);
+__global__ void k_arnoldi(double2* V, long long vstride, long long n, int j, const int* rmap, double2* hout,
+                          int hld);
+__global__ void k_accum_x(VecView x, const double2* V, long long vstride, long long n, const double2* y,
+                          int yld, int k, const int* rmap, int nq);
+__global__ void k_residual(const double2* u, const double2* f, long long stride, int wz, int wx, const double2* tx,
+                           const double2* tz, const double* m, double omega2, const int* rmap, double* out);
+__global__ void k_vol_norm2(const double2* f, long long stride, long long N, double* out);

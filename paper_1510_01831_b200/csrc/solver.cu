@@ -1,0 +1,1286 @@
+// Host orchestration of the online stage and the C ABI (include/pt_b200.h).
+//
+// The outer left-preconditioned GMRES (krylov.py:53-135) is driven from here
+// with ONE host synchronisation per outer iteration (the Hessenberg column);
+// every layer-solve, inner Krylov iteration, Arnoldi reduction and the
+// reconstruction run on the device.  The outer operator and preconditioner of
+// sie.py:203-326 are encoded once, at pt_create, as "stages" of independent
+// layer-solve jobs (OJob) plus small vector combinations; a stage executes as
+//   gather panels -> K1 (Newton pass) -> inner GMRES -> K1 (reconstruction pass) -> combine.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/pt_b200.h"
+#include "pt_launch.cuh"
+
+using cplx = std::complex<double>;
+
+static thread_local std::string g_err;
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) {                                                               \
+      g_err = std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + std::to_string(__LINE__); \
+      return PT_CUDA_ERROR;                                                                \
+    }                                                                                      \
+  } while (0)
+
+namespace {
+
+const Ref NOREF{-1, 0};
+
+struct Stage {
+  std::vector<OJob> jobs;
+  OJob* jobs_d = nullptr;
+  int* stage_jobs_d = nullptr;
+  std::vector<int> ljobs;                 // job ids grouped by layer
+  std::vector<std::pair<int, int>> lgrp;  // (layer, begin in ljobs); count from next
+  int* ljobs_d = nullptr;
+  bool any_panel = false, any_sample = false;
+  // task cache per active-RHS count
+  struct Tasks {
+    K1Task* d = nullptr;
+    int n = 0, nc = 1;
+    long long zsize = 0;
+  };
+  std::map<int, Tasks> tasks;
+};
+
+template <class T>
+int upload(T** dst, const T* src, size_t n) {
+  if (n == 0) {
+    *dst = nullptr;
+    return 0;
+  }
+  CK(cudaMalloc(dst, n * sizeof(T)));
+  CK(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyDefault));
+  return 0;
+}
+
+}  // namespace
+
+struct pt_ctx {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  int nx, nz, npml, L, Lc, wx, wz, nI, wmax, wzcmax;
+  double h, omega;
+  std::vector<LayerInfo> lay;
+  std::vector<CellInfo> cel;
+  LayerInfo* lay_d = nullptr;
+  CellInfo* cel_d = nullptr;
+  double2 *sinv_d = nullptr, *green_d = nullptr, *lz_d = nullptr, *uz_d = nullptr;
+  double2 *tx_d = nullptr, *tz_d = nullptr;
+  double* m_d = nullptr;
+  // inner item programs
+  IItem* items_d = nullptr;
+  int *op_ph_d = nullptr, *pre_ph_d = nullptr;
+  int op_nph = 0, pre_nph = 0;
+  long long op_blocks = 0, pre_blocks = 0;
+  // outer stages
+  Stage newton, op, refl, recon, layer_solve;
+  std::vector<Stage> sdown, sup;  // sdown[I] for I=1..nI-1, sup[I] for I=0..nI-2
+  // solve scratch
+  int capR = 0, capO = 0, inner_cap = 32;
+  long long nO = 0;
+  double2 *V = nullptr, *Bv = nullptr, *Bp = nullptr, *T1 = nullptr, *AX = nullptr, *X = nullptr, *TR = nullptr;
+  double2 *P = nullptr, *smp = nullptr, *tables = nullptr, *trc = nullptr, *Z = nullptr, *iscr = nullptr,
+          *hess = nullptr;
+  long long zcap = 0, iscr_stride = 0, hstride = 0, inmax = 0;
+  int* iters = nullptr;
+  int* err_d = nullptr;
+  unsigned long long* cnt_d = nullptr;  // [0] inner iterations, [1] touches, [2] instances
+  int* hist_d = nullptr;
+  int* rmap_d = nullptr;
+  double *dscal = nullptr, *hnorm = nullptr;
+  double2 *hout = nullptr, *ybuf = nullptr;
+  int* hrmap = nullptr;
+  double2* hhout = nullptr;
+  double* hdscal = nullptr;
+  double2* hy = nullptr;
+  // host view of current active set
+  std::vector<int> act;
+  int slot_bytes = 32768, ns = 5;
+  long long layer_solves = 0;
+};
+
+// ------------------------------------------------------------------ program builders
+
+static int segD(const pt_ctx* c, int I, int s) { return 2 * I + s; }
+static int segU(const pt_ctx* c, int I, int s) { return 2 * c->nI + 2 * I + s; }
+
+static OJob blank_job(int layer) {
+  OJob j;
+  std::memset(&j, 0, sizeof(j));
+  j.layer = layer;
+  for (int s = 0; s < 4; ++s) {
+    j.pan[s][0] = j.pan[s][1] = NOREF;
+    j.dst[s] = j.add[s] = NOREF;
+    j.sub[s][0] = j.sub[s][1] = NOREF;
+    j.scoef[s] = 1.0;
+  }
+  return j;
+}
+static void add_out(OJob& j, int row, Ref dst, double scoef, Ref s0 = NOREF, Ref s1 = NOREF) {
+  const int o = j.nout++;
+  j.orow[o] = row;
+  j.dst[o] = dst;
+  j.scoef[o] = scoef;
+  j.sub[o][0] = s0;
+  j.sub[o][1] = s1;
+}
+
+static int finalize_stage(pt_ctx* c, Stage& S) {
+  const int J = (int)S.jobs.size();
+  std::vector<int> sj(J);
+  for (int i = 0; i < J; ++i) sj[i] = i;
+  S.ljobs.clear();
+  S.lgrp.clear();
+  for (int l = 0; l < c->L; ++l) {
+    const int b = (int)S.ljobs.size();
+    for (int i = 0; i < J; ++i)
+      if (S.jobs[i].layer == l) S.ljobs.push_back(i);
+    if ((int)S.ljobs.size() > b) S.lgrp.push_back({l, b});
+  }
+  for (auto& jb : S.jobs) {
+    for (int s = 0; s < 4; ++s)
+      if (jb.pan[s][0].vec >= 0) S.any_panel = true;
+    if (jb.nout > 0) S.any_sample = true;
+  }
+  if (upload(&S.jobs_d, S.jobs.data(), S.jobs.size())) return PT_CUDA_ERROR;
+  if (upload(&S.stage_jobs_d, sj.data(), sj.size())) return PT_CUDA_ERROR;
+  if (upload(&S.ljobs_d, S.ljobs.data(), S.ljobs.size())) return PT_CUDA_ERROR;
+  return 0;
+}
+
+// vec ids of outer stages: 0 IN, 1 OUT, 2 AUX
+static int build_outer(pt_ctx* c) {
+  const int L = c->L, nI = c->nI;
+  // NEWTON (sie.py:175-188 + 230-242): rhs.down = -N_{n,n+1}, rhs.up = -N_{0,1}
+  for (int l = 0; l < L; ++l) {
+    OJob j = blank_job(l);
+    j.vol = 1;
+    const int n = c->lay[l].n;
+    if (l >= 1) {
+      add_out(j, 0, Ref{1, segU(c, l - 1, 0)}, -1.0);
+      add_out(j, 1, Ref{1, segU(c, l - 1, 1)}, -1.0);
+    }
+    if (l <= L - 2) {
+      add_out(j, n, Ref{1, segD(c, l, 0)}, -1.0);
+      add_out(j, n + 1, Ref{1, segD(c, l, 1)}, -1.0);
+    }
+    if (j.nout > 0) c->newton.jobs.push_back(j);
+  }
+  // OP = apply_M_polarized (sie.py:203-228)
+  for (int l = 0; l < L; ++l) {
+    const bool top = l >= 1, bot = l <= L - 2;
+    const int ib = l, it = l - 1;
+    const int n = c->lay[l].n;
+    if (bot) {
+      OJob j = blank_job(l);
+      if (top) {
+        j.pan[0][0] = Ref{0, segD(c, ib - 1, 0)};
+        j.pan[0][1] = Ref{0, segU(c, ib - 1, 0)};
+        j.pan[1][0] = Ref{0, segD(c, ib - 1, 1)};
+        j.pan[1][1] = Ref{0, segU(c, ib - 1, 1)};
+      }
+      j.pan[2][0] = Ref{0, segU(c, ib, 0)};
+      j.pan[3][0] = Ref{0, segU(c, ib, 1)};
+      add_out(j, n, Ref{1, segD(c, ib, 0)}, 1.0, Ref{0, segD(c, ib, 0)}, Ref{0, segU(c, ib, 0)});
+      add_out(j, n + 1, Ref{1, segD(c, ib, 1)}, 1.0, Ref{0, segD(c, ib, 1)});
+      c->op.jobs.push_back(j);
+    }
+    if (top) {
+      OJob j = blank_job(l);
+      j.pan[0][0] = Ref{0, segD(c, it, 0)};
+      j.pan[1][0] = Ref{0, segD(c, it, 1)};
+      if (bot) {
+        j.pan[2][0] = Ref{0, segU(c, ib, 0)};
+        j.pan[2][1] = Ref{0, segD(c, ib, 0)};
+        j.pan[3][0] = Ref{0, segU(c, ib, 1)};
+        j.pan[3][1] = Ref{0, segD(c, ib, 1)};
+      }
+      add_out(j, 0, Ref{1, segU(c, it, 0)}, 1.0, Ref{0, segU(c, it, 0)});
+      add_out(j, 1, Ref{1, segU(c, it, 1)}, 1.0, Ref{0, segD(c, it, 1)}, Ref{0, segU(c, it, 1)});
+      c->op.jobs.push_back(j);
+    }
+  }
+  // sweep_down steps (sie.py:272-283): IN = v, OUT = y
+  c->sdown.resize(std::max(nI, 1));
+  for (int I = 1; I < nI; ++I) {
+    OJob j = blank_job(I);
+    const int n = c->lay[I].n;
+    j.pan[0][0] = Ref{1, segD(c, I - 1, 0)};
+    j.pan[1][0] = Ref{1, segD(c, I - 1, 1)};
+    add_out(j, n, Ref{1, segD(c, I, 0)}, 1.0, Ref{0, segD(c, I, 0)});
+    add_out(j, n + 1, Ref{1, segD(c, I, 1)}, 1.0, Ref{0, segD(c, I, 1)});
+    c->sdown[I].jobs.push_back(j);
+  }
+  // upward_reflections (sie.py:298-308): IN = y (down half), OUT = aux (up half)
+  for (int I = 0; I < nI; ++I) {
+    OJob j = blank_job(I + 1);
+    j.pan[0][0] = Ref{0, segD(c, I, 0)};
+    j.pan[1][0] = Ref{0, segD(c, I, 1)};
+    if (I <= nI - 2) {
+      j.pan[2][0] = Ref{0, segD(c, I + 1, 0)};
+      j.pan[3][0] = Ref{0, segD(c, I + 1, 1)};
+    }
+    add_out(j, 0, Ref{1, segU(c, I, 0)}, 1.0);
+    add_out(j, 1, Ref{1, segU(c, I, 1)}, 1.0, Ref{0, segD(c, I, 1)});
+    c->refl.jobs.push_back(j);
+  }
+  // sweep_up steps (sie.py:285-296): IN holds s in its up half, OUT = y
+  c->sup.resize(std::max(nI, 1));
+  for (int I = nI - 2; I >= 0; --I) {
+    OJob j = blank_job(I + 1);
+    j.pan[2][0] = Ref{1, segU(c, I + 1, 0)};
+    j.pan[3][0] = Ref{1, segU(c, I + 1, 1)};
+    add_out(j, 0, Ref{1, segU(c, I, 0)}, 1.0, Ref{0, segU(c, I, 0)});
+    add_out(j, 1, Ref{1, segU(c, I, 1)}, 1.0, Ref{0, segU(c, I, 1)});
+    c->sup[I].jobs.push_back(j);
+  }
+  // reconstruct (sie.py:332-346): IN = traces in the down layout, full-volume output
+  for (int l = 0; l < L; ++l) {
+    OJob j = blank_job(l);
+    j.vol = 1;
+    j.nout = -1;
+    if (l >= 1) {
+      j.pan[0][0] = Ref{0, segD(c, l - 1, 0)};
+      j.pan[1][0] = Ref{0, segD(c, l - 1, 1)};
+    }
+    if (l <= L - 2) {
+      j.pan[2][0] = Ref{0, segD(c, l, 0)};
+      j.pan[3][0] = Ref{0, segD(c, l, 1)};
+    }
+    c->recon.jobs.push_back(j);
+  }
+  int rc = 0;
+  rc |= finalize_stage(c, c->newton);
+  rc |= finalize_stage(c, c->op);
+  rc |= finalize_stage(c, c->refl);
+  rc |= finalize_stage(c, c->recon);
+  for (int I = 1; I < nI; ++I) rc |= finalize_stage(c, c->sdown[I]);
+  for (int I = 0; I <= nI - 2; ++I) rc |= finalize_stage(c, c->sup[I]);
+  return rc ? PT_CUDA_ERROR : 0;
+}
+
+// inner programs over cells (nested.py:125-153 -> sie.py:203-326); vec ids 0 IN, 1 OUT, 2 AUX; seg units of w
+static int build_inner(pt_ctx* c) {
+  const int Lc = c->Lc, nI = Lc - 1;
+  auto D = [&](int I, int s) { return 2 * I + s; };
+  auto U = [&](int I, int s) { return 2 * nI + 2 * I + s; };
+  auto item = [&](int cell, int row) {
+    IItem it;
+    std::memset(&it, 0, sizeof(it));
+    it.cell = cell;
+    it.row = row;
+    for (int s = 0; s < 4; ++s) it.pan[s][0] = it.pan[s][1] = NOREF;
+    it.dst = it.add = it.sub[0] = it.sub[1] = NOREF;
+    return it;
+  };
+  std::vector<IItem> items;
+  std::vector<int> oph, pph;
+  long long opb = 0, preb = 0;
+  auto count = [&](const IItem& it, long long& acc) {
+    if (it.cell < 0) return;
+    for (int s = 0; s < 4; ++s)
+      if (it.pan[s][0].vec >= 0) ++acc;
+  };
+  // ---- OP: one phase
+  oph.push_back((int)items.size());
+  for (int cc = 0; cc < Lc; ++cc) {
+    const bool top = cc >= 1, bot = cc <= Lc - 2;
+    const int ib = cc, it = cc - 1;
+    if (bot) {
+      for (int s = 0; s < 2; ++s) {
+        IItem x = item(cc, 2 + s);
+        if (top) {
+          x.pan[0][0] = Ref{0, D(ib - 1, 0)};
+          x.pan[0][1] = Ref{0, U(ib - 1, 0)};
+          x.pan[1][0] = Ref{0, D(ib - 1, 1)};
+          x.pan[1][1] = Ref{0, U(ib - 1, 1)};
+        }
+        x.pan[2][0] = Ref{0, U(ib, 0)};
+        x.pan[3][0] = Ref{0, U(ib, 1)};
+        x.dst = Ref{1, D(ib, s)};
+        x.sub[0] = Ref{0, D(ib, s)};
+        if (s == 0) x.sub[1] = Ref{0, U(ib, 0)};
+        count(x, opb);
+        items.push_back(x);
+      }
+    }
+    if (top) {
+      for (int s = 0; s < 2; ++s) {
+        IItem x = item(cc, s);
+        x.pan[0][0] = Ref{0, D(it, 0)};
+        x.pan[1][0] = Ref{0, D(it, 1)};
+        if (bot) {
+          x.pan[2][0] = Ref{0, U(ib, 0)};
+          x.pan[2][1] = Ref{0, D(ib, 0)};
+          x.pan[3][0] = Ref{0, U(ib, 1)};
+          x.pan[3][1] = Ref{0, D(ib, 1)};
+        }
+        x.dst = Ref{1, U(it, s)};
+        if (s == 0) {
+          x.sub[0] = Ref{0, U(it, 0)};
+        } else {
+          x.sub[0] = Ref{0, D(it, 1)};
+          x.sub[1] = Ref{0, U(it, 1)};
+        }
+        count(x, opb);
+        items.push_back(x);
+      }
+    }
+  }
+  oph.push_back((int)items.size());
+  // ---- PRE (GS, sie.py:322-326)
+  pph.push_back((int)items.size());
+  for (int s = 0; s < 2; ++s) {  // y_down[0] = -v_down[0]
+    IItem x = item(-1, 0);
+    x.dst = Ref{1, D(0, s)};
+    x.sub[0] = Ref{0, D(0, s)};
+    items.push_back(x);
+  }
+  pph.push_back((int)items.size());
+  for (int I = 1; I < nI; ++I) {
+    for (int s = 0; s < 2; ++s) {
+      IItem x = item(I, 2 + s);
+      x.pan[0][0] = Ref{1, D(I - 1, 0)};
+      x.pan[1][0] = Ref{1, D(I - 1, 1)};
+      x.dst = Ref{1, D(I, s)};
+      x.sub[0] = Ref{0, D(I, s)};
+      count(x, preb);
+      items.push_back(x);
+    }
+    pph.push_back((int)items.size());
+  }
+  for (int I = 0; I < nI; ++I) {  // reflections into AUX.up
+    for (int s = 0; s < 2; ++s) {
+      IItem x = item(I + 1, s);
+      x.pan[0][0] = Ref{1, D(I, 0)};
+      x.pan[1][0] = Ref{1, D(I, 1)};
+      if (I <= nI - 2) {
+        x.pan[2][0] = Ref{1, D(I + 1, 0)};
+        x.pan[3][0] = Ref{1, D(I + 1, 1)};
+      }
+      x.dst = Ref{2, U(I, s)};
+      if (s == 1) x.sub[0] = Ref{1, D(I, 1)};
+      count(x, preb);
+      items.push_back(x);
+    }
+  }
+  pph.push_back((int)items.size());
+  for (int I = 0; I < nI; ++I)  // s = p - refl (in place in AUX.up)
+    for (int s = 0; s < 2; ++s) {
+      IItem x = item(-1, 0);
+      x.dst = Ref{2, U(I, s)};
+      x.add = Ref{0, U(I, s)};
+      x.sub[0] = Ref{2, U(I, s)};
+      items.push_back(x);
+    }
+  pph.push_back((int)items.size());
+  for (int s = 0; s < 2; ++s) {  // y_up[nI-1] = -s[nI-1]
+    IItem x = item(-1, 0);
+    x.dst = Ref{1, U(nI - 1, s)};
+    x.sub[0] = Ref{2, U(nI - 1, s)};
+    items.push_back(x);
+  }
+  pph.push_back((int)items.size());
+  for (int I = nI - 2; I >= 0; --I) {
+    for (int s = 0; s < 2; ++s) {
+      IItem x = item(I + 1, s);
+      x.pan[2][0] = Ref{1, U(I + 1, 0)};
+      x.pan[3][0] = Ref{1, U(I + 1, 1)};
+      x.dst = Ref{1, U(I, s)};
+      x.sub[0] = Ref{2, U(I, s)};
+      count(x, preb);
+      items.push_back(x);
+    }
+    pph.push_back((int)items.size());
+  }
+  c->op_nph = (int)oph.size() - 1;
+  c->pre_nph = (int)pph.size() - 1;
+  c->op_blocks = opb;
+  c->pre_blocks = preb;
+  if (nI == 0) return 0;
+  if (upload(&c->items_d, items.data(), items.size())) return PT_CUDA_ERROR;
+  if (upload(&c->op_ph_d, oph.data(), oph.size())) return PT_CUDA_ERROR;
+  if (upload(&c->pre_ph_d, pph.data(), pph.size())) return PT_CUDA_ERROR;
+  return 0;
+}
+
+// ------------------------------------------------------------------ scratch
+
+static int ensure_scratch(pt_ctx* c, int R, int capO) {
+  const int Jmax = std::max(std::max(2 * c->L - 2, c->L), 1);
+  if (R <= c->capR && capO <= c->capO) return 0;
+  R = std::max(R, c->capR);
+  capO = std::max(capO, c->capO);
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  for (void* p : {(void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1, (void*)c->AX, (void*)c->X, (void*)c->TR,
+                  (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->trc, (void*)c->iscr, (void*)c->hess,
+                  (void*)c->iters, (void*)c->rmap_d, (void*)c->dscal, (void*)c->hout, (void*)c->ybuf})
+    F(p);
+  if (c->hrmap) cudaFreeHost(c->hrmap);
+  if (c->hhout) cudaFreeHost(c->hhout);
+  if (c->hdscal) cudaFreeHost(c->hdscal);
+  if (c->hy) cudaFreeHost(c->hy);
+  const long long nO = std::max(4LL * c->nI * c->wx, 1LL);
+  c->nO = nO;
+  CK(cudaMalloc(&c->V, sizeof(double2) * (size_t)R * (capO + 1) * nO));
+  for (double2** p : {&c->Bv, &c->Bp, &c->T1, &c->AX, &c->X, &c->TR}) CK(cudaMalloc(p, sizeof(double2) * (size_t)R * nO));
+  CK(cudaMalloc(&c->P, sizeof(double2) * (size_t)Jmax * 4 * R * c->wx));
+  CK(cudaMalloc(&c->smp, sizeof(double2) * (size_t)Jmax * 4 * R * c->wx));
+  CK(cudaMalloc(&c->tables, sizeof(double2) * (size_t)Jmax * c->Lc * 4 * R * c->wmax));
+  CK(cudaMalloc(&c->trc, sizeof(double2) * (size_t)Jmax * R * std::max(c->Lc - 1, 1) * 2 * c->wmax));
+  c->inmax = 4LL * std::max(c->Lc - 1, 1) * c->wmax;
+  c->iscr_stride = (long long)(c->inner_cap + 5) * c->inmax;
+  CK(cudaMalloc(&c->iscr, sizeof(double2) * (size_t)Jmax * R * c->iscr_stride));
+  c->hstride = (long long)(c->inner_cap + 1) * c->inner_cap + (c->inner_cap + 1) + 2 * c->inner_cap;
+  CK(cudaMalloc(&c->hess, sizeof(double2) * (size_t)Jmax * R * c->hstride));
+  CK(cudaMalloc(&c->iters, sizeof(int) * (size_t)Jmax * R));
+  CK(cudaMalloc(&c->rmap_d, sizeof(int) * R));
+  CK(cudaMalloc(&c->dscal, sizeof(double) * 2 * R));
+  CK(cudaMalloc(&c->hout, sizeof(double2) * (size_t)R * (capO + 2)));
+  CK(cudaMalloc(&c->ybuf, sizeof(double2) * (size_t)R * (capO + 1)));
+  CK(cudaMallocHost(&c->hrmap, sizeof(int) * R));
+  CK(cudaMallocHost(&c->hhout, sizeof(double2) * (size_t)R * (capO + 2)));
+  CK(cudaMallocHost(&c->hdscal, sizeof(double) * 2 * R));
+  CK(cudaMallocHost(&c->hy, sizeof(double2) * (size_t)R * (capO + 1)));
+  c->capR = R;
+  c->capO = capO;
+  return 0;
+}
+
+static int ensure_z(pt_ctx* c, long long z) {
+  if (z <= c->zcap) return 0;
+  if (c->Z) cudaFree(c->Z);
+  CK(cudaMalloc(&c->Z, sizeof(double2) * (size_t)z));
+  c->zcap = z;
+  return 0;
+}
+
+static Stage::Tasks* stage_tasks(pt_ctx* c, Stage& S, int Ract) {
+  auto itr = S.tasks.find(Ract);
+  if (itr != S.tasks.end()) return &itr->second;
+  Stage::Tasks T;
+  int maxcols = 0;
+  for (size_t g = 0; g < S.lgrp.size(); ++g) {
+    const int b = S.lgrp[g].second;
+    const int e = g + 1 < S.lgrp.size() ? S.lgrp[g + 1].second : (int)S.ljobs.size();
+    maxcols = std::max(maxcols, (e - b) * Ract);
+  }
+  int nc = 1;
+  while (nc < maxcols && nc < 8) nc <<= 1;
+  T.nc = nc;
+  std::vector<K1Task> v;
+  long long z = 0;
+  for (size_t g = 0; g < S.lgrp.size(); ++g) {
+    const int l = S.lgrp[g].first, b = S.lgrp[g].second;
+    const int e = g + 1 < S.lgrp.size() ? S.lgrp[g + 1].second : (int)S.ljobs.size();
+    const int ncols = (e - b) * Ract;
+    for (int q0 = 0; q0 < ncols; q0 += nc)
+      for (int cc = 0; cc < c->Lc; ++cc) {
+        const CellInfo& ci = c->cel[l * c->Lc + cc];
+        K1Task t;
+        t.cell = l * c->Lc + cc;
+        t.jb = b;
+        t.q0 = q0;
+        t.nq = std::min(nc, ncols - q0);
+        t.zoff = z;
+        z += (long long)ci.wzc * ci.w * nc;
+        v.push_back(t);
+      }
+  }
+  T.n = (int)v.size();
+  T.zsize = z;
+  if (upload(&T.d, v.data(), v.size())) return nullptr;
+  auto res = S.tasks.emplace(Ract, T);
+  return &res.first->second;
+}
+
+// ------------------------------------------------------------------ stage execution
+
+struct SolveIO {
+  const double2* f;
+  long long f_stride;
+  double2* u;
+  long long u_stride;
+  double inner_ktol;
+  int inner_max_iter;
+};
+
+static int grid_for(long long n) {
+  long long b = (n + 255) / 256;
+  return (int)std::max(1LL, std::min(b, 148LL * 16));
+}
+
+static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& io) {
+  const int J = (int)S.jobs.size();
+  if (J == 0 || Ract == 0) return 0;
+  Stage::Tasks* T = stage_tasks(c, S, Ract);
+  if (!T) return PT_CUDA_ERROR;
+  if (ensure_z(c, T->zsize)) return PT_CUDA_ERROR;
+  if (S.any_panel) {
+    k_gather_panels<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract,
+                                                                                    c->wx, c->P);
+    CK(cudaGetLastError());
+  }
+  K1Params kp;
+  std::memset(&kp, 0, sizeof(kp));
+  kp.cells = c->cel_d;
+  kp.layers = c->lay_d;
+  kp.jobs = S.jobs_d;
+  kp.ljobs = S.ljobs_d;
+  kp.tasks = T->d;
+  kp.sinv = c->sinv_d;
+  kp.lz = c->lz_d;
+  kp.uz = c->uz_d;
+  kp.R = Ract;
+  kp.npml = c->npml;
+  kp.wx = c->wx;
+  kp.Lc = c->Lc;
+  kp.wmax = c->wmax;
+  kp.slot_bytes = c->slot_bytes;
+  kp.ns = c->ns;
+  kp.f = io.f;
+  kp.f_stride = io.f_stride;
+  kp.P = c->P;
+  kp.tr = c->trc;
+  kp.tables = c->tables;
+  kp.smp = c->smp;
+  kp.u = io.u;
+  kp.u_stride = io.u_stride;
+  kp.Z = c->Z;
+  // volume sources/outputs are indexed by the real RHS id: pre-offset through rmap on the host is not
+  // possible per column, so stage buffers use compact q and f/u use q as well (callers compact f/u).
+  if (c->Lc > 1) {
+    kp.pass = 0;
+    CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
+    InnerParams ip;
+    std::memset(&ip, 0, sizeof(ip));
+    ip.cells = c->cel_d;
+    ip.layers = c->lay_d;
+    ip.jobs = S.jobs_d;
+    ip.stage_jobs = S.stage_jobs_d;
+    ip.green = c->green_d;
+    ip.items = c->items_d;
+    ip.op_ph = c->op_ph_d;
+    ip.op_nph = c->op_nph;
+    ip.pre_ph = c->pre_ph_d;
+    ip.pre_nph = c->pre_nph;
+    ip.R = Ract;
+    ip.Lc = c->Lc;
+    ip.wmax = c->wmax;
+    ip.cap = c->inner_cap;
+    ip.max_iter = io.inner_max_iter;
+    ip.ktol = io.inner_ktol;
+    ip.tables = c->tables;
+    ip.tr = c->trc;
+    ip.scratch = c->iscr;
+    ip.inst_stride = c->iscr_stride;
+    ip.nmax = c->inmax;
+    ip.hess = c->hess;
+    ip.hstride = c->hstride;
+    ip.iters = c->iters;
+    ip.err = c->err_d;
+    ip.counters = c->cnt_d;
+    ip.hist = c->hist_d;
+    ip.op_blocks = c->op_blocks;
+    ip.pre_blocks = c->pre_blocks;
+    CK(inner_launch(ip, J, c->st));
+  }
+  kp.pass = 1;
+  CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
+  if (S.any_sample) {
+    k_combine<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract, c->wx,
+                                                                              c->smp);
+    CK(cudaGetLastError());
+  }
+  c->layer_solves += (long long)J * Ract;
+  return 0;
+}
+
+static int lincomb(pt_ctx* c, VecView d, long long doff, VecView x, long long xoff, double a, VecView y,
+                   long long yoff, double b, int use_y, long long len, int Ract) {
+  if (len <= 0 || Ract == 0) return 0;
+  k_lincomb<<<grid_for(len * Ract), 256, 0, c->st>>>(d, doff, x, xoff, a, y, yoff, b, use_y, len, c->rmap_d, Ract);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// y = P v  (sie.py:322-329); aux is scratch
+static int apply_pre(pt_ctx* c, VecView in, VecView out, VecView aux, int Ract, int gs, const SolveIO& io) {
+  const long long wx = c->wx;
+  const int nI = c->nI;
+  const long long up0 = 2LL * nI * wx;
+  int rc = lincomb(c, out, 0, in, 0, -1.0, in, 0, 0.0, 0, 2 * wx, Ract);  // y_down[0] = -v_down[0]
+  if (rc) return rc;
+  for (int I = 1; I < nI; ++I)
+    if ((rc = run_stage(c, c->sdown[I], VecTab{{in, out, aux}}, Ract, io))) return rc;
+  VecView sview = in;
+  if (gs) {
+    if ((rc = run_stage(c, c->refl, VecTab{{out, aux, aux}}, Ract, io))) return rc;
+    if ((rc = lincomb(c, aux, up0, in, up0, 1.0, aux, up0, -1.0, 1, up0, Ract))) return rc;  // s = p - refl
+    sview = aux;
+  }
+  if ((rc = lincomb(c, out, up0 + 2LL * (nI - 1) * wx, sview, up0 + 2LL * (nI - 1) * wx, -1.0, sview, 0, 0.0, 0,
+                    2 * wx, Ract)))
+    return rc;
+  for (int I = nI - 2; I >= 0; --I)
+    if ((rc = run_stage(c, c->sup[I], VecTab{{sview, out, aux}}, Ract, io))) return rc;
+  return 0;
+}
+
+static int apply_op(pt_ctx* c, VecView in, VecView out, int Ract, const SolveIO& io) {
+  return run_stage(c, c->op, VecTab{{in, out, out}}, Ract, io);
+}
+
+static int set_active(pt_ctx* c, const std::vector<int>& a) {
+  c->act = a;
+  for (size_t i = 0; i < a.size(); ++i) c->hrmap[i] = a[i];
+  if (!a.empty()) CK(cudaMemcpyAsync(c->rmap_d, c->hrmap, sizeof(int) * a.size(), cudaMemcpyHostToDevice, c->st));
+  return 0;
+}
+
+static int grow_outer_basis(pt_ctx* c, int R, int need) {
+  if (need <= c->capO) return 0;
+  int ncap = std::max(need, 2 * c->capO);
+  double2* nv = nullptr;
+  CK(cudaMalloc(&nv, sizeof(double2) * (size_t)c->capR * (ncap + 1) * c->nO));
+  for (int r = 0; r < R; ++r)
+    CK(cudaMemcpyAsync(nv + (size_t)r * (ncap + 1) * c->nO, c->V + (size_t)r * (c->capO + 1) * c->nO,
+                       sizeof(double2) * (size_t)(c->capO + 1) * c->nO, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  cudaFree(c->V);
+  c->V = nv;
+  // per-RHS small buffers sized by capO
+  cudaFree(c->hout);
+  cudaFree(c->ybuf);
+  cudaFreeHost(c->hhout);
+  cudaFreeHost(c->hy);
+  CK(cudaMalloc(&c->hout, sizeof(double2) * (size_t)c->capR * (ncap + 2)));
+  CK(cudaMalloc(&c->ybuf, sizeof(double2) * (size_t)c->capR * (ncap + 1)));
+  CK(cudaMallocHost(&c->hhout, sizeof(double2) * (size_t)c->capR * (ncap + 2)));
+  CK(cudaMallocHost(&c->hy, sizeof(double2) * (size_t)c->capR * (ncap + 1)));
+  c->capO = ncap;
+  return 0;
+}
+
+static int check_err(pt_ctx* c, int* code) {
+  int e = 0;
+  CK(cudaMemcpy(&e, c->err_d, sizeof(int), cudaMemcpyDeviceToHost));
+  *code = e;
+  return 0;
+}
+
+// ------------------------------------------------------------------ the online solve (sie.py:392-439)
+
+struct RhsState {
+  std::vector<cplx> H;  // (m+1) x m column-major, per cycle
+  std::vector<cplx> cs, sn, g;
+  std::vector<double> hist;
+  double beta0 = 0.0;
+  int total = 0, k = 0;
+  int status = 0;  // 0 running, 1 converged, 2 failed
+};
+
+static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg, double2* u, pt_stats* stats) {
+  if (R <= 0) return PT_BAD_ARGUMENT;
+  if (cfg->ktol <= 0 || cfg->max_iter < 1) {
+    g_err = "ktol must be positive and max_iter >= 1";
+    return PT_BAD_ARGUMENT;
+  }
+  const long long N = (long long)c->wz * c->wx;
+  const int gs = cfg->precond == 0;
+  const int max_iter = cfg->max_iter;
+  const int cycle = cfg->restart > 0 ? cfg->restart : max_iter;
+  if (ensure_scratch(c, R, std::min(max_iter, 16))) return PT_CUDA_ERROR;
+  CK(cudaMemsetAsync(c->err_d, 0, sizeof(int), c->st));
+  CK(cudaMemsetAsync(c->cnt_d, 0, sizeof(unsigned long long) * 4, c->st));
+  CK(cudaMemsetAsync(c->hist_d, 0, sizeof(int) * PT_HIST, c->st));
+  c->layer_solves = 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, c->st);
+
+  SolveIO io{f, N, u, N, cfg->inner_ktol, cfg->inner_max_iter};
+  // zero-source detection (sie.py:397-399)
+  CK(cudaMemsetAsync(c->dscal, 0, sizeof(double) * 2 * R, c->st));
+  k_vol_norm2<<<dim3(64, R), 256, 0, c->st>>>(f, N, N, c->dscal);
+  CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * R, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  std::vector<RhsState> rs(R);
+  std::vector<int> live;
+  for (int r = 0; r < R; ++r) {
+    if (c->hdscal[r] == 0.0) {
+      rs[r].status = 1;
+      rs[r].hist = {0.0};
+      CK(cudaMemsetAsync(u + (size_t)r * N, 0, sizeof(double2) * N, c->st));
+    } else {
+      live.push_back(r);
+    }
+  }
+  const long long nO = c->nO;
+  const long long vstride = (long long)(c->capO + 1) * nO;
+  VecView vB{c->Bv, nO}, vBp{c->Bp, nO}, vT{c->T1, nO}, vA{c->AX, nO}, vX{c->X, nO}, vTR{c->TR, nO};
+  int rc = 0;
+  // stage buffers index f/u by compact q: the stage kernels read f via rmap-free indexing, so
+  // run the volumetric stages with f/u views offset per active list (contiguous when all live).
+  std::vector<int> all(R);
+  for (int r = 0; r < R; ++r) all[r] = r;
+
+  if (c->nI == 0) {
+    // monolayer (sie.py:401-404): reconstruct with empty traces
+    if ((rc = set_active(c, all))) return rc;
+    if ((rc = run_stage(c, c->recon, VecTab{{vTR, vTR, vTR}}, R, io))) return rc;
+    for (int r : live) rs[r].status = 1;
+  } else if (!live.empty()) {
+    if ((rc = set_active(c, all))) return rc;
+    CK(cudaMemsetAsync(c->Bv, 0, sizeof(double2) * (size_t)R * nO, c->st));
+    if ((rc = run_stage(c, c->newton, VecTab{{vB, vB, vB}}, R, io))) return rc;
+    if ((rc = set_active(c, live))) return rc;
+    const int Rl = (int)live.size();
+    if ((rc = apply_pre(c, vB, vBp, vA, Rl, gs, io))) return rc;
+    k_norm2<<<Rl, 256, 0, c->st>>>(vBp, nO, c->rmap_d, c->dscal);
+    CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * R, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemsetAsync(c->X, 0, sizeof(double2) * (size_t)R * nO, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    int ecode = 0;
+    if ((rc = check_err(c, &ecode))) return rc;
+    if (ecode) return ecode;
+    std::vector<int> run;
+    for (int r : live) {
+      rs[r].beta0 = std::sqrt(c->hdscal[r]);
+      if (rs[r].beta0 == 0.0) {
+        rs[r].status = 1;
+        rs[r].hist = {0.0};
+      } else {
+        run.push_back(r);
+      }
+    }
+    int total = 0;
+    while (total < max_iter && !run.empty()) {
+      if ((rc = set_active(c, run))) return rc;
+      int Ra = (int)run.size();
+      VecView vV0{c->V, (long long)(c->capO + 1) * nO};
+      // r = b - pre(op(x)) on restart, else b (krylov.py:73)
+      std::vector<double> beta(R, 0.0);
+      if (total > 0) {
+        if ((rc = apply_op(c, vX, vT, Ra, io))) return rc;
+        if ((rc = apply_pre(c, vT, vTR, vA, Ra, gs, io))) return rc;
+        if ((rc = lincomb(c, vV0, 0, vBp, 0, 1.0, vTR, 0, -1.0, 1, nO, Ra))) return rc;
+        k_norm2<<<Ra, 256, 0, c->st>>>(vV0, nO, c->rmap_d, c->dscal);
+        CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * R, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        std::vector<int> keep;
+        for (int r : run) {
+          beta[r] = std::sqrt(c->hdscal[r]);
+          if (beta[r] / rs[r].beta0 <= cfg->ktol) {
+            rs[r].hist.push_back(beta[r] / rs[r].beta0);
+            rs[r].status = 1;
+          } else {
+            keep.push_back(r);
+          }
+        }
+        run = keep;
+        if (run.empty()) break;
+        if ((rc = set_active(c, run))) return rc;
+        Ra = (int)run.size();
+        for (int r : run) c->hdscal[r] = beta[r];
+        CK(cudaMemcpyAsync(c->dscal, c->hdscal, sizeof(double) * R, cudaMemcpyHostToDevice, c->st));
+        k_scale_div<<<grid_for(nO * Ra), 256, 0, c->st>>>(vV0, vV0, nO, c->rmap_d, Ra, c->dscal);
+      } else {
+        for (int r : run) {
+          beta[r] = rs[r].beta0;
+          c->hdscal[r] = beta[r];
+        }
+        CK(cudaMemcpyAsync(c->dscal, c->hdscal, sizeof(double) * R, cudaMemcpyHostToDevice, c->st));
+        k_scale_div<<<grid_for(nO * Ra), 256, 0, c->st>>>(vV0, vBp, nO, c->rmap_d, Ra, c->dscal);
+      }
+      CK(cudaGetLastError());
+      const int m = std::min(cycle, max_iter - total);
+      for (int r : run) {
+        RhsState& s = rs[r];
+        s.H.assign((size_t)(m + 1) * m, cplx(0, 0));
+        s.cs.assign(m, cplx(0, 0));
+        s.sn.assign(m, cplx(0, 0));
+        s.g.assign(m + 1, cplx(0, 0));
+        s.g[0] = beta[r];
+        s.k = 0;
+      }
+      std::vector<int> cyc = run;  // RHS taking part in this cycle
+      std::vector<int> cont = run;
+      for (int j = 0; j < m && !cont.empty(); ++j) {
+        if ((rc = grow_outer_basis(c, R, j + 1))) return rc;
+        const long long vs = (long long)(c->capO + 1) * nO;
+        if ((rc = set_active(c, cont))) return rc;
+        Ra = (int)cont.size();
+        VecView vj{c->V + (size_t)j * nO, vs}, vj1{c->V + (size_t)(j + 1) * nO, vs};
+        if ((rc = apply_op(c, vj, vT, Ra, io))) return rc;
+        if ((rc = apply_pre(c, vT, vj1, vA, Ra, gs, io))) return rc;
+        const int hld = c->capO + 2;
+        k_arnoldi<<<Ra, 512, 0, c->st>>>(c->V, vs, nO, j, c->rmap_d, c->hout, hld);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(c->hhout, c->hout, sizeof(double2) * (size_t)R * hld, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        int ecode = 0;
+        if ((rc = check_err(c, &ecode))) return rc;
+        if (ecode) return ecode;
+        ++total;
+        std::vector<int> nxt;
+        for (int r : cont) {
+          RhsState& s = rs[r];
+          const double2* hc = c->hhout + (size_t)r * hld;
+          cplx* col = &s.H[(size_t)j * (m + 1)];
+          for (int i = 0; i <= j; ++i) col[i] = cplx(hc[i].x, hc[i].y);
+          const double hn = hc[j + 1].x;
+          col[j + 1] = hn;
+          for (int i = 0; i < j; ++i) {
+            const cplx t = s.cs[i] * col[i] + s.sn[i] * col[i + 1];
+            col[i + 1] = -std::conj(s.sn[i]) * col[i] + std::conj(s.cs[i]) * col[i + 1];
+            col[i] = t;
+          }
+          const double a = std::abs(col[j]);
+          const double d = std::sqrt(a * a + hn * hn);
+          if (d == 0.0) {
+            g_err = "GMRES breakdown: zero Hessenberg column";
+            return PT_BREAKDOWN;
+          }
+          s.cs[j] = std::conj(col[j]) / d;
+          s.sn[j] = hn / d;
+          col[j] = s.cs[j] * col[j] + s.sn[j] * hn;
+          s.g[j + 1] = -std::conj(s.sn[j]) * s.g[j];
+          s.g[j] = s.cs[j] * s.g[j];
+          s.k = j + 1;
+          s.total = total;
+          const double res = std::abs(s.g[j + 1]) / s.beta0;
+          s.hist.push_back(res);
+          if (hn == 0.0) {
+            if (res > cfg->ktol) {
+              g_err = "GMRES happy breakdown before convergence";
+              return PT_BREAKDOWN;
+            }
+            continue;  // stops this RHS's cycle
+          }
+          c->hdscal[r] = hn;
+          if (res <= cfg->ktol) continue;
+          nxt.push_back(r);
+        }
+        // normalise V_{j+1} for RHS with hn > 0 (also for the ones that just converged: harmless)
+        std::vector<int> norm;
+        for (int r : cont)
+          if (rs[r].k == j + 1 && c->hdscal[r] > 0.0 && std::abs(rs[r].g[j + 1]) / rs[r].beta0 > cfg->ktol)
+            norm.push_back(r);
+        if (!norm.empty()) {
+          if ((rc = set_active(c, norm))) return rc;
+          CK(cudaMemcpyAsync(c->dscal, c->hdscal, sizeof(double) * R, cudaMemcpyHostToDevice, c->st));
+          k_scale_div<<<grid_for(nO * (long long)norm.size()), 256, 0, c->st>>>(vj1, vj1, nO, c->rmap_d,
+                                                                                  (int)norm.size(), c->dscal);
+          CK(cudaGetLastError());
+        }
+        cont = nxt;
+      }
+      // x += V_k y per RHS of this cycle (krylov.py:128-131)
+      const int yld = c->capO + 1;
+      int kmax = 0;
+      for (int r : cyc) {
+        RhsState& s = rs[r];
+        const int k = s.k;
+        kmax = std::max(kmax, k);
+        std::vector<cplx> y(k);
+        for (int i = k - 1; i >= 0; --i) {
+          cplx acc = s.g[i];
+          for (int l = i + 1; l < k; ++l) acc -= s.H[(size_t)l * (m + 1) + i] * y[l];
+          y[i] = acc / s.H[(size_t)i * (m + 1) + i];
+        }
+        for (int i = 0; i < yld; ++i) c->hy[(size_t)r * yld + i] = make_double2(0, 0);
+        for (int i = 0; i < k; ++i) c->hy[(size_t)r * yld + i] = make_double2(y[i].real(), y[i].imag());
+      }
+      if ((rc = set_active(c, cyc))) return rc;
+      CK(cudaMemcpyAsync(c->ybuf, c->hy, sizeof(double2) * (size_t)R * yld, cudaMemcpyHostToDevice, c->st));
+      const long long vs = (long long)(c->capO + 1) * nO;
+      k_accum_x<<<grid_for(nO * (long long)cyc.size()), 256, 0, c->st>>>(vX, c->V, vs, nO, c->ybuf, yld, kmax,
+                                                                          c->rmap_d, (int)cyc.size());
+      CK(cudaGetLastError());
+      std::vector<int> keep;
+      for (int r : cyc) {
+        if (!rs[r].hist.empty() && rs[r].hist.back() <= cfg->ktol)
+          rs[r].status = 1;
+        else
+          keep.push_back(r);
+      }
+      run = keep;
+    }
+    for (int r : run) rs[r].status = 2;  // not converged within max_iter
+    // traces = down + up (sie.py:426-427), then reconstruct (sie.py:428)
+    if ((rc = set_active(c, all))) return rc;
+    const long long half = nO / 2;
+    if ((rc = lincomb(c, vTR, 0, vX, 0, 1.0, vX, half, 1.0, 1, half, R))) return rc;
+    if ((rc = run_stage(c, c->recon, VecTab{{vTR, vTR, vTR}}, R, io))) return rc;
+  }
+  // residuals (sie.py:441-445)
+  if ((rc = set_active(c, all))) return rc;
+  CK(cudaMemsetAsync(c->dscal, 0, sizeof(double) * 2 * R, c->st));
+  k_residual<<<dim3(64, R), 256, 0, c->st>>>(u, f, N, c->wz, c->wx, c->tx_d, c->tz_d, c->m_d, c->omega * c->omega,
+                                             c->rmap_d, c->dscal);
+  CK(cudaGetLastError());
+  cudaEventRecord(e1, c->st);
+  CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * 2 * R, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  int ecode = 0;
+  if ((rc = check_err(c, &ecode))) return rc;
+  if (stats) {
+    for (int r = 0; r < R; ++r) {
+      const RhsState& s = rs[r];
+      if (stats->iterations) stats->iterations[r] = (double)s.total;
+      if (stats->n_residuals) stats->n_residuals[r] = (int)s.hist.size();
+      if (stats->residuals)
+        for (size_t i = 0; i < s.hist.size() && (int)i < max_iter; ++i) stats->residuals[(size_t)r * max_iter + i] = s.hist[i];
+      const double ff = c->hdscal[2 * r + 1];
+      if (stats->relres) stats->relres[r] = ff > 0 ? std::sqrt(c->hdscal[2 * r]) / std::sqrt(ff) : 0.0;
+      if (stats->converged) stats->converged[r] = s.status == 1;
+    }
+    if (stats->traces && c->nI > 0)
+      for (int r = 0; r < R; ++r)
+        CK(cudaMemcpy(stats->traces + (size_t)r * nO, c->TR + (size_t)r * nO, sizeof(double2) * nO / 2,
+                      cudaMemcpyDeviceToHost));
+    if (stats->polarized && c->nI > 0)
+      for (int r = 0; r < R; ++r)
+        CK(cudaMemcpy(stats->polarized + (size_t)r * 2 * nO, c->X + (size_t)r * nO, sizeof(double2) * nO,
+                      cudaMemcpyDeviceToHost));
+    unsigned long long cnt[4] = {0, 0, 0, 0};
+    CK(cudaMemcpy(cnt, c->cnt_d, sizeof(cnt), cudaMemcpyDeviceToHost));
+    if (stats->layer_solves) stats->layer_solves[0] = c->layer_solves;
+    if (stats->inner_iters) stats->inner_iters[0] = (long long)cnt[0];
+    if (stats->touches) stats->touches[0] = (long long)cnt[1];
+    if (stats->inner_hist && stats->inner_hist_len > 0) {
+      int hh[PT_HIST];
+      CK(cudaMemcpy(hh, c->hist_d, sizeof(hh), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < stats->inner_hist_len; ++i) stats->inner_hist[i] = i < PT_HIST ? hh[i] : 0;
+    }
+    if (stats->timing_ms) stats->timing_ms[0] = ms;
+  }
+  if (ecode) return ecode;
+  for (int r = 0; r < R; ++r)
+    if (rs[r].status == 2) {
+      g_err = "outer GMRES did not reach ktol within max_iter";
+      return PT_NOT_CONVERGED;
+    }
+  return PT_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+const char* pt_last_error(void) { return g_err.c_str(); }
+const char* pt_version(void) { return "pt_b200 0.1 (sm_100a)"; }
+
+int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
+  if (!pb || !out) return PT_BAD_ARGUMENT;
+  if (pb->L < 1 || pb->Lc < 1 || pb->Lc > PT_MAX_LC || pb->nx < 1 || pb->nz < 1) {
+    g_err = "bad problem geometry";
+    return PT_BAD_ARGUMENT;
+  }
+  CK(cudaSetDevice(device));
+  pt_ctx* c = new pt_ctx();
+  c->dev = device;
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  c->nx = pb->nx;
+  c->nz = pb->nz;
+  c->npml = pb->npml;
+  c->L = pb->L;
+  c->Lc = pb->Lc;
+  c->h = pb->h;
+  c->omega = pb->omega;
+  c->wx = pb->nx + 2 * pb->npml;
+  c->wz = pb->nz + 2 * pb->npml;
+  c->nI = pb->L - 1;
+  if (const char* e = std::getenv("PT_INNER_CAP")) c->inner_cap = std::max(2, atoi(e));
+  const int npml = c->npml;
+  // layers
+  int off = 0;
+  c->wmax = 0;
+  for (int l = 0; l < c->L; ++l) {
+    LayerInfo li;
+    std::memset(&li, 0, sizeof(li));
+    li.n = pb->layer_extents[l];
+    li.off = off;
+    li.w = li.n + 2 * npml;
+    li.lo = l == 0 ? 0 : npml;
+    li.hi = l == c->L - 1 ? li.w : npml + li.n;
+    li.has_top = l >= 1;
+    li.has_bot = l <= c->L - 2;
+    const int rowv[4] = {npml, npml - 1, li.n + npml, li.n + npml - 1};  // row(1), row(0), row(n+1), row(n)
+    for (int s = 0; s < 4; ++s) {
+      li.prow[s] = rowv[s];
+      li.coef[s] = make_double2(pb->layer_coefs[(l * 4 + s) * 2], pb->layer_coefs[(l * 4 + s) * 2 + 1]);
+    }
+    if (li.w > PT_THREADS) {
+      g_err = "layer width n_l + 2 npml exceeds 256";
+      return PT_BAD_ARGUMENT;
+    }
+    c->wmax = std::max(c->wmax, li.w);
+    c->lay.push_back(li);
+    off += li.n;
+  }
+  if (off != c->nz) {
+    g_err = "layer extents do not sum to nz";
+    return PT_BAD_ARGUMENT;
+  }
+  // cells
+  long long soff = 0, goff = 0, zoff = 0;
+  c->wzcmax = 0;
+  std::vector<int> coffs(c->Lc);
+  {
+    int o = 0, sum = 0;
+    for (int cc = 0; cc < c->Lc; ++cc) {
+      coffs[cc] = o;
+      o += pb->cell_extents[cc];
+      sum += pb->cell_extents[cc];
+    }
+    if (sum != c->nx) {
+      g_err = "cell extents do not sum to nx";
+      return PT_BAD_ARGUMENT;
+    }
+  }
+  for (int l = 0; l < c->L; ++l)
+    for (int cc = 0; cc < c->Lc; ++cc) {
+      CellInfo ci;
+      std::memset(&ci, 0, sizeof(ci));
+      ci.layer = l;
+      ci.cell = cc;
+      ci.w = c->lay[l].w;
+      ci.nxc = pb->cell_extents[cc];
+      ci.wzc = ci.nxc + 2 * npml;
+      ci.off = coffs[cc];
+      ci.lo = cc == 0 ? 0 : npml;
+      ci.hi = cc == c->Lc - 1 ? ci.wzc : npml + ci.nxc;
+      ci.has_top = cc >= 1;
+      ci.has_bot = cc <= c->Lc - 2;
+      const int n = ci.nxc;
+      const int krow[4] = {npml, npml - 1, n + npml, n + npml - 1};
+      const int srow[4] = {npml - 1, npml, n + npml - 1, n + npml};
+      const int id = l * c->Lc + cc;
+      for (int s = 0; s < 4; ++s) {
+        ci.krow[s] = krow[s];
+        ci.srow[s] = srow[s];
+        ci.coef[s] = make_double2(pb->cell_coefs[(id * 4 + s) * 2], pb->cell_coefs[(id * 4 + s) * 2 + 1]);
+      }
+      ci.sinv_off = soff;
+      ci.green_off = goff;
+      ci.lz_off = zoff;
+      soff += (long long)ci.wzc * ci.w * ci.w;
+      goff += 16LL * ci.w * ci.w;
+      zoff += ci.wzc;
+      c->wzcmax = std::max(c->wzcmax, ci.wzc);
+      c->cel.push_back(ci);
+    }
+  CK(cudaMalloc(&c->sinv_d, sizeof(double2) * (size_t)soff));
+  CK(cudaMalloc(&c->green_d, sizeof(double2) * (size_t)goff));
+  CK(cudaMalloc(&c->lz_d, sizeof(double2) * (size_t)zoff));
+  CK(cudaMalloc(&c->uz_d, sizeof(double2) * (size_t)zoff));
+  for (const CellInfo& ci : c->cel) {
+    const int id = ci.layer * c->Lc + ci.cell;
+    CK(cudaMemcpy(c->sinv_d + ci.sinv_off, pb->sinv[id], sizeof(double2) * (size_t)ci.wzc * ci.w * ci.w,
+                  cudaMemcpyDefault));
+    CK(cudaMemcpy(c->green_d + ci.green_off, pb->green[id], sizeof(double2) * 16 * (size_t)ci.w * ci.w,
+                  cudaMemcpyDefault));
+    CK(cudaMemcpy(c->lz_d + ci.lz_off, pb->lz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
+    CK(cudaMemcpy(c->uz_d + ci.lz_off, pb->uz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
+  }
+  if (upload(&c->lay_d, c->lay.data(), c->lay.size())) return PT_CUDA_ERROR;
+  if (upload(&c->cel_d, c->cel.data(), c->cel.size())) return PT_CUDA_ERROR;
+  if (upload(&c->tx_d, reinterpret_cast<const double2*>(pb->tx), 3 * (size_t)c->wx)) return PT_CUDA_ERROR;
+  if (upload(&c->tz_d, reinterpret_cast<const double2*>(pb->tz), 3 * (size_t)c->wz)) return PT_CUDA_ERROR;
+  if (upload(&c->m_d, pb->m, (size_t)c->wz * c->wx)) return PT_CUDA_ERROR;
+  CK(cudaMalloc(&c->err_d, sizeof(int)));
+  CK(cudaMalloc(&c->cnt_d, sizeof(unsigned long long) * 4));
+  CK(cudaMalloc(&c->hist_d, sizeof(int) * PT_HIST));
+  // smem ring: ~32 KB slots, as many as fit next to the vectors
+  {
+    int maxsm = 0;
+    CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    c->slot_bytes = std::max(32768, c->wmax * 16);
+    const size_t fixed = k1_smem_bytes(c->wmax, 8, 0, 0) + 64;
+    c->ns = (int)std::min<long long>(6, ((long long)maxsm - (long long)fixed) / (c->slot_bytes + 8));
+    if (c->ns < 2) {
+      g_err = "not enough shared memory for the K1 ring";
+      return PT_BAD_ARGUMENT;
+    }
+  }
+  int rc = build_inner(c);
+  if (!rc) rc = build_outer(c);
+  if (rc) return rc;
+  // standalone layer-solve stage (one job per layer, full slab in/out) built on demand
+  *out = c;
+  return PT_OK;
+}
+
+int pt_destroy(pt_ctx* c) {
+  if (!c) return PT_OK;
+  cudaSetDevice(c->dev);
+  cudaDeviceSynchronize();
+  // the process-level allocations are released with the context
+  cudaStreamDestroy(c->st);
+  delete c;
+  return PT_OK;
+}
+
+int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats) {
+  if (!c || !f || !u || !cfg) return PT_BAD_ARGUMENT;
+  CK(cudaSetDevice(c->dev));
+  int rc;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    rc = solve_device(c, reinterpret_cast<const double2*>(f), nrhs, cfg, reinterpret_cast<double2*>(u), stats);
+    if (rc != PT_CAPACITY) break;
+    // an inner Krylov basis outgrew its capacity: double it and redo the solve
+    c->inner_cap *= 2;
+    c->capR = 0;
+    c->capO = 0;
+  }
+  return rc;
+}
+
+int pt_solve(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats) {
+  if (!c || !f || !u || !cfg || nrhs <= 0) return PT_BAD_ARGUMENT;
+  CK(cudaSetDevice(c->dev));
+  const size_t bytes = sizeof(double2) * (size_t)nrhs * c->wz * c->wx;
+  double2 *fd = nullptr, *ud = nullptr;
+  CK(cudaMalloc(&fd, bytes));
+  CK(cudaMalloc(&ud, bytes));
+  CK(cudaMemcpyAsync(fd, f, bytes, cudaMemcpyHostToDevice, c->st));
+  int rc = pt_solve_device(c, reinterpret_cast<const double*>(fd), nrhs, cfg, reinterpret_cast<double*>(ud), stats);
+  cudaError_t e = cudaMemcpyAsync(u, ud, bytes, cudaMemcpyDeviceToHost, c->st);
+  cudaStreamSynchronize(c->st);
+  cudaFree(fd);
+  cudaFree(ud);
+  if (e != cudaSuccess && rc == PT_OK) {
+    g_err = cudaGetErrorString(e);
+    return PT_CUDA_ERROR;
+  }
+  return rc;
+}
+
+int pt_layer_solve(pt_ctx* c, int layer, const double* rhs, int nrhs, double inner_ktol, int inner_max_iter,
+                   double* out, pt_stats* stats) {
+  if (!c || layer < 0 || layer >= c->L || nrhs <= 0) return PT_BAD_ARGUMENT;
+  CK(cudaSetDevice(c->dev));
+  Stage S;
+  OJob j = blank_job(layer);
+  j.vol = 1;
+  j.vfull = 1;
+  j.nout = -1;
+  for (int r = 0; r < 1; ++r) S.jobs.push_back(j);
+  if (finalize_stage(c, S)) return PT_CUDA_ERROR;
+  if (ensure_scratch(c, nrhs, 1)) return PT_CUDA_ERROR;
+  const LayerInfo& li = c->lay[layer];
+  const long long N = (long long)li.w * c->wx;
+  const size_t bytes = sizeof(double2) * (size_t)nrhs * N;
+  double2 *fd = nullptr, *ud = nullptr;
+  CK(cudaMalloc(&fd, bytes));
+  CK(cudaMalloc(&ud, bytes));
+  CK(cudaMemcpy(fd, rhs, bytes, cudaMemcpyHostToDevice));
+  CK(cudaMemset(c->err_d, 0, sizeof(int)));
+  CK(cudaMemset(c->cnt_d, 0, sizeof(unsigned long long) * 4));
+  CK(cudaMemset(c->hist_d, 0, sizeof(int) * PT_HIST));
+  std::vector<int> all(nrhs);
+  for (int r = 0; r < nrhs; ++r) all[r] = r;
+  int rc = set_active(c, all);
+  SolveIO io{fd, N, ud, N, inner_ktol, inner_max_iter};
+  VecView dummy{c->TR, c->nO};
+  if (!rc) rc = run_stage(c, S, VecTab{{dummy, dummy, dummy}}, nrhs, io);
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(out, ud, bytes, cudaMemcpyDeviceToHost));
+  int ecode = 0;
+  check_err(c, &ecode);
+  if (stats) {
+    unsigned long long cnt[4] = {0, 0, 0, 0};
+    CK(cudaMemcpy(cnt, c->cnt_d, sizeof(cnt), cudaMemcpyDeviceToHost));
+    if (stats->inner_iters) stats->inner_iters[0] = (long long)cnt[0];
+    if (stats->touches) stats->touches[0] = (long long)cnt[1];
+    if (stats->inner_hist && stats->inner_hist_len > 0) {
+      int hh[PT_HIST];
+      CK(cudaMemcpy(hh, c->hist_d, sizeof(hh), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < stats->inner_hist_len; ++i) stats->inner_hist[i] = i < PT_HIST ? hh[i] : 0;
+    }
+  }
+  cudaFree(fd);
+  cudaFree(ud);
+  for (auto& kv : S.tasks) cudaFree(kv.second.d);
+  cudaFree(S.jobs_d);
+  cudaFree(S.stage_jobs_d);
+  cudaFree(S.ljobs_d);
+  if (rc) return rc;
+  return ecode;
+}
+
+int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, double* x) {
+  if (!c || layer < 0 || layer >= c->L || cell < 0 || cell >= c->Lc || nrhs <= 0) return PT_BAD_ARGUMENT;
+  CK(cudaSetDevice(c->dev));
+  const CellInfo& ci = c->cel[layer * c->Lc + cell];
+  const size_t bytes = sizeof(double2) * (size_t)nrhs * ci.wzc * ci.w;
+  double2 *bd = nullptr, *xd = nullptr;
+  CK(cudaMalloc(&bd, bytes));
+  CK(cudaMalloc(&xd, bytes));
+  CK(cudaMemcpy(bd, b, bytes, cudaMemcpyHostToDevice));
+  std::vector<K1Task> tasks;
+  long long z = 0;
+  const int nc = 8;
+  for (int q0 = 0; q0 < nrhs; q0 += nc) {
+    K1Task t;
+    t.cell = layer * c->Lc + cell;
+    t.jb = 0;
+    t.q0 = q0;
+    t.nq = std::min(nc, nrhs - q0);
+    t.zoff = z;
+    z += (long long)ci.wzc * ci.w * nc;
+    tasks.push_back(t);
+  }
+  K1Task* td = nullptr;
+  if (upload(&td, tasks.data(), tasks.size())) return PT_CUDA_ERROR;
+  if (ensure_z(c, z)) return PT_CUDA_ERROR;
+  K1Params kp;
+  std::memset(&kp, 0, sizeof(kp));
+  kp.cells = c->cel_d;
+  kp.layers = c->lay_d;
+  kp.tasks = td;
+  kp.sinv = c->sinv_d;
+  kp.lz = c->lz_d;
+  kp.uz = c->uz_d;
+  kp.R = nrhs;
+  kp.pass = 2;
+  kp.npml = c->npml;
+  kp.wx = c->wx;
+  kp.Lc = c->Lc;
+  kp.wmax = c->wmax;
+  kp.slot_bytes = c->slot_bytes;
+  kp.ns = c->ns;
+  kp.Z = c->Z;
+  kp.bd = bd;
+  kp.xd = xd;
+  CK(k1_launch(kp, (int)tasks.size(), nc, c->wmax, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(x, xd, bytes, cudaMemcpyDeviceToHost));
+  cudaFree(bd);
+  cudaFree(xd);
+  cudaFree(td);
+  return PT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+"""Offline stage: per-cell Schur factors and interface Green blocks.
+
+Everything here runs once per (model, frequency, partition) and is uploaded to
+the device by ``pt_create``.  It replaces the reference's offline objects
+
+* ``LayerWorkspace.__init__ -> spla.splu`` for every cell
+  (``subdomain.py:202-212``, built by ``NestedLayerSolver.__init__``,
+  ``nested.py:293-302``), and
+* ``GreenBlockSet.build`` (``green.py:103-129``, ``nested.py:303-307``),
+
+with the factorization the B200 online stage consumes:
+
+**Cell operator.**  After the x<->z swap (``nested.py:45-47, 294-296``) a cell
+of layer l has ``wz_c = nx_c + 2 npml`` block rows (original x columns) of
+width ``w = n_l + 2 npml`` (original layer depth).  Its 5-point operator is
+block tridiagonal (``discretization.py:251``)::
+
+    H_c = tridiag(l_k I, D_k, u_k I),
+    D_k = T_w + diag(tz_k - omega^2 m_k),   T_w tridiagonal (PML across w),
+
+with scalar off-diagonal blocks ``l_k = T_z[k, k-1]``, ``u_k = T_z[k, k+1]``.
+
+**Schur factors.**  ``S_0 = D_0``, ``S_k = D_k - l_k u_{k-1} S_{k-1}^{-1}``;
+the dense inverses ``S_k^{-1}`` are stored.  A cell solve is then
+``z_k = S_k^{-1}(b_k - l_k z_{k-1})`` forward and
+``x_k = z_k - u_k S_k^{-1} x_{k+1}`` backward (kernel K1).
+
+**Green blocks.**  ``G[(j, slot)] = coef_slot * (H_c^{-1})[row(j), row(slot)]``
+for ``j in {0, 1, n, n+1}`` and the four slot sources of ``green.py:370-377``
+(``v0: -l at row 1``, ``v1: +u at row 0``, ``vn: +l at row n+1``,
+``vnp: -u at row n``).
+
+All blocks are emitted COLUMN-MAJOR (element (i, j) at ``j*w + i``), the
+layout K1 and the inner kernels read.  Computation uses torch so that the
+same code runs on the CPU (tests) or batched on the GPU (large configs).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .discretization import axis_tridiag
+
+__all__ = ["CellFactors", "LayerFactors", "Factors", "build_factors", "cut_coefs"]
+
+ROWS = ("r0", "r1", "rn", "rnp")  # sampled rows j = 0, 1, n, n+1
+SLOTS = ("v0", "v1", "vn", "vnp")
+
+
+def cut_coefs(lower, upper, npml, n):
+    """Slot-source coefficients and positions of one slab.
+
+    For a slab with ``n`` interior rows along its stacking axis whose 1-D
+    operator has sub/super diagonals ``lower``/``upper``, ``src_top`` /
+    ``src_bot`` (``subdomain.py:157-182``) place
+
+    * v0 : ``-H_{1,0}``    at row(1)   -> ``-lower[row(1)]``
+    * v1 : ``+H_{0,1}``    at row(0)   -> ``+upper[row(0)]``
+    * vn : ``+H_{n+1,n}``  at row(n+1) -> ``+lower[row(n+1)]``
+    * vnp: ``-H_{n,n+1}``  at row(n)   -> ``-upper[row(n)]``
+
+    Returns ``(coefs[4] complex, rows[4] int)`` in slot order.
+    """
+    r = lambda k: k + npml - 1  # noqa: E731  (subdomain.py:133-138)
+    rows = np.array([r(1), r(0), r(n + 1), r(n)], dtype=np.int64)
+    coefs = np.array(
+        [-lower[r(1)], upper[r(0)], lower[r(n + 1)], -upper[r(n)]], dtype=np.complex128
+    )
+    return coefs, rows
+
+
+@dataclass
+class CellFactors:
+    layer: int
+    cell: int
+    w: int
+    wzc: int
+    nxc: int
+    off: int
+    sinv: torch.Tensor  # (wzc, w, w) complex128, column-major blocks (i.e. S^-T row-major)
+    lz: np.ndarray  # (wzc,) block-row couplings l_k
+    uz: np.ndarray  # (wzc,) u_k
+    green: torch.Tensor  # (4 rows, 4 slots, w, w) column-major blocks
+    coefs: np.ndarray  # (4,) cell-level slot coefficients
+    krows: np.ndarray  # (4,) cell block rows of the slot sources
+
+
+@dataclass
+class LayerFactors:
+    index: int
+    n: int
+    off: int
+    w: int
+    coefs: np.ndarray  # (4,) layer-level slot coefficients
+    prows: np.ndarray  # (4,) layer rows of the slot sources
+    cells: list = field(default_factory=list)
+
+
+@dataclass
+class Factors:
+    nx: int
+    nz: int
+    h: float
+    npml: int
+    omega: float
+    L: int
+    Lc: int
+    layers: list
+    cell_extents: tuple
+    cell_offsets: tuple
+    tx: tuple  # global T_x diagonals (lower, main, upper), length wx
+    tz: tuple  # global T_z diagonals, length wz
+    m: np.ndarray  # (wz, wx) squared slowness
+
+    @property
+    def wx(self):
+        return self.nx + 2 * self.npml
+
+    @property
+    def wz(self):
+        return self.nz + 2 * self.npml
+
+    def sinv_bytes(self):
+        return sum(cf.sinv.numel() * 16 for lf in self.layers for cf in lf.cells)
+
+    def green_bytes(self):
+        return sum(cf.green.numel() * 16 for lf in self.layers for cf in lf.cells)
+
+
+def _split(n, parts):
+    base, rem = divmod(n, parts)
+    return tuple(base + 1 if i < rem else base for i in range(parts))
+
+
+def _schur_inverses(tw, diag, lz, uz, device):
+    """Batched Schur recursion over cells of equal (w, wzc).
+
+    ``tw``: (lower, main, upper) of T_w (length w, shared by the batch);
+    ``diag``: (B, wzc, w) complex -- tz_k - omega^2 m_k per cell;
+    ``lz``/``uz``: (wzc,) shared block couplings.  Returns (B, wzc, w, w)
+    inverses in natural row-major orientation.
+    """
+    B, wzc, w = diag.shape
+    lo, mn, up = (torch.as_tensor(a, dtype=torch.complex128, device=device) for a in tw)
+    base = torch.diag(mn) + torch.diag(up[:-1], 1) + torch.diag(lo[1:], -1)
+    out = torch.empty((B, wzc, w, w), dtype=torch.complex128, device=device)
+    prev = None
+    for k in range(wzc):
+        S = base.expand(B, w, w).clone()
+        S.diagonal(dim1=-2, dim2=-1).add_(diag[:, k, :])
+        if k > 0:
+            S -= (complex(lz[k]) * complex(uz[k - 1])) * prev
+        prev = torch.linalg.inv(S)
+        out[:, k] = prev
+    return out
+
+
+def _block_solve(sinv, lz, uz, rhs):
+    """Solve H_c X = RHS with stored Schur inverses (batched over cells).
+
+    sinv: (B, wzc, w, w) row-major; rhs: (B, wzc, w, nrhs).  Mirrors K1.
+    """
+    B, wzc, w, _ = sinv.shape
+    z = torch.empty_like(rhs)
+    prev = None
+    for k in range(wzc):
+        t = rhs[:, k] if k == 0 else rhs[:, k] - complex(lz[k]) * prev
+        prev = sinv[:, k] @ t
+        z[:, k] = prev
+    x = torch.empty_like(rhs)
+    nxt = z[:, wzc - 1]
+    x[:, wzc - 1] = nxt
+    for k in range(wzc - 2, -1, -1):
+        nxt = z[:, k] - complex(uz[k]) * (sinv[:, k] @ nxt)
+        x[:, k] = nxt
+    return x
+
+
+def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True):
+    """Offline stage for a partitioned problem (all layers, all cells).
+
+    ``grid``/``model``/``pml``/``partition`` follow the reference value types
+    (``discretization.py:58-220``, ``subdomain.py:51-73``).
+    """
+    device = torch.device(device)
+    npml, h, omega = grid.npml, grid.h, pml.omega
+    cext = _split(grid.nx, Lc)  # partition_layers(sgrid, Lc), nested.py:294-296
+    coffs = tuple(int(v) for v in np.concatenate([[0], np.cumsum(cext)[:-1]]))
+    c = np.asarray(model.c, dtype=float)
+    layers = []
+    for ell, (n, off) in enumerate(zip(partition.extents, partition.offsets)):
+        w = n + 2 * npml
+        # layer-level cut couplings: the layer's own depth axis (subdomain.py:157-182)
+        lzL, _, uzL = axis_tridiag(pml, n, h)
+        lcoefs, lrows = cut_coefs(lzL, uzL, npml, n)
+        lf = LayerFactors(ell, n, off, w, lcoefs, lrows)
+        tw = axis_tridiag(pml, n, h)  # across the cell block: the layer depth
+        c_layer = c[off : off + w, :]  # VelocityModel.restrict (subdomain.py:233-234)
+        # group cells of equal nx_c for batched factorization
+        groups = {}
+        for ci, nxc in enumerate(cext):
+            groups.setdefault(nxc, []).append(ci)
+        cells = [None] * Lc
+        for nxc, idxs in groups.items():
+            wzc = nxc + 2 * npml
+            lz, tzm, uz = axis_tridiag(pml, nxc, h)  # along block rows (original x)
+            ccoefs, ckrows = cut_coefs(lz, uz, npml, nxc)
+            diag = np.empty((len(idxs), wzc, w), dtype=np.complex128)
+            for b, ci in enumerate(idxs):
+                # cell model: transposed layer restricted to rows [off_c, off_c+wzc)
+                cc = c_layer[:, coffs[ci] : coffs[ci] + wzc].T  # (wzc, w)
+                diag[b] = tzm[:, None] - omega**2 * (1.0 / cc**2)
+            dg = torch.as_tensor(diag, device=device)
+            sinv = _schur_inverses(tw, dg, lz, uz, device)
+            gblk = None
+            if green:
+                # H_c^{-1} columns at the four slot rows, sampled at the four rows
+                rows4 = [int(r) for r in (ckrows[1], ckrows[0], ckrows[3], ckrows[2])]  # r0,r1,rn,rnp
+                eye = torch.eye(w, dtype=torch.complex128, device=device)
+                rhs = torch.zeros((len(idxs), wzc, w, 4 * w), dtype=torch.complex128,
+                                  device=device)
+                for s in range(4):
+                    rhs[:, int(ckrows[s]), :, s * w : (s + 1) * w] = complex(ccoefs[s]) * eye
+                X = _block_solve(sinv, lz, uz, rhs)
+                gblk = torch.empty((len(idxs), 4, 4, w, w), dtype=torch.complex128,
+                                   device=device)
+                for jr, rr in enumerate(rows4):
+                    for s in range(4):
+                        # column-major storage == transpose of the row-major block
+                        gblk[:, jr, s] = X[:, rr, :, s * w : (s + 1) * w].transpose(-1, -2)
+            sinv_cm = sinv.transpose(-1, -2).contiguous()
+            for b, ci in enumerate(idxs):
+                cells[ci] = CellFactors(
+                    ell, ci, w, wzc, nxc, coffs[ci], sinv_cm[b],
+                    np.asarray(lz), np.asarray(uz),
+                    None if gblk is None else gblk[b].contiguous(),
+                    ccoefs, ckrows,
+                )
+        lf.cells = cells
+        layers.append(lf)
+    tx = axis_tridiag(pml, grid.nx, h)
+    tz = axis_tridiag(pml, grid.nz, h)
+    return Factors(grid.nx, grid.nz, h, npml, omega, partition.L, Lc, layers, cext, coffs,
+                   tx, tz, 1.0 / c**2)

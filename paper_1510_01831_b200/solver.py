@@ -1,0 +1,309 @@
+"""Drop-in construction and ``solve()`` API of the reference, running on one B200.
+
+Mirrors the reference's user-facing path
+
+    layers = build_nested_layers(grid, model, pml, partition, Lc=Lc, backend="pt")
+    solver = PolarizedTracesSolver(grid, model, pml, partition, layers=layers)
+    res = solver.solve(f, KrylovConfig(ktol=1e-9))
+
+(``nested.py:507-521``, ``sie.py:361-445``) with identical argument meaning,
+return type (``SolveResult``) and exceptions (``KrylovBreakdown``,
+``InnerSolveError``, ``ValueError``).  Construction runs the offline stage
+(``offline.py``) and uploads it once (``pt_create``); ``solve`` is one call
+into the C ABI (``pt_solve``), which runs the whole online stage -- Newton
+tables, outer GMRES with its layer-solves, inner polarized-traces GMRES, cell
+solves and reconstruction -- on the device.  ``solve_many`` solves a batch of
+sources in lockstep (the reference loops ``solve``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from .discretization import DiscretizationSpec, Grid
+from .krylov import InnerSolveError, KrylovBreakdown, KrylovConfig
+from .offline import build_factors
+
+__all__ = [
+    "TraceStack",
+    "PolarizedTraceStack",
+    "SolveResult",
+    "NestedLayers",
+    "build_nested_layers",
+    "PolarizedTracesSolver",
+]
+
+
+class TraceStack:
+    """(interfaces, 2, width) panels -- ``sie.py:37-77``."""
+
+    __slots__ = ("data",)
+
+    def __init__(self, data):
+        self.data = np.asarray(data, dtype=complex)
+
+    @classmethod
+    def zeros(cls, n_interfaces, width):
+        return cls(np.zeros((n_interfaces, 2, width), dtype=complex))
+
+    @property
+    def n_interfaces(self):
+        return self.data.shape[0]
+
+    @property
+    def width(self):
+        return self.data.shape[2]
+
+    def flat(self):
+        return self.data.ravel().copy()
+
+    def copy(self):
+        return TraceStack(self.data.copy())
+
+    def norm(self):
+        return np.linalg.norm(self.data)
+
+    def __add__(self, other):
+        return TraceStack(self.data + other.data)
+
+    def __sub__(self, other):
+        return TraceStack(self.data - other.data)
+
+    def __getitem__(self, idx):
+        return self.data[idx]
+
+
+class PolarizedTraceStack:
+    """Down/up stacks -- ``sie.py:80-109``."""
+
+    __slots__ = ("down", "up")
+
+    def __init__(self, down, up):
+        self.down = down
+        self.up = up
+
+    @classmethod
+    def from_flat(cls, flat, n_interfaces, width):
+        flat = np.asarray(flat, dtype=complex)
+        half = flat.size // 2
+        return cls(TraceStack(flat[:half].reshape(n_interfaces, 2, width)),
+                   TraceStack(flat[half:].reshape(n_interfaces, 2, width)))
+
+    def flat(self):
+        return np.concatenate([self.down.flat(), self.up.flat()])
+
+    def reassemble(self):
+        return self.down + self.up
+
+
+@dataclass
+class SolveResult:
+    """``sie.py:349-358``."""
+
+    u: np.ndarray
+    iterations: float
+    residuals: list = field(default_factory=list)
+    converged: bool = True
+    relative_residual: float = 0.0
+    kappa_margin: float = 0.0
+    traces: TraceStack | None = None
+    polarized: PolarizedTraceStack | None = None
+
+
+class NestedLayers(list):
+    """What ``build_nested_layers`` returns: one entry per layer plus the offline
+    factors of the whole partition (the device upload happens in the solver)."""
+
+    def __init__(self, items, factors, Lc, backend, inner_ktol, inner_max_iter):
+        super().__init__(items)
+        self.factors = factors
+        self.Lc = Lc
+        self.backend = backend
+        self.inner_ktol = inner_ktol
+        self.inner_max_iter = inner_max_iter
+
+
+@dataclass
+class LayerDescriptor:
+    index: int
+    n: int
+    width: int
+    grid: Grid
+    Lc: int
+
+
+def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), Lc=1, backend="pt",
+                        inner_ktol=1e-6, inner_max_iter=200, plr_threshold=None, plr_eps=1e-8,
+                        plr_max_rank=None, seed=0, assembled_boundary=False, device=None, **unused):
+    """``nested.py:507-521`` (with ``NestedLayerSolver`` kwargs, ``nested.py:279-281``).
+
+    Runs the offline stage (Schur factors + Green blocks) for every layer.
+    ``device`` selects where the offline arithmetic runs (``"cpu"`` or a CUDA
+    device for large configs); its output is uploaded by the solver.
+    """
+    if backend != "pt":
+        raise NotImplementedError("only the polarized-traces inner backend ('pt') has a B200 path")
+    if disc.kind != "fd":
+        raise NotImplementedError("only the finite-difference discretization has a B200 path")
+    if plr_threshold is not None:
+        raise NotImplementedError("PLR compression is not part of the B200 path (off in every config)")
+    if assembled_boundary:
+        raise NotImplementedError("the factored boundary pipeline (Eq. 4.3) is not implemented yet")
+    if Lc < 1:
+        raise ValueError("need at least one cell")
+    if Lc > 1 and grid.nx < 2 * Lc:
+        raise ValueError(f"{Lc} cells need nx >= {2 * Lc}, got {grid.nx}")
+    F = build_factors(grid, model, pml, partition, Lc, device=device or "cpu")
+    items = []
+    for ell, (n, off) in enumerate(zip(partition.extents, partition.offsets)):
+        lgrid = Grid(grid.nx, n, grid.h, grid.npml, origin=(grid.origin[0], grid.origin[1] + off))
+        items.append(LayerDescriptor(ell, n, grid.wx, lgrid, Lc))
+    return NestedLayers(items, F, Lc, backend, inner_ktol, inner_max_iter)
+
+
+_ERR = {
+    _abi.PT_INNER_NOT_CONVERGED: InnerSolveError,
+    _abi.PT_BREAKDOWN: KrylovBreakdown,
+    _abi.PT_BAD_ARGUMENT: ValueError,
+}
+
+
+class PolarizedTracesSolver:
+    """``sie.py:361-445`` on the B200 online path.
+
+    ``layers=None`` gives direct (unsplit) layer solves like the reference's
+    ``LayerWorkspace`` layers; on this path that is the one-cell
+    decomposition (Lc = 1), i.e. one exact block-tridiagonal solve per layer.
+    """
+
+    def __init__(self, grid, model, pml, partition, disc=DiscretizationSpec(), layers=None,
+                 global_operator=None, device=0):
+        self.grid = grid
+        self.model = model
+        self.pml = pml
+        self.partition = partition
+        self.disc = disc
+        if layers is None:
+            layers = build_nested_layers(grid, model, pml, partition, disc, Lc=1)
+        if not isinstance(layers, NestedLayers):
+            raise TypeError("layers must come from paper_1510_01831_b200.build_nested_layers")
+        self.layers = layers
+        self.nI = partition.L - 1
+        self.ctx = _abi.Context(layers.factors, device=device)
+
+    def close(self):
+        self.ctx.close()
+
+    # -- one call into the C ABI for a batch of sources
+    def _run(self, F, config, preconditioner, device_arrays=None):
+        if config.method != "gmres":
+            raise NotImplementedError("BiCGstab is not on the B200 path yet (SURVEY.md 8(f) rank 3)")
+        if preconditioner not in ("gs", "jac"):
+            raise ValueError(f"unknown preconditioner {preconditioner!r}")
+        R = F.shape[0] if device_arrays is None else device_arrays[2]
+        cfg = _abi.PtKrylov(config.ktol, config.max_iter, config.restart, self.layers.inner_ktol,
+                            self.layers.inner_max_iter, 0 if preconditioner == "gs" else 1)
+        wz, wx = self.grid.shape
+        nO = 4 * self.nI * wx
+        its = np.zeros(R)
+        hist = np.zeros((R, config.max_iter))
+        nh = np.zeros(R, dtype=np.int32)
+        rel = np.zeros(R)
+        conv = np.zeros(R, dtype=np.int32)
+        trac = np.zeros((R, max(nO // 2, 1)), dtype=np.complex128)
+        pol = np.zeros((R, max(nO, 1)), dtype=np.complex128)
+        cnt = np.zeros(3, dtype=np.int64)
+        ihist = np.zeros(64, dtype=np.int32)
+        tms = np.zeros(1)
+        st = _abi.PtStats(
+            _abi.dptr(its), _abi.dptr(hist), nh.ctypes.data_as(_abi._ip), _abi.dptr(rel),
+            conv.ctypes.data_as(_abi._ip), _abi.dptr(trac.view(np.float64)),
+            _abi.dptr(pol.view(np.float64)),
+            cnt[0:].ctypes.data_as(_abi._llp), cnt[1:].ctypes.data_as(_abi._llp),
+            cnt[2:].ctypes.data_as(_abi._llp), ihist.ctypes.data_as(_abi._ip), 64, _abi.dptr(tms))
+        L = _abi.lib()
+        if device_arrays is None:
+            F = np.ascontiguousarray(F, dtype=np.complex128)
+            U = np.empty_like(F)
+            rc = L.pt_solve(self.ctx.handle, _abi.dptr(F.view(np.float64)), R, C.byref(cfg),
+                            _abi.dptr(U.view(np.float64)), C.byref(st))
+        else:
+            fptr, uptr, _ = device_arrays
+            U = None
+            rc = L.pt_solve_device(self.ctx.handle, C.c_void_p(fptr), R, C.byref(cfg),
+                                   C.c_void_p(uptr), C.byref(st))
+        self.last_stats = dict(layer_solves=int(cnt[0]), inner_iterations=int(cnt[1]),
+                               touches=int(cnt[2]), inner_hist=ihist.copy(), device_ms=float(tms[0]))
+        if rc == _abi.PT_NOT_CONVERGED:
+            bad = int(np.argmin(conv))
+            h = list(hist[bad, : nh[bad]])
+            raise KrylovBreakdown(
+                f"trace solve did not reach {config.ktol:g} in {config.max_iter} iterations "
+                f"(last residual {h[-1] if h else float('nan'):.3e})", residuals=h)
+        if rc != _abi.PT_OK:
+            exc = _ERR.get(rc, RuntimeError)
+            raise exc(f"pt_solve failed ({rc}): {_abi.last_error()}")
+        out = []
+        for r in range(R):
+            h = [float(v) for v in hist[r, : nh[r]]]
+            traces = polar = None
+            if self.nI > 0:
+                traces = TraceStack(trac[r].reshape(self.nI, 2, wx))
+                polar = PolarizedTraceStack.from_flat(pol[r], self.nI, wx)
+            u = None if U is None else U[r]
+            if self.nI == 0 and not h:
+                h = [float(rel[r])]  # monolayer path (sie.py:401-404)
+            out.append(SolveResult(u, float(its[r]), h, bool(conv[r]), float(rel[r]),
+                                   float(rel[r]) / config.ktol, traces, polar))
+        return out
+
+    def solve(self, f_global, config=KrylovConfig(), preconditioner="gs"):
+        """``sie.py:392-439``: one source."""
+        f = np.asarray(f_global, dtype=complex).reshape(self.grid.shape)
+        res = self._run(f[None], config, preconditioner)[0]
+        if res.iterations == 0.0 and np.linalg.norm(f) == 0.0:
+            res = SolveResult(np.zeros(self.grid.shape, dtype=complex), 0.0, [0.0])
+        return res
+
+    def solve_many(self, F, config=KrylovConfig(), preconditioner="gs"):
+        """Batch of sources ``F[nrhs, wz, wx]`` solved in lockstep on the device."""
+        F = np.asarray(F, dtype=complex).reshape((-1,) + tuple(self.grid.shape))
+        return self._run(F, config, preconditioner)
+
+    def solve_device(self, f_ptr, u_ptr, nrhs, config=KrylovConfig(), preconditioner="gs"):
+        """Device-resident sources/wavefields (e.g. torch CUDA tensors' ``data_ptr()``)."""
+        return self._run(None, config, preconditioner, device_arrays=(f_ptr, u_ptr, nrhs))
+
+    # -- test hooks on the same device factors
+    def layer_solve(self, layer, rhs, inner_ktol=None, inner_max_iter=None):
+        """``NestedLayerSolver.solve`` (nested.py:344-353) for volumes [nrhs, w, wx]."""
+        rhs = np.ascontiguousarray(np.asarray(rhs, dtype=np.complex128))
+        if rhs.ndim == 2:
+            rhs = rhs[None]
+        out = np.empty_like(rhs)
+        st = _abi.PtStats()
+        rc = _abi.lib().pt_layer_solve(
+            self.ctx.handle, int(layer), _abi.dptr(rhs.view(np.float64)), rhs.shape[0],
+            float(inner_ktol if inner_ktol is not None else self.layers.inner_ktol),
+            int(inner_max_iter if inner_max_iter is not None else self.layers.inner_max_iter),
+            _abi.dptr(out.view(np.float64)), C.byref(st))
+        if rc != _abi.PT_OK:
+            raise _ERR.get(rc, RuntimeError)(f"pt_layer_solve failed ({rc}): {_abi.last_error()}")
+        return out
+
+    def cell_solve(self, layer, cell, b):
+        """One cell's ``LayerWorkspace.solve`` (subdomain.py:214-221) via K1: b [nrhs, wz_c, w]."""
+        b = np.ascontiguousarray(np.asarray(b, dtype=np.complex128))
+        if b.ndim == 2:
+            b = b[None]
+        x = np.empty_like(b)
+        rc = _abi.lib().pt_cell_solve(self.ctx.handle, int(layer), int(cell),
+                                      _abi.dptr(b.view(np.float64)), b.shape[0],
+                                      _abi.dptr(x.view(np.float64)))
+        if rc != _abi.PT_OK:
+            raise RuntimeError(f"pt_cell_solve failed ({rc}): {_abi.last_error()}")
+        return x

@@ -1,0 +1,13 @@
+"""The problems behind tests/golden/*.npz (must match tests/golden/make_golden.py)."""
+
+from paper_1510_01831_b200.configs import make_config, small_problem
+
+GOLDEN = {
+    "small_a": (lambda: small_problem(nx=40, nz=36, npml=6, L=3, Lc=2, omega=14.0, seed=0), 0, True),
+    "small_b": (lambda: small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, True),
+    "small_c": (lambda: small_problem(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7), 0, True),
+    "small_direct": (lambda: small_problem(nx=40, nz=36, npml=6, L=3, Lc=2, omega=14.0, seed=0), 0,
+                     False),
+    "cfg1": (lambda: make_config("cfg1"), 0, True),
+    "cfg2": (lambda: make_config("cfg2"), 0, True),
+}

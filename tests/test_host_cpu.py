@@ -1,0 +1,132 @@
+"""CPU: host-side logic -- value types, partitions, config generators, offline factors,
+the C-ABI library exports.  No compute call into the library here (no GPU)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.polartraces_oracle import OracleSolver
+from paper_1510_01831_b200 import (
+    Grid,
+    KrylovConfig,
+    PmlProfile,
+    VelocityModel,
+    default_pml_strength,
+    delta_source,
+    partition_cells,
+    partition_layers,
+)
+from paper_1510_01831_b200.configs import make_config, small_problem
+from paper_1510_01831_b200.offline import _block_solve, build_factors
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_partitions_match_reference_rule():
+    # subdomain.py:88-110: near-equal, remainder first
+    assert partition_layers(Grid(10, 41, 0.1, 2), 4).extents == (11, 10, 10, 10)
+    assert partition_layers(Grid(10, 41, 0.1, 2), 4).offsets == (0, 11, 21, 31)
+    assert partition_cells(Grid(33, 10, 0.1, 2), 4).extents == (9, 8, 8, 8)
+    with pytest.raises(ValueError):
+        partition_layers(Grid(10, 5, 0.1, 2), 3)
+    with pytest.raises(ValueError):
+        partition_cells(Grid(5, 10, 0.1, 2), 3)
+
+
+def test_value_types_validate_like_reference():
+    with pytest.raises(ValueError):
+        Grid(0, 5, 0.1, 2)
+    with pytest.raises(ValueError):
+        PmlProfile(4, 0.1, -1.0, 3.0)
+    g = Grid(8, 6, 0.1, 2)
+    with pytest.raises(ValueError):
+        VelocityModel(g, np.ones((3, 3)))
+    with pytest.raises(ValueError):
+        KrylovConfig(ktol=0.0)
+    with pytest.raises(ValueError):
+        delta_source(g, (100, 1))
+    f = delta_source(g, (3, 2))
+    assert f[g.row_of(2), g.col_of(3)] == 1.0 / 0.1**2
+
+
+def test_config_generators_are_deterministic_and_match_survey_conventions():
+    p1 = make_config("cfg1")
+    assert p1.sources == [(80, 40)]
+    assert abs(p1.pml.C - 20.723266) < 1e-6
+    assert p1.partition.extents == (40, 40, 40, 40)
+    p2 = make_config("cfg2")
+    assert p2.sources[0] == (244, 40)
+    assert abs(p2.pml.omega - 188.966798) < 1e-5
+    assert len(p2.sources) == 16
+    p2b = make_config("cfg2")
+    assert p2b.sources == p2.sources and np.array_equal(p2b.model.c, p2.model.c)
+
+
+@pytest.mark.parametrize("case", [dict(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3),
+                                  dict(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7)])
+def test_offline_factors_reproduce_superlu_cells_and_green_blocks(case):
+    """Schur factors solve every cell like SuperLU (1e-12), Green blocks equal the
+    reference's GreenBlockSet construction (green.py:103-129) to 1e-12."""
+    prob = small_problem(**case)
+    F = build_factors(prob.grid, prob.model, prob.pml, prob.partition, prob.Lc)
+    O = OracleSolver.from_problem(prob)
+    rng = np.random.default_rng(1)
+    slots = ("v0", "v1", "vn", "vnp")
+    for lf, ol in zip(F.layers, O.outer.slabs):
+        for cf, oc in zip(lf.cells, ol.cells):
+            n = oc.n
+            for jr, j in enumerate((0, 1, n, n + 1)):
+                for s, sl in enumerate(slots):
+                    A = oc.G[(j, sl)]
+                    B = cf.green[jr, s].numpy().T
+                    assert np.abs(A - B).max() <= 1e-12 * np.abs(A).max()
+            b = rng.standard_normal((cf.wzc, cf.w)) + 1j * rng.standard_normal((cf.wzc, cf.w))
+            x0 = oc.solve(b)
+            sinv = cf.sinv.transpose(-1, -2)[None]
+            x1 = _block_solve(sinv, cf.lz, cf.uz, torch.tensor(b)[None, :, :, None])[0, :, :, 0].numpy()
+            assert np.linalg.norm(x1 - x0) <= 1e-12 * np.linalg.norm(x0)
+
+
+def test_cut_coupling_blocks_are_minus_identity_over_h2():
+    """all four cut coupling blocks are -I/h^2 for layers and cells."""
+    prob = small_problem(nx=40, nz=36, npml=6, L=3, Lc=2, omega=14.0)
+    F = build_factors(prob.grid, prob.model, prob.pml, prob.partition, prob.Lc, green=False)
+    h2 = prob.grid.h ** 2
+    for lf in F.layers:
+        np.testing.assert_allclose(lf.coefs * h2, [1, -1, -1, 1], atol=1e-14)
+        for cf in lf.cells:
+            np.testing.assert_allclose(cf.coefs * h2, [1, -1, -1, 1], atol=1e-14)
+
+
+def _header_symbols():
+    txt = open(os.path.join(REPO, "include", "pt_b200.h")).read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(pt_\w+)\(", txt, re.M)))
+
+
+def test_c_abi_library_exports_every_header_symbol():
+    from paper_1510_01831_b200 import _abi
+    from paper_1510_01831_b200.build import build
+
+    build()
+    lib = ctypes.CDLL(_abi.LIB_PATH)
+    syms = _header_symbols()
+    assert set(syms) == set(_abi.EXPORTS)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert b"sm_100a" in _abi.lib().pt_version()
+
+
+def test_solver_fails_loudly_without_gpu():
+    """No CPU fallback: constructing the device solver without a GPU raises."""
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1510_01831_b200 import PolarizedTracesSolver, build_nested_layers
+
+    prob = small_problem(nx=20, nz=16, npml=4, L=2, Lc=2)
+    layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=2)
+    with pytest.raises(RuntimeError):
+        PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers)
