@@ -19,6 +19,7 @@
  *                   the "layer object" protocol of sie.py:112-118 (test/plugin hook).
  *   pt_cell_solve   LayerWorkspace.solve on one cell (subdomain.py:214-221 -> SuperLU
  *                   solve): the K1 kernel alone (test hook).
+ *   pt_set_stream / pt_set_profiling: run on a caller stream (e.g. torch's) / time every launch.
  *   pt_destroy / pt_last_error / pt_version.
  *
  * Return codes (errors map to the reference's exceptions, sie.py:420-425,
@@ -92,9 +93,18 @@ typedef struct {
   int* inner_hist;           /* [inner_hist_len] histogram of inner iteration counts */
   int inner_hist_len;
   double* timing_ms;         /* [1] device time of the online solve (CUDA events) */
+  /* profiling (filled when pt_set_profiling(ctx, 1)): CUDA events around every launch */
+  double* kernel_ms;         /* [3] summed device time: K1 cell solves, inner GMRES, other kernels */
+  double* k1_bytes;          /* [1] algorithmic S^-1 bytes of all K1 launches: 32*wz_c*w_c^2 per cell solve */
+  long long* launches;       /* [1] kernels launched by this solve */
+  long long* k1_launches;    /* [1] K1 launches */
 } pt_stats;
 
 int pt_create(const pt_problem* prob, int device, pt_ctx** out);
+/* run subsequent work on a caller-owned cudaStream_t (NULL = the context's own stream) */
+int pt_set_stream(pt_ctx* ctx, void* stream);
+/* 1 = bracket every launch with CUDA events and report per-kernel-class times in pt_stats */
+int pt_set_profiling(pt_ctx* ctx, int enable);
 int pt_destroy(pt_ctx* ctx);
 
 int pt_solve(pt_ctx* ctx, const double* f, int nrhs, const pt_krylov* cfg, double* u,

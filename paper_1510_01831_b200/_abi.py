@@ -26,6 +26,8 @@ PT_CUDA_ERROR = -1
 EXPORTS = (
     "pt_create",
     "pt_destroy",
+    "pt_set_stream",
+    "pt_set_profiling",
     "pt_solve",
     "pt_solve_device",
     "pt_layer_solve",
@@ -64,6 +66,7 @@ class PtStats(C.Structure):
         ("converged", _ip), ("traces", _dp), ("polarized", _dp),
         ("layer_solves", _llp), ("inner_iters", _llp), ("touches", _llp),
         ("inner_hist", _ip), ("inner_hist_len", C.c_int), ("timing_ms", _dp),
+        ("kernel_ms", _dp), ("k1_bytes", _dp), ("launches", _llp), ("k1_launches", _llp),
     ]
 
 
@@ -76,6 +79,8 @@ def load():
     lib = C.CDLL(LIB_PATH)
     lib.pt_create.argtypes = [C.POINTER(PtProblem), C.c_int, C.POINTER(C.c_void_p)]
     lib.pt_destroy.argtypes = [C.c_void_p]
+    lib.pt_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+    lib.pt_set_profiling.argtypes = [C.c_void_p, C.c_int]
     lib.pt_solve.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(PtKrylov), _dp, C.POINTER(PtStats)]
     lib.pt_solve_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(PtKrylov), C.c_void_p,
                                     C.POINTER(PtStats)]
@@ -85,7 +90,7 @@ def load():
     lib.pt_last_error.restype = C.c_char_p
     lib.pt_version.restype = C.c_char_p
     for name in ("pt_create", "pt_destroy", "pt_solve", "pt_solve_device", "pt_layer_solve",
-                 "pt_cell_solve"):
+                 "pt_cell_solve", "pt_set_stream", "pt_set_profiling"):
         getattr(lib, name).restype = C.c_int
     return lib
 

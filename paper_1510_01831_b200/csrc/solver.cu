@@ -50,6 +50,7 @@ struct Stage {
     K1Task* d = nullptr;
     int n = 0, nc = 1;
     long long zsize = 0;
+    double bytes = 0.0;  // algorithmic S^-1 bytes of one pass: 32 wz_c w^2 per (cell, column)
   };
   std::map<int, Tasks> tasks;
 };
@@ -102,6 +103,8 @@ struct pt_ctx {
   double *dscal = nullptr, *hnorm = nullptr;
   double2 *hout = nullptr, *ybuf = nullptr;
   int* hrmap = nullptr;
+  double2 *io_f = nullptr, *io_u = nullptr;  // pt_solve staging buffers (reused)
+  size_t io_bytes = 0;
   double2* hhout = nullptr;
   double* hdscal = nullptr;
   double2* hy = nullptr;
@@ -109,6 +112,49 @@ struct pt_ctx {
   std::vector<int> act;
   int slot_bytes = 32768, ns = 5;
   long long layer_solves = 0;
+  // stream + profiling
+  cudaStream_t own_st = nullptr;
+  bool prof = false;
+  struct EvRec {
+    cudaEvent_t a, b;
+    int cls;  // 0 K1, 1 inner, 2 other
+  };
+  std::vector<cudaEvent_t> evpool;
+  size_t ev_next = 0;
+  std::vector<EvRec> evs;
+  double k1_bytes = 0.0;
+  long long launches = 0, k1_launches = 0;
+};
+
+static cudaEvent_t pool_event(pt_ctx* c) {
+  if (c->ev_next == c->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->evpool.push_back(e);
+  }
+  return c->evpool[c->ev_next++];
+}
+
+// Counts every launch; with profiling on, brackets it with CUDA events on the launch stream.
+struct LaunchScope {
+  pt_ctx* c;
+  int cls;
+  cudaEvent_t a = nullptr;
+  LaunchScope(pt_ctx* c_, int cls_) : c(c_), cls(cls_) {
+    c->launches++;
+    if (cls == 0) c->k1_launches++;
+    if (c->prof) {
+      a = pool_event(c);
+      cudaEventRecord(a, c->st);
+    }
+  }
+  ~LaunchScope() {
+    if (c->prof) {
+      cudaEvent_t b = pool_event(c);
+      cudaEventRecord(b, c->st);
+      c->evs.push_back({a, b, cls});
+    }
+  }
 };
 
 // ------------------------------------------------------------------ program builders
@@ -498,6 +544,7 @@ static Stage::Tasks* stage_tasks(pt_ctx* c, Stage& S, int Ract) {
         t.nq = std::min(nc, ncols - q0);
         t.zoff = z;
         z += (long long)ci.wzc * ci.w * nc;
+        T.bytes += 32.0 * ci.wzc * (double)ci.w * ci.w * t.nq;
         v.push_back(t);
       }
   }
@@ -531,6 +578,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   if (!T) return PT_CUDA_ERROR;
   if (ensure_z(c, T->zsize)) return PT_CUDA_ERROR;
   if (S.any_panel) {
+    LaunchScope ls(c, 2);
     k_gather_panels<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract,
                                                                                     c->wx, c->P);
     CK(cudaGetLastError());
@@ -565,7 +613,11 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   // possible per column, so stage buffers use compact q and f/u use q as well (callers compact f/u).
   if (c->Lc > 1) {
     kp.pass = 0;
-    CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
+    {
+      LaunchScope ls(c, 0);
+      CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
+      c->k1_bytes += T->bytes;
+    }
     InnerParams ip;
     std::memset(&ip, 0, sizeof(ip));
     ip.cells = c->cel_d;
@@ -597,11 +649,17 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     ip.hist = c->hist_d;
     ip.op_blocks = c->op_blocks;
     ip.pre_blocks = c->pre_blocks;
+    LaunchScope ls(c, 1);
     CK(inner_launch(ip, J, c->st));
   }
   kp.pass = 1;
-  CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
+  {
+    LaunchScope ls(c, 0);
+    CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
+    c->k1_bytes += T->bytes;
+  }
   if (S.any_sample) {
+    LaunchScope ls(c, 2);
     k_combine<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract, c->wx,
                                                                               c->smp);
     CK(cudaGetLastError());
@@ -613,6 +671,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
 static int lincomb(pt_ctx* c, VecView d, long long doff, VecView x, long long xoff, double a, VecView y,
                    long long yoff, double b, int use_y, long long len, int Ract) {
   if (len <= 0 || Ract == 0) return 0;
+  LaunchScope ls(c, 2);
   k_lincomb<<<grid_for(len * Ract), 256, 0, c->st>>>(d, doff, x, xoff, a, y, yoff, b, use_y, len, c->rmap_d, Ract);
   CK(cudaGetLastError());
   return 0;
@@ -709,6 +768,10 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   CK(cudaMemsetAsync(c->cnt_d, 0, sizeof(unsigned long long) * 4, c->st));
   CK(cudaMemsetAsync(c->hist_d, 0, sizeof(int) * PT_HIST, c->st));
   c->layer_solves = 0;
+  c->launches = c->k1_launches = 0;
+  c->k1_bytes = 0.0;
+  c->evs.clear();
+  c->ev_next = 0;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -717,6 +780,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   SolveIO io{f, N, u, N, cfg->inner_ktol, cfg->inner_max_iter};
   // zero-source detection (sie.py:397-399)
   CK(cudaMemsetAsync(c->dscal, 0, sizeof(double) * 2 * R, c->st));
+  { LaunchScope ls_(c, 2); }
   k_vol_norm2<<<dim3(64, R), 256, 0, c->st>>>(f, N, N, c->dscal);
   CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * R, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -752,6 +816,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     if ((rc = set_active(c, live))) return rc;
     const int Rl = (int)live.size();
     if ((rc = apply_pre(c, vB, vBp, vA, Rl, gs, io))) return rc;
+    { LaunchScope ls_(c, 2); }
     k_norm2<<<Rl, 256, 0, c->st>>>(vBp, nO, c->rmap_d, c->dscal);
     CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * R, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemsetAsync(c->X, 0, sizeof(double2) * (size_t)R * nO, c->st));
@@ -780,6 +845,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
         if ((rc = apply_op(c, vX, vT, Ra, io))) return rc;
         if ((rc = apply_pre(c, vT, vTR, vA, Ra, gs, io))) return rc;
         if ((rc = lincomb(c, vV0, 0, vBp, 0, 1.0, vTR, 0, -1.0, 1, nO, Ra))) return rc;
+        { LaunchScope ls_(c, 2); }
         k_norm2<<<Ra, 256, 0, c->st>>>(vV0, nO, c->rmap_d, c->dscal);
         CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * R, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
@@ -799,6 +865,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
         Ra = (int)run.size();
         for (int r : run) c->hdscal[r] = beta[r];
         CK(cudaMemcpyAsync(c->dscal, c->hdscal, sizeof(double) * R, cudaMemcpyHostToDevice, c->st));
+        { LaunchScope ls_(c, 2); }
         k_scale_div<<<grid_for(nO * Ra), 256, 0, c->st>>>(vV0, vV0, nO, c->rmap_d, Ra, c->dscal);
       } else {
         for (int r : run) {
@@ -806,6 +873,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
           c->hdscal[r] = beta[r];
         }
         CK(cudaMemcpyAsync(c->dscal, c->hdscal, sizeof(double) * R, cudaMemcpyHostToDevice, c->st));
+        { LaunchScope ls_(c, 2); }
         k_scale_div<<<grid_for(nO * Ra), 256, 0, c->st>>>(vV0, vBp, nO, c->rmap_d, Ra, c->dscal);
       }
       CK(cudaGetLastError());
@@ -830,6 +898,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
         if ((rc = apply_op(c, vj, vT, Ra, io))) return rc;
         if ((rc = apply_pre(c, vT, vj1, vA, Ra, gs, io))) return rc;
         const int hld = c->capO + 2;
+        { LaunchScope ls_(c, 2); }
         k_arnoldi<<<Ra, 512, 0, c->st>>>(c->V, vs, nO, j, c->rmap_d, c->hout, hld);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(c->hhout, c->hout, sizeof(double2) * (size_t)R * hld, cudaMemcpyDeviceToHost, c->st));
@@ -885,6 +954,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
         if (!norm.empty()) {
           if ((rc = set_active(c, norm))) return rc;
           CK(cudaMemcpyAsync(c->dscal, c->hdscal, sizeof(double) * R, cudaMemcpyHostToDevice, c->st));
+          { LaunchScope ls_(c, 2); }
           k_scale_div<<<grid_for(nO * (long long)norm.size()), 256, 0, c->st>>>(vj1, vj1, nO, c->rmap_d,
                                                                                   (int)norm.size(), c->dscal);
           CK(cudaGetLastError());
@@ -910,6 +980,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
       if ((rc = set_active(c, cyc))) return rc;
       CK(cudaMemcpyAsync(c->ybuf, c->hy, sizeof(double2) * (size_t)R * yld, cudaMemcpyHostToDevice, c->st));
       const long long vs = (long long)(c->capO + 1) * nO;
+      { LaunchScope ls_(c, 2); }
       k_accum_x<<<grid_for(nO * (long long)cyc.size()), 256, 0, c->st>>>(vX, c->V, vs, nO, c->ybuf, yld, kmax,
                                                                           c->rmap_d, (int)cyc.size());
       CK(cudaGetLastError());
@@ -932,6 +1003,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   // residuals (sie.py:441-445)
   if ((rc = set_active(c, all))) return rc;
   CK(cudaMemsetAsync(c->dscal, 0, sizeof(double) * 2 * R, c->st));
+  { LaunchScope ls_(c, 2); }
   k_residual<<<dim3(64, R), 256, 0, c->st>>>(u, f, N, c->wz, c->wx, c->tx_d, c->tz_d, c->m_d, c->omega * c->omega,
                                              c->rmap_d, c->dscal);
   CK(cudaGetLastError());
@@ -974,6 +1046,20 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
       for (int i = 0; i < stats->inner_hist_len; ++i) stats->inner_hist[i] = i < PT_HIST ? hh[i] : 0;
     }
     if (stats->timing_ms) stats->timing_ms[0] = ms;
+    if (stats->kernel_ms) {
+      double acc[3] = {0, 0, 0};
+      for (const auto& e : c->evs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e.a, e.b);
+        acc[e.cls] += t;
+      }
+      stats->kernel_ms[0] = acc[0];
+      stats->kernel_ms[1] = acc[1];
+      stats->kernel_ms[2] = c->prof ? std::max(0.0, (double)ms - acc[0] - acc[1]) : 0.0;
+    }
+    if (stats->k1_bytes) stats->k1_bytes[0] = c->k1_bytes;
+    if (stats->launches) stats->launches[0] = c->launches;
+    if (stats->k1_launches) stats->k1_launches[0] = c->k1_launches;
   }
   if (ecode) return ecode;
   for (int r = 0; r < R; ++r)
@@ -1001,6 +1087,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   pt_ctx* c = new pt_ctx();
   c->dev = device;
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  c->own_st = c->st;
   c->nx = pb->nx;
   c->nz = pb->nz;
   c->npml = pb->npml;
@@ -1132,12 +1219,44 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   return PT_OK;
 }
 
+int pt_set_stream(pt_ctx* c, void* stream) {
+  if (!c) return PT_BAD_ARGUMENT;
+  c->st = stream ? static_cast<cudaStream_t>(stream) : c->own_st;
+  return PT_OK;
+}
+
+int pt_set_profiling(pt_ctx* c, int enable) {
+  if (!c) return PT_BAD_ARGUMENT;
+  c->prof = enable != 0;
+  return PT_OK;
+}
+
 int pt_destroy(pt_ctx* c) {
   if (!c) return PT_OK;
   cudaSetDevice(c->dev);
   cudaDeviceSynchronize();
   // the process-level allocations are released with the context
-  cudaStreamDestroy(c->st);
+  for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
+  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->lz_d,
+                  (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->items_d,
+                  (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
+                  (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables,
+                  (void*)c->trc, (void*)c->Z, (void*)c->iscr, (void*)c->hess, (void*)c->iters, (void*)c->err_d,
+                  (void*)c->cnt_d, (void*)c->hist_d, (void*)c->rmap_d, (void*)c->dscal, (void*)c->hout,
+                  (void*)c->ybuf, (void*)c->io_f, (void*)c->io_u})
+    if (p) cudaFree(p);
+  for (void* p : {(void*)c->hrmap, (void*)c->hhout, (void*)c->hdscal, (void*)c->hy})
+    if (p) cudaFreeHost(p);
+  std::vector<Stage*> stages = {&c->newton, &c->op, &c->refl, &c->recon};
+  for (auto& st : c->sdown) stages.push_back(&st);
+  for (auto& st : c->sup) stages.push_back(&st);
+  for (Stage* st : stages) {
+    for (auto& kv : st->tasks) cudaFree(kv.second.d);
+    if (st->jobs_d) cudaFree(st->jobs_d);
+    if (st->stage_jobs_d) cudaFree(st->stage_jobs_d);
+    if (st->ljobs_d) cudaFree(st->ljobs_d);
+  }
+  cudaStreamDestroy(c->own_st);
   delete c;
   return PT_OK;
 }
@@ -1161,15 +1280,19 @@ int pt_solve(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double*
   if (!c || !f || !u || !cfg || nrhs <= 0) return PT_BAD_ARGUMENT;
   CK(cudaSetDevice(c->dev));
   const size_t bytes = sizeof(double2) * (size_t)nrhs * c->wz * c->wx;
-  double2 *fd = nullptr, *ud = nullptr;
-  CK(cudaMalloc(&fd, bytes));
-  CK(cudaMalloc(&ud, bytes));
+  if (bytes > c->io_bytes) {
+    if (c->io_f) cudaFree(c->io_f);
+    if (c->io_u) cudaFree(c->io_u);
+    c->io_f = c->io_u = nullptr;
+    CK(cudaMalloc(&c->io_f, bytes));
+    CK(cudaMalloc(&c->io_u, bytes));
+    c->io_bytes = bytes;
+  }
+  double2 *fd = c->io_f, *ud = c->io_u;
   CK(cudaMemcpyAsync(fd, f, bytes, cudaMemcpyHostToDevice, c->st));
   int rc = pt_solve_device(c, reinterpret_cast<const double*>(fd), nrhs, cfg, reinterpret_cast<double*>(ud), stats);
   cudaError_t e = cudaMemcpyAsync(u, ud, bytes, cudaMemcpyDeviceToHost, c->st);
   cudaStreamSynchronize(c->st);
-  cudaFree(fd);
-  cudaFree(ud);
   if (e != cudaSuccess && rc == PT_OK) {
     g_err = cudaGetErrorString(e);
     return PT_CUDA_ERROR;

@@ -199,7 +199,7 @@ class PolarizedTracesSolver:
         self.ctx.close()
 
     # -- one call into the C ABI for a batch of sources
-    def _run(self, F, config, preconditioner, device_arrays=None):
+    def _run(self, F, config, preconditioner, device_arrays=None, out=None):
         if config.method != "gmres":
             raise NotImplementedError("BiCGstab is not on the B200 path yet (SURVEY.md 8(f) rank 3)")
         if preconditioner not in ("gs", "jac"):
@@ -219,16 +219,26 @@ class PolarizedTracesSolver:
         cnt = np.zeros(3, dtype=np.int64)
         ihist = np.zeros(64, dtype=np.int32)
         tms = np.zeros(1)
+        kms = np.zeros(3)
+        kb = np.zeros(1)
+        lc = np.zeros(2, dtype=np.int64)
         st = _abi.PtStats(
             _abi.dptr(its), _abi.dptr(hist), nh.ctypes.data_as(_abi._ip), _abi.dptr(rel),
             conv.ctypes.data_as(_abi._ip), _abi.dptr(trac.view(np.float64)),
             _abi.dptr(pol.view(np.float64)),
             cnt[0:].ctypes.data_as(_abi._llp), cnt[1:].ctypes.data_as(_abi._llp),
-            cnt[2:].ctypes.data_as(_abi._llp), ihist.ctypes.data_as(_abi._ip), 64, _abi.dptr(tms))
+            cnt[2:].ctypes.data_as(_abi._llp), ihist.ctypes.data_as(_abi._ip), 64, _abi.dptr(tms),
+            _abi.dptr(kms), _abi.dptr(kb), lc[0:].ctypes.data_as(_abi._llp),
+            lc[1:].ctypes.data_as(_abi._llp))
         L = _abi.lib()
         if device_arrays is None:
             F = np.ascontiguousarray(F, dtype=np.complex128)
-            U = np.empty_like(F)
+            if out is not None:
+                if out.shape != F.shape or out.dtype != np.complex128 or not out.flags.c_contiguous:
+                    raise ValueError("out must be a C-contiguous complex128 array shaped like F")
+                U = out
+            else:
+                U = np.empty_like(F)
             rc = L.pt_solve(self.ctx.handle, _abi.dptr(F.view(np.float64)), R, C.byref(cfg),
                             _abi.dptr(U.view(np.float64)), C.byref(st))
         else:
@@ -237,7 +247,9 @@ class PolarizedTracesSolver:
             rc = L.pt_solve_device(self.ctx.handle, C.c_void_p(fptr), R, C.byref(cfg),
                                    C.c_void_p(uptr), C.byref(st))
         self.last_stats = dict(layer_solves=int(cnt[0]), inner_iterations=int(cnt[1]),
-                               touches=int(cnt[2]), inner_hist=ihist.copy(), device_ms=float(tms[0]))
+                               touches=int(cnt[2]), inner_hist=ihist.copy(), device_ms=float(tms[0]),
+                               k1_ms=float(kms[0]), inner_ms=float(kms[1]), other_ms=float(kms[2]),
+                               k1_bytes=float(kb[0]), launches=int(lc[0]), k1_launches=int(lc[1]))
         if rc == _abi.PT_NOT_CONVERGED:
             bad = int(np.argmin(conv))
             h = list(hist[bad, : nh[bad]])
@@ -269,10 +281,12 @@ class PolarizedTracesSolver:
             res = SolveResult(np.zeros(self.grid.shape, dtype=complex), 0.0, [0.0])
         return res
 
-    def solve_many(self, F, config=KrylovConfig(), preconditioner="gs"):
-        """Batch of sources ``F[nrhs, wz, wx]`` solved in lockstep on the device."""
+    def solve_many(self, F, config=KrylovConfig(), preconditioner="gs", out=None):
+        """Batch of sources ``F[nrhs, wz, wx]`` solved in lockstep on the device.
+
+        ``out`` (optional, e.g. a pinned buffer) receives the wavefields."""
         F = np.asarray(F, dtype=complex).reshape((-1,) + tuple(self.grid.shape))
-        return self._run(F, config, preconditioner)
+        return self._run(F, config, preconditioner, out=out)
 
     def solve_device(self, f_ptr, u_ptr, nrhs, config=KrylovConfig(), preconditioner="gs"):
         """Device-resident sources/wavefields (e.g. torch CUDA tensors' ``data_ptr()``)."""
