@@ -1,70 +1,88 @@
-// K1: batched cell solves H_c X = B by block-tridiagonal substitution with
-// precomputed dense Schur inverses (replaces SuperLU.solve, subdomain.py:214-221).
+// K1: batched cell solves H_c X = B with a TWISTED block-tridiagonal
+// factorization (replaces SuperLU.solve, subdomain.py:214-221).
 //
-//   forward   z_k = S_k^{-1} (b_k - l_k z_{k-1})          k = 0 .. wz_c-1
-//   backward  x_k = z_k - u_k S_k^{-1} x_{k+1}            k = wz_c-2 .. 0
+// With m = wz_c/2 the offline stage stores S_k^{-1} (k < m, top Schur
+// complements), T_k^{-1} (k > m, bottom Schur complements) and M^{-1} (k = m),
+// see offline._twisted_inverses.  A solve is two half-length chains that run
+// concurrently on a CTA pair of one thread-block cluster:
 //
-// One CTA per task = (cell, up to NC columns).  A column is one (layer-solve job,
-// RHS) pair.  The right-hand side b_k is generated on the fly in the prologue of
-// every step from the job description (equivalent interface sources at the four
-// cut rows, the split volume source, and -- on the reconstruction pass -- the
-// cell trace sources), so no layer volume is ever materialised.  The epilogue
-// writes only what the caller consumes: the four Newton rows of each cell, the
-// sampled layer rows, or the full stitched volume.
+//   top    z_k = S_k^{-1}(b_k - l_k z_{k-1}),  k = 0..m-1
+//   bottom y_k = T_k^{-1}(b_k - u_k y_{k+1}),  k = wz_c-1..m+1
+//   middle x_m = M^{-1}(b_m - l_m z_{m-1} - u_m y_{m+1})   (vectors swapped over DSMEM)
+//   top    x_k = z_k - u_k S_k^{-1} x_{k+1},   k = m-1..0
+//   bottom x_k = y_k - l_k T_k^{-1} x_{k-1},   k = m+1..wz_c-1
 //
-// S_k^{-1} does not depend on data, so it is streamed through an NS-slot shared
-// memory ring by 1-D bulk async copies (cp.async.bulk, SASS UBLKCP) issued
-// NS chunks ahead of the consumer; every byte of the factor is read exactly once
-// per pass from HBM/L2.
-#include "pt_device.cuh"
+// so the dependent chain is wz_c+1 block matvecs instead of 2 wz_c - 1.
+// A cluster is 2*CM CTAs: CM column CTAs per half, each owning NC right-hand
+// side columns (a column = one (layer-solve job, RHS) pair).  The factor
+// blocks do not depend on data: a producer warp streams them through an
+// NS-slot shared-memory ring with 1-D bulk async copies (cp.async.bulk ->
+// SASS UBLKCP), multicast to the CM CTAs of the half that consume the same
+// block; consumers release slots through mbarriers, so no CTA-wide barrier
+// guards the ring.
+//
+// The right-hand side b_k is generated in the prologue of every step from the
+// job description (equivalent interface sources at the four cut rows, the
+// split volume source, the cell trace sources on the reconstruction pass), so
+// no layer volume is ever materialised; the epilogue writes only what the
+// caller consumes (four Newton rows per cell, the sampled layer rows, or the
+// stitched volume).
+#include <cooperative_groups.h>
 
 #include "pt_launch.cuh"
 
+namespace cg = cooperative_groups;
 
 struct ColInfo {
-  int jid, r, panmask, vol;  // vol: 0 none, 1 split slab of the global f, 2 full layer slab
+  int jid, r, panmask, vol, nout, vfull, opos[4], pad[6];
 };
 
 template <int NC>
-__global__ void __launch_bounds__(PT_THREADS) k1_cell_solve(const K1Params p) {
+__global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const K1Task task = p.tasks[blockIdx.x];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int CM = p.cm;
+  const int h = rank / CM, cm = rank - h * CM;
+  const K1Task task = p.tasks[blockIdx.x / (2 * CM)];
   const CellInfo cell = p.cells[task.cell];
   const LayerInfo lay = p.layers[cell.layer];
   const int w = cell.w, wzc = cell.wzc;
+  const int m = wzc >> 1, mb = wzc - 1 - m;
+  const int nst = h == 0 ? 2 * m + 1 : 2 * mb + 1;
   const int tid = threadIdx.x;
-  const int G = blockDim.x / w;
+  const int NS = p.ns;
   const int nIc = p.Lc - 1;
 
-  // ---- shared memory carve-up
   unsigned char* ring = smem;
-  double2* va = reinterpret_cast<double2*>(ring + (size_t)p.ns * p.slot_bytes);
-  double2* vb = va + w * NC;
-  double2* red = vb + w * NC;
-  ColInfo* cols = reinterpret_cast<ColInfo*>(red + (size_t)G * w * NC);
-  uint64_t* full = reinterpret_cast<uint64_t*>(cols + NC + (NC & 1));
+  double2* VA = reinterpret_cast<double2*>(ring + (size_t)NS * p.slot_bytes);
+  double2* VB = VA + w * NC;
+  double2* XC = VB + w * NC;  // partner's half-chain vector at the middle block
+  double2* red = XC + w * NC;
+  ColInfo* cols = reinterpret_cast<ColInfo*>(red + K1_CONSUMERS * NC);
+  uint64_t* full = reinterpret_cast<uint64_t*>(cols + NC);
+  uint64_t* lempty = full + NS;
+  uint64_t* cempty = lempty + NS;
+  uint64_t* xbar = cempty + NS;
 
   const int jc = max(1, min(w, p.slot_bytes / (w * 16)));
   const int nch = (w + jc - 1) / jc;
-  const int nsteps = 2 * wzc - 1;
-  const int total = nsteps * nch;
+  const int total = nst * nch;
   const double2* S = p.sinv + cell.sinv_off;
-
-  auto issue = [&](int s) {
-    const int st = s / nch, ch = s - st * nch;
-    const int kmat = st < wzc ? st : 2 * wzc - 2 - st;
-    const int c0 = ch * jc;
-    const int cw = min(jc, w - c0);
-    const uint32_t bytes = (uint32_t)cw * w * 16u;
-    uint64_t* bar = &full[s % p.ns];
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(ring + (size_t)(s % p.ns) * p.slot_bytes, S + (size_t)kmat * w * w + (size_t)c0 * w, bytes, bar);
+  // factor block used by step s of this half
+  auto kblk = [&](int s) -> int {
+    if (h == 0) return s <= m ? s : 2 * m - s;
+    return s < mb ? wzc - 1 - s : (s == mb ? m : m + (s - mb));
   };
 
   if (tid < NC) {
-    ColInfo ci{-1, 0, 0, 0};
-    if (tid < task.nq) {
-      const int q = task.q0 + tid;
+    ColInfo ci;
+    ci.jid = -1;
+    ci.r = 0;
+    ci.panmask = ci.vol = ci.nout = ci.vfull = 0;
+    const int ql = cm * NC + tid;
+    if (ql < task.nq) {
+      const int q = task.q0 + ql;
       if (p.pass == 2) {
         ci.jid = 0;
         ci.r = q;
@@ -72,99 +90,97 @@ __global__ void __launch_bounds__(PT_THREADS) k1_cell_solve(const K1Params p) {
         ci.jid = p.ljobs[task.jb + q / p.R];
         ci.r = q % p.R;
         const OJob& jb = p.jobs[ci.jid];
-        int m = 0;
+        int msk = 0;
         for (int s = 0; s < 4; ++s)
-          if (jb.pan[s][0].vec >= 0) m |= 1 << s;
-        ci.panmask = m;
+          if (jb.pan[s][0].vec >= 0) msk |= 1 << s;
+        ci.panmask = msk;
         ci.vol = jb.vol ? (jb.vfull ? 2 : 1) : 0;
+        ci.vfull = jb.vfull;
+        ci.nout = jb.nout;
+        for (int o = 0; o < 4; ++o) ci.opos[o] = o < jb.nout ? jb.orow[o] + p.npml - 1 : -1;
       }
     }
     cols[tid] = ci;
   }
   if (tid == 0) {
-    for (int s = 0; s < p.ns; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&lempty[s], K1_CONSUMERS / 32);
+      mbar_init(&cempty[s], CM);
+    }
+    mbar_init(xbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < min(p.ns, total); ++s) issue(s);
+  cl.sync();  // every barrier of the cluster is initialised before any remote traffic
+  if (tid == 0) mbar_expect_tx(xbar, (uint32_t)(w * NC * 16));
 
-  const bool active = tid < G * w;
-  const int mi = tid % w, mg = tid / w;
-  double2 acc[NC];
-  int s = 0;
-
-  // one matvec y = S_kmat^{-1} vin, reduced into red-sum per (i,q); returns via red buffer
-  auto matvec = [&](const double2* vin) {
-#pragma unroll
-    for (int q = 0; q < NC; ++q) acc[q] = czero();
-    for (int ch = 0; ch < nch; ++ch, ++s) {
-      mbar_wait(&full[s % p.ns], (uint32_t)((s / p.ns) & 1));
-      const double2* slot = reinterpret_cast<const double2*>(ring + (size_t)(s % p.ns) * p.slot_bytes);
-      const int c0 = ch * jc;
-      const int cw = min(jc, w - c0);
-      if (active) {
-        for (int jj = mg; jj < cw; jj += G) {
-          const double2 a = slot[jj * w + mi];
-          const double2* tv = vin + (c0 + jj) * NC;
-#pragma unroll
-          for (int q = 0; q < NC; ++q) cfma(acc[q], a, tv[q]);
-        }
-      }
-      __syncthreads();
-      if (tid == 0 && s + p.ns < total) issue(s + p.ns);
-    }
-    if (active) {
-#pragma unroll
-      for (int q = 0; q < NC; ++q) red[(mg * w + mi) * NC + q] = acc[q];
-    }
-    __syncthreads();
-  };
-  auto reduced = [&](int i, int q) {
-    double2 y = red[i * NC + q];
-    for (int g = 1; g < G; ++g) y = cadd(y, red[(g * w + i) * NC + q]);
-    return y;
-  };
-
-  // right-hand side element b_k[j] of column q
-  auto rhs = [&](int k, int j, int q) -> double2 {
-    const ColInfo ci = cols[q];
-    if (ci.jid < 0) return czero();
-    if (p.pass == 2) return p.bd[((size_t)ci.r * wzc + k) * w + j];
-    double2 inner = czero();
-    if (k >= cell.lo && k < cell.hi) {
-      const int X = cell.off + k;
-#pragma unroll
-      for (int sl = 0; sl < 4; ++sl)
-        if ((ci.panmask >> sl & 1) && j == lay.prow[sl])
-          inner = cadd(inner, cmul(lay.coef[sl], p.P[((size_t)(ci.jid * 4 + sl) * p.R + ci.r) * p.wx + X]));
-      if (ci.vol == 1 && j >= lay.lo && j < lay.hi)
-        inner = cadd(inner, p.f[ci.r * p.f_stride + (size_t)(lay.off + j) * p.wx + X]);
-      else if (ci.vol == 2)
-        inner = cadd(inner, p.f[ci.r * p.f_stride + (size_t)j * p.wx + X]);
-    }
-    if (p.pass == 1) {
-#pragma unroll
-      for (int sl = 0; sl < 4; ++sl) {
-        const bool has = sl < 2 ? cell.has_top : cell.has_bot;
-        if (has && k == cell.krow[sl]) {
-          const int I = sl < 2 ? cell.cell - 1 : cell.cell;
-          const double2 t =
-              p.tr[((((size_t)ci.jid * p.R + ci.r) * nIc + I) * 2 + (sl & 1)) * p.wmax + j];
-          return cadd(cmul(cell.coef[sl], t), inner);
+  if (tid >= K1_CONSUMERS) {
+    // ------------------------------------------------------------ producer warp
+    if (tid == K1_CONSUMERS) {
+      const uint16_t mask = (uint16_t)(((1u << CM) - 1u) << (h * CM));
+      for (int c = 0; c < total; ++c) {
+        const int slot = c % NS, u = c / NS;
+        if (u > 0) mbar_wait(&lempty[slot], (uint32_t)((u - 1) & 1));
+        const int s = c / nch, ch = c - s * nch;
+        const int c0 = ch * jc, cw = min(jc, w - c0);
+        const uint32_t bytes = (uint32_t)cw * w * 16u;
+        mbar_expect_tx(&full[slot], bytes);
+        const int issuer = slot % CM;
+        const double2* src = S + (size_t)kblk(s) * w * w + (size_t)c0 * w;
+        unsigned char* dst = ring + (size_t)slot * p.slot_bytes;
+        if (CM == 1) {
+          bulk_g2s(dst, src, bytes, &full[slot]);
+        } else {
+          if (u > 0) mbar_arrive_remote(mapa(&cempty[slot], (uint32_t)(h * CM + issuer)));
+          if (issuer == cm) {
+            if (u > 0) mbar_wait(&cempty[slot], (uint32_t)((u - 1) & 1));
+            bulk_g2s_mc(dst, src, bytes, &full[slot], mask);
+          }
         }
       }
     }
-    return inner;
-  };
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int G = K1_CONSUMERS / w;
+    const bool mact = tid < G * w;
+    const int mi = tid % w, mg = tid / w;
+    double2* Z = p.Z + task.zoff + (size_t)cm * wzc * w * NC;
 
-  // epilogue of backward step k: x_k lives in vx ([w][NC])
-  auto emit = [&](int k, const double2* vx) {
-    for (int e = tid; e < w * NC; e += blockDim.x) {
+    auto rhs = [&](int k, int j, int q) -> double2 {
+      const ColInfo& ci = cols[q];
+      if (ci.jid < 0) return czero();
+      if (p.pass == 2) return p.bd[((size_t)ci.r * wzc + k) * w + j];
+      double2 inner = czero();
+      if (k >= cell.lo && k < cell.hi) {
+        const int X = cell.off + k;
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl)
+          if ((ci.panmask >> sl & 1) && j == lay.prow[sl])
+            inner = cadd(inner, cmul(lay.coef[sl], p.P[((size_t)(ci.jid * 4 + sl) * p.R + ci.r) * p.wx + X]));
+        if (ci.vol == 1 && j >= lay.lo && j < lay.hi)
+          inner = cadd(inner, p.f[ci.r * p.f_stride + (size_t)(lay.off + j) * p.wx + X]);
+        else if (ci.vol == 2)
+          inner = cadd(inner, p.f[ci.r * p.f_stride + (size_t)j * p.wx + X]);
+      }
+      if (p.pass == 1) {
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl) {
+          const bool has = sl < 2 ? cell.has_top : cell.has_bot;
+          if (has && k == cell.krow[sl]) {
+            const int I = sl < 2 ? cell.cell - 1 : cell.cell;
+            const double2 t = p.tr[((((size_t)ci.jid * p.R + ci.r) * nIc + I) * 2 + (sl & 1)) * p.wmax + j];
+            return cadd(cmul(cell.coef[sl], t), inner);
+          }
+        }
+      }
+      return inner;
+    };
+
+    auto emit = [&](int k, int e, double2 x) {
       const int i = e / NC, q = e - (e / NC) * NC;
-      const ColInfo ci = cols[q];
-      if (ci.jid < 0) continue;
-      const double2 x = vx[e];
+      const ColInfo& ci = cols[q];
+      if (ci.jid < 0) return;
       if (p.pass == 2) {
         p.xd[((size_t)ci.r * wzc + k) * w + i] = x;
       } else if (p.pass == 0) {
@@ -176,78 +192,147 @@ __global__ void __launch_bounds__(PT_THREADS) k1_cell_solve(const K1Params p) {
         }
       } else if (k >= cell.lo && k < cell.hi) {
         const int X = cell.off + k;
-        const OJob& jb = p.jobs[ci.jid];
-        if (jb.nout < 0) {
-          if (jb.vfull)
+        if (ci.nout < 0) {
+          if (ci.vfull)
             p.u[ci.r * p.u_stride + (size_t)i * p.wx + X] = x;
           else if (i >= lay.lo && i < lay.hi)
             p.u[ci.r * p.u_stride + (size_t)(lay.off + i) * p.wx + X] = x;
         } else {
-          for (int o = 0; o < jb.nout; ++o)
-            if (i == jb.orow[o] + p.npml - 1) p.smp[((size_t)(ci.jid * 4 + o) * p.R + ci.r) * p.wx + X] = x;
+#pragma unroll
+          for (int o = 0; o < 4; ++o)
+            if (i == ci.opos[o]) p.smp[((size_t)(ci.jid * 4 + o) * p.R + ci.r) * p.wx + X] = x;
         }
       }
-    }
-  };
+    };
 
-  double2* Z = p.Z + task.zoff;
-  // ---------------- forward sweep
-  double2* vin = va;
-  double2* vz = vb;  // z_{k-1}
-  for (int k = 0; k < wzc; ++k) {
-    const double2 lk = p.lz[cell.lz_off + k];
-    for (int e = tid; e < w * NC; e += blockDim.x) {
-      const int j = e / NC, q = e - (e / NC) * NC;
-      double2 b = rhs(k, j, q);
-      if (k > 0) b = csub(b, cmul(lk, vz[e]));
-      vin[e] = b;
+    const int nel = w * NC;
+    double2* cur = VA;
+    double2* nxt = VB;
+    int c = 0;
+    const int partner = (1 - h) * CM + cm;
+    for (int s = 0; s < nst; ++s) {
+      const int kb = kblk(s);
+      const int kind = (h == 0) ? (s < m ? 0 : (s == m ? 1 : 2)) : (s < mb ? 0 : (s == mb ? 1 : 2));
+      double2 zr[4];
+      // ---- prologue: matvec input in cur (in place: every thread owns the same elements throughout)
+      if (kind == 0) {
+        const double2 cf = h == 0 ? p.lz[cell.lz_off + kb] : p.uz[cell.lz_off + kb];
+        const bool first = s == 0;
+        for (int e = tid; e < nel; e += K1_CONSUMERS) {
+          double2 b = rhs(kb, e / NC, e % NC);
+          if (!first) b = csub(b, cmul(cf, cur[e]));
+          cur[e] = b;
+        }
+      } else if (kind == 1) {
+        const uint32_t rx = mapa(XC, (uint32_t)partner), rb = mapa(xbar, (uint32_t)partner);
+        for (int e = tid; e < nel; e += K1_CONSUMERS) st_async_c(rx + (uint32_t)e * 16u, cur[e], rb);
+        mbar_wait(xbar, 0);
+        const double2 lm = p.lz[cell.lz_off + m], um = p.uz[cell.lz_off + m];
+        for (int e = tid; e < nel; e += K1_CONSUMERS) {
+          const double2 zt = h == 0 ? cur[e] : XC[e];  // z_{m-1} (top chain)
+          const double2 yb = h == 0 ? XC[e] : cur[e];  // y_{m+1} (bottom chain)
+          cur[e] = csub(csub(rhs(m, e / NC, e % NC), cmul(lm, zt)), cmul(um, yb));
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int e = tid + t * K1_CONSUMERS;
+          if (e < nel) zr[t] = Z[(size_t)kb * nel + e];
+        }
+      }
+      named_bar(1, K1_CONSUMERS);
+      // ---- y = Blk[kb] cur
+      double2 acc[NC], acc2[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) acc[q] = acc2[q] = czero();
+      for (int ch = 0; ch < nch; ++ch, ++c) {
+        const int slot = c % NS;
+        mbar_wait(&full[slot], (uint32_t)((c / NS) & 1));
+        const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
+        const int c0 = ch * jc, cw = min(jc, w - c0);
+        if (mact) {
+          int jj = mg;
+          for (; jj + G < cw; jj += 2 * G) {
+            const double2 a0 = blk[jj * w + mi], a1 = blk[(jj + G) * w + mi];
+            const double2* t0 = cur + (c0 + jj) * NC;
+            const double2* t1 = cur + (c0 + jj + G) * NC;
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+              cfma(acc[q], a0, t0[q]);
+              cfma(acc2[q], a1, t1[q]);
+            }
+          }
+          if (jj < cw) {
+            const double2 a0 = blk[jj * w + mi];
+            const double2* t0 = cur + (c0 + jj) * NC;
+#pragma unroll
+            for (int q = 0; q < NC; ++q) cfma(acc[q], a0, t0[q]);
+          }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&lempty[slot]);
+      }
+      if (mact) {
+#pragma unroll
+        for (int q = 0; q < NC; ++q) red[(mg * w + mi) * NC + q] = cadd(acc[q], acc2[q]);
+      }
+      named_bar(1, K1_CONSUMERS);
+      // ---- epilogue
+      const double2 cf = kind == 2 ? (h == 0 ? p.uz[cell.lz_off + kb] : p.lz[cell.lz_off + kb]) : czero();
+      for (int t = 0; t < 4; ++t) {
+        const int e = tid + t * K1_CONSUMERS;
+        if (e >= nel) break;
+        const int i = e / NC, q = e - (e / NC) * NC;
+        double2 y = red[i * NC + q];
+        for (int g = 1; g < G; ++g) y = cadd(y, red[(g * w + i) * NC + q]);
+        if (kind == 0) {
+          nxt[e] = y;
+          Z[(size_t)kb * nel + e] = y;
+        } else if (kind == 1) {
+          nxt[e] = y;
+          if (h == 0) emit(m, e, y);
+        } else {
+          const double2 x = csub(zr[t], cmul(cf, y));
+          nxt[e] = x;
+          emit(kb, e, x);
+        }
+      }
+      double2* tmp = cur;
+      cur = nxt;
+      nxt = tmp;
     }
-    __syncthreads();
-    matvec(vin);
-    for (int e = tid; e < w * NC; e += blockDim.x) {
-      const int i = e / NC, q = e - (e / NC) * NC;
-      const double2 y = reduced(i, q);
-      vz[e] = y;
-      Z[(size_t)k * w * NC + e] = y;
-    }
-    __syncthreads();
   }
-  // ---------------- backward sweep: vz holds z_{wzc-1} = x_{wzc-1}
-  emit(wzc - 1, vz);
-  double2* vx = vz;
-  double2* vo = va;
-  for (int k = wzc - 2; k >= 0; --k) {
-    __syncthreads();
-    matvec(vx);
-    const double2 uk = p.uz[cell.lz_off + k];
-    for (int e = tid; e < w * NC; e += blockDim.x) {
-      const int i = e / NC, q = e - (e / NC) * NC;
-      const double2 y = reduced(i, q);
-      vo[e] = csub(Z[(size_t)k * w * NC + e], cmul(uk, y));
-    }
-    __syncthreads();
-    emit(k, vo);
-    double2* t = vx;
-    vx = vo;
-    vo = t;
-  }
+  __syncwarp();
+  cl.sync();  // no CTA leaves while a partner may still write into its shared memory
 }
 
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns) {
-  // ring + two [w][NC] vectors + the [G][w][NC] reduction buffer (G*w <= 256) + column info + barriers
-  return (size_t)ns * slot_bytes + (size_t)(2 * wmax + PT_THREADS) * nc * 16 + (size_t)(nc + 2) * 16 + 16 +
-         (size_t)ns * 8;
+  return (size_t)ns * slot_bytes + (size_t)(3 * wmax + K1_CONSUMERS) * nc * 16 + (size_t)nc * sizeof(ColInfo) +
+         (size_t)(3 * ns + 1) * 8 + 128;
 }
 
 cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
+  if (nc * wmax > 4 * K1_CONSUMERS) return cudaErrorInvalidValue;  // epilogue holds <= 4 elements/thread
   const size_t smax = k1_smem_bytes(wmax, nc, p.slot_bytes, p.ns);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ntasks * 2 * p.cm, 1, 1);
+  cfg.blockDim = dim3(K1_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smax;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * p.cm;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   switch (nc) {
-#define PT_K1_CASE(N)                                                                                \
-  case N:                                                                                            \
-    cudaFuncSetAttribute(k1_cell_solve<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax); \
-    k1_cell_solve<N><<<ntasks, PT_THREADS, smax, st>>>(p);                                           \
-    break;
+#define PT_K1_CASE(N)                                                                                 \
+  case N:                                                                                             \
+    cudaFuncSetAttribute(k1_twisted<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);     \
+    if (2 * p.cm > 8) cudaFuncSetAttribute(k1_twisted<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+    return cudaLaunchKernelEx(&cfg, k1_twisted<N>, p);
     PT_K1_CASE(1)
     PT_K1_CASE(2)
     PT_K1_CASE(4)
@@ -256,5 +341,4 @@ cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStrea
     default:
       return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }

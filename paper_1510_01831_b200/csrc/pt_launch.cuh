@@ -4,6 +4,7 @@
 #include "pt_device.cuh"
 
 #define INNER_NC 8
+#define INNER_CS 8  // CTAs per inner-GMRES cluster (portable cluster size)
 #define PT_HIST 64
 
 struct VecView {
@@ -25,6 +26,7 @@ struct K1Params {
   const double2* uz;
   int R, pass, npml, wx, Lc, wmax;
   int slot_bytes, ns;
+  int cm;             // column CTAs per half-chain (cluster = 2*cm CTAs, factor chunks multicast)
   const double2* f;
   long long f_stride;
   const double2* P;   // [job][4][R][wx]
@@ -58,6 +60,8 @@ struct InnerParams {
   double2* hess;
   long long hstride;
   int* iters;             // [job][R] inner iterations (-1 = error)
+  int* state;             // [job][R] 0 running, 1 converged, 2 failed (cluster-shared)
+  double* beta0;          // [job][R] initial preconditioned residual norms
   int* err;               // PT_* code (atomicMax)
   unsigned long long* counters;  // [0] inner iterations, [1] Green touches, [2] instances
   int* hist;              // [PT_HIST] histogram of inner iteration counts
@@ -66,6 +70,8 @@ struct InnerParams {
 
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns);
 cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStream_t st);
+#define K1_CONSUMERS 256
+#define K1_THREADS (K1_CONSUMERS + 32)
 size_t inner_smem_bytes(int wmax, int R);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
 

@@ -50,6 +50,7 @@ struct Stage {
     K1Task* d = nullptr;
     int n = 0, nc = 1;
     long long zsize = 0;
+    int cm = 1;
     double bytes = 0.0;  // algorithmic S^-1 bytes of one pass: 32 wz_c w^2 per (cell, column)
   };
   std::map<int, Tasks> tasks;
@@ -96,6 +97,8 @@ struct pt_ctx {
           *hess = nullptr;
   long long zcap = 0, iscr_stride = 0, hstride = 0, inmax = 0;
   int* iters = nullptr;
+  int* istate = nullptr;
+  double* ibeta0 = nullptr;
   int* err_d = nullptr;
   unsigned long long* cnt_d = nullptr;  // [0] inner iterations, [1] touches, [2] instances
   int* hist_d = nullptr;
@@ -110,7 +113,7 @@ struct pt_ctx {
   double2* hy = nullptr;
   // host view of current active set
   std::vector<int> act;
-  int slot_bytes = 32768, ns = 5;
+  int slot_bytes = 32768, ns = 8, num_sms = 148;
   long long layer_solves = 0;
   // stream + profiling
   cudaStream_t own_st = nullptr;
@@ -474,7 +477,8 @@ static int ensure_scratch(pt_ctx* c, int R, int capO) {
   };
   for (void* p : {(void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1, (void*)c->AX, (void*)c->X, (void*)c->TR,
                   (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->trc, (void*)c->iscr, (void*)c->hess,
-                  (void*)c->iters, (void*)c->rmap_d, (void*)c->dscal, (void*)c->hout, (void*)c->ybuf})
+                  (void*)c->iters, (void*)c->istate, (void*)c->ibeta0, (void*)c->rmap_d, (void*)c->dscal,
+                  (void*)c->hout, (void*)c->ybuf})
     F(p);
   if (c->hrmap) cudaFreeHost(c->hrmap);
   if (c->hhout) cudaFreeHost(c->hhout);
@@ -494,6 +498,8 @@ static int ensure_scratch(pt_ctx* c, int R, int capO) {
   c->hstride = (long long)(c->inner_cap + 1) * c->inner_cap + (c->inner_cap + 1) + 2 * c->inner_cap;
   CK(cudaMalloc(&c->hess, sizeof(double2) * (size_t)Jmax * R * c->hstride));
   CK(cudaMalloc(&c->iters, sizeof(int) * (size_t)Jmax * R));
+  CK(cudaMalloc(&c->istate, sizeof(int) * (size_t)Jmax * R));
+  CK(cudaMalloc(&c->ibeta0, sizeof(double) * (size_t)Jmax * R));
   CK(cudaMalloc(&c->rmap_d, sizeof(int) * R));
   CK(cudaMalloc(&c->dscal, sizeof(double) * 2 * R));
   CK(cudaMalloc(&c->hout, sizeof(double2) * (size_t)R * (capO + 2)));
@@ -515,35 +521,58 @@ static int ensure_z(pt_ctx* c, long long z) {
   return 0;
 }
 
+// K1 launch geometry for a stage: NC columns per CTA, CM column-CTAs per half-chain (multicast
+// group); a task = (cell, CM*NC columns of one layer) = one cluster of 2*CM CTAs.
+static void k1_policy(pt_ctx* c, const std::vector<int>& ncols_per_group, int* nc_out, int* cm_out) {
+  int cm = 1;
+  if (const char* e = std::getenv("PT_K1_CM")) cm = std::max(1, std::min(8, atoi(e)));
+  int nc = 0;
+  if (const char* e = std::getenv("PT_K1_NC")) nc = atoi(e);
+  if (nc != 1 && nc != 2 && nc != 4 && nc != 8) {
+    nc = 1;
+    for (int cand : {8, 4, 2, 1}) {
+      long long tasks = 0;
+      for (int n : ncols_per_group) tasks += (long long)c->Lc * ((n + cand * cm - 1) / (cand * cm));
+      if (2LL * cm * tasks >= c->num_sms || cand == 1) {
+        nc = cand;
+        break;
+      }
+    }
+  }
+  while (cm > 1 && c->ns % cm) --cm;
+  *nc_out = nc;
+  *cm_out = cm;
+}
+
 static Stage::Tasks* stage_tasks(pt_ctx* c, Stage& S, int Ract) {
   auto itr = S.tasks.find(Ract);
   if (itr != S.tasks.end()) return &itr->second;
   Stage::Tasks T;
-  int maxcols = 0;
+  std::vector<int> ncols;
   for (size_t g = 0; g < S.lgrp.size(); ++g) {
     const int b = S.lgrp[g].second;
     const int e = g + 1 < S.lgrp.size() ? S.lgrp[g + 1].second : (int)S.ljobs.size();
-    maxcols = std::max(maxcols, (e - b) * Ract);
+    ncols.push_back((e - b) * Ract);
   }
-  int nc = 1;
-  while (nc < maxcols && nc < 8) nc <<= 1;
+  int nc = 1, cm = 1;
+  k1_policy(c, ncols, &nc, &cm);
   T.nc = nc;
+  T.cm = cm;
   std::vector<K1Task> v;
   long long z = 0;
   for (size_t g = 0; g < S.lgrp.size(); ++g) {
     const int l = S.lgrp[g].first, b = S.lgrp[g].second;
-    const int e = g + 1 < S.lgrp.size() ? S.lgrp[g + 1].second : (int)S.ljobs.size();
-    const int ncols = (e - b) * Ract;
-    for (int q0 = 0; q0 < ncols; q0 += nc)
+    const int n = ncols[g];
+    for (int q0 = 0; q0 < n; q0 += nc * cm)
       for (int cc = 0; cc < c->Lc; ++cc) {
         const CellInfo& ci = c->cel[l * c->Lc + cc];
         K1Task t;
         t.cell = l * c->Lc + cc;
         t.jb = b;
         t.q0 = q0;
-        t.nq = std::min(nc, ncols - q0);
+        t.nq = std::min(nc * cm, n - q0);
         t.zoff = z;
-        z += (long long)ci.wzc * ci.w * nc;
+        z += (long long)cm * ci.wzc * ci.w * nc;
         T.bytes += 32.0 * ci.wzc * (double)ci.w * ci.w * t.nq;
         v.push_back(t);
       }
@@ -600,6 +629,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   kp.wmax = c->wmax;
   kp.slot_bytes = c->slot_bytes;
   kp.ns = c->ns;
+  kp.cm = T->cm;
   kp.f = io.f;
   kp.f_stride = io.f_stride;
   kp.P = c->P;
@@ -644,6 +674,8 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     ip.hess = c->hess;
     ip.hstride = c->hstride;
     ip.iters = c->iters;
+    ip.state = c->istate;
+    ip.beta0 = c->ibeta0;
     ip.err = c->err_d;
     ip.counters = c->cnt_d;
     ip.hist = c->hist_d;
@@ -1199,18 +1231,26 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   CK(cudaMalloc(&c->err_d, sizeof(int)));
   CK(cudaMalloc(&c->cnt_d, sizeof(unsigned long long) * 4));
   CK(cudaMalloc(&c->hist_d, sizeof(int) * PT_HIST));
-  // smem ring: ~32 KB slots, as many as fit next to the vectors
+  // K1 shared-memory ring: 8 slots (a multiple of every multicast group size), as large as fit
   {
     int maxsm = 0;
     CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    c->slot_bytes = std::max(32768, c->wmax * 16);
-    const size_t fixed = k1_smem_bytes(c->wmax, 8, 0, 0) + 64;
-    c->ns = (int)std::min<long long>(6, ((long long)maxsm - (long long)fixed) / (c->slot_bytes + 8));
-    if (c->ns < 2) {
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    c->ns = 8;
+    const long long fixed = (long long)k1_smem_bytes(c->wmax, 8, 0, c->ns);
+    long long slot = ((long long)maxsm - fixed) / c->ns;
+    slot = std::min(slot, 32768LL) / 16 * 16;
+    if (slot < 16LL * c->wmax) {
       g_err = "not enough shared memory for the K1 ring";
       return PT_BAD_ARGUMENT;
     }
+    c->slot_bytes = (int)slot;
   }
+  for (const CellInfo& ci : c->cel)
+    if (ci.wzc < 3) {
+      g_err = "cells need nx_c + 2 npml >= 3 block rows";
+      return PT_BAD_ARGUMENT;
+    }
   int rc = build_inner(c);
   if (!rc) rc = build_outer(c);
   if (rc) return rc;
@@ -1241,7 +1281,8 @@ int pt_destroy(pt_ctx* c) {
                   (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->items_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
                   (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables,
-                  (void*)c->trc, (void*)c->Z, (void*)c->iscr, (void*)c->hess, (void*)c->iters, (void*)c->err_d,
+                  (void*)c->trc, (void*)c->Z, (void*)c->iscr, (void*)c->hess, (void*)c->iters, (void*)c->istate,
+                  (void*)c->ibeta0, (void*)c->err_d,
                   (void*)c->cnt_d, (void*)c->hist_d, (void*)c->rmap_d, (void*)c->dscal, (void*)c->hout,
                   (void*)c->ybuf, (void*)c->io_f, (void*)c->io_u})
     if (p) cudaFree(p);
@@ -1365,7 +1406,7 @@ int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, dou
   std::vector<K1Task> tasks;
   long long z = 0;
   const int nc = 8;
-  for (int q0 = 0; q0 < nrhs; q0 += nc) {
+  for (int q0 = 0; q0 < nrhs; q0 += nc) {  // one cluster pair per 8 columns (cm = 1)
     K1Task t;
     t.cell = layer * c->Lc + cell;
     t.jb = 0;
@@ -1394,6 +1435,7 @@ int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, dou
   kp.wmax = c->wmax;
   kp.slot_bytes = c->slot_bytes;
   kp.ns = c->ns;
+  kp.cm = 1;
   kp.Z = c->Z;
   kp.bd = bd;
   kp.xd = xd;

@@ -80,7 +80,7 @@ class CellFactors:
     wzc: int
     nxc: int
     off: int
-    sinv: torch.Tensor  # (wzc, w, w) complex128, column-major blocks (i.e. S^-T row-major)
+    sinv: torch.Tensor  # (wzc, w, w) complex128 twisted factors (see _twisted_inverses), column-major blocks
     lz: np.ndarray  # (wzc,) block-row couplings l_k
     uz: np.ndarray  # (wzc,) u_k
     green: torch.Tensor  # (4 rows, 4 slots, w, w) column-major blocks
@@ -158,6 +158,68 @@ def _schur_inverses(tw, diag, lz, uz, device):
     return out
 
 
+def _twisted_inverses(tw, diag, lz, uz, sinv_fwd, device):
+    """Two-sided ("twisted") block factorization used by K1.
+
+    Top blocks k < m keep the forward Schur inverses S_k^{-1}; bottom blocks
+    k > m hold T_k^{-1} with T_{wz-1} = D_{wz-1}, T_k = D_k - u_k l_{k+1} T_{k+1}^{-1};
+    the middle block holds M^{-1} with
+    M = D_m - l_m u_{m-1} S_{m-1}^{-1} - u_m l_{m+1} T_{m+1}^{-1}, m = wz_c // 2.
+    A solve is then two independent half-length chains that meet at block m.
+    """
+    B, wzc, w = diag.shape
+    m = wzc // 2
+    lo, mn, up = (torch.as_tensor(a, dtype=torch.complex128, device=device) for a in tw)
+    base = torch.diag(mn) + torch.diag(up[:-1], 1) + torch.diag(lo[1:], -1)
+    out = sinv_fwd.clone()
+    prev = None
+    for k in range(wzc - 1, m, -1):
+        T = base.expand(B, w, w).clone()
+        T.diagonal(dim1=-2, dim2=-1).add_(diag[:, k, :])
+        if k < wzc - 1:
+            T -= (complex(uz[k]) * complex(lz[k + 1])) * prev
+        prev = torch.linalg.inv(T)
+        out[:, k] = prev
+    Mm = base.expand(B, w, w).clone()
+    Mm.diagonal(dim1=-2, dim2=-1).add_(diag[:, m, :])
+    if m > 0:
+        Mm -= (complex(lz[m]) * complex(uz[m - 1])) * sinv_fwd[:, m - 1]
+    if m < wzc - 1:
+        Mm -= (complex(uz[m]) * complex(lz[m + 1])) * prev
+    out[:, m] = torch.linalg.inv(Mm)
+    return out
+
+
+def _twisted_solve(tinv, lz, uz, rhs):
+    """Solve with twisted factors (mirrors the K1 kernel's two half-chains)."""
+    B, wzc, w, _ = tinv.shape
+    m = wzc // 2
+    z = torch.empty_like(rhs)
+    prev = None
+    for k in range(m):
+        t = rhs[:, k] if k == 0 else rhs[:, k] - complex(lz[k]) * prev
+        prev = tinv[:, k] @ t
+        z[:, k] = prev
+    zt = prev
+    prev = None
+    for k in range(wzc - 1, m, -1):
+        t = rhs[:, k] if k == wzc - 1 else rhs[:, k] - complex(uz[k]) * prev
+        prev = tinv[:, k] @ t
+        z[:, k] = prev
+    t = rhs[:, m]
+    if m > 0:
+        t = t - complex(lz[m]) * zt
+    if m < wzc - 1:
+        t = t - complex(uz[m]) * prev
+    x = torch.empty_like(rhs)
+    x[:, m] = tinv[:, m] @ t
+    for k in range(m - 1, -1, -1):
+        x[:, k] = z[:, k] - complex(uz[k]) * (tinv[:, k] @ x[:, k + 1])
+    for k in range(m + 1, wzc):
+        x[:, k] = z[:, k] - complex(lz[k]) * (tinv[:, k] @ x[:, k - 1])
+    return x
+
+
 def _block_solve(sinv, lz, uz, rhs):
     """Solve H_c X = RHS with stored Schur inverses (batched over cells).
 
@@ -231,7 +293,10 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True):
                     for s in range(4):
                         # column-major storage == transpose of the row-major block
                         gblk[:, jr, s] = X[:, rr, :, s * w : (s + 1) * w].transpose(-1, -2)
-            sinv_cm = sinv.transpose(-1, -2).contiguous()
+            if wzc < 3:
+                raise ValueError("cells need at least 3 block rows (nx_c + 2 npml >= 3)")
+            tinv = _twisted_inverses(tw, dg, lz, uz, sinv, device)
+            sinv_cm = tinv.transpose(-1, -2).contiguous()
             for b, ci in enumerate(idxs):
                 cells[ci] = CellFactors(
                     ell, ci, w, wzc, nxc, coffs[ci], sinv_cm[b],

@@ -21,7 +21,7 @@ from paper_1510_01831_b200 import (
     partition_layers,
 )
 from paper_1510_01831_b200.configs import make_config, small_problem
-from paper_1510_01831_b200.offline import _block_solve, build_factors
+from paper_1510_01831_b200.offline import _twisted_solve, build_factors
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -69,7 +69,7 @@ def test_config_generators_are_deterministic_and_match_survey_conventions():
 @pytest.mark.parametrize("case", [dict(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3),
                                   dict(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7)])
 def test_offline_factors_reproduce_superlu_cells_and_green_blocks(case):
-    """Schur factors solve every cell like SuperLU (1e-12), Green blocks equal the
+    """Twisted Schur factors solve every cell like SuperLU (1e-12), Green blocks equal the
     reference's GreenBlockSet construction (green.py:103-129) to 1e-12."""
     prob = small_problem(**case)
     F = build_factors(prob.grid, prob.model, prob.pml, prob.partition, prob.Lc)
@@ -87,7 +87,7 @@ def test_offline_factors_reproduce_superlu_cells_and_green_blocks(case):
             b = rng.standard_normal((cf.wzc, cf.w)) + 1j * rng.standard_normal((cf.wzc, cf.w))
             x0 = oc.solve(b)
             sinv = cf.sinv.transpose(-1, -2)[None]
-            x1 = _block_solve(sinv, cf.lz, cf.uz, torch.tensor(b)[None, :, :, None])[0, :, :, 0].numpy()
+            x1 = _twisted_solve(sinv, cf.lz, cf.uz, torch.tensor(b)[None, :, :, None])[0, :, :, 0].numpy()
             assert np.linalg.norm(x1 - x0) <= 1e-12 * np.linalg.norm(x0)
 
 
