@@ -29,6 +29,8 @@
 // stitched volume).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "pt_launch.cuh"
 
 namespace cg = cooperative_groups;
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   const int m = wzc >> 1, mb = wzc - 1 - m;
   const int nst = h == 0 ? 2 * m + 1 : 2 * mb + 1;
   const int tid = threadIdx.x;
-  const int NS = p.ns;
+  constexpr int NS = K1_NS;  // power of two: slot = c & (NS-1), use = c >> log2(NS)
   const int nIc = p.Lc - 1;
 
   unsigned char* ring = smem;
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     if (tid == K1_CONSUMERS) {
       const uint16_t mask = (uint16_t)(((1u << CM) - 1u) << (h * CM));
       for (int c = 0; c < total; ++c) {
-        const int slot = c % NS, u = c / NS;
+        const int slot = c & (NS - 1), u = c >> K1_NS_LOG2;
         if (u > 0) mbar_wait(&lempty[slot], (uint32_t)((u - 1) & 1));
         const int s = c / nch, ch = c - s * nch;
         const int c0 = ch * jc, cw = min(jc, w - c0);
@@ -210,44 +212,63 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     double2* nxt = VB;
     int c = 0;
     const int partner = (1 - h) * CM + cm;
+    auto kind_of = [&](int s) -> int {
+      return (h == 0) ? (s < m ? 0 : (s == m ? 1 : 2)) : (s < mb ? 0 : (s == mb ? 1 : 2));
+    };
+    // per-thread operand of a step that does not depend on the chain: b_k (elimination and
+    // middle steps) or the stored z_k / y_k (back-substitution).  Loaded one step ahead so the
+    // global-load latency overlaps the previous step's matvec.
+    auto pre_load = [&](int s, double2* v) {
+      const int kb = kblk(s);
+      const int kd = kind_of(s);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = tid + t * K1_CONSUMERS;
+        if (e < nel) v[t] = kd == 2 ? Z[(size_t)kb * nel + e] : rhs(kb, e / NC, e - (e / NC) * NC);
+      }
+    };
+    double2 pv[4];
+    pre_load(0, pv);
     for (int s = 0; s < nst; ++s) {
       const int kb = kblk(s);
-      const int kind = (h == 0) ? (s < m ? 0 : (s == m ? 1 : 2)) : (s < mb ? 0 : (s == mb ? 1 : 2));
+      const int kind = kind_of(s);
       double2 zr[4];
       // ---- prologue: matvec input in cur (in place: every thread owns the same elements throughout)
       if (kind == 0) {
         const double2 cf = h == 0 ? p.lz[cell.lz_off + kb] : p.uz[cell.lz_off + kb];
         const bool first = s == 0;
-        for (int e = tid; e < nel; e += K1_CONSUMERS) {
-          double2 b = rhs(kb, e / NC, e % NC);
-          if (!first) b = csub(b, cmul(cf, cur[e]));
-          cur[e] = b;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int e = tid + t * K1_CONSUMERS;
+          if (e < nel) cur[e] = first ? pv[t] : csub(pv[t], cmul(cf, cur[e]));
         }
       } else if (kind == 1) {
         const uint32_t rx = mapa(XC, (uint32_t)partner), rb = mapa(xbar, (uint32_t)partner);
         for (int e = tid; e < nel; e += K1_CONSUMERS) st_async_c(rx + (uint32_t)e * 16u, cur[e], rb);
         mbar_wait(xbar, 0);
         const double2 lm = p.lz[cell.lz_off + m], um = p.uz[cell.lz_off + m];
-        for (int e = tid; e < nel; e += K1_CONSUMERS) {
-          const double2 zt = h == 0 ? cur[e] : XC[e];  // z_{m-1} (top chain)
-          const double2 yb = h == 0 ? XC[e] : cur[e];  // y_{m+1} (bottom chain)
-          cur[e] = csub(csub(rhs(m, e / NC, e % NC), cmul(lm, zt)), cmul(um, yb));
-        }
-      } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int e = tid + t * K1_CONSUMERS;
-          if (e < nel) zr[t] = Z[(size_t)kb * nel + e];
+          if (e < nel) {
+            const double2 zt = h == 0 ? cur[e] : XC[e];  // z_{m-1} (top chain)
+            const double2 yb = h == 0 ? XC[e] : cur[e];  // y_{m+1} (bottom chain)
+            cur[e] = csub(csub(pv[t], cmul(lm, zt)), cmul(um, yb));
+          }
         }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) zr[t] = pv[t];
       }
+      if (s + 1 < nst) pre_load(s + 1, pv);
       named_bar(1, K1_CONSUMERS);
       // ---- y = Blk[kb] cur
       double2 acc[NC], acc2[NC];
 #pragma unroll
       for (int q = 0; q < NC; ++q) acc[q] = acc2[q] = czero();
       for (int ch = 0; ch < nch; ++ch, ++c) {
-        const int slot = c % NS;
-        mbar_wait(&full[slot], (uint32_t)((c / NS) & 1));
+        const int slot = c & (NS - 1);
+        mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
         const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
         const int c0 = ch * jc, cw = min(jc, w - c0);
         if (mact) {
@@ -307,14 +328,29 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
 }
 
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns) {
+  (void)ns;
+  ns = K1_NS;
   return (size_t)ns * slot_bytes + (size_t)(3 * wmax + K1_CONSUMERS) * nc * 16 + (size_t)nc * sizeof(ColInfo) +
          (size_t)(3 * ns + 1) * 8 + 128;
 }
 
-cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStream_t st) {
+cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
   if (nc * wmax > 4 * K1_CONSUMERS) return cudaErrorInvalidValue;  // epilogue holds <= 4 elements/thread
-  const size_t smax = k1_smem_bytes(wmax, nc, p.slot_bytes, p.ns);
+  static int maxsm = 0;
+  if (!maxsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  // ring slots as large as the shared memory left next to this NC's vectors allows (<= 48 KB)
+  K1Params p = p0;
+  const long long fixed = (long long)k1_smem_bytes(wmax, nc, 0, K1_NS);
+  long long slot = std::min(((long long)maxsm - fixed) / K1_NS, 49152LL) / 16 * 16;
+  if (slot < 16LL * wmax) return cudaErrorInvalidValue;
+  p.slot_bytes = (int)slot;
+  p.ns = K1_NS;
+  const size_t smax = k1_smem_bytes(wmax, nc, p.slot_bytes, K1_NS);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ntasks * 2 * p.cm, 1, 1);
   cfg.blockDim = dim3(K1_THREADS, 1, 1);

@@ -72,6 +72,8 @@ size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns);
 cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStream_t st);
 #define K1_CONSUMERS 256
 #define K1_THREADS (K1_CONSUMERS + 32)
+#define K1_NS 8       // ring slots (multiple of every multicast group size)
+#define K1_NS_LOG2 3
 size_t inner_smem_bytes(int wmax, int R);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
 
