@@ -1,28 +1,34 @@
 // Inner polarized-traces GMRES (replaces _InnerPT.solve_traces, nested.py:134-153).
 //
-// One thread-block CLUSTER (INNER_CS CTAs) per layer-solve job; the job's R
-// right-hand-side instances advance in lockstep and are frozen individually
-// when they converge, so every instance runs exactly the Krylov process of
-// krylov.gmres (krylov.py:53-135): same operator (inner apply_M_polarized on
-// the dense Green blocks, sie.py:203-228 / nested.py:113-122), same left GS
-// preconditioner (sie.py:272-326), MGS Arnoldi with vdot, complex Givens, stop
-// when |g_{j+1}|/beta0 <= inner_ktol, x = V_k y.  The data-dependent iteration
-// count never leaves the device.
+// One thread-block CLUSTER (INNER_CS CTAs) per (layer-solve job, group of up to 8
+// right-hand-side instances).  The instances of a group advance in lockstep and
+// are frozen individually when they converge, so every instance runs exactly the
+// Krylov process of krylov.gmres (krylov.py:53-135): same operator (inner
+// apply_M_polarized on the dense Green blocks, sie.py:203-228 /
+// nested.py:113-122), same left GS preconditioner (sie.py:272-326), MGS Arnoldi
+// with vdot, complex Givens, stop when |g_{j+1}|/beta0 <= inner_ktol, x = V_k y.
+// The data-dependent iteration count never leaves the device.
 //
-// The operator and preconditioner are executed from "item programs" built on
-// the host: each item is one sampled panel = sum_slot G[cell][row][slot] @
-// panel_slot + add - (sub0 + sub1), i.e. exactly the arithmetic of the
-// reference's TraceSystem methods.  Items of one phase are independent: the
-// (item x instance-batch x row-chunk) units of a phase are spread over the
-// cluster's CTAs and phases are separated by cluster barriers
-// (barrier.cluster release/acquire).  Arnoldi, Givens and the final x = V y of
-// instance r run on CTA (r mod INNER_CS) only, so no cross-CTA reduction is
-// needed and the reductions are deterministic.
+// Operator and preconditioner run from host-built "item programs": one item is
+// one sampled panel  sum_slot G[cell][row][slot] @ panel_slot + add - (sub0+sub1),
+// i.e. exactly the arithmetic of the reference's TraceSystem methods; the items
+// of a phase are independent and phases are separated by cluster barriers.
+// A work unit is (item, group of two 8-row tiles of the output panel): its Green
+// tiles (stored tile-major, [row tile][k][8 rows], so one tile is one contiguous
+// bulk copy) arrive by cp.async.bulk on an mbarrier while the CTA gathers the
+// slot panels, and the product runs on the FP64 tensor cores (mma.sync m8n8k4,
+// SASS DMMA) with the group's 8 instances as the N dimension.  Arnoldi, Givens
+// and x = V y of an instance run on one CTA of the cluster, so reductions are
+// deterministic and need no cross-CTA traffic.
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include "pt_launch.cuh"
 
 namespace cg = cooperative_groups;
+
+#define IN_MG 2   // max 8-row tiles per group (2 for w <= 80, else 1)
+#define IN_THREADS 256
 
 __device__ __forceinline__ double2* vecp(const InnerParams& p, int job, int r, int v) {
   return p.scratch + (size_t)(job * p.R + r) * p.inst_stride + (size_t)v * p.nmax;
@@ -30,125 +36,215 @@ __device__ __forceinline__ double2* vecp(const InnerParams& p, int job, int r, i
 
 __device__ __forceinline__ void csync() { cg::this_cluster().sync(); }
 
-// Execute one program (list of phases) for the active instances, spread over the cluster.
+// optional clock64 segment totals (PT_INNER_TPROF): 0 tile issue+add/sub prefetch, 1 panel gather,
+// 2 tile wait, 3 dmma, 4 combine, 5 cluster barriers, 6 arnoldi+givens, 7 rest
+__device__ long long g_in_t[8];
+struct Ticker {
+  bool on;
+  long long t0;
+  __device__ void start() {
+    if (on) t0 = clock64();
+  }
+  __device__ void tick(int i) {
+    if (on) {
+      const long long t = clock64();
+      atomicAdd((unsigned long long*)&g_in_t[i], (unsigned long long)(t - t0));
+      t0 = t;
+    }
+  }
+};
+
+struct InSmem {
+  double2* tiles;   // [2 buffers][4 slots][IN_MG][w][8]
+  double2* pan;     // [4 slots][w][8]
+  double2* red;     // [8 warps][IN_MG*8][8]
+  uint64_t* tbar;   // [2] one mbarrier per tile buffer
+  int* act;         // active local instances
+  IItem* items;     // the op + pre programs (staged once)
+};
+
+// Execute one program (list of phases) for the active instances of this cluster.
 // vmap: program vec ids {0:IN,1:OUT,2:AUX} -> scratch vector index.
-__device__ void run_program(const InnerParams& p, int job, int layer, int w, const int* ph, int nph,
-                            const int vmap[3], const int* act, int nact, double2* pan, double2* red, int q,
-                            int CS) {
-  const int tid = threadIdx.x;
-  const int nb = (nact + INNER_NC - 1) / INNER_NC;
+__device__ void run_program(const InnerParams& p, int job, int layer, int w, int r0, const int* ph, int nph,
+                            const int vmap[3], int nact, const InSmem& S, int q, int CS, uint32_t* tphase,
+                            Ticker& T) {
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const int nmt = (w + 7) >> 3;
+  const int MG = p.mg;  // 8-row tiles per group (shared-memory budget, from the widest layer)
+  const int ngrp = (nmt + MG - 1) / MG;
+  const int kps = (w + 3) >> 2;  // k-steps per slot
+  const CellInfo* cells = p.cells + layer * p.Lc;
+  const size_t tbuf = (size_t)4 * MG * w * 8;  // double2 per tile buffer
+  const uint32_t tbytes = (uint32_t)w * 8u * 16u;
   for (int phz = 0; phz < nph; ++phz) {
     const int it0 = ph[phz], nit = ph[phz + 1] - it0;
-    const int base = nit * nb;
-    int nchunk = 1;
-    if (base > 0 && base < CS) nchunk = min((CS + base - 1) / base, max(1, w / 8));
-    const int units = base * nchunk;
+    // units: an item's tile groups are split into upi contiguous ranges so that small phases
+    // still occupy the whole cluster; the panels of a unit are gathered once
+    const int upi = nit >= CS ? 1 : min(ngrp, (CS + nit - 1) / nit);
+    const int units = nit * upi;
     for (int u = q; u < units; u += CS) {
-      const int ii = u / (nb * nchunk);
-      const int rem = u - ii * nb * nchunk;
-      const int b = rem / nchunk, rc = rem - (rem / nchunk) * nchunk;
-      const IItem item = p.items[it0 + ii];
-      const int b0 = b * INNER_NC;
-      const int nbat = min(INNER_NC, nact - b0);
-      const int i0 = rc * w / nchunk, rows = (rc + 1) * w / nchunk - i0;
-      const int Gc = blockDim.x / rows;
-      if (item.cell >= 0) {
-        // ---- stage slot panels in smem: pan[s][qq][j]
-        for (int e = tid; e < 4 * INNER_NC * w; e += blockDim.x) {
-          const int s = e / (INNER_NC * w);
-          const int r2 = e - s * INNER_NC * w;
-          const int qq = r2 / w, j = r2 - qq * w;
-          double2 v = czero();
-          if (qq < nbat && item.pan[s][0].vec >= 0) {
-            const int r = act[b0 + qq];
-            v = ld_cg(vecp(p, job, r, vmap[item.pan[s][0].vec]) + item.pan[s][0].seg * w + j);
-            if (item.pan[s][1].vec >= 0)
-              v = cadd(v, ld_cg(vecp(p, job, r, vmap[item.pan[s][1].vec]) + item.pan[s][1].seg * w + j));
-          }
-          pan[(s * INNER_NC + qq) * w + j] = v;
+      const int ii = u / upi, part = u - ii * upi;
+      const int g0 = part * ngrp / upi, g1 = (part + 1) * ngrp / upi;
+      const IItem& item = S.items[it0 + ii];
+      int slots[4], ns = 0;
+      if (item.cell >= 0)
+        for (int s = 0; s < 4; ++s)
+          if (item.pan[s][0].vec >= 0) slots[ns++] = s;
+      const CellInfo& cell = cells[item.cell >= 0 ? item.cell : 0];
+      auto issue_tiles = [&](int g, int buf) {
+        const int mt0 = g * MG, nt = min(MG, nmt - mt0);
+        mbar_expect_tx(&S.tbar[buf], tbytes * (uint32_t)(ns * nt));
+        for (int si = 0; si < ns; ++si)
+          for (int t = 0; t < nt; ++t)
+            bulk_g2s(S.tiles + buf * tbuf + ((size_t)si * MG + t) * w * 8,
+                     p.green + cell.green_off + ((size_t)(item.row * 4 + slots[si]) * nmt + mt0 + t) * w * 8,
+                     tbytes, &S.tbar[buf]);
+      };
+      if (ns > 0) {
+        if (tid == 0) issue_tiles(g0, 0);
+        // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill)
+        for (int e = tid; e < ns * w * 8; e += IN_THREADS) {
+          const int si = e / (w * 8), rem = e - si * w * 8;
+          const int k = rem >> 3, qq = rem & 7;
+          const bool okq = qq < nact;
+          const Ref pr = item.pan[slots[si]][0];
+          cp_async16(S.pan + e, vecp(p, job, okq ? r0 + S.act[qq] : r0, vmap[pr.vec]) + pr.seg * w + k, okq);
         }
-        __syncthreads();
-        if (tid < Gc * rows) {
-          const int mi = tid % rows, mg = tid / rows;
-          double2 acc[INNER_NC];
+      }
+      T.tick(0);
+      for (int g = g0; g < g1; ++g) {
+        const int buf = (g - g0) & 1;
+        const int mt0 = g * MG, nt = min(MG, nmt - mt0);
+        const int row0 = mt0 * 8, rows = min(w, row0 + nt * 8) - row0;
+        if (ns > 0 && tid == 0 && g + 1 < g1) issue_tiles(g + 1, buf ^ 1);  // buffer freed last iteration
+        // this thread's output (row, instance) and its combine operands
+        const int oq = tid & 7, orow = tid >> 3;
+        const bool own = orow < rows && oq < nact;
+        const int rr = own ? r0 + S.act[oq] : r0;
+        const int gi = row0 + orow;
+        double2 addv = czero(), subv = czero();
+        if (own) {
 #pragma unroll
-          for (int qq = 0; qq < INNER_NC; ++qq) acc[qq] = czero();
-          const CellInfo& cell = p.cells[layer * p.Lc + item.cell];
-          for (int s = 0; s < 4; ++s) {
-            if (item.pan[s][0].vec < 0) continue;
-            const double2* Gb = p.green + cell.green_off + (size_t)(item.row * 4 + s) * w * w + i0 + mi;
-            const double2* ps = pan + (size_t)s * INNER_NC * w;
-            for (int j = mg; j < w; j += Gc) {
-              const double2 a = __ldg(Gb + (size_t)j * w);
+          for (int t = 0; t < 2; ++t) {
+            if (item.add[t].vec >= 0) addv = cadd(addv, ld_cg(vecp(p, job, rr, vmap[item.add[t].vec]) + item.add[t].seg * w + gi));
+            if (item.sub[t].vec >= 0) subv = cadd(subv, ld_cg(vecp(p, job, rr, vmap[item.sub[t].vec]) + item.sub[t].seg * w + gi));
+          }
+        }
+        double2 y = czero();
+        if (ns > 0) {
+          if (g == g0) {
+            cp_async_wait_all();
+            __syncthreads();
+          }
+          T.tick(1);
+          mbar_wait(&S.tbar[buf], tphase[buf] & 1);
+          tphase[buf]++;
+          T.tick(2);
+          // DMMA: warp wp takes k-steps ks = wp mod 8 of every slot, both tiles of the group:
+          // Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br
+          const int ar = lane >> 2, ak = lane & 3;
+          double c[IN_MG][4];
 #pragma unroll
-              for (int qq = 0; qq < INNER_NC; ++qq) cfma(acc[qq], a, ps[qq * w + j]);
+          for (int t = 0; t < IN_MG; ++t) c[t][0] = c[t][1] = c[t][2] = c[t][3] = 0.0;
+          const double2* tl = S.tiles + buf * tbuf;
+          const int nks = ns * kps;
+          for (int ks = wp; ks < nks; ks += IN_THREADS / 32) {
+            const int si = ks / kps, k = (ks - si * kps) * 4 + ak;
+            const bool kin = k < w;
+            const double2 bv = kin ? S.pan[((size_t)si * w + k) * 8 + ar] : czero();
+#pragma unroll
+            for (int t = 0; t < IN_MG; ++t) {
+              if (t < nt) {
+                const double2 av = kin ? tl[(((size_t)si * MG + t) * w + k) * 8 + ar] : czero();
+                dmma_f64(c[t][0], c[t][1], av.x, bv.x);
+                dmma_f64(c[t][2], c[t][3], av.x, bv.y);
+                dmma_f64(c[t][0], c[t][1], -av.y, bv.y);
+                dmma_f64(c[t][2], c[t][3], av.y, bv.x);
+              }
             }
           }
 #pragma unroll
-          for (int qq = 0; qq < INNER_NC; ++qq) red[(mg * rows + mi) * INNER_NC + qq] = acc[qq];
+          for (int t = 0; t < IN_MG; ++t) {
+            S.red[((wp * IN_MG + t) * 8 + ar) * 8 + 2 * ak] = make_double2(c[t][0], c[t][2]);
+            S.red[((wp * IN_MG + t) * 8 + ar) * 8 + 2 * ak + 1] = make_double2(c[t][1], c[t][3]);
+          }
+          __syncthreads();
+          T.tick(3);
+          if (own) {
+            y = S.red[orow * 8 + oq];
+#pragma unroll
+            for (int g2 = 1; g2 < IN_THREADS / 32; ++g2) y = cadd(y, S.red[(g2 * IN_MG * 8 + orow) * 8 + oq]);
+          }
+        }
+        // ---- combine: out = y + (add0 + add1) - (sub0 + sub1)
+        if (own) {
+          if (item.add[0].vec >= 0) y = cadd(y, addv);
+          if (item.sub[0].vec >= 0) y = csub(y, subv);
+          vecp(p, job, rr, vmap[item.dst.vec])[item.dst.seg * w + gi] = y;
         }
         __syncthreads();
+        T.tick(4);
       }
-      // ---- combine: out = y + add - (sub0 + sub1)
-      for (int e = tid; e < nbat * rows; e += blockDim.x) {
-        const int qq = e / rows, i = i0 + (e - qq * rows);
-        const int r = act[b0 + qq];
-        double2 y = czero();
-        if (item.cell >= 0) {
-          const int li = i - i0;
-          y = red[li * INNER_NC + qq];
-          for (int g = 1; g < Gc; ++g) y = cadd(y, red[(g * rows + li) * INNER_NC + qq]);
-        }
-        if (item.add.vec >= 0) y = cadd(y, ld_cg(vecp(p, job, r, vmap[item.add.vec]) + item.add.seg * w + i));
-        if (item.sub[0].vec >= 0) {
-          double2 sb = ld_cg(vecp(p, job, r, vmap[item.sub[0].vec]) + item.sub[0].seg * w + i);
-          if (item.sub[1].vec >= 0)
-            sb = cadd(sb, ld_cg(vecp(p, job, r, vmap[item.sub[1].vec]) + item.sub[1].seg * w + i));
-          y = csub(y, sb);
-        }
-        vecp(p, job, r, vmap[item.dst.vec])[item.dst.seg * w + i] = y;
-      }
-      __syncthreads();
     }
     csync();
+    T.tick(5);
   }
 }
 
-// rebuild the (cluster-consistent) list of active instances from global state
-__device__ __forceinline__ void rebuild_active(const InnerParams& p, int job, int* act, int* s_nact) {
+// rebuild the (cluster-consistent) list of active local instances from global state
+__device__ __forceinline__ void rebuild_active(const InnerParams& p, int job, int r0, int ni, int* act, int* s_nact) {
   if (threadIdx.x == 0) {
     int na = 0;
-    for (int r = 0; r < p.R; ++r)
-      if (__ldcg(p.state + job * p.R + r) == 0) act[na++] = r;
+    for (int l = 0; l < ni; ++l)
+      if (__ldcg(p.state + job * p.R + r0 + l) == 0) act[na++] = l;
     *s_nact = na;
   }
   __syncthreads();
 }
 
-__global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(PT_THREADS)
+__global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(IN_THREADS, 1)
     inner_gmres_kernel(const InnerParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int CS = INNER_CS;
   const int q = (int)cg::this_cluster().block_rank();
-  const int job = p.stage_jobs[blockIdx.x / CS];
+  const int ngroups = (p.R + 7) >> 3;
+  const int cid = blockIdx.x / CS;
+  const int job = p.stage_jobs[cid / ngroups];
+  const int r0 = (cid % ngroups) * 8;
+  const int ni = min(8, p.R - r0);  // instances of this cluster: r0 .. r0+ni-1
   const int layer = p.jobs[job].layer;
   const int w = p.layers[layer].w;
   const int nIc = p.Lc - 1;
   const int n = 4 * nIc * w;
   const int tid = threadIdx.x;
 
-  double2* pan = reinterpret_cast<double2*>(smem);
-  double2* red = pan + 4 * INNER_NC * w;
-  double* dred = reinterpret_cast<double*>(red + (size_t)PT_THREADS * INNER_NC);
-  int* act = reinterpret_cast<int*>(dred + 64);
-  __shared__ int s_nact, s_st;
+  InSmem S;
+  S.tiles = reinterpret_cast<double2*>(smem);
+  S.pan = S.tiles + (size_t)2 * 4 * p.mg * p.wmax * 8;
+  S.red = S.pan + (size_t)4 * p.wmax * 8;
+  double* dred = reinterpret_cast<double*>(S.red + (IN_THREADS / 32) * IN_MG * 8 * 8);
+  S.tbar = reinterpret_cast<uint64_t*>(dred + 64);
+  S.act = reinterpret_cast<int*>(S.tbar + 2);
+  S.items = reinterpret_cast<IItem*>(S.act + 16);
+  __shared__ int s_nact;
   if (nIc == 0) return;
+  if (tid == 0) {
+    mbar_init(&S.tbar[0], 1);
+    mbar_init(&S.tbar[1], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < p.nitems; i += blockDim.x) S.items[i] = p.items[i];
+  uint32_t tphase[2] = {0, 0};
+  Ticker T;
+  T.on = p.tprof && blockIdx.x == 0 && tid == 0;
+  T.start();
   const int VB = p.cap + 1, VY = p.cap + 2, VT = p.cap + 3, VA = p.cap + 4;
   const size_t hld = (size_t)p.cap + 1;
   auto Hp = [&](int r) { return p.hess + (size_t)(job * p.R + r) * p.hstride; };
 
   // ---- rhs_pol from the Newton tables (sie.py:230-242, negated); elements split over the cluster
-  for (int r = 0; r < p.R; ++r) {
+  for (int l = 0; l < ni; ++l) {
+    const int r = r0 + l;
     double2* B = vecp(p, job, r, VB);
     for (int e = q * blockDim.x + tid; e < n; e += CS * blockDim.x) {
       const int seg = e / w, j = e - seg * w;
@@ -160,16 +256,17 @@ __global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(PT_THREADS)
       B[e] = make_double2(-t.x, -t.y);
     }
   }
-  if (tid < p.R) act[tid] = tid;
-  if (tid == 0) s_nact = p.R;
+  if (tid < ni) S.act[tid] = tid;
+  if (tid == 0) s_nact = ni;
   csync();
 
   // ---- b = pre(rhs), beta0 = ||b||, V_0 = b / beta0 (krylov.py:61-80)
   {
     const int vm[3] = {VB, VY, VA};
-    run_program(p, job, layer, w, p.pre_ph, p.pre_nph, vm, act, s_nact, pan, red, q, CS);
+    run_program(p, job, layer, w, r0, p.pre_ph, p.pre_nph, vm, s_nact, S, q, CS, tphase, T);
   }
-  for (int r = q; r < p.R; r += CS) {
+  for (int l = q; l < ni; l += CS) {
+    const int r = r0 + l;
     const double2* Y = vecp(p, job, r, VY);
     double ss = 0.0;
     for (int e = tid; e < n; e += blockDim.x) {
@@ -194,33 +291,35 @@ __global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(PT_THREADS)
     __syncthreads();
   }
   csync();
-  rebuild_active(p, job, act, &s_nact);
+  rebuild_active(p, job, r0, ni, S.act, &s_nact);
 
   for (int j = 0; j < p.max_iter && s_nact > 0; ++j) {
     const int nact = s_nact;
     if (j + 1 > p.cap) {  // basis capacity exhausted: the host retries with a larger capacity
       for (int a = 0; a < nact; ++a) {
-        const int r = act[a];
-        if (r % CS == q && tid == 0) {
-          p.state[job * p.R + r] = 2;
-          p.iters[job * p.R + r] = -1;
+        const int l = S.act[a];
+        if (l % CS == q && tid == 0) {
+          p.state[job * p.R + r0 + l] = 2;
+          p.iters[job * p.R + r0 + l] = -1;
           atomicMax(p.err, 5);
         }
       }
       csync();
-      rebuild_active(p, job, act, &s_nact);
+      rebuild_active(p, job, r0, ni, S.act, &s_nact);
       break;
     }
     {
       const int vm1[3] = {j, VT, VA};
-      run_program(p, job, layer, w, p.op_ph, p.op_nph, vm1, act, nact, pan, red, q, CS);
+      run_program(p, job, layer, w, r0, p.op_ph, p.op_nph, vm1, nact, S, q, CS, tphase, T);
       const int vm2[3] = {VT, j + 1, VA};
-      run_program(p, job, layer, w, p.pre_ph, p.pre_nph, vm2, act, nact, pan, red, q, CS);
+      run_program(p, job, layer, w, r0, p.pre_ph, p.pre_nph, vm2, nact, S, q, CS, tphase, T);
+      T.tick(7);
     }
     // ---- MGS Arnoldi + Givens for the instances this CTA owns (krylov.py:89-127)
     for (int a = 0; a < nact; ++a) {
-      const int r = act[a];
-      if (r % CS != q) continue;
+      const int l = S.act[a];
+      if (l % CS != q) continue;
+      const int r = r0 + l;
       double2* W = vecp(p, job, r, j + 1);
       double2* H = Hp(r);
       double2* col = H + (size_t)j * hld;
@@ -246,6 +345,7 @@ __global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(PT_THREADS)
       }
       ss = block_sum(ss, dred);
       const double hn = sqrt(ss);
+      __shared__ int s_st;
       if (tid == 0) {
         double2* g = H + hld * p.cap;
         double2* cs = g + (p.cap + 1);
@@ -296,20 +396,23 @@ __global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(PT_THREADS)
         }
       __syncthreads();
     }
+    T.tick(6);
     csync();
-    rebuild_active(p, job, act, &s_nact);
+    rebuild_active(p, job, r0, ni, S.act, &s_nact);
+    T.tick(5);
   }
 
   // ---- x = V_k y, traces = down + up (nested.py:153), owner CTA per instance
-  double2* yv = pan;  // reuse smem: y[cap]
-  for (int r = q; r < p.R; r += CS) {
+  double2* yv = S.pan;  // reuse smem: y[cap]
+  for (int l = q; l < ni; l += CS) {
+    const int r = r0 + l;
     const int k = p.iters[job * p.R + r];
     if (tid == 0 && k > 0) {
       const double2* H = Hp(r);
       const double2* g = H + hld * p.cap;
       for (int i = k - 1; i >= 0; --i) {
         double2 s = czero();
-        for (int l = i + 1; l < k; ++l) cfma(s, H[(size_t)l * hld + i], yv[l]);
+        for (int m = i + 1; m < k; ++m) cfma(s, H[(size_t)m * hld + i], yv[m]);
         const double2 num = csub(g[i], s);
         const double2 den = H[(size_t)i * hld + i];
         const double dd = den.x * den.x + den.y * den.y;
@@ -342,15 +445,28 @@ __global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(PT_THREADS)
   }
 }
 
-size_t inner_smem_bytes(int wmax, int R) {
+int inner_mg(int wmax) { return wmax <= 80 ? 2 : 1; }
+
+size_t inner_smem_bytes(int wmax, int nitems) {
   const int w = wmax < 8 ? 8 : wmax;
-  return (size_t)4 * INNER_NC * w * 16 + (size_t)PT_THREADS * INNER_NC * 16 + 64 * 8 + (size_t)R * 4 + 64;
+  return (size_t)(2 * 4 * inner_mg(wmax) + 4) * w * 8 * 16 + (size_t)(IN_THREADS / 32) * IN_MG * 8 * 8 * 16 + 64 * 8 +
+         16 + 64 + (size_t)nitems * sizeof(IItem) + 128;
 }
 
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   if (njobs == 0 || p.Lc < 2) return cudaSuccess;
-  const size_t sm = inner_smem_bytes(p.wmax, p.R);
+  const size_t sm = inner_smem_bytes(p.wmax, p.nitems);
   cudaFuncSetAttribute(inner_gmres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  inner_gmres_kernel<<<njobs * INNER_CS, PT_THREADS, sm, st>>>(p);
+  const int ngroups = (p.R + 7) / 8;
+  inner_gmres_kernel<<<njobs * ngroups * INNER_CS, IN_THREADS, sm, st>>>(p);
   return cudaGetLastError();
+}
+
+void inner_tprof_dump() {
+  long long t[8];
+  cudaMemcpyFromSymbol(t, g_in_t, sizeof(t));
+  fprintf(stderr, "inner tprof (cycles, CTA 0): tiles+prefetch %lld gather %lld tilewait %lld dmma %lld combine %lld "
+          "cluster-bar %lld arnoldi %lld rest %lld\n", t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
+  long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_in_t, z, sizeof(z));
 }

@@ -30,6 +30,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "pt_launch.cuh"
 
@@ -37,6 +38,17 @@ namespace cg = cooperative_groups;
 
 struct ColInfo {
   int jid, r, panmask, vol, nout, vfull, opos[4], pad[6];
+};
+
+// Per-element descriptor of K1 (see the consumer section): base pointers of the per-step operands.
+struct Desc {
+  const double2* pb;
+  const double2* vb;
+  const double2* tt;
+  const double2* tbm;
+  double2* ob;
+  double2 pc;
+  int vstride, ostride, okind;  // okind: 0 none, 1 Newton tables, 2 base[k*ostride]
 };
 
 template <int NC>
@@ -61,13 +73,13 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   double2* VB = VA + w * NC;
   double2* XC = VB + w * NC;  // partner's half-chain vector at the middle block
   double2* red = XC + w * NC;
-  ColInfo* cols = reinterpret_cast<ColInfo*>(red + K1_CONSUMERS * NC);
+  ColInfo* cols = reinterpret_cast<ColInfo*>(red + (K1_CONSUMERS / 32) * w * NC);
   uint64_t* full = reinterpret_cast<uint64_t*>(cols + NC);
   uint64_t* lempty = full + NS;
   uint64_t* cempty = lempty + NS;
   uint64_t* xbar = cempty + NS;
 
-  const int jc = max(1, min(w, p.slot_bytes / (w * 16)));
+  const int jc = max(4, min((w + 3) & ~3, p.slot_bytes / (w * 16)) & ~3);  // multiple of 4 (DMMA k-steps)
   const int nch = (w + jc - 1) / jc;
   const int total = nst * nch;
   const double2* S = p.sinv + cell.sinv_off;
@@ -121,9 +133,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     // ------------------------------------------------------------ producer warp
     if (tid == K1_CONSUMERS) {
       const uint16_t mask = (uint16_t)(((1u << CM) - 1u) << (h * CM));
-      for (int c = 0; c < total; ++c) {
+      for (int c = 0; c < total && !(p.dbg & 1); ++c) {
         const int slot = c & (NS - 1), u = c >> K1_NS_LOG2;
-        if (u > 0) mbar_wait(&lempty[slot], (uint32_t)((u - 1) & 1));
+        if (u > 0) mbar_wait_sleep(&lempty[slot], (uint32_t)((u - 1) & 1));
         const int s = c / nch, ch = c - s * nch;
         const int c0 = ch * jc, cw = min(jc, w - c0);
         const uint32_t bytes = (uint32_t)cw * w * 16u;
@@ -136,7 +148,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         } else {
           if (u > 0) mbar_arrive_remote(mapa(&cempty[slot], (uint32_t)(h * CM + issuer)));
           if (issuer == cm) {
-            if (u > 0) mbar_wait(&cempty[slot], (uint32_t)((u - 1) & 1));
+            if (u > 0) mbar_wait_sleep(&cempty[slot], (uint32_t)((u - 1) & 1));
             bulk_g2s_mc(dst, src, bytes, &full[slot], mask);
           }
         }
@@ -144,91 +156,158 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     }
   } else {
     // ------------------------------------------------------------ consumers
-    const int G = K1_CONSUMERS / w;
-    const bool mact = tid < G * w;
-    const int mi = tid % w, mg = tid / w;
+    const int lane = tid & 31, wp = tid >> 5;
+    const int rw = (w + 31) >> 5;  // row blocks of 32 lanes
     double2* Z = p.Z + task.zoff + (size_t)cm * wzc * w * NC;
-
-    auto rhs = [&](int k, int j, int q) -> double2 {
-      const ColInfo& ci = cols[q];
-      if (ci.jid < 0) return czero();
-      if (p.pass == 2) return p.bd[((size_t)ci.r * wzc + k) * w + j];
-      double2 inner = czero();
-      if (k >= cell.lo && k < cell.hi) {
-        const int X = cell.off + k;
-#pragma unroll
-        for (int sl = 0; sl < 4; ++sl)
-          if ((ci.panmask >> sl & 1) && j == lay.prow[sl])
-            inner = cadd(inner, cmul(lay.coef[sl], p.P[((size_t)(ci.jid * 4 + sl) * p.R + ci.r) * p.wx + X]));
-        if (ci.vol == 1 && j >= lay.lo && j < lay.hi)
-          inner = cadd(inner, p.f[ci.r * p.f_stride + (size_t)(lay.off + j) * p.wx + X]);
-        else if (ci.vol == 2)
-          inner = cadd(inner, p.f[ci.r * p.f_stride + (size_t)j * p.wx + X]);
-      }
-      if (p.pass == 1) {
-#pragma unroll
-        for (int sl = 0; sl < 4; ++sl) {
-          const bool has = sl < 2 ? cell.has_top : cell.has_bot;
-          if (has && k == cell.krow[sl]) {
-            const int I = sl < 2 ? cell.cell - 1 : cell.cell;
-            const double2 t = p.tr[((((size_t)ci.jid * p.R + ci.r) * nIc + I) * 2 + (sl & 1)) * p.wmax + j];
-            return cadd(cmul(cell.coef[sl], t), inner);
-          }
-        }
-      }
-      return inner;
-    };
-
-    auto emit = [&](int k, int e, double2 x) {
-      const int i = e / NC, q = e - (e / NC) * NC;
-      const ColInfo& ci = cols[q];
-      if (ci.jid < 0) return;
-      if (p.pass == 2) {
-        p.xd[((size_t)ci.r * wzc + k) * w + i] = x;
-      } else if (p.pass == 0) {
-#pragma unroll
-        for (int idx = 0; idx < 4; ++idx) {
-          const bool need = idx < 2 ? cell.has_top : cell.has_bot;
-          if (need && k == cell.srow[idx])
-            p.tables[((((size_t)ci.jid * p.Lc + cell.cell) * 4 + idx) * p.R + ci.r) * p.wmax + i] = x;
-        }
-      } else if (k >= cell.lo && k < cell.hi) {
-        const int X = cell.off + k;
-        if (ci.nout < 0) {
-          if (ci.vfull)
-            p.u[ci.r * p.u_stride + (size_t)i * p.wx + X] = x;
-          else if (i >= lay.lo && i < lay.hi)
-            p.u[ci.r * p.u_stride + (size_t)(lay.off + i) * p.wx + X] = x;
-        } else {
-#pragma unroll
-          for (int o = 0; o < 4; ++o)
-            if (i == ci.opos[o]) p.smp[((size_t)(ci.jid * 4 + o) * p.R + ci.r) * p.wx + X] = x;
-        }
-      }
-    };
-
     const int nel = w * NC;
-    double2* cur = VA;
-    double2* nxt = VB;
-    int c = 0;
     const int partner = (1 - h) * CM + cm;
     auto kind_of = [&](int s) -> int {
       return (h == 0) ? (s < m ? 0 : (s == m ? 1 : 2)) : (s < mb ? 0 : (s == mb ? 1 : 2));
     };
-    // per-thread operand of a step that does not depend on the chain: b_k (elimination and
-    // middle steps) or the stored z_k / y_k (back-substitution).  Loaded one step ahead so the
-    // global-load latency overlaps the previous step's matvec.
-    auto pre_load = [&](int s, double2* v) {
-      const int kb = kblk(s);
-      const int kd = kind_of(s);
+    // Per-element descriptors, built once: every per-step operand is base[k*stride], so a step's
+    // prologue/epilogue is a few loads and FMAs instead of index arithmetic and branches.
+    //   pb  panel source P[job][slot][rhs][off_c + k]   (pc = layer slot coefficient)
+    //   vb  volume source f (split or full slab) / dense test rhs
+    //   tt, tbm  cell trace sources of the interfaces above / below (reconstruction pass)
+    //   ob  output: Newton table rows, sampled layer row, stitched volume or dense test output
+    Desc* dsm = reinterpret_cast<Desc*>(full + 3 * NS + 2);  // [nel] descriptors in shared memory
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int e = tid + t * K1_CONSUMERS;
-        if (e < nel) v[t] = kd == 2 ? Z[(size_t)kb * nel + e] : rhs(kb, e / NC, e - (e / NC) * NC);
+    for (int t = 0; t < 4; ++t) {
+      Desc d;
+      d.pb = d.vb = d.tt = d.tbm = nullptr;
+      d.ob = nullptr;
+      d.pc = czero();
+      d.vstride = 1;
+      d.ostride = 1;
+      d.okind = 0;
+      const int e = tid + t * K1_CONSUMERS;
+      if (e >= nel) continue;
+      const int j = e / NC, q = e - (e / NC) * NC;
+      const ColInfo ci = cols[q];
+      if (ci.jid < 0) {
+        dsm[e] = d;
+        continue;
+      }
+      if (p.pass == 2) {
+        d.vb = p.bd + (size_t)ci.r * wzc * w + j;
+        d.vstride = w;
+        d.ob = p.xd + (size_t)ci.r * wzc * w + j;
+        d.ostride = w;
+        d.okind = 2;
+        dsm[e] = d;
+        continue;
+      }
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl)
+        if ((ci.panmask >> sl & 1) && j == lay.prow[sl]) {
+          d.pb = p.P + ((size_t)(ci.jid * 4 + sl) * p.R + ci.r) * p.wx + cell.off;
+          d.pc = lay.coef[sl];
+        }
+      if (ci.vol == 1 && j >= lay.lo && j < lay.hi)
+        d.vb = p.f + ci.r * p.f_stride + (size_t)(lay.off + j) * p.wx + cell.off;
+      else if (ci.vol == 2)
+        d.vb = p.f + ci.r * p.f_stride + (size_t)j * p.wx + cell.off;
+      if (p.pass == 1) {
+        const size_t tb0 = ((size_t)ci.jid * p.R + ci.r) * nIc;
+        if (cell.has_top) d.tt = p.tr + ((tb0 + cell.cell - 1) * 2) * p.wmax + j;
+        if (cell.has_bot) d.tbm = p.tr + ((tb0 + cell.cell) * 2) * p.wmax + j;
+        if (ci.nout < 0) {
+          if (ci.vfull) {
+            d.ob = p.u + ci.r * p.u_stride + (size_t)j * p.wx + cell.off;
+            d.okind = 2;
+          } else if (j >= lay.lo && j < lay.hi) {
+            d.ob = p.u + ci.r * p.u_stride + (size_t)(lay.off + j) * p.wx + cell.off;
+            d.okind = 2;
+          }
+        } else {
+#pragma unroll
+          for (int o = 0; o < 4; ++o)
+            if (j == ci.opos[o]) {
+              d.ob = p.smp + ((size_t)(ci.jid * 4 + o) * p.R + ci.r) * p.wx + cell.off;
+              d.okind = 2;
+            }
+        }
+      } else {
+        d.ob = p.tables + (((size_t)ci.jid * p.Lc + cell.cell) * 4 * p.R + ci.r) * p.wmax + j;
+        d.okind = 1;
+      }
+      dsm[e] = d;
+    }
+    // Operands of a step that do not depend on the chain are fetched ONE STEP AHEAD as raw values
+    // into registers (pa: panel value, or the stored z_k / y_k of a back-substitution step;
+    // pb: volume value); no arithmetic touches them until their step runs.
+#define K1_FETCH(S_)                                                                                \
+  do {                                                                                              \
+    const int kb_ = kblk(S_);                                                                       \
+    const bool back_ = kind_of(S_) == 2;                                                            \
+    const bool kept_ = kb_ >= cell.lo && kb_ < cell.hi;                                             \
+    _Pragma("unroll") for (int t = 0; t < 4; ++t) {                                                 \
+      const int e = tid + t * K1_CONSUMERS;                                                         \
+      pa[t] = czero();                                                                              \
+      pb[t] = czero();                                                                              \
+      if (e < nel) {                                                                                \
+        if (back_) {                                                                                \
+          pa[t] = Z[(size_t)kb_ * nel + e];                                                         \
+        } else if (p.pass == 2) {                                                                   \
+          const double2* vb_ = dsm[e].vb;                                                           \
+          if (vb_) pb[t] = vb_[(size_t)kb_ * w];                                                    \
+        } else if (kept_) {                                                                         \
+          const double2* pb_ = dsm[e].pb;                                                           \
+          const double2* vb_ = dsm[e].vb;                                                           \
+          if (pb_) pa[t] = pb_[kb_];                                                                \
+          if (vb_) pb[t] = vb_[kb_];                                                                \
+        }                                                                                           \
+      }                                                                                             \
+    }                                                                                               \
+  } while (0)
+    // b_k[j] from the prefetched raw operands: cell trace source + (panel + volume), the reference's
+    // order of additions (sie.py:338-340)
+    auto bval = [&](int k, int e, double2 va, double2 vb) -> double2 {
+      const Desc& d = dsm[e];
+      if (p.pass == 2) return vb;
+      double2 inner = (d.pb && k >= cell.lo && k < cell.hi) ? cmul(d.pc, va) : czero();
+      inner = cadd(inner, vb);
+      if (p.pass == 1) {
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl)
+          if (k == cell.krow[sl]) {
+            const double2* base = sl < 2 ? d.tt : d.tbm;
+            if (base) inner = cadd(cmul(cell.coef[sl], base[(sl & 1) * p.wmax]), inner);
+          }
+      }
+      return inner;
+    };
+    auto emit = [&](int k, int e, double2 x) {
+      const Desc& d = dsm[e];
+      if (d.okind == 2) {
+        if (p.pass == 2 || (k >= cell.lo && k < cell.hi)) d.ob[(size_t)k * d.ostride] = x;
+      } else if (d.okind == 1) {
+#pragma unroll
+        for (int idx = 0; idx < 4; ++idx) {
+          const bool need = idx < 2 ? cell.has_top : cell.has_bot;
+          if (need && k == cell.srow[idx]) d.ob[(size_t)idx * p.R * p.wmax] = x;
+        }
       }
     };
-    double2 pv[4];
-    pre_load(0, pv);
+
+    // optional per-phase clock64 totals of CTA 0 / thread 0 (PT_K1_TPROF)
+    const bool tp = p.tprof != nullptr && blockIdx.x == 0 && tid == 0;
+    long long t0 = 0, tacc[6] = {0, 0, 0, 0, 0, 0};
+#define K1_TICK(I_)                           \
+  do {                                        \
+    if (tp) {                                 \
+      const long long t_ = clock64();         \
+      if ((I_) >= 0) tacc[(I_)] += t_ - t0;   \
+      t0 = t_;                                \
+    }                                         \
+  } while (0)
+
+    double2* cur = VA;
+    double2* nxt = VB;
+    int c = 0;
+    double2 pa[4], pb[4];
+    K1_FETCH(0);
+    K1_TICK(-1);
     for (int s = 0; s < nst; ++s) {
       const int kb = kblk(s);
       const int kind = kind_of(s);
@@ -236,11 +315,13 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       // ---- prologue: matvec input in cur (in place: every thread owns the same elements throughout)
       if (kind == 0) {
         const double2 cf = h == 0 ? p.lz[cell.lz_off + kb] : p.uz[cell.lz_off + kb];
-        const bool first = s == 0;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int e = tid + t * K1_CONSUMERS;
-          if (e < nel) cur[e] = first ? pv[t] : csub(pv[t], cmul(cf, cur[e]));
+          if (e < nel) {
+            const double2 b = bval(kb, e, pa[t], pb[t]);
+            cur[e] = s == 0 ? b : csub(b, cmul(cf, cur[e]));
+          }
         }
       } else if (kind == 1) {
         const uint32_t rx = mapa(XC, (uint32_t)partner), rb = mapa(xbar, (uint32_t)partner);
@@ -253,75 +334,149 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           if (e < nel) {
             const double2 zt = h == 0 ? cur[e] : XC[e];  // z_{m-1} (top chain)
             const double2 yb = h == 0 ? XC[e] : cur[e];  // y_{m+1} (bottom chain)
-            cur[e] = csub(csub(pv[t], cmul(lm, zt)), cmul(um, yb));
+            cur[e] = csub(csub(bval(m, e, pa[t], pb[t]), cmul(lm, zt)), cmul(um, yb));
           }
         }
       } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) zr[t] = pv[t];
+        for (int t = 0; t < 4; ++t) zr[t] = pa[t];
       }
-      if (s + 1 < nst) pre_load(s + 1, pv);
+      K1_TICK(0);
+      if (s + 1 < nst) K1_FETCH(s + 1);
+      K1_TICK(1);
       named_bar(1, K1_CONSUMERS);
-      // ---- y = Blk[kb] cur
-      double2 acc[NC], acc2[NC];
+      K1_TICK(2);
+      if constexpr (NC == 8) {
+        // ---- y = Blk[kb] cur on the FP64 tensor cores: mma.sync m8n8k4 f64 (SASS DMMA.8x8x4).
+        // Work items (8-row tile mt, k-step parity par) are dealt to the 7 consumer warps; per
+        // k-step of 4 columns: Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br.  A fragments come from
+        // the column-major block in the ring, B fragments from cur[k][0..8).
+        const int nmt = (w + 7) >> 3;
+        const int nitems = 2 * nmt;
+        const int ar = lane >> 2, ak = lane & 3;
+        double cm_[K1_DMMA_ITEMS][4];
 #pragma unroll
-      for (int q = 0; q < NC; ++q) acc[q] = acc2[q] = czero();
-      for (int ch = 0; ch < nch; ++ch, ++c) {
-        const int slot = c & (NS - 1);
-        mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
-        const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
-        const int c0 = ch * jc, cw = min(jc, w - c0);
-        if (mact) {
-          int jj = mg;
-          for (; jj + G < cw; jj += 2 * G) {
-            const double2 a0 = blk[jj * w + mi], a1 = blk[(jj + G) * w + mi];
-            const double2* t0 = cur + (c0 + jj) * NC;
-            const double2* t1 = cur + (c0 + jj + G) * NC;
+        for (int it = 0; it < K1_DMMA_ITEMS; ++it) cm_[it][0] = cm_[it][1] = cm_[it][2] = cm_[it][3] = 0.0;
+        for (int ch = 0; ch < nch; ++ch, ++c) {
+          const int slot = c & (NS - 1);
+          if (!(p.dbg & 1)) mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
+          const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
+          const int c0 = ch * jc, c1 = min(w, c0 + jc);
+          const int ksa = c0 >> 2, ksb = (c1 + 3) >> 2;  // jc is a multiple of 4
 #pragma unroll
-            for (int q = 0; q < NC; ++q) {
-              cfma(acc[q], a0, t0[q]);
-              cfma(acc2[q], a1, t1[q]);
+          for (int it = 0; it < K1_DMMA_ITEMS; ++it) {
+            const int u = wp + (K1_CONSUMERS / 32) * it;
+            if (u < nitems) {
+              const int mt = u >> 1, par = u & 1;
+              for (int ks = ksa + ((par - ksa) & 1); ks < ksb; ks += 2) {
+                const int k = 4 * ks + ak;
+                double2 av = czero(), bv = czero();
+                if (k < c1) {
+                  av = blk[(k - c0) * w + mt * 8 + ar];
+                  bv = cur[k * 8 + ar];
+                }
+                dmma_f64(cm_[it][0], cm_[it][1], av.x, bv.x);
+                dmma_f64(cm_[it][2], cm_[it][3], av.x, bv.y);
+                dmma_f64(cm_[it][0], cm_[it][1], -av.y, bv.y);
+                dmma_f64(cm_[it][2], cm_[it][3], av.y, bv.x);
+              }
             }
           }
-          if (jj < cw) {
-            const double2 a0 = blk[jj * w + mi];
-            const double2* t0 = cur + (c0 + jj) * NC;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&lempty[slot]);
+        }
+        K1_TICK(3);
 #pragma unroll
-            for (int q = 0; q < NC; ++q) cfma(acc[q], a0, t0[q]);
+        for (int it = 0; it < K1_DMMA_ITEMS; ++it) {
+          const int u = wp + (K1_CONSUMERS / 32) * it;
+          if (u < nitems) {
+            const int mt = u >> 1, par = u & 1;
+            const int row = mt * 8 + ar;
+            if (row < w) {
+              red[(par * w + row) * 8 + 2 * ak] = make_double2(cm_[it][0], cm_[it][2]);
+              red[(par * w + row) * 8 + 2 * ak + 1] = make_double2(cm_[it][1], cm_[it][3]);
+            }
+          }
+        }
+      } else {
+      // ---- y = Blk[kb] cur.  Lane l owns rows l, l+32, l+64, l+96 (consecutive rows across a warp:
+      // conflict-free 16-byte loads of the column-major block); warp wp owns columns j = wp mod 8
+      // of every ring chunk and reads each vector entry cur[j][0..NC) once (broadcast).
+      double2 acc[K1_RW][NC];
+#pragma unroll
+      for (int r = 0; r < K1_RW; ++r)
+#pragma unroll
+        for (int q = 0; q < NC; ++q) acc[r][q] = czero();
+      for (int ch = 0; ch < nch; ++ch, ++c) {
+        const int slot = c & (NS - 1);
+        if (!(p.dbg & 1)) mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
+        const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
+        const int c0 = ch * jc, cw = min(jc, w - c0);
+        if (!(p.dbg & 2)) {
+          for (int jj = wp; jj < cw; jj += K1_CONSUMERS / 32) {
+            double2 tv[NC];
+#pragma unroll
+            for (int q = 0; q < NC; ++q) tv[q] = cur[(c0 + jj) * NC + q];
+            const double2* col = blk + jj * w + lane;
+            // warp-uniform row-block bound; rows >= w of the last block read neighbouring shared
+            // memory (still inside the allocation) and are discarded at the partial-sum write
+#pragma unroll
+            for (int r = 0; r < K1_RW; ++r) {
+              if (r < rw) {
+                const double2 a = col[32 * r];
+#pragma unroll
+                for (int q = 0; q < NC; ++q) cfma(acc[r][q], a, tv[q]);
+              }
+            }
           }
         }
         __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&lempty[slot]);
+        if (lane == 0) mbar_arrive(&lempty[slot]);
       }
-      if (mact) {
+      K1_TICK(3);
 #pragma unroll
-        for (int q = 0; q < NC; ++q) red[(mg * w + mi) * NC + q] = cadd(acc[q], acc2[q]);
+      for (int r = 0; r < K1_RW; ++r) {
+        const int i = lane + 32 * r;
+        if (i < w)
+#pragma unroll
+          for (int q = 0; q < NC; ++q) red[(wp * w + i) * NC + q] = acc[r][q];
+      }
       }
       named_bar(1, K1_CONSUMERS);
+      K1_TICK(4);
       // ---- epilogue
       const double2 cf = kind == 2 ? (h == 0 ? p.uz[cell.lz_off + kb] : p.lz[cell.lz_off + kb]) : czero();
+#pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int e = tid + t * K1_CONSUMERS;
-        if (e >= nel) break;
-        const int i = e / NC, q = e - (e / NC) * NC;
-        double2 y = red[i * NC + q];
-        for (int g = 1; g < G; ++g) y = cadd(y, red[(g * w + i) * NC + q]);
-        if (kind == 0) {
-          nxt[e] = y;
-          Z[(size_t)kb * nel + e] = y;
-        } else if (kind == 1) {
-          nxt[e] = y;
-          if (h == 0) emit(m, e, y);
-        } else {
-          const double2 x = csub(zr[t], cmul(cf, y));
-          nxt[e] = x;
-          emit(kb, e, x);
+        if (e < nel) {
+          const int i = e / NC, q = e - (e / NC) * NC;
+          double2 y = red[i * NC + q];
+          constexpr int npart = NC == 8 ? 2 : K1_CONSUMERS / 32;  // DMMA: 2 k-parities; DFMA: 7 warps
+#pragma unroll
+          for (int g = 1; g < npart; ++g) y = cadd(y, red[(g * w + i) * NC + q]);
+          if (kind == 0) {
+            nxt[e] = y;
+            Z[(size_t)kb * nel + e] = y;
+          } else if (kind == 1) {
+            nxt[e] = y;
+            if (h == 0) emit(m, e, y);
+          } else {
+            const double2 x = csub(zr[t], cmul(cf, y));
+            nxt[e] = x;
+            emit(kb, e, x);
+          }
         }
       }
+      K1_TICK(5);
       double2* tmp = cur;
       cur = nxt;
       nxt = tmp;
     }
+    if (tp)
+      for (int i = 0; i < 6; ++i) p.tprof[i] = tacc[i];
+#undef K1_FETCH
+#undef K1_TICK
   }
   __syncwarp();
   cl.sync();  // no CTA leaves while a partner may still write into its shared memory
@@ -330,13 +485,15 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns) {
   (void)ns;
   ns = K1_NS;
-  return (size_t)ns * slot_bytes + (size_t)(3 * wmax + K1_CONSUMERS) * nc * 16 + (size_t)nc * sizeof(ColInfo) +
-         (size_t)(3 * ns + 1) * 8 + 128;
+  // ring + three [w][NC] vectors + the [8 warps][w][NC] partial sums + column info + barriers
+  return (size_t)ns * slot_bytes + (size_t)(3 + K1_CONSUMERS / 32) * wmax * nc * 16 + (size_t)nc * sizeof(ColInfo) +
+         (size_t)(3 * ns + 2) * 8 + (size_t)wmax * nc * sizeof(Desc) + 128;
 }
 
 cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
   if (nc * wmax > 4 * K1_CONSUMERS) return cudaErrorInvalidValue;  // epilogue holds <= 4 elements/thread
+  if (wmax > 32 * K1_RW) return cudaErrorInvalidValue;             // lanes own <= K1_RW rows each
   static int maxsm = 0;
   if (!maxsm) {
     int dev = 0;
@@ -368,7 +525,16 @@ cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStre
   case N:                                                                                             \
     cudaFuncSetAttribute(k1_twisted<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);     \
     if (2 * p.cm > 8) cudaFuncSetAttribute(k1_twisted<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
-    return cudaLaunchKernelEx(&cfg, k1_twisted<N>, p);
+    {                                                                                                 \
+      cudaError_t e_ = cudaLaunchKernelEx(&cfg, k1_twisted<N>, p);                                    \
+      if (e_ != cudaSuccess) {                                                                        \
+        cudaFuncAttributes fa;                                                                        \
+        cudaFuncGetAttributes(&fa, k1_twisted<N>);                                                    \
+        fprintf(stderr, "k1_twisted<%d> launch failed: regs %d maxthreads %d smem %zu dyn %zu grid %d cm %d\n", \
+                N, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smax, cfg.gridDim.x, p.cm);  \
+      }                                                                                               \
+      return e_;                                                                                      \
+    }
     PT_K1_CASE(1)
     PT_K1_CASE(2)
     PT_K1_CASE(4)

@@ -194,3 +194,21 @@ __global__ void k_vol_norm2(const double2* f, long long stride, long long N, dou
   s = block_sum(s, red);
   if (threadIdx.x == 0) atomicAdd(out + r, s);
 }
+
+// Green blocks, column-major [16 blocks][w cols][w rows] -> tile-major [16][ceil(w/8)][w][8]
+// (rows >= w zero-padded), the layout the inner kernel streams with one bulk copy per tile.
+__global__ void k_green_tiles(const double2* src, double2* dst, int w) {
+  const int nmt = (w + 7) >> 3;
+  const long long total = 16LL * nmt * w * 8;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e & 7);
+    long long rest = e >> 3;
+    const int k = (int)(rest % w);
+    rest /= w;
+    const int mt = (int)(rest % nmt);
+    const int b = (int)(rest / nmt);
+    const int i = mt * 8 + r;
+    dst[e] = i < w ? src[((size_t)b * w + k) * w + i] : make_double2(0.0, 0.0);
+  }
+}

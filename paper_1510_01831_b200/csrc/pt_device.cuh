@@ -53,11 +53,11 @@ struct OJob {
   Ref dst[4], add[4], sub[4][2];
 };
 
-// One inner item: output panel = sum_slot G[cell][row][slot] @ panel_slot + add - (sub0+sub1).
+// One inner item: output panel = sum_slot G[cell][row][slot] @ panel_slot + (add0+add1) - (sub0+sub1).
 struct IItem {
   int cell, row;     // cell < 0: no Green product (pure combination)
-  Ref pan[4][2];
-  Ref dst, add, sub[2];
+  Ref pan[4][2];     // slot panels (the inner kernel uses pan[s][0] only)
+  Ref dst, add[2], sub[2];
 };
 
 // K1 task: one cell, a contiguous range of columns (job, rhs) of its layer.
@@ -118,6 +118,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// wait with exponential nanosleep backoff: for a lone producer thread whose spinning would
+// otherwise steal issue slots from the consumer warps of its SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ns = 32;
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    ns = ns < 256 ? ns * 2 : 256;
+  }
+}
 // 1-D bulk async copy global -> shared, completion counted on an mbarrier (SASS UBLKCP)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -159,6 +175,23 @@ __device__ __forceinline__ void st_async_c(uint32_t cluster_addr, double2 v, uin
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+
+// FP64 tensor-core MMA: C(8x8) += A(8x4) B(4x8), one double of A, B and two of C per thread
+// (row-major A fragment: row = lane/4, k = lane%4; col-major B: k = lane%4, col = lane/4;
+//  C: row = lane/4, cols 2*(lane%4) and +1).  SASS: DMMA.8x8x4.
+__device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// 16-byte global -> shared async copy (LDGSTS), L2 only (.cg: coherent with data written by other
+// CTAs before a cluster barrier); pred = false zero-fills the destination
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(pred ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ---------------------------------------------------------------- reductions
 

@@ -38,6 +38,8 @@ struct K1Params {
   double2* Z;
   const double2* bd;  // pass 2 (dense test mode): b [q][wzc][w]
   double2* xd;        // pass 2: x [q][wzc][w]
+  long long* tprof;   // optional per-phase clock64 totals of CTA 0 (debug instrumentation)
+  int dbg;            // debug: 1 = no factor streaming (timing only), 2 = no matvec (timing only)
 };
 
 struct InnerParams {
@@ -66,15 +68,21 @@ struct InnerParams {
   unsigned long long* counters;  // [0] inner iterations, [1] Green touches, [2] instances
   int* hist;              // [PT_HIST] histogram of inner iteration counts
   long long op_blocks, pre_blocks;  // block matvecs per inner op / preconditioner application
+  int tprof;              // debug: accumulate clock64 segment totals of CTA 0 (PT_INNER_TPROF)
+  int nitems;             // op + pre program items (staged in shared memory)
+  int mg;                 // 8-row Green tiles per work group (inner_mg(wmax))
 };
 
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns);
 cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStream_t st);
-#define K1_CONSUMERS 256
+#define K1_CONSUMERS 224  // 7 consumer warps + 1 producer warp: 8 warps keep 255 registers per thread
 #define K1_THREADS (K1_CONSUMERS + 32)
 #define K1_NS 8       // ring slots (multiple of every multicast group size)
 #define K1_NS_LOG2 3
-size_t inner_smem_bytes(int wmax, int R);
+#define K1_RW 4       // rows per lane in the K1 matvec: cell width w <= 128
+#define K1_DMMA_ITEMS 5  // (8-row tile, k parity) work items per warp: 2*ceil(128/8) <= 5*7
+size_t inner_smem_bytes(int wmax, int nitems);
+int inner_mg(int wmax);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
 
 __global__ void k_gather_panels(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
@@ -93,3 +101,4 @@ __global__ void k_accum_x(VecView x, const double2* V, long long vstride, long l
 __global__ void k_residual(const double2* u, const double2* f, long long stride, int wz, int wx, const double2* tx,
                            const double2* tz, const double* m, double omega2, const int* rmap, double* out);
 __global__ void k_vol_norm2(const double2* f, long long stride, long long N, double* out);
+__global__ void k_green_tiles(const double2* src, double2* dst, int w);

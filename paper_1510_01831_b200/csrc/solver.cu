@@ -84,7 +84,7 @@ struct pt_ctx {
   // inner item programs
   IItem* items_d = nullptr;
   int *op_ph_d = nullptr, *pre_ph_d = nullptr;
-  int op_nph = 0, pre_nph = 0;
+  int op_nph = 0, pre_nph = 0, nitems = 0;
   long long op_blocks = 0, pre_blocks = 0;
   // outer stages
   Stage newton, op, refl, recon, layer_solve;
@@ -331,7 +331,7 @@ static int build_inner(pt_ctx* c) {
     it.cell = cell;
     it.row = row;
     for (int s = 0; s < 4; ++s) it.pan[s][0] = it.pan[s][1] = NOREF;
-    it.dst = it.add = it.sub[0] = it.sub[1] = NOREF;
+    it.dst = it.add[0] = it.add[1] = it.sub[0] = it.sub[1] = NOREF;
     return it;
   };
   std::vector<IItem> items;
@@ -342,7 +342,18 @@ static int build_inner(pt_ctx* c) {
     for (int s = 0; s < 4; ++s)
       if (it.pan[s][0].vec >= 0) ++acc;
   };
-  // ---- OP: one phase
+  // ---- OP (sie.py:203-228).  Phase 0: full traces T = d + p into AUX's down half (the panels
+  // d[i]+p[i] / p[i]+d[i] of the reference -- complex addition commutes, so one vector serves
+  // both); phase 1: every item reads single panels.
+  oph.push_back((int)items.size());
+  for (int I = 0; I < nI; ++I)
+    for (int s = 0; s < 2; ++s) {
+      IItem x = item(-1, 0);
+      x.dst = Ref{2, D(I, s)};
+      x.add[0] = Ref{0, D(I, s)};
+      x.add[1] = Ref{0, U(I, s)};
+      items.push_back(x);
+    }
   oph.push_back((int)items.size());
   for (int cc = 0; cc < Lc; ++cc) {
     const bool top = cc >= 1, bot = cc <= Lc - 2;
@@ -351,16 +362,17 @@ static int build_inner(pt_ctx* c) {
       for (int s = 0; s < 2; ++s) {
         IItem x = item(cc, 2 + s);
         if (top) {
-          x.pan[0][0] = Ref{0, D(ib - 1, 0)};
-          x.pan[0][1] = Ref{0, U(ib - 1, 0)};
-          x.pan[1][0] = Ref{0, D(ib - 1, 1)};
-          x.pan[1][1] = Ref{0, U(ib - 1, 1)};
+          x.pan[0][0] = Ref{2, D(ib - 1, 0)};  // d + p above
+          x.pan[1][0] = Ref{2, D(ib - 1, 1)};
         }
         x.pan[2][0] = Ref{0, U(ib, 0)};
         x.pan[3][0] = Ref{0, U(ib, 1)};
         x.dst = Ref{1, D(ib, s)};
-        x.sub[0] = Ref{0, D(ib, s)};
-        if (s == 0) x.sub[1] = Ref{0, U(ib, 0)};
+        if (s == 0) {
+          x.sub[0] = Ref{2, D(ib, 0)};  // wb[0] - (d + p)
+        } else {
+          x.sub[0] = Ref{0, D(ib, 1)};  // wb[1] - d
+        }
         count(x, opb);
         items.push_back(x);
       }
@@ -371,17 +383,14 @@ static int build_inner(pt_ctx* c) {
         x.pan[0][0] = Ref{0, D(it, 0)};
         x.pan[1][0] = Ref{0, D(it, 1)};
         if (bot) {
-          x.pan[2][0] = Ref{0, U(ib, 0)};
-          x.pan[2][1] = Ref{0, D(ib, 0)};
-          x.pan[3][0] = Ref{0, U(ib, 1)};
-          x.pan[3][1] = Ref{0, D(ib, 1)};
+          x.pan[2][0] = Ref{2, D(ib, 0)};  // p + d below
+          x.pan[3][0] = Ref{2, D(ib, 1)};
         }
         x.dst = Ref{1, U(it, s)};
         if (s == 0) {
-          x.sub[0] = Ref{0, U(it, 0)};
+          x.sub[0] = Ref{0, U(it, 0)};  // wt[0] - p
         } else {
-          x.sub[0] = Ref{0, D(it, 1)};
-          x.sub[1] = Ref{0, U(it, 1)};
+          x.sub[0] = Ref{2, D(it, 1)};  // wt[1] - (d + p)
         }
         count(x, opb);
         items.push_back(x);
@@ -430,7 +439,7 @@ static int build_inner(pt_ctx* c) {
     for (int s = 0; s < 2; ++s) {
       IItem x = item(-1, 0);
       x.dst = Ref{2, U(I, s)};
-      x.add = Ref{0, U(I, s)};
+      x.add[0] = Ref{0, U(I, s)};
       x.sub[0] = Ref{2, U(I, s)};
       items.push_back(x);
     }
@@ -458,6 +467,7 @@ static int build_inner(pt_ctx* c) {
   c->pre_nph = (int)pph.size() - 1;
   c->op_blocks = opb;
   c->pre_blocks = preb;
+  c->nitems = (int)items.size();
   if (nI == 0) return 0;
   if (upload(&c->items_d, items.data(), items.size())) return PT_CUDA_ERROR;
   if (upload(&c->op_ph_d, oph.data(), oph.size())) return PT_CUDA_ERROR;
@@ -531,6 +541,7 @@ static void k1_policy(pt_ctx* c, const std::vector<int>& ncols_per_group, int* n
   if (nc != 1 && nc != 2 && nc != 4 && nc != 8) {
     nc = 1;
     for (int cand : {8, 4, 2, 1}) {
+      if (cand * c->wmax > 640 && cand > 1) continue;  // keep the partial sums next to the ring
       long long tasks = 0;
       for (int n : ncols_per_group) tasks += (long long)c->Lc * ((n + cand * cm - 1) / (cand * cm));
       if (2LL * cm * tasks >= c->num_sms || cand == 1) {
@@ -639,6 +650,11 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   kp.u = io.u;
   kp.u_stride = io.u_stride;
   kp.Z = c->Z;
+  static long long* tprof_d = nullptr;
+  static bool tprof_on = std::getenv("PT_K1_TPROF") != nullptr;
+  if (tprof_on && !tprof_d) cudaMalloc(&tprof_d, 6 * sizeof(long long));
+  kp.tprof = tprof_on ? tprof_d : nullptr;
+  kp.dbg = std::getenv("PT_K1_DBG") ? atoi(std::getenv("PT_K1_DBG")) : 0;
   // volume sources/outputs are indexed by the real RHS id: pre-offset through rmap on the host is not
   // possible per column, so stage buffers use compact q and f/u use q as well (callers compact f/u).
   if (c->Lc > 1) {
@@ -681,6 +697,9 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     ip.hist = c->hist_d;
     ip.op_blocks = c->op_blocks;
     ip.pre_blocks = c->pre_blocks;
+    ip.tprof = std::getenv("PT_INNER_TPROF") != nullptr;
+    ip.nitems = c->nitems;
+    ip.mg = inner_mg(c->wmax);
     LaunchScope ls(c, 1);
     CK(inner_launch(ip, J, c->st));
   }
@@ -689,6 +708,13 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     LaunchScope ls(c, 0);
     CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
     c->k1_bytes += T->bytes;
+  }
+  if (tprof_on) {
+    long long tt[6];
+    cudaStreamSynchronize(c->st);
+    cudaMemcpy(tt, tprof_d, sizeof(tt), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "K1 tprof nc=%d ntasks=%d: prologue %lld preload %lld bar1 %lld matvec %lld bar2 %lld epi %lld\n",
+            T->nc, T->n, tt[0], tt[1], tt[2], tt[3], tt[4], tt[5]);
   }
   if (S.any_sample) {
     LaunchScope ls(c, 2);
@@ -774,6 +800,7 @@ static int check_err(pt_ctx* c, int* code) {
   return 0;
 }
 
+void inner_tprof_dump();
 // ------------------------------------------------------------------ the online solve (sie.py:392-439)
 
 struct RhsState {
@@ -1044,6 +1071,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   CK(cudaStreamSynchronize(c->st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
+  if (std::getenv("PT_INNER_TPROF")) inner_tprof_dump();
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   int ecode = 0;
@@ -1150,8 +1178,8 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       li.prow[s] = rowv[s];
       li.coef[s] = make_double2(pb->layer_coefs[(l * 4 + s) * 2], pb->layer_coefs[(l * 4 + s) * 2 + 1]);
     }
-    if (li.w > PT_THREADS) {
-      g_err = "layer width n_l + 2 npml exceeds 256";
+    if (li.w > 128) {
+      g_err = "layer width n_l + 2 npml exceeds 128 (K1 holds <= 4 rows per lane)";
       return PT_BAD_ARGUMENT;
     }
     c->wmax = std::max(c->wmax, li.w);
@@ -1205,7 +1233,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       ci.green_off = goff;
       ci.lz_off = zoff;
       soff += (long long)ci.wzc * ci.w * ci.w;
-      goff += 16LL * ci.w * ci.w;
+      goff += 16LL * ((ci.w + 7) / 8) * 8 * ci.w;  // tile-major, rows padded to 8
       zoff += ci.wzc;
       c->wzcmax = std::max(c->wzcmax, ci.wzc);
       c->cel.push_back(ci);
@@ -1218,8 +1246,15 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
     const int id = ci.layer * c->Lc + ci.cell;
     CK(cudaMemcpy(c->sinv_d + ci.sinv_off, pb->sinv[id], sizeof(double2) * (size_t)ci.wzc * ci.w * ci.w,
                   cudaMemcpyDefault));
-    CK(cudaMemcpy(c->green_d + ci.green_off, pb->green[id], sizeof(double2) * 16 * (size_t)ci.w * ci.w,
-                  cudaMemcpyDefault));
+    {
+      double2* tmp = nullptr;
+      CK(cudaMalloc(&tmp, sizeof(double2) * 16 * (size_t)ci.w * ci.w));
+      CK(cudaMemcpy(tmp, pb->green[id], sizeof(double2) * 16 * (size_t)ci.w * ci.w, cudaMemcpyDefault));
+      k_green_tiles<<<256, 256>>>(tmp, c->green_d + ci.green_off, ci.w);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+      cudaFree(tmp);
+    }
     CK(cudaMemcpy(c->lz_d + ci.lz_off, pb->lz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
     CK(cudaMemcpy(c->uz_d + ci.lz_off, pb->uz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
   }
