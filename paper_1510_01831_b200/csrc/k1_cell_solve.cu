@@ -40,18 +40,22 @@ struct ColInfo {
   int jid, r, panmask, vol, nout, vfull, opos[4], pad[6];
 };
 
+// partial-sum sets of the matvec: DMMA path (NC == 8) splits k by parity, DFMA path by warp
+__host__ __device__ constexpr int k1_nparts(int nc) { return K1_CONSUMERS / 32; }  // one partial set per warp
+
 // Per-element descriptor of K1 (see the consumer section): base pointers of the per-step operands.
+// 32-bit element offsets (-1 = absent) keep it at 24 bytes so the shared-memory ring stays large.
 struct Desc {
-  const double2* pb;
-  const double2* vb;
-  const double2* tt;
-  const double2* tbm;
-  double2* ob;
-  double2 pc;
-  int vstride, ostride, okind;  // okind: 0 none, 1 Newton tables, 2 base[k*ostride]
+  int pb;                // into P (panel source; coefficient = layer coef[slot])
+  int vb;                // into f (passes 0/1) or the dense test rhs (pass 2)
+  int tt, tbm;           // into tr: cell trace sources above / below (reconstruction pass)
+  int ob;                // into the output array selected by okind
+  unsigned char slot;    // panel slot of pb
+  unsigned char okind;   // 0 none, 1 Newton tables, 2 volume u, 3 sampled smp, 4 dense test xd
+  unsigned char pad[2];
 };
 
-template <int NC>
+template <int NC, int NMT>
 __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cl = cg::this_cluster();
@@ -70,17 +74,19 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
 
   unsigned char* ring = smem;
   double2* VA = reinterpret_cast<double2*>(ring + (size_t)NS * p.slot_bytes);
-  double2* VB = VA + w * NC;
-  double2* XC = VB + w * NC;  // partner's half-chain vector at the middle block
-  double2* red = XC + w * NC;
-  ColInfo* cols = reinterpret_cast<ColInfo*>(red + (K1_CONSUMERS / 32) * w * NC);
+  const int w4v = (w + 3) & ~3;
+  double2* VB = VA + w4v * NC;
+  double2* XC = VB + w4v * NC;  // partner's half-chain vector at the middle block
+  double2* red = XC + w4v * NC;
+  ColInfo* cols = reinterpret_cast<ColInfo*>(red + k1_nparts(NC) * w * NC);
   uint64_t* full = reinterpret_cast<uint64_t*>(cols + NC);
   uint64_t* lempty = full + NS;
   uint64_t* cempty = lempty + NS;
   uint64_t* xbar = cempty + NS;
 
-  const int jc = max(4, min((w + 3) & ~3, p.slot_bytes / (w * 16)) & ~3);  // multiple of 4 (DMMA k-steps)
-  const int nch = (w + jc - 1) / jc;
+  const int w4 = (w + 3) & ~3;  // stored columns per block (zero padded)
+  const int jc = NC == 8 ? K1_JC8 : max(4, min(w4, p.slot_bytes / (w * 16)) & ~3);  // multiple of 4
+  const int nch = (w4 + jc - 1) / jc;
   const int total = nst * nch;
   const double2* S = p.sinv + cell.sinv_off;
   // factor block used by step s of this half
@@ -89,6 +95,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     return s < mb ? wzc - 1 - s : (s == mb ? m : m + (s - mb));
   };
 
+  for (int e = tid; e < 2 * w4v * NC; e += blockDim.x) VA[e] = czero();
   if (tid < NC) {
     ColInfo ci;
     ci.jid = -1;
@@ -135,20 +142,20 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       const uint16_t mask = (uint16_t)(((1u << CM) - 1u) << (h * CM));
       for (int c = 0; c < total && !(p.dbg & 1); ++c) {
         const int slot = c & (NS - 1), u = c >> K1_NS_LOG2;
-        if (u > 0) mbar_wait_sleep(&lempty[slot], (uint32_t)((u - 1) & 1));
+        if (u > 0) mbar_wait(&lempty[slot], (uint32_t)((u - 1) & 1));  // try_wait sleeps in hardware
         const int s = c / nch, ch = c - s * nch;
-        const int c0 = ch * jc, cw = min(jc, w - c0);
+        const int c0 = ch * jc, cw = min(jc, w4 - c0);
         const uint32_t bytes = (uint32_t)cw * w * 16u;
         mbar_expect_tx(&full[slot], bytes);
         const int issuer = slot % CM;
-        const double2* src = S + (size_t)kblk(s) * w * w + (size_t)c0 * w;
+        const double2* src = S + (size_t)kblk(s) * w * w4 + (size_t)c0 * w;
         unsigned char* dst = ring + (size_t)slot * p.slot_bytes;
         if (CM == 1) {
           bulk_g2s(dst, src, bytes, &full[slot]);
         } else {
           if (u > 0) mbar_arrive_remote(mapa(&cempty[slot], (uint32_t)(h * CM + issuer)));
           if (issuer == cm) {
-            if (u > 0) mbar_wait_sleep(&cempty[slot], (uint32_t)((u - 1) & 1));
+            if (u > 0) mbar_wait(&cempty[slot], (uint32_t)((u - 1) & 1));
             bulk_g2s_mc(dst, src, bytes, &full[slot], mask);
           }
         }
@@ -174,62 +181,52 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       Desc d;
-      d.pb = d.vb = d.tt = d.tbm = nullptr;
-      d.ob = nullptr;
-      d.pc = czero();
-      d.vstride = 1;
-      d.ostride = 1;
+      d.pb = d.vb = d.tt = d.tbm = d.ob = -1;
+      d.slot = 0;
       d.okind = 0;
       const int e = tid + t * K1_CONSUMERS;
       if (e >= nel) continue;
       const int j = e / NC, q = e - (e / NC) * NC;
       const ColInfo ci = cols[q];
-      if (ci.jid < 0) {
-        dsm[e] = d;
-        continue;
-      }
-      if (p.pass == 2) {
-        d.vb = p.bd + (size_t)ci.r * wzc * w + j;
-        d.vstride = w;
-        d.ob = p.xd + (size_t)ci.r * wzc * w + j;
-        d.ostride = w;
-        d.okind = 2;
-        dsm[e] = d;
-        continue;
-      }
+      if (ci.jid >= 0 && p.pass == 2) {
+        d.vb = (ci.r * wzc) * w + j;
+        d.ob = (ci.r * wzc) * w + j;
+        d.okind = 4;
+      } else if (ci.jid >= 0) {
 #pragma unroll
-      for (int sl = 0; sl < 4; ++sl)
-        if ((ci.panmask >> sl & 1) && j == lay.prow[sl]) {
-          d.pb = p.P + ((size_t)(ci.jid * 4 + sl) * p.R + ci.r) * p.wx + cell.off;
-          d.pc = lay.coef[sl];
-        }
-      if (ci.vol == 1 && j >= lay.lo && j < lay.hi)
-        d.vb = p.f + ci.r * p.f_stride + (size_t)(lay.off + j) * p.wx + cell.off;
-      else if (ci.vol == 2)
-        d.vb = p.f + ci.r * p.f_stride + (size_t)j * p.wx + cell.off;
-      if (p.pass == 1) {
-        const size_t tb0 = ((size_t)ci.jid * p.R + ci.r) * nIc;
-        if (cell.has_top) d.tt = p.tr + ((tb0 + cell.cell - 1) * 2) * p.wmax + j;
-        if (cell.has_bot) d.tbm = p.tr + ((tb0 + cell.cell) * 2) * p.wmax + j;
-        if (ci.nout < 0) {
-          if (ci.vfull) {
-            d.ob = p.u + ci.r * p.u_stride + (size_t)j * p.wx + cell.off;
-            d.okind = 2;
-          } else if (j >= lay.lo && j < lay.hi) {
-            d.ob = p.u + ci.r * p.u_stride + (size_t)(lay.off + j) * p.wx + cell.off;
-            d.okind = 2;
+        for (int sl = 0; sl < 4; ++sl)
+          if ((ci.panmask >> sl & 1) && j == lay.prow[sl]) {
+            d.pb = ((ci.jid * 4 + sl) * p.R + ci.r) * p.wx + cell.off;
+            d.slot = (unsigned char)sl;
           }
-        } else {
-#pragma unroll
-          for (int o = 0; o < 4; ++o)
-            if (j == ci.opos[o]) {
-              d.ob = p.smp + ((size_t)(ci.jid * 4 + o) * p.R + ci.r) * p.wx + cell.off;
+        if (ci.vol == 1 && j >= lay.lo && j < lay.hi)
+          d.vb = (int)(ci.r * p.f_stride) + (lay.off + j) * p.wx + cell.off;
+        else if (ci.vol == 2)
+          d.vb = (int)(ci.r * p.f_stride) + j * p.wx + cell.off;
+        if (p.pass == 1) {
+          const int tb0 = (ci.jid * p.R + ci.r) * nIc;
+          if (cell.has_top) d.tt = ((tb0 + cell.cell - 1) * 2) * p.wmax + j;
+          if (cell.has_bot) d.tbm = ((tb0 + cell.cell) * 2) * p.wmax + j;
+          if (ci.nout < 0) {
+            if (ci.vfull) {
+              d.ob = (int)(ci.r * p.u_stride) + j * p.wx + cell.off;
+              d.okind = 2;
+            } else if (j >= lay.lo && j < lay.hi) {
+              d.ob = (int)(ci.r * p.u_stride) + (lay.off + j) * p.wx + cell.off;
               d.okind = 2;
             }
+          } else {
+#pragma unroll
+            for (int o = 0; o < 4; ++o)
+              if (j == ci.opos[o]) {
+                d.ob = ((ci.jid * 4 + o) * p.R + ci.r) * p.wx + cell.off;
+                d.okind = 3;
+              }
+          }
+        } else {
+          d.ob = ((ci.jid * p.Lc + cell.cell) * 4 * p.R + ci.r) * p.wmax + j;
+          d.okind = 1;
         }
-      } else {
-        d.ob = p.tables + (((size_t)ci.jid * p.Lc + cell.cell) * 4 * p.R + ci.r) * p.wmax + j;
-        d.okind = 1;
       }
       dsm[e] = d;
     }
@@ -249,13 +246,12 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         if (back_) {                                                                                \
           pa[t] = Z[(size_t)kb_ * nel + e];                                                         \
         } else if (p.pass == 2) {                                                                   \
-          const double2* vb_ = dsm[e].vb;                                                           \
-          if (vb_) pb[t] = vb_[(size_t)kb_ * w];                                                    \
+          const int vb_ = dsm[e].vb;                                                                \
+          if (vb_ >= 0) pb[t] = p.bd[(size_t)vb_ + (size_t)kb_ * w];                                \
         } else if (kept_) {                                                                         \
-          const double2* pb_ = dsm[e].pb;                                                           \
-          const double2* vb_ = dsm[e].vb;                                                           \
-          if (pb_) pa[t] = pb_[kb_];                                                                \
-          if (vb_) pb[t] = vb_[kb_];                                                                \
+          const int pb_ = dsm[e].pb, vb_ = dsm[e].vb;                                               \
+          if (pb_ >= 0) pa[t] = p.P[(size_t)pb_ + kb_];                                             \
+          if (vb_ >= 0) pb[t] = p.f[(size_t)vb_ + kb_];                                             \
         }                                                                                           \
       }                                                                                             \
     }                                                                                               \
@@ -263,29 +259,31 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     // b_k[j] from the prefetched raw operands: cell trace source + (panel + volume), the reference's
     // order of additions (sie.py:338-340)
     auto bval = [&](int k, int e, double2 va, double2 vb) -> double2 {
-      const Desc& d = dsm[e];
+      const Desc d = dsm[e];
       if (p.pass == 2) return vb;
-      double2 inner = (d.pb && k >= cell.lo && k < cell.hi) ? cmul(d.pc, va) : czero();
+      double2 inner = (d.pb >= 0 && k >= cell.lo && k < cell.hi) ? cmul(lay.coef[d.slot & 3], va) : czero();
       inner = cadd(inner, vb);
       if (p.pass == 1) {
 #pragma unroll
         for (int sl = 0; sl < 4; ++sl)
           if (k == cell.krow[sl]) {
-            const double2* base = sl < 2 ? d.tt : d.tbm;
-            if (base) inner = cadd(cmul(cell.coef[sl], base[(sl & 1) * p.wmax]), inner);
+            const int base = sl < 2 ? d.tt : d.tbm;
+            if (base >= 0) inner = cadd(cmul(cell.coef[sl], p.tr[(size_t)base + (sl & 1) * p.wmax]), inner);
           }
       }
       return inner;
     };
     auto emit = [&](int k, int e, double2 x) {
-      const Desc& d = dsm[e];
-      if (d.okind == 2) {
-        if (p.pass == 2 || (k >= cell.lo && k < cell.hi)) d.ob[(size_t)k * d.ostride] = x;
+      const Desc d = dsm[e];
+      if (d.okind == 4) {
+        p.xd[(size_t)d.ob + (size_t)k * w] = x;
+      } else if (d.okind >= 2) {
+        if (k >= cell.lo && k < cell.hi) (d.okind == 2 ? p.u : p.smp)[(size_t)d.ob + k] = x;
       } else if (d.okind == 1) {
 #pragma unroll
         for (int idx = 0; idx < 4; ++idx) {
           const bool need = idx < 2 ? cell.has_top : cell.has_bot;
-          if (need && k == cell.srow[idx]) d.ob[(size_t)idx * p.R * p.wmax] = x;
+          if (need && k == cell.srow[idx]) p.tables[(size_t)d.ob + (size_t)idx * p.R * p.wmax] = x;
         }
       }
     };
@@ -319,7 +317,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         for (int t = 0; t < 4; ++t) {
           const int e = tid + t * K1_CONSUMERS;
           if (e < nel) {
-            const double2 b = bval(kb, e, pa[t], pb[t]);
+            const double2 b = (p.dbg & 4) ? pa[t] : bval(kb, e, pa[t], pb[t]);
             cur[e] = s == 0 ? b : csub(b, cmul(cf, cur[e]));
           }
         }
@@ -342,7 +340,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         for (int t = 0; t < 4; ++t) zr[t] = pa[t];
       }
       K1_TICK(0);
-      if (s + 1 < nst) K1_FETCH(s + 1);
+      if (s + 1 < nst && !(p.dbg & 16)) K1_FETCH(s + 1);
       K1_TICK(1);
       named_bar(1, K1_CONSUMERS);
       K1_TICK(2);
@@ -351,51 +349,45 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         // Work items (8-row tile mt, k-step parity par) are dealt to the 7 consumer warps; per
         // k-step of 4 columns: Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br.  A fragments come from
         // the column-major block in the ring, B fragments from cur[k][0..8).
-        const int nmt = (w + 7) >> 3;
-        const int nitems = 2 * nmt;
+        // K split: warp wp takes the k-steps ks = wp (mod 7) of the block and ALL NMT 8-row tiles, so
+        // each warp carries 2*NMT independent accumulator chains (no per-tile predicates); the B
+        // fragment of a k-step is loaded once and shared by the tiles.  Every warp arrives on every
+        // chunk (count 7), having waited only for the chunks it reads.
         const int ar = lane >> 2, ak = lane & 3;
-        double cm_[K1_DMMA_ITEMS][4];
+        double cm_[NMT][4];
 #pragma unroll
-        for (int it = 0; it < K1_DMMA_ITEMS; ++it) cm_[it][0] = cm_[it][1] = cm_[it][2] = cm_[it][3] = 0.0;
+        for (int t = 0; t < NMT; ++t) cm_[t][0] = cm_[t][1] = cm_[t][2] = cm_[t][3] = 0.0;
         for (int ch = 0; ch < nch; ++ch, ++c) {
           const int slot = c & (NS - 1);
-          if (!(p.dbg & 1)) mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
-          const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
-          const int c0 = ch * jc, c1 = min(w, c0 + jc);
-          const int ksa = c0 >> 2, ksb = (c1 + 3) >> 2;  // jc is a multiple of 4
+          const int ks0 = ch * (K1_JC8 / 4), ks1 = min(w4, (ch + 1) * K1_JC8) >> 2;
+          int ks = ks0 + ((wp - ks0) % 7 + 7) % 7;  // first k-step of this warp in the chunk
+          if (ks < ks1) {
+            if (!(p.dbg & 1)) mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
+            const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
+            for (; ks < ks1; ks += K1_CONSUMERS / 32) {
+              const int kl = (ks - ks0) * 4 + ak;  // column inside the chunk
+              const double2 bv = cur[(ks * 4 + ak) * 8 + ar];
+              const double2* ap = blk + kl * w + ar;
 #pragma unroll
-          for (int it = 0; it < K1_DMMA_ITEMS; ++it) {
-            const int u = wp + (K1_CONSUMERS / 32) * it;
-            if (u < nitems) {
-              const int mt = u >> 1, par = u & 1;
-              for (int ks = ksa + ((par - ksa) & 1); ks < ksb; ks += 2) {
-                const int k = 4 * ks + ak;
-                double2 av = czero(), bv = czero();
-                if (k < c1) {
-                  av = blk[(k - c0) * w + mt * 8 + ar];
-                  bv = cur[k * 8 + ar];
-                }
-                dmma_f64(cm_[it][0], cm_[it][1], av.x, bv.x);
-                dmma_f64(cm_[it][2], cm_[it][3], av.x, bv.y);
-                dmma_f64(cm_[it][0], cm_[it][1], -av.y, bv.y);
-                dmma_f64(cm_[it][2], cm_[it][3], av.y, bv.x);
+              for (int t = 0; t < NMT; ++t) {
+                const double2 av = ap[t * 8];
+                dmma_f64(cm_[t][0], cm_[t][1], av.x, bv.x);
+                dmma_f64(cm_[t][2], cm_[t][3], av.x, bv.y);
+                dmma_f64(cm_[t][0], cm_[t][1], -av.y, bv.y);
+                dmma_f64(cm_[t][2], cm_[t][3], av.y, bv.x);
               }
             }
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&lempty[slot]);
+          if (lane == 0) mbar_arrive_relaxed(&lempty[slot]);
         }
         K1_TICK(3);
 #pragma unroll
-        for (int it = 0; it < K1_DMMA_ITEMS; ++it) {
-          const int u = wp + (K1_CONSUMERS / 32) * it;
-          if (u < nitems) {
-            const int mt = u >> 1, par = u & 1;
-            const int row = mt * 8 + ar;
-            if (row < w) {
-              red[(par * w + row) * 8 + 2 * ak] = make_double2(cm_[it][0], cm_[it][2]);
-              red[(par * w + row) * 8 + 2 * ak + 1] = make_double2(cm_[it][1], cm_[it][3]);
-            }
+        for (int t = 0; t < NMT; ++t) {
+          const int row = t * 8 + ar;
+          if (row < w) {
+            red[(wp * w + row) * 8 + 2 * ak] = make_double2(cm_[t][0], cm_[t][2]);
+            red[(wp * w + row) * 8 + 2 * ak + 1] = make_double2(cm_[t][1], cm_[t][3]);
           }
         }
       } else {
@@ -431,7 +423,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&lempty[slot]);
+        if (lane == 0) mbar_arrive_relaxed(&lempty[slot]);
       }
       K1_TICK(3);
 #pragma unroll
@@ -452,7 +444,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         if (e < nel) {
           const int i = e / NC, q = e - (e / NC) * NC;
           double2 y = red[i * NC + q];
-          constexpr int npart = NC == 8 ? 2 : K1_CONSUMERS / 32;  // DMMA: 2 k-parities; DFMA: 7 warps
+          constexpr int npart = k1_nparts(NC);  // one partial-sum set per consumer warp (k split)
 #pragma unroll
           for (int g = 1; g < npart; ++g) y = cadd(y, red[(g * w + i) * NC + q]);
           if (kind == 0) {
@@ -464,7 +456,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           } else {
             const double2 x = csub(zr[t], cmul(cf, y));
             nxt[e] = x;
-            emit(kb, e, x);
+            if (!(p.dbg & 8)) emit(kb, e, x);
           }
         }
       }
@@ -486,7 +478,8 @@ size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns) {
   (void)ns;
   ns = K1_NS;
   // ring + three [w][NC] vectors + the [8 warps][w][NC] partial sums + column info + barriers
-  return (size_t)ns * slot_bytes + (size_t)(3 + K1_CONSUMERS / 32) * wmax * nc * 16 + (size_t)nc * sizeof(ColInfo) +
+  return (size_t)ns * slot_bytes + (size_t)(3 * ((wmax + 3) & ~3) + k1_nparts(nc) * wmax) * nc * 16 +
+         (size_t)nc * sizeof(ColInfo) +
          (size_t)(3 * ns + 2) * 8 + (size_t)wmax * nc * sizeof(Desc) + 128;
 }
 
@@ -504,7 +497,8 @@ cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStre
   K1Params p = p0;
   const long long fixed = (long long)k1_smem_bytes(wmax, nc, 0, K1_NS);
   long long slot = std::min(((long long)maxsm - fixed) / K1_NS, 49152LL) / 16 * 16;
-  if (slot < 16LL * wmax) return cudaErrorInvalidValue;
+  // every chunk must fit its slot: DMMA path K1_JC8 columns, DFMA path at least 4
+  if (slot < 16LL * wmax * (nc == 8 ? K1_JC8 : 4)) return cudaErrorInvalidValue;
   p.slot_bytes = (int)slot;
   p.ns = K1_NS;
   const size_t smax = k1_smem_bytes(wmax, nc, p.slot_bytes, K1_NS);
@@ -520,27 +514,29 @@ cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStre
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  switch (nc) {
-#define PT_K1_CASE(N)                                                                                 \
-  case N:                                                                                             \
-    cudaFuncSetAttribute(k1_twisted<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);     \
-    if (2 * p.cm > 8) cudaFuncSetAttribute(k1_twisted<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
-    {                                                                                                 \
-      cudaError_t e_ = cudaLaunchKernelEx(&cfg, k1_twisted<N>, p);                                    \
-      if (e_ != cudaSuccess) {                                                                        \
-        cudaFuncAttributes fa;                                                                        \
-        cudaFuncGetAttributes(&fa, k1_twisted<N>);                                                    \
-        fprintf(stderr, "k1_twisted<%d> launch failed: regs %d maxthreads %d smem %zu dyn %zu grid %d cm %d\n", \
-                N, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smax, cfg.gridDim.x, p.cm);  \
-      }                                                                                               \
-      return e_;                                                                                      \
-    }
-    PT_K1_CASE(1)
-    PT_K1_CASE(2)
-    PT_K1_CASE(4)
-    PT_K1_CASE(8)
-#undef PT_K1_CASE
-    default:
-      return cudaErrorInvalidValue;
+#define PT_K1_GO(N, M)                                                                                \
+  {                                                                                                   \
+    cudaFuncSetAttribute(k1_twisted<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);  \
+    if (2 * p.cm > 8) cudaFuncSetAttribute(k1_twisted<N, M>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+    return cudaLaunchKernelEx(&cfg, k1_twisted<N, M>, p);                                             \
   }
+  if (nc == 8) {
+    switch ((wmax + 7) >> 3) {  // 8-row tiles of the widest layer (DMMA path)
+      case 1: case 2: case 3: case 4: case 5: case 6: case 7: case 8: PT_K1_GO(8, 8)
+      case 9: PT_K1_GO(8, 9)
+      case 10: PT_K1_GO(8, 10)
+      case 11: PT_K1_GO(8, 11)
+      case 12: PT_K1_GO(8, 12)
+      case 13: case 14: PT_K1_GO(8, 14)
+      case 15: case 16: PT_K1_GO(8, 16)
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (nc) {
+    case 1: PT_K1_GO(1, 1)
+    case 2: PT_K1_GO(2, 1)
+    case 4: PT_K1_GO(4, 1)
+    default: return cudaErrorInvalidValue;
+  }
+#undef PT_K1_GO
 }

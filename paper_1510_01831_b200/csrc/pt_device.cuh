@@ -156,6 +156,13 @@ __device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Relaxed arrive: no release fence.  For consumers releasing a ring slot whose shared-memory
+// contents have already been consumed by executed instructions: a release arrive would wait for
+// ALL outstanding memory operations of the thread (prefetch loads a step ahead, global stores),
+// serialising every chunk on HBM latency.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // shared::cta address of this CTA -> the same variable in CTA `rank` of the cluster
 __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
   uint32_t out;

@@ -1232,7 +1232,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       ci.sinv_off = soff;
       ci.green_off = goff;
       ci.lz_off = zoff;
-      soff += (long long)ci.wzc * ci.w * ci.w;
+      soff += (long long)ci.wzc * ci.w * ((ci.w + 3) & ~3);  // blocks padded to a multiple of 4 columns
       goff += 16LL * ((ci.w + 7) / 8) * 8 * ci.w;  // tile-major, rows padded to 8
       zoff += ci.wzc;
       c->wzcmax = std::max(c->wzcmax, ci.wzc);
@@ -1244,8 +1244,14 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   CK(cudaMalloc(&c->uz_d, sizeof(double2) * (size_t)zoff));
   for (const CellInfo& ci : c->cel) {
     const int id = ci.layer * c->Lc + ci.cell;
-    CK(cudaMemcpy(c->sinv_d + ci.sinv_off, pb->sinv[id], sizeof(double2) * (size_t)ci.wzc * ci.w * ci.w,
-                  cudaMemcpyDefault));
+    {
+      // column-major blocks, zero-padded from w to w4 = roundup(w, 4) columns (DMMA k-steps of 4)
+      const int w4 = (ci.w + 3) & ~3;
+      CK(cudaMemset(c->sinv_d + ci.sinv_off, 0, sizeof(double2) * (size_t)ci.wzc * ci.w * w4));
+      CK(cudaMemcpy2D(c->sinv_d + ci.sinv_off, sizeof(double2) * (size_t)ci.w * w4, pb->sinv[id],
+                      sizeof(double2) * (size_t)ci.w * ci.w, sizeof(double2) * (size_t)ci.w * ci.w, ci.wzc,
+                      cudaMemcpyDefault));
+    }
     {
       double2* tmp = nullptr;
       CK(cudaMalloc(&tmp, sizeof(double2) * 16 * (size_t)ci.w * ci.w));
@@ -1440,8 +1446,8 @@ int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, dou
   CK(cudaMemcpy(bd, b, bytes, cudaMemcpyHostToDevice));
   std::vector<K1Task> tasks;
   long long z = 0;
-  const int nc = 8;
-  for (int q0 = 0; q0 < nrhs; q0 += nc) {  // one cluster pair per 8 columns (cm = 1)
+  const int nc = std::getenv("PT_K1_NC") ? atoi(std::getenv("PT_K1_NC")) : 8;
+  for (int q0 = 0; q0 < nrhs; q0 += nc) {  // one cluster pair per nc columns (cm = 1)
     K1Task t;
     t.cell = layer * c->Lc + cell;
     t.jb = 0;
@@ -1472,6 +1478,12 @@ int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, dou
   kp.ns = c->ns;
   kp.cm = 1;
   kp.Z = c->Z;
+  kp.dbg = std::getenv("PT_K1_DBG") ? atoi(std::getenv("PT_K1_DBG")) : 0;
+  {
+    static long long* tprof_d2 = nullptr;
+    if (std::getenv("PT_K1_TPROF") && !tprof_d2) cudaMalloc(&tprof_d2, 6 * sizeof(long long));
+    kp.tprof = std::getenv("PT_K1_TPROF") ? tprof_d2 : nullptr;
+  }
   kp.bd = bd;
   kp.xd = xd;
   CK(k1_launch(kp, (int)tasks.size(), nc, c->wmax, c->st));
