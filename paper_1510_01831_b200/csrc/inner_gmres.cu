@@ -61,6 +61,7 @@ struct InSmem {
   uint64_t* tbar;   // [2] one mbarrier per tile buffer
   int* act;         // active local instances
   IItem* items;     // the op + pre programs (staged once)
+  long long* goff;  // [Lc] Green-pool offsets of this layer's cells (staged once)
 };
 
 // Execute one program (list of phases) for the active instances of this cluster.
@@ -73,9 +74,9 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
   const int MG = p.mg;  // 8-row tiles per group (shared-memory budget, from the widest layer)
   const int ngrp = (nmt + MG - 1) / MG;
   const int kps = (w + 3) >> 2;  // k-steps per slot
-  const CellInfo* cells = p.cells + layer * p.Lc;
   const size_t tbuf = (size_t)4 * MG * w * 8;  // double2 per tile buffer
   const uint32_t tbytes = (uint32_t)w * 8u * 16u;
+  auto VM = [&](int i) { return i == 0 ? vmap[0] : (i == 1 ? vmap[1] : vmap[2]); };
   for (int phz = 0; phz < nph; ++phz) {
     const int it0 = ph[phz], nit = ph[phz + 1] - it0;
     // units: an item's tile groups are split into upi contiguous ranges so that small phases
@@ -86,29 +87,55 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
       const int ii = u / upi, part = u - ii * upi;
       const int g0 = part * ngrp / upi, g1 = (part + 1) * ngrp / upi;
       const IItem& item = S.items[it0 + ii];
-      int slots[4], ns = 0;
+      int slotp = 0, ns = 0;  // packed slot list: slot of si in bits [2si, 2si+2)
       if (item.cell >= 0)
         for (int s = 0; s < 4; ++s)
-          if (item.pan[s][0].vec >= 0) slots[ns++] = s;
-      const CellInfo& cell = cells[item.cell >= 0 ? item.cell : 0];
+          if (item.pan[s][0].vec >= 0) slotp |= s << (2 * ns++);
+      auto slot_of = [&](int si) { return slotp >> (2 * si) & 3; };
+      const long long goff = S.goff[item.cell >= 0 ? item.cell : 0];
       auto issue_tiles = [&](int g, int buf) {
         const int mt0 = g * MG, nt = min(MG, nmt - mt0);
         mbar_expect_tx(&S.tbar[buf], tbytes * (uint32_t)(ns * nt));
         for (int si = 0; si < ns; ++si)
           for (int t = 0; t < nt; ++t)
             bulk_g2s(S.tiles + buf * tbuf + ((size_t)si * MG + t) * w * 8,
-                     p.green + cell.green_off + ((size_t)(item.row * 4 + slots[si]) * nmt + mt0 + t) * w * 8,
+                     p.green + goff + ((size_t)(item.row * 4 + slot_of(si)) * nmt + mt0 + t) * w * 8,
                      tbytes, &S.tbar[buf]);
       };
+      int negm = 0;  // bit si: slot panel si enters negated (exact)
+      for (int si = 0; si < ns; ++si) negm |= (item.flags >> slot_of(si) & 1) << si;
       if (ns > 0) {
         if (tid == 0) issue_tiles(g0, 0);
-        // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill)
-        for (int e = tid; e < ns * w * 8; e += IN_THREADS) {
-          const int si = e / (w * 8), rem = e - si * w * 8;
-          const int k = rem >> 3, qq = rem & 7;
-          const bool okq = qq < nact;
-          const Ref pr = item.pan[slots[si]][0];
-          cp_async16(S.pan + e, vecp(p, job, okq ? r0 + S.act[qq] : r0, vmap[pr.vec]) + pr.seg * w + k, okq);
+        // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill);
+        // a two-term panel (d + p) is summed on the way in
+        for (int e0 = tid; e0 < ns * w * 8; e0 += 4 * IN_THREADS) {
+          double2 va[4], vb[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {  // all loads of the batch in flight before any store
+            const int e = e0 + u * IN_THREADS;
+            va[u] = vb[u] = czero();
+            if (e < ns * w * 8) {
+              const int si = e / (w * 8), rem = e - si * w * 8;
+              const int k = rem >> 3, qq = rem & 7;
+              const bool okq = qq < nact;
+              const Ref pr = item.pan[slot_of(si)][0], pr2 = item.pan[slot_of(si)][1];
+              const int rr = okq ? r0 + S.act[qq] : r0;
+              if (pr2.vec < 0) {
+                cp_async16(S.pan + e, vecp(p, job, rr, VM(pr.vec)) + pr.seg * w + k, okq);
+              } else if (okq) {
+                va[u] = ld_cg(vecp(p, job, rr, VM(pr.vec)) + pr.seg * w + k);
+                vb[u] = ld_cg(vecp(p, job, rr, VM(pr2.vec)) + pr2.seg * w + k);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * IN_THREADS;
+            if (e < ns * w * 8) {
+              const int si = e / (w * 8);
+              if (item.pan[slot_of(si)][1].vec >= 0) S.pan[e] = cadd(va[u], vb[u]);
+            }
+          }
         }
       }
       T.tick(0);
@@ -122,13 +149,14 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
         const bool own = orow < rows && oq < nact;
         const int rr = own ? r0 + S.act[oq] : r0;
         const int gi = row0 + orow;
-        double2 addv = czero(), subv = czero();
+        double2 addv = czero(), subv = czero(), revv = czero();
         if (own) {
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            if (item.add[t].vec >= 0) addv = cadd(addv, ld_cg(vecp(p, job, rr, vmap[item.add[t].vec]) + item.add[t].seg * w + gi));
-            if (item.sub[t].vec >= 0) subv = cadd(subv, ld_cg(vecp(p, job, rr, vmap[item.sub[t].vec]) + item.sub[t].seg * w + gi));
+            if (item.add[t].vec >= 0) addv = cadd(addv, ld_cg(vecp(p, job, rr, VM(item.add[t].vec)) + item.add[t].seg * w + gi));
+            if (item.sub[t].vec >= 0) subv = cadd(subv, ld_cg(vecp(p, job, rr, VM(item.sub[t].vec)) + item.sub[t].seg * w + gi));
           }
+          if (item.rev.vec >= 0) revv = ld_cg(vecp(p, job, rr, VM(item.rev.vec)) + item.rev.seg * w + gi);
         }
         double2 y = czero();
         if (ns > 0) {
@@ -151,7 +179,10 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
           for (int ks = wp; ks < nks; ks += IN_THREADS / 32) {
             const int si = ks / kps, k = (ks - si * kps) * 4 + ak;
             const bool kin = k < w;
-            const double2 bv = kin ? S.pan[((size_t)si * w + k) * 8 + ar] : czero();
+            double2 bv = kin ? S.pan[((size_t)si * w + k) * 8 + ar] : czero();
+            const double sg = (negm >> si & 1) ? -1.0 : 1.0;
+            bv.x *= sg;
+            bv.y *= sg;
 #pragma unroll
             for (int t = 0; t < IN_MG; ++t) {
               if (t < nt) {
@@ -176,11 +207,14 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
             for (int g2 = 1; g2 < IN_THREADS / 32; ++g2) y = cadd(y, S.red[(g2 * IN_MG * 8 + orow) * 8 + oq]);
           }
         }
-        // ---- combine: out = y + (add0 + add1) - (sub0 + sub1)
+        // ---- combine: t = y + (add0 + add1) - (sub0 + sub1); out = t | rev - t | t - rev
         if (own) {
           if (item.add[0].vec >= 0) y = cadd(y, addv);
           if (item.sub[0].vec >= 0) y = csub(y, subv);
-          vecp(p, job, rr, vmap[item.dst.vec])[item.dst.seg * w + gi] = y;
+          const int mode = item.flags >> 8 & 3;
+          if (mode == 1) y = csub(revv, y);
+          else if (mode == 2) y = csub(y, revv);
+          vecp(p, job, rr, VM(item.dst.vec))[item.dst.seg * w + gi] = y;
         }
         __syncthreads();
         T.tick(4);
@@ -225,7 +259,8 @@ __global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(IN_THREADS, 1
   double* dred = reinterpret_cast<double*>(S.red + (IN_THREADS / 32) * IN_MG * 8 * 8);
   S.tbar = reinterpret_cast<uint64_t*>(dred + 64);
   S.act = reinterpret_cast<int*>(S.tbar + 2);
-  S.items = reinterpret_cast<IItem*>(S.act + 16);
+  S.goff = reinterpret_cast<long long*>(S.act + 16);
+  S.items = reinterpret_cast<IItem*>(S.goff + PT_MAX_LC);
   __shared__ int s_nact;
   if (nIc == 0) return;
   if (tid == 0) {
@@ -234,6 +269,7 @@ __global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(IN_THREADS, 1
     fence_mbar_init();
   }
   for (int i = tid; i < p.nitems; i += blockDim.x) S.items[i] = p.items[i];
+  for (int i = tid; i < p.Lc; i += blockDim.x) S.goff[i] = p.cells[layer * p.Lc + i].green_off;
   uint32_t tphase[2] = {0, 0};
   Ticker T;
   T.on = p.tprof && blockIdx.x == 0 && tid == 0;
@@ -450,7 +486,7 @@ int inner_mg(int wmax) { return wmax <= 80 ? 2 : 1; }
 size_t inner_smem_bytes(int wmax, int nitems) {
   const int w = wmax < 8 ? 8 : wmax;
   return (size_t)(2 * 4 * inner_mg(wmax) + 4) * w * 8 * 16 + (size_t)(IN_THREADS / 32) * IN_MG * 8 * 8 * 16 + 64 * 8 +
-         16 + 64 + (size_t)nitems * sizeof(IItem) + 128;
+         16 + 64 + PT_MAX_LC * 8 + (size_t)nitems * sizeof(IItem) + 128;
 }
 
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {

@@ -41,7 +41,8 @@ struct ColInfo {
 };
 
 // partial-sum sets of the matvec: DMMA path (NC == 8) splits k by parity, DFMA path by warp
-__host__ __device__ constexpr int k1_nparts(int nc) { return K1_CONSUMERS / 32; }  // one partial set per warp
+// rows of the partial-sum area: one [w][NC] set per consumer warp
+__host__ __device__ constexpr int k1_red_rows(int w) { return 7 * w; }
 
 // Per-element descriptor of K1 (see the consumer section): base pointers of the per-step operands.
 // 32-bit element offsets (-1 = absent) keep it at 24 bytes so the shared-memory ring stays large.
@@ -70,6 +71,8 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   const int nst = h == 0 ? 2 * m + 1 : 2 * mb + 1;
   const int tid = threadIdx.x;
   constexpr int NS = K1_NS;  // power of two: slot = c & (NS-1), use = c >> log2(NS)
+  // elements (row, column) per consumer thread: w*NC <= (NC == 8 ? 8*NMT : 32*NMT) * NC
+  constexpr int TT = ((NC == 8 ? 8 * NMT : 32 * NMT) * NC + K1_CONSUMERS - 1) / K1_CONSUMERS;
   const int nIc = p.Lc - 1;
 
   unsigned char* ring = smem;
@@ -78,14 +81,14 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   double2* VB = VA + w4v * NC;
   double2* XC = VB + w4v * NC;  // partner's half-chain vector at the middle block
   double2* red = XC + w4v * NC;
-  ColInfo* cols = reinterpret_cast<ColInfo*>(red + k1_nparts(NC) * w * NC);
+  ColInfo* cols = reinterpret_cast<ColInfo*>(red + k1_red_rows(w) * NC);
   uint64_t* full = reinterpret_cast<uint64_t*>(cols + NC);
   uint64_t* lempty = full + NS;
   uint64_t* cempty = lempty + NS;
   uint64_t* xbar = cempty + NS;
 
   const int w4 = (w + 3) & ~3;  // stored columns per block (zero padded)
-  const int jc = NC == 8 ? K1_JC8 : max(4, min(w4, p.slot_bytes / (w * 16)) & ~3);  // multiple of 4
+  const int jc = NC == 8 ? K1_JC8 : K1_JCD;  // columns per ring chunk
   const int nch = (w4 + jc - 1) / jc;
   const int total = nst * nch;
   const double2* S = p.sinv + cell.sinv_off;
@@ -164,7 +167,6 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   } else {
     // ------------------------------------------------------------ consumers
     const int lane = tid & 31, wp = tid >> 5;
-    const int rw = (w + 31) >> 5;  // row blocks of 32 lanes
     double2* Z = p.Z + task.zoff + (size_t)cm * wzc * w * NC;
     const int nel = w * NC;
     const int partner = (1 - h) * CM + cm;
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     //   ob  output: Newton table rows, sampled layer row, stitched volume or dense test output
     Desc* dsm = reinterpret_cast<Desc*>(full + 3 * NS + 2);  // [nel] descriptors in shared memory
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < TT; ++t) {
       Desc d;
       d.pb = d.vb = d.tt = d.tbm = d.ob = -1;
       d.slot = 0;
@@ -238,7 +240,11 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     const int kb_ = kblk(S_);                                                                       \
     const bool back_ = kind_of(S_) == 2;                                                            \
     const bool kept_ = kb_ >= cell.lo && kb_ < cell.hi;                                             \
-    _Pragma("unroll") for (int t = 0; t < 4; ++t) {                                                 \
+    const int kd_ = kind_of(S_);                                                                    \
+    pcf = czero();                                                                                  \
+    if (kd_ == 0) pcf = h == 0 ? p.lz[cell.lz_off + kb_] : p.uz[cell.lz_off + kb_];                 \
+    else if (kd_ == 2) pcf = h == 0 ? p.uz[cell.lz_off + kb_] : p.lz[cell.lz_off + kb_];            \
+    _Pragma("unroll") for (int t = 0; t < TT; ++t) {                                                \
       const int e = tid + t * K1_CONSUMERS;                                                         \
       pa[t] = czero();                                                                              \
       pb[t] = czero();                                                                              \
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     auto bval = [&](int k, int e, double2 va, double2 vb) -> double2 {
       const Desc d = dsm[e];
       if (p.pass == 2) return vb;
-      double2 inner = (d.pb >= 0 && k >= cell.lo && k < cell.hi) ? cmul(lay.coef[d.slot & 3], va) : czero();
+      double2 inner = (d.pb >= 0 && k >= cell.lo && k < cell.hi) ? cmul(sel4(lay.coef, d.slot), va) : czero();
       inner = cadd(inner, vb);
       if (p.pass == 1) {
 #pragma unroll
@@ -303,31 +309,30 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     double2* cur = VA;
     double2* nxt = VB;
     int c = 0;
-    double2 pa[4], pb[4];
+    double2 pa[TT], pb[TT];
+    double2 pcf;  // chain coefficient of the prefetched step (l_k / u_k), fetched with its operands
     K1_FETCH(0);
+    // step 0 (first block of either half chain): no previous chain value
+#pragma unroll
+    for (int t = 0; t < TT; ++t) {
+      const int e = tid + t * K1_CONSUMERS;
+      if (e < nel) cur[e] = (p.dbg & 4) ? pa[t] : bval(kblk(0), e, pa[t], pb[t]);
+    }
     K1_TICK(-1);
+    // Invariant at the top of step s: cur holds the matvec input of step s (formed by the previous
+    // epilogue), except at the middle step, and pa/pb/pcf hold the prefetched operands of step s.
     for (int s = 0; s < nst; ++s) {
       const int kb = kblk(s);
       const int kind = kind_of(s);
-      double2 zr[4];
-      // ---- prologue: matvec input in cur (in place: every thread owns the same elements throughout)
-      if (kind == 0) {
-        const double2 cf = h == 0 ? p.lz[cell.lz_off + kb] : p.uz[cell.lz_off + kb];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int e = tid + t * K1_CONSUMERS;
-          if (e < nel) {
-            const double2 b = (p.dbg & 4) ? pa[t] : bval(kb, e, pa[t], pb[t]);
-            cur[e] = s == 0 ? b : csub(b, cmul(cf, cur[e]));
-          }
-        }
-      } else if (kind == 1) {
+      const double2 cf = pcf;
+      double2 zr[TT];
+      if (kind == 1) {
         const uint32_t rx = mapa(XC, (uint32_t)partner), rb = mapa(xbar, (uint32_t)partner);
         for (int e = tid; e < nel; e += K1_CONSUMERS) st_async_c(rx + (uint32_t)e * 16u, cur[e], rb);
         mbar_wait(xbar, 0);
         const double2 lm = p.lz[cell.lz_off + m], um = p.uz[cell.lz_off + m];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < TT; ++t) {
           const int e = tid + t * K1_CONSUMERS;
           if (e < nel) {
             const double2 zt = h == 0 ? cur[e] : XC[e];  // z_{m-1} (top chain)
@@ -335,12 +340,12 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
             cur[e] = csub(csub(bval(m, e, pa[t], pb[t]), cmul(lm, zt)), cmul(um, yb));
           }
         }
-      } else {
+      } else if (kind == 2) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) zr[t] = pa[t];
+        for (int t = 0; t < TT; ++t) zr[t] = pa[t];
       }
       K1_TICK(0);
-      if (s + 1 < nst && !(p.dbg & 16)) K1_FETCH(s + 1);
+      if (s + 1 < nst) K1_FETCH(s + 1);
       K1_TICK(1);
       named_bar(1, K1_CONSUMERS);
       K1_TICK(2);
@@ -391,30 +396,33 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           }
         }
       } else {
-      // ---- y = Blk[kb] cur.  Lane l owns rows l, l+32, l+64, l+96 (consecutive rows across a warp:
-      // conflict-free 16-byte loads of the column-major block); warp wp owns columns j = wp mod 8
-      // of every ring chunk and reads each vector entry cur[j][0..NC) once (broadcast).
-      double2 acc[K1_RW][NC];
+      // ---- y = Blk[kb] cur on the FP64 pipes.  Lane l owns rows l + 32 r (r < RW, RW = NMT here,
+      // from the widest layer); warp wp owns columns wp*K1_JW .. +K1_JW of every ring chunk of
+      // K1_JCD = 7*K1_JW columns.  Fixed trip counts: the loop body is K1_JW columns x RW row blocks
+      // x NC right-hand sides of straight-line loads and FMAs.  Rows >= w of the last row block read
+      // neighbouring shared memory and are discarded at the partial-sum write.
+      constexpr int RW = NMT;
+      double2 acc[RW][NC];
 #pragma unroll
-      for (int r = 0; r < K1_RW; ++r)
+      for (int r = 0; r < RW; ++r)
 #pragma unroll
         for (int q = 0; q < NC; ++q) acc[r][q] = czero();
       for (int ch = 0; ch < nch; ++ch, ++c) {
         const int slot = c & (NS - 1);
         if (!(p.dbg & 1)) mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
         const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
-        const int c0 = ch * jc, cw = min(jc, w - c0);
+        const int c0 = ch * K1_JCD, cw = min(K1_JCD, w - c0);
         if (!(p.dbg & 2)) {
-          for (int jj = wp; jj < cw; jj += K1_CONSUMERS / 32) {
-            double2 tv[NC];
 #pragma unroll
-            for (int q = 0; q < NC; ++q) tv[q] = cur[(c0 + jj) * NC + q];
-            const double2* col = blk + jj * w + lane;
-            // warp-uniform row-block bound; rows >= w of the last block read neighbouring shared
-            // memory (still inside the allocation) and are discarded at the partial-sum write
+          for (int u = 0; u < K1_JW; ++u) {
+            const int jj = wp * K1_JW + u;
+            if (jj < cw) {
+              double2 tv[NC];
 #pragma unroll
-            for (int r = 0; r < K1_RW; ++r) {
-              if (r < rw) {
+              for (int q = 0; q < NC; ++q) tv[q] = cur[(c0 + jj) * NC + q];
+              const double2* col = blk + jj * w + lane;
+#pragma unroll
+              for (int r = 0; r < RW; ++r) {
                 const double2 a = col[32 * r];
 #pragma unroll
                 for (int q = 0; q < NC; ++q) cfma(acc[r][q], a, tv[q]);
@@ -427,7 +435,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       }
       K1_TICK(3);
 #pragma unroll
-      for (int r = 0; r < K1_RW; ++r) {
+      for (int r = 0; r < RW; ++r) {
         const int i = lane + 32 * r;
         if (i < w)
 #pragma unroll
@@ -436,28 +444,34 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       }
       named_bar(1, K1_CONSUMERS);
       K1_TICK(4);
-      // ---- epilogue
-      const double2 cf = kind == 2 ? (h == 0 ? p.uz[cell.lz_off + kb] : p.lz[cell.lz_off + kb]) : czero();
+      // ---- epilogue: this step's output, and the matvec input of step s+1 (b_{k'} - coef * out for a
+      // forward step; out itself before the middle step and for back-substitution steps)
+      const int kn = s + 1 < nst ? kind_of(s + 1) : -1;
+      const int kbn = s + 1 < nst ? kblk(s + 1) : 0;
+      const double2 cfn = pcf;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < TT; ++t) {
         const int e = tid + t * K1_CONSUMERS;
         if (e < nel) {
           const int i = e / NC, q = e - (e / NC) * NC;
           double2 y = red[i * NC + q];
-          constexpr int npart = k1_nparts(NC);  // one partial-sum set per consumer warp (k split)
+          // partial sums: one set per consumer warp (DMMA k split / DFMA column split)
 #pragma unroll
-          for (int g = 1; g < npart; ++g) y = cadd(y, red[(g * w + i) * NC + q]);
+          for (int g = 1; g < K1_CONSUMERS / 32; ++g) y = cadd(y, red[(g * w + i) * NC + q]);
+          double2 out = y;
           if (kind == 0) {
-            nxt[e] = y;
             Z[(size_t)kb * nel + e] = y;
           } else if (kind == 1) {
-            nxt[e] = y;
             if (h == 0) emit(m, e, y);
           } else {
-            const double2 x = csub(zr[t], cmul(cf, y));
-            nxt[e] = x;
-            if (!(p.dbg & 8)) emit(kb, e, x);
+            out = csub(zr[t], cmul(cf, y));
+            if (!(p.dbg & 8)) emit(kb, e, out);
           }
+          if (kn == 0) {
+            const double2 b = (p.dbg & 4) ? pa[t] : bval(kbn, e, pa[t], pb[t]);
+            out = csub(b, cmul(cfn, out));
+          }
+          nxt[e] = out;
         }
       }
       K1_TICK(5);
@@ -478,7 +492,7 @@ size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns) {
   (void)ns;
   ns = K1_NS;
   // ring + three [w][NC] vectors + the [8 warps][w][NC] partial sums + column info + barriers
-  return (size_t)ns * slot_bytes + (size_t)(3 * ((wmax + 3) & ~3) + k1_nparts(nc) * wmax) * nc * 16 +
+  return (size_t)ns * slot_bytes + (size_t)(3 * ((wmax + 3) & ~3) + k1_red_rows(wmax)) * nc * 16 +
          (size_t)nc * sizeof(ColInfo) +
          (size_t)(3 * ns + 2) * 8 + (size_t)wmax * nc * sizeof(Desc) + 128;
 }
@@ -486,7 +500,7 @@ size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns) {
 cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStream_t st) {
   if (ntasks == 0) return cudaSuccess;
   if (nc * wmax > 4 * K1_CONSUMERS) return cudaErrorInvalidValue;  // epilogue holds <= 4 elements/thread
-  if (wmax > 32 * K1_RW) return cudaErrorInvalidValue;             // lanes own <= K1_RW rows each
+  if (wmax > 32 * K1_RW) return cudaErrorInvalidValue;             // w <= 128 (DFMA groups, DMMA tiles)
   static int maxsm = 0;
   if (!maxsm) {
     int dev = 0;
@@ -498,7 +512,7 @@ cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStre
   const long long fixed = (long long)k1_smem_bytes(wmax, nc, 0, K1_NS);
   long long slot = std::min(((long long)maxsm - fixed) / K1_NS, 49152LL) / 16 * 16;
   // every chunk must fit its slot: DMMA path K1_JC8 columns, DFMA path at least 4
-  if (slot < 16LL * wmax * (nc == 8 ? K1_JC8 : 4)) return cudaErrorInvalidValue;
+  if (slot < 16LL * wmax * (nc == 8 ? K1_JC8 : K1_JCD)) return cudaErrorInvalidValue;
   p.slot_bytes = (int)slot;
   p.ns = K1_NS;
   const size_t smax = k1_smem_bytes(wmax, nc, p.slot_bytes, K1_NS);
@@ -532,11 +546,21 @@ cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStre
       default: return cudaErrorInvalidValue;
     }
   }
+  const int rw = (wmax + 31) >> 5;  // DFMA path: row blocks of 32 lanes
+#define PT_K1_RW(N)                        \
+  switch (rw) {                            \
+    case 1: PT_K1_GO(N, 1)                 \
+    case 2: PT_K1_GO(N, 2)                 \
+    case 3: PT_K1_GO(N, 3)                 \
+    case 4: PT_K1_GO(N, 4)                 \
+    default: return cudaErrorInvalidValue; \
+  }
   switch (nc) {
-    case 1: PT_K1_GO(1, 1)
-    case 2: PT_K1_GO(2, 1)
-    case 4: PT_K1_GO(4, 1)
+    case 1: PT_K1_RW(1)
+    case 2: PT_K1_RW(2)
+    case 4: PT_K1_RW(4)
     default: return cudaErrorInvalidValue;
   }
+#undef PT_K1_RW
 #undef PT_K1_GO
 }

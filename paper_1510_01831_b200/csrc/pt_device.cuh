@@ -25,6 +25,12 @@ struct LayerInfo {
   double2 coef[4];        // slot coefficients (subdomain.py:157-182)
 };
 
+// a[i & 3] without a dynamically indexed (local-memory) array
+__device__ __forceinline__ double2 sel4(const double2 (&a)[4], int i) {
+  const double2 lo = (i & 1) ? a[1] : a[0], hi = (i & 1) ? a[3] : a[2];
+  return (i & 2) ? hi : lo;
+}
+
 struct CellInfo {
   int layer, cell, w, wzc, nxc, off, lo, hi;  // cell c of layer: block rows [0,wzc), kept [lo,hi)
   int has_top, has_bot;
@@ -54,10 +60,16 @@ struct OJob {
 };
 
 // One inner item: output panel = sum_slot G[cell][row][slot] @ panel_slot + (add0+add1) - (sub0+sub1).
+// One inner work item:
+//   y   = sum_slot G[cell][row][slot] @ (sgn_slot * (pan[slot][0] + pan[slot][1]))
+//   t   = y + (add0 + add1) - (sub0 + sub1)
+//   dst = t (mode 0) | rev - t (mode 1) | t - rev (mode 2)
+// sgn_slot = -1 when bit slot of flags is set; mode = (flags >> 8) & 3.
 struct IItem {
   int cell, row;     // cell < 0: no Green product (pure combination)
-  Ref pan[4][2];     // slot panels (the inner kernel uses pan[s][0] only)
-  Ref dst, add[2], sub[2];
+  Ref pan[4][2];     // slot panels: pan[s][1] (if present) is added to pan[s][0]
+  Ref dst, add[2], sub[2], rev;
+  int flags;
 };
 
 // K1 task: one cell, a contiguous range of columns (job, rhs) of its layer.

@@ -331,7 +331,8 @@ static int build_inner(pt_ctx* c) {
     it.cell = cell;
     it.row = row;
     for (int s = 0; s < 4; ++s) it.pan[s][0] = it.pan[s][1] = NOREF;
-    it.dst = it.add[0] = it.add[1] = it.sub[0] = it.sub[1] = NOREF;
+    it.dst = it.add[0] = it.add[1] = it.sub[0] = it.sub[1] = it.rev = NOREF;
+    it.flags = 0;
     return it;
   };
   std::vector<IItem> items;
@@ -342,18 +343,8 @@ static int build_inner(pt_ctx* c) {
     for (int s = 0; s < 4; ++s)
       if (it.pan[s][0].vec >= 0) ++acc;
   };
-  // ---- OP (sie.py:203-228).  Phase 0: full traces T = d + p into AUX's down half (the panels
-  // d[i]+p[i] / p[i]+d[i] of the reference -- complex addition commutes, so one vector serves
-  // both); phase 1: every item reads single panels.
-  oph.push_back((int)items.size());
-  for (int I = 0; I < nI; ++I)
-    for (int s = 0; s < 2; ++s) {
-      IItem x = item(-1, 0);
-      x.dst = Ref{2, D(I, s)};
-      x.add[0] = Ref{0, D(I, s)};
-      x.add[1] = Ref{0, U(I, s)};
-      items.push_back(x);
-    }
+  // ---- OP (sie.py:203-228): one phase.  The full traces d + p of the reference are summed
+  // element-wise while the panels are gathered (pan[s][1]), and "- (d + p)" is sub0 + sub1.
   oph.push_back((int)items.size());
   for (int cc = 0; cc < Lc; ++cc) {
     const bool top = cc >= 1, bot = cc <= Lc - 2;
@@ -361,18 +352,17 @@ static int build_inner(pt_ctx* c) {
     if (bot) {
       for (int s = 0; s < 2; ++s) {
         IItem x = item(cc, 2 + s);
-        if (top) {
-          x.pan[0][0] = Ref{2, D(ib - 1, 0)};  // d + p above
-          x.pan[1][0] = Ref{2, D(ib - 1, 1)};
+        if (top) {  // v0, v1 = d + p above
+          for (int k = 0; k < 2; ++k) {
+            x.pan[k][0] = Ref{0, D(ib - 1, k)};
+            x.pan[k][1] = Ref{0, U(ib - 1, k)};
+          }
         }
         x.pan[2][0] = Ref{0, U(ib, 0)};
         x.pan[3][0] = Ref{0, U(ib, 1)};
         x.dst = Ref{1, D(ib, s)};
-        if (s == 0) {
-          x.sub[0] = Ref{2, D(ib, 0)};  // wb[0] - (d + p)
-        } else {
-          x.sub[0] = Ref{0, D(ib, 1)};  // wb[1] - d
-        }
+        x.sub[0] = Ref{0, D(ib, s)};        // wb[0] - (d + p) ; wb[1] - d
+        if (s == 0) x.sub[1] = Ref{0, U(ib, 0)};
         count(x, opb);
         items.push_back(x);
       }
@@ -382,32 +372,34 @@ static int build_inner(pt_ctx* c) {
         IItem x = item(cc, s);
         x.pan[0][0] = Ref{0, D(it, 0)};
         x.pan[1][0] = Ref{0, D(it, 1)};
-        if (bot) {
-          x.pan[2][0] = Ref{2, D(ib, 0)};  // p + d below
-          x.pan[3][0] = Ref{2, D(ib, 1)};
+        if (bot) {  // vn, vnp = p + d below
+          for (int k = 0; k < 2; ++k) {
+            x.pan[2 + k][0] = Ref{0, U(ib, k)};
+            x.pan[2 + k][1] = Ref{0, D(ib, k)};
+          }
         }
         x.dst = Ref{1, U(it, s)};
-        if (s == 0) {
-          x.sub[0] = Ref{0, U(it, 0)};  // wt[0] - p
-        } else {
-          x.sub[0] = Ref{2, D(it, 1)};  // wt[1] - (d + p)
-        }
+        x.sub[0] = Ref{0, U(it, s)};        // wt[0] - p ; wt[1] - (d + p)
+        if (s == 1) x.sub[1] = Ref{0, D(it, 1)};
         count(x, opb);
         items.push_back(x);
       }
     }
   }
   oph.push_back((int)items.size());
-  // ---- PRE (GS, sie.py:322-326)
-  pph.push_back((int)items.size());
-  for (int s = 0; s < 2; ++s) {  // y_down[0] = -v_down[0]
+  // ---- PRE (GS, sie.py:322-326) in 2 nI - 1 phases: the down sweep (phase k computes y_down[k];
+  // phase 1 also y_down[0] = -v_down[0]), each reflection as soon as its y_down panels exist, and
+  // the up sweep.  The combinations s = p - refl and y_up[nI-1] = -s[nI-1] are folded into the
+  // reflection items (modes 1 and 2; exact: -(p - t) == t - p in IEEE arithmetic).  Items of
+  // phase 1 read y_down[0] as the negated v_down[0] (also exact).
+  std::vector<std::vector<IItem>> P(2 * nI + 1);  // P[1 .. 2nI-1]
+  for (int s = 0; s < 2 && nI > 0; ++s) {          // y_down[0] = -v_down[0]
     IItem x = item(-1, 0);
     x.dst = Ref{1, D(0, s)};
     x.sub[0] = Ref{0, D(0, s)};
-    items.push_back(x);
+    P[1].push_back(x);
   }
-  pph.push_back((int)items.size());
-  for (int I = 1; I < nI; ++I) {
+  for (int I = 1; I < nI; ++I)
     for (int s = 0; s < 2; ++s) {
       IItem x = item(I, 2 + s);
       x.pan[0][0] = Ref{1, D(I - 1, 0)};
@@ -415,11 +407,9 @@ static int build_inner(pt_ctx* c) {
       x.dst = Ref{1, D(I, s)};
       x.sub[0] = Ref{0, D(I, s)};
       count(x, preb);
-      items.push_back(x);
+      P[I].push_back(x);
     }
-    pph.push_back((int)items.size());
-  }
-  for (int I = 0; I < nI; ++I) {  // reflections into AUX.up
+  for (int I = 0; I < nI; ++I)
     for (int s = 0; s < 2; ++s) {
       IItem x = item(I + 1, s);
       x.pan[0][0] = Ref{1, D(I, 0)};
@@ -428,30 +418,31 @@ static int build_inner(pt_ctx* c) {
         x.pan[2][0] = Ref{1, D(I + 1, 0)};
         x.pan[3][0] = Ref{1, D(I + 1, 1)};
       }
-      x.dst = Ref{2, U(I, s)};
       if (s == 1) x.sub[0] = Ref{1, D(I, 1)};
+      x.rev = Ref{0, U(I, s)};
+      if (I == nI - 1) {
+        x.dst = Ref{1, U(I, s)};  // y_up[nI-1] = -(p - refl) = refl - p
+        x.flags |= 2 << 8;
+      } else {
+        x.dst = Ref{2, U(I, s)};  // s = p - refl
+        x.flags |= 1 << 8;
+      }
       count(x, preb);
-      items.push_back(x);
+      const int ph = I <= nI - 2 ? I + 2 : nI;
+      if (ph == 1) {  // nI == 1: y_down[0] is produced in this same phase; read -v_down[0]
+        for (int k = 0; k < 2; ++k)
+          if (x.pan[k][0].vec == 1 && x.pan[k][0].seg == D(0, k)) {
+            x.pan[k][0].vec = 0;
+            x.flags |= 1 << k;
+          }
+        if (x.sub[0].vec == 1 && x.sub[0].seg == D(0, 1)) {  // - (-v) == + v
+          x.add[0] = Ref{0, D(0, 1)};
+          x.sub[0] = NOREF;
+        }
+      }
+      P[ph].push_back(x);
     }
-  }
-  pph.push_back((int)items.size());
-  for (int I = 0; I < nI; ++I)  // s = p - refl (in place in AUX.up)
-    for (int s = 0; s < 2; ++s) {
-      IItem x = item(-1, 0);
-      x.dst = Ref{2, U(I, s)};
-      x.add[0] = Ref{0, U(I, s)};
-      x.sub[0] = Ref{2, U(I, s)};
-      items.push_back(x);
-    }
-  pph.push_back((int)items.size());
-  for (int s = 0; s < 2; ++s) {  // y_up[nI-1] = -s[nI-1]
-    IItem x = item(-1, 0);
-    x.dst = Ref{1, U(nI - 1, s)};
-    x.sub[0] = Ref{2, U(nI - 1, s)};
-    items.push_back(x);
-  }
-  pph.push_back((int)items.size());
-  for (int I = nI - 2; I >= 0; --I) {
+  for (int I = nI - 2; I >= 0; --I)
     for (int s = 0; s < 2; ++s) {
       IItem x = item(I + 1, s);
       x.pan[2][0] = Ref{1, U(I + 1, 0)};
@@ -459,8 +450,19 @@ static int build_inner(pt_ctx* c) {
       x.dst = Ref{1, U(I, s)};
       x.sub[0] = Ref{2, U(I, s)};
       count(x, preb);
-      items.push_back(x);
+      P[nI + (nI - 1 - I)].push_back(x);
     }
+  // phase 1: the down-sweep items read y_down[0] = -v_down[0] directly
+  for (IItem& x : P[nI > 0 ? 1 : 0])
+    if (x.cell >= 0)
+      for (int k = 0; k < 2; ++k)
+        if (x.pan[k][0].vec == 1 && x.pan[k][0].seg == D(0, k)) {
+          x.pan[k][0].vec = 0;
+          x.flags |= 1 << k;
+        }
+  pph.push_back((int)items.size());
+  for (int ph = 1; ph <= 2 * nI - 1; ++ph) {
+    for (const IItem& x : P[ph]) items.push_back(x);
     pph.push_back((int)items.size());
   }
   c->op_nph = (int)oph.size() - 1;
@@ -1486,8 +1488,27 @@ int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, dou
   }
   kp.bd = bd;
   kp.xd = xd;
+  const bool timed = kp.tprof != nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->st);
+  }
   CK(k1_launch(kp, (int)tasks.size(), nc, c->wmax, c->st));
   CK(cudaStreamSynchronize(c->st));
+  if (timed) {  // PT_K1_TPROF: launch time and the per-phase clock64 totals of CTA 0
+    cudaEventRecord(e1, c->st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long tt[6];
+    cudaMemcpy(tt, kp.tprof, sizeof(tt), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "cell_solve nc=%d tasks=%d dbg=%d: %.1f us | prologue %lld preload %lld bar1 %lld matvec %lld "
+            "bar2 %lld epi %lld\n", nc, (int)tasks.size(), kp.dbg, ms * 1e3f, tt[0], tt[1], tt[2], tt[3], tt[4], tt[5]);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
   CK(cudaMemcpy(x, xd, bytes, cudaMemcpyDeviceToHost));
   cudaFree(bd);
   cudaFree(xd);
