@@ -70,26 +70,27 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   const int m = wzc >> 1, mb = wzc - 1 - m;
   const int nst = h == 0 ? 2 * m + 1 : 2 * mb + 1;
   const int tid = threadIdx.x;
-  constexpr int NS = K1_NS;  // power of two: slot = c & (NS-1), use = c >> log2(NS)
+  const int NS = p.ns;  // ring slots (<= K1_NS; a multiple of CM)
   // elements (row, column) per consumer thread: w*NC <= (NC == 8 ? 8*NMT : 32*NMT) * NC
   constexpr int TT = ((NC == 8 ? 8 * NMT : 32 * NMT) * NC + K1_CONSUMERS - 1) / K1_CONSUMERS;
   const int nIc = p.Lc - 1;
 
   unsigned char* ring = smem;
-  double2* VA = reinterpret_cast<double2*>(ring + (size_t)NS * p.slot_bytes);
+  double2* VA = reinterpret_cast<double2*>(ring + (size_t)NS * p.slot_bytes);  // slot_bytes % 128 == 0
   const int w4v = (w + 3) & ~3;
   double2* VB = VA + w4v * NC;
   double2* XC = VB + w4v * NC;  // partner's half-chain vector at the middle block
   double2* red = XC + w4v * NC;
   ColInfo* cols = reinterpret_cast<ColInfo*>(red + k1_red_rows(w) * NC);
   uint64_t* full = reinterpret_cast<uint64_t*>(cols + NC);
-  uint64_t* lempty = full + NS;
-  uint64_t* cempty = lempty + NS;
-  uint64_t* xbar = cempty + NS;
+  uint64_t* lempty = full + K1_NS;
+  uint64_t* cempty = lempty + K1_NS;
+  uint64_t* xbar = cempty + K1_NS;
 
   const int w4 = (w + 3) & ~3;  // stored columns per block (zero padded)
-  const int jc = NC == 8 ? K1_JC8 : K1_JCD;  // columns per ring chunk
-  const int nch = (w4 + jc - 1) / jc;
+  const int jc = NC == 8 ? K1_JC8 : 7 * k1_jw(NC);  // columns per ring chunk
+  const int wcols = NC == 8 ? w4 : w;                // streamed columns (DMMA: zero padded to w4)
+  const int nch = (wcols + jc - 1) / jc;
   const int total = nst * nch;
   const double2* S = p.sinv + cell.sinv_off;
   // factor block used by step s of this half
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     cols[tid] = ci;
   }
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < K1_NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&lempty[s], K1_CONSUMERS / 32);
       mbar_init(&cempty[s], CM);
@@ -143,11 +144,13 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     // ------------------------------------------------------------ producer warp
     if (tid == K1_CONSUMERS) {
       const uint16_t mask = (uint16_t)(((1u << CM) - 1u) << (h * CM));
+      int slot = 0;
+      uint32_t ph = 0;  // parity of the current use of `slot`
       for (int c = 0; c < total && !(p.dbg & 1); ++c) {
-        const int slot = c & (NS - 1), u = c >> K1_NS_LOG2;
-        if (u > 0) mbar_wait(&lempty[slot], (uint32_t)((u - 1) & 1));  // try_wait sleeps in hardware
+        const bool reuse = c >= NS;
+        if (reuse) mbar_wait(&lempty[slot], ph ^ 1u);  // try_wait sleeps in hardware
         const int s = c / nch, ch = c - s * nch;
-        const int c0 = ch * jc, cw = min(jc, w4 - c0);
+        const int c0 = ch * jc, cw = min(jc, wcols - c0);
         const uint32_t bytes = (uint32_t)cw * w * 16u;
         mbar_expect_tx(&full[slot], bytes);
         const int issuer = slot % CM;
@@ -156,11 +159,15 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         if (CM == 1) {
           bulk_g2s(dst, src, bytes, &full[slot]);
         } else {
-          if (u > 0) mbar_arrive_remote(mapa(&cempty[slot], (uint32_t)(h * CM + issuer)));
+          if (reuse) mbar_arrive_remote(mapa(&cempty[slot], (uint32_t)(h * CM + issuer)));
           if (issuer == cm) {
-            if (u > 0) mbar_wait(&cempty[slot], (uint32_t)((u - 1) & 1));
+            if (reuse) mbar_wait(&cempty[slot], ph ^ 1u);
             bulk_g2s_mc(dst, src, bytes, &full[slot], mask);
           }
+        }
+        if (++slot == NS) {
+          slot = 0;
+          ph ^= 1u;
         }
       }
     }
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     //   vb  volume source f (split or full slab) / dense test rhs
     //   tt, tbm  cell trace sources of the interfaces above / below (reconstruction pass)
     //   ob  output: Newton table rows, sampled layer row, stitched volume or dense test output
-    Desc* dsm = reinterpret_cast<Desc*>(full + 3 * NS + 2);  // [nel] descriptors in shared memory
+    Desc* dsm = reinterpret_cast<Desc*>(full + 3 * K1_NS + 2);  // [nel] descriptors in shared memory
 #pragma unroll
     for (int t = 0; t < TT; ++t) {
       Desc d;
@@ -308,7 +315,14 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
 
     double2* cur = VA;
     double2* nxt = VB;
-    int c = 0;
+    int rslot = 0;      // ring slot of the next chunk
+    uint32_t rph = 0;   // its fill parity
+    auto ring_next = [&]() {
+      if (++rslot == NS) {
+        rslot = 0;
+        rph ^= 1u;
+      }
+    };
     double2 pa[TT], pb[TT];
     double2 pcf;  // chain coefficient of the prefetched step (l_k / u_k), fetched with its operands
     K1_FETCH(0);
@@ -362,12 +376,12 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         double cm_[NMT][4];
 #pragma unroll
         for (int t = 0; t < NMT; ++t) cm_[t][0] = cm_[t][1] = cm_[t][2] = cm_[t][3] = 0.0;
-        for (int ch = 0; ch < nch; ++ch, ++c) {
-          const int slot = c & (NS - 1);
+        for (int ch = 0; ch < nch; ++ch) {
+          const int slot = rslot;
           const int ks0 = ch * (K1_JC8 / 4), ks1 = min(w4, (ch + 1) * K1_JC8) >> 2;
           int ks = ks0 + ((wp - ks0) % 7 + 7) % 7;  // first k-step of this warp in the chunk
           if (ks < ks1) {
-            if (!(p.dbg & 1)) mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
+            if (!(p.dbg & 1)) mbar_wait(&full[slot], rph);
             const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
             for (; ks < ks1; ks += K1_CONSUMERS / 32) {
               const int kl = (ks - ks0) * 4 + ak;  // column inside the chunk
@@ -385,6 +399,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           }
           __syncwarp();
           if (lane == 0) mbar_arrive_relaxed(&lempty[slot]);
+          ring_next();
         }
         K1_TICK(3);
 #pragma unroll
@@ -402,36 +417,45 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       // x NC right-hand sides of straight-line loads and FMAs.  Rows >= w of the last row block read
       // neighbouring shared memory and are discarded at the partial-sum write.
       constexpr int RW = NMT;
+      constexpr int JW = k1_jw(NC);
+      constexpr int JCD = 7 * JW;
       double2 acc[RW][NC];
 #pragma unroll
       for (int r = 0; r < RW; ++r)
 #pragma unroll
         for (int q = 0; q < NC; ++q) acc[r][q] = czero();
-      for (int ch = 0; ch < nch; ++ch, ++c) {
-        const int slot = c & (NS - 1);
-        if (!(p.dbg & 1)) mbar_wait(&full[slot], (uint32_t)((c >> K1_NS_LOG2) & 1));
-        const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)slot * p.slot_bytes);
-        const int c0 = ch * K1_JCD, cw = min(K1_JCD, w - c0);
+      for (int ch = 0; ch < nch; ++ch) {
+        if (!(p.dbg & 1)) mbar_wait(&full[rslot], rph);
+        const double2* blk = reinterpret_cast<const double2*>(ring + (size_t)rslot * p.slot_bytes);
+        const int c0 = ch * JCD, cw = min(JCD, w - c0);
         if (!(p.dbg & 2)) {
+          // all loads of the warp's JW columns first (branch-free: a column past the chunk reads
+          // column 0 and multiplies a zero vector entry), then the FMAs
+          double2 av[JW][RW], tv[JW][NC];
 #pragma unroll
-          for (int u = 0; u < K1_JW; ++u) {
-            const int jj = wp * K1_JW + u;
-            if (jj < cw) {
-              double2 tv[NC];
+          for (int u = 0; u < JW; ++u) {
+            const int jj = wp * JW + u;
+            const bool ok = jj < cw;
+            const int jl = ok ? jj : 0;
 #pragma unroll
-              for (int q = 0; q < NC; ++q) tv[q] = cur[(c0 + jj) * NC + q];
-              const double2* col = blk + jj * w + lane;
-#pragma unroll
-              for (int r = 0; r < RW; ++r) {
-                const double2 a = col[32 * r];
-#pragma unroll
-                for (int q = 0; q < NC; ++q) cfma(acc[r][q], a, tv[q]);
-              }
+            for (int q = 0; q < NC; ++q) {
+              const double2 t = cur[(c0 + jl) * NC + q];
+              tv[u][q] = ok ? t : czero();
             }
+            const double2* col = blk + jl * w + lane;
+#pragma unroll
+            for (int r = 0; r < RW; ++r) av[u][r] = (lane + 32 * r < w) ? col[32 * r] : czero();
           }
+#pragma unroll
+          for (int u = 0; u < JW; ++u)
+#pragma unroll
+            for (int r = 0; r < RW; ++r)
+#pragma unroll
+              for (int q = 0; q < NC; ++q) cfma(acc[r][q], av[u][r], tv[u][q]);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive_relaxed(&lempty[slot]);
+        if (lane == 0) mbar_arrive_relaxed(&lempty[rslot]);
+        ring_next();
       }
       K1_TICK(3);
 #pragma unroll
@@ -489,12 +513,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
 }
 
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns) {
-  (void)ns;
-  ns = K1_NS;
   // ring + three [w][NC] vectors + the [8 warps][w][NC] partial sums + column info + barriers
   return (size_t)ns * slot_bytes + (size_t)(3 * ((wmax + 3) & ~3) + k1_red_rows(wmax)) * nc * 16 +
          (size_t)nc * sizeof(ColInfo) +
-         (size_t)(3 * ns + 2) * 8 + (size_t)wmax * nc * sizeof(Desc) + 128;
+         (size_t)(3 * K1_NS + 2) * 8 + (size_t)wmax * nc * sizeof(Desc) + 128;
 }
 
 cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStream_t st) {
@@ -507,15 +529,18 @@ cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStre
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
-  // ring slots as large as the shared memory left next to this NC's vectors allows (<= 48 KB)
+  // one ring slot holds one chunk (DMMA path K1_JC8 columns, DFMA path 7 * k1_jw(nc)); as many slots
+  // as the shared memory left next to this NC's vectors allows (<= K1_NS, a multiple of cm)
   K1Params p = p0;
-  const long long fixed = (long long)k1_smem_bytes(wmax, nc, 0, K1_NS);
-  long long slot = std::min(((long long)maxsm - fixed) / K1_NS, 49152LL) / 16 * 16;
-  // every chunk must fit its slot: DMMA path K1_JC8 columns, DFMA path at least 4
-  if (slot < 16LL * wmax * (nc == 8 ? K1_JC8 : K1_JCD)) return cudaErrorInvalidValue;
+  const int jc = nc == 8 ? K1_JC8 : 7 * k1_jw(nc);
+  const long long slot = (16LL * wmax * jc + 127) / 128 * 128;
+  const long long fixed = (long long)k1_smem_bytes(wmax, nc, 0, 0);
+  int ns = (int)std::min<long long>(K1_NS, ((long long)maxsm - fixed) / slot);
+  ns -= ns % p.cm;
+  if (ns < 2) return cudaErrorInvalidValue;
   p.slot_bytes = (int)slot;
-  p.ns = K1_NS;
-  const size_t smax = k1_smem_bytes(wmax, nc, p.slot_bytes, K1_NS);
+  p.ns = ns;
+  const size_t smax = k1_smem_bytes(wmax, nc, p.slot_bytes, ns);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ntasks * 2 * p.cm, 1, 1);
   cfg.blockDim = dim3(K1_THREADS, 1, 1);

@@ -81,8 +81,8 @@ cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStrea
 #define K1_NS_LOG2 3
 #define K1_RW 4       // rows per lane in the K1 matvec: cell width w <= 128
 #define K1_DMMA_ITEMS 3  // 8-row tiles per warp in the DMMA path: ceil(128/8) <= 3*7
-#define K1_JW 2       // DFMA path: columns per consumer warp per ring chunk
-#define K1_JCD (7 * K1_JW)  // DFMA path: columns per ring chunk
+// DFMA path: columns per consumer warp per ring chunk (7 warps per chunk)
+__host__ __device__ constexpr int k1_jw(int nc) { return nc == 1 ? 5 : (nc == 2 ? 4 : 2); }
 #define K1_JC8 12        // ring chunk width (columns) of the DMMA path: 3 k-steps
 size_t inner_smem_bytes(int wmax, int nitems);
 int inner_mg(int wmax);

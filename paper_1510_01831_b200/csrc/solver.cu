@@ -38,6 +38,7 @@ namespace {
 const Ref NOREF{-1, 0};
 
 struct Stage {
+  const char* name = "";  // for the PT_STAGE_PROF breakdown
   std::vector<OJob> jobs;
   OJob* jobs_d = nullptr;
   int* stage_jobs_d = nullptr;
@@ -121,7 +122,9 @@ struct pt_ctx {
   struct EvRec {
     cudaEvent_t a, b;
     int cls;  // 0 K1, 1 inner, 2 other
+    const char* tag;
   };
+  const char* cur_tag = "";
   std::vector<cudaEvent_t> evpool;
   size_t ev_next = 0;
   std::vector<EvRec> evs;
@@ -155,7 +158,7 @@ struct LaunchScope {
     if (c->prof) {
       cudaEvent_t b = pool_event(c);
       cudaEventRecord(b, c->st);
-      c->evs.push_back({a, b, cls});
+      c->evs.push_back({a, b, cls, c->cur_tag});
     }
   }
 };
@@ -262,7 +265,12 @@ static int build_outer(pt_ctx* c) {
     }
   }
   // sweep_down steps (sie.py:272-283): IN = v, OUT = y
+  c->newton.name = "newton";
+  c->op.name = "op";
+  c->refl.name = "refl";
+  c->recon.name = "recon";
   c->sdown.resize(std::max(nI, 1));
+  for (auto& st : c->sdown) st.name = "sdown";
   for (int I = 1; I < nI; ++I) {
     OJob j = blank_job(I);
     const int n = c->lay[I].n;
@@ -287,6 +295,7 @@ static int build_outer(pt_ctx* c) {
   }
   // sweep_up steps (sie.py:285-296): IN holds s in its up half, OUT = y
   c->sup.resize(std::max(nI, 1));
+  for (auto& st : c->sup) st.name = "sup";
   for (int I = nI - 2; I >= 0; --I) {
     OJob j = blank_job(I + 1);
     j.pan[2][0] = Ref{1, segU(c, I + 1, 0)};
@@ -614,6 +623,7 @@ static int grid_for(long long n) {
 }
 
 static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& io) {
+  c->cur_tag = S.name;
   const int J = (int)S.jobs.size();
   if (J == 0 || Ract == 0) return 0;
   Stage::Tasks* T = stage_tasks(c, S, Ract);
@@ -833,6 +843,9 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   c->k1_bytes = 0.0;
   c->evs.clear();
   c->ev_next = 0;
+  static const bool stage_prof = std::getenv("PT_STAGE_PROF") != nullptr;
+  if (stage_prof) c->prof = true;
+  c->cur_tag = "outer";
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -1118,6 +1131,21 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
       stats->kernel_ms[0] = acc[0];
       stats->kernel_ms[1] = acc[1];
       stats->kernel_ms[2] = c->prof ? std::max(0.0, (double)ms - acc[0] - acc[1]) : 0.0;
+    }
+    if (stage_prof) {  // per (stage, kernel class) device time, launch count
+      std::map<std::string, std::pair<double, int>> agg;
+      static const char* cls_name[3] = {"k1", "inner", "glue"};
+      for (const auto& e : c->evs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e.a, e.b);
+        auto& v = agg[std::string(e.tag) + "/" + cls_name[e.cls]];
+        v.first += t;
+        v.second += 1;
+      }
+      fprintf(stderr, "stage profile (total %.3f ms):\n", ms);
+      for (const auto& kv : agg)
+        fprintf(stderr, "  %-16s %8.3f ms  %5d launches  %8.1f us/launch\n", kv.first.c_str(), kv.second.first,
+                kv.second.second, 1e3 * kv.second.first / kv.second.second);
     }
     if (stats->k1_bytes) stats->k1_bytes[0] = c->k1_bytes;
     if (stats->launches) stats->launches[0] = c->launches;
