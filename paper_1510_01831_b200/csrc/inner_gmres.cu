@@ -22,6 +22,7 @@
 // deterministic and need no cross-CTA traffic.
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 
 #include "pt_launch.cuh"
 
@@ -236,10 +237,10 @@ __device__ __forceinline__ void rebuild_active(const InnerParams& p, int job, in
   __syncthreads();
 }
 
-__global__ void __cluster_dims__(INNER_CS, 1, 1) __launch_bounds__(IN_THREADS, 1)
+__global__ void __launch_bounds__(IN_THREADS, 1)
     inner_gmres_kernel(const InnerParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const int CS = INNER_CS;
+  const int CS = (int)cg::this_cluster().num_blocks();  // 8 or 16 (launch attribute)
   const int q = (int)cg::this_cluster().block_rank();
   const int ngroups = (p.R + 7) >> 3;
   const int cid = blockIdx.x / CS;
@@ -493,9 +494,40 @@ cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   if (njobs == 0 || p.Lc < 2) return cudaSuccess;
   const size_t sm = inner_smem_bytes(p.wmax, p.nitems);
   cudaFuncSetAttribute(inner_gmres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(inner_gmres_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const int ngroups = (p.R + 7) / 8;
-  inner_gmres_kernel<<<njobs * ngroups * INNER_CS, IN_THREADS, sm, st>>>(p);
-  return cudaGetLastError();
+  const int nclusters = njobs * ngroups;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(IN_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // Clusters of 16 CTAs (twice the FP64 tensor throughput per RHS group) when they all fit at once;
+  // otherwise the portable 8.  PT_INNER_CS overrides.
+  int cs = INNER_CS;
+  if (const char* e = std::getenv("PT_INNER_CS")) {
+    cs = atoi(e) >= 16 ? 16 : INNER_CS;
+  } else if (nclusters * 16 <= nsm) {
+    cfg.gridDim = dim3(nclusters * 16, 1, 1);
+    attr[0].val.clusterDim.x = 16;
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, inner_gmres_kernel, &cfg) == cudaSuccess && active >= nclusters) cs = 16;
+    cudaGetLastError();
+  }
+  cfg.gridDim = dim3(nclusters * cs, 1, 1);
+  attr[0].val.clusterDim.x = cs;
+  return cudaLaunchKernelEx(&cfg, inner_gmres_kernel, p);
 }
 
 void inner_tprof_dump() {
