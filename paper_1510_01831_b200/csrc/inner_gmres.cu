@@ -58,6 +58,7 @@ struct Ticker {
 struct InSmem {
   double2* tiles;   // [2 buffers][4 slots][IN_MG][w][8]
   double2* pan;     // [4 slots][w][8]
+  double2* pan2;    // [2][w][8] second terms of two-term panels
   double2* red;     // [8 warps][IN_MG*8][8]
   uint64_t* tbar;   // [2] one mbarrier per tile buffer
   int* act;         // active local instances
@@ -105,37 +106,24 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
       };
       int negm = 0;  // bit si: slot panel si enters negated (exact)
       for (int si = 0; si < ns; ++si) negm |= (item.flags >> slot_of(si) & 1) << si;
+      int twom = 0;  // bit si: two-term slot panel (d + p); its second term is staged in pan2
+      for (int si = 0; si < ns; ++si) twom |= (item.pan[slot_of(si)][1].vec >= 0) << si;
       if (ns > 0) {
         if (tid == 0) issue_tiles(g0, 0);
-        // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill);
-        // a two-term panel (d + p) is summed on the way in
-        for (int e0 = tid; e0 < ns * w * 8; e0 += 4 * IN_THREADS) {
-          double2 va[4], vb[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {  // all loads of the batch in flight before any store
-            const int e = e0 + u * IN_THREADS;
-            va[u] = vb[u] = czero();
-            if (e < ns * w * 8) {
-              const int si = e / (w * 8), rem = e - si * w * 8;
-              const int k = rem >> 3, qq = rem & 7;
-              const bool okq = qq < nact;
-              const Ref pr = item.pan[slot_of(si)][0], pr2 = item.pan[slot_of(si)][1];
-              const int rr = okq ? r0 + S.act[qq] : r0;
-              if (pr2.vec < 0) {
-                cp_async16(S.pan + e, vecp(p, job, rr, VM(pr.vec)) + pr.seg * w + k, okq);
-              } else if (okq) {
-                va[u] = ld_cg(vecp(p, job, rr, VM(pr.vec)) + pr.seg * w + k);
-                vb[u] = ld_cg(vecp(p, job, rr, VM(pr2.vec)) + pr2.seg * w + k);
-              }
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * IN_THREADS;
-            if (e < ns * w * 8) {
-              const int si = e / (w * 8);
-              if (item.pan[slot_of(si)][1].vec >= 0) S.pan[e] = cadd(va[u], vb[u]);
-            }
+        // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill).
+        // IN_THREADS % 8 == 0, so a thread's instance qq is fixed and its scratch base is computed once.
+        const int qq = tid & 7;
+        const bool okq = qq < nact;
+        const double2* ibase = p.scratch + (size_t)(job * p.R + (okq ? r0 + S.act[qq] : r0)) * p.inst_stride;
+        for (int si = 0, n2 = 0; si < ns; ++si) {
+          const Ref pr = item.pan[slot_of(si)][0], pr2 = item.pan[slot_of(si)][1];
+          const double2* src = ibase + (size_t)VM(pr.vec) * p.nmax + pr.seg * w;
+          double2* dst = S.pan + (size_t)si * w * 8 + qq;
+          for (int k = tid >> 3; k < w; k += IN_THREADS / 8) cp_async16(dst + k * 8, src + k, okq);
+          if (pr2.vec >= 0) {
+            const double2* src2 = ibase + (size_t)VM(pr2.vec) * p.nmax + pr2.seg * w;
+            double2* dst2 = S.pan2 + (size_t)n2++ * w * 8 + qq;
+            for (int k = tid >> 3; k < w; k += IN_THREADS / 8) cp_async16(dst2 + k * 8, src2 + k, okq);
           }
         }
       }
@@ -181,6 +169,10 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
             const int si = ks / kps, k = (ks - si * kps) * 4 + ak;
             const bool kin = k < w;
             double2 bv = kin ? S.pan[((size_t)si * w + k) * 8 + ar] : czero();
+            if (twom >> si & 1) {  // d + p, summed in the reference's order
+              const int i2 = __popc(twom & ((1 << si) - 1));
+              bv = cadd(bv, kin ? S.pan2[((size_t)i2 * w + k) * 8 + ar] : czero());
+            }
             const double sg = (negm >> si & 1) ? -1.0 : 1.0;
             bv.x *= sg;
             bv.y *= sg;
@@ -256,7 +248,8 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   InSmem S;
   S.tiles = reinterpret_cast<double2*>(smem);
   S.pan = S.tiles + (size_t)2 * 4 * p.mg * p.wmax * 8;
-  S.red = S.pan + (size_t)4 * p.wmax * 8;
+  S.pan2 = S.pan + (size_t)4 * p.wmax * 8;
+  S.red = S.pan2 + (size_t)2 * p.wmax * 8;
   double* dred = reinterpret_cast<double*>(S.red + (IN_THREADS / 32) * IN_MG * 8 * 8);
   S.tbar = reinterpret_cast<uint64_t*>(dred + 64);
   S.act = reinterpret_cast<int*>(S.tbar + 2);
@@ -486,7 +479,7 @@ int inner_mg(int wmax) { return wmax <= 80 ? 2 : 1; }
 
 size_t inner_smem_bytes(int wmax, int nitems) {
   const int w = wmax < 8 ? 8 : wmax;
-  return (size_t)(2 * 4 * inner_mg(wmax) + 4) * w * 8 * 16 + (size_t)(IN_THREADS / 32) * IN_MG * 8 * 8 * 16 + 64 * 8 +
+  return (size_t)(2 * 4 * inner_mg(wmax) + 4 + 2) * w * 8 * 16 + (size_t)(IN_THREADS / 32) * IN_MG * 8 * 8 * 16 + 64 * 8 +
          16 + 64 + PT_MAX_LC * 8 + (size_t)nitems * sizeof(IItem) + 128;
 }
 
