@@ -550,14 +550,21 @@ static void k1_policy(pt_ctx* c, const std::vector<int>& ncols_per_group, int* n
   int nc = 0;
   if (const char* e = std::getenv("PT_K1_NC")) nc = atoi(e);
   if (nc != 1 && nc != 2 && nc != 4 && nc != 8) {
+    // Minimise (waves of CTA pairs) x (relative cost of one launch wave at this NC): one K1 CTA per
+    // SM, so a stage with more CTAs than SMs runs in several waves.  Relative per-wave costs were
+    // measured on the B200 for w = 70 (tools/k1_probe.py): NC=1 1.0, 2 1.45, 4 2.15, 8 2.5.
     nc = 1;
-    for (int cand : {8, 4, 2, 1}) {
+    double best = 1e30;
+    for (int cand : {1, 2, 4, 8}) {
       if (cand * c->wmax > 640 && cand > 1) continue;  // keep the partial sums next to the ring
       long long tasks = 0;
       for (int n : ncols_per_group) tasks += (long long)c->Lc * ((n + cand * cm - 1) / (cand * cm));
-      if (2LL * cm * tasks >= c->num_sms || cand == 1) {
+      const double cost = cand == 1 ? 1.0 : cand == 2 ? 1.45 : cand == 4 ? 2.15 : 2.5;
+      const long long waves = (2LL * cm * tasks + c->num_sms - 1) / c->num_sms;
+      const double t = (double)waves * cost;
+      if (t < best - 1e-9) {
+        best = t;
         nc = cand;
-        break;
       }
     }
   }
