@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpt_b200.so")
+# PT_LIB_VARIANT=x loads libpt_b200.x.so (an in-tree experimental build) instead
+LIB_PATH = os.path.join(HERE, "libpt_b200.%s.so" % os.environ["PT_LIB_VARIANT"]
+                        if os.environ.get("PT_LIB_VARIANT") else "libpt_b200.so")
 
 PT_OK = 0
 PT_NOT_CONVERGED = 1

@@ -36,7 +36,7 @@ def build(verbose=False, force=False):
             return LIB
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
            "-rdc=false", "-I", os.path.join(REPO, "include"), "-Xptxas", "-v" if verbose else "-O3",
-           "-o", LIB + ".tmp", *srcs, "-lcudart"]
+           *os.environ.get("PT_NVCC_FLAGS", "").split(), "-o", LIB + ".tmp", *srcs, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

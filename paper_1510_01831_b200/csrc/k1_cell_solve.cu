@@ -34,6 +34,10 @@
 
 #include "pt_launch.cuh"
 
+#ifndef K1_FETCH_POS
+#define K1_FETCH_POS 0  // where the next step's operands are fetched: 0 before the matvec
+#endif
+
 namespace cg = cooperative_groups;
 
 struct ColInfo {
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       uint32_t ph = 0;  // parity of the current use of `slot`
       for (int c = 0; c < total && !(p.dbg & 1); ++c) {
         const bool reuse = c >= NS;
-        if (reuse) mbar_wait(&lempty[slot], ph ^ 1u);  // try_wait sleeps in hardware
+        if (reuse) mbar_wait_suspend(&lempty[slot], ph ^ 1u);
         const int s = c / nch, ch = c - s * nch;
         const int c0 = ch * jc, cw = min(jc, wcols - c0);
         const uint32_t bytes = (uint32_t)cw * w * 16u;
@@ -187,6 +191,14 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
     //   tt, tbm  cell trace sources of the interfaces above / below (reconstruction pass)
     //   ob  output: Newton table rows, sampled layer row, stitched volume or dense test output
     Desc* dsm = reinterpret_cast<Desc*>(full + 3 * K1_NS + 2);  // [nel] descriptors in shared memory
+    // this thread's element descriptors: registers for NC < 8 (static indices), shared memory for the
+    // register-heavy DMMA path
+    constexpr bool DREG = NC < 8;
+    Desc dreg[DREG ? TT : 1] = {};
+    auto getd = [&](int t) -> Desc {
+      if constexpr (DREG) return dreg[t];
+      else return dsm[tid + t * K1_CONSUMERS];
+    };
 #pragma unroll
     for (int t = 0; t < TT; ++t) {
       Desc d;
@@ -194,6 +206,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       d.slot = 0;
       d.okind = 0;
       const int e = tid + t * K1_CONSUMERS;
+      if constexpr (DREG) dreg[t] = d;
       if (e >= nel) continue;
       const int j = e / NC, q = e - (e / NC) * NC;
       const ColInfo ci = cols[q];
@@ -238,6 +251,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         }
       }
       dsm[e] = d;
+      if constexpr (DREG) dreg[t] = d;
     }
     // Operands of a step that do not depend on the chain are fetched ONE STEP AHEAD as raw values
     // into registers (pa: panel value, or the stored z_k / y_k of a back-substitution step;
@@ -259,10 +273,11 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         if (back_) {                                                                                \
           pa[t] = Z[(size_t)kb_ * nel + e];                                                         \
         } else if (p.pass == 2) {                                                                   \
-          const int vb_ = dsm[e].vb;                                                                \
+          const int vb_ = getd(t).vb;                                                               \
           if (vb_ >= 0) pb[t] = p.bd[(size_t)vb_ + (size_t)kb_ * w];                                \
         } else if (kept_) {                                                                         \
-          const int pb_ = dsm[e].pb, vb_ = dsm[e].vb;                                               \
+          const Desc d_ = getd(t);                                                                  \
+          const int pb_ = d_.pb, vb_ = d_.vb;                                                       \
           if (pb_ >= 0) pa[t] = p.P[(size_t)pb_ + kb_];                                             \
           if (vb_ >= 0) pb[t] = p.f[(size_t)vb_ + kb_];                                             \
         }                                                                                           \
@@ -271,8 +286,8 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   } while (0)
     // b_k[j] from the prefetched raw operands: cell trace source + (panel + volume), the reference's
     // order of additions (sie.py:338-340)
-    auto bval = [&](int k, int e, double2 va, double2 vb) -> double2 {
-      const Desc d = dsm[e];
+    auto bval = [&](int k, int t, double2 va, double2 vb) -> double2 {
+      const Desc d = getd(t);
       if (p.pass == 2) return vb;
       double2 inner = (d.pb >= 0 && k >= cell.lo && k < cell.hi) ? cmul(sel4(lay.coef, d.slot), va) : czero();
       inner = cadd(inner, vb);
@@ -286,8 +301,8 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       }
       return inner;
     };
-    auto emit = [&](int k, int e, double2 x) {
-      const Desc d = dsm[e];
+    auto emit = [&](int k, int t, double2 x) {
+      const Desc d = getd(t);
       if (d.okind == 4) {
         p.xd[(size_t)d.ob + (size_t)k * w] = x;
       } else if (d.okind >= 2) {
@@ -330,7 +345,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
 #pragma unroll
     for (int t = 0; t < TT; ++t) {
       const int e = tid + t * K1_CONSUMERS;
-      if (e < nel) cur[e] = (p.dbg & 4) ? pa[t] : bval(kblk(0), e, pa[t], pb[t]);
+      if (e < nel) cur[e] = (p.dbg & 4) ? pa[t] : bval(kblk(0), t, pa[t], pb[t]);
     }
     K1_TICK(-1);
     // Invariant at the top of step s: cur holds the matvec input of step s (formed by the previous
@@ -351,7 +366,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           if (e < nel) {
             const double2 zt = h == 0 ? cur[e] : XC[e];  // z_{m-1} (top chain)
             const double2 yb = h == 0 ? XC[e] : cur[e];  // y_{m+1} (bottom chain)
-            cur[e] = csub(csub(bval(m, e, pa[t], pb[t]), cmul(lm, zt)), cmul(um, yb));
+            cur[e] = csub(csub(bval(m, t, pa[t], pb[t]), cmul(lm, zt)), cmul(um, yb));
           }
         }
       } else if (kind == 2) {
@@ -359,7 +374,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         for (int t = 0; t < TT; ++t) zr[t] = pa[t];
       }
       K1_TICK(0);
+#if K1_FETCH_POS == 0
       if (s + 1 < nst) K1_FETCH(s + 1);
+#endif
       K1_TICK(1);
       named_bar(1, K1_CONSUMERS);
       K1_TICK(2);
@@ -400,6 +417,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           __syncwarp();
           if (lane == 0) mbar_arrive_relaxed(&lempty[slot]);
           ring_next();
+#if K1_FETCH_POS == 1
+          // operands of the next step, issued under the matvec (used by this step's epilogue)
+          if (ch == 0 && s + 1 < nst) K1_FETCH(s + 1);
+#endif
         }
         K1_TICK(3);
 #pragma unroll
@@ -456,6 +477,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         __syncwarp();
         if (lane == 0) mbar_arrive_relaxed(&lempty[rslot]);
         ring_next();
+#if K1_FETCH_POS == 1
+        // operands of the next step, issued under the matvec (used by this step's epilogue)
+        if (ch == 0 && s + 1 < nst) K1_FETCH(s + 1);
+#endif
       }
       K1_TICK(3);
 #pragma unroll
@@ -466,6 +491,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           for (int q = 0; q < NC; ++q) red[(wp * w + i) * NC + q] = acc[r][q];
       }
       }
+#if K1_FETCH_POS == 2
+      if (s + 1 < nst) K1_FETCH(s + 1);
+#endif
       named_bar(1, K1_CONSUMERS);
       K1_TICK(4);
       // ---- epilogue: this step's output, and the matvec input of step s+1 (b_{k'} - coef * out for a
@@ -480,19 +508,24 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
           const int i = e / NC, q = e - (e / NC) * NC;
           double2 y = red[i * NC + q];
           // partial sums: one set per consumer warp (DMMA k split / DFMA column split)
-#pragma unroll
-          for (int g = 1; g < K1_CONSUMERS / 32; ++g) y = cadd(y, red[(g * w + i) * NC + q]);
+          static_assert(K1_CONSUMERS / 32 == 7, "partial-sum tree assumes 7 consumer warps");
+          {
+            const double2 p1 = red[(1 * w + i) * NC + q], p2 = red[(2 * w + i) * NC + q];
+            const double2 p3 = red[(3 * w + i) * NC + q], p4 = red[(4 * w + i) * NC + q];
+            const double2 p5 = red[(5 * w + i) * NC + q], p6 = red[(6 * w + i) * NC + q];
+            y = cadd(cadd(cadd(y, p1), cadd(p2, p3)), cadd(cadd(p4, p5), p6));
+          }
           double2 out = y;
           if (kind == 0) {
             Z[(size_t)kb * nel + e] = y;
           } else if (kind == 1) {
-            if (h == 0) emit(m, e, y);
+            if (h == 0) emit(m, t, y);
           } else {
             out = csub(zr[t], cmul(cf, y));
-            if (!(p.dbg & 8)) emit(kb, e, out);
+            if (!(p.dbg & 8)) emit(kb, t, out);
           }
           if (kn == 0) {
-            const double2 b = (p.dbg & 4) ? pa[t] : bval(kbn, e, pa[t], pb[t]);
+            const double2 b = (p.dbg & 4) ? pa[t] : bval(kbn, t, pa[t], pb[t]);
             out = csub(b, cmul(cfn, out));
           }
           nxt[e] = out;

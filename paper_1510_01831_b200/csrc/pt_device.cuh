@@ -130,6 +130,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// wait with a suspend-time hint: the thread sleeps in the barrier unit until the phase completes
+// (or the hint expires), so a waiting producer lane does not steal issue slots from its SMSP
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 // wait with exponential nanosleep backoff: for a lone producer thread whose spinning would
 // otherwise steal issue slots from the consumer warps of its SM sub-partition
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
