@@ -67,6 +67,10 @@ typedef struct {
   const double* const* uz;   /* [L*Lc] -> [wz_c] complex block super-diagonal scalars */
   const double* const* sinv; /* [L*Lc] -> [wz_c][w][w] complex Schur inverses, column-major blocks */
   const double* const* green;/* [L*Lc] -> [4 rows][4 slots][w][w] complex, column-major blocks */
+  /* optional (NULL: sampled outputs come from a second cell-solve pass):
+   * [L*Lc] -> [wz_c][4 layer trace rows 0,1,n,n+1][4 slots][w] complex, the trace-source
+   * response H_c^{-1}(coef_s E_krow_s) sampled at every block row and the layer trace rows */
+  const double* const* gsmp;
 } pt_problem;
 
 typedef struct {

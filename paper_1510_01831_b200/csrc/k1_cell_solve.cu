@@ -58,6 +58,7 @@ struct Desc {
   unsigned char slot;    // panel slot of pb
   unsigned char okind;   // 0 none, 1 Newton tables, 2 volume u, 3 sampled smp, 4 dense test xd
   unsigned char pad[2];
+  int ob2;               // pass 0 with s0: into smp (layer-row sample of the pass-0 solution), -1 none
 };
 
 template <int NC, int NMT>
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
 #pragma unroll
     for (int t = 0; t < TT; ++t) {
       Desc d;
-      d.pb = d.vb = d.tt = d.tbm = d.ob = -1;
+      d.pb = d.vb = d.tt = d.tbm = d.ob = d.ob2 = -1;
       d.slot = 0;
       d.okind = 0;
       const int e = tid + t * K1_CONSUMERS;
@@ -248,6 +249,11 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         } else {
           d.ob = ((ci.jid * p.Lc + cell.cell) * 4 * p.R + ci.r) * p.wmax + j;
           d.okind = 1;
+          if (p.s0 && ci.nout > 0) {
+#pragma unroll
+            for (int o = 0; o < 4; ++o)
+              if (j == ci.opos[o]) d.ob2 = ((ci.jid * 4 + o) * p.R + ci.r) * p.wx + cell.off;
+          }
         }
       }
       dsm[e] = d;
@@ -308,6 +314,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
       } else if (d.okind >= 2) {
         if (k >= cell.lo && k < cell.hi) (d.okind == 2 ? p.u : p.smp)[(size_t)d.ob + k] = x;
       } else if (d.okind == 1) {
+        if (d.ob2 >= 0 && k >= cell.lo && k < cell.hi) p.smp[(size_t)d.ob2 + k] = x;
 #pragma unroll
         for (int idx = 0; idx < 4; ++idx) {
           const bool need = idx < 2 ? cell.has_top : cell.has_bot;

@@ -7,6 +7,8 @@
 // cost nothing and never feed garbage into an inner solve.
 #include "pt_device.cuh"
 
+#include <algorithm>
+
 #include "pt_launch.cuh"
 
 
@@ -211,4 +213,75 @@ __global__ void k_green_tiles(const double2* src, double2* dst, int w) {
     const int i = mt * 8 + r;
     dst[e] = i < w ? src[((size_t)b * w + k) * w + i] : make_double2(0.0, 0.0);
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Sampled trace-source response (replaces the second cell-solve pass of a layer solve whose only
+// outputs are layer-row samples).  By linearity the reconstruction-pass solution is
+//   u1 = H_c^{-1}(f + panels) + sum_s H_c^{-1}(coef_s E_krow_s) tr_s = u0 + sum_s G_s tr_s,
+// so its samples at the layer trace rows are the pass-0 samples (written by K1 pass 0) plus
+// gsmp[k][row][s][:] . tr_s for every kept block row k.
+// grid: x = job * Lc + cell, y = group of 8 RHS, z = chunk of kept block rows.
+__global__ void k_green_samples(const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
+                                const LayerInfo* __restrict__ layers, const double2* __restrict__ gsmp,
+                                const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,
+                                int wmax) {
+  extern __shared__ double2 trs[];  // [4 slots][w][8 rhs]
+  const int jid = blockIdx.x / Lc, c = blockIdx.x - (blockIdx.x / Lc) * Lc;
+  const OJob& jb = jobs[jid];
+  const int nout = jb.nout;
+  if (nout <= 0) return;
+  const LayerInfo& lay = layers[jb.layer];
+  const CellInfo& ci = cells[jb.layer * Lc + c];
+  const int w = ci.w, nIc = Lc - 1;
+  const int r0 = blockIdx.y * 8, nr = min(8, R - r0);
+  for (int e = threadIdx.x; e < 4 * w * 8; e += blockDim.x) {
+    const int rr = e & 7, sj = e >> 3, s = sj / w, j = sj - (sj / w) * w;
+    const int I = s < 2 ? c - 1 : c;
+    double2 v = make_double2(0.0, 0.0);
+    if (rr < nr && I >= 0 && I < nIc) v = tr[(((size_t)(jid * R + r0 + rr) * nIc + I) * 2 + (s & 1)) * wmax + j];
+    trs[e] = v;
+  }
+  __syncthreads();
+  const int s_lo = ci.has_top ? 0 : 2, s_hi = ci.has_bot ? 4 : 2;
+  const int nk = ci.hi - ci.lo;
+  const int k0 = ci.lo + (int)((long long)blockIdx.z * nk / gridDim.z);
+  const int k1 = ci.lo + (int)((long long)(blockIdx.z + 1) * nk / gridDim.z);
+  const int nitems = (k1 - k0) * nout * 8;
+  for (int it = threadIdx.x; it < nitems; it += blockDim.x) {
+    const int rr = it & 7, rest = it >> 3;
+    if (rr >= nr) continue;
+    const int o = rest % nout, k = k0 + rest / nout;
+    const int orow = jb.orow[o];
+    const int oi = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
+    const double2* g = gsmp + ci.gsmp_off + ((size_t)k * 4 + oi) * 4 * w;  // [4 slots][w]
+    double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+    for (int s = s_lo; s < s_hi; ++s) {
+      const double2* gs = g + s * w;
+      const double2* ts = trs + (size_t)s * w * 8 + rr;
+      int j = 0;
+      for (; j + 4 <= w; j += 4) {
+        cfma(a0, __ldg(gs + j), ts[(j + 0) * 8]);
+        cfma(a1, __ldg(gs + j + 1), ts[(j + 1) * 8]);
+        cfma(a2, __ldg(gs + j + 2), ts[(j + 2) * 8]);
+        cfma(a3, __ldg(gs + j + 3), ts[(j + 3) * 8]);
+      }
+      for (; j < w; ++j) cfma(a0, __ldg(gs + j), ts[j * 8]);
+    }
+    double2* dst = smp + ((size_t)(jid * 4 + o) * R + r0 + rr) * wx + ci.off + k;
+    *dst = cadd(*dst, cadd(cadd(a0, a1), cadd(a2, a3)));
+  }
+}
+
+cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
+                                 const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,
+                                 int wmax, int num_sms, cudaStream_t st) {
+  if (J == 0 || R == 0) return cudaSuccess;
+  const int gy = (R + 7) / 8;
+  const int xy = J * Lc * gy;
+  const int gz = std::max(1, std::min(64, (2 * num_sms + xy - 1) / xy));
+  const size_t sm = sizeof(double2) * 4 * (size_t)wmax * 8;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_green_samples, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_green_samples<<<dim3(J * Lc, gy, gz), 256, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax);
+  return cudaGetLastError();
 }

@@ -40,6 +40,7 @@ struct CellInfo {
   long long sinv_off;     // double2 offset into the Schur-inverse pool
   long long green_off;    // double2 offset into the Green-block pool
   long long lz_off;       // offset into lz/uz pools
+  long long gsmp_off;     // double2 offset into the sampled trace-response pool (-1: none)
 };
 
 // A reference to one panel (segment) of a vector: vec < 0 = absent.

@@ -40,6 +40,7 @@ struct K1Params {
   double2* xd;        // pass 2: x [q][wzc][w]
   long long* tprof;   // optional per-phase clock64 totals of CTA 0 (debug instrumentation)
   int dbg;            // debug: 1 = no factor streaming (timing only), 2 = no matvec (timing only)
+  int s0;             // pass 0 also writes the layer-row samples of its solution into smp
 };
 
 struct InnerParams {
@@ -87,6 +88,10 @@ __host__ __device__ constexpr int k1_jw(int nc) { return nc == 1 ? 5 : (nc == 2 
 size_t inner_smem_bytes(int wmax, int nitems);
 int inner_mg(int wmax);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
+// smp += trace-source response (sampled Green rows) for every (job, cell, output row, RHS)
+cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
+                                 const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,
+                                 int wmax, int num_sms, cudaStream_t st);
 
 __global__ void k_gather_panels(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
                                 double2* P);

@@ -46,6 +46,7 @@ struct Stage {
   std::vector<std::pair<int, int>> lgrp;  // (layer, begin in ljobs); count from next
   int* ljobs_d = nullptr;
   bool any_panel = false, any_sample = false;
+  bool samples_only = true;  // every job's outputs are layer-row samples (no volume output)
   // task cache per active-RHS count
   struct Tasks {
     K1Task* d = nullptr;
@@ -80,6 +81,7 @@ struct pt_ctx {
   LayerInfo* lay_d = nullptr;
   CellInfo* cel_d = nullptr;
   double2 *sinv_d = nullptr, *green_d = nullptr, *lz_d = nullptr, *uz_d = nullptr;
+  double2* gsmp_d = nullptr;  // sampled trace responses (optional; enables the one-pass layer solve)
   double2 *tx_d = nullptr, *tz_d = nullptr;
   double* m_d = nullptr;
   // inner item programs
@@ -205,6 +207,7 @@ static int finalize_stage(pt_ctx* c, Stage& S) {
     for (int s = 0; s < 4; ++s)
       if (jb.pan[s][0].vec >= 0) S.any_panel = true;
     if (jb.nout > 0) S.any_sample = true;
+    if (jb.nout <= 0) S.samples_only = false;
   }
   if (upload(&S.jobs_d, S.jobs.data(), S.jobs.size())) return PT_CUDA_ERROR;
   if (upload(&S.stage_jobs_d, sj.data(), sj.size())) return PT_CUDA_ERROR;
@@ -676,6 +679,10 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   kp.dbg = std::getenv("PT_K1_DBG") ? atoi(std::getenv("PT_K1_DBG")) : 0;
   // volume sources/outputs are indexed by the real RHS id: pre-offset through rmap on the host is not
   // possible per column, so stage buffers use compact q and f/u use q as well (callers compact f/u).
+  // one-pass layer solve: samples = pass-0 samples + sampled trace responses (linearity)
+  static const bool no_gsmp = std::getenv("PT_NO_GSMP") != nullptr;
+  const bool gpath = c->Lc > 1 && c->gsmp_d && S.samples_only && !no_gsmp;
+  kp.s0 = gpath ? 1 : 0;
   if (c->Lc > 1) {
     kp.pass = 0;
     {
@@ -722,8 +729,13 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     LaunchScope ls(c, 1);
     CK(inner_launch(ip, J, c->st));
   }
-  kp.pass = 1;
-  {
+  if (gpath) {
+    LaunchScope ls(c, 2);
+    CK(green_samples_launch(S.jobs_d, J, c->cel_d, c->lay_d, c->gsmp_d, c->trc, c->smp, Ract, c->Lc, c->wx,
+                            c->wmax, c->num_sms, c->st));
+  } else {
+    kp.pass = 1;
+    kp.s0 = 0;
     LaunchScope ls(c, 0);
     CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
     c->k1_bytes += T->bytes;
@@ -1228,7 +1240,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
     return PT_BAD_ARGUMENT;
   }
   // cells
-  long long soff = 0, goff = 0, zoff = 0;
+  long long soff = 0, goff = 0, zoff = 0, gsoff = 0;
   c->wzcmax = 0;
   std::vector<int> coffs(c->Lc);
   {
@@ -1269,6 +1281,8 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       ci.sinv_off = soff;
       ci.green_off = goff;
       ci.lz_off = zoff;
+      ci.gsmp_off = pb->gsmp ? gsoff : -1;
+      gsoff += 16LL * ci.wzc * ci.w;
       soff += (long long)ci.wzc * ci.w * ((ci.w + 3) & ~3);  // blocks padded to a multiple of 4 columns
       goff += 16LL * ((ci.w + 7) / 8) * 8 * ci.w;  // tile-major, rows padded to 8
       zoff += ci.wzc;
@@ -1277,6 +1291,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
     }
   CK(cudaMalloc(&c->sinv_d, sizeof(double2) * (size_t)soff));
   CK(cudaMalloc(&c->green_d, sizeof(double2) * (size_t)goff));
+  if (pb->gsmp) CK(cudaMalloc(&c->gsmp_d, sizeof(double2) * (size_t)gsoff));
   CK(cudaMalloc(&c->lz_d, sizeof(double2) * (size_t)zoff));
   CK(cudaMalloc(&c->uz_d, sizeof(double2) * (size_t)zoff));
   for (const CellInfo& ci : c->cel) {
@@ -1298,6 +1313,9 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       CK(cudaDeviceSynchronize());
       cudaFree(tmp);
     }
+    if (pb->gsmp)
+      CK(cudaMemcpy(c->gsmp_d + ci.gsmp_off, pb->gsmp[id], sizeof(double2) * 16 * (size_t)ci.wzc * ci.w,
+                    cudaMemcpyDefault));
     CK(cudaMemcpy(c->lz_d + ci.lz_off, pb->lz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
     CK(cudaMemcpy(c->uz_d + ci.lz_off, pb->uz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
   }
@@ -1355,7 +1373,7 @@ int pt_destroy(pt_ctx* c) {
   cudaDeviceSynchronize();
   // the process-level allocations are released with the context
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
-  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->lz_d,
+  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->lz_d,
                   (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->items_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
                   (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables,

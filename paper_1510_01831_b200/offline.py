@@ -86,6 +86,9 @@ class CellFactors:
     green: torch.Tensor  # (4 rows, 4 slots, w, w) column-major blocks
     coefs: np.ndarray  # (4,) cell-level slot coefficients
     krows: np.ndarray  # (4,) cell block rows of the slot sources
+    # (wzc, 4 layer trace rows, 4 slots, w): H_c^{-1} (coef_s E_{krow_s}) sampled at every block row
+    # and at the layer trace rows 0, 1, n, n+1 -- the trace-source response of the sampled rows
+    gsmp: torch.Tensor = None
 
 
 @dataclass
@@ -278,6 +281,7 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True):
             dg = torch.as_tensor(diag, device=device)
             sinv = _schur_inverses(tw, dg, lz, uz, device)
             gblk = None
+            gsmp = None
             if green:
                 # H_c^{-1} columns at the four slot rows, sampled at the four rows
                 rows4 = [int(r) for r in (ckrows[1], ckrows[0], ckrows[3], ckrows[2])]  # r0,r1,rn,rnp
@@ -293,6 +297,9 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True):
                     for s in range(4):
                         # column-major storage == transpose of the row-major block
                         gblk[:, jr, s] = X[:, rr, :, s * w : (s + 1) * w].transpose(-1, -2)
+                # layer trace rows 0, 1, n, n+1 in the cell-local frame (offset npml - 1), every block row
+                jrows = [npml - 1, npml, n + npml - 1, n + npml]
+                gsmp = X[:, :, jrows, :].reshape(len(idxs), wzc, 4, 4, w).contiguous()
             if wzc < 3:
                 raise ValueError("cells need at least 3 block rows (nx_c + 2 npml >= 3)")
             tinv = _twisted_inverses(tw, dg, lz, uz, sinv, device)
@@ -303,6 +310,7 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True):
                     np.asarray(lz), np.asarray(uz),
                     None if gblk is None else gblk[b].contiguous(),
                     ccoefs, ckrows,
+                    None if gsmp is None else gsmp[b].contiguous(),
                 )
         lf.cells = cells
         layers.append(lf)
