@@ -39,7 +39,7 @@ __device__ __forceinline__ void csync() { cg::this_cluster().sync(); }
 
 // optional clock64 segment totals (PT_INNER_TPROF): 0 tile issue+add/sub prefetch, 1 panel gather,
 // 2 tile wait, 3 dmma, 4 combine, 5 cluster barriers, 6 arnoldi+givens, 7 rest
-__device__ long long g_in_t[8];
+__device__ long long g_in_t[12];  // 8 setup, 9 final x = V y, 10 programs run, 11 kernel total
 struct Ticker {
   bool on;
   long long t0;
@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   const int nIc = p.Lc - 1;
   const int n = 4 * nIc * w;
   const int tid = threadIdx.x;
+  const long long tk_entry = clock64();
 
   InSmem S;
   S.tiles = reinterpret_cast<double2*>(smem);
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   if (tid < ni) S.act[tid] = tid;
   if (tid == 0) s_nact = ni;
   csync();
+  T.tick(8);
 
   // ---- b = pre(rhs), beta0 = ||b||, V_0 = b / beta0 (krylov.py:61-80)
   {
@@ -430,6 +432,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
     csync();
     rebuild_active(p, job, r0, ni, S.act, &s_nact);
     T.tick(5);
+    if (T.on) atomicAdd((unsigned long long*)&g_in_t[10], 1ULL);
   }
 
   // ---- x = V_k y, traces = down + up (nested.py:153), owner CTA per instance
@@ -473,6 +476,8 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
     }
     __syncthreads();
   }
+  T.tick(9);
+  if (T.on) atomicAdd((unsigned long long*)&g_in_t[11], (unsigned long long)(clock64() - tk_entry));
 }
 
 int inner_mg(int wmax) { return wmax <= 80 ? 2 : 1; }
@@ -523,11 +528,13 @@ cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, inner_gmres_kernel, p);
 }
 
-void inner_tprof_dump() {
-  long long t[8];
+void inner_tprof_dump(const char* tag) {
+  long long t[12];
+  cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(t, g_in_t, sizeof(t));
-  fprintf(stderr, "inner tprof (cycles, CTA 0): tiles+prefetch %lld gather %lld tilewait %lld dmma %lld combine %lld "
-          "cluster-bar %lld arnoldi %lld rest %lld\n", t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
-  long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  fprintf(stderr, "inner tprof [%s] (cycles, CTA 0): setup %lld tiles+prefetch %lld gather %lld tilewait %lld dmma %lld "
+          "combine %lld cluster-bar %lld arnoldi %lld rest %lld final %lld | iterations %lld total %lld\n", tag, t[8],
+          t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[9], t[10], t[11]);
+  long long z[12] = {0};
   cudaMemcpyToSymbol(g_in_t, z, sizeof(z));
 }

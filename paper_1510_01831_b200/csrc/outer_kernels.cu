@@ -222,65 +222,93 @@ __global__ void k_green_tiles(const double2* src, double2* dst, int w) {
 // so its samples at the layer trace rows are the pass-0 samples (written by K1 pass 0) plus
 // gsmp[k][row][s][:] . tr_s for every kept block row k.
 // grid: x = job * Lc + cell, y = group of 8 RHS, z = chunk of kept block rows.
-__global__ void k_green_samples(const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
+#define GS_KS 4  // kept block rows per staged sub-chunk
+__global__ void __launch_bounds__(256) k_green_samples(const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
                                 const LayerInfo* __restrict__ layers, const double2* __restrict__ gsmp,
                                 const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,
                                 int wmax) {
-  extern __shared__ double2 trs[];  // [4 slots][w][8 rhs]
+  extern __shared__ double2 gs_smem[];
+  double2* trs = gs_smem;                        // [4 slots][w][8 rhs]
+  double2* gsm = gs_smem + (size_t)4 * wmax * 8;  // [GS_KS][4 rows][4 slots][w]
   const int jid = blockIdx.x / Lc, c = blockIdx.x - (blockIdx.x / Lc) * Lc;
   const OJob& jb = jobs[jid];
   const int nout = jb.nout;
   if (nout <= 0) return;
   const LayerInfo& lay = layers[jb.layer];
   const CellInfo& ci = cells[jb.layer * Lc + c];
-  const int w = ci.w, nIc = Lc - 1;
+  const int w = ci.w, nIc = Lc - 1, tid = threadIdx.x;
   const int r0 = blockIdx.y * 8, nr = min(8, R - r0);
-  for (int e = threadIdx.x; e < 4 * w * 8; e += blockDim.x) {
-    const int rr = e & 7, sj = e >> 3, s = sj / w, j = sj - (sj / w) * w;
-    const int I = s < 2 ? c - 1 : c;
-    double2 v = make_double2(0.0, 0.0);
-    if (rr < nr && I >= 0 && I < nIc) v = tr[(((size_t)(jid * R + r0 + rr) * nIc + I) * 2 + (s & 1)) * wmax + j];
-    trs[e] = v;
+  const int lane = tid & 31, wp = tid >> 5;
+  for (int row = wp; row < 32; row += 8) {  // (slot, rhs) rows of the trace panels
+    const int sl = row >> 3, rr = row & 7;
+    const int I = sl < 2 ? c - 1 : c;
+    const bool okr = rr < nr && I >= 0 && I < nIc;
+    const double2* src = tr + (((size_t)(jid * R + r0 + (okr ? rr : 0)) * nIc + (okr ? I : 0)) * 2 + (sl & 1)) * wmax;
+    for (int j = lane; j < w; j += 32) trs[((size_t)sl * w + j) * 8 + rr] = okr ? src[j] : make_double2(0.0, 0.0);
   }
-  __syncthreads();
-  const int s_lo = ci.has_top ? 0 : 2, s_hi = ci.has_bot ? 4 : 2;
+  int oidx[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const int orow = o < nout ? jb.orow[o] : 0;
+    oidx[o] = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
+  }
+  const int s_lo = ci.has_top ? 0 : 2, s_hi = ci.has_bot ? 4 : 2, nsl = s_hi - s_lo;
   const int nk = ci.hi - ci.lo;
   const int k0 = ci.lo + (int)((long long)blockIdx.z * nk / gridDim.z);
   const int k1 = ci.lo + (int)((long long)(blockIdx.z + 1) * nk / gridDim.z);
-  const int nitems = (k1 - k0) * nout * 8;
-  for (int it = threadIdx.x; it < nitems; it += blockDim.x) {
-    const int rr = it & 7, rest = it >> 3;
-    if (rr >= nr) continue;
-    const int o = rest % nout, k = k0 + rest / nout;
-    const int orow = jb.orow[o];
-    const int oi = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
-    const double2* g = gsmp + ci.gsmp_off + ((size_t)k * 4 + oi) * 4 * w;  // [4 slots][w]
-    double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
-    for (int s = s_lo; s < s_hi; ++s) {
-      const double2* gs = g + s * w;
-      const double2* ts = trs + (size_t)s * w * 8 + rr;
-      int j = 0;
-      for (; j + 4 <= w; j += 4) {
-        cfma(a0, __ldg(gs + j), ts[(j + 0) * 8]);
-        cfma(a1, __ldg(gs + j + 1), ts[(j + 1) * 8]);
-        cfma(a2, __ldg(gs + j + 2), ts[(j + 2) * 8]);
-        cfma(a3, __ldg(gs + j + 3), ts[(j + 3) * 8]);
-      }
-      for (; j < w; ++j) cfma(a0, __ldg(gs + j), ts[j * 8]);
+  const int q = tid & 3;  // lane quarter of an item: columns j = q, q + 4, ...
+  for (int kb = k0; kb < k1; kb += GS_KS) {
+    const int nks = min(GS_KS, k1 - kb);
+    __syncthreads();  // traces staged / previous sub-chunk consumed
+    const int nrows = nks * nout * nsl;
+    for (int row = wp; row < nrows; row += 8) {  // coalesced rows of the sampled Green pool
+      const int sl = s_lo + row % nsl, t2 = row / nsl, o = t2 % nout, kk = t2 / nout;
+      const double2* src = gsmp + ci.gsmp_off + (((size_t)(kb + kk) * 4 + oidx[o]) * 4 + sl) * w;
+      double2* dst = gsm + (((size_t)kk * 4 + o) * 4 + sl) * w;
+      for (int j = lane; j < w; j += 32) dst[j] = __ldg(src + j);
     }
-    double2* dst = smp + ((size_t)(jid * 4 + o) * R + r0 + rr) * wx + ci.off + k;
-    *dst = cadd(*dst, cadd(cadd(a0, a1), cadd(a2, a3)));
+    __syncthreads();
+    // item = (kk, o, rr): 4 lanes per item split the columns, reduced with shuffles
+    const int nitems = nks * nout * 8;
+    for (int it0 = tid >> 2; it0 < ((nitems + 63) / 64) * 64; it0 += 64) {
+      const bool ok = it0 < nitems;
+      const int it = ok ? it0 : 0;
+      const int rr = it & 7, rest = it >> 3, o = rest % nout, kk = rest / nout;
+      const double2* g = gsm + ((size_t)kk * 4 + o) * 4 * w;
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+      for (int sl = s_lo; sl < s_hi; ++sl) {
+        const double2* gr = g + sl * w;
+        const double2* tv = trs + (size_t)sl * w * 8 + rr;
+        int j = q;
+        for (; j + 4 < w; j += 8) {
+          cfma(a0, gr[j], tv[j * 8]);
+          cfma(a1, gr[j + 4], tv[(j + 4) * 8]);
+        }
+        if (j < w) cfma(a0, gr[j], tv[j * 8]);
+      }
+      double2 a = cadd(a0, a1);
+#pragma unroll
+      for (int m = 1; m < 4; m <<= 1) {
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, m);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, m);
+      }
+      if (ok && q == 0 && rr < nr) {
+        double2* dst = smp + ((size_t)(jid * 4 + o) * R + r0 + rr) * wx + ci.off + kb + kk;
+        *dst = cadd(*dst, a);
+      }
+    }
   }
 }
 
 cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                  const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,
-                                 int wmax, int num_sms, cudaStream_t st) {
+                                 int wmax, int kmax, int num_sms, cudaStream_t st) {
   if (J == 0 || R == 0) return cudaSuccess;
   const int gy = (R + 7) / 8;
   const int xy = J * Lc * gy;
-  const int gz = std::max(1, std::min(64, (2 * num_sms + xy - 1) / xy));
-  const size_t sm = sizeof(double2) * 4 * (size_t)wmax * 8;
+  // one staged sub-chunk of kept rows per CTA when the grid stays below ~8 CTAs per SM
+  const int gz = std::max(1, std::min((kmax + GS_KS - 1) / GS_KS, (8 * num_sms + xy - 1) / xy));
+  const size_t sm = sizeof(double2) * ((size_t)4 * wmax * 8 + (size_t)GS_KS * 16 * wmax);
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_green_samples, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_green_samples<<<dim3(J * Lc, gy, gz), 256, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax);
   return cudaGetLastError();

@@ -123,7 +123,7 @@ struct pt_ctx {
   bool prof = false;
   struct EvRec {
     cudaEvent_t a, b;
-    int cls;  // 0 K1, 1 inner, 2 other
+    int cls;  // 0 K1, 1 inner, 2 other, 3 sampled trace response (counted as other)
     const char* tag;
   };
   const char* cur_tag = "";
@@ -726,13 +726,16 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     ip.tprof = std::getenv("PT_INNER_TPROF") != nullptr;
     ip.nitems = c->nitems;
     ip.mg = inner_mg(c->wmax);
-    LaunchScope ls(c, 1);
-    CK(inner_launch(ip, J, c->st));
+    {
+      LaunchScope ls(c, 1);
+      CK(inner_launch(ip, J, c->st));
+    }
+    if (ip.tprof) inner_tprof_dump(S.name);
   }
   if (gpath) {
-    LaunchScope ls(c, 2);
+    LaunchScope ls(c, 3);
     CK(green_samples_launch(S.jobs_d, J, c->cel_d, c->lay_d, c->gsmp_d, c->trc, c->smp, Ract, c->Lc, c->wx,
-                            c->wmax, c->num_sms, c->st));
+                            c->wmax, c->wzcmax, c->num_sms, c->st));
   } else {
     kp.pass = 1;
     kp.s0 = 0;
@@ -831,7 +834,6 @@ static int check_err(pt_ctx* c, int* code) {
   return 0;
 }
 
-void inner_tprof_dump();
 // ------------------------------------------------------------------ the online solve (sie.py:392-439)
 
 struct RhsState {
@@ -1105,7 +1107,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   CK(cudaStreamSynchronize(c->st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
-  if (std::getenv("PT_INNER_TPROF")) inner_tprof_dump();
+
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   int ecode = 0;
@@ -1141,7 +1143,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     }
     if (stats->timing_ms) stats->timing_ms[0] = ms;
     if (stats->kernel_ms) {
-      double acc[3] = {0, 0, 0};
+      double acc[4] = {0, 0, 0, 0};
       for (const auto& e : c->evs) {
         float t = 0.f;
         cudaEventElapsedTime(&t, e.a, e.b);
@@ -1153,7 +1155,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     }
     if (stage_prof) {  // per (stage, kernel class) device time, launch count
       std::map<std::string, std::pair<double, int>> agg;
-      static const char* cls_name[3] = {"k1", "inner", "glue"};
+      static const char* cls_name[4] = {"k1", "inner", "glue", "green"};
       for (const auto& e : c->evs) {
         float t = 0.f;
         cudaEventElapsedTime(&t, e.a, e.b);
