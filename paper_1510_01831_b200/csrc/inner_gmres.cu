@@ -81,13 +81,29 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
   auto VM = [&](int i) { return i == 0 ? vmap[0] : (i == 1 ? vmap[1] : vmap[2]); };
   for (int phz = 0; phz < nph; ++phz) {
     const int it0 = ph[phz], nit = ph[phz + 1] - it0;
-    // units: an item's tile groups are split into upi contiguous ranges so that small phases
-    // still occupy the whole cluster; the panels of a unit are gathered once
-    const int upi = nit >= CS ? 1 : min(ngrp, (CS + nit - 1) / nit);
-    const int units = nit * upi;
-    for (int u = q; u < units; u += CS) {
-      const int ii = u / upi, part = u - ii * upi;
-      const int g0 = part * ngrp / upi, g1 = (part + 1) * ngrp / upi;
+    // Weighted split of the phase's (item, tile group) pairs over the cluster: a pair weighs its
+    // number of slot products (1 for a pure combination).  CTA q takes the pairs whose weight
+    // midpoints fall in [q W / CS, (q+1) W / CS); a unit = (item, contiguous group range), its
+    // panels gathered once.
+    auto item_w = [&](int ii) {
+      const IItem& it = S.items[it0 + ii];
+      int ns_ = 0;
+      if (it.cell >= 0)
+        for (int s = 0; s < 4; ++s) ns_ += it.pan[s][0].vec >= 0;
+      return ns_ > 0 ? ns_ : 1;
+    };
+    int wtot = 0;
+    for (int ii = 0; ii < nit; ++ii) wtot += item_w(ii) * ngrp;
+    const int wlo2 = 2 * (int)((long long)q * wtot / CS), whi2 = 2 * (int)((long long)(q + 1) * wtot / CS);
+    auto cdiv = [](int a, int b) { return a <= 0 ? -((-a) / b) : (a + b - 1) / b; };
+    int wcum = 0;
+    for (int ii = 0; ii < nit; ++ii) {
+      const int wi = item_w(ii), wa = wcum;
+      wcum += wi * ngrp;
+      // group g's midpoint (doubled): 2 wa + wi (2g + 1)
+      const int g0 = max(0, cdiv(wlo2 - 2 * wa - wi, 2 * wi));
+      const int g1 = min(ngrp, cdiv(whi2 - 2 * wa - wi, 2 * wi));
+      if (g0 >= g1) continue;
       const IItem& item = S.items[it0 + ii];
       int slotp = 0, ns = 0;  // packed slot list: slot of si in bits [2si, 2si+2)
       if (item.cell >= 0)
@@ -355,25 +371,56 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
       double2* W = vecp(p, job, r, j + 1);
       double2* H = Hp(r);
       double2* col = H + (size_t)j * hld;
-      for (int i = 0; i <= j; ++i) {
-        const double2* Vi = vecp(p, job, r, i);
-        double sr = 0.0, si = 0.0;
-        for (int e = tid; e < n; e += blockDim.x) {
-          const double2 c = cconjmul(ld_cg(Vi + e), ld_cg(W + e));
-          sr += c.x;
-          si += c.y;
-        }
-        sr = block_sum(sr, dred);
-        si = block_sum(si, dred);
-        const double2 h = make_double2(sr, si);
-        if (tid == 0) col[i] = h;
-        for (int e = tid; e < n; e += blockDim.x) W[e] = csub(ld_cg(W + e), cmul(h, ld_cg(Vi + e)));
-        __syncthreads();
-      }
       double ss = 0.0;
-      for (int e = tid; e < n; e += blockDim.x) {
-        const double2 x = W[e];
-        ss += x.x * x.x + x.y * x.y;
+      constexpr int EPT = 8;  // register-resident w for n <= EPT * IN_THREADS
+      if (n <= EPT * IN_THREADS) {
+        double2 wv[EPT];
+#pragma unroll
+        for (int t = 0; t < EPT; ++t) {
+          const int e = tid + t * IN_THREADS;
+          wv[t] = e < n ? ld_cg(W + e) : czero();
+        }
+        for (int i = 0; i <= j; ++i) {
+          const double2* Vi = vecp(p, job, r, i);
+          double2 vv[EPT];
+          double sr = 0.0, si = 0.0;
+#pragma unroll
+          for (int t = 0; t < EPT; ++t) {
+            const int e = tid + t * IN_THREADS;
+            vv[t] = e < n ? ld_cg(Vi + e) : czero();
+            const double2 c = cconjmul(vv[t], wv[t]);
+            sr += c.x;
+            si += c.y;
+          }
+          const double2 h = block_sum2(sr, si, dred);
+          if (tid == 0) col[i] = h;
+#pragma unroll
+          for (int t = 0; t < EPT; ++t) wv[t] = csub(wv[t], cmul(h, vv[t]));
+        }
+#pragma unroll
+        for (int t = 0; t < EPT; ++t) {
+          const int e = tid + t * IN_THREADS;
+          if (e < n) W[e] = wv[t];
+          ss += wv[t].x * wv[t].x + wv[t].y * wv[t].y;
+        }
+      } else {
+        for (int i = 0; i <= j; ++i) {
+          const double2* Vi = vecp(p, job, r, i);
+          double sr = 0.0, si = 0.0;
+          for (int e = tid; e < n; e += blockDim.x) {
+            const double2 c = cconjmul(ld_cg(Vi + e), ld_cg(W + e));
+            sr += c.x;
+            si += c.y;
+          }
+          const double2 h = block_sum2(sr, si, dred);
+          if (tid == 0) col[i] = h;
+          for (int e = tid; e < n; e += blockDim.x) W[e] = csub(ld_cg(W + e), cmul(h, ld_cg(Vi + e)));
+          __syncthreads();
+        }
+        for (int e = tid; e < n; e += blockDim.x) {
+          const double2 x = W[e];
+          ss += x.x * x.x + x.y * x.y;
+        }
       }
       ss = block_sum(ss, dred);
       const double hn = sqrt(ss);

@@ -229,6 +229,27 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ---------------------------------------------------------------- reductions
 
 // block-wide sum of one double (all threads get the result); red: >= 32 doubles of smem
+// two block sums with one pair of barriers (red: >= 2 * warps doubles); fixed order: deterministic
+__device__ __forceinline__ double2 block_sum2(double a, double b, double* red) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    red[2 * wid] = a;
+    red[2 * wid + 1] = b;
+  }
+  __syncthreads();
+  double sa = 0.0, sb = 0.0;
+  const int nw = (blockDim.x + 31) >> 5;
+  for (int i = 0; i < nw; ++i) {
+    sa += red[2 * i];
+    sb += red[2 * i + 1];
+  }
+  return make_double2(sa, sb);
+}
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
