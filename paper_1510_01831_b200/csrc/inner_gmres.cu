@@ -39,7 +39,7 @@ __device__ __forceinline__ void csync() { cg::this_cluster().sync(); }
 
 // optional clock64 segment totals (PT_INNER_TPROF): 0 tile issue+add/sub prefetch, 1 panel gather,
 // 2 tile wait, 3 dmma, 4 combine, 5 cluster barriers, 6 arnoldi+givens, 7 rest
-__device__ long long g_in_t[12];  // 8 setup, 9 final x = V y, 10 programs run, 11 kernel total
+__device__ long long g_in_t[16];  // 8 setup, 9 final x = V y, 10 programs run, 11 kernel total
 struct Ticker {
   bool on;
   long long t0;
@@ -64,6 +64,8 @@ struct InSmem {
   int* act;         // active local instances
   IItem* items;     // the op + pre programs (staged once)
   long long* goff;  // [Lc] Green-pool offsets of this layer's cells (staged once)
+  int* oph;         // op program phase offsets (staged once)
+  int* pph;         // pre program phase offsets (staged once)
 };
 
 // Execute one program (list of phases) for the active instances of this cluster.
@@ -85,13 +87,7 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
     // number of slot products (1 for a pure combination).  CTA q takes the pairs whose weight
     // midpoints fall in [q W / CS, (q+1) W / CS); a unit = (item, contiguous group range), its
     // panels gathered once.
-    auto item_w = [&](int ii) {
-      const IItem& it = S.items[it0 + ii];
-      int ns_ = 0;
-      if (it.cell >= 0)
-        for (int s = 0; s < 4; ++s) ns_ += it.pan[s][0].vec >= 0;
-      return ns_ > 0 ? ns_ : 1;
-    };
+    auto item_w = [&](int ii) { return S.items[it0 + ii].wgt; };
     int wtot = 0;
     for (int ii = 0; ii < nit; ++ii) wtot += item_w(ii) * ngrp;
     const int wlo2 = 2 * (int)((long long)q * wtot / CS), whi2 = 2 * (int)((long long)(q + 1) * wtot / CS);
@@ -104,6 +100,7 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
       const int g0 = max(0, cdiv(wlo2 - 2 * wa - wi, 2 * wi));
       const int g1 = min(ngrp, cdiv(whi2 - 2 * wa - wi, 2 * wi));
       if (g0 >= g1) continue;
+      T.tick(12);  // phase/unit bookkeeping
       const IItem& item = S.items[it0 + ii];
       int slotp = 0, ns = 0;  // packed slot list: slot of si in bits [2si, 2si+2)
       if (item.cell >= 0)
@@ -111,21 +108,25 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
           if (item.pan[s][0].vec >= 0) slotp |= s << (2 * ns++);
       auto slot_of = [&](int si) { return slotp >> (2 * si) & 3; };
       const long long goff = S.goff[item.cell >= 0 ? item.cell : 0];
+      // called by all of warp 0: lane 0 arms the barrier, then one lane per (slot, tile) issues its bulk copy
       auto issue_tiles = [&](int g, int buf) {
         const int mt0 = g * MG, nt = min(MG, nmt - mt0);
-        mbar_expect_tx(&S.tbar[buf], tbytes * (uint32_t)(ns * nt));
-        for (int si = 0; si < ns; ++si)
-          for (int t = 0; t < nt; ++t)
-            bulk_g2s(S.tiles + buf * tbuf + ((size_t)si * MG + t) * w * 8,
-                     p.green + goff + ((size_t)(item.row * 4 + slot_of(si)) * nmt + mt0 + t) * w * 8,
-                     tbytes, &S.tbar[buf]);
+        if (lane == 0) mbar_expect_tx(&S.tbar[buf], tbytes * (uint32_t)(ns * nt));
+        __syncwarp();
+        if (lane < ns * nt) {
+          const int si = lane / nt, t = lane - (lane / nt) * nt;
+          bulk_g2s(S.tiles + buf * tbuf + ((size_t)si * MG + t) * w * 8,
+                   p.green + goff + ((size_t)(item.row * 4 + slot_of(si)) * nmt + mt0 + t) * w * 8, tbytes,
+                   &S.tbar[buf]);
+        }
       };
       int negm = 0;  // bit si: slot panel si enters negated (exact)
       for (int si = 0; si < ns; ++si) negm |= (item.flags >> slot_of(si) & 1) << si;
       int twom = 0;  // bit si: two-term slot panel (d + p); its second term is staged in pan2
       for (int si = 0; si < ns; ++si) twom |= (item.pan[slot_of(si)][1].vec >= 0) << si;
       if (ns > 0) {
-        if (tid == 0) issue_tiles(g0, 0);
+        if (wp == 0) issue_tiles(g0, 0);
+        T.tick(13);  // tile issue
         // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill).
         // IN_THREADS % 8 == 0, so a thread's instance qq is fixed and its scratch base is computed once.
         const int qq = tid & 7;
@@ -148,7 +149,7 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
         const int buf = (g - g0) & 1;
         const int mt0 = g * MG, nt = min(MG, nmt - mt0);
         const int row0 = mt0 * 8, rows = min(w, row0 + nt * 8) - row0;
-        if (ns > 0 && tid == 0 && g + 1 < g1) issue_tiles(g + 1, buf ^ 1);  // buffer freed last iteration
+        if (ns > 0 && wp == 0 && g + 1 < g1) issue_tiles(g + 1, buf ^ 1);  // buffer freed last iteration
         // this thread's output (row, instance) and its combine operands
         const int oq = tid & 7, orow = tid >> 3;
         const bool own = orow < rows && oq < nact;
@@ -271,7 +272,9 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   S.tbar = reinterpret_cast<uint64_t*>(dred + 64);
   S.act = reinterpret_cast<int*>(S.tbar + 2);
   S.goff = reinterpret_cast<long long*>(S.act + 16);
-  S.items = reinterpret_cast<IItem*>(S.goff + PT_MAX_LC);
+  S.oph = reinterpret_cast<int*>(S.goff + PT_MAX_LC);
+  S.pph = S.oph + 2 * PT_MAX_LC + 2;
+  S.items = reinterpret_cast<IItem*>(S.pph + 2 * PT_MAX_LC + 2);
   __shared__ int s_nact;
   if (nIc == 0) return;
   if (tid == 0) {
@@ -280,6 +283,8 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
     fence_mbar_init();
   }
   for (int i = tid; i < p.nitems; i += blockDim.x) S.items[i] = p.items[i];
+  for (int i = tid; i <= p.op_nph; i += blockDim.x) S.oph[i] = p.op_ph[i];
+  for (int i = tid; i <= p.pre_nph; i += blockDim.x) S.pph[i] = p.pre_ph[i];
   for (int i = tid; i < p.Lc; i += blockDim.x) S.goff[i] = p.cells[layer * p.Lc + i].green_off;
   uint32_t tphase[2] = {0, 0};
   Ticker T;
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   // ---- b = pre(rhs), beta0 = ||b||, V_0 = b / beta0 (krylov.py:61-80)
   {
     const int vm[3] = {VB, VY, VA};
-    run_program(p, job, layer, w, r0, p.pre_ph, p.pre_nph, vm, s_nact, S, q, CS, tphase, T);
+    run_program(p, job, layer, w, r0, S.pph, p.pre_nph, vm, s_nact, S, q, CS, tphase, T);
   }
   for (int l = q; l < ni; l += CS) {
     const int r = r0 + l;
@@ -358,9 +363,9 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
     }
     {
       const int vm1[3] = {j, VT, VA};
-      run_program(p, job, layer, w, r0, p.op_ph, p.op_nph, vm1, nact, S, q, CS, tphase, T);
+      run_program(p, job, layer, w, r0, S.oph, p.op_nph, vm1, nact, S, q, CS, tphase, T);
       const int vm2[3] = {VT, j + 1, VA};
-      run_program(p, job, layer, w, r0, p.pre_ph, p.pre_nph, vm2, nact, S, q, CS, tphase, T);
+      run_program(p, job, layer, w, r0, S.pph, p.pre_nph, vm2, nact, S, q, CS, tphase, T);
       T.tick(7);
     }
     // ---- MGS Arnoldi + Givens for the instances this CTA owns (krylov.py:89-127)
@@ -532,7 +537,7 @@ int inner_mg(int wmax) { return wmax <= 80 ? 2 : 1; }
 size_t inner_smem_bytes(int wmax, int nitems) {
   const int w = wmax < 8 ? 8 : wmax;
   return (size_t)(2 * 4 * inner_mg(wmax) + 4 + 2) * w * 8 * 16 + (size_t)(IN_THREADS / 32) * IN_MG * 8 * 8 * 16 + 64 * 8 +
-         16 + 64 + PT_MAX_LC * 8 + (size_t)nitems * sizeof(IItem) + 128;
+         16 + 64 + PT_MAX_LC * 8 + 2 * (2 * PT_MAX_LC + 2) * 4 + (size_t)nitems * sizeof(IItem) + 128;
 }
 
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
@@ -576,12 +581,12 @@ cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
 }
 
 void inner_tprof_dump(const char* tag) {
-  long long t[12];
+  long long t[16];
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(t, g_in_t, sizeof(t));
   fprintf(stderr, "inner tprof [%s] (cycles, CTA 0): setup %lld tiles+prefetch %lld gather %lld tilewait %lld dmma %lld "
-          "combine %lld cluster-bar %lld arnoldi %lld rest %lld final %lld | iterations %lld total %lld\n", tag, t[8],
-          t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[9], t[10], t[11]);
-  long long z[12] = {0};
+          "combine %lld cluster-bar %lld arnoldi %lld rest %lld final %lld | iterations %lld total %lld | bookkeeping %lld "
+          "tile-issue %lld\n", tag, t[8], t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[9], t[10], t[11], t[12], t[13]);
+  long long z[16] = {0};
   cudaMemcpyToSymbol(g_in_t, z, sizeof(z));
 }

@@ -71,6 +71,7 @@ struct IItem {
   Ref pan[4][2];     // slot panels: pan[s][1] (if present) is added to pan[s][0]
   Ref dst, add[2], sub[2], rev;
   int flags;
+  int wgt;           // work weight: number of slot products (1 for a pure combination)
 };
 
 // K1 task: one cell, a contiguous range of columns (job, rhs) of its layer.

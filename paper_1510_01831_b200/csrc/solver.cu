@@ -477,6 +477,12 @@ static int build_inner(pt_ctx* c) {
     for (const IItem& x : P[ph]) items.push_back(x);
     pph.push_back((int)items.size());
   }
+  for (IItem& x : items) {
+    int ns = 0;
+    if (x.cell >= 0)
+      for (int k = 0; k < 4; ++k) ns += x.pan[k][0].vec >= 0;
+    x.wgt = ns > 0 ? ns : 1;
+  }
   c->op_nph = (int)oph.size() - 1;
   c->pre_nph = (int)pph.size() - 1;
   c->op_blocks = opb;
