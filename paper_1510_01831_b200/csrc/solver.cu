@@ -1169,7 +1169,9 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
         v.first += t;
         v.second += 1;
       }
-      fprintf(stderr, "stage profile (total %.3f ms):\n", ms);
+      double ksum = 0.0;
+      for (const auto& kv : agg) ksum += kv.second.first;
+      fprintf(stderr, "stage profile (total %.3f ms, launches %.3f ms, gaps %.3f ms):\n", ms, ksum, ms - ksum);
       for (const auto& kv : agg)
         fprintf(stderr, "  %-16s %8.3f ms  %5d launches  %8.1f us/launch\n", kv.first.c_str(), kv.second.first,
                 kv.second.second, 1e3 * kv.second.first / kv.second.second);
