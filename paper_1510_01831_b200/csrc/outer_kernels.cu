@@ -222,80 +222,69 @@ __global__ void k_green_tiles(const double2* src, double2* dst, int w) {
 // so its samples at the layer trace rows are the pass-0 samples (written by K1 pass 0) plus
 // gsmp[k][row][s][:] . tr_s for every kept block row k.
 // grid: x = job * Lc + cell, y = group of 8 RHS, z = chunk of kept block rows.
-#define GS_KS 4  // kept block rows per staged sub-chunk
-__global__ void __launch_bounds__(256) k_green_samples(const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
-                                const LayerInfo* __restrict__ layers, const double2* __restrict__ gsmp,
-                                const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,
-                                int wmax) {
-  extern __shared__ double2 gs_smem[];
-  double2* trs = gs_smem;                        // [4 slots][w][8 rhs]
-  double2* gsm = gs_smem + (size_t)4 * wmax * 8;  // [GS_KS][4 rows][4 slots][w]
+// DMMA formulation: rows = (kept block row k, output row o) of a cell, N = 8 RHS, K = (slot, column j):
+//   C[(k,o)][r] += sum_{s,j} G[k][o][s][j] * tr_s[r][j]   (complex: Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br)
+// A fragments straight from the sampled Green pool (each element used once per CTA), B fragments from the
+// trace panels staged in shared memory as [slot][j (padded to w4, zeros)][8 RHS]; one 8-row tile per warp.
+#define GS_WARPS 8
+__global__ void __launch_bounds__(GS_WARPS * 32) k_green_samples(
+    const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells, const LayerInfo* __restrict__ layers,
+    const double2* __restrict__ gsmp, const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,
+    int wmax) {
+  extern __shared__ double2 trs[];  // [4 slots][w4][8 rhs]
   const int jid = blockIdx.x / Lc, c = blockIdx.x - (blockIdx.x / Lc) * Lc;
   const OJob& jb = jobs[jid];
   const int nout = jb.nout;
   if (nout <= 0) return;
   const LayerInfo& lay = layers[jb.layer];
   const CellInfo& ci = cells[jb.layer * Lc + c];
-  const int w = ci.w, nIc = Lc - 1, tid = threadIdx.x;
-  const int r0 = blockIdx.y * 8, nr = min(8, R - r0);
+  const int w = ci.w, w4 = (w + 3) & ~3, nIc = Lc - 1, tid = threadIdx.x;
   const int lane = tid & 31, wp = tid >> 5;
-  for (int row = wp; row < 32; row += 8) {  // (slot, rhs) rows of the trace panels
+  const int r0 = blockIdx.y * 8, nr = min(8, R - r0);
+  for (int row = wp; row < 32; row += GS_WARPS) {  // (slot, rhs) rows of the trace panels
     const int sl = row >> 3, rr = row & 7;
     const int I = sl < 2 ? c - 1 : c;
     const bool okr = rr < nr && I >= 0 && I < nIc;
     const double2* src = tr + (((size_t)(jid * R + r0 + (okr ? rr : 0)) * nIc + (okr ? I : 0)) * 2 + (sl & 1)) * wmax;
-    for (int j = lane; j < w; j += 32) trs[((size_t)sl * w + j) * 8 + rr] = okr ? src[j] : make_double2(0.0, 0.0);
+    for (int j = lane; j < w4; j += 32)
+      trs[((size_t)sl * w4 + j) * 8 + rr] = (okr && j < w) ? src[j] : make_double2(0.0, 0.0);
   }
-  int oidx[4];
-#pragma unroll
-  for (int o = 0; o < 4; ++o) {
-    const int orow = o < nout ? jb.orow[o] : 0;
-    oidx[o] = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
-  }
-  const int s_lo = ci.has_top ? 0 : 2, s_hi = ci.has_bot ? 4 : 2, nsl = s_hi - s_lo;
-  const int nk = ci.hi - ci.lo;
-  const int k0 = ci.lo + (int)((long long)blockIdx.z * nk / gridDim.z);
-  const int k1 = ci.lo + (int)((long long)(blockIdx.z + 1) * nk / gridDim.z);
-  const int q = tid & 3;  // lane quarter of an item: columns j = q, q + 4, ...
-  for (int kb = k0; kb < k1; kb += GS_KS) {
-    const int nks = min(GS_KS, k1 - kb);
-    __syncthreads();  // traces staged / previous sub-chunk consumed
-    const int nrows = nks * nout * nsl;
-    for (int row = wp; row < nrows; row += 8) {  // coalesced rows of the sampled Green pool
-      const int sl = s_lo + row % nsl, t2 = row / nsl, o = t2 % nout, kk = t2 / nout;
-      const double2* src = gsmp + ci.gsmp_off + (((size_t)(kb + kk) * 4 + oidx[o]) * 4 + sl) * w;
-      double2* dst = gsm + (((size_t)kk * 4 + o) * 4 + sl) * w;
-      for (int j = lane; j < w; j += 32) dst[j] = __ldg(src + j);
+  __syncthreads();
+  const int s_lo = ci.has_top ? 0 : 2, s_hi = ci.has_bot ? 4 : 2;
+  const int nrows = (ci.hi - ci.lo) * nout;  // (k, o) rows of this cell, k-major
+  const int tile = blockIdx.z * GS_WARPS + wp;
+  if (tile * 8 >= nrows) return;
+  const int ar = lane >> 2, ak = lane & 3;
+  // this lane's A row
+  const int m = tile * 8 + ar;
+  const bool mok = m < nrows;
+  const int mk = mok ? m / nout : 0, mo = mok ? m - (m / nout) * nout : 0;
+  const int orow = jb.orow[mo];
+  const int oi = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
+  const double2* grow = gsmp + ci.gsmp_off + ((size_t)(ci.lo + mk) * 4 + oi) * 4 * w;  // [4 slots][w]
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  for (int sl = s_lo; sl < s_hi; ++sl) {
+    const double2* ga = grow + sl * w;
+    const double2* tb = trs + (size_t)sl * w4 * 8 + ar;
+#pragma unroll 6
+    for (int j0 = 0; j0 < w4; j0 += 4) {
+      const int j = j0 + ak;
+      const double2 av = (mok && j < w) ? __ldg(ga + j) : make_double2(0.0, 0.0);
+      const double2 bv = tb[(size_t)j * 8];
+      dmma_f64(c0, c1, av.x, bv.x);
+      dmma_f64(c2, c3, av.x, bv.y);
+      dmma_f64(c0, c1, -av.y, bv.y);
+      dmma_f64(c2, c3, av.y, bv.x);
     }
-    __syncthreads();
-    // item = (kk, o, rr): 4 lanes per item split the columns, reduced with shuffles
-    const int nitems = nks * nout * 8;
-    for (int it0 = tid >> 2; it0 < ((nitems + 63) / 64) * 64; it0 += 64) {
-      const bool ok = it0 < nitems;
-      const int it = ok ? it0 : 0;
-      const int rr = it & 7, rest = it >> 3, o = rest % nout, kk = rest / nout;
-      const double2* g = gsm + ((size_t)kk * 4 + o) * 4 * w;
-      double2 a0 = make_double2(0.0, 0.0), a1 = a0;
-      for (int sl = s_lo; sl < s_hi; ++sl) {
-        const double2* gr = g + sl * w;
-        const double2* tv = trs + (size_t)sl * w * 8 + rr;
-        int j = q;
-        for (; j + 4 < w; j += 8) {
-          cfma(a0, gr[j], tv[j * 8]);
-          cfma(a1, gr[j + 4], tv[(j + 4) * 8]);
-        }
-        if (j < w) cfma(a0, gr[j], tv[j * 8]);
-      }
-      double2 a = cadd(a0, a1);
+  }
+  // C fragment: row ar, columns (RHS) 2 ak and 2 ak + 1; (c0, c2) and (c1, c3) are complex
+  if (!mok) return;
 #pragma unroll
-      for (int m = 1; m < 4; m <<= 1) {
-        a.x += __shfl_xor_sync(0xffffffffu, a.x, m);
-        a.y += __shfl_xor_sync(0xffffffffu, a.y, m);
-      }
-      if (ok && q == 0 && rr < nr) {
-        double2* dst = smp + ((size_t)(jid * 4 + o) * R + r0 + rr) * wx + ci.off + kb + kk;
-        *dst = cadd(*dst, a);
-      }
+  for (int h = 0; h < 2; ++h) {
+    const int rr = 2 * ak + h;
+    if (rr < nr) {
+      double2* dst = smp + ((size_t)(jid * 4 + mo) * R + r0 + rr) * wx + ci.off + ci.lo + mk;
+      *dst = cadd(*dst, h == 0 ? make_double2(c0, c2) : make_double2(c1, c3));
     }
   }
 }
@@ -303,13 +292,13 @@ __global__ void __launch_bounds__(256) k_green_samples(const OJob* __restrict__ 
 cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                  const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,
                                  int wmax, int kmax, int num_sms, cudaStream_t st) {
+  (void)num_sms;
   if (J == 0 || R == 0) return cudaSuccess;
   const int gy = (R + 7) / 8;
-  const int xy = J * Lc * gy;
-  // one staged sub-chunk of kept rows per CTA when the grid stays below ~8 CTAs per SM
-  const int gz = std::max(1, std::min((kmax + GS_KS - 1) / GS_KS, (8 * num_sms + xy - 1) / xy));
-  const size_t sm = sizeof(double2) * ((size_t)4 * wmax * 8 + (size_t)GS_KS * 16 * wmax);
+  // rows per cell <= kmax kept block rows x 4 output rows; one 8-row tile per warp
+  const int gz = (kmax * 4 + 8 * GS_WARPS - 1) / (8 * GS_WARPS);
+  const size_t sm = sizeof(double2) * 4 * (size_t)((wmax + 3) & ~3) * 8;
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_green_samples, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_green_samples<<<dim3(J * Lc, gy, gz), 256, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax);
+  k_green_samples<<<dim3(J * Lc, gy, gz), GS_WARPS * 32, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax);
   return cudaGetLastError();
 }
