@@ -71,6 +71,12 @@ typedef struct {
    * [L*Lc] -> [wz_c][4 layer trace rows 0,1,n,n+1][4 slots][w] complex, the trace-source
    * response H_c^{-1}(coef_s E_krow_s) sampled at every block row and the layer trace rows */
   const double* const* gsmp;
+  /* optional (NULL: layer solves without a volume source run the first cell-solve pass):
+   * [L*Lc] -> [M][4 nk4] complex row-major, the cell response to the layer slot sources
+   * (coef_s E at layer row prow_s, every kept block row k; nk = kept rows, nk4 = roundup(nk, 4))
+   * sampled at the Newton-table block rows (4 x w) and the layer trace rows of every kept block
+   * row (4 nk); M = roundup(4 w + 4 nk, 8) */
+  const double* const* q0;
 } pt_problem;
 
 typedef struct {

@@ -52,6 +52,7 @@ class PtProblem(C.Structure):
         ("layer_coefs", _dp), ("cell_coefs", _dp),
         ("lz", C.POINTER(_dp)), ("uz", C.POINTER(_dp)),
         ("sinv", C.POINTER(_dp)), ("green", C.POINTER(_dp)), ("gsmp", C.POINTER(_dp)),
+        ("q0", C.POINTER(_dp)),
     ]
 
 
@@ -141,9 +142,9 @@ class Context:
         pb.layer_coefs = dptr(arr(np.stack([lf.coefs for lf in F.layers]), np.complex128))
         pb.cell_coefs = dptr(arr(np.stack([cf.coefs for cf in cells]), np.complex128))
         ptr_arrays = {}
-        for name in ("lz", "uz", "sinv", "green", "gsmp"):
-            if name == "gsmp" and any(getattr(cf, "gsmp", None) is None for cf in cells):
-                continue  # optional: the second cell-solve pass produces the samples
+        for name in ("lz", "uz", "sinv", "green", "gsmp", "q0"):
+            if name in ("gsmp", "q0") and any(getattr(cf, name, None) is None for cf in cells):
+                continue  # optional: the cell-solve passes produce these outputs
             P = (_dp * nid)()
             for i, cf in enumerate(cells):
                 v = getattr(cf, name)

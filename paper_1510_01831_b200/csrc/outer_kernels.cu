@@ -29,7 +29,10 @@ __global__ void k_gather_panels(const OJob* jobs, int njobs, VecTab t, const int
     const int s = (int)(rest % 4);
     const int j = (int)(rest / 4);
     const Ref* pr = jobs[j].pan[s];
-    if (pr[0].vec < 0) continue;
+    if (pr[0].vec < 0) {  // absent slot: zero (the dense pass-0 product reads every slot)
+      P[e] = make_double2(0.0, 0.0);
+      continue;
+    }
     const int r = rmap[q];
     double2 v = vref(t, pr[0], r, x, wx);
     if (pr[1].vec >= 0) v = cadd(v, vref(t, pr[1], r, x, wx));
@@ -300,5 +303,111 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
   const size_t sm = sizeof(double2) * 4 * (size_t)((wmax + 3) & ~3) * 8;
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_green_samples, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_green_samples<<<dim3(J * Lc, gy, gz), GS_WARPS * 32, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// First pass of a layer solve without a volume source, as one dense product per cell:
+//   out[m][n] = sum_{s,k} Q0[m][(s,k)] * P[job(n)][s][q(n)][off_c + lo + k]
+// m < 4w: Newton-table rows (block row r0/r1/rn/rnp, column j); m >= 4w: layer-row samples
+// (kept block row k, row 0/1/n/n+1).  DMMA m8n8k4 f64 complex (4 products per k-step), one 8-row
+// tile x up to 32 columns (4 groups of 8) per warp, A from the operator pool, B from the gathered panels.
+// grid: x = layer group g * Lc + cell, y = chunk of 8 row tiles, z = chunk of 32 columns.
+#define P0_COLS 16  // columns (job, RHS) per CTA: two DMMA column groups of 8
+__global__ void __launch_bounds__(256) k_pass0(const int* __restrict__ grp, const int* __restrict__ ljobs,
+                                               const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
+                                               const LayerInfo* __restrict__ layers, const double2* __restrict__ q0,
+                                               const double2* __restrict__ P, double2* __restrict__ tables,
+                                               double2* __restrict__ smp, int R, int Lc, int wx, int wmax) {
+  extern __shared__ double2 bs[];  // [K][P0_COLS]: the CTA's panel columns
+  const int g = blockIdx.x / Lc, c = blockIdx.x - (blockIdx.x / Lc) * Lc;
+  const int layer = grp[3 * g], jb0 = grp[3 * g + 1], nj = grp[3 * g + 2];
+  const CellInfo& ci = cells[layer * Lc + c];
+  const LayerInfo& lay = layers[layer];
+  const int w = ci.w, nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3, K = 4 * nk4;
+  const int M = 4 * w + 4 * nk, Mp = (M + 7) & ~7;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int N = nj * R, n0 = blockIdx.z * P0_COLS;
+  if (n0 >= N || blockIdx.y * 64 >= Mp) return;
+  // stage B = the CTA's panel columns (zero past nk and past N), 16-byte cp.async
+  for (int e = threadIdx.x; e < K * P0_COLS; e += blockDim.x) {
+    const int col = e % P0_COLS, kr = e / P0_COLS;
+    const int sl = kr / nk4, k = kr - (kr / nk4) * nk4;
+    const int n = n0 + col;
+    const bool ok = n < N && k < nk;
+    const int jid = ljobs[jb0 + (ok ? n / R : 0)], q = ok ? n % R : 0;
+    cp_async16(bs + e, P + ((size_t)(jid * 4 + sl) * R + q) * wx + ci.off + ci.lo + (ok ? k : 0), ok);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int tile = blockIdx.y * 8 + wp;
+  if (tile * 8 >= Mp) return;
+  const int ngq = min(2, (N - n0 + 7) >> 3);
+  const int ar = lane >> 2, ak = lane & 3;
+  const double2* arow = q0 + ci.q0_off + (size_t)(tile * 8 + ar) * K + ak;
+  double acc[2][4];
+#pragma unroll
+  for (int gq = 0; gq < 2; ++gq) acc[gq][0] = acc[gq][1] = acc[gq][2] = acc[gq][3] = 0.0;
+  const int nks = K >> 2;  // k-steps (a multiple of 4: K = 4 nk4 = 16 nk4 / 4)
+  for (int ks0 = 0; ks0 < nks; ks0 += 8) {
+    double2 av[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) av[u] = ks0 + u < nks ? __ldg(arow + (ks0 + u) * 4) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (ks0 + u < nks) {
+        const double2* br = bs + (size_t)((ks0 + u) * 4 + ak) * P0_COLS + ar;
+#pragma unroll
+        for (int gq = 0; gq < 2; ++gq) {
+          if (gq < ngq) {
+            const double2 bv = br[gq * 8];
+            dmma_f64(acc[gq][0], acc[gq][1], av[u].x, bv.x);
+            dmma_f64(acc[gq][2], acc[gq][3], av[u].x, bv.y);
+            dmma_f64(acc[gq][0], acc[gq][1], -av[u].y, bv.y);
+            dmma_f64(acc[gq][2], acc[gq][3], av[u].y, bv.x);
+          }
+        }
+      }
+    }
+  }
+  // C fragment: row ar of the tile, columns 2 ak, 2 ak + 1 of each group
+  const int m = tile * 8 + ar;
+  if (m >= M) return;
+#pragma unroll
+  for (int gq = 0; gq < 2; ++gq) {
+    if (gq >= ngq) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int n = n0 + 8 * gq + 2 * ak + h;
+      if (n >= N) continue;
+      const int jid = ljobs[jb0 + n / R], q = n % R;
+      const double2 v = make_double2(acc[gq][h], acc[gq][2 + h]);
+      if (m < 4 * w) {
+        const int idx = m / w, j = m - (m / w) * w;
+        tables[((((size_t)jid * Lc + c) * 4 + idx) * R + q) * wmax + j] = v;
+      } else {
+        const int mm = m - 4 * w, kk = mm >> 2, oi = mm & 3;
+        const OJob& jb = jobs[jid];
+        for (int o = 0; o < jb.nout; ++o) {
+          const int orow = jb.orow[o];
+          const int ok_ = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
+          if (ok_ == oi) smp[((size_t)(jid * 4 + o) * R + q) * wx + ci.off + ci.lo + kk] = v;
+        }
+      }
+    }
+  }
+}
+
+cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
+                         const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,
+                         int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st) {
+  if (ngroups == 0 || R == 0) return cudaSuccess;
+  const int mp = (4 * wmax + 4 * kmax + 7) / 8 * 8;
+  const int gy = (mp / 8 + 7) / 8;
+  const int gz = (max_jobs_per_layer * R + P0_COLS - 1) / P0_COLS;
+  const size_t sm = sizeof(double2) * (size_t)(4 * ((kmax + 3) & ~3)) * P0_COLS;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_pass0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_pass0<<<dim3(ngroups * Lc, gy, gz), 256, sm, st>>>(grp, ljobs, jobs, cells, layers, q0, P, tables, smp, R, Lc,
+                                                       wx, wmax);
   return cudaGetLastError();
 }

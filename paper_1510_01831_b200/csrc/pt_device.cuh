@@ -41,6 +41,7 @@ struct CellInfo {
   long long green_off;    // double2 offset into the Green-block pool
   long long lz_off;       // offset into lz/uz pools
   long long gsmp_off;     // double2 offset into the sampled trace-response pool (-1: none)
+  long long q0_off;       // double2 offset into the pass-0 operator pool (-1: none)
 };
 
 // A reference to one panel (segment) of a vector: vec < 0 = absent.

@@ -88,7 +88,11 @@ __host__ __device__ constexpr int k1_jw(int nc) { return nc == 1 ? 5 : (nc == 2 
 size_t inner_smem_bytes(int wmax, int nitems);
 int inner_mg(int wmax);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
-void inner_tprof_dump(const char* tag);  // PT_INNER_TPROF: print and reset CTA 0's segment clocks
+void inner_tprof_dump(const char* tag);
+// first layer-solve pass (no volume source) as a dense product with the offline pass-0 operators
+cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
+                         const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,
+                         int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st);  // PT_INNER_TPROF: print and reset CTA 0's segment clocks
 // smp += trace-source response (sampled Green rows) for every (job, cell, output row, RHS)
 cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                  const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,

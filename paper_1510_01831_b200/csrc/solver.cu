@@ -47,6 +47,8 @@ struct Stage {
   int* ljobs_d = nullptr;
   bool any_panel = false, any_sample = false;
   bool samples_only = true;  // every job's outputs are layer-row samples (no volume output)
+  bool no_volume = true;     // no job has a volume source
+  int* grp_d = nullptr;      // [ngroups][3]: layer, first index into ljobs, job count
   // task cache per active-RHS count
   struct Tasks {
     K1Task* d = nullptr;
@@ -82,6 +84,7 @@ struct pt_ctx {
   CellInfo* cel_d = nullptr;
   double2 *sinv_d = nullptr, *green_d = nullptr, *lz_d = nullptr, *uz_d = nullptr;
   double2* gsmp_d = nullptr;  // sampled trace responses (optional; enables the one-pass layer solve)
+  double2* q0_d = nullptr;    // pass-0 operators (optional; layer solves without volume sources skip K1)
   double2 *tx_d = nullptr, *tz_d = nullptr;
   double* m_d = nullptr;
   // inner item programs
@@ -123,7 +126,7 @@ struct pt_ctx {
   bool prof = false;
   struct EvRec {
     cudaEvent_t a, b;
-    int cls;  // 0 K1, 1 inner, 2 other, 3 sampled trace response (counted as other)
+    int cls;  // 0 K1, 1 inner, 2 other, 3 sampled trace response, 4 pass-0 product (3, 4 counted as other)
     const char* tag;
   };
   const char* cur_tag = "";
@@ -208,6 +211,18 @@ static int finalize_stage(pt_ctx* c, Stage& S) {
       if (jb.pan[s][0].vec >= 0) S.any_panel = true;
     if (jb.nout > 0) S.any_sample = true;
     if (jb.nout <= 0) S.samples_only = false;
+    if (jb.vol) S.no_volume = false;
+  }
+  {
+    std::vector<int> g;
+    for (size_t i = 0; i < S.lgrp.size(); ++i) {
+      const int b = S.lgrp[i].second;
+      const int e = i + 1 < S.lgrp.size() ? S.lgrp[i + 1].second : (int)S.ljobs.size();
+      g.push_back(S.lgrp[i].first);
+      g.push_back(b);
+      g.push_back(e - b);
+    }
+    if (!g.empty() && upload(&S.grp_d, g.data(), g.size())) return PT_CUDA_ERROR;
   }
   if (upload(&S.jobs_d, S.jobs.data(), S.jobs.size())) return PT_CUDA_ERROR;
   if (upload(&S.stage_jobs_d, sj.data(), sj.size())) return PT_CUDA_ERROR;
@@ -689,9 +704,20 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   static const bool no_gsmp = std::getenv("PT_NO_GSMP") != nullptr;
   const bool gpath = c->Lc > 1 && c->gsmp_d && S.samples_only && !no_gsmp;
   kp.s0 = gpath ? 1 : 0;
+  static const bool no_q0 = std::getenv("PT_NO_Q0") != nullptr;
+  const bool qpath = gpath && c->q0_d && S.no_volume && S.any_panel && S.grp_d && !no_q0;
   if (c->Lc > 1) {
     kp.pass = 0;
-    {
+    if (qpath) {  // first pass as one dense product with the offline pass-0 operators (no volume source)
+      LaunchScope ls(c, 4);
+      int maxj = 0;
+      for (size_t i = 0; i < S.lgrp.size(); ++i) {
+        const int e = i + 1 < S.lgrp.size() ? S.lgrp[i + 1].second : (int)S.ljobs.size();
+        maxj = std::max(maxj, e - S.lgrp[i].second);
+      }
+      CK(pass0_launch(S.grp_d, (int)S.lgrp.size(), S.ljobs_d, S.jobs_d, c->cel_d, c->lay_d, c->q0_d, c->P, c->tables,
+                      c->smp, Ract, c->Lc, c->wx, c->wmax, c->wzcmax, maxj, c->st));
+    } else {
       LaunchScope ls(c, 0);
       CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
       c->k1_bytes += T->bytes;
@@ -1149,7 +1175,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     }
     if (stats->timing_ms) stats->timing_ms[0] = ms;
     if (stats->kernel_ms) {
-      double acc[4] = {0, 0, 0, 0};
+      double acc[5] = {0, 0, 0, 0, 0};
       for (const auto& e : c->evs) {
         float t = 0.f;
         cudaEventElapsedTime(&t, e.a, e.b);
@@ -1161,7 +1187,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     }
     if (stage_prof) {  // per (stage, kernel class) device time, launch count
       std::map<std::string, std::pair<double, int>> agg;
-      static const char* cls_name[4] = {"k1", "inner", "glue", "green"};
+      static const char* cls_name[5] = {"k1", "inner", "glue", "green", "pass0"};
       for (const auto& e : c->evs) {
         float t = 0.f;
         cudaEventElapsedTime(&t, e.a, e.b);
@@ -1250,7 +1276,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
     return PT_BAD_ARGUMENT;
   }
   // cells
-  long long soff = 0, goff = 0, zoff = 0, gsoff = 0;
+  long long soff = 0, goff = 0, zoff = 0, gsoff = 0, q0off = 0;
   c->wzcmax = 0;
   std::vector<int> coffs(c->Lc);
   {
@@ -1293,6 +1319,12 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       ci.lz_off = zoff;
       ci.gsmp_off = pb->gsmp ? gsoff : -1;
       gsoff += 16LL * ci.wzc * ci.w;
+      {
+        const int nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3;
+        const long long mp = (4LL * ci.w + 4LL * nk + 7) / 8 * 8;
+        ci.q0_off = pb->q0 ? q0off : -1;
+        q0off += mp * 4 * nk4;
+      }
       soff += (long long)ci.wzc * ci.w * ((ci.w + 3) & ~3);  // blocks padded to a multiple of 4 columns
       goff += 16LL * ((ci.w + 7) / 8) * 8 * ci.w;  // tile-major, rows padded to 8
       zoff += ci.wzc;
@@ -1302,6 +1334,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   CK(cudaMalloc(&c->sinv_d, sizeof(double2) * (size_t)soff));
   CK(cudaMalloc(&c->green_d, sizeof(double2) * (size_t)goff));
   if (pb->gsmp) CK(cudaMalloc(&c->gsmp_d, sizeof(double2) * (size_t)gsoff));
+  if (pb->q0) CK(cudaMalloc(&c->q0_d, sizeof(double2) * (size_t)q0off));
   CK(cudaMalloc(&c->lz_d, sizeof(double2) * (size_t)zoff));
   CK(cudaMalloc(&c->uz_d, sizeof(double2) * (size_t)zoff));
   for (const CellInfo& ci : c->cel) {
@@ -1326,6 +1359,11 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
     if (pb->gsmp)
       CK(cudaMemcpy(c->gsmp_d + ci.gsmp_off, pb->gsmp[id], sizeof(double2) * 16 * (size_t)ci.wzc * ci.w,
                     cudaMemcpyDefault));
+    if (pb->q0) {
+      const int nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3;
+      const long long mp = (4LL * ci.w + 4LL * nk + 7) / 8 * 8;
+      CK(cudaMemcpy(c->q0_d + ci.q0_off, pb->q0[id], sizeof(double2) * (size_t)(mp * 4 * nk4), cudaMemcpyDefault));
+    }
     CK(cudaMemcpy(c->lz_d + ci.lz_off, pb->lz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
     CK(cudaMemcpy(c->uz_d + ci.lz_off, pb->uz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
   }
@@ -1383,7 +1421,7 @@ int pt_destroy(pt_ctx* c) {
   cudaDeviceSynchronize();
   // the process-level allocations are released with the context
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
-  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->lz_d,
+  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->lz_d,
                   (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->items_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
                   (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables,
@@ -1402,6 +1440,7 @@ int pt_destroy(pt_ctx* c) {
     if (st->jobs_d) cudaFree(st->jobs_d);
     if (st->stage_jobs_d) cudaFree(st->stage_jobs_d);
     if (st->ljobs_d) cudaFree(st->ljobs_d);
+    if (st->grp_d) cudaFree(st->grp_d);
   }
   cudaStreamDestroy(c->own_st);
   delete c;

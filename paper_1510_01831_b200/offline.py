@@ -89,6 +89,11 @@ class CellFactors:
     # (wzc, 4 layer trace rows, 4 slots, w): H_c^{-1} (coef_s E_{krow_s}) sampled at every block row
     # and at the layer trace rows 0, 1, n, n+1 -- the trace-source response of the sampled rows
     gsmp: torch.Tensor = None
+    # (M, K) pass-0 operator for layer solves without a volume source: columns (slot s, kept block row k;
+    # each slot block zero-padded to nk4 = roundup(nk, 4))
+    # = lay.coef[s] E_{(k, prow_s)}, rows = the Newton-table block rows (4 x w, order r0 r1 rn rnp) then the
+    # layer trace rows of every kept block row ((k, row) k-major, rows 0, 1, n, n+1); M padded to 8
+    q0: torch.Tensor = None
 
 
 @dataclass
@@ -244,13 +249,15 @@ def _block_solve(sinv, lz, uz, rhs):
     return x
 
 
-def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True):
+def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=None):
     """Offline stage for a partitioned problem (all layers, all cells).
 
     ``grid``/``model``/``pml``/``partition`` follow the reference value types
     (``discretization.py:58-220``, ``subdomain.py:51-73``).
     """
     device = torch.device(device)
+    if q0 is None:
+        q0 = green
     npml, h, omega = grid.npml, grid.h, pml.omega
     cext = _split(grid.nx, Lc)  # partition_layers(sgrid, Lc), nested.py:294-296
     coffs = tuple(int(v) for v in np.concatenate([[0], np.cumsum(cext)[:-1]]))
@@ -300,6 +307,32 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True):
                 # layer trace rows 0, 1, n, n+1 in the cell-local frame (offset npml - 1), every block row
                 jrows = [npml - 1, npml, n + npml - 1, n + npml]
                 gsmp = X[:, :, jrows, :].reshape(len(idxs), wzc, 4, 4, w).contiguous()
+                del X, rhs
+            q0c = [None] * len(idxs)
+            if q0:
+                # responses to the layer slot sources at every block row: K_full = 4 wzc columns
+                rows4 = [int(r) for r in (ckrows[1], ckrows[0], ckrows[3], ckrows[2])]  # r0,r1,rn,rnp
+                jrows = [npml - 1, npml, n + npml - 1, n + npml]
+                kf = torch.arange(wzc, device=device)
+                rhs = torch.zeros((len(idxs), wzc, w, 4 * wzc), dtype=torch.complex128, device=device)
+                for s in range(4):
+                    rhs[:, kf, int(lrows[s]), s * wzc + kf] = complex(lcoefs[s])
+                X = _block_solve(sinv, lz, uz, rhs)
+                del rhs
+                for b, ci in enumerate(idxs):
+                    lo = 0 if ci == 0 else npml
+                    hi = wzc if ci == Lc - 1 else npml + nxc
+                    nk = hi - lo
+                    nk4 = (nk + 3) // 4 * 4  # slot column blocks padded to whole DMMA k-steps
+                    cols = torch.cat([s * wzc + torch.arange(lo, hi, device=device) for s in range(4)])
+                    qt = X[b][rows4][:, :, cols].reshape(4 * w, 4, nk)
+                    qs = X[b][lo:hi][:, jrows][:, :, cols].reshape(4 * nk, 4, nk)
+                    m = 4 * w + 4 * nk
+                    mp = (m + 7) // 8 * 8
+                    q = torch.zeros((mp, 4, nk4), dtype=torch.complex128, device=device)
+                    q[:m, :, :nk] = torch.cat([qt, qs])
+                    q0c[b] = q.reshape(mp, 4 * nk4)
+                del X
             if wzc < 3:
                 raise ValueError("cells need at least 3 block rows (nx_c + 2 npml >= 3)")
             tinv = _twisted_inverses(tw, dg, lz, uz, sinv, device)
@@ -311,6 +344,7 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True):
                     None if gblk is None else gblk[b].contiguous(),
                     ccoefs, ckrows,
                     None if gsmp is None else gsmp[b].contiguous(),
+                    q0c[b],
                 )
         lf.cells = cells
         layers.append(lf)
