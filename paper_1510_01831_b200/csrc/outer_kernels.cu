@@ -314,12 +314,15 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
 // tile x up to 32 columns (4 groups of 8) per warp, A from the operator pool, B from the gathered panels.
 // grid: x = layer group g * Lc + cell, y = chunk of 8 row tiles, z = chunk of 32 columns.
 #define P0_COLS 16  // columns (job, RHS) per CTA: two DMMA column groups of 8
-__global__ void __launch_bounds__(256) k_pass0(const int* __restrict__ grp, const int* __restrict__ ljobs,
-                                               const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
-                                               const LayerInfo* __restrict__ layers, const double2* __restrict__ q0,
-                                               const double2* __restrict__ P, double2* __restrict__ tables,
-                                               double2* __restrict__ smp, int R, int Lc, int wx, int wmax) {
-  extern __shared__ double2 bs[];  // [K][P0_COLS]: the CTA's panel columns
+#define P0_KQ 4      // k parts per row tile (one warp each), summed in shared memory in a fixed order
+__global__ void __launch_bounds__(P0_KQ * 32) k_pass0(const int* __restrict__ grp, const int* __restrict__ ljobs,
+                                                      const OJob* __restrict__ jobs,
+                                                      const CellInfo* __restrict__ cells,
+                                                      const LayerInfo* __restrict__ layers,
+                                                      const double2* __restrict__ q0, const double2* __restrict__ P,
+                                                      double2* __restrict__ tables, double2* __restrict__ smp, int R,
+                                                      int Lc, int wx, int wmax) {
+  __shared__ double part[P0_KQ - 1][2][4][32];
   const int g = blockIdx.x / Lc, c = blockIdx.x - (blockIdx.x / Lc) * Lc;
   const int layer = grp[3 * g], jb0 = grp[3 * g + 1], nj = grp[3 * g + 2];
   const CellInfo& ci = cells[layer * Lc + c];
@@ -328,48 +331,65 @@ __global__ void __launch_bounds__(256) k_pass0(const int* __restrict__ grp, cons
   const int M = 4 * w + 4 * nk, Mp = (M + 7) & ~7;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int N = nj * R, n0 = blockIdx.z * P0_COLS;
-  if (n0 >= N || blockIdx.y * 64 >= Mp) return;
-  // stage B = the CTA's panel columns (zero past nk and past N), 16-byte cp.async
-  for (int e = threadIdx.x; e < K * P0_COLS; e += blockDim.x) {
-    const int col = e % P0_COLS, kr = e / P0_COLS;
-    const int sl = kr / nk4, k = kr - (kr / nk4) * nk4;
-    const int n = n0 + col;
-    const bool ok = n < N && k < nk;
-    const int jid = ljobs[jb0 + (ok ? n / R : 0)], q = ok ? n % R : 0;
-    cp_async16(bs + e, P + ((size_t)(jid * 4 + sl) * R + q) * wx + ci.off + ci.lo + (ok ? k : 0), ok);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const int tile = blockIdx.y * 8 + wp;
-  if (tile * 8 >= Mp) return;
+  const int tile = blockIdx.y;
+  if (n0 >= N || tile * 8 >= Mp) return;
   const int ngq = min(2, (N - n0 + 7) >> 3);
   const int ar = lane >> 2, ak = lane & 3;
   const double2* arow = q0 + ci.q0_off + (size_t)(tile * 8 + ar) * K + ak;
+  const double2* bcol[2];
+  bool bok[2];
+#pragma unroll
+  for (int gq = 0; gq < 2; ++gq) {
+    const int n = n0 + 8 * gq + ar;
+    bok[gq] = n < N;
+    const int jid = ljobs[jb0 + (bok[gq] ? n / R : 0)], q = bok[gq] ? n % R : 0;
+    bcol[gq] = P + ((size_t)(jid * 4) * R + q) * wx + ci.off + ci.lo + ak;
+  }
+  const size_t sstride = (size_t)R * wx;  // slot stride in P
   double acc[2][4];
 #pragma unroll
   for (int gq = 0; gq < 2; ++gq) acc[gq][0] = acc[gq][1] = acc[gq][2] = acc[gq][3] = 0.0;
-  const int nks = K >> 2;  // k-steps (a multiple of 4: K = 4 nk4 = 16 nk4 / 4)
-  for (int ks0 = 0; ks0 < nks; ks0 += 8) {
-    double2 av[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) av[u] = ks0 + u < nks ? __ldg(arow + (ks0 + u) * 4) : make_double2(0.0, 0.0);
+  const int nks = K >> 2, kps = nk4 >> 2;  // k-steps in all / per slot
+  const int kb = wp * nks / P0_KQ, ke = (wp + 1) * nks / P0_KQ;
+  for (int ks0 = kb; ks0 < ke; ks0 += 8) {
+    double2 av[8], bv[8][2];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      if (ks0 + u < nks) {
-        const double2* br = bs + (size_t)((ks0 + u) * 4 + ak) * P0_COLS + ar;
+      const int ks = ks0 + u;
+      const bool kin = ks < ke;
+      const int sl = kin ? ks / kps : 0, kk = (ks - sl * kps) * 4;  // column within the slot block (+ ak)
+      av[u] = kin ? __ldg(arow + ks * 4) : make_double2(0.0, 0.0);
 #pragma unroll
-        for (int gq = 0; gq < 2; ++gq) {
-          if (gq < ngq) {
-            const double2 bv = br[gq * 8];
-            dmma_f64(acc[gq][0], acc[gq][1], av[u].x, bv.x);
-            dmma_f64(acc[gq][2], acc[gq][3], av[u].x, bv.y);
-            dmma_f64(acc[gq][0], acc[gq][1], -av[u].y, bv.y);
-            dmma_f64(acc[gq][2], acc[gq][3], av[u].y, bv.x);
-          }
+      for (int gq = 0; gq < 2; ++gq)
+        bv[u][gq] = (kin && bok[gq] && kk + ak < nk) ? __ldg(bcol[gq] + sl * sstride + kk) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int gq = 0; gq < 2; ++gq) {
+        if (gq < ngq) {
+          dmma_f64(acc[gq][0], acc[gq][1], av[u].x, bv[u][gq].x);
+          dmma_f64(acc[gq][2], acc[gq][3], av[u].x, bv[u][gq].y);
+          dmma_f64(acc[gq][0], acc[gq][1], -av[u].y, bv[u][gq].y);
+          dmma_f64(acc[gq][2], acc[gq][3], av[u].y, bv[u][gq].x);
         }
       }
     }
   }
+  if (wp > 0) {
+#pragma unroll
+    for (int gq = 0; gq < 2; ++gq)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) part[wp - 1][gq][t][lane] = acc[gq][t];
+  }
+  __syncthreads();
+  if (wp > 0) return;
+#pragma unroll
+  for (int p2 = 0; p2 < P0_KQ - 1; ++p2)
+#pragma unroll
+    for (int gq = 0; gq < 2; ++gq)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[gq][t] += part[p2][gq][t][lane];
   // C fragment: row ar of the tile, columns 2 ak, 2 ak + 1 of each group
   const int m = tile * 8 + ar;
   if (m >= M) return;
@@ -403,11 +423,8 @@ cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJ
                          int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st) {
   if (ngroups == 0 || R == 0) return cudaSuccess;
   const int mp = (4 * wmax + 4 * kmax + 7) / 8 * 8;
-  const int gy = (mp / 8 + 7) / 8;
   const int gz = (max_jobs_per_layer * R + P0_COLS - 1) / P0_COLS;
-  const size_t sm = sizeof(double2) * (size_t)(4 * ((kmax + 3) & ~3)) * P0_COLS;
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_pass0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_pass0<<<dim3(ngroups * Lc, gy, gz), 256, sm, st>>>(grp, ljobs, jobs, cells, layers, q0, P, tables, smp, R, Lc,
-                                                       wx, wmax);
+  k_pass0<<<dim3(ngroups * Lc, mp / 8, gz), P0_KQ * 32, 0, st>>>(grp, ljobs, jobs, cells, layers, q0, P, tables, smp,
+                                                                 R, Lc, wx, wmax);
   return cudaGetLastError();
 }
