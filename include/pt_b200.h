@@ -77,6 +77,10 @@ typedef struct {
    * sampled at the Newton-table block rows (4 x w) and the layer trace rows of every kept block
    * row (4 nk); M = roundup(4 w + 4 nk, 8) */
   const double* const* q0;
+  /* optional (NULL: the inner GMRES applies its operator and preconditioner panel by panel):
+   * [L] -> [2][n][n] complex row-major, n = 4 (Lc-1) w: the layer's inner GS preconditioner
+   * and preconditioned operator pre(op(.)) as dense matrices (sie.py:203-329) */
+  const double* const* inner_dense;
 } pt_problem;
 
 typedef struct {

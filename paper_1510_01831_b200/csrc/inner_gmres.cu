@@ -66,6 +66,8 @@ struct InSmem {
   long long* goff;  // [Lc] Green-pool offsets of this layer's cells (staged once)
   int* oph;         // op program phase offsets (staged once)
   int* pph;         // pre program phase offsets (staged once)
+  uint64_t* dbar;   // [2 * DA_NS] dense-apply ring barriers: full[DA_NS], empty[DA_NS]
+  size_t region;    // bytes from tiles to the end of red (the dense-apply ring lives there)
 };
 
 // Execute one program (list of phases) for the active instances of this cluster.
@@ -235,6 +237,115 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
   }
 }
 
+// y[inst][row] = sum_k M[row][k] x[inst][k] for the cluster's active instances, M row-major n x n: the dense
+// inner operators (offline.py:inner_dense_operators).  DMMA m8n8k4 with the (up to 8) instances as N; CTA q
+// takes row tiles [q T / CS, (q+1) T / CS) in chunks of DA_T, its 8 warps split the k-steps, and the partial
+// tiles are summed in shared memory in a fixed warp order (deterministic).  Ends with a cluster barrier.
+// y[inst][row] = sum_k M[row][k] x[inst][k] for the cluster's active instances: the dense inner operators
+// (offline.py:inner_dense_operators), stored DMMA-fragment tile-major (k_dense_tiles).  CTA q takes the row
+// tiles [q T / CS, (q+1) T / CS) in passes of up to DA_T tiles.  A pass streams, chunk by chunk (DA_KC k-steps),
+// its tiles' fragments and the instances' x entries into a shared-memory ring with cp.async.bulk (thread 0
+// produces, every warp releases each slot); warp wp takes k-step wp of each chunk and accumulates all the
+// pass's tiles on DMMA (N = instances); the 8 warps' partial tiles are summed in a fixed order.  `dch` counts
+// the chunks this CTA has streamed so far (ring phases persist across calls).  Ends with a cluster barrier.
+#define DA_T 8
+#define DA_NS 8
+__device__ void dense_apply(const InnerParams& p, const double2* __restrict__ Mt, int n, int job, int r0, int src,
+                            int dst, int nact, const InSmem& S, int q, int CS, unsigned& dch) {
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const int ar = lane >> 2, ak = lane & 3;
+  const int T8 = (n + 7) >> 3, nks = n >> 2;
+  const int t0 = q * T8 / CS, t1 = (q + 1) * T8 / CS;
+  constexpr int XST = DA_KC * 4 + 4;                                // padded x row (double2) per instance
+  const uint32_t abytes = (uint32_t)DA_T * DA_KC * 512u;            // A part of a slot
+  const uint32_t slot_bytes = abytes + 8u * XST * 16u;
+  const int ns = (int)min((size_t)DA_NS, S.region / slot_bytes);
+  unsigned char* ring = reinterpret_cast<unsigned char*>(S.tiles);
+  uint64_t* full = S.dbar;
+  uint64_t* empty = S.dbar + DA_NS;
+  const int nch = (nks + DA_KC - 1) / DA_KC;
+  int rr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rr[i] = i < nact ? r0 + S.act[i] : r0;
+  for (int tc = t0; tc < t1; tc += DA_T) {
+    const int nt = min(DA_T, t1 - tc);
+    const unsigned base = dch;  // global index of this pass's chunk 0
+    // warp 0 streams chunk c of this pass into its slot: lane 0 arms the barrier and copies the tiles of
+    // the pass (one contiguous block in the chunk-major layout), lane i copies the x entries of instance i
+    auto issue = [&](int c) {
+      const unsigned g = base + (unsigned)c;
+      const int sl = (int)(g % (unsigned)ns);
+      const int kc = min(DA_KC, nks - c * DA_KC);
+      unsigned char* sp = ring + (size_t)sl * slot_bytes;
+      if (lane == 0) {
+        if (g >= (unsigned)ns) mbar_wait(&empty[sl], ((g / ns) - 1) & 1);
+        mbar_expect_tx(&full[sl], (uint32_t)(nt * DA_KC * 512 + nact * kc * 64));
+        bulk_g2s(sp, Mt + ((size_t)c * T8 + tc) * DA_KC * 32, (uint32_t)nt * DA_KC * 512u, &full[sl]);
+      }
+      __syncwarp();
+      if (lane < nact)
+        bulk_g2s(sp + abytes + (size_t)lane * XST * 16, vecp(p, job, rr[lane], src) + (size_t)c * DA_KC * 4,
+                 (uint32_t)kc * 64u, &full[sl]);
+    };
+    if (wp == 0)
+      for (int c = 0; c < min(ns - 1, nch); ++c) issue(c);
+    double acc[DA_T][4];
+#pragma unroll
+    for (int t = 0; t < DA_T; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      if (wp == 0 && c + ns - 1 < nch) issue(c + ns - 1);
+      const unsigned g = base + (unsigned)c;
+      const int sl = (int)(g % (unsigned)ns);
+      mbar_wait(&full[sl], (g / ns) & 1);
+      const int kc = min(DA_KC, nks - c * DA_KC);
+      if (wp < kc) {
+        const unsigned char* sp = ring + (size_t)sl * slot_bytes;
+        const double2* xs = reinterpret_cast<const double2*>(sp + abytes);
+        const double2 bv = ar < nact ? xs[ar * XST + wp * 4 + ak] : czero();
+        const double2* af = reinterpret_cast<const double2*>(sp) + wp * 32 + lane;
+#pragma unroll
+        for (int t = 0; t < DA_T; ++t) {
+          if (t < nt) {
+            const double2 av = af[t * DA_KC * 32];
+            dmma_f64(acc[t][0], acc[t][1], av.x, bv.x);
+            dmma_f64(acc[t][2], acc[t][3], av.x, bv.y);
+            dmma_f64(acc[t][0], acc[t][1], -av.y, bv.y);
+            dmma_f64(acc[t][2], acc[t][3], av.y, bv.x);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sl]);
+    }
+    dch = base + (unsigned)nch;
+    __syncthreads();  // every chunk consumed: the ring holds the partial tiles now
+    double* part = reinterpret_cast<double*>(S.tiles);  // [8 warps][DA_T][4][32]
+#pragma unroll
+    for (int t = 0; t < DA_T; ++t)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) part[((wp * DA_T + t) * 4 + v) * 32 + lane] = acc[t][v];
+    __syncthreads();
+    if (wp < nt) {  // warp wp owns tile tc + wp: fixed-order sum over the 8 k parts
+      double c4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int g = 0; g < IN_THREADS / 32; ++g)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) c4[v] += part[((g * DA_T + wp) * 4 + v) * 32 + lane];
+      const int row = (tc + wp) * 8 + ar;
+      if (row < n) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int a = 2 * ak + h;  // instance slot
+          if (a < nact) vecp(p, job, rr[a], dst)[row] = make_double2(c4[h], c4[2 + h]);
+        }
+      }
+    }
+    // the ring's generic-proxy use (partial tiles) must be ordered before the next bulk copies into it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
+  csync();
+}
+
 // rebuild the (cluster-consistent) list of active local instances from global state
 __device__ __forceinline__ void rebuild_active(const InnerParams& p, int job, int r0, int ni, int* act, int* s_nact) {
   if (threadIdx.x == 0) {
@@ -270,7 +381,9 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   S.red = S.pan2 + (size_t)2 * p.wmax * 8;
   double* dred = reinterpret_cast<double*>(S.red + (IN_THREADS / 32) * IN_MG * 8 * 8);
   S.tbar = reinterpret_cast<uint64_t*>(dred + 64);
-  S.act = reinterpret_cast<int*>(S.tbar + 2);
+  S.region = (size_t)(reinterpret_cast<unsigned char*>(dred) - reinterpret_cast<unsigned char*>(S.tiles));
+  S.dbar = S.tbar + 2;
+  S.act = reinterpret_cast<int*>(S.dbar + 2 * DA_NS);
   S.goff = reinterpret_cast<long long*>(S.act + 16);
   S.oph = reinterpret_cast<int*>(S.goff + PT_MAX_LC);
   S.pph = S.oph + 2 * PT_MAX_LC + 2;
@@ -280,6 +393,10 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   if (tid == 0) {
     mbar_init(&S.tbar[0], 1);
     mbar_init(&S.tbar[1], 1);
+    for (int i = 0; i < DA_NS; ++i) {
+      mbar_init(&S.dbar[i], 1);
+      mbar_init(&S.dbar[DA_NS + i], IN_THREADS / 32);
+    }
     fence_mbar_init();
   }
   for (int i = tid; i < p.nitems; i += blockDim.x) S.items[i] = p.items[i];
@@ -313,8 +430,19 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   csync();
   T.tick(8);
 
+  // dense inner operators [pre; pre o op] of this layer, if provided
+  const long long doff = p.layers[layer].dense_off;
+  // the dense path needs two ring slots (DA_T tiles x DA_KC k-steps + 8 x-rows) and the partial tiles
+  const bool dense_ok = S.region >= 2 * ((size_t)DA_T * DA_KC * 512 + 8 * (DA_KC * 4 + 4) * 16) &&
+                        S.region >= (size_t)(IN_THREADS / 32) * DA_T * 4 * 32 * 8;
+  const double2* Dm = (p.dense != nullptr && doff >= 0 && dense_ok) ? p.dense + doff : nullptr;
+  const long long dmat = dense_matrix_elems(n);  // one stored matrix
+  unsigned dch = 0;
   // ---- b = pre(rhs), beta0 = ||b||, V_0 = b / beta0 (krylov.py:61-80)
-  {
+  if (Dm) {
+    dense_apply(p, Dm, n, job, r0, VB, VY, s_nact, S, q, CS, dch);
+    T.tick(3);
+  } else {
     const int vm[3] = {VB, VY, VA};
     run_program(p, job, layer, w, r0, S.pph, p.pre_nph, vm, s_nact, S, q, CS, tphase, T);
   }
@@ -361,7 +489,10 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
       rebuild_active(p, job, r0, ni, S.act, &s_nact);
       break;
     }
-    {
+    if (Dm) {  // w = pre(op(V_j)) as one dense product
+      dense_apply(p, Dm + dmat, n, job, r0, j, j + 1, nact, S, q, CS, dch);
+      T.tick(3);
+    } else {
       const int vm1[3] = {j, VT, VA};
       run_program(p, job, layer, w, r0, S.oph, p.op_nph, vm1, nact, S, q, CS, tphase, T);
       const int vm2[3] = {VT, j + 1, VA};
@@ -537,7 +668,7 @@ int inner_mg(int wmax) { return wmax <= 80 ? 2 : 1; }
 size_t inner_smem_bytes(int wmax, int nitems) {
   const int w = wmax < 8 ? 8 : wmax;
   return (size_t)(2 * 4 * inner_mg(wmax) + 4 + 2) * w * 8 * 16 + (size_t)(IN_THREADS / 32) * IN_MG * 8 * 8 * 16 + 64 * 8 +
-         16 + 64 + PT_MAX_LC * 8 + 2 * (2 * PT_MAX_LC + 2) * 4 + (size_t)nitems * sizeof(IItem) + 128;
+         16 + 2 * DA_NS * 8 + 64 + PT_MAX_LC * 8 + 2 * (2 * PT_MAX_LC + 2) * 4 + (size_t)nitems * sizeof(IItem) + 128;
 }
 
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {

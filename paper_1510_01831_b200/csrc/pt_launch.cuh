@@ -49,6 +49,7 @@ struct InnerParams {
   const OJob* jobs;
   const int* stage_jobs;  // job id per CTA
   const double2* green;
+  const double2* dense;   // dense inner operators (LayerInfo.dense_off), or null: item programs
   const IItem* items;
   const int* op_ph;       // phase begin offsets into items (op_nph + 1 entries)
   int op_nph;
@@ -89,6 +90,13 @@ size_t inner_smem_bytes(int wmax, int nitems);
 int inner_mg(int wmax);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
 void inner_tprof_dump(const char* tag);
+__global__ void k_dense_tiles(const double2* src, double2* dst, int n, int kc);
+#define DA_KC 8  // k-steps per dense-apply chunk (inner_gmres.cu; the stored fragment layout depends on it)
+// double2 size of one stored dense inner matrix (k_dense_tiles layout)
+__host__ __device__ inline long long dense_matrix_elems(long long n) {
+  const long long T8 = (n + 7) / 8, nks = n / 4, nch = (nks + DA_KC - 1) / DA_KC;
+  return nch * T8 * DA_KC * 32;
+}
 // first layer-solve pass (no volume source) as a dense product with the offline pass-0 operators
 cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
                          const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,

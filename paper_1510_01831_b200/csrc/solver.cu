@@ -85,6 +85,7 @@ struct pt_ctx {
   double2 *sinv_d = nullptr, *green_d = nullptr, *lz_d = nullptr, *uz_d = nullptr;
   double2* gsmp_d = nullptr;  // sampled trace responses (optional; enables the one-pass layer solve)
   double2* q0_d = nullptr;    // pass-0 operators (optional; layer solves without volume sources skip K1)
+  double2* dense_d = nullptr; // dense inner operators (optional)
   double2 *tx_d = nullptr, *tz_d = nullptr;
   double* m_d = nullptr;
   // inner item programs
@@ -729,6 +730,8 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     ip.jobs = S.jobs_d;
     ip.stage_jobs = S.stage_jobs_d;
     ip.green = c->green_d;
+    static const bool no_dense = std::getenv("PT_NO_DENSE") != nullptr;
+    ip.dense = no_dense ? nullptr : c->dense_d;
     ip.items = c->items_d;
     ip.op_ph = c->op_ph_d;
     ip.op_nph = c->op_nph;
@@ -1263,6 +1266,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       li.prow[s] = rowv[s];
       li.coef[s] = make_double2(pb->layer_coefs[(l * 4 + s) * 2], pb->layer_coefs[(l * 4 + s) * 2 + 1]);
     }
+    li.dense_off = -1;
     if (li.w > 128) {
       g_err = "layer width n_l + 2 npml exceeds 128 (K1 holds <= 4 rows per lane)";
       return PT_BAD_ARGUMENT;
@@ -1367,6 +1371,31 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
     CK(cudaMemcpy(c->lz_d + ci.lz_off, pb->lz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
     CK(cudaMemcpy(c->uz_d + ci.lz_off, pb->uz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
   }
+  // dense inner operators (optional): [L] x [2][n][n], n = 4 nI w
+  if (pb->inner_dense && c->Lc > 1) {
+    // stored DMMA-fragment tile-major (k_dense_tiles), rows padded to whole 8-row tiles
+    long long doff = 0;
+    for (auto& li : c->lay) {
+      const long long n = 4LL * (c->Lc - 1) * li.w;
+      li.dense_off = doff;
+      doff += 2 * dense_matrix_elems(n);
+    }
+    CK(cudaMalloc(&c->dense_d, sizeof(double2) * (size_t)doff));
+    double2* tmp = nullptr;
+    const long long nmx = 4LL * (c->Lc - 1) * c->wmax;
+    CK(cudaMalloc(&tmp, sizeof(double2) * (size_t)(2 * nmx * nmx)));
+    for (int l = 0; l < c->L; ++l) {
+      const long long n = 4LL * (c->Lc - 1) * c->lay[l].w, me = dense_matrix_elems(n);
+      CK(cudaMemcpy(tmp, pb->inner_dense[l], sizeof(double2) * (size_t)(2 * n * n), cudaMemcpyDefault));
+      for (int m = 0; m < 2; ++m) {
+        k_dense_tiles<<<512, 256>>>(tmp + (size_t)m * n * n, c->dense_d + c->lay[l].dense_off + (size_t)m * me,
+                                    (int)n, DA_KC);
+        CK(cudaGetLastError());
+      }
+      CK(cudaDeviceSynchronize());
+    }
+    cudaFree(tmp);
+  }
   if (upload(&c->lay_d, c->lay.data(), c->lay.size())) return PT_CUDA_ERROR;
   if (upload(&c->cel_d, c->cel.data(), c->cel.size())) return PT_CUDA_ERROR;
   if (upload(&c->tx_d, reinterpret_cast<const double2*>(pb->tx), 3 * (size_t)c->wx)) return PT_CUDA_ERROR;
@@ -1421,7 +1450,7 @@ int pt_destroy(pt_ctx* c) {
   cudaDeviceSynchronize();
   // the process-level allocations are released with the context
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
-  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->lz_d,
+  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->dense_d, (void*)c->lz_d,
                   (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->items_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
                   (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables,

@@ -105,6 +105,8 @@ class LayerFactors:
     coefs: np.ndarray  # (4,) layer-level slot coefficients
     prows: np.ndarray  # (4,) layer rows of the slot sources
     cells: list = field(default_factory=list)
+    # (2, n, n) complex: the inner trace problem's dense preconditioner and pre o op (n = 4 (Lc-1) w)
+    dense: torch.Tensor = None
 
 
 @dataclass
@@ -249,7 +251,96 @@ def _block_solve(sinv, lz, uz, rhs):
     return x
 
 
-def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=None):
+def inner_dense_operators(lf):
+    """Dense inner operators of one layer: ``(Pm, Bm)`` with ``Pm = pre`` and ``Bm = pre o op``.
+
+    ``op`` is ``apply_M_polarized`` (``sie.py:203-228``) and ``pre`` the Gauss-Seidel
+    preconditioner (``sweep_down``, ``upward_reflections``, ``sweep_up``: ``sie.py:272-329``)
+    of the layer's inner trace problem, whose "slabs" are the cells and whose
+    ``boundary_samples`` are the cell Green blocks (``nested.py:113-122``).  The trace
+    vector is ``[down (nI, 2, w); up (nI, 2, w)]`` flattened.  Both maps are linear, so the
+    inner GMRES (``nested.py:134-153``) can apply ``pre(op(v))`` as one dense product.
+    Returns complex128 tensors of shape ``(n, n)``, ``n = 4 nI w``, or ``None`` for Lc == 1.
+    """
+    cells = lf.cells
+    Lc = len(cells)
+    nI = Lc - 1
+    if nI == 0:
+        return None
+    w = lf.w
+    n = 4 * nI * w
+    dev = cells[0].green.device
+    # row-major Green blocks G[c][row jr][slot s]: rows r0, r1, rn, rnp; slots v0, v1, vn, vnp
+    G = [cf.green.transpose(-1, -2) for cf in cells]
+    R0, R1, RN, RNP = 0, 1, 2, 3
+
+    def bs(c, pans, rows):
+        out = []
+        for jr in rows:
+            acc = None
+            for s in range(4):
+                if pans[s] is not None:
+                    t = G[c][jr, s] @ pans[s]
+                    acc = t if acc is None else acc + t
+            out.append(acc)
+        return out
+
+    def unpack(X):
+        return X[: 2 * nI * w].reshape(nI, 2, w, -1), X[2 * nI * w :].reshape(nI, 2, w, -1)
+
+    def op(X):  # sie.py:203-228
+        d, p = unpack(X)
+        od = torch.zeros_like(d)
+        ou = torch.zeros_like(p)
+        for ell in range(1, Lc + 1):
+            top, bot = ell >= 2, ell <= Lc - 1
+            it, ib = ell - 2, ell - 1
+            c = ell - 1
+            if bot:
+                v0 = d[ib - 1, 0] + p[ib - 1, 0] if top else None
+                v1 = d[ib - 1, 1] + p[ib - 1, 1] if top else None
+                wb = bs(c, [v0, v1, p[ib, 0], p[ib, 1]], (RN, RNP))
+                od[ib, 0] = wb[0] - (d[ib, 0] + p[ib, 0])
+                od[ib, 1] = wb[1] - d[ib, 1]
+            if top:
+                vn = p[ib, 0] + d[ib, 0] if bot else None
+                vnp = p[ib, 1] + d[ib, 1] if bot else None
+                wt = bs(c, [d[it, 0], d[it, 1], vn, vnp], (R0, R1))
+                ou[it, 0] = wt[0] - p[it, 0]
+                ou[it, 1] = wt[1] - (d[it, 1] + p[it, 1])
+        return torch.cat([od.reshape(2 * nI * w, -1), ou.reshape(2 * nI * w, -1)])
+
+    def pre(X):  # sie.py:272-329 (kind "gs")
+        v, pv = unpack(X)
+        yd = torch.zeros_like(v)
+        yd[0] = -v[0]
+        for i in range(2, nI + 1):  # sweep_down, slab i-1 = cell i-1, rows n, n+1
+            wv = bs(i - 1, [yd[i - 2, 0], yd[i - 2, 1], None, None], (RN, RNP))
+            yd[i - 1, 0] = wv[0] - v[i - 1, 0]
+            yd[i - 1, 1] = wv[1] - v[i - 1, 1]
+        refl = torch.zeros_like(v)
+        for i in range(1, nI + 1):  # upward_reflections, slab i = cell i, rows 0, 1
+            b0 = yd[i, 0] if i <= nI - 1 else None
+            b1 = yd[i, 1] if i <= nI - 1 else None
+            wv = bs(i, [yd[i - 1, 0], yd[i - 1, 1], b0, b1], (R0, R1))
+            refl[i - 1, 0] = wv[0]
+            refl[i - 1, 1] = wv[1] - yd[i - 1, 1]
+        sv = pv - refl
+        yu = torch.zeros_like(v)
+        yu[nI - 1] = -sv[nI - 1]
+        for i in range(nI - 1, 0, -1):  # sweep_up, slab i = cell i, rows 0, 1
+            wv = bs(i, [None, None, yu[i, 0], yu[i, 1]], (R0, R1))
+            yu[i - 1, 0] = wv[0] - sv[i - 1, 0]
+            yu[i - 1, 1] = wv[1] - sv[i - 1, 1]
+        return torch.cat([yd.reshape(2 * nI * w, -1), yu.reshape(2 * nI * w, -1)])
+
+    eye = torch.eye(n, dtype=torch.complex128, device=dev)
+    Pm = pre(eye)
+    Bm = pre(op(eye))
+    return Pm, Bm
+
+
+def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=None, inner_dense=None):
     """Offline stage for a partitioned problem (all layers, all cells).
 
     ``grid``/``model``/``pml``/``partition`` follow the reference value types
@@ -258,6 +349,8 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
     device = torch.device(device)
     if q0 is None:
         q0 = green
+    if inner_dense is None:
+        inner_dense = green
     npml, h, omega = grid.npml, grid.h, pml.omega
     cext = _split(grid.nx, Lc)  # partition_layers(sgrid, Lc), nested.py:294-296
     coffs = tuple(int(v) for v in np.concatenate([[0], np.cumsum(cext)[:-1]]))
@@ -347,6 +440,10 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
                     q0c[b],
                 )
         lf.cells = cells
+        if green and inner_dense:
+            ops = inner_dense_operators(lf)
+            if ops is not None:
+                lf.dense = torch.stack(ops).contiguous()
         layers.append(lf)
     tx = axis_tridiag(pml, grid.nx, h)
     tz = axis_tridiag(pml, grid.nz, h)
