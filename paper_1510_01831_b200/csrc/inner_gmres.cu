@@ -296,7 +296,10 @@ __device__ void dense_apply(const InnerParams& p, const double2* __restrict__ Mt
       if (wp == 0 && c + ns - 1 < nch) issue(c + ns - 1);
       const unsigned g = base + (unsigned)c;
       const int sl = (int)(g % (unsigned)ns);
+      const bool tw = p.tprof && blockIdx.x == 0 && tid == 32;  // warp 1: time spent waiting for data
+      const long long tw0 = tw ? clock64() : 0;
       mbar_wait(&full[sl], (g / ns) & 1);
+      if (tw) atomicAdd((unsigned long long*)&g_in_t[14], (unsigned long long)(clock64() - tw0));
       const int kc = min(DA_KC, nks - c * DA_KC);
       if (wp < kc) {
         const unsigned char* sp = ring + (size_t)sl * slot_bytes;
@@ -717,7 +720,8 @@ void inner_tprof_dump(const char* tag) {
   cudaMemcpyFromSymbol(t, g_in_t, sizeof(t));
   fprintf(stderr, "inner tprof [%s] (cycles, CTA 0): setup %lld tiles+prefetch %lld gather %lld tilewait %lld dmma %lld "
           "combine %lld cluster-bar %lld arnoldi %lld rest %lld final %lld | iterations %lld total %lld | bookkeeping %lld "
-          "tile-issue %lld\n", tag, t[8], t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[9], t[10], t[11], t[12], t[13]);
+          "tile-issue %lld | dense data-wait (warp 1) %lld\n", tag, t[8], t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[9], t[10],
+          t[11], t[12], t[13], t[14]);
   long long z[16] = {0};
   cudaMemcpyToSymbol(g_in_t, z, sizeof(z));
 }
