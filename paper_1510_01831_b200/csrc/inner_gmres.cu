@@ -250,23 +250,22 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
 // the chunks this CTA has streamed so far (ring phases persist across calls).  Ends with a cluster barrier.
 #define DA_T 8
 #define DA_NS 8
-__device__ void dense_apply(const InnerParams& p, const double2* __restrict__ Mt, int n, int job, int r0, int src,
-                            int dst, int nact, const InSmem& S, int q, int CS, unsigned& dch) {
+// One streaming pass over row tiles [t0, t1) of M for the instances rr[0..nact): see dense_apply.
+// ring/region: the shared-memory ring; dbar: DA_NS full + DA_NS empty barriers; red: partial tiles
+// (>= 8 warps x DA_T x 4 x 32 doubles, may alias the ring).
+__device__ void dense_pass(const InnerParams& p, const double2* __restrict__ Mt, int n, int job, const int* rr,
+                           int nact, int src, int dst, int t0, int t1, unsigned char* ring, size_t region,
+                           uint64_t* dbar, unsigned& dch) {
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   const int ar = lane >> 2, ak = lane & 3;
   const int T8 = (n + 7) >> 3, nks = n >> 2;
-  const int t0 = q * T8 / CS, t1 = (q + 1) * T8 / CS;
   constexpr int XST = DA_KC * 4 + 4;                                // padded x row (double2) per instance
   const uint32_t abytes = (uint32_t)DA_T * DA_KC * 512u;            // A part of a slot
   const uint32_t slot_bytes = abytes + 8u * XST * 16u;
-  const int ns = (int)min((size_t)DA_NS, S.region / slot_bytes);
-  unsigned char* ring = reinterpret_cast<unsigned char*>(S.tiles);
-  uint64_t* full = S.dbar;
-  uint64_t* empty = S.dbar + DA_NS;
+  const int ns = (int)min((size_t)DA_NS, region / slot_bytes);
+  uint64_t* full = dbar;
+  uint64_t* empty = dbar + DA_NS;
   const int nch = (nks + DA_KC - 1) / DA_KC;
-  int rr[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) rr[i] = i < nact ? r0 + S.act[i] : r0;
   for (int tc = t0; tc < t1; tc += DA_T) {
     const int nt = min(DA_T, t1 - tc);
     const unsigned base = dch;  // global index of this pass's chunk 0
@@ -322,7 +321,7 @@ __device__ void dense_apply(const InnerParams& p, const double2* __restrict__ Mt
     }
     dch = base + (unsigned)nch;
     __syncthreads();  // every chunk consumed: the ring holds the partial tiles now
-    double* part = reinterpret_cast<double*>(S.tiles);  // [8 warps][DA_T][4][32]
+    double* part = reinterpret_cast<double*>(ring);  // [8 warps][DA_T][4][32]
 #pragma unroll
     for (int t = 0; t < DA_T; ++t)
 #pragma unroll
@@ -346,7 +345,206 @@ __device__ void dense_apply(const InnerParams& p, const double2* __restrict__ Mt
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
   }
+}
+
+// Cluster version: CTA q of the cluster takes row tiles [q T / CS, (q+1) T / CS); ends with a cluster barrier.
+__device__ void dense_apply(const InnerParams& p, const double2* __restrict__ Mt, int n, int job, int r0, int src,
+                            int dst, int nact, const InSmem& S, int q, int CS, unsigned& dch) {
+  const int T8 = (n + 7) >> 3;
+  int rr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rr[i] = i < nact ? r0 + S.act[i] : r0;
+  dense_pass(p, Mt, n, job, rr, nact, src, dst, q * T8 / CS, (q + 1) * T8 / CS, reinterpret_cast<unsigned char*>(S.tiles),
+             S.region, S.dbar, dch);
   csync();
+}
+
+// ---- per-instance GMRES steps (krylov.py:53-135), executed by the instance's owner CTA
+
+// b = Y = pre(rhs): beta0 = ||b||, V_0 = b / beta0, Givens rhs g[0] = beta0, state
+__device__ void instance_init(const InnerParams& p, int job, int r, int n, int VY, double* dred) {
+  const int tid = threadIdx.x;
+  const size_t hld = (size_t)p.cap + 1;
+  const double2* Y = vecp(p, job, r, VY);
+  double ss = 0.0;
+  for (int e = tid; e < n; e += blockDim.x) {
+    const double2 y = ld_cg(Y + e);
+    ss += y.x * y.x + y.y * y.y;
+  }
+  ss = block_sum(ss, dred);
+  const double b0 = sqrt(ss);
+  double2* V0 = vecp(p, job, r, 0);
+  if (b0 != 0.0)
+    for (int e = tid; e < n; e += blockDim.x) {
+      const double2 y = ld_cg(Y + e);
+      V0[e] = make_double2(y.x / b0, y.y / b0);
+    }
+  if (tid == 0) {
+    double2* g = p.hess + (size_t)(job * p.R + r) * p.hstride + hld * p.cap;
+    g[0] = make_double2(b0, 0.0);
+    p.beta0[job * p.R + r] = b0;
+    p.state[job * p.R + r] = b0 == 0.0 ? 1 : 0;
+    p.iters[job * p.R + r] = b0 == 0.0 ? 0 : -1;
+  }
+  __syncthreads();
+}
+
+// MGS Arnoldi + complex Givens for instance r at step j (krylov.py:89-127): W = V_{j+1} holds pre(op(V_j))
+__device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, int n, double* dred) {
+  const int tid = threadIdx.x;
+  const size_t hld = (size_t)p.cap + 1;
+  auto Hp = [&](int rr_) { return p.hess + (size_t)(job * p.R + rr_) * p.hstride; };
+  double2* W = vecp(p, job, r, j + 1);
+  double2* H = Hp(r);
+  double2* col = H + (size_t)j * hld;
+  double ss = 0.0;
+  constexpr int EPT = 8;  // register-resident w for n <= EPT * IN_THREADS
+  if (n <= EPT * IN_THREADS) {
+    double2 wv[EPT];
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+      const int e = tid + t * IN_THREADS;
+      wv[t] = e < n ? ld_cg(W + e) : czero();
+    }
+    for (int i = 0; i <= j; ++i) {
+      const double2* Vi = vecp(p, job, r, i);
+      double2 vv[EPT];
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int t = 0; t < EPT; ++t) {
+        const int e = tid + t * IN_THREADS;
+        vv[t] = e < n ? ld_cg(Vi + e) : czero();
+        const double2 c = cconjmul(vv[t], wv[t]);
+        sr += c.x;
+        si += c.y;
+      }
+      const double2 h = block_sum2(sr, si, dred);
+      if (tid == 0) col[i] = h;
+#pragma unroll
+      for (int t = 0; t < EPT; ++t) wv[t] = csub(wv[t], cmul(h, vv[t]));
+    }
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+      const int e = tid + t * IN_THREADS;
+      if (e < n) W[e] = wv[t];
+      ss += wv[t].x * wv[t].x + wv[t].y * wv[t].y;
+    }
+  } else {
+    for (int i = 0; i <= j; ++i) {
+      const double2* Vi = vecp(p, job, r, i);
+      double sr = 0.0, si = 0.0;
+      for (int e = tid; e < n; e += blockDim.x) {
+        const double2 c = cconjmul(ld_cg(Vi + e), ld_cg(W + e));
+        sr += c.x;
+        si += c.y;
+      }
+      const double2 h = block_sum2(sr, si, dred);
+      if (tid == 0) col[i] = h;
+      for (int e = tid; e < n; e += blockDim.x) W[e] = csub(ld_cg(W + e), cmul(h, ld_cg(Vi + e)));
+      __syncthreads();
+    }
+    for (int e = tid; e < n; e += blockDim.x) {
+      const double2 x = W[e];
+      ss += x.x * x.x + x.y * x.y;
+    }
+  }
+  ss = block_sum(ss, dred);
+  const double hn = sqrt(ss);
+  __shared__ int s_st;
+  if (tid == 0) {
+    double2* g = H + hld * p.cap;
+    double2* cs = g + (p.cap + 1);
+    double2* sn = cs + p.cap;
+    col[j + 1] = make_double2(hn, 0.0);
+    for (int i = 0; i < j; ++i) {
+      const double2 t = cadd(cmul(cs[i], col[i]), cmul(sn[i], col[i + 1]));
+      const double2 nsc = make_double2(-sn[i].x, sn[i].y);  // -conj(sn)
+      const double2 csc = make_double2(cs[i].x, -cs[i].y);  // conj(cs)
+      col[i + 1] = cadd(cmul(nsc, col[i]), cmul(csc, col[i + 1]));
+      col[i] = t;
+    }
+    const double aa = hypot(col[j].x, col[j].y);
+    const double d = sqrt(aa * aa + hn * hn);
+    int st = 0;  // 0 continue, 1 converged, 2 failed
+    if (d == 0.0) {
+      st = 2;
+      atomicMax(p.err, 3);
+    } else {
+      const double2 c = make_double2(col[j].x / d, -col[j].y / d);
+      const double2 s = make_double2(hn / d, 0.0);
+      cs[j] = c;
+      sn[j] = s;
+      col[j] = cadd(cmul(c, col[j]), make_double2(s.x * hn, 0.0));
+      const double2 gj = g[j];
+      g[j + 1] = cmul(make_double2(-s.x, s.y), gj);
+      g[j] = cmul(c, gj);
+      const double res = hypot(g[j + 1].x, g[j + 1].y) / p.beta0[job * p.R + r];
+      if (hn == 0.0) {
+        st = res > p.ktol ? 2 : 1;  // happy breakdown (krylov.py:116-124)
+        if (st == 2) atomicMax(p.err, 3);
+      } else if (res <= p.ktol) {
+        st = 1;
+      } else if (j + 1 == p.max_iter) {
+        st = 2;
+        atomicMax(p.err, 2);  // InnerSolveError (nested.py:148-152)
+      }
+    }
+    s_st = st;
+    p.state[job * p.R + r] = st;
+    if (st != 0) p.iters[job * p.R + r] = st == 1 ? j + 1 : -1;
+  }
+  __syncthreads();
+  if (s_st == 0)  // V_{j+1} = w / hn (krylov.py:125)
+    for (int e = tid; e < n; e += blockDim.x) {
+      const double2 x = W[e];
+      W[e] = make_double2(x.x / hn, x.y / hn);
+    }
+  __syncthreads();
+}
+
+// x = V_k y (back substitution on the triangularized Hessenberg), traces = down + up (nested.py:153),
+// TouchCounter accounting (nested.py:54-73); yv: shared scratch of >= cap double2
+__device__ void instance_final(const InnerParams& p, int job, int r, int n, int w, double2* yv) {
+  const int tid = threadIdx.x;
+  const int nIc = p.Lc - 1;
+  const size_t hld = (size_t)p.cap + 1;
+  auto Hp = [&](int rr_) { return p.hess + (size_t)(job * p.R + rr_) * p.hstride; };
+  const int k = p.iters[job * p.R + r];
+  if (tid == 0 && k > 0) {
+    const double2* H = Hp(r);
+    const double2* g = H + hld * p.cap;
+    for (int i = k - 1; i >= 0; --i) {
+      double2 s = czero();
+      for (int m = i + 1; m < k; ++m) cfma(s, H[(size_t)m * hld + i], yv[m]);
+      const double2 num = csub(g[i], s);
+      const double2 den = H[(size_t)i * hld + i];
+      const double dd = den.x * den.x + den.y * den.y;
+      yv[i] = make_double2((num.x * den.x + num.y * den.y) / dd, (num.y * den.x - num.x * den.y) / dd);
+    }
+  }
+  __syncthreads();
+  const int half = n / 2;
+  double2* out = p.tr + (size_t)(job * p.R + r) * nIc * 2 * p.wmax;
+  for (int e = tid; e < half; e += blockDim.x) {
+    double2 xd = czero(), xu = czero();
+    for (int i = 0; i < k; ++i) {
+      const double2* Vi = vecp(p, job, r, i);
+      cfma(xd, ld_cg(Vi + e), yv[i]);
+      cfma(xu, ld_cg(Vi + half + e), yv[i]);
+    }
+    const int seg = e / w, jj = e - seg * w;
+    out[(size_t)seg * p.wmax + jj] = cadd(xd, xu);
+  }
+  // ---- accounting: TouchCounter.total equivalent (nested.py:54-73)
+  if (tid == 0 && k >= 0) {
+    atomicAdd(&p.hist[min(k, PT_HIST - 1)], 1);
+    atomicAdd(&p.counters[0], (unsigned long long)k);
+    const unsigned long long t =
+        ((unsigned long long)(k + 1) * p.pre_blocks + (unsigned long long)k * p.op_blocks) * w * w;
+    atomicAdd(&p.counters[1], t);
+    atomicAdd(&p.counters[2], 1ULL);
+  }
+  __syncthreads();
 }
 
 // rebuild the (cluster-consistent) list of active local instances from global state
@@ -411,8 +609,6 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   T.on = p.tprof && blockIdx.x == 0 && tid == 0;
   T.start();
   const int VB = p.cap + 1, VY = p.cap + 2, VT = p.cap + 3, VA = p.cap + 4;
-  const size_t hld = (size_t)p.cap + 1;
-  auto Hp = [&](int r) { return p.hess + (size_t)(job * p.R + r) * p.hstride; };
 
   // ---- rhs_pol from the Newton tables (sie.py:230-242, negated); elements split over the cluster
   for (int l = 0; l < ni; ++l) {
@@ -449,31 +645,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
     const int vm[3] = {VB, VY, VA};
     run_program(p, job, layer, w, r0, S.pph, p.pre_nph, vm, s_nact, S, q, CS, tphase, T);
   }
-  for (int l = q; l < ni; l += CS) {
-    const int r = r0 + l;
-    const double2* Y = vecp(p, job, r, VY);
-    double ss = 0.0;
-    for (int e = tid; e < n; e += blockDim.x) {
-      const double2 y = ld_cg(Y + e);
-      ss += y.x * y.x + y.y * y.y;
-    }
-    ss = block_sum(ss, dred);
-    const double b0 = sqrt(ss);
-    double2* V0 = vecp(p, job, r, 0);
-    if (b0 != 0.0)
-      for (int e = tid; e < n; e += blockDim.x) {
-        const double2 y = ld_cg(Y + e);
-        V0[e] = make_double2(y.x / b0, y.y / b0);
-      }
-    if (tid == 0) {
-      double2* g = Hp(r) + hld * p.cap;
-      g[0] = make_double2(b0, 0.0);
-      p.beta0[job * p.R + r] = b0;
-      p.state[job * p.R + r] = b0 == 0.0 ? 1 : 0;
-      p.iters[job * p.R + r] = b0 == 0.0 ? 0 : -1;
-    }
-    __syncthreads();
-  }
+  for (int l = q; l < ni; l += CS) instance_init(p, job, r0 + l, n, VY, dred);
   csync();
   rebuild_active(p, job, r0, ni, S.act, &s_nact);
 
@@ -506,113 +678,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
     for (int a = 0; a < nact; ++a) {
       const int l = S.act[a];
       if (l % CS != q) continue;
-      const int r = r0 + l;
-      double2* W = vecp(p, job, r, j + 1);
-      double2* H = Hp(r);
-      double2* col = H + (size_t)j * hld;
-      double ss = 0.0;
-      constexpr int EPT = 8;  // register-resident w for n <= EPT * IN_THREADS
-      if (n <= EPT * IN_THREADS) {
-        double2 wv[EPT];
-#pragma unroll
-        for (int t = 0; t < EPT; ++t) {
-          const int e = tid + t * IN_THREADS;
-          wv[t] = e < n ? ld_cg(W + e) : czero();
-        }
-        for (int i = 0; i <= j; ++i) {
-          const double2* Vi = vecp(p, job, r, i);
-          double2 vv[EPT];
-          double sr = 0.0, si = 0.0;
-#pragma unroll
-          for (int t = 0; t < EPT; ++t) {
-            const int e = tid + t * IN_THREADS;
-            vv[t] = e < n ? ld_cg(Vi + e) : czero();
-            const double2 c = cconjmul(vv[t], wv[t]);
-            sr += c.x;
-            si += c.y;
-          }
-          const double2 h = block_sum2(sr, si, dred);
-          if (tid == 0) col[i] = h;
-#pragma unroll
-          for (int t = 0; t < EPT; ++t) wv[t] = csub(wv[t], cmul(h, vv[t]));
-        }
-#pragma unroll
-        for (int t = 0; t < EPT; ++t) {
-          const int e = tid + t * IN_THREADS;
-          if (e < n) W[e] = wv[t];
-          ss += wv[t].x * wv[t].x + wv[t].y * wv[t].y;
-        }
-      } else {
-        for (int i = 0; i <= j; ++i) {
-          const double2* Vi = vecp(p, job, r, i);
-          double sr = 0.0, si = 0.0;
-          for (int e = tid; e < n; e += blockDim.x) {
-            const double2 c = cconjmul(ld_cg(Vi + e), ld_cg(W + e));
-            sr += c.x;
-            si += c.y;
-          }
-          const double2 h = block_sum2(sr, si, dred);
-          if (tid == 0) col[i] = h;
-          for (int e = tid; e < n; e += blockDim.x) W[e] = csub(ld_cg(W + e), cmul(h, ld_cg(Vi + e)));
-          __syncthreads();
-        }
-        for (int e = tid; e < n; e += blockDim.x) {
-          const double2 x = W[e];
-          ss += x.x * x.x + x.y * x.y;
-        }
-      }
-      ss = block_sum(ss, dred);
-      const double hn = sqrt(ss);
-      __shared__ int s_st;
-      if (tid == 0) {
-        double2* g = H + hld * p.cap;
-        double2* cs = g + (p.cap + 1);
-        double2* sn = cs + p.cap;
-        col[j + 1] = make_double2(hn, 0.0);
-        for (int i = 0; i < j; ++i) {
-          const double2 t = cadd(cmul(cs[i], col[i]), cmul(sn[i], col[i + 1]));
-          const double2 nsc = make_double2(-sn[i].x, sn[i].y);  // -conj(sn)
-          const double2 csc = make_double2(cs[i].x, -cs[i].y);  // conj(cs)
-          col[i + 1] = cadd(cmul(nsc, col[i]), cmul(csc, col[i + 1]));
-          col[i] = t;
-        }
-        const double aa = hypot(col[j].x, col[j].y);
-        const double d = sqrt(aa * aa + hn * hn);
-        int st = 0;  // 0 continue, 1 converged, 2 failed
-        if (d == 0.0) {
-          st = 2;
-          atomicMax(p.err, 3);
-        } else {
-          const double2 c = make_double2(col[j].x / d, -col[j].y / d);
-          const double2 s = make_double2(hn / d, 0.0);
-          cs[j] = c;
-          sn[j] = s;
-          col[j] = cadd(cmul(c, col[j]), make_double2(s.x * hn, 0.0));
-          const double2 gj = g[j];
-          g[j + 1] = cmul(make_double2(-s.x, s.y), gj);
-          g[j] = cmul(c, gj);
-          const double res = hypot(g[j + 1].x, g[j + 1].y) / p.beta0[job * p.R + r];
-          if (hn == 0.0) {
-            st = res > p.ktol ? 2 : 1;  // happy breakdown (krylov.py:116-124)
-            if (st == 2) atomicMax(p.err, 3);
-          } else if (res <= p.ktol) {
-            st = 1;
-          } else if (j + 1 == p.max_iter) {
-            st = 2;
-            atomicMax(p.err, 2);  // InnerSolveError (nested.py:148-152)
-          }
-        }
-        s_st = st;
-        p.state[job * p.R + r] = st;
-        if (st != 0) p.iters[job * p.R + r] = st == 1 ? j + 1 : -1;
-      }
-      __syncthreads();
-      if (s_st == 0)  // V_{j+1} = w / hn (krylov.py:125)
-        for (int e = tid; e < n; e += blockDim.x) {
-          const double2 x = W[e];
-          W[e] = make_double2(x.x / hn, x.y / hn);
-        }
-      __syncthreads();
+      instance_arnoldi(p, job, r0 + l, j, n, dred);
     }
     T.tick(6);
     csync();
@@ -622,46 +688,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   }
 
   // ---- x = V_k y, traces = down + up (nested.py:153), owner CTA per instance
-  double2* yv = S.pan;  // reuse smem: y[cap]
-  for (int l = q; l < ni; l += CS) {
-    const int r = r0 + l;
-    const int k = p.iters[job * p.R + r];
-    if (tid == 0 && k > 0) {
-      const double2* H = Hp(r);
-      const double2* g = H + hld * p.cap;
-      for (int i = k - 1; i >= 0; --i) {
-        double2 s = czero();
-        for (int m = i + 1; m < k; ++m) cfma(s, H[(size_t)m * hld + i], yv[m]);
-        const double2 num = csub(g[i], s);
-        const double2 den = H[(size_t)i * hld + i];
-        const double dd = den.x * den.x + den.y * den.y;
-        yv[i] = make_double2((num.x * den.x + num.y * den.y) / dd, (num.y * den.x - num.x * den.y) / dd);
-      }
-    }
-    __syncthreads();
-    const int half = n / 2;
-    double2* out = p.tr + (size_t)(job * p.R + r) * nIc * 2 * p.wmax;
-    for (int e = tid; e < half; e += blockDim.x) {
-      double2 xd = czero(), xu = czero();
-      for (int i = 0; i < k; ++i) {
-        const double2* Vi = vecp(p, job, r, i);
-        cfma(xd, ld_cg(Vi + e), yv[i]);
-        cfma(xu, ld_cg(Vi + half + e), yv[i]);
-      }
-      const int seg = e / w, jj = e - seg * w;
-      out[(size_t)seg * p.wmax + jj] = cadd(xd, xu);
-    }
-    // ---- accounting: TouchCounter.total equivalent (nested.py:54-73)
-    if (tid == 0 && k >= 0) {
-      atomicAdd(&p.hist[min(k, PT_HIST - 1)], 1);
-      atomicAdd(&p.counters[0], (unsigned long long)k);
-      const unsigned long long t =
-          ((unsigned long long)(k + 1) * p.pre_blocks + (unsigned long long)k * p.op_blocks) * w * w;
-      atomicAdd(&p.counters[1], t);
-      atomicAdd(&p.counters[2], 1ULL);
-    }
-    __syncthreads();
-  }
+  for (int l = q; l < ni; l += CS) instance_final(p, job, r0 + l, n, w, S.pan);
   T.tick(9);
   if (T.on) atomicAdd((unsigned long long*)&g_in_t[11], (unsigned long long)(clock64() - tk_entry));
 }
