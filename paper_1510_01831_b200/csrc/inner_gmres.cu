@@ -21,6 +21,7 @@
 // and x = V y of an instance run on one CTA of the cluster, so reductions are
 // deterministic and need no cross-CTA traffic.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -250,88 +251,111 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
 // the chunks this CTA has streamed so far (ring phases persist across calls).  Ends with a cluster barrier.
 #define DA_T 8
 #define DA_NS 8
+#define GV_MAX 128  // Arnoldi steps whose Givens state is staged in shared memory
 // One streaming pass over row tiles [t0, t1) of M for the instances rr[0..nact): see dense_apply.
-// ring/region: the shared-memory ring; dbar: DA_NS full + DA_NS empty barriers; red: partial tiles
-// (>= 8 warps x DA_T x 4 x 32 doubles, may alias the ring).
+// ring/region: the shared-memory ring; dbar: DA_NS full + DA_NS empty barriers; the partial tiles reuse the
+// ring.  A ring slot holds SC stored chunks (SC = DA_T / nt, at most scmax) of the pass's tiles plus the
+// instances' x entries for those k-steps, so passes over few tiles still move large slots.
+__device__ __forceinline__ uint32_t dense_slot_bytes(int scmax) {
+  return (uint32_t)DA_T * DA_KC * 512u + 8u * (uint32_t)(scmax * DA_KC * 4 + 4) * 16u;
+}
 __device__ void dense_pass(const InnerParams& p, const double2* __restrict__ Mt, int n, int job, const int* rr,
                            int nact, int src, int dst, int t0, int t1, unsigned char* ring, size_t region,
-                           uint64_t* dbar, unsigned& dch) {
+                           uint64_t* dbar, unsigned& dch, int scmax) {
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   const int ar = lane >> 2, ak = lane & 3;
   const int T8 = (n + 7) >> 3, nks = n >> 2;
-  constexpr int XST = DA_KC * 4 + 4;                                // padded x row (double2) per instance
+  const int XST = scmax * DA_KC * 4 + 4;                            // padded x row (double2) per instance
   const uint32_t abytes = (uint32_t)DA_T * DA_KC * 512u;            // A part of a slot
-  const uint32_t slot_bytes = abytes + 8u * XST * 16u;
+  const uint32_t slot_bytes = dense_slot_bytes(scmax);
   const int ns = (int)min((size_t)DA_NS, region / slot_bytes);
   uint64_t* full = dbar;
   uint64_t* empty = dbar + DA_NS;
-  const int nch = (nks + DA_KC - 1) / DA_KC;
+  const int nchs = (nks + DA_KC - 1) / DA_KC;  // stored chunks
   for (int tc = t0; tc < t1; tc += DA_T) {
     const int nt = min(DA_T, t1 - tc);
-    const unsigned base = dch;  // global index of this pass's chunk 0
-    // warp 0 streams chunk c of this pass into its slot: lane 0 arms the barrier and copies the tiles of
-    // the pass (one contiguous block in the chunk-major layout), lane i copies the x entries of instance i
+    const int sc = max(1, min(scmax, DA_T / nt));
+    const int kslot = sc * DA_KC;                  // k-steps per slot
+    const int nsl = (nks + kslot - 1) / kslot;     // slots of this pass
+    const unsigned base = dch;  // global index of this pass's slot 0
+    // warp 0 fills slot c of this pass: lane 0 arms the barrier, lanes < nsub copy one stored chunk of the
+    // pass's tiles each (contiguous in the chunk-major layout), lanes < nact copy instance x entries
     auto issue = [&](int c) {
       const unsigned g = base + (unsigned)c;
       const int sl = (int)(g % (unsigned)ns);
-      const int kc = min(DA_KC, nks - c * DA_KC);
+      const int k0 = c * kslot, kx = min(kslot, nks - k0);
+      const int nsub = min(sc, nchs - c * sc);
       unsigned char* sp = ring + (size_t)sl * slot_bytes;
       if (lane == 0) {
         if (g >= (unsigned)ns) mbar_wait(&empty[sl], ((g / ns) - 1) & 1);
-        mbar_expect_tx(&full[sl], (uint32_t)(nt * DA_KC * 512 + nact * kc * 64));
-        bulk_g2s(sp, Mt + ((size_t)c * T8 + tc) * DA_KC * 32, (uint32_t)nt * DA_KC * 512u, &full[sl]);
+        mbar_expect_tx(&full[sl], (uint32_t)(nsub * nt * DA_KC * 512 + nact * kx * 64));
       }
       __syncwarp();
+      if (lane < nsub)
+        bulk_g2s(sp + (size_t)lane * nt * DA_KC * 512, Mt + ((size_t)(c * sc + lane) * T8 + tc) * DA_KC * 32,
+                 (uint32_t)nt * DA_KC * 512u, &full[sl]);
       if (lane < nact)
-        bulk_g2s(sp + abytes + (size_t)lane * XST * 16, vecp(p, job, rr[lane], src) + (size_t)c * DA_KC * 4,
-                 (uint32_t)kc * 64u, &full[sl]);
+        bulk_g2s(sp + abytes + (size_t)lane * XST * 16, vecp(p, job, rr[lane], src) + (size_t)k0 * 4,
+                 (uint32_t)kx * 64u, &full[sl]);
     };
     if (wp == 0)
-      for (int c = 0; c < min(ns - 1, nch); ++c) issue(c);
+      for (int c = 0; c < min(ns - 1, nsl); ++c) issue(c);
     double acc[DA_T][4];
 #pragma unroll
     for (int t = 0; t < DA_T; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
-    for (int c = 0; c < nch; ++c) {
-      if (wp == 0 && c + ns - 1 < nch) issue(c + ns - 1);
+    for (int c = 0; c < nsl; ++c) {
+      if (wp == 0 && c + ns - 1 < nsl) issue(c + ns - 1);
       const unsigned g = base + (unsigned)c;
       const int sl = (int)(g % (unsigned)ns);
       const bool tw = p.tprof && blockIdx.x == 0 && tid == 32;  // warp 1: time spent waiting for data
       const long long tw0 = tw ? clock64() : 0;
       mbar_wait(&full[sl], (g / ns) & 1);
       if (tw) atomicAdd((unsigned long long*)&g_in_t[14], (unsigned long long)(clock64() - tw0));
-      const int kc = min(DA_KC, nks - c * DA_KC);
-      if (wp < kc) {
-        const unsigned char* sp = ring + (size_t)sl * slot_bytes;
-        const double2* xs = reinterpret_cast<const double2*>(sp + abytes);
-        const double2 bv = ar < nact ? xs[ar * XST + wp * 4 + ak] : czero();
-        const double2* af = reinterpret_cast<const double2*>(sp) + wp * 32 + lane;
-#pragma unroll
-        for (int t = 0; t < DA_T; ++t) {
-          if (t < nt) {
-            const double2 av = af[t * DA_KC * 32];
-            dmma_f64(acc[t][0], acc[t][1], av.x, bv.x);
-            dmma_f64(acc[t][2], acc[t][3], av.x, bv.y);
-            dmma_f64(acc[t][0], acc[t][1], -av.y, bv.y);
-            dmma_f64(acc[t][2], acc[t][3], av.y, bv.x);
-          }
-        }
+      const int kx = min(kslot, nks - c * kslot);
+      const unsigned char* sp = ring + (size_t)sl * slot_bytes;
+      const double2* xs = reinterpret_cast<const double2*>(sp + abytes);
+      // the tile count is a compile-time constant in each branch: no predicated-off DMMAs
+#define DA_CONSUME(NT)                                                                                   \
+  for (int kl = wp; kl < kx; kl += IN_THREADS / 32) {                                                    \
+    const double2 bv = ar < nact ? xs[ar * XST + kl * 4 + ak] : czero();                                 \
+    const int sub = kl / DA_KC, kk = kl - sub * DA_KC;                                                    \
+    const double2* af = reinterpret_cast<const double2*>(sp) + ((size_t)sub * NT * DA_KC + kk) * 32 + lane; \
+    _Pragma("unroll") for (int t = 0; t < NT; ++t) {                                                     \
+      const double2 av = af[t * DA_KC * 32];                                                              \
+      dmma_f64(acc[t][0], acc[t][1], av.x, bv.x);                                                         \
+      dmma_f64(acc[t][2], acc[t][3], av.x, bv.y);                                                         \
+      dmma_f64(acc[t][0], acc[t][1], -av.y, bv.y);                                                        \
+      dmma_f64(acc[t][2], acc[t][3], av.y, bv.x);                                                         \
+    }                                                                                                     \
+  }
+      switch (nt) {
+        case 1: DA_CONSUME(1) break;
+        case 2: DA_CONSUME(2) break;
+        case 3: DA_CONSUME(3) break;
+        case 4: DA_CONSUME(4) break;
+        case 5: DA_CONSUME(5) break;
+        case 6: DA_CONSUME(6) break;
+        case 7: DA_CONSUME(7) break;
+        default: DA_CONSUME(8) break;
       }
+#undef DA_CONSUME
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[sl]);
     }
-    dch = base + (unsigned)nch;
-    __syncthreads();  // every chunk consumed: the ring holds the partial tiles now
+    dch = base + (unsigned)nsl;
+    __syncthreads();  // every slot consumed: the ring holds the partial tiles now
     double* part = reinterpret_cast<double*>(ring);  // [8 warps][DA_T][4][32]
 #pragma unroll
     for (int t = 0; t < DA_T; ++t)
+      if (t < nt)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) part[((wp * DA_T + t) * 4 + v) * 32 + lane] = acc[t][v];
+        for (int v = 0; v < 4; ++v) part[((wp * DA_T + t) * 4 + v) * 32 + lane] = acc[t][v];
     __syncthreads();
     if (wp < nt) {  // warp wp owns tile tc + wp: fixed-order sum over the 8 k parts
       double c4[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int g = 0; g < IN_THREADS / 32; ++g)
+      for (int gw = 0; gw < IN_THREADS / 32; ++gw)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) c4[v] += part[((g * DA_T + wp) * 4 + v) * 32 + lane];
+        for (int v = 0; v < 4; ++v) c4[v] += part[((gw * DA_T + wp) * 4 + v) * 32 + lane];
       const int row = (tc + wp) * 8 + ar;
       if (row < n) {
 #pragma unroll
@@ -355,7 +379,7 @@ __device__ void dense_apply(const InnerParams& p, const double2* __restrict__ Mt
 #pragma unroll
   for (int i = 0; i < 8; ++i) rr[i] = i < nact ? r0 + S.act[i] : r0;
   dense_pass(p, Mt, n, job, rr, nact, src, dst, q * T8 / CS, (q + 1) * T8 / CS, reinterpret_cast<unsigned char*>(S.tiles),
-             S.region, S.dbar, dch);
+             S.region, S.dbar, dch, 1);
   csync();
 }
 
@@ -397,6 +421,25 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
   double2* W = vecp(p, job, r, j + 1);
   double2* H = Hp(r);
   double2* col = H + (size_t)j * hld;
+  // Givens state staged in shared memory: s_gv[0..j] = this column, s_gv[GV_MAX + i] = cs[i],
+  // s_gv[2 GV_MAX + i] = sn[i]; the previous rotations and g[j] are loaded in parallel here, so the
+  // serial rotation loop below runs on shared memory instead of dependent L2 round trips
+  __shared__ double2 s_gv[3 * GV_MAX + 2];
+  __shared__ double s_b0;
+  const bool gsm = j + 2 <= GV_MAX;
+  if (gsm) {
+    const double2* gg = H + hld * p.cap;
+    const double2* css = gg + (p.cap + 1);
+    const double2* snn = css + p.cap;
+    for (int i = tid; i < j; i += blockDim.x) {
+      s_gv[GV_MAX + i] = css[i];
+      s_gv[2 * GV_MAX + i] = snn[i];
+    }
+    if (tid == 0) {
+      s_gv[3 * GV_MAX] = gg[j];
+      s_b0 = p.beta0[job * p.R + r];
+    }
+  }
   double ss = 0.0;
   constexpr int EPT = 8;  // register-resident w for n <= EPT * IN_THREADS
   if (n <= EPT * IN_THREADS) {
@@ -419,7 +462,10 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
         si += c.y;
       }
       const double2 h = block_sum2(sr, si, dred);
-      if (tid == 0) col[i] = h;
+      if (tid == 0) {
+        col[i] = h;
+        if (i < GV_MAX) s_gv[i] = h;
+      }
 #pragma unroll
       for (int t = 0; t < EPT; ++t) wv[t] = csub(wv[t], cmul(h, vv[t]));
     }
@@ -439,7 +485,10 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
         si += c.y;
       }
       const double2 h = block_sum2(sr, si, dred);
-      if (tid == 0) col[i] = h;
+      if (tid == 0) {
+        col[i] = h;
+        if (i < GV_MAX) s_gv[i] = h;
+      }
       for (int e = tid; e < n; e += blockDim.x) W[e] = csub(ld_cg(W + e), cmul(h, ld_cg(Vi + e)));
       __syncthreads();
     }
@@ -451,7 +500,53 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
   ss = block_sum(ss, dred);
   const double hn = sqrt(ss);
   __shared__ int s_st;
-  if (tid == 0) {
+  if (tid == 0 && gsm) {  // rotations on shared memory, results written back to the global Hessenberg
+    double2* g = H + hld * p.cap;
+    double2* cs = g + (p.cap + 1);
+    double2* sn = cs + p.cap;
+    double2* cl = s_gv;
+    cl[j + 1] = make_double2(hn, 0.0);
+    for (int i = 0; i < j; ++i) {
+      const double2 csi = s_gv[GV_MAX + i], sni = s_gv[2 * GV_MAX + i];
+      const double2 t = cadd(cmul(csi, cl[i]), cmul(sni, cl[i + 1]));
+      const double2 nsc = make_double2(-sni.x, sni.y);  // -conj(sn)
+      const double2 csc = make_double2(csi.x, -csi.y);  // conj(cs)
+      cl[i + 1] = cadd(cmul(nsc, cl[i]), cmul(csc, cl[i + 1]));
+      cl[i] = t;
+    }
+    const double aa = hypot(cl[j].x, cl[j].y);
+    const double d = sqrt(aa * aa + hn * hn);
+    int st = 0;  // 0 continue, 1 converged, 2 failed
+    if (d == 0.0) {
+      st = 2;
+      atomicMax(p.err, 3);
+    } else {
+      const double2 c = make_double2(cl[j].x / d, -cl[j].y / d);
+      const double2 sv = make_double2(hn / d, 0.0);
+      cs[j] = c;
+      sn[j] = sv;
+      cl[j] = cadd(cmul(c, cl[j]), make_double2(sv.x * hn, 0.0));
+      const double2 gj = s_gv[3 * GV_MAX];
+      const double2 gj1 = cmul(make_double2(-sv.x, sv.y), gj);
+      g[j + 1] = gj1;
+      g[j] = cmul(c, gj);
+      const double res = hypot(gj1.x, gj1.y) / s_b0;
+      if (hn == 0.0) {
+        st = res > p.ktol ? 2 : 1;  // happy breakdown (krylov.py:116-124)
+        if (st == 2) atomicMax(p.err, 3);
+      } else if (res <= p.ktol) {
+        st = 1;
+      } else if (j + 1 == p.max_iter) {
+        st = 2;
+        atomicMax(p.err, 2);  // InnerSolveError (nested.py:148-152)
+      }
+    }
+    for (int i = 0; i <= j + 1; ++i) col[i] = cl[i];
+    s_st = st;
+    p.state[job * p.R + r] = st;
+    if (st != 0) p.iters[job * p.R + r] = st == 1 ? j + 1 : -1;
+  }
+  if (tid == 0 && !gsm) {
     double2* g = H + hld * p.cap;
     double2* cs = g + (p.cap + 1);
     double2* sn = cs + p.cap;
@@ -509,15 +604,34 @@ __device__ void instance_final(const InnerParams& p, int job, int r, int n, int 
   const int nIc = p.Lc - 1;
   const size_t hld = (size_t)p.cap + 1;
   auto Hp = [&](int rr_) { return p.hess + (size_t)(job * p.R + rr_) * p.hstride; };
-  const int k = p.iters[job * p.R + r];
+  __shared__ int s_k;
+  if (tid == 0) s_k = p.iters[job * p.R + r];
+  __syncthreads();
+  const int k = s_k;
+  // the upper triangle H[0..k)[0..k) and g[0..k) staged in shared memory by all threads (k <= 24: 300
+  // entries after yv), then the back substitution runs on thread 0 without dependent L2 round trips
+  constexpr int KS = 24;
+  double2* hs = yv + KS;  // [k(k+1)/2] column m holds rows 0..m
+  double2* gs = hs + KS * (KS + 1) / 2;
+  const double2* H = Hp(r);
+  const double2* g = H + hld * p.cap;
+  if (k > 0 && k <= KS) {
+    for (int e = tid; e < k * (k + 1) / 2; e += blockDim.x) {
+      int m = 0;
+      while ((m + 1) * (m + 2) / 2 <= e) ++m;
+      const int i = e - m * (m + 1) / 2;
+      hs[e] = H[(size_t)m * hld + i];
+    }
+    for (int i = tid; i < k; i += blockDim.x) gs[i] = g[i];
+  }
+  __syncthreads();
   if (tid == 0 && k > 0) {
-    const double2* H = Hp(r);
-    const double2* g = H + hld * p.cap;
+    const bool sm = k <= KS;
     for (int i = k - 1; i >= 0; --i) {
       double2 s = czero();
-      for (int m = i + 1; m < k; ++m) cfma(s, H[(size_t)m * hld + i], yv[m]);
-      const double2 num = csub(g[i], s);
-      const double2 den = H[(size_t)i * hld + i];
+      for (int m = i + 1; m < k; ++m) cfma(s, sm ? hs[m * (m + 1) / 2 + i] : H[(size_t)m * hld + i], yv[m]);
+      const double2 num = csub(sm ? gs[i] : g[i], s);
+      const double2 den = sm ? hs[i * (i + 1) / 2 + i] : H[(size_t)i * hld + i];
       const double dd = den.x * den.x + den.y * den.y;
       yv[i] = make_double2((num.x * den.x + num.y * den.y) / dd, (num.y * den.x - num.x * den.y) / dd);
     }
@@ -691,6 +805,196 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   for (int l = q; l < ni; l += CS) instance_final(p, job, r0 + l, n, w, S.pan);
   T.tick(9);
   if (T.on) atomicAdd((unsigned long long*)&g_in_t[11], (unsigned long long)(clock64() - tk_entry));
+}
+
+// ---------------------------------------------------------------------------------------------
+// Whole-GPU inner GMRES (cooperative launch, one CTA per SM) for every (job, group of <= 8 instances)
+// unit of a stage whose layers carry dense inner operators.  Every step is spread over all CTAs:
+// rhs_pol elementwise, each dense product as (unit, row-tile range) passes of dense_pass, the Arnoldi /
+// Givens / x = V y of an instance on its owner CTA; grid-wide barriers separate the steps.  Same
+// arithmetic, per instance, as the cluster kernel's dense path.
+#define COOP_MAXU 256
+__global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerParams p, int nunits) {
+  cg::grid_group grid = cg::this_grid();
+  Ticker T;
+  T.on = p.tprof && blockIdx.x == 0 && threadIdx.x == 0;
+  T.start();
+  auto gsync = [&]() {
+    T.tick(7);
+    grid.sync();
+    T.tick(5);
+  };
+  extern __shared__ __align__(128) unsigned char smem[];
+  const size_t region = (size_t)p.coop_region;
+  unsigned char* ring = smem;
+  uint64_t* dbar = reinterpret_cast<uint64_t*>(smem + region);
+  double* dred = reinterpret_cast<double*>(dbar + 2 * DA_NS);
+  int* utile = reinterpret_cast<int*>(dred + 64);     // [nunits + 1] tile prefix of the active units
+  int* unact = utile + COOP_MAXU + 1;                 // [nunits] active instances
+  unsigned char* uact = reinterpret_cast<unsigned char*>(unact + COOP_MAXU);  // [nunits][8] active local ids
+  unsigned char* sst = uact + COOP_MAXU * 8;          // [nunits][8] instance states (1 = frozen/absent)
+  double2* yv = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(sst + COOP_MAXU * 8) + 127) & ~(uintptr_t)127);
+
+  const int tid = threadIdx.x, G = gridDim.x, b = blockIdx.x;
+  const int ngroups = (p.R + 7) >> 3;
+  const int nIc = p.Lc - 1;
+  const int VB = p.cap + 1, VY = p.cap + 2;
+  if (tid == 0) {
+    for (int i = 0; i < DA_NS; ++i) {
+      mbar_init(&dbar[i], 1);
+      mbar_init(&dbar[DA_NS + i], IN_THREADS / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // every instance's state, loaded by all threads in parallel
+  auto load_states = [&](bool all) {
+    for (int t = tid; t < nunits * 8; t += blockDim.x) {
+      const int u = t >> 3, l = t & 7;
+      const int r0_ = (u % ngroups) * 8;
+      const bool ex = l < min(8, p.R - r0_);
+      sst[t] = !ex ? 1 : (all ? 0 : (__ldcg(p.state + p.stage_jobs[u / ngroups] * p.R + r0_ + l) == 0 ? 0 : 1));
+    }
+    __syncthreads();
+  };
+  auto ujob = [&](int u) { return p.stage_jobs[u / ngroups]; };
+  auto ur0 = [&](int u) { return (u % ngroups) * 8; };
+  auto uni = [&](int u) { return min(8, p.R - (u % ngroups) * 8); };
+  auto uw = [&](int u) { return p.layers[p.jobs[ujob(u)].layer].w; };
+  // ---- rhs_pol from the Newton tables (sie.py:230-242, negated)
+  for (int u = 0; u < nunits; ++u) {
+    const int job = ujob(u), r0 = ur0(u), ni = uni(u), w = uw(u), n = 4 * nIc * w;
+    for (long long t = (long long)b * blockDim.x + tid; t < (long long)ni * n; t += (long long)G * blockDim.x) {
+      const int l = (int)(t / n), e = (int)(t - (long long)l * n), r = r0 + l;
+      const int seg = e / w, j = e - seg * w;
+      const int half = seg / (2 * nIc);  // 0 down, 1 up
+      const int I = (seg % (2 * nIc)) / 2, s_ = seg & 1;
+      const int c = half == 0 ? I : I + 1;
+      const int idx = half == 0 ? 2 + s_ : s_;
+      const double2 tv = __ldcg(p.tables + ((((size_t)job * p.Lc + c) * 4 + idx) * p.R + r) * p.wmax + j);
+      vecp(p, job, r, VB)[e] = make_double2(-tv.x, -tv.y);
+    }
+  }
+  gsync();
+  unsigned dch = 0;
+  // y = M_which x over the active instances of every unit; all = every instance (the first product)
+  auto coop_apply = [&](int which, int src, int dst, bool all) {
+    T.tick(7);
+    load_states(all);
+    if (tid == 0) {
+      int tot = 0;
+      for (int u = 0; u < nunits; ++u) {
+        int na = 0;
+        for (int l = 0; l < 8; ++l)
+          if (sst[u * 8 + l] == 0) uact[u * 8 + na++] = (unsigned char)l;
+        unact[u] = na;
+        utile[u] = tot;
+        if (na > 0) tot += (4 * nIc * uw(u) + 7) >> 3;
+      }
+      utile[nunits] = tot;
+    }
+    __syncthreads();
+    const int tot = utile[nunits];
+    const int lo = (int)((long long)b * tot / G), hi = (int)((long long)(b + 1) * tot / G);
+    for (int u = 0; u < nunits && lo < hi; ++u) {
+      const int na = unact[u];
+      if (na == 0) continue;
+      const int t0 = max(lo, utile[u]) - utile[u], t1 = min(hi, utile[u + 1]) - utile[u];  // unit u's tiles
+      if (t0 >= t1) continue;
+      const int job = ujob(u), r0 = ur0(u), w = uw(u), n = 4 * nIc * w;
+      int rr[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rr[i] = i < na ? r0 + uact[u * 8 + i] : r0;
+      const double2* Mt = p.dense + p.layers[p.jobs[job].layer].dense_off + (size_t)which * dense_matrix_elems(n);
+      T.tick(12);
+      dense_pass(p, Mt, n, job, rr, na, src, dst, t0, t1, ring, region, dbar, dch, 8);
+      T.tick(13);
+    }
+  };
+  // ---- b = pre(rhs) (krylov.py:61), beta0, V_0
+  T.tick(8);  // setup (rhs_pol) before the first barrier is in 5/7
+  coop_apply(0, VB, VY, true);
+  T.tick(3);
+  gsync();
+  for (int t = b; t < nunits * 8; t += G) {
+    const int u = t >> 3, l = t & 7;
+    if (l < uni(u)) instance_init(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), VY, dred);
+  }
+  T.tick(6);
+  gsync();
+  for (int j = 0; j < p.max_iter; ++j) {
+    load_states(false);
+    int any = 0;
+    for (int t = tid; t < nunits * 8; t += blockDim.x) any |= sst[t] == 0;
+    if (!__syncthreads_or(any)) break;
+    if (j + 1 > p.cap) {  // basis capacity exhausted: the host retries with a larger capacity
+      for (int t = b; t < nunits * 8; t += G) {
+        const int u = t >> 3, l = t & 7;
+        if (tid == 0 && l < uni(u)) {
+          const int r = ur0(u) + l, job = ujob(u);
+          if (__ldcg(p.state + job * p.R + r) == 0) {
+            p.state[job * p.R + r] = 2;
+            p.iters[job * p.R + r] = -1;
+            atomicMax(p.err, 5);
+          }
+        }
+      }
+      gsync();
+      break;
+    }
+    T.tick(4);  // loop head (active scan)
+    coop_apply(1, j, j + 1, false);  // w = pre(op(V_j))
+    T.tick(3);
+    gsync();
+    for (int t = b; t < nunits * 8; t += G) {
+      const int u = t >> 3, l = t & 7;
+      if (l >= uni(u)) continue;
+      const int job = ujob(u), r = ur0(u) + l;
+      if (__ldcg(p.state + job * p.R + r) == 0) instance_arnoldi(p, job, r, j, 4 * nIc * uw(u), dred);
+    }
+    T.tick(6);
+    gsync();
+  }
+  for (int t = b; t < nunits * 8; t += G) {
+    const int u = t >> 3, l = t & 7;
+    if (l < uni(u)) instance_final(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), uw(u), yv);
+  }
+  T.tick(9);
+}
+
+size_t inner_coop_smem(const InnerParams& p, size_t region) {
+  return region + 2 * DA_NS * 8 + 64 * 8 + (COOP_MAXU + 1) * 4 + COOP_MAXU * 4 + 2 * COOP_MAXU * 8 + 128 +
+         (size_t)(p.cap + 2 + 24 + 300 + 24) * 16 + 128;
+}
+
+// returns cudaErrorNotSupported when the cooperative path does not apply (caller falls back)
+cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st) {
+  static int nsm = 0, maxsm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!nsm) {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  const int nunits = njobs * ((p0.R + 7) / 8);
+  if (!p0.dense || nunits > COOP_MAXU || p0.Lc < 2) return cudaErrorNotSupported;
+  InnerParams p = p0;
+  // ring: as many DA_KC-chunk slots as fit next to the small arrays (>= 2), and >= the partial tiles
+  const size_t slot = (size_t)DA_T * DA_KC * 512 + 8 * (8 * DA_KC * 4 + 4) * 16;  // dense_slot_bytes(8)
+  const size_t fixed = inner_coop_smem(p, 0);
+  size_t region = std::min((size_t)DA_NS * slot, ((size_t)maxsm - fixed) / slot * slot);
+  if (region < 2 * slot || region < (size_t)(IN_THREADS / 32) * DA_T * 4 * 32 * 8) return cudaErrorNotSupported;
+  p.coop_region = (long long)region;
+  const size_t sm = inner_coop_smem(p, region);
+  cudaFuncSetAttribute(inner_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_coop_kernel, IN_THREADS, sm);
+  if (per_sm < 1) return cudaErrorNotSupported;
+  const int grid = nsm;  // one CTA per SM
+  void* args[] = {(void*)&p, (void*)&nunits};
+  int nu = nunits;
+  args[1] = (void*)&nu;
+  return cudaLaunchCooperativeKernel((const void*)inner_coop_kernel, dim3(grid), dim3(IN_THREADS), args, sm, st);
 }
 
 int inner_mg(int wmax) { return wmax <= 80 ? 2 : 1; }

@@ -50,6 +50,7 @@ struct InnerParams {
   const int* stage_jobs;  // job id per CTA
   const double2* green;
   const double2* dense;   // dense inner operators (LayerInfo.dense_off), or null: item programs
+  long long coop_region;  // cooperative kernel: bytes of its shared-memory ring (set by the launcher)
   const IItem* items;
   const int* op_ph;       // phase begin offsets into items (op_nph + 1 entries)
   int op_nph;
@@ -89,6 +90,8 @@ __host__ __device__ constexpr int k1_jw(int nc) { return nc == 1 ? 5 : (nc == 2 
 size_t inner_smem_bytes(int wmax, int nitems);
 int inner_mg(int wmax);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
+// whole-GPU cooperative inner GMRES (dense operators); cudaErrorNotSupported: use inner_launch
+cudaError_t inner_coop_launch(const InnerParams& p, int njobs, cudaStream_t st);
 void inner_tprof_dump(const char* tag);
 __global__ void k_dense_tiles(const double2* src, double2* dst, int n, int kc);
 #define DA_KC 8  // k-steps per dense-apply chunk (inner_gmres.cu; the stored fragment layout depends on it)

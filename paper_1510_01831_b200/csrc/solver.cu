@@ -763,7 +763,13 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     ip.mg = inner_mg(c->wmax);
     {
       LaunchScope ls(c, 1);
-      CK(inner_launch(ip, J, c->st));
+      static const bool no_coop = std::getenv("PT_NO_COOP") != nullptr;
+      cudaError_t e = no_coop ? cudaErrorNotSupported : inner_coop_launch(ip, J, c->st);
+      if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        e = inner_launch(ip, J, c->st);
+      }
+      CK(e);
     }
     if (ip.tprof) inner_tprof_dump(S.name);
   }
