@@ -130,3 +130,80 @@ def test_solver_fails_loudly_without_gpu():
     layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=2)
     with pytest.raises(RuntimeError):
         PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers)
+
+
+# --- offline operators of the one-pass layer solve and the dense inner GMRES (CPU, torch) -----------
+
+def _offline_case():
+    from paper_1510_01831_b200.configs import small_problem
+    from paper_1510_01831_b200.offline import build_factors
+
+    prob = small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3)
+    return prob, build_factors(prob.grid, prob.model, prob.pml, prob.partition, 3)
+
+
+def _cell_solve(cf, rhs):
+    import torch
+
+    from paper_1510_01831_b200.offline import _twisted_solve
+
+    tinv = cf.sinv.transpose(-1, -2)  # stored column-major blocks -> row-major twisted factors
+    x = _twisted_solve(tinv[None], cf.lz, cf.uz, torch.as_tensor(rhs)[None, :, :, None])
+    return x[0, :, :, 0].numpy()
+
+
+def test_pass0_operator_matches_cell_solves():
+    """Q0 (offline.py) = the first layer-solve pass without volume source: Newton rows + trace samples."""
+    prob, F = _offline_case()
+    npml = F.npml
+    rng = np.random.default_rng(0)
+    for lf in F.layers:
+        for ci, cf in enumerate(lf.cells):
+            lo = 0 if ci == 0 else npml
+            hi = cf.wzc if ci == len(lf.cells) - 1 else npml + cf.nxc
+            nk, nk4 = hi - lo, (hi - lo + 3) // 4 * 4
+            P = rng.standard_normal((4, nk)) + 1j * rng.standard_normal((4, nk))
+            rhs = np.zeros((cf.wzc, cf.w), complex)
+            for s in range(4):
+                rhs[lo:hi, lf.prows[s]] += lf.coefs[s] * P[s]
+            x = _cell_solve(cf, rhs)
+            rows4 = [int(r) for r in (cf.krows[1], cf.krows[0], cf.krows[3], cf.krows[2])]
+            jrows = [npml - 1, npml, lf.n + npml - 1, lf.n + npml]
+            want = np.concatenate([x[rows4].reshape(-1), x[lo:hi][:, jrows].reshape(-1)])
+            Pp = np.zeros((4, nk4), complex)
+            Pp[:, :nk] = P
+            got = cf.q0.numpy()[: 4 * cf.w + 4 * nk] @ Pp.reshape(-1)
+            assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_sampled_trace_response_matches_cell_solves():
+    """gsmp (offline.py): the trace-source response sampled at the layer trace rows, every block row."""
+    prob, F = _offline_case()
+    npml = F.npml
+    rng = np.random.default_rng(1)
+    for lf in F.layers:
+        for cf in lf.cells:
+            tr = rng.standard_normal((4, cf.w)) + 1j * rng.standard_normal((4, cf.w))
+            rhs = np.zeros((cf.wzc, cf.w), complex)
+            for s in range(4):
+                rhs[int(cf.krows[s])] += cf.coefs[s] * tr[s]
+            x = _cell_solve(cf, rhs)
+            jrows = [npml - 1, npml, lf.n + npml - 1, lf.n + npml]
+            want = x[:, jrows]  # (wzc, 4)
+            got = np.einsum("kosj,sj->ko", cf.gsmp.numpy(), tr)
+            assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_dense_inner_operators_match_oracle():
+    """pre and pre o op of the inner trace problem (sie.py:203-329) as dense matrices."""
+    from oracle.polartraces_oracle import OracleSolver
+
+    prob, F = _offline_case()
+    orc = OracleSolver.from_problem(prob)
+    rng = np.random.default_rng(2)
+    for l, lf in enumerate(F.layers):
+        op, pre, _ = orc.outer.slabs[l].inner.flat_ops("gs")
+        Pm, Bm = (m.numpy() for m in lf.dense)
+        v = rng.standard_normal(Pm.shape[0]) + 1j * rng.standard_normal(Pm.shape[0])
+        for got, want in ((Pm @ v, pre(v)), (Bm @ v, pre(op(v)))):
+            assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
