@@ -112,6 +112,9 @@ typedef struct {
   double* k1_bytes;          /* [1] algorithmic S^-1 bytes of all K1 launches: 32*wz_c*w_c^2 per cell solve */
   long long* launches;       /* [1] kernels launched by this solve */
   long long* k1_launches;    /* [1] K1 launches */
+  double* class_ms;          /* [5] device time per launch class: K1, inner GMRES, glue, sampled trace
+                                response, pass-0 product (profiling only) */
+  double* dense_flops;       /* [1] algorithmic flops of the dense inner products: 8 n^2 per instance per product */
 } pt_stats;
 
 int pt_create(const pt_problem* prob, int device, pt_ctx** out);

@@ -1212,6 +1212,24 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
                 kv.second.second, 1e3 * kv.second.first / kv.second.second);
     }
     if (stats->k1_bytes) stats->k1_bytes[0] = c->k1_bytes;
+    if (stats->class_ms) {
+      double acc5[5] = {0, 0, 0, 0, 0};
+      for (const auto& e : c->evs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e.a, e.b);
+        acc5[e.cls] += t;
+      }
+      for (int i = 0; i < 5; ++i) stats->class_ms[i] = acc5[i];
+    }
+    if (stats->dense_flops) {
+      // dense inner products: pre(rhs) once and pre(op(.)) once per inner iteration, per instance
+      double f = 0.0;
+      if (c->dense_d) {
+        const double n = 4.0 * (c->Lc - 1) * c->wmax;  // n from the widest layer (exact when all are equal)
+        f = 8.0 * n * n * (double)(cnt[0] + (long long)c->layer_solves);
+      }
+      stats->dense_flops[0] = f;
+    }
     if (stats->launches) stats->launches[0] = c->launches;
     if (stats->k1_launches) stats->k1_launches[0] = c->k1_launches;
   }
