@@ -26,6 +26,7 @@
 #include <cstdlib>
 
 #include "pt_launch.cuh"
+#include "stage_dev.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -861,6 +862,37 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
   auto ur0 = [&](int u) { return (u % ngroups) * 8; };
   auto uni = [&](int u) { return min(8, p.R - (u % ngroups) * 8); };
   auto uw = [&](int u) { return p.layers[p.jobs[ujob(u)].layer].w; };
+  const int lane_ = tid & 31, wp_ = tid >> 5;
+  (void)lane_;
+  if (p.fused) {
+    // ---- gather the job panels (k_gather_panels), then the pass-0 product (k_pass0): two 4-warp
+    // items per CTA step, each with its own named barrier and partial-sum area in the ring region
+    const long long tot = (long long)nunits / ngroups * 4 * p.R * p.wx;
+    for (long long e = (long long)b * blockDim.x + tid; e < tot; e += (long long)G * blockDim.x)
+      gather_elem(p.jobs, p.tab, p.rmap, p.R, p.wx, p.P, e);
+    gsync();
+    const int mp8 = (4 * p.wmax + 4 * p.kmax + 7) / 8;
+    const int gz0 = (p.maxj * p.R + P0_COLS - 1) / P0_COLS;
+    const long long n0items = (long long)p.ngl * p.Lc * mp8 * gz0;
+    const int half = wp_ >> 2;
+    double* part = reinterpret_cast<double*>(ring) + half * (P0_KQ - 1) * 2 * 4 * 32;
+    for (long long it = (long long)b * 2 + half; it < n0items + 1; it += (long long)G * 2) {
+      if (it >= n0items) break;
+      long long rest = it;
+      const int z = (int)(rest % gz0);
+      rest /= gz0;
+      const int tile = (int)(rest % mp8);
+      rest /= mp8;
+      const int cc = (int)(rest % p.Lc), g = (int)(rest / p.Lc);
+      pass0_item(p.grp, p.ljobs, p.jobs, p.cells, p.layers, p.q0, p.P, const_cast<double2*>(p.tables), p.smp, p.R, p.Lc,
+                 p.wx, p.wmax, g,
+                 cc, tile, z, wp_ & 3, part, 1 + half);
+    }
+    // generic-proxy writes to the ring must be ordered before the bulk copies of the dense products
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    gsync();
+  }
   // ---- rhs_pol from the Newton tables (sie.py:230-242, negated)
   for (int u = 0; u < nunits; ++u) {
     const int job = ujob(u), r0 = ur0(u), ni = uni(u), w = uw(u), n = 4 * nIc * w;
@@ -960,6 +992,25 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
     if (l < uni(u)) instance_final(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), uw(u), yv);
   }
   T.tick(9);
+  if (p.fused) {
+    // ---- sampled trace response (k_green_samples) on the fresh traces, then the combination (k_combine)
+    gsync();
+    const int J = nunits / ngroups;
+    const int gy = (p.R + 7) / 8;
+    const int gzg = (p.kmax * 4 + 8 * GS_WARPS - 1) / (8 * GS_WARPS);
+    const long long ngitems = (long long)J * p.Lc * gy * gzg;
+    double2* trs = reinterpret_cast<double2*>(ring);
+    for (long long it = b; it < ngitems; it += G) {
+      const int z = (int)(it % gzg);
+      const long long rest = it / gzg;
+      const int y = (int)(rest % gy), x = (int)(rest / gy);
+      green_item(p.jobs, p.cells, p.layers, p.gsmp, p.tr, p.smp, p.R, p.Lc, p.wx, p.wmax, x, y, z, trs);
+    }
+    gsync();
+    const long long tot = (long long)J * 4 * p.R * p.wx;
+    for (long long e = (long long)b * blockDim.x + tid; e < tot; e += (long long)G * blockDim.x)
+      combine_elem(p.jobs, p.tab, p.rmap, p.R, p.wx, p.smp, e);
+  }
 }
 
 size_t inner_coop_smem(const InnerParams& p, size_t region) {
@@ -984,6 +1035,8 @@ cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st)
   const size_t fixed = inner_coop_smem(p, 0);
   size_t region = std::min((size_t)DA_NS * slot, ((size_t)maxsm - fixed) / slot * slot);
   if (region < 2 * slot || region < (size_t)(IN_THREADS / 32) * DA_T * 4 * 32 * 8) return cudaErrorNotSupported;
+  if (p.fused && (region < (size_t)4 * ((p.wmax + 3) & ~3) * 8 * 16 || region < 2 * (P0_KQ - 1) * 2 * 4 * 32 * 8))
+    return cudaErrorNotSupported;
   p.coop_region = (long long)region;
   const size_t sm = inner_coop_smem(p, region);
   cudaFuncSetAttribute(inner_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -10,61 +10,45 @@
 #include <algorithm>
 
 #include "pt_launch.cuh"
+#include "stage_dev.cuh"
 
 
-__device__ __forceinline__ double2 vref(const VecTab& t, Ref rf, int r, int x, int wx) {
-  return ld_cg(t.v[rf.vec].p + (size_t)r * t.v[rf.vec].stride + (size_t)rf.seg * wx + x);
-}
 
-// P[job][s][q][x] = sum of the slot's refs (sie.py:203-308 panel expressions)
+
 __global__ void k_gather_panels(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
                                 double2* P) {
   const long long total = (long long)njobs * 4 * nq * wx;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(e % wx);
-    long long rest = e / wx;
-    const int q = (int)(rest % nq);
-    rest /= nq;
-    const int s = (int)(rest % 4);
-    const int j = (int)(rest / 4);
-    const Ref* pr = jobs[j].pan[s];
-    if (pr[0].vec < 0) {  // absent slot: zero (the dense pass-0 product reads every slot)
-      P[e] = make_double2(0.0, 0.0);
-      continue;
-    }
-    const int r = rmap[q];
-    double2 v = vref(t, pr[0], r, x, wx);
-    if (pr[1].vec >= 0) v = cadd(v, vref(t, pr[1], r, x, wx));
-    P[e] = v;
-  }
+       e += (long long)gridDim.x * blockDim.x)
+    gather_elem(jobs, t, rmap, nq, wx, P, e);
 }
 
-// dst = scoef*sample + add - (sub0 + sub1)
 __global__ void k_combine(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
                           const double2* smp) {
   const long long total = (long long)njobs * 4 * nq * wx;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(e % wx);
-    long long rest = e / wx;
-    const int q = (int)(rest % nq);
-    rest /= nq;
-    const int o = (int)(rest % 4);
-    const int j = (int)(rest / 4);
-    const OJob& jb = jobs[j];
-    if (o >= jb.nout) continue;
-    const int r = rmap[q];
-    double2 y = cscale(smp[e], jb.scoef[o]);
-    if (jb.add[o].vec >= 0) y = cadd(y, vref(t, jb.add[o], r, x, wx));
-    if (jb.sub[o][0].vec >= 0) {
-      double2 sb = vref(t, jb.sub[o][0], r, x, wx);
-      if (jb.sub[o][1].vec >= 0) sb = cadd(sb, vref(t, jb.sub[o][1], r, x, wx));
-      y = csub(y, sb);
-    }
-    const VecView& dv = t.v[jb.dst[o].vec];
-    dv.p[(size_t)r * dv.stride + (size_t)jb.dst[o].seg * wx + x] = y;
-  }
+       e += (long long)gridDim.x * blockDim.x)
+    combine_elem(jobs, t, rmap, nq, wx, smp, e);
+}
+
+__global__ void __launch_bounds__(P0_KQ * 32) k_pass0(const int* __restrict__ grp, const int* __restrict__ ljobs,
+                                                      const OJob* __restrict__ jobs,
+                                                      const CellInfo* __restrict__ cells,
+                                                      const LayerInfo* __restrict__ layers,
+                                                      const double2* __restrict__ q0, const double2* __restrict__ P,
+                                                      double2* __restrict__ tables, double2* __restrict__ smp, int R,
+                                                      int Lc, int wx, int wmax) {
+  __shared__ double part[(P0_KQ - 1) * 2 * 4 * 32];
+  pass0_item(grp, ljobs, jobs, cells, layers, q0, P, tables, smp, R, Lc, wx, wmax, blockIdx.x / Lc,
+             blockIdx.x % Lc, blockIdx.y, blockIdx.z, threadIdx.x >> 5, part, 1);
+}
+
+__global__ void __launch_bounds__(GS_WARPS * 32) k_green_samples(
+    const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells, const LayerInfo* __restrict__ layers,
+    const double2* __restrict__ gsmp, const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,
+    int wmax) {
+  extern __shared__ double2 trs[];  // [4 slots][w4][8 rhs]
+  green_item(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax, blockIdx.x, blockIdx.y, blockIdx.z, trs);
 }
 
 // dst[seg..] = a*x[seg..] (+ b*y[seg..]) over len elements, for the active RHS
@@ -243,73 +227,6 @@ __global__ void k_dense_tiles(const double2* src, double2* dst, int n, int kc) {
 // so its samples at the layer trace rows are the pass-0 samples (written by K1 pass 0) plus
 // gsmp[k][row][s][:] . tr_s for every kept block row k.
 // grid: x = job * Lc + cell, y = group of 8 RHS, z = chunk of kept block rows.
-// DMMA formulation: rows = (kept block row k, output row o) of a cell, N = 8 RHS, K = (slot, column j):
-//   C[(k,o)][r] += sum_{s,j} G[k][o][s][j] * tr_s[r][j]   (complex: Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br)
-// A fragments straight from the sampled Green pool (each element used once per CTA), B fragments from the
-// trace panels staged in shared memory as [slot][j (padded to w4, zeros)][8 RHS]; one 8-row tile per warp.
-#define GS_WARPS 8
-__global__ void __launch_bounds__(GS_WARPS * 32) k_green_samples(
-    const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells, const LayerInfo* __restrict__ layers,
-    const double2* __restrict__ gsmp, const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,
-    int wmax) {
-  extern __shared__ double2 trs[];  // [4 slots][w4][8 rhs]
-  const int jid = blockIdx.x / Lc, c = blockIdx.x - (blockIdx.x / Lc) * Lc;
-  const OJob& jb = jobs[jid];
-  const int nout = jb.nout;
-  if (nout <= 0) return;
-  const LayerInfo& lay = layers[jb.layer];
-  const CellInfo& ci = cells[jb.layer * Lc + c];
-  const int w = ci.w, w4 = (w + 3) & ~3, nIc = Lc - 1, tid = threadIdx.x;
-  const int lane = tid & 31, wp = tid >> 5;
-  const int r0 = blockIdx.y * 8, nr = min(8, R - r0);
-  for (int row = wp; row < 32; row += GS_WARPS) {  // (slot, rhs) rows of the trace panels
-    const int sl = row >> 3, rr = row & 7;
-    const int I = sl < 2 ? c - 1 : c;
-    const bool okr = rr < nr && I >= 0 && I < nIc;
-    const double2* src = tr + (((size_t)(jid * R + r0 + (okr ? rr : 0)) * nIc + (okr ? I : 0)) * 2 + (sl & 1)) * wmax;
-    for (int j = lane; j < w4; j += 32)
-      trs[((size_t)sl * w4 + j) * 8 + rr] = (okr && j < w) ? src[j] : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  const int s_lo = ci.has_top ? 0 : 2, s_hi = ci.has_bot ? 4 : 2;
-  const int nrows = (ci.hi - ci.lo) * nout;  // (k, o) rows of this cell, k-major
-  const int tile = blockIdx.z * GS_WARPS + wp;
-  if (tile * 8 >= nrows) return;
-  const int ar = lane >> 2, ak = lane & 3;
-  // this lane's A row
-  const int m = tile * 8 + ar;
-  const bool mok = m < nrows;
-  const int mk = mok ? m / nout : 0, mo = mok ? m - (m / nout) * nout : 0;
-  const int orow = jb.orow[mo];
-  const int oi = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
-  const double2* grow = gsmp + ci.gsmp_off + ((size_t)(ci.lo + mk) * 4 + oi) * 4 * w;  // [4 slots][w]
-  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-  for (int sl = s_lo; sl < s_hi; ++sl) {
-    const double2* ga = grow + sl * w;
-    const double2* tb = trs + (size_t)sl * w4 * 8 + ar;
-#pragma unroll 6
-    for (int j0 = 0; j0 < w4; j0 += 4) {
-      const int j = j0 + ak;
-      const double2 av = (mok && j < w) ? __ldg(ga + j) : make_double2(0.0, 0.0);
-      const double2 bv = tb[(size_t)j * 8];
-      dmma_f64(c0, c1, av.x, bv.x);
-      dmma_f64(c2, c3, av.x, bv.y);
-      dmma_f64(c0, c1, -av.y, bv.y);
-      dmma_f64(c2, c3, av.y, bv.x);
-    }
-  }
-  // C fragment: row ar, columns (RHS) 2 ak and 2 ak + 1; (c0, c2) and (c1, c3) are complex
-  if (!mok) return;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int rr = 2 * ak + h;
-    if (rr < nr) {
-      double2* dst = smp + ((size_t)(jid * 4 + mo) * R + r0 + rr) * wx + ci.off + ci.lo + mk;
-      *dst = cadd(*dst, h == 0 ? make_double2(c0, c2) : make_double2(c1, c3));
-    }
-  }
-}
-
 cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                  const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,
                                  int wmax, int kmax, int num_sms, cudaStream_t st) {
@@ -331,111 +248,6 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
 // (kept block row k, row 0/1/n/n+1).  DMMA m8n8k4 f64 complex (4 products per k-step), one 8-row
 // tile x up to 32 columns (4 groups of 8) per warp, A from the operator pool, B from the gathered panels.
 // grid: x = layer group g * Lc + cell, y = chunk of 8 row tiles, z = chunk of 32 columns.
-#define P0_COLS 16  // columns (job, RHS) per CTA: two DMMA column groups of 8
-#define P0_KQ 4      // k parts per row tile (one warp each), summed in shared memory in a fixed order
-__global__ void __launch_bounds__(P0_KQ * 32) k_pass0(const int* __restrict__ grp, const int* __restrict__ ljobs,
-                                                      const OJob* __restrict__ jobs,
-                                                      const CellInfo* __restrict__ cells,
-                                                      const LayerInfo* __restrict__ layers,
-                                                      const double2* __restrict__ q0, const double2* __restrict__ P,
-                                                      double2* __restrict__ tables, double2* __restrict__ smp, int R,
-                                                      int Lc, int wx, int wmax) {
-  __shared__ double part[P0_KQ - 1][2][4][32];
-  const int g = blockIdx.x / Lc, c = blockIdx.x - (blockIdx.x / Lc) * Lc;
-  const int layer = grp[3 * g], jb0 = grp[3 * g + 1], nj = grp[3 * g + 2];
-  const CellInfo& ci = cells[layer * Lc + c];
-  const LayerInfo& lay = layers[layer];
-  const int w = ci.w, nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3, K = 4 * nk4;
-  const int M = 4 * w + 4 * nk, Mp = (M + 7) & ~7;
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int N = nj * R, n0 = blockIdx.z * P0_COLS;
-  const int tile = blockIdx.y;
-  if (n0 >= N || tile * 8 >= Mp) return;
-  const int ngq = min(2, (N - n0 + 7) >> 3);
-  const int ar = lane >> 2, ak = lane & 3;
-  const double2* arow = q0 + ci.q0_off + (size_t)(tile * 8 + ar) * K + ak;
-  const double2* bcol[2];
-  bool bok[2];
-#pragma unroll
-  for (int gq = 0; gq < 2; ++gq) {
-    const int n = n0 + 8 * gq + ar;
-    bok[gq] = n < N;
-    const int jid = ljobs[jb0 + (bok[gq] ? n / R : 0)], q = bok[gq] ? n % R : 0;
-    bcol[gq] = P + ((size_t)(jid * 4) * R + q) * wx + ci.off + ci.lo + ak;
-  }
-  const size_t sstride = (size_t)R * wx;  // slot stride in P
-  double acc[2][4];
-#pragma unroll
-  for (int gq = 0; gq < 2; ++gq) acc[gq][0] = acc[gq][1] = acc[gq][2] = acc[gq][3] = 0.0;
-  const int nks = K >> 2, kps = nk4 >> 2;  // k-steps in all / per slot
-  const int kb = wp * nks / P0_KQ, ke = (wp + 1) * nks / P0_KQ;
-  for (int ks0 = kb; ks0 < ke; ks0 += 8) {
-    double2 av[8], bv[8][2];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int ks = ks0 + u;
-      const bool kin = ks < ke;
-      const int sl = kin ? ks / kps : 0, kk = (ks - sl * kps) * 4;  // column within the slot block (+ ak)
-      av[u] = kin ? __ldg(arow + ks * 4) : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int gq = 0; gq < 2; ++gq)
-        bv[u][gq] = (kin && bok[gq] && kk + ak < nk) ? __ldg(bcol[gq] + sl * sstride + kk) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-#pragma unroll
-      for (int gq = 0; gq < 2; ++gq) {
-        if (gq < ngq) {
-          dmma_f64(acc[gq][0], acc[gq][1], av[u].x, bv[u][gq].x);
-          dmma_f64(acc[gq][2], acc[gq][3], av[u].x, bv[u][gq].y);
-          dmma_f64(acc[gq][0], acc[gq][1], -av[u].y, bv[u][gq].y);
-          dmma_f64(acc[gq][2], acc[gq][3], av[u].y, bv[u][gq].x);
-        }
-      }
-    }
-  }
-  if (wp > 0) {
-#pragma unroll
-    for (int gq = 0; gq < 2; ++gq)
-#pragma unroll
-      for (int t = 0; t < 4; ++t) part[wp - 1][gq][t][lane] = acc[gq][t];
-  }
-  __syncthreads();
-  if (wp > 0) return;
-#pragma unroll
-  for (int p2 = 0; p2 < P0_KQ - 1; ++p2)
-#pragma unroll
-    for (int gq = 0; gq < 2; ++gq)
-#pragma unroll
-      for (int t = 0; t < 4; ++t) acc[gq][t] += part[p2][gq][t][lane];
-  // C fragment: row ar of the tile, columns 2 ak, 2 ak + 1 of each group
-  const int m = tile * 8 + ar;
-  if (m >= M) return;
-#pragma unroll
-  for (int gq = 0; gq < 2; ++gq) {
-    if (gq >= ngq) continue;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int n = n0 + 8 * gq + 2 * ak + h;
-      if (n >= N) continue;
-      const int jid = ljobs[jb0 + n / R], q = n % R;
-      const double2 v = make_double2(acc[gq][h], acc[gq][2 + h]);
-      if (m < 4 * w) {
-        const int idx = m / w, j = m - (m / w) * w;
-        tables[((((size_t)jid * Lc + c) * 4 + idx) * R + q) * wmax + j] = v;
-      } else {
-        const int mm = m - 4 * w, kk = mm >> 2, oi = mm & 3;
-        const OJob& jb = jobs[jid];
-        for (int o = 0; o < jb.nout; ++o) {
-          const int orow = jb.orow[o];
-          const int ok_ = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
-          if (ok_ == oi) smp[((size_t)(jid * 4 + o) * R + q) * wx + ci.off + ci.lo + kk] = v;
-        }
-      }
-    }
-  }
-}
-
 cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
                          const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,
                          int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st) {

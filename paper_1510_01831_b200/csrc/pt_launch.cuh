@@ -51,6 +51,18 @@ struct InnerParams {
   const double2* green;
   const double2* dense;   // dense inner operators (LayerInfo.dense_off), or null: item programs
   long long coop_region;  // cooperative kernel: bytes of its shared-memory ring (set by the launcher)
+  // fused sample-only stage (cooperative kernel): gather -> pass-0 product -> inner -> sampled trace
+  // response -> combine in one launch (stage_dev.cuh bodies); fused = 0: inner GMRES only
+  int fused;
+  VecTab tab;
+  const int* rmap;
+  int wx, ngl, maxj, kmax;
+  double2* P;
+  double2* smp;
+  const double2* q0;
+  const double2* gsmp;
+  const int* grp;
+  const int* ljobs;
   const IItem* items;
   const int* op_ph;       // phase begin offsets into items (op_nph + 1 entries)
   int op_nph;

@@ -654,6 +654,48 @@ static int grid_for(long long n) {
   return (int)std::max(1LL, std::min(b, 148LL * 16));
 }
 
+static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io) {
+  InnerParams ip;
+  std::memset(&ip, 0, sizeof(ip));
+  ip.cells = c->cel_d;
+  ip.layers = c->lay_d;
+  ip.jobs = S.jobs_d;
+  ip.stage_jobs = S.stage_jobs_d;
+  ip.green = c->green_d;
+  static const bool no_dense = std::getenv("PT_NO_DENSE") != nullptr;
+  ip.dense = no_dense ? nullptr : c->dense_d;
+  ip.items = c->items_d;
+  ip.op_ph = c->op_ph_d;
+  ip.op_nph = c->op_nph;
+  ip.pre_ph = c->pre_ph_d;
+  ip.pre_nph = c->pre_nph;
+  ip.R = Ract;
+  ip.Lc = c->Lc;
+  ip.wmax = c->wmax;
+  ip.cap = c->inner_cap;
+  ip.max_iter = io.inner_max_iter;
+  ip.ktol = io.inner_ktol;
+  ip.tables = c->tables;
+  ip.tr = c->trc;
+  ip.scratch = c->iscr;
+  ip.inst_stride = c->iscr_stride;
+  ip.nmax = c->inmax;
+  ip.hess = c->hess;
+  ip.hstride = c->hstride;
+  ip.iters = c->iters;
+  ip.state = c->istate;
+  ip.beta0 = c->ibeta0;
+  ip.err = c->err_d;
+  ip.counters = c->cnt_d;
+  ip.hist = c->hist_d;
+  ip.op_blocks = c->op_blocks;
+  ip.pre_blocks = c->pre_blocks;
+  ip.tprof = std::getenv("PT_INNER_TPROF") != nullptr;
+  ip.nitems = c->nitems;
+  ip.mg = inner_mg(c->wmax);
+  return ip;
+}
+
 static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& io) {
   c->cur_tag = S.name;
   const int J = (int)S.jobs.size();
@@ -661,6 +703,50 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   Stage::Tasks* T = stage_tasks(c, S, Ract);
   if (!T) return PT_CUDA_ERROR;
   if (ensure_z(c, T->zsize)) return PT_CUDA_ERROR;
+  // optionally one cooperative launch for a whole sample-only stage without volume source (gather, pass-0
+  // product, inner GMRES, sampled response, combine); falls back to the launch sequence below
+  {
+    // opt-in (PT_FUSE=1): measured slower than the separate launches on cfg2 (one 8-warp CTA per SM hides
+    // less latency in the pass-0 / sampled-response products than their own many-CTA grids)
+    static const bool no_fuse = std::getenv("PT_FUSE") == nullptr;
+    static const bool no_q0e = std::getenv("PT_NO_Q0") != nullptr, no_gsmpe = std::getenv("PT_NO_GSMP") != nullptr;
+    static const bool no_dense = std::getenv("PT_NO_DENSE") != nullptr, no_coop = std::getenv("PT_NO_COOP") != nullptr;
+    if (!no_fuse && !no_q0e && !no_gsmpe && !no_dense && !no_coop && c->Lc > 1 && c->gsmp_d && c->q0_d &&
+        c->dense_d && S.samples_only && S.no_volume && S.any_panel && S.grp_d) {
+      InnerParams ip = inner_params(c, S, Ract, io);
+      ip.fused = 1;
+      ip.tab = tab;
+      ip.rmap = c->rmap_d;
+      ip.wx = c->wx;
+      ip.ngl = (int)S.lgrp.size();
+      int maxj = 0;
+      for (size_t i = 0; i < S.lgrp.size(); ++i) {
+        const int e = i + 1 < S.lgrp.size() ? S.lgrp[i + 1].second : (int)S.ljobs.size();
+        maxj = std::max(maxj, e - S.lgrp[i].second);
+      }
+      ip.maxj = maxj;
+      ip.kmax = c->wzcmax;
+      ip.P = c->P;
+      ip.smp = c->smp;
+      ip.q0 = c->q0_d;
+      ip.gsmp = c->gsmp_d;
+      ip.grp = S.grp_d;
+      ip.ljobs = S.ljobs_d;
+      c->cur_tag = S.name;
+      cudaError_t e;
+      {
+        LaunchScope ls(c, 1);
+        e = inner_coop_launch(ip, J, c->st);
+      }
+      if (e == cudaSuccess) {
+        if (ip.tprof) inner_tprof_dump(S.name);
+        c->layer_solves += (long long)J * Ract;
+        return 0;
+      }
+      if (e != cudaErrorNotSupported) CK(e);
+      cudaGetLastError();
+    }
+  }
   if (S.any_panel) {
     LaunchScope ls(c, 2);
     k_gather_panels<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract,
@@ -723,44 +809,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
       CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
       c->k1_bytes += T->bytes;
     }
-    InnerParams ip;
-    std::memset(&ip, 0, sizeof(ip));
-    ip.cells = c->cel_d;
-    ip.layers = c->lay_d;
-    ip.jobs = S.jobs_d;
-    ip.stage_jobs = S.stage_jobs_d;
-    ip.green = c->green_d;
-    static const bool no_dense = std::getenv("PT_NO_DENSE") != nullptr;
-    ip.dense = no_dense ? nullptr : c->dense_d;
-    ip.items = c->items_d;
-    ip.op_ph = c->op_ph_d;
-    ip.op_nph = c->op_nph;
-    ip.pre_ph = c->pre_ph_d;
-    ip.pre_nph = c->pre_nph;
-    ip.R = Ract;
-    ip.Lc = c->Lc;
-    ip.wmax = c->wmax;
-    ip.cap = c->inner_cap;
-    ip.max_iter = io.inner_max_iter;
-    ip.ktol = io.inner_ktol;
-    ip.tables = c->tables;
-    ip.tr = c->trc;
-    ip.scratch = c->iscr;
-    ip.inst_stride = c->iscr_stride;
-    ip.nmax = c->inmax;
-    ip.hess = c->hess;
-    ip.hstride = c->hstride;
-    ip.iters = c->iters;
-    ip.state = c->istate;
-    ip.beta0 = c->ibeta0;
-    ip.err = c->err_d;
-    ip.counters = c->cnt_d;
-    ip.hist = c->hist_d;
-    ip.op_blocks = c->op_blocks;
-    ip.pre_blocks = c->pre_blocks;
-    ip.tprof = std::getenv("PT_INNER_TPROF") != nullptr;
-    ip.nitems = c->nitems;
-    ip.mg = inner_mg(c->wmax);
+    InnerParams ip = inner_params(c, S, Ract, io);
     {
       LaunchScope ls(c, 1);
       static const bool no_coop = std::getenv("PT_NO_COOP") != nullptr;
