@@ -848,20 +848,32 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
     fence_mbar_init();
   }
   __syncthreads();
+  // per-job info staged once (the chained job -> layer -> width/offset loads stay off the step paths)
+  __shared__ int s_job[COOP_MAXU], s_w[COOP_MAXU];
+  __shared__ long long s_doff[COOP_MAXU];
+  const int njob_ = nunits / ngroups;
+  for (int jx = tid; jx < njob_; jx += blockDim.x) {
+    const int job = p.stage_jobs[jx];
+    const int layer = p.jobs[job].layer;
+    s_job[jx] = job;
+    s_w[jx] = p.layers[layer].w;
+    s_doff[jx] = p.layers[layer].dense_off;
+  }
+  __syncthreads();
   // every instance's state, loaded by all threads in parallel
   auto load_states = [&](bool all) {
     for (int t = tid; t < nunits * 8; t += blockDim.x) {
       const int u = t >> 3, l = t & 7;
       const int r0_ = (u % ngroups) * 8;
       const bool ex = l < min(8, p.R - r0_);
-      sst[t] = !ex ? 1 : (all ? 0 : (__ldcg(p.state + p.stage_jobs[u / ngroups] * p.R + r0_ + l) == 0 ? 0 : 1));
+      sst[t] = !ex ? 1 : (all ? 0 : (__ldcg(p.state + s_job[u / ngroups] * p.R + r0_ + l) == 0 ? 0 : 1));
     }
     __syncthreads();
   };
-  auto ujob = [&](int u) { return p.stage_jobs[u / ngroups]; };
+  auto ujob = [&](int u) { return s_job[u / ngroups]; };
   auto ur0 = [&](int u) { return (u % ngroups) * 8; };
   auto uni = [&](int u) { return min(8, p.R - (u % ngroups) * 8); };
-  auto uw = [&](int u) { return p.layers[p.jobs[ujob(u)].layer].w; };
+  auto uw = [&](int u) { return s_w[u / ngroups]; };
   const int lane_ = tid & 31, wp_ = tid >> 5;
   (void)lane_;
   if (p.fused) {
@@ -937,7 +949,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
       int rr[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) rr[i] = i < na ? r0 + uact[u * 8 + i] : r0;
-      const double2* Mt = p.dense + p.layers[p.jobs[job].layer].dense_off + (size_t)which * dense_matrix_elems(n);
+      const double2* Mt = p.dense + s_doff[u / ngroups] + (size_t)which * dense_matrix_elems(n);
       T.tick(12);
       dense_pass(p, Mt, n, job, rr, na, src, dst, t0, t1, ring, region, dbar, dch, 8);
       T.tick(13);
