@@ -115,7 +115,8 @@ __host__ __device__ inline long long dense_matrix_elems(long long n) {
 // first layer-solve pass (no volume source) as a dense product with the offline pass-0 operators
 cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
                          const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,
-                         int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st);  // PT_INNER_TPROF: print and reset CTA 0's segment clocks
+                         int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st,
+                         int accum = 0);  // PT_INNER_TPROF: print and reset CTA 0's segment clocks
 // smp += trace-source response (sampled Green rows) for every (job, cell, output row, RHS)
 cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                  const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,

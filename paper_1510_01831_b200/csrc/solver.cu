@@ -86,6 +86,9 @@ struct pt_ctx {
   double2* gsmp_d = nullptr;  // sampled trace responses (optional; enables the one-pass layer solve)
   double2* q0_d = nullptr;    // pass-0 operators (optional; layer solves without volume sources skip K1)
   double2* dense_d = nullptr; // dense inner operators (optional)
+  double2* tables_f = nullptr;  // Newton tables of the volume sources alone (NEWTON stage), reused by RECON
+  bool tables_f_ok = false;
+  int tables_f_R = 0;
   double2 *tx_d = nullptr, *tz_d = nullptr;
   double* m_d = nullptr;
   // inner item programs
@@ -522,8 +525,8 @@ static int ensure_scratch(pt_ctx* c, int R, int capO) {
     if (p) cudaFree(p);
   };
   for (void* p : {(void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1, (void*)c->AX, (void*)c->X, (void*)c->TR,
-                  (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->trc, (void*)c->iscr, (void*)c->hess,
-                  (void*)c->iters, (void*)c->istate, (void*)c->ibeta0, (void*)c->rmap_d, (void*)c->dscal,
+                  (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->tables_f, (void*)c->trc, (void*)c->iscr,
+                  (void*)c->hess, (void*)c->iters, (void*)c->istate, (void*)c->ibeta0, (void*)c->rmap_d, (void*)c->dscal,
                   (void*)c->hout, (void*)c->ybuf})
     F(p);
   if (c->hrmap) cudaFreeHost(c->hrmap);
@@ -537,6 +540,7 @@ static int ensure_scratch(pt_ctx* c, int R, int capO) {
   CK(cudaMalloc(&c->P, sizeof(double2) * (size_t)Jmax * 4 * R * c->wx));
   CK(cudaMalloc(&c->smp, sizeof(double2) * (size_t)Jmax * 4 * R * c->wx));
   CK(cudaMalloc(&c->tables, sizeof(double2) * (size_t)Jmax * c->Lc * 4 * R * c->wmax));
+  CK(cudaMalloc(&c->tables_f, sizeof(double2) * (size_t)Jmax * c->Lc * 4 * R * c->wmax));
   CK(cudaMalloc(&c->trc, sizeof(double2) * (size_t)Jmax * R * std::max(c->Lc - 1, 1) * 2 * c->wmax));
   c->inmax = 4LL * std::max(c->Lc - 1, 1) * c->wmax;
   c->iscr_stride = (long long)(c->inner_cap + 5) * c->inmax;
@@ -793,9 +797,20 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   kp.s0 = gpath ? 1 : 0;
   static const bool no_q0 = std::getenv("PT_NO_Q0") != nullptr;
   const bool qpath = gpath && c->q0_d && S.no_volume && S.any_panel && S.grp_d && !no_q0;
+  // RECON: first pass by linearity = Newton tables of f (saved by the NEWTON stage) + pass-0 product of
+  // the trace panels (the jobs of both stages are the L layers in order, same RHS set)
+  static const bool no_reuse = std::getenv("PT_NO_REUSE") != nullptr;
+  const bool rpath = &S == &c->recon && c->tables_f_ok && c->q0_d && S.any_panel && S.grp_d && !no_reuse &&
+                     Ract == c->tables_f_R;
   if (c->Lc > 1) {
     kp.pass = 0;
-    if (qpath) {  // first pass as one dense product with the offline pass-0 operators (no volume source)
+    if (rpath) {
+      LaunchScope ls(c, 4);
+      CK(cudaMemcpyAsync(c->tables, c->tables_f, sizeof(double2) * (size_t)J * c->Lc * 4 * Ract * c->wmax,
+                         cudaMemcpyDeviceToDevice, c->st));
+      CK(pass0_launch(S.grp_d, (int)S.lgrp.size(), S.ljobs_d, S.jobs_d, c->cel_d, c->lay_d, c->q0_d, c->P, c->tables,
+                      c->smp, Ract, c->Lc, c->wx, c->wmax, c->wzcmax, 1, c->st, 1));
+    } else if (qpath) {  // first pass as one dense product with the offline pass-0 operators (no volume source)
       LaunchScope ls(c, 4);
       int maxj = 0;
       for (size_t i = 0; i < S.lgrp.size(); ++i) {
@@ -997,7 +1012,16 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   } else if (!live.empty()) {
     if ((rc = set_active(c, all))) return rc;
     CK(cudaMemsetAsync(c->Bv, 0, sizeof(double2) * (size_t)R * nO, c->st));
+    c->tables_f_ok = false;
     if ((rc = run_stage(c, c->newton, VecTab{{vB, vB, vB}}, R, io))) return rc;
+    // the Newton tables of f alone: RECON's first pass is these plus the pass-0 product of its panels
+    if (c->q0_d && c->Lc > 1 && c->newton.jobs.size() == c->recon.jobs.size()) {
+      CK(cudaMemcpyAsync(c->tables_f, c->tables,
+                         sizeof(double2) * c->newton.jobs.size() * c->Lc * 4 * (size_t)R * c->wmax,
+                         cudaMemcpyDeviceToDevice, c->st));
+      c->tables_f_ok = true;
+      c->tables_f_R = R;
+    }
     if ((rc = set_active(c, live))) return rc;
     const int Rl = (int)live.size();
     if ((rc = apply_pre(c, vB, vBp, vA, Rl, gs, io))) return rc;
@@ -1526,7 +1550,7 @@ int pt_destroy(pt_ctx* c) {
   for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->dense_d, (void*)c->lz_d,
                   (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->items_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
-                  (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables,
+                  (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->tables_f,
                   (void*)c->trc, (void*)c->Z, (void*)c->iscr, (void*)c->hess, (void*)c->iters, (void*)c->istate,
                   (void*)c->ibeta0, (void*)c->err_d,
                   (void*)c->cnt_d, (void*)c->hist_d, (void*)c->rmap_d, (void*)c->dscal, (void*)c->hout,

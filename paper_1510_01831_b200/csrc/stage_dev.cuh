@@ -53,13 +53,14 @@ __device__ __forceinline__ void combine_elem(const OJob* jobs, const VecTab& t, 
 #define P0_COLS 16  // columns (job, RHS) per CTA: two DMMA column groups of 8
 #define P0_KQ 4      // k parts per row tile (one warp each), summed in shared memory in a fixed order
 // One (layer group g, cell c, row tile, 16-column chunk z) item, executed by P0_KQ warps (wq = warp index in
-// the group); part: [P0_KQ-1][2][4][32] doubles of shared memory; barid: named barrier of the group.
+// the group); part: [P0_KQ-1][2][4][32] doubles of shared memory; barid: named barrier of the group;
+// accum: add to the Newton tables instead of overwriting them.
 __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const int* __restrict__ ljobs,
                                            const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
                                            const LayerInfo* __restrict__ layers, const double2* __restrict__ q0,
                                            const double2* __restrict__ P, double2* __restrict__ tables,
                                            double2* __restrict__ smp, int R, int Lc, int wx, int wmax, int g, int c,
-                                           int tile, int z, int wq, double* part, int barid) {
+                                           int tile, int z, int wq, double* part, int barid, int accum = 0) {
   const int layer = grp[3 * g], jb0 = grp[3 * g + 1], nj = grp[3 * g + 2];
   const CellInfo& ci = cells[layer * Lc + c];
   const LayerInfo& lay = layers[layer];
@@ -139,7 +140,8 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
       const double2 v = make_double2(acc[gq][h], acc[gq][2 + h]);
       if (m < 4 * w) {
         const int idx = m / w, j = m - (m / w) * w;
-        tables[((((size_t)jid * Lc + c) * 4 + idx) * R + q) * wmax + j] = v;
+        double2* tp = tables + ((((size_t)jid * Lc + c) * 4 + idx) * R + q) * wmax + j;
+        *tp = accum ? cadd(*tp, v) : v;
       } else {
         const int mm = m - 4 * w, kk = mm >> 2, oi = mm & 3;
         const OJob& jb = jobs[jid];

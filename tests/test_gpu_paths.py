@@ -3,8 +3,9 @@ library reads the switches once per process).
 
 Default: pass-0 product + cooperative dense inner GMRES + sampled trace response.  The switches select
 the direct paths that the restructuring replaces: K1 passes (PT_NO_Q0, PT_NO_GSMP), the
-item-program inner GMRES (PT_NO_DENSE), the cluster dense inner GMRES (PT_NO_COOP), and the fused
-cooperative stage (PT_FUSE).  Each must reproduce the live-reference fixture with the same iteration
+item-program inner GMRES (PT_NO_DENSE), the cluster dense inner GMRES (PT_NO_COOP), the fused
+cooperative stage (PT_FUSE), and RECON's own first cell-solve pass instead of the saved Newton tables
+plus the pass-0 product (PT_NO_REUSE).  Each must reproduce the live-reference fixture with the same iteration
 counts and Green-block touches.
 """
 
@@ -46,6 +47,7 @@ SWITCHES = {
     "item-programs": {"PT_NO_DENSE": "1"},
     "cluster-dense": {"PT_NO_COOP": "1"},
     "fused-stage": {"PT_FUSE": "1"},
+    "recon-k1": {"PT_NO_REUSE": "1"},
 }
 
 
