@@ -1051,10 +1051,15 @@ cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st)
     return cudaErrorNotSupported;
   p.coop_region = (long long)region;
   const size_t sm = inner_coop_smem(p, region);
-  cudaFuncSetAttribute(inner_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_coop_kernel, IN_THREADS, sm);
-  if (per_sm < 1) return cudaErrorNotSupported;
+  set_smem_attr((const void*)inner_coop_kernel, sm);
+  static std::unordered_map<size_t, int> occ;  // co-residency per shared-memory size (queried once)
+  auto it = occ.find(sm);
+  if (it == occ.end()) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_coop_kernel, IN_THREADS, sm);
+    it = occ.emplace(sm, per_sm).first;
+  }
+  if (it->second < 1) return cudaErrorNotSupported;
   const int grid = nsm;  // one CTA per SM
   void* args[] = {(void*)&p, (void*)&nunits};
   int nu = nunits;
@@ -1073,8 +1078,12 @@ size_t inner_smem_bytes(int wmax, int nitems) {
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   if (njobs == 0 || p.Lc < 2) return cudaSuccess;
   const size_t sm = inner_smem_bytes(p.wmax, p.nitems);
-  cudaFuncSetAttribute(inner_gmres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaFuncSetAttribute(inner_gmres_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  set_smem_attr((const void*)inner_gmres_kernel, sm);
+  static bool nonportable = false;
+  if (!nonportable) {
+    cudaFuncSetAttribute(inner_gmres_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    nonportable = true;
+  }
   const int ngroups = (p.R + 7) / 8;
   const int nclusters = njobs * ngroups;
   static int nsm = 0;
@@ -1101,9 +1110,15 @@ cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   } else if (nclusters * 16 <= nsm) {
     cfg.gridDim = dim3(nclusters * 16, 1, 1);
     attr[0].val.clusterDim.x = 16;
-    int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, inner_gmres_kernel, &cfg) == cudaSuccess && active >= nclusters) cs = 16;
-    cudaGetLastError();
+    static std::unordered_map<size_t, int> act16;  // co-resident 16-CTA clusters per shared-memory size
+    auto it = act16.find(sm);
+    if (it == act16.end()) {
+      int active = 0;
+      if (cudaOccupancyMaxActiveClusters(&active, inner_gmres_kernel, &cfg) != cudaSuccess) active = 0;
+      cudaGetLastError();
+      it = act16.emplace(sm, active).first;
+    }
+    if (it->second >= nclusters) cs = 16;
   }
   cfg.gridDim = dim3(nclusters * cs, 1, 1);
   attr[0].val.clusterDim.x = cs;

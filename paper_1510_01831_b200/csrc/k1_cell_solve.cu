@@ -595,7 +595,7 @@ cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStre
   cfg.numAttrs = 1;
 #define PT_K1_GO(N, M)                                                                                \
   {                                                                                                   \
-    cudaFuncSetAttribute(k1_twisted<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);  \
+    set_smem_attr((const void*)k1_twisted<N, M>, smax);                                              \
     if (2 * p.cm > 8) cudaFuncSetAttribute(k1_twisted<N, M>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
     return cudaLaunchKernelEx(&cfg, k1_twisted<N, M>, p);                                             \
   }

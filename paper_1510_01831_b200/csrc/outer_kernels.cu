@@ -37,18 +37,21 @@ __global__ void __launch_bounds__(P0_KQ * 32) k_pass0(const int* __restrict__ gr
                                                       const LayerInfo* __restrict__ layers,
                                                       const double2* __restrict__ q0, const double2* __restrict__ P,
                                                       double2* __restrict__ tables, double2* __restrict__ smp, int R,
-                                                      int Lc, int wx, int wmax, int accum) {
+                                                      int Lc, int wx, int wmax, int accum, VecTab tab,
+                                                      const int* rmap, int direct) {
   __shared__ double part[(P0_KQ - 1) * 2 * 4 * 32];
   pass0_item(grp, ljobs, jobs, cells, layers, q0, P, tables, smp, R, Lc, wx, wmax, blockIdx.x / Lc,
-             blockIdx.x % Lc, blockIdx.y, blockIdx.z, threadIdx.x >> 5, part, 1, accum);
+             blockIdx.x % Lc, blockIdx.y, blockIdx.z, threadIdx.x >> 5, part, 1, accum, direct ? &tab : nullptr,
+             rmap);
 }
 
 __global__ void __launch_bounds__(GS_WARPS * 32) k_green_samples(
     const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells, const LayerInfo* __restrict__ layers,
     const double2* __restrict__ gsmp, const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,
-    int wmax) {
+    int wmax, VecTab tab, const int* rmap, int fuse_combine) {
   extern __shared__ double2 trs[];  // [4 slots][w4][8 rhs]
-  green_item(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax, blockIdx.x, blockIdx.y, blockIdx.z, trs);
+  green_item(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax, blockIdx.x, blockIdx.y, blockIdx.z, trs,
+             fuse_combine ? &tab : nullptr, rmap);
 }
 
 // dst[seg..] = a*x[seg..] (+ b*y[seg..]) over len elements, for the active RHS
@@ -229,15 +232,19 @@ __global__ void k_dense_tiles(const double2* src, double2* dst, int n, int kc) {
 // grid: x = job * Lc + cell, y = group of 8 RHS, z = chunk of kept block rows.
 cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                  const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,
-                                 int wmax, int kmax, int num_sms, cudaStream_t st) {
+                                 int wmax, int kmax, int num_sms, cudaStream_t st, const VecTab* tab,
+                                 const int* rmap) {
+  const int fuse_combine = tab != nullptr;
+  const VecTab tabv = tab ? *tab : VecTab{};
   (void)num_sms;
   if (J == 0 || R == 0) return cudaSuccess;
   const int gy = (R + 7) / 8;
   // rows per cell <= kmax kept block rows x 4 output rows; one 8-row tile per warp
   const int gz = (kmax * 4 + 8 * GS_WARPS - 1) / (8 * GS_WARPS);
   const size_t sm = sizeof(double2) * 4 * (size_t)((wmax + 3) & ~3) * 8;
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_green_samples, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_green_samples<<<dim3(J * Lc, gy, gz), GS_WARPS * 32, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax);
+  if (sm > 48 * 1024) set_smem_attr((const void*)k_green_samples, sm);
+  k_green_samples<<<dim3(J * Lc, gy, gz), GS_WARPS * 32, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax, tabv, rmap,
+                                                                        fuse_combine);
   return cudaGetLastError();
 }
 
@@ -251,11 +258,12 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
 cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
                          const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,
                          int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st,
-                         int accum) {
+                         int accum, const VecTab* tab, const int* rmap) {
   if (ngroups == 0 || R == 0) return cudaSuccess;
+  const VecTab tabv = tab ? *tab : VecTab{};
   const int mp = (4 * wmax + 4 * kmax + 7) / 8 * 8;
   const int gz = (max_jobs_per_layer * R + P0_COLS - 1) / P0_COLS;
   k_pass0<<<dim3(ngroups * Lc, mp / 8, gz), P0_KQ * 32, 0, st>>>(grp, ljobs, jobs, cells, layers, q0, P, tables, smp,
-                                                                 R, Lc, wx, wmax, accum);
+                                                                 R, Lc, wx, wmax, accum, tabv, rmap, tab != nullptr);
   return cudaGetLastError();
 }

@@ -4,6 +4,18 @@
 #include "pt_device.cuh"
 
 #define INNER_NC 8
+
+#include <unordered_map>
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs more than it was given so far:
+// the attribute calls cost microseconds of host time per launch otherwise
+inline void set_smem_attr(const void* fn, size_t bytes) {
+  static std::unordered_map<const void*, size_t> done;
+  size_t& v = done[fn];
+  if (bytes > v) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    v = bytes;
+  }
+}
 #define INNER_CS 8  // CTAs per inner-GMRES cluster (portable cluster size)
 #define PT_HIST 64
 
@@ -116,11 +128,12 @@ __host__ __device__ inline long long dense_matrix_elems(long long n) {
 cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
                          const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,
                          int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st,
-                         int accum = 0);  // PT_INNER_TPROF: print and reset CTA 0's segment clocks
+                         int accum = 0, const VecTab* tab = nullptr, const int* rmap = nullptr);  // PT_INNER_TPROF: print and reset CTA 0's segment clocks
 // smp += trace-source response (sampled Green rows) for every (job, cell, output row, RHS)
 cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                  const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,
-                                 int wmax, int kmax, int num_sms, cudaStream_t st);
+                                 int wmax, int kmax, int num_sms, cudaStream_t st, const VecTab* tab = nullptr,
+                                 const int* rmap = nullptr);
 
 __global__ void k_gather_panels(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
                                 double2* P);

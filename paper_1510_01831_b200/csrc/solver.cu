@@ -751,7 +751,22 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
       cudaGetLastError();
     }
   }
-  if (S.any_panel) {
+  // one-pass layer solve: samples = pass-0 samples + sampled trace responses (linearity)
+  static const bool no_gsmp = std::getenv("PT_NO_GSMP") != nullptr;
+  const bool gpath = c->Lc > 1 && c->gsmp_d && S.samples_only && !no_gsmp;
+  static const bool no_q0 = std::getenv("PT_NO_Q0") != nullptr;
+  const bool qpath = gpath && c->q0_d && S.no_volume && S.any_panel && S.grp_d && !no_q0;
+  // RECON: first pass by linearity = Newton tables of f (saved by the NEWTON stage) + pass-0 product of
+  // the trace panels (the jobs of both stages are the L layers in order, same RHS set)
+  static const bool no_reuse = std::getenv("PT_NO_REUSE") != nullptr;
+  const bool rpath = &S == &c->recon && c->tables_f_ok && c->q0_d && S.any_panel && S.grp_d && !no_reuse &&
+                     Ract == c->tables_f_R;
+  // opt-in (PT_FUSE_GLUE=1): gather and combine fused into the pass-0 product / sampled response where
+  // nothing else needs P or smp; measured slower on cfg2 (the panel refs are re-read in the inner loops)
+  static const bool no_fuse_glue = std::getenv("PT_FUSE_GLUE") == nullptr;
+  const bool direct_b = qpath && !no_fuse_glue;   // pass-0 reads the panels straight from the vectors
+  const bool fuse_comb = gpath && !no_fuse_glue;  // the sampled response writes the combined outputs
+  if (S.any_panel && !direct_b) {
     LaunchScope ls(c, 2);
     k_gather_panels<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract,
                                                                                     c->wx, c->P);
@@ -791,17 +806,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   kp.dbg = std::getenv("PT_K1_DBG") ? atoi(std::getenv("PT_K1_DBG")) : 0;
   // volume sources/outputs are indexed by the real RHS id: pre-offset through rmap on the host is not
   // possible per column, so stage buffers use compact q and f/u use q as well (callers compact f/u).
-  // one-pass layer solve: samples = pass-0 samples + sampled trace responses (linearity)
-  static const bool no_gsmp = std::getenv("PT_NO_GSMP") != nullptr;
-  const bool gpath = c->Lc > 1 && c->gsmp_d && S.samples_only && !no_gsmp;
   kp.s0 = gpath ? 1 : 0;
-  static const bool no_q0 = std::getenv("PT_NO_Q0") != nullptr;
-  const bool qpath = gpath && c->q0_d && S.no_volume && S.any_panel && S.grp_d && !no_q0;
-  // RECON: first pass by linearity = Newton tables of f (saved by the NEWTON stage) + pass-0 product of
-  // the trace panels (the jobs of both stages are the L layers in order, same RHS set)
-  static const bool no_reuse = std::getenv("PT_NO_REUSE") != nullptr;
-  const bool rpath = &S == &c->recon && c->tables_f_ok && c->q0_d && S.any_panel && S.grp_d && !no_reuse &&
-                     Ract == c->tables_f_R;
   if (c->Lc > 1) {
     kp.pass = 0;
     if (rpath) {
@@ -818,7 +823,8 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
         maxj = std::max(maxj, e - S.lgrp[i].second);
       }
       CK(pass0_launch(S.grp_d, (int)S.lgrp.size(), S.ljobs_d, S.jobs_d, c->cel_d, c->lay_d, c->q0_d, c->P, c->tables,
-                      c->smp, Ract, c->Lc, c->wx, c->wmax, c->wzcmax, maxj, c->st));
+                      c->smp, Ract, c->Lc, c->wx, c->wmax, c->wzcmax, maxj, c->st, 0, direct_b ? &tab : nullptr,
+                      c->rmap_d));
     } else {
       LaunchScope ls(c, 0);
       CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
@@ -840,7 +846,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   if (gpath) {
     LaunchScope ls(c, 3);
     CK(green_samples_launch(S.jobs_d, J, c->cel_d, c->lay_d, c->gsmp_d, c->trc, c->smp, Ract, c->Lc, c->wx,
-                            c->wmax, c->wzcmax, c->num_sms, c->st));
+                            c->wmax, c->wzcmax, c->num_sms, c->st, fuse_comb ? &tab : nullptr, c->rmap_d));
   } else {
     kp.pass = 1;
     kp.s0 = 0;
@@ -855,7 +861,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     fprintf(stderr, "K1 tprof nc=%d ntasks=%d: prologue %lld preload %lld bar1 %lld matvec %lld bar2 %lld epi %lld\n",
             T->nc, T->n, tt[0], tt[1], tt[2], tt[3], tt[4], tt[5]);
   }
-  if (S.any_sample) {
+  if (S.any_sample && !fuse_comb) {
     LaunchScope ls(c, 2);
     k_combine<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract, c->wx,
                                                                               c->smp);

@@ -60,7 +60,8 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
                                            const LayerInfo* __restrict__ layers, const double2* __restrict__ q0,
                                            const double2* __restrict__ P, double2* __restrict__ tables,
                                            double2* __restrict__ smp, int R, int Lc, int wx, int wmax, int g, int c,
-                                           int tile, int z, int wq, double* part, int barid, int accum = 0) {
+                                           int tile, int z, int wq, double* part, int barid, int accum = 0,
+                                           const VecTab* tabd = nullptr, const int* rmap = nullptr) {
   const int layer = grp[3 * g], jb0 = grp[3 * g + 1], nj = grp[3 * g + 2];
   const CellInfo& ci = cells[layer * Lc + c];
   const LayerInfo& lay = layers[layer];
@@ -74,14 +75,26 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
   const double2* arow = q0 + ci.q0_off + (size_t)(tile * 8 + ar) * K + ak;
   const double2* bcol[2];
   bool bok[2];
+  int jidg[2], rg[2];
 #pragma unroll
   for (int gq = 0; gq < 2; ++gq) {
     const int n = n0 + 8 * gq + ar;
     bok[gq] = n < N;
     const int jid = ljobs[jb0 + (bok[gq] ? n / R : 0)], q = bok[gq] ? n % R : 0;
+    jidg[gq] = jid;
+    rg[gq] = tabd ? rmap[q] : 0;
     bcol[gq] = P + ((size_t)(jid * 4) * R + q) * wx + ci.off + ci.lo + ak;
   }
   const size_t sstride = (size_t)R * wx;  // slot stride in P
+  // B element: the gathered panel P, or (tabd) the panel sum read straight from the outer vectors
+  auto bload = [&](int gq, int sl, int kk) -> double2 {
+    if (!tabd) return __ldg(bcol[gq] + sl * sstride + kk);
+    const Ref ra = jobs[jidg[gq]].pan[sl][0], rb = jobs[jidg[gq]].pan[sl][1];
+    const int x = ci.off + ci.lo + kk + ak;
+    double2 v = ra.vec >= 0 ? vref(*tabd, ra, rg[gq], x, wx) : make_double2(0.0, 0.0);
+    if (rb.vec >= 0) v = cadd(v, vref(*tabd, rb, rg[gq], x, wx));
+    return v;
+  };
   double acc[2][4];
 #pragma unroll
   for (int gq = 0; gq < 2; ++gq) acc[gq][0] = acc[gq][1] = acc[gq][2] = acc[gq][3] = 0.0;
@@ -97,7 +110,7 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
       av[u] = kin ? __ldg(arow + ks * 4) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int gq = 0; gq < 2; ++gq)
-        bv[u][gq] = (kin && bok[gq] && kk + ak < nk) ? __ldg(bcol[gq] + sl * sstride + kk) : make_double2(0.0, 0.0);
+        bv[u][gq] = (kin && bok[gq] && kk + ak < nk) ? bload(gq, sl, kk) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -166,7 +179,8 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
 __device__ __forceinline__ void green_item(const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
                                            const LayerInfo* __restrict__ layers, const double2* __restrict__ gsmp,
                                            const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc,
-                                           int wx, int wmax, int x, int y, int z, double2* trs) {
+                                           int wx, int wmax, int x, int y, int z, double2* trs,
+                                           const VecTab* tabd = nullptr, const int* rmap = nullptr) {
   __syncthreads();  // trs of the previous item consumed
   const int jid = x / Lc, c = x - (x / Lc) * Lc;
   const OJob& jb = jobs[jid];
@@ -220,7 +234,21 @@ __device__ __forceinline__ void green_item(const OJob* __restrict__ jobs, const 
     const int rr = 2 * ak + h;
     if (rr < nr) {
       double2* dst = smp + ((size_t)(jid * 4 + mo) * R + r0 + rr) * wx + ci.off + ci.lo + mk;
-      *dst = cadd(*dst, h == 0 ? make_double2(c0, c2) : make_double2(c1, c3));
+      const double2 yv = cadd(*dst, h == 0 ? make_double2(c0, c2) : make_double2(c1, c3));
+      if (!tabd) {
+        *dst = yv;
+      } else {  // combine fused in: out = scoef*sample + add - (sub0 + sub1) (k_combine)
+        const int xg = ci.off + ci.lo + mk, r = rmap[r0 + rr];
+        double2 o = cscale(yv, jb.scoef[mo]);
+        if (jb.add[mo].vec >= 0) o = cadd(o, vref(*tabd, jb.add[mo], r, xg, wx));
+        if (jb.sub[mo][0].vec >= 0) {
+          double2 sb = vref(*tabd, jb.sub[mo][0], r, xg, wx);
+          if (jb.sub[mo][1].vec >= 0) sb = cadd(sb, vref(*tabd, jb.sub[mo][1], r, xg, wx));
+          o = csub(o, sb);
+        }
+        const VecView& dv = tabd->v[jb.dst[mo].vec];
+        dv.p[(size_t)r * dv.stride + (size_t)jb.dst[mo].seg * wx + xg] = o;
+      }
     }
   }
 }
