@@ -254,6 +254,7 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
 #define DA_NS 8
 #define GV_MAX 128  // Arnoldi steps whose Givens state is staged in shared memory
 // One streaming pass over row tiles [t0, t1) of M for the instances rr[0..nact): see dense_apply.
+// src < 0: x is rhs_pol gathered from the Newton tables (negated) instead of a scratch vector.
 // ring/region: the shared-memory ring; dbar: DA_NS full + DA_NS empty barriers; the partial tiles reuse the
 // ring.  A ring slot holds SC stored chunks (SC = DA_T / nt, at most scmax) of the pass's tiles plus the
 // instances' x entries for those k-steps, so passes over few tiles still move large slots.
@@ -287,15 +288,33 @@ __device__ void dense_pass(const InnerParams& p, const double2* __restrict__ Mt,
       const int k0 = c * kslot, kx = min(kslot, nks - k0);
       const int nsub = min(sc, nchs - c * sc);
       unsigned char* sp = ring + (size_t)sl * slot_bytes;
-      if (lane == 0) {
-        if (g >= (unsigned)ns) mbar_wait(&empty[sl], ((g / ns) - 1) & 1);
-        mbar_expect_tx(&full[sl], (uint32_t)(nsub * nt * DA_KC * 512 + nact * kx * 64));
+      if (lane == 0 && g >= (unsigned)ns) mbar_wait(&empty[sl], ((g / ns) - 1) & 1);
+      __syncwarp();
+      if (src < 0) {
+        // x = rhs_pol gathered from the Newton tables (sie.py:230-242, negated) by the lanes of warp 0
+        const int nIc = p.Lc - 1, w = n / (4 * nIc);
+        double2* xs = reinterpret_cast<double2*>(sp + abytes);
+        for (int ix = lane; ix < nact * kx * 4; ix += 32) {
+          const int i = ix / (kx * 4), e = k0 * 4 + (ix - i * kx * 4);
+          const int seg = e / w, j = e - seg * w;
+          const int half = seg / (2 * nIc);  // 0 down, 1 up
+          const int I = (seg % (2 * nIc)) / 2, s_ = seg & 1;
+          const int cc = half == 0 ? I : I + 1;
+          const int idx = half == 0 ? 2 + s_ : s_;
+          const double2 tv = __ldcg(p.tables + ((((size_t)job * p.Lc + cc) * 4 + idx) * p.R + rr[i]) * p.wmax + j);
+          xs[i * XST + (e - k0 * 4)] = make_double2(-tv.x, -tv.y);
+        }
+        // these generic stores precede later bulk copies into the same slot; published by the arrive below
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
       }
+      if (lane == 0)
+        mbar_expect_tx(&full[sl], (uint32_t)(nsub * nt * DA_KC * 512 + (src >= 0 ? nact * kx * 64 : 0)));
       __syncwarp();
       if (lane < nsub)
         bulk_g2s(sp + (size_t)lane * nt * DA_KC * 512, Mt + ((size_t)(c * sc + lane) * T8 + tc) * DA_KC * 32,
                  (uint32_t)nt * DA_KC * 512u, &full[sl]);
-      if (lane < nact)
+      if (src >= 0 && lane < nact)
         bulk_g2s(sp + abytes + (size_t)lane * XST * 16, vecp(p, job, rr[lane], src) + (size_t)k0 * 4,
                  (uint32_t)kx * 64u, &full[sl]);
     };
@@ -415,7 +434,8 @@ __device__ void instance_init(const InnerParams& p, int job, int r, int n, int V
 }
 
 // MGS Arnoldi + complex Givens for instance r at step j (krylov.py:89-127): W = V_{j+1} holds pre(op(V_j))
-__device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, int n, double* dred) {
+__device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, int n, double* dred,
+                                 double wscale = 1.0) {
   const int tid = threadIdx.x;
   const size_t hld = (size_t)p.cap + 1;
   auto Hp = [&](int rr_) { return p.hess + (size_t)(job * p.R + rr_) * p.hstride; };
@@ -449,6 +469,8 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
     for (int t = 0; t < EPT; ++t) {
       const int e = tid + t * IN_THREADS;
       wv[t] = e < n ? ld_cg(W + e) : czero();
+      wv[t].x *= wscale;
+      wv[t].y *= wscale;
     }
     for (int i = 0; i <= j; ++i) {
       const double2* Vi = vecp(p, job, r, i);
@@ -477,6 +499,13 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
       ss += wv[t].x * wv[t].x + wv[t].y * wv[t].y;
     }
   } else {
+    if (wscale != 1.0) {
+      for (int e = tid; e < n; e += blockDim.x) {
+        const double2 x = ld_cg(W + e);
+        W[e] = make_double2(x.x * wscale, x.y * wscale);
+      }
+      __syncthreads();
+    }
     for (int i = 0; i <= j; ++i) {
       const double2* Vi = vecp(p, job, r, i);
       double sr = 0.0, si = 0.0;
@@ -596,6 +625,18 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
       W[e] = make_double2(x.x / hn, x.y / hn);
     }
   __syncthreads();
+}
+
+// b = Y = pre(rhs) and W = V_1 = pre(op(b)) (the product taken on the unnormalized b): beta0 = ||b||,
+// V_0 = b / beta0, then the Arnoldi step j = 0 on W / beta0 (= pre(op(V_0)) up to rounding)
+__device__ void instance_arnoldi0(const InnerParams& p, int job, int r, int n, int VY, double* dred) {
+  instance_init(p, job, r, n, VY, dred);
+  __shared__ double s_b0i;
+  if (threadIdx.x == 0) s_b0i = p.beta0[job * p.R + r];
+  __syncthreads();
+  const double b0 = s_b0i;
+  if (b0 == 0.0) return;  // converged with zero iterations (krylov.py:62-65)
+  instance_arnoldi(p, job, r, 0, n, dred, 1.0 / b0);
 }
 
 // x = V_k y (back substitution on the triangularized Hessenberg), traces = down + up (nested.py:153),
@@ -905,21 +946,6 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
     __syncthreads();
     gsync();
   }
-  // ---- rhs_pol from the Newton tables (sie.py:230-242, negated)
-  for (int u = 0; u < nunits; ++u) {
-    const int job = ujob(u), r0 = ur0(u), ni = uni(u), w = uw(u), n = 4 * nIc * w;
-    for (long long t = (long long)b * blockDim.x + tid; t < (long long)ni * n; t += (long long)G * blockDim.x) {
-      const int l = (int)(t / n), e = (int)(t - (long long)l * n), r = r0 + l;
-      const int seg = e / w, j = e - seg * w;
-      const int half = seg / (2 * nIc);  // 0 down, 1 up
-      const int I = (seg % (2 * nIc)) / 2, s_ = seg & 1;
-      const int c = half == 0 ? I : I + 1;
-      const int idx = half == 0 ? 2 + s_ : s_;
-      const double2 tv = __ldcg(p.tables + ((((size_t)job * p.Lc + c) * 4 + idx) * p.R + r) * p.wmax + j);
-      vecp(p, job, r, VB)[e] = make_double2(-tv.x, -tv.y);
-    }
-  }
-  gsync();
   unsigned dch = 0;
   // y = M_which x over the active instances of every unit; all = every instance (the first product)
   auto coop_apply = [&](int which, int src, int dst, bool all) {
@@ -955,22 +981,33 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
       T.tick(13);
     }
   };
-  // ---- b = pre(rhs) (krylov.py:61), beta0, V_0
-  T.tick(8);  // setup (rhs_pol) before the first barrier is in 5/7
+  // ---- rhs_pol from the Newton tables (sie.py:230-242, negated)
+  for (int u = 0; u < nunits; ++u) {
+    const int job = ujob(u), r0 = ur0(u), ni = uni(u), w = uw(u), n = 4 * nIc * w;
+    for (long long t = (long long)b * blockDim.x + tid; t < (long long)ni * n; t += (long long)G * blockDim.x) {
+      const int l = (int)(t / n), e = (int)(t - (long long)l * n), r = r0 + l;
+      const int seg = e / w, j = e - seg * w;
+      const int half = seg / (2 * nIc);  // 0 down, 1 up
+      const int I = (seg % (2 * nIc)) / 2, s_ = seg & 1;
+      const int c = half == 0 ? I : I + 1;
+      const int idx = half == 0 ? 2 + s_ : s_;
+      const double2 tv = __ldcg(p.tables + ((((size_t)job * p.Lc + c) * 4 + idx) * p.R + r) * p.wmax + j);
+      vecp(p, job, r, VB)[e] = make_double2(-tv.x, -tv.y);
+    }
+  }
+  gsync();
+  // ---- b = pre(rhs) (krylov.py:61)
+  T.tick(8);
   coop_apply(0, VB, VY, true);
   T.tick(3);
   gsync();
-  for (int t = b; t < nunits * 8; t += G) {
-    const int u = t >> 3, l = t & 7;
-    if (l < uni(u)) instance_init(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), VY, dred);
-  }
-  T.tick(6);
-  gsync();
   for (int j = 0; j < p.max_iter; ++j) {
-    load_states(false);
-    int any = 0;
-    for (int t = tid; t < nunits * 8; t += blockDim.x) any |= sst[t] == 0;
-    if (!__syncthreads_or(any)) break;
+    if (j > 0) {  // at j = 0 every instance enters (its state is set by the first Arnoldi step)
+      load_states(false);
+      int any = 0;
+      for (int t = tid; t < nunits * 8; t += blockDim.x) any |= sst[t] == 0;
+      if (!__syncthreads_or(any)) break;
+    }
     if (j + 1 > p.cap) {  // basis capacity exhausted: the host retries with a larger capacity
       for (int t = b; t < nunits * 8; t += G) {
         const int u = t >> 3, l = t & 7;
@@ -987,14 +1024,18 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
       break;
     }
     T.tick(4);  // loop head (active scan)
-    coop_apply(1, j, j + 1, false);  // w = pre(op(V_j))
+    // w = pre(op(V_j)); at j = 0 on the unnormalized b (every instance: beta0 is taken in the Arnoldi step)
+    coop_apply(1, j == 0 ? VY : j, j + 1, j == 0);
     T.tick(3);
     gsync();
     for (int t = b; t < nunits * 8; t += G) {
       const int u = t >> 3, l = t & 7;
       if (l >= uni(u)) continue;
       const int job = ujob(u), r = ur0(u) + l;
-      if (__ldcg(p.state + job * p.R + r) == 0) instance_arnoldi(p, job, r, j, 4 * nIc * uw(u), dred);
+      if (j == 0)
+        instance_arnoldi0(p, job, r, 4 * nIc * uw(u), VY, dred);
+      else if (__ldcg(p.state + job * p.R + r) == 0)
+        instance_arnoldi(p, job, r, j, 4 * nIc * uw(u), dred);
     }
     T.tick(6);
     gsync();
