@@ -1066,6 +1066,8 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
   }
 }
 
+int inner_coop_max_units() { return COOP_MAXU; }
+
 size_t inner_coop_smem(const InnerParams& p, size_t region) {
   return region + 2 * DA_NS * 8 + 64 * 8 + (COOP_MAXU + 1) * 4 + COOP_MAXU * 4 + 2 * COOP_MAXU * 8 + 128 +
          (size_t)(p.cap + 2 + 24 + 300 + 24) * 16 + 128;

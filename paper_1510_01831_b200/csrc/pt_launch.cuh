@@ -116,6 +116,7 @@ int inner_mg(int wmax);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
 // whole-GPU cooperative inner GMRES (dense operators); cudaErrorNotSupported: use inner_launch
 cudaError_t inner_coop_launch(const InnerParams& p, int njobs, cudaStream_t st);
+int inner_coop_max_units();  // (job, 8-RHS group) units one cooperative inner launch holds
 void inner_tprof_dump(const char* tag);
 __global__ void k_dense_tiles(const double2* src, double2* dst, int n, int kc);
 #define DA_KC 8  // k-steps per dense-apply chunk (inner_gmres.cu; the stored fragment layout depends on it)

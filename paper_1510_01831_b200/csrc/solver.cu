@@ -1579,9 +1579,7 @@ int pt_destroy(pt_ctx* c) {
   return PT_OK;
 }
 
-int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats) {
-  if (!c || !f || !u || !cfg) return PT_BAD_ARGUMENT;
-  CK(cudaSetDevice(c->dev));
+static int solve_batch(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats) {
   int rc;
   for (int attempt = 0; attempt < 4; ++attempt) {
     rc = solve_device(c, reinterpret_cast<const double2*>(f), nrhs, cfg, reinterpret_cast<double2*>(u), stats);
@@ -1592,6 +1590,85 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
     c->capO = 0;
   }
   return rc;
+}
+
+// RHS per lockstep batch: every stage's inner GMRES runs as ONE cooperative launch over its (job, group of
+// 8 RHS) units, which holds at most inner_coop_max_units() units (the widest stage has max(2L-2, L) jobs)
+static int batch_rhs(const pt_ctx* c) {
+  const int maxj = std::max(std::max((int)c->op.jobs.size(), (int)c->newton.jobs.size()),
+                            std::max((int)c->recon.jobs.size(), (int)c->refl.jobs.size()));
+  if (c->Lc < 2 || maxj == 0) return 1 << 30;
+  return 8 * std::max(1, inner_coop_max_units() / maxj);
+}
+
+int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats) {
+  if (!c || !f || !u || !cfg) return PT_BAD_ARGUMENT;
+  CK(cudaSetDevice(c->dev));
+  const int B = batch_rhs(c);
+  if (nrhs <= B) return solve_batch(c, f, nrhs, cfg, u, stats);
+  // large source sets: consecutive lockstep batches; per-RHS outputs land at their offsets, totals add up
+  const long long N = 2LL * c->wz * c->wx;  // doubles per wavefield
+  const long long nO = 4LL * c->nI * c->wx;
+  pt_stats acc;
+  std::memset(&acc, 0, sizeof(acc));
+  long long ls = 0, ii = 0, to = 0, la = 0, k1l = 0;
+  double tms = 0, kms[3] = {0, 0, 0}, k1b = 0, cms[5] = {0, 0, 0, 0, 0}, dfl = 0;
+  std::vector<int> hist(stats && stats->inner_hist_len > 0 ? stats->inner_hist_len : 0, 0);
+  int worst = PT_OK;
+  for (int r0 = 0; r0 < nrhs; r0 += B) {
+    const int nb = std::min(B, nrhs - r0);
+    pt_stats sb;
+    std::memset(&sb, 0, sizeof(sb));
+    long long bls = 0, bii = 0, bto = 0, bla = 0, bk1l = 0;
+    double btms = 0, bkms[3] = {0, 0, 0}, bk1b = 0, bcms[5] = {0, 0, 0, 0, 0}, bdfl = 0;
+    std::vector<int> bh(hist.size(), 0);
+    if (stats) {
+      const int mi = cfg->max_iter;
+      sb.iterations = stats->iterations ? stats->iterations + r0 : nullptr;
+      sb.residuals = stats->residuals ? stats->residuals + (size_t)r0 * mi : nullptr;
+      sb.n_residuals = stats->n_residuals ? stats->n_residuals + r0 : nullptr;
+      sb.relres = stats->relres ? stats->relres + r0 : nullptr;
+      sb.converged = stats->converged ? stats->converged + r0 : nullptr;
+      sb.traces = stats->traces ? stats->traces + (size_t)r0 * nO : nullptr;
+      sb.polarized = stats->polarized ? stats->polarized + (size_t)r0 * 2 * nO : nullptr;
+      sb.layer_solves = &bls;
+      sb.inner_iters = &bii;
+      sb.touches = &bto;
+      sb.inner_hist = bh.empty() ? nullptr : bh.data();
+      sb.inner_hist_len = (int)bh.size();
+      sb.timing_ms = &btms;
+      sb.kernel_ms = bkms;
+      sb.k1_bytes = &bk1b;
+      sb.launches = &bla;
+      sb.k1_launches = &bk1l;
+      sb.class_ms = bcms;
+      sb.dense_flops = &bdfl;
+    }
+    const int rc = solve_batch(c, f + (size_t)r0 * N, nb, cfg, u + (size_t)r0 * N, stats ? &sb : nullptr);
+    if (rc != PT_OK && rc != PT_NOT_CONVERGED) return rc;
+    if (rc == PT_NOT_CONVERGED) worst = rc;
+    ls += bls, ii += bii, to += bto, la += bla, k1l += bk1l, tms += btms, k1b += bk1b, dfl += bdfl;
+    for (int i = 0; i < 3; ++i) kms[i] += bkms[i];
+    for (int i = 0; i < 5; ++i) cms[i] += bcms[i];
+    for (size_t i = 0; i < hist.size(); ++i) hist[i] += bh[i];
+  }
+  if (stats) {
+    if (stats->layer_solves) stats->layer_solves[0] = ls;
+    if (stats->inner_iters) stats->inner_iters[0] = ii;
+    if (stats->touches) stats->touches[0] = to;
+    for (size_t i = 0; i < hist.size(); ++i) stats->inner_hist[i] = hist[i];
+    if (stats->timing_ms) stats->timing_ms[0] = tms;
+    if (stats->kernel_ms)
+      for (int i = 0; i < 3; ++i) stats->kernel_ms[i] = kms[i];
+    if (stats->k1_bytes) stats->k1_bytes[0] = k1b;
+    if (stats->launches) stats->launches[0] = la;
+    if (stats->k1_launches) stats->k1_launches[0] = k1l;
+    if (stats->class_ms)
+      for (int i = 0; i < 5; ++i) stats->class_ms[i] = cms[i];
+    if (stats->dense_flops) stats->dense_flops[0] = dfl;
+  }
+  if (worst != PT_OK) g_err = "outer GMRES did not reach ktol within max_iter";
+  return worst;
 }
 
 int pt_solve(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats) {

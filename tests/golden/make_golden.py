@@ -111,7 +111,18 @@ def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1):
     return out
 
 
-def main():
+BIG = {"cfg1": 4, "cfg2": 8, "cfg3": 8, "cfg4": 8, "cfg5": 12}  # wavefield decimation
+
+
+def main(argv):
+    # ``make_golden.py cfg3 [cfg4 ...]`` regenerates only the named large configs
+    # (cfg3 takes minutes, cfg4 tens of minutes, cfg5 hours on the reference)
+    if argv:
+        for name in argv:
+            prob = make_config(name)
+            out = run_case(prob, 0, full_u=False, decim=BIG[name])
+            np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+        return
     cases = {
         "small_a": (small_problem(nx=40, nz=36, npml=6, L=3, Lc=2, omega=14.0, seed=0), 0, True),
         "small_b": (small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, True),
@@ -129,4 +140,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])

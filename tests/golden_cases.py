@@ -10,4 +10,5 @@ GOLDEN = {
                      False),
     "cfg1": (lambda: make_config("cfg1"), 0, True),
     "cfg2": (lambda: make_config("cfg2"), 0, True),
+    "cfg3": (lambda: make_config("cfg3"), 0, True),
 }
