@@ -32,6 +32,7 @@ namespace cg = cooperative_groups;
 
 #define IN_MG 2   // max 8-row tiles per group (2 for w <= 80, else 1)
 #define IN_THREADS 256
+#define IN_TRMAX 16  // max Green-tile ring slots of the item-program path
 
 __device__ __forceinline__ double2* vecp(const InnerParams& p, int job, int r, int v) {
   return p.scratch + (size_t)(job * p.R + r) * p.inst_stride + (size_t)v * p.nmax;
@@ -58,11 +59,11 @@ struct Ticker {
 };
 
 struct InSmem {
-  double2* tiles;   // [2 buffers][4 slots][IN_MG][w][8]
+  double2* tiles;   // [p.tring][w][8] ring of single Green tiles
   double2* pan;     // [4 slots][w][8]
   double2* pan2;    // [2][w][8] second terms of two-term panels
   double2* red;     // [8 warps][IN_MG*8][8]
-  uint64_t* tbar;   // [2] one mbarrier per tile buffer
+  uint64_t* tbar;   // [IN_TRMAX] one mbarrier per tile ring slot
   int* act;         // active local instances
   IItem* items;     // the op + pre programs (staged once)
   long long* goff;  // [Lc] Green-pool offsets of this layer's cells (staged once)
@@ -75,7 +76,7 @@ struct InSmem {
 // Execute one program (list of phases) for the active instances of this cluster.
 // vmap: program vec ids {0:IN,1:OUT,2:AUX} -> scratch vector index.
 __device__ void run_program(const InnerParams& p, int job, int layer, int w, int r0, const int* ph, int nph,
-                            const int vmap[3], int nact, const InSmem& S, int q, int CS, uint32_t* tphase,
+                            const int vmap[3], int nact, const InSmem& S, int q, int CS, uint32_t* tseq,
                             Ticker& T) {
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   const int nmt = (w + 7) >> 3;
@@ -112,24 +113,39 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
           if (item.pan[s][0].vec >= 0) slotp |= s << (2 * ns++);
       auto slot_of = [&](int si) { return slotp >> (2 * si) & 3; };
       const long long goff = S.goff[item.cell >= 0 ? item.cell : 0];
-      // called by all of warp 0: lane 0 arms the barrier, then one lane per (slot, tile) issues its bulk copy
-      auto issue_tiles = [&](int g, int buf) {
-        const int mt0 = g * MG, nt = min(MG, nmt - mt0);
-        if (lane == 0) mbar_expect_tx(&S.tbar[buf], tbytes * (uint32_t)(ns * nt));
-        __syncwarp();
-        if (lane < ns * nt) {
-          const int si = lane / nt, t = lane - (lane / nt) * nt;
-          bulk_g2s(S.tiles + buf * tbuf + ((size_t)si * MG + t) * w * 8,
-                   p.green + goff + ((size_t)(item.row * 4 + slot_of(si)) * nmt + mt0 + t) * w * 8, tbytes,
-                   &S.tbar[buf]);
-        }
+      // The unit's Green tiles stream through a ring of p.tring single-tile slots (one 8-row tile of one slot
+      // block per copy, so the ring fits any w <= 128): local tile j = (group g0 + j / (ns MG), then slot-major
+      // (si, t) within the group).  tseq counts this CTA's tiles across units and programs (slot tseq % TR,
+      // mbarrier parity (tseq / TR) & 1).  Issued by lane 0 of warp 0; consumers release a slot at the
+      // __syncthreads that ends its tile.
+      const int TR = p.tring;
+      auto tile_of = [&](int j, int& g, int& si, int& t) {
+        const int per = ns * MG;
+        g = g0 + j / per;
+        const int mt0 = g * MG, nt = min(MG, nmt - mt0), rem = j - (j / per) * per;
+        si = rem / nt;
+        t = rem - si * nt;
+      };
+      int ntl = 0;
+      for (int g = g0; g < g1; ++g) ntl += ns * min(MG, nmt - g * MG);
+      const uint32_t tbase = *tseq;
+      auto issue_tile = [&](int j) {  // lane 0 of warp 0 only
+        int g, si, t;
+        tile_of(j, g, si, t);
+        const uint32_t sq = tbase + (uint32_t)j;
+        const int slot = (int)(sq % (uint32_t)TR);
+        mbar_expect_tx(&S.tbar[slot], tbytes);
+        bulk_g2s(S.tiles + (size_t)slot * w * 8,
+                 p.green + goff + ((size_t)(item.row * 4 + slot_of(si)) * nmt + g * MG + t) * w * 8, tbytes,
+                 &S.tbar[slot]);
       };
       int negm = 0;  // bit si: slot panel si enters negated (exact)
       for (int si = 0; si < ns; ++si) negm |= (item.flags >> slot_of(si) & 1) << si;
       int twom = 0;  // bit si: two-term slot panel (d + p); its second term is staged in pan2
       for (int si = 0; si < ns; ++si) twom |= (item.pan[slot_of(si)][1].vec >= 0) << si;
       if (ns > 0) {
-        if (wp == 0) issue_tiles(g0, 0);
+        if (tid == 0)
+          for (int j = 0; j < min(TR, ntl); ++j) issue_tile(j);
         T.tick(13);  // tile issue
         // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill).
         // IN_THREADS % 8 == 0, so a thread's instance qq is fixed and its scratch base is computed once.
@@ -149,11 +165,10 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
         }
       }
       T.tick(0);
+      int jt = 0;  // next local tile to consume
       for (int g = g0; g < g1; ++g) {
-        const int buf = (g - g0) & 1;
         const int mt0 = g * MG, nt = min(MG, nmt - mt0);
         const int row0 = mt0 * 8, rows = min(w, row0 + nt * 8) - row0;
-        if (ns > 0 && wp == 0 && g + 1 < g1) issue_tiles(g + 1, buf ^ 1);  // buffer freed last iteration
         // this thread's output (row, instance) and its combine operands
         const int oq = tid & 7, orow = tid >> 3;
         const bool own = orow < rows && oq < nact;
@@ -175,37 +190,42 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
             __syncthreads();
           }
           T.tick(1);
-          mbar_wait(&S.tbar[buf], tphase[buf] & 1);
-          tphase[buf]++;
-          T.tick(2);
-          // DMMA: warp wp takes k-steps ks = wp mod 8 of every slot, both tiles of the group:
+          // DMMA: per tile (slot si, row tile t) warp wp takes k-steps wp, wp + 8, ... of the slot:
           // Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br
           const int ar = lane >> 2, ak = lane & 3;
           double c[IN_MG][4];
 #pragma unroll
           for (int t = 0; t < IN_MG; ++t) c[t][0] = c[t][1] = c[t][2] = c[t][3] = 0.0;
-          const double2* tl = S.tiles + buf * tbuf;
-          const int nks = ns * kps;
-          for (int ks = wp; ks < nks; ks += IN_THREADS / 32) {
-            const int si = ks / kps, k = (ks - si * kps) * 4 + ak;
-            const bool kin = k < w;
-            double2 bv = kin ? S.pan[((size_t)si * w + k) * 8 + ar] : czero();
-            if (twom >> si & 1) {  // d + p, summed in the reference's order
-              const int i2 = __popc(twom & ((1 << si) - 1));
-              bv = cadd(bv, kin ? S.pan2[((size_t)i2 * w + k) * 8 + ar] : czero());
-            }
+          for (int si = 0; si < ns; ++si) {
             const double sg = (negm >> si & 1) ? -1.0 : 1.0;
-            bv.x *= sg;
-            bv.y *= sg;
+            const bool two = twom >> si & 1;
+            const int i2 = __popc(twom & ((1 << si) - 1));
+            for (int t = 0; t < nt; ++t, ++jt) {
+              const uint32_t sq = tbase + (uint32_t)jt;
+              const int slot = (int)(sq % (uint32_t)TR);
+              T.tick(1);
+              mbar_wait(&S.tbar[slot], (sq / (uint32_t)TR) & 1);
+              T.tick(2);
+              const double2* tl = S.tiles + (size_t)slot * w * 8;
+              for (int ks = wp; ks < kps; ks += IN_THREADS / 32) {
+                const int k = ks * 4 + ak;
+                const bool kin = k < w;
+                double2 bv = kin ? S.pan[((size_t)si * w + k) * 8 + ar] : czero();
+                if (two) bv = cadd(bv, kin ? S.pan2[((size_t)i2 * w + k) * 8 + ar] : czero());  // d + p
+                bv.x *= sg;
+                bv.y *= sg;
+                const double2 av = kin ? tl[(size_t)k * 8 + ar] : czero();
 #pragma unroll
-            for (int t = 0; t < IN_MG; ++t) {
-              if (t < nt) {
-                const double2 av = kin ? tl[(((size_t)si * MG + t) * w + k) * 8 + ar] : czero();
-                dmma_f64(c[t][0], c[t][1], av.x, bv.x);
-                dmma_f64(c[t][2], c[t][3], av.x, bv.y);
-                dmma_f64(c[t][0], c[t][1], -av.y, bv.y);
-                dmma_f64(c[t][2], c[t][3], av.y, bv.x);
+                for (int tt = 0; tt < IN_MG; ++tt)
+                  if (tt == t) {
+                    dmma_f64(c[tt][0], c[tt][1], av.x, bv.x);
+                    dmma_f64(c[tt][2], c[tt][3], av.x, bv.y);
+                    dmma_f64(c[tt][0], c[tt][1], -av.y, bv.y);
+                    dmma_f64(c[tt][2], c[tt][3], av.y, bv.x);
+                  }
               }
+              __syncthreads();  // slot free
+              if (tid == 0 && jt + TR < ntl) issue_tile(jt + TR);
             }
           }
 #pragma unroll
@@ -233,6 +253,7 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
         __syncthreads();
         T.tick(4);
       }
+      *tseq += (uint32_t)ntl;
     }
     csync();
     T.tick(5);
@@ -733,13 +754,13 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
 
   InSmem S;
   S.tiles = reinterpret_cast<double2*>(smem);
-  S.pan = S.tiles + (size_t)2 * 4 * p.mg * p.wmax * 8;
+  S.pan = S.tiles + (size_t)p.tring * p.wmax * 8;
   S.pan2 = S.pan + (size_t)4 * p.wmax * 8;
   S.red = S.pan2 + (size_t)2 * p.wmax * 8;
   double* dred = reinterpret_cast<double*>(S.red + (IN_THREADS / 32) * IN_MG * 8 * 8);
   S.tbar = reinterpret_cast<uint64_t*>(dred + 64);
   S.region = (size_t)(reinterpret_cast<unsigned char*>(dred) - reinterpret_cast<unsigned char*>(S.tiles));
-  S.dbar = S.tbar + 2;
+  S.dbar = S.tbar + IN_TRMAX;
   S.act = reinterpret_cast<int*>(S.dbar + 2 * DA_NS);
   S.goff = reinterpret_cast<long long*>(S.act + 16);
   S.oph = reinterpret_cast<int*>(S.goff + PT_MAX_LC);
@@ -748,8 +769,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   __shared__ int s_nact;
   if (nIc == 0) return;
   if (tid == 0) {
-    mbar_init(&S.tbar[0], 1);
-    mbar_init(&S.tbar[1], 1);
+    for (int i = 0; i < IN_TRMAX; ++i) mbar_init(&S.tbar[i], 1);
     for (int i = 0; i < DA_NS; ++i) {
       mbar_init(&S.dbar[i], 1);
       mbar_init(&S.dbar[DA_NS + i], IN_THREADS / 32);
@@ -760,7 +780,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
   for (int i = tid; i <= p.op_nph; i += blockDim.x) S.oph[i] = p.op_ph[i];
   for (int i = tid; i <= p.pre_nph; i += blockDim.x) S.pph[i] = p.pre_ph[i];
   for (int i = tid; i < p.Lc; i += blockDim.x) S.goff[i] = p.cells[layer * p.Lc + i].green_off;
-  uint32_t tphase[2] = {0, 0};
+  uint32_t tseq = 0;
   Ticker T;
   T.on = p.tprof && blockIdx.x == 0 && tid == 0;
   T.start();
@@ -799,7 +819,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
     T.tick(3);
   } else {
     const int vm[3] = {VB, VY, VA};
-    run_program(p, job, layer, w, r0, S.pph, p.pre_nph, vm, s_nact, S, q, CS, tphase, T);
+    run_program(p, job, layer, w, r0, S.pph, p.pre_nph, vm, s_nact, S, q, CS, &tseq, T);
   }
   for (int l = q; l < ni; l += CS) instance_init(p, job, r0 + l, n, VY, dred);
   csync();
@@ -825,9 +845,9 @@ __global__ void __launch_bounds__(IN_THREADS, 1)
       T.tick(3);
     } else {
       const int vm1[3] = {j, VT, VA};
-      run_program(p, job, layer, w, r0, S.oph, p.op_nph, vm1, nact, S, q, CS, tphase, T);
+      run_program(p, job, layer, w, r0, S.oph, p.op_nph, vm1, nact, S, q, CS, &tseq, T);
       const int vm2[3] = {VT, j + 1, VA};
-      run_program(p, job, layer, w, r0, S.pph, p.pre_nph, vm2, nact, S, q, CS, tphase, T);
+      run_program(p, job, layer, w, r0, S.pph, p.pre_nph, vm2, nact, S, q, CS, &tseq, T);
       T.tick(7);
     }
     // ---- MGS Arnoldi + Givens for the instances this CTA owns (krylov.py:89-127)
@@ -1112,15 +1132,41 @@ cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st)
 
 int inner_mg(int wmax) { return wmax <= 80 ? 2 : 1; }
 
-size_t inner_smem_bytes(int wmax, int nitems) {
+// shared memory of the cluster kernel without its Green-tile ring
+static size_t inner_smem_fixed(int wmax, int nitems) {
   const int w = wmax < 8 ? 8 : wmax;
-  return (size_t)(2 * 4 * inner_mg(wmax) + 4 + 2) * w * 8 * 16 + (size_t)(IN_THREADS / 32) * IN_MG * 8 * 8 * 16 + 64 * 8 +
-         16 + 2 * DA_NS * 8 + 64 + PT_MAX_LC * 8 + 2 * (2 * PT_MAX_LC + 2) * 4 + (size_t)nitems * sizeof(IItem) + 128;
+  return (size_t)(4 + 2) * w * 8 * 16 + (size_t)(IN_THREADS / 32) * IN_MG * 8 * 8 * 16 + 64 * 8 + IN_TRMAX * 8 +
+         2 * DA_NS * 8 + 64 + PT_MAX_LC * 8 + 2 * (2 * PT_MAX_LC + 2) * 4 + (size_t)nitems * sizeof(IItem) + 128;
+}
+
+// Green-tile ring slots: as many single tiles (8 rows x w) as fit next to the rest (<= IN_TRMAX, >= 2)
+int inner_tring(int wmax, int nitems) {
+  static int maxsm = 0;
+  if (!maxsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  const int w = wmax < 8 ? 8 : wmax;
+  // (static __shared__ of the kernel and alignment slack come off the opt-in limit)
+  long long room = (long long)maxsm - 8192 - (long long)inner_smem_fixed(wmax, nitems);
+  if (const char* e = std::getenv("PT_TRING")) room = std::min(room, (long long)atoi(e) * w * 8 * 16);
+  const long long t = room / ((long long)w * 8 * 16);
+  return (int)std::max(0LL, std::min((long long)IN_TRMAX, t));
+}
+
+size_t inner_smem_bytes(int wmax, int nitems, int tring) {
+  const int w = wmax < 8 ? 8 : wmax;
+  return inner_smem_fixed(wmax, nitems) + (size_t)tring * w * 8 * 16;
 }
 
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   if (njobs == 0 || p.Lc < 2) return cudaSuccess;
-  const size_t sm = inner_smem_bytes(p.wmax, p.nitems);
+  if (p.tring < 2) {  // program items do not fit in shared memory
+    fprintf(stderr, "inner_launch: %d program items leave no room for the Green-tile ring\n", p.nitems);
+    return cudaErrorInvalidValue;
+  }
+  const size_t sm = inner_smem_bytes(p.wmax, p.nitems, p.tring);
   set_smem_attr((const void*)inner_gmres_kernel, sm);
   static bool nonportable = false;
   if (!nonportable) {
@@ -1148,9 +1194,18 @@ cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   // Clusters of 16 CTAs (twice the FP64 tensor throughput per RHS group) when they all fit at once;
   // otherwise the portable 8.  PT_INNER_CS overrides.
   int cs = INNER_CS;
+  static int occ1 = -1;  // co-resident CTAs per SM at this kernel's shared-memory size
+  if (occ1 < 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, inner_gmres_kernel, IN_THREADS, sm);
+    cudaGetLastError();
+    occ1 = std::max(occ1, 1);
+  }
   if (const char* e = std::getenv("PT_INNER_CS")) {
-    cs = atoi(e) >= 16 ? 16 : INNER_CS;
-  } else if (nclusters * 16 <= nsm) {
+    const int v = atoi(e);
+    cs = v >= 16 ? 16 : (v >= 8 ? 8 : (v >= 4 ? 4 : (v >= 2 ? 2 : 1)));
+  } else if (nclusters * 16 <= nsm * occ1) {
+    // (smaller clusters over more waves were measured slower: a unit's phases are latency-bound, cfg4
+    // 9.3 / 16.2 / 25.6 s per 256-source step at 8 / 4 / 2 CTAs per cluster)
     cfg.gridDim = dim3(nclusters * 16, 1, 1);
     attr[0].val.clusterDim.x = 16;
     static std::unordered_map<size_t, int> act16;  // co-resident 16-CTA clusters per shared-memory size
@@ -1165,7 +1220,11 @@ cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   }
   cfg.gridDim = dim3(nclusters * cs, 1, 1);
   attr[0].val.clusterDim.x = cs;
-  return cudaLaunchKernelEx(&cfg, inner_gmres_kernel, p);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, inner_gmres_kernel, p);
+  if (e != cudaSuccess)
+    fprintf(stderr, "inner_launch: %s (smem %zu, tring %d, nitems %d, wmax %d, clusters %d x %d)\n",
+            cudaGetErrorString(e), sm, p.tring, p.nitems, p.wmax, nclusters, cs);
+  return e;
 }
 
 void inner_tprof_dump(const char* tag) {

@@ -98,6 +98,7 @@ struct InnerParams {
   int tprof;              // debug: accumulate clock64 segment totals of CTA 0 (PT_INNER_TPROF)
   int nitems;             // op + pre program items (staged in shared memory)
   int mg;                 // 8-row Green tiles per work group (inner_mg(wmax))
+  int tring;              // Green-tile ring slots of the item-program path (inner_tring)
 };
 
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns);
@@ -111,7 +112,8 @@ cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStrea
 // DFMA path: columns per consumer warp per ring chunk (7 warps per chunk)
 __host__ __device__ constexpr int k1_jw(int nc) { return nc == 1 ? 5 : (nc == 2 ? 4 : 2); }
 #define K1_JC8 12        // ring chunk width (columns) of the DMMA path: 3 k-steps
-size_t inner_smem_bytes(int wmax, int nitems);
+size_t inner_smem_bytes(int wmax, int nitems, int tring);
+int inner_tring(int wmax, int nitems);
 int inner_mg(int wmax);
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
 // whole-GPU cooperative inner GMRES (dense operators); cudaErrorNotSupported: use inner_launch

@@ -697,6 +697,7 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   ip.tprof = std::getenv("PT_INNER_TPROF") != nullptr;
   ip.nitems = c->nitems;
   ip.mg = inner_mg(c->wmax);
+  ip.tring = inner_tring(c->wmax, ip.nitems);
   return ip;
 }
 

@@ -350,7 +350,10 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
     if q0 is None:
         q0 = green
     if inner_dense is None:
-        inner_dense = green
+        # dense pre / pre.op matrices cost 128 (Lc-1)^2 w^2 flops per inner product against the Green-block
+        # programs' O(Lc w^2): one product wins up to Lc = 8 (measured on cfg2 and cfg3); the memory
+        # (2 (4 (Lc-1) w)^2 per layer) also grows with (Lc-1)^2
+        inner_dense = green and Lc <= 8
     npml, h, omega = grid.npml, grid.h, pml.omega
     cext = _split(grid.nx, Lc)  # partition_layers(sgrid, Lc), nested.py:294-296
     coffs = tuple(int(v) for v in np.concatenate([[0], np.cumsum(cext)[:-1]]))

@@ -138,12 +138,15 @@ class LayerDescriptor:
 
 def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), Lc=1, backend="pt",
                         inner_ktol=1e-6, inner_max_iter=200, plr_threshold=None, plr_eps=1e-8,
-                        plr_max_rank=None, seed=0, assembled_boundary=False, device=None, **unused):
+                        plr_max_rank=None, seed=0, assembled_boundary=False, device=None, inner_dense=None,
+                        **unused):
     """``nested.py:507-521`` (with ``NestedLayerSolver`` kwargs, ``nested.py:279-281``).
 
     Runs the offline stage (Schur factors + Green blocks) for every layer.
     ``device`` selects where the offline arithmetic runs (``"cpu"`` or a CUDA
     device for large configs); its output is uploaded by the solver.
+    ``inner_dense`` (None = by Lc) builds the dense inner operators that let
+    the inner GMRES run as one dense product per step.
     """
     if backend != "pt":
         raise NotImplementedError("only the polarized-traces inner backend ('pt') has a B200 path")
@@ -157,7 +160,7 @@ def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), 
         raise ValueError("need at least one cell")
     if Lc > 1 and grid.nx < 2 * Lc:
         raise ValueError(f"{Lc} cells need nx >= {2 * Lc}, got {grid.nx}")
-    F = build_factors(grid, model, pml, partition, Lc, device=device or "cpu")
+    F = build_factors(grid, model, pml, partition, Lc, device=device or "cpu", inner_dense=inner_dense)
     items = []
     for ell, (n, off) in enumerate(zip(partition.extents, partition.offsets)):
         lgrid = Grid(grid.nx, n, grid.h, grid.npml, origin=(grid.origin[0], grid.origin[1] + off))

@@ -11,4 +11,6 @@ GOLDEN = {
     "cfg1": (lambda: make_config("cfg1"), 0, True),
     "cfg2": (lambda: make_config("cfg2"), 0, True),
     "cfg3": (lambda: make_config("cfg3"), 0, True),
+    "cfg4": (lambda: make_config("cfg4"), 0, True),
+    "cfg5": (lambda: make_config("cfg5"), 0, True),
 }

@@ -61,3 +61,17 @@ def test_cfg2_known_answer_anchors():
     assert abs(float(g["unorm"]) - 10.37541) < 1e-5
     assert int(g["touches"]) == 118_227_200
     assert len(g["inner_iterations"]) == 134  # N_ls = 2L + (3L-5) + k(5L-7), L=8, k=3
+
+
+@pytest.mark.parametrize("name,L,its", [("cfg3", 16, 7), ("cfg4", 20, 9), ("cfg5", 32, 11)])
+def test_large_config_fixtures_are_consistent(name, L, its):
+    """cfg3-5 fixtures (live reference, one source each; too slow to re-run the oracle here): the outer
+    iteration count, a monotone residual history ending below ktol, and one inner GMRES per layer solve,
+    N_ls = 2L + (3L-5) + k(5L-7)."""
+    g = load(name)
+    k = int(g["iterations"])
+    assert k == its
+    r = np.asarray(g["residuals"])
+    assert len(r) == k and r[-1] <= float(g["ktol"]) and np.all(np.diff(r) < 0)
+    assert len(g["inner_iterations"]) == 2 * L + (3 * L - 5) + k * (5 * L - 7)
+    assert float(g["relres"]) < 1e-5
