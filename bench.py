@@ -216,9 +216,10 @@ def run_reference(args):
 
 def _config(args, prob):
     g = prob.grid
+    R = len(prob.sources) if getattr(args, "nrhs", 0) <= 0 else min(args.nrhs, len(prob.sources))
     return {"workload": f"{args.config}: {g.nx}x{g.nz} interior + {g.npml}-pt PML, L={prob.partition.L}, "
-                        f"Lc={prob.Lc}, {len(prob.sources)} point sources batched per step",
-            "unknowns": g.nx * g.nz, "nrhs": len(prob.sources), "ktol": prob.ktol,
+                        f"Lc={prob.Lc}, {R} point sources batched per step",
+            "unknowns": g.nx * g.nz, "nrhs": R, "ktol": prob.ktol,
             "inner_ktol": prob.inner_ktol, "preconditioner": "gs",
             "l2": "factor working set (Schur inverses) larger than the 126 MB L2; no explicit flush",
             "parallelism": f"rhs-replica x{args.gpus}"}
@@ -248,8 +249,8 @@ def run_ours(args):
     solver = PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers,
                                    device=local)
     offline_s = time.time() - t0
-    R = len(prob.sources)
-    Fh = prob.rhs()
+    R = len(prob.sources) if args.nrhs <= 0 else min(args.nrhs, len(prob.sources))
+    Fh = prob.rhs(list(range(R)))
     F = torch.from_numpy(Fh).to(f"cuda:{local}")
     U = torch.empty_like(F)
     cfg = KrylovConfig(ktol=prob.ktol, max_iter=prob.max_iter)
@@ -338,6 +339,16 @@ def run_ours(args):
     dom = int(np.argmax(cls_ms[:2]))
     achieved_tf = inner_tf if dom == 1 else k1_tf
     its = sorted({r.iterations for r in res})
+    # SURVEY 8(d) algorithmic work of the reference's online solve for this batch: every layer solve is
+    # 2 cell solves per cell, each reading its Schur factors twice (2 x 32 wz_c w_c^2 B), plus 16 B per
+    # inner Green-block touch; layer solves and touches are this step's own counts (identical to the
+    # reference's), per-layer bytes averaged over the layers (their heights differ by at most one row)
+    st_last = solver.last_stats
+    F_ = layers.factors
+    per_layer = [sum(64.0 * cf.wzc * cf.w * cf.w for cf in lf.cells) for lf in F_.layers]
+    alg_bytes = st_last["layer_solves"] * float(np.mean(per_layer)) + 16.0 * st_last["touches"]
+    alg_gbs = alg_bytes / (ms * 1e-3) / 1e9
+    alg_tf = alg_bytes / 2.0 / (ms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -357,6 +368,13 @@ def run_ours(args):
             "class_share_of_step": {nm: float(c / prof_steps / ms) for nm, c in zip(names, cls_ms)},
             "k1_tflops": k1_tf, "inner_dense_tflops": inner_tf,
             "profiled_ms_per_step": prof_ms / prof_steps,
+        },
+        "solve_roofline": {
+            "formula": "SURVEY 8(d): sum_l N_l sum_c 2*32*wz_c*w_c^2 B + 16 B per inner touch; flops = bytes/2",
+            "bytes_per_rhs": alg_bytes / R, "achieved_gbs": alg_gbs, "hbm_peak_gbs": peaks["hbm_gbs"],
+            "hbm_frac": alg_gbs / peaks["hbm_gbs"], "achieved_tflops": alg_tf,
+            "fp64_peak_tflops": peaks["fp64_tflops"], "fp64_frac": alg_tf / peaks["fp64_tflops"],
+            "regime": "1 RHS: HBM bound" if R == 1 else f"{R} RHS per step: FP64 tensor bound",
         },
         "clocks": clk.summary(),
         "outer_iterations": its,
@@ -393,6 +411,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nrhs", type=int, default=0, help="solve the config's first N sources (0 = all)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

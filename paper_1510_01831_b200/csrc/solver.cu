@@ -139,6 +139,18 @@ struct pt_ctx {
   std::vector<EvRec> evs;
   double k1_bytes = 0.0;
   long long launches = 0, k1_launches = 0;
+  // CUDA graphs of the fixed launch sequences of a solve (graphed()): one executable per key, captured
+  // the second time the key is seen (the first, eager run makes every lazy allocation); gen changes
+  // whenever a buffer the sequences use is reallocated, which retires the old keys
+  struct GraphEnt {
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+    long long d_layer_solves = 0, d_launches = 0, d_k1_launches = 0;
+    double d_k1_bytes = 0.0;
+  };
+  std::map<std::vector<long long>, GraphEnt> graphs;
+  long long gen = 0;
+  bool graphs_off = false;
 };
 
 static cudaEvent_t pool_event(pt_ctx* c) {
@@ -560,6 +572,7 @@ static int ensure_scratch(pt_ctx* c, int R, int capO) {
   CK(cudaMallocHost(&c->hy, sizeof(double2) * (size_t)R * (capO + 1)));
   c->capR = R;
   c->capO = capO;
+  c->gen++;
   return 0;
 }
 
@@ -568,6 +581,7 @@ static int ensure_z(pt_ctx* c, long long z) {
   if (c->Z) cudaFree(c->Z);
   CK(cudaMalloc(&c->Z, sizeof(double2) * (size_t)z));
   c->zcap = z;
+  c->gen++;
   return 0;
 }
 
@@ -638,6 +652,7 @@ static Stage::Tasks* stage_tasks(pt_ctx* c, Stage& S, int Ract) {
   T.n = (int)v.size();
   T.zsize = z;
   if (upload(&T.d, v.data(), v.size())) return nullptr;
+  c->gen++;
   auto res = S.tasks.emplace(Ract, T);
   return &res.first->second;
 }
@@ -936,6 +951,7 @@ static int grow_outer_basis(pt_ctx* c, int R, int need) {
   CK(cudaMallocHost(&c->hhout, sizeof(double2) * (size_t)c->capR * (ncap + 2)));
   CK(cudaMallocHost(&c->hy, sizeof(double2) * (size_t)c->capR * (ncap + 1)));
   c->capO = ncap;
+  c->gen++;
   return 0;
 }
 
@@ -943,6 +959,58 @@ static int check_err(pt_ctx* c, int* code) {
   int e = 0;
   CK(cudaMemcpy(&e, c->err_d, sizeof(int), cudaMemcpyDeviceToHost));
   *code = e;
+  return 0;
+}
+
+// Run `body` (a launch sequence with no host synchronisation and no host decision on device results) as a
+// CUDA graph.  The key names the sequence and every host value it depends on besides c->gen (active count,
+// Arnoldi step, io pointers, ...); kernels still read the CURRENT rmap / scalars from device memory.  The
+// first sighting runs eagerly, the second captures, instantiates and launches, later ones only launch;
+// the host-side counters the body would have advanced are replayed from the capture.  Off while
+// profiling (per-launch events), under PT_NO_GRAPH, or after a capture failed.
+template <class Body>
+static int graphed(pt_ctx* c, std::vector<long long> key, Body&& body) {
+  static const bool no_graph = std::getenv("PT_NO_GRAPH") != nullptr || std::getenv("PT_INNER_TPROF") != nullptr ||
+                               std::getenv("PT_K1_TPROF") != nullptr;
+  if (no_graph || c->prof || c->graphs_off) return body();
+  key.push_back(c->gen);
+  key.push_back((long long)(uintptr_t)c->st);
+  pt_ctx::GraphEnt& g = c->graphs[key];
+  if (g.exec) {
+    CK(cudaGraphLaunch(g.exec, c->st));
+    c->layer_solves += g.d_layer_solves;
+    c->launches += g.d_launches;
+    c->k1_launches += g.d_k1_launches;
+    c->k1_bytes += g.d_k1_bytes;
+    return 0;
+  }
+  if (g.seen++ == 0) return body();
+  const long long ls0 = c->layer_solves, la0 = c->launches, k10 = c->k1_launches;
+  const double kb0 = c->k1_bytes;
+  const long long gen0 = c->gen;
+  CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  const int rc = body();  // records the launches (and advances the host counters by what they will do)
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+  if (rc == 0 && e == cudaSuccess && c->gen == gen0) e = cudaGraphInstantiate(&g.exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (rc != 0 || e != cudaSuccess || !g.exec) {
+    // capture not possible here (e.g. a launch kind the driver cannot capture): eager from now on
+    cudaGetLastError();
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    c->graphs_off = true;
+    c->layer_solves = ls0;
+    c->launches = la0;
+    c->k1_launches = k10;
+    c->k1_bytes = kb0;
+    return body();
+  }
+  g.d_layer_solves = c->layer_solves - ls0;
+  g.d_launches = c->launches - la0;
+  g.d_k1_launches = c->k1_launches - k10;
+  g.d_k1_bytes = c->k1_bytes - kb0;
+  CK(cudaGraphLaunch(g.exec, c->st));
   return 0;
 }
 
@@ -985,6 +1053,13 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   cudaEventRecord(e0, c->st);
 
   SolveIO io{f, N, u, N, cfg->inner_ktol, cfg->inner_max_iter};
+  const long long kio[4] = {(long long)(uintptr_t)f, (long long)(uintptr_t)u, cfg->inner_max_iter,
+                            (long long)(cfg->inner_ktol * 1e15)};
+  auto gkey = [&](std::initializer_list<long long> a) {
+    std::vector<long long> k(a);
+    k.insert(k.end(), kio, kio + 4);
+    return k;
+  };
   // zero-source detection (sie.py:397-399)
   CK(cudaMemsetAsync(c->dscal, 0, sizeof(double) * 2 * R, c->st));
   { LaunchScope ls_(c, 2); }
@@ -1020,20 +1095,33 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     if ((rc = set_active(c, all))) return rc;
     CK(cudaMemsetAsync(c->Bv, 0, sizeof(double2) * (size_t)R * nO, c->st));
     c->tables_f_ok = false;
-    if ((rc = run_stage(c, c->newton, VecTab{{vB, vB, vB}}, R, io))) return rc;
     // the Newton tables of f alone: RECON's first pass is these plus the pass-0 product of its panels
-    if (c->q0_d && c->Lc > 1 && c->newton.jobs.size() == c->recon.jobs.size()) {
-      CK(cudaMemcpyAsync(c->tables_f, c->tables,
-                         sizeof(double2) * c->newton.jobs.size() * c->Lc * 4 * (size_t)R * c->wmax,
-                         cudaMemcpyDeviceToDevice, c->st));
+    const bool keep_tables = c->q0_d && c->Lc > 1 && c->newton.jobs.size() == c->recon.jobs.size();
+    rc = graphed(c, gkey({2, R, keep_tables}), [&]() -> int {
+      int r2 = run_stage(c, c->newton, VecTab{{vB, vB, vB}}, R, io);
+      if (r2) return r2;
+      if (keep_tables)
+        CK(cudaMemcpyAsync(c->tables_f, c->tables,
+                           sizeof(double2) * c->newton.jobs.size() * c->Lc * 4 * (size_t)R * c->wmax,
+                           cudaMemcpyDeviceToDevice, c->st));
+      return 0;
+    });
+    if (rc) return rc;
+    if (keep_tables) {
       c->tables_f_ok = true;
       c->tables_f_R = R;
     }
     if ((rc = set_active(c, live))) return rc;
     const int Rl = (int)live.size();
-    if ((rc = apply_pre(c, vB, vBp, vA, Rl, gs, io))) return rc;
-    { LaunchScope ls_(c, 2); }
-    k_norm2<<<Rl, 256, 0, c->st>>>(vBp, nO, c->rmap_d, c->dscal);
+    rc = graphed(c, gkey({3, Rl, gs}), [&]() -> int {
+      int r3 = apply_pre(c, vB, vBp, vA, Rl, gs, io);
+      if (r3) return r3;
+      { LaunchScope ls_(c, 2); }
+      k_norm2<<<Rl, 256, 0, c->st>>>(vBp, nO, c->rmap_d, c->dscal);
+      CK(cudaGetLastError());
+      return 0;
+    });
+    if (rc) return rc;
     CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * R, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemsetAsync(c->X, 0, sizeof(double2) * (size_t)R * nO, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -1111,12 +1199,17 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
         if ((rc = set_active(c, cont))) return rc;
         Ra = (int)cont.size();
         VecView vj{c->V + (size_t)j * nO, vs}, vj1{c->V + (size_t)(j + 1) * nO, vs};
-        if ((rc = apply_op(c, vj, vT, Ra, io))) return rc;
-        if ((rc = apply_pre(c, vT, vj1, vA, Ra, gs, io))) return rc;
         const int hld = c->capO + 2;
-        { LaunchScope ls_(c, 2); }
-        k_arnoldi<<<Ra, 512, 0, c->st>>>(c->V, vs, nO, j, c->rmap_d, c->hout, hld);
-        CK(cudaGetLastError());
+        rc = graphed(c, gkey({1, j, Ra, gs}), [&]() -> int {
+          int r1 = apply_op(c, vj, vT, Ra, io);
+          if (r1) return r1;
+          if ((r1 = apply_pre(c, vT, vj1, vA, Ra, gs, io))) return r1;
+          { LaunchScope ls_(c, 2); }
+          k_arnoldi<<<Ra, 512, 0, c->st>>>(c->V, vs, nO, j, c->rmap_d, c->hout, hld);
+          CK(cudaGetLastError());
+          return 0;
+        });
+        if (rc) return rc;
         CK(cudaMemcpyAsync(c->hhout, c->hout, sizeof(double2) * (size_t)R * hld, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         int ecode = 0;
@@ -1213,8 +1306,12 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     // traces = down + up (sie.py:426-427), then reconstruct (sie.py:428)
     if ((rc = set_active(c, all))) return rc;
     const long long half = nO / 2;
-    if ((rc = lincomb(c, vTR, 0, vX, 0, 1.0, vX, half, 1.0, 1, half, R))) return rc;
-    if ((rc = run_stage(c, c->recon, VecTab{{vTR, vTR, vTR}}, R, io))) return rc;
+    rc = graphed(c, gkey({4, R, c->tables_f_ok, c->tables_f_R}), [&]() -> int {
+      int r4 = lincomb(c, vTR, 0, vX, 0, 1.0, vX, half, 1.0, 1, half, R);
+      if (r4) return r4;
+      return run_stage(c, c->recon, VecTab{{vTR, vTR, vTR}}, R, io);
+    });
+    if (rc) return rc;
   }
   // residuals (sie.py:441-445)
   if ((rc = set_active(c, all))) return rc;
@@ -1575,6 +1672,8 @@ int pt_destroy(pt_ctx* c) {
     if (st->ljobs_d) cudaFree(st->ljobs_d);
     if (st->grp_d) cudaFree(st->grp_d);
   }
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   cudaStreamDestroy(c->own_st);
   delete c;
   return PT_OK;

@@ -146,3 +146,30 @@ def test_monolayer_and_one_cell():
     want = orc.solve(f, ktol=1e-9)
     assert got.iterations == 0.0
     assert rel(got.u, want.u) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["small_b", "cfg1", "cfg2"])
+def test_repeated_solves_replay_graphs(name):
+    """The fixed launch sequences of a solve run eagerly the first time, are captured as CUDA graphs the
+    second time and replayed after that: all three must give the same wavefield (bitwise: same kernels,
+    same order) and the same counters, matching the live-reference fixture."""
+    make, si, nested = GOLDEN[name]
+    prob = make()
+    g = np.load(os.path.join(HERE, "golden", f"{name}.npz"))
+    layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=prob.Lc,
+                                 inner_ktol=prob.inner_ktol)
+    dev = PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers)
+    f = prob.rhs([si])[0]
+    cfg = KrylovConfig(ktol=float(g["ktol"]), max_iter=200)
+    outs, stats = [], []
+    for _ in range(4):
+        r = dev.solve(f, cfg)
+        outs.append(r.u.copy())
+        stats.append((r.iterations, dev.last_stats["touches"], dev.last_stats["layer_solves"],
+                      dev.last_stats["launches"]))
+    for k in range(1, 4):
+        assert np.array_equal(outs[k], outs[0])
+        assert stats[k] == stats[0], (stats[k], stats[0])
+    d = int(g["decim"])
+    assert rel(outs[-1][::d, ::d], g["u"]) <= 1e-8
+    dev.close()
