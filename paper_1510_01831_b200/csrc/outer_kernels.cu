@@ -9,6 +9,7 @@
 
 #include <algorithm>
 
+#include <cstdlib>
 #include "pt_launch.cuh"
 #include "stage_dev.cuh"
 
@@ -52,6 +53,122 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_green_samples(
   extern __shared__ double2 trs[];  // [4 slots][w4][8 rhs]
   green_item(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax, blockIdx.x, blockIdx.y, blockIdx.z, trs,
              fuse_combine ? &tab : nullptr, rmap);
+}
+
+// Sampled trace response, many-warp form: CTA = (job x cell, GS2_NG groups of 8 RHS, GS2_TPC row tiles);
+// each row tile's K = (slot, column) range is split over GS2_KQ warps (A loads of a warp issued 8 k-steps
+// at a time), every A fragment serves all GS2_NG RHS groups, and the partial tiles are summed in a fixed
+// order by the kq = 0 warp.  Same products as green_item; the sum over K is split in GS2_KQ parts.
+#define GS2_KQ 4
+#define GS2_TPC 2
+#define GS2_NG 2
+__global__ void __launch_bounds__(GS2_KQ * GS2_TPC * 32) k_green_samples2(
+    const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells, const LayerInfo* __restrict__ layers,
+    const double2* __restrict__ gsmp, const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,
+    int wmax, VecTab tab, const int* rmap, int fuse_combine) {
+  extern __shared__ double2 trs[];  // [4 slots][w4][8 GS2_NG rhs], then the partial tiles
+  const int jid = blockIdx.x / Lc, c = blockIdx.x - jid * Lc;
+  const OJob& jb = jobs[jid];
+  const int nout = jb.nout;
+  if (nout <= 0) return;
+  const LayerInfo& lay = layers[jb.layer];
+  const CellInfo& ci = cells[jb.layer * Lc + c];
+  const int w = ci.w, w4 = (w + 3) & ~3, nIc = Lc - 1, tid = threadIdx.x;
+  const int lane = tid & 31, wp = tid >> 5;
+  const int nrows = (ci.hi - ci.lo) * nout;  // (k, o) rows of this cell, k-major
+  if (blockIdx.z * GS2_TPC * 8 >= nrows) return;  // whole CTA: no barrier is skipped by part of it
+  constexpr int NR = 8 * GS2_NG;
+  const int r0 = blockIdx.y * NR, nr = min(NR, R - r0);
+  const int s_lo = ci.has_top ? 0 : 2, s_hi = ci.has_bot ? 4 : 2;
+  for (int row = wp; row < 4 * NR; row += GS2_KQ * GS2_TPC) {  // (slot, rhs) rows of the trace panels
+    const int sl = row / NR, rr = row - sl * NR;
+    if (sl < s_lo || sl >= s_hi) continue;
+    const int I = sl < 2 ? c - 1 : c;
+    const bool okr = rr < nr && I >= 0 && I < nIc;
+    const double2* src = tr + (((size_t)(jid * R + r0 + (okr ? rr : 0)) * nIc + (okr ? I : 0)) * 2 + (sl & 1)) * wmax;
+    for (int j = lane; j < w4; j += 32)
+      trs[((size_t)sl * w4 + j) * NR + rr] = (okr && j < w) ? src[j] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int t = wp / GS2_KQ, kq = wp - t * GS2_KQ;
+  const int tile = blockIdx.z * GS2_TPC + t;
+  const int ar = lane >> 2, ak = lane & 3;
+  const int m = tile * 8 + ar;
+  const bool mok = m < nrows;
+  const int mk = mok ? m / nout : 0, mo = mok ? m - (m / nout) * nout : 0;
+  const int orow = jb.orow[mo];
+  const int oi = orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3));
+  const double2* grow = gsmp + ci.gsmp_off + ((size_t)(ci.lo + mk) * 4 + oi) * 4 * w;  // [4 slots][w]
+  const int kps = w4 >> 2, nks = (s_hi - s_lo) * kps;
+  const int kb = kq * nks / GS2_KQ, ke = (kq + 1) * nks / GS2_KQ;
+  double acc[GS2_NG][4];
+#pragma unroll
+  for (int g = 0; g < GS2_NG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0;
+  if (tile * 8 < nrows) {
+    for (int ks0 = kb; ks0 < ke; ks0 += 8) {
+      double2 av[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ks = ks0 + u;
+        const int sl = s_lo + ks / kps, j = (ks - (ks / kps) * kps) * 4 + ak;
+        av[u] = (ks < ke && mok && j < w) ? __ldg(grow + sl * w + j) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ks = ks0 + u;
+        if (ks >= ke) break;
+        const int sl = s_lo + ks / kps, j = (ks - (ks / kps) * kps) * 4 + ak;
+        const double2* tb = trs + ((size_t)sl * w4 + j) * NR + ar;
+#pragma unroll
+        for (int g = 0; g < GS2_NG; ++g) {
+          const double2 bv = tb[g * 8];
+          dmma_f64(acc[g][0], acc[g][1], av[u].x, bv.x);
+          dmma_f64(acc[g][2], acc[g][3], av[u].x, bv.y);
+          dmma_f64(acc[g][0], acc[g][1], -av[u].y, bv.y);
+          dmma_f64(acc[g][2], acc[g][3], av[u].y, bv.x);
+        }
+      }
+    }
+  }
+  double* part = reinterpret_cast<double*>(trs + (size_t)4 * w4 * NR);  // [TPC][KQ-1][NG][4][32]
+  if (kq > 0) {
+#pragma unroll
+    for (int g = 0; g < GS2_NG; ++g)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) part[((((size_t)t * (GS2_KQ - 1) + kq - 1) * GS2_NG + g) * 4 + q) * 32 + lane] = acc[g][q];
+  }
+  __syncthreads();
+  if (kq > 0 || !mok) return;
+#pragma unroll
+  for (int p2 = 0; p2 < GS2_KQ - 1; ++p2)
+#pragma unroll
+    for (int g = 0; g < GS2_NG; ++g)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[g][q] += part[((((size_t)t * (GS2_KQ - 1) + p2) * GS2_NG + g) * 4 + q) * 32 + lane];
+  // C fragment: row ar, columns (RHS) 2 ak and 2 ak + 1 of each group
+#pragma unroll
+  for (int g = 0; g < GS2_NG; ++g)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rr = g * 8 + 2 * ak + h;
+      if (rr >= nr) continue;
+      double2* dst = smp + ((size_t)(jid * 4 + mo) * R + r0 + rr) * wx + ci.off + ci.lo + mk;
+      const double2 yv = cadd(*dst, h == 0 ? make_double2(acc[g][0], acc[g][2]) : make_double2(acc[g][1], acc[g][3]));
+      if (!fuse_combine) {
+        *dst = yv;
+      } else {  // combine fused in: out = scoef*sample + add - (sub0 + sub1) (k_combine)
+        const int xg = ci.off + ci.lo + mk, r = rmap[r0 + rr];
+        double2 o = cscale(yv, jb.scoef[mo]);
+        if (jb.add[mo].vec >= 0) o = cadd(o, vref(tab, jb.add[mo], r, xg, wx));
+        if (jb.sub[mo][0].vec >= 0) {
+          double2 sb = vref(tab, jb.sub[mo][0], r, xg, wx);
+          if (jb.sub[mo][1].vec >= 0) sb = cadd(sb, vref(tab, jb.sub[mo][1], r, xg, wx));
+          o = csub(o, sb);
+        }
+        const VecView& dv = tab.v[jb.dst[mo].vec];
+        dv.p[(size_t)r * dv.stride + (size_t)jb.dst[mo].seg * wx + xg] = o;
+      }
+    }
 }
 
 // dst[seg..] = a*x[seg..] (+ b*y[seg..]) over len elements, for the active RHS
@@ -241,10 +358,21 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
   const int gy = (R + 7) / 8;
   // rows per cell <= kmax kept block rows x 4 output rows; one 8-row tile per warp
   const int gz = (kmax * 4 + 8 * GS_WARPS - 1) / (8 * GS_WARPS);
-  const size_t sm = sizeof(double2) * 4 * (size_t)((wmax + 3) & ~3) * 8;
-  if (sm > 48 * 1024) set_smem_attr((const void*)k_green_samples, sm);
-  k_green_samples<<<dim3(J * Lc, gy, gz), GS_WARPS * 32, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax, tabv, rmap,
-                                                                        fuse_combine);
+  static const bool v1 = std::getenv("PT_GS_V1") != nullptr;
+  if (v1) {
+    const size_t sm = sizeof(double2) * 4 * (size_t)((wmax + 3) & ~3) * 8;
+    if (sm > 48 * 1024) set_smem_attr((const void*)k_green_samples, sm);
+    k_green_samples<<<dim3(J * Lc, gy, gz), GS_WARPS * 32, sm, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax,
+                                                                          tabv, rmap, fuse_combine);
+    return cudaGetLastError();
+  }
+  const int gy2 = (R + 8 * GS2_NG - 1) / (8 * GS2_NG);
+  const int gz2 = (kmax * 4 + 8 * GS2_TPC - 1) / (8 * GS2_TPC);
+  const size_t sm2 = sizeof(double2) * 4 * (size_t)((wmax + 3) & ~3) * 8 * GS2_NG +
+                     sizeof(double) * GS2_TPC * (GS2_KQ - 1) * GS2_NG * 4 * 32;
+  if (sm2 > 48 * 1024) set_smem_attr((const void*)k_green_samples2, sm2);
+  k_green_samples2<<<dim3(J * Lc, gy2, gz2), GS2_KQ * GS2_TPC * 32, sm2, st>>>(jobs, cells, layers, gsmp, tr, smp, R, Lc,
+                                                                               wx, wmax, tabv, rmap, fuse_combine);
   return cudaGetLastError();
 }
 
