@@ -73,19 +73,172 @@ struct InSmem {
   size_t region;    // bytes from tiles to the end of red (the dense-apply ring lives there)
 };
 
+// One unit of a program phase: item `item` over its tile groups [g0, g1), for the nact active instances
+// act[0..nact) (local ids from r0) of job `job` (layer width w, Green pool offset goff of the item's cell).
+// Gathers the item's panels, streams its Green tiles through the ring, runs the DMMA products and writes the
+// combined outputs.  Used by the cluster kernel (run_program) and the cooperative item kernel.
+__device__ void item_unit(const InnerParams& p, int job, int w, int r0, const int* act, int nact, const IItem& item,
+                          int g0, int g1, const int vmap[3], const InSmem& S, uint32_t* tseq, Ticker& T, long long goff) {
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const int nmt = (w + 7) >> 3;
+  const int MG = p.mg;
+  const int kps = (w + 3) >> 2;  // k-steps per slot
+  const uint32_t tbytes = (uint32_t)w * 8u * 16u;
+  auto VM = [&](int i) { return i == 0 ? vmap[0] : (i == 1 ? vmap[1] : vmap[2]); };
+  int slotp = 0, ns = 0;  // packed slot list: slot of si in bits [2si, 2si+2)
+  if (item.cell >= 0)
+    for (int s = 0; s < 4; ++s)
+      if (item.pan[s][0].vec >= 0) slotp |= s << (2 * ns++);
+  auto slot_of = [&](int si) { return slotp >> (2 * si) & 3; };
+  // The unit's Green tiles stream through a ring of p.tring single-tile slots (one 8-row tile of one slot
+  // block per copy, so the ring fits any w <= 128): local tile j = (group g0 + j / (ns MG), then slot-major
+  // (si, t) within the group).  tseq counts this CTA's tiles across units and programs (slot tseq % TR,
+  // mbarrier parity (tseq / TR) & 1).  Issued by lane 0 of warp 0; consumers release a slot at the
+  // __syncthreads that ends its tile.
+  const int TR = p.tring;
+  auto tile_of = [&](int j, int& g, int& si, int& t) {
+    const int per = ns * MG;
+    g = g0 + j / per;
+    const int mt0 = g * MG, nt = min(MG, nmt - mt0), rem = j - (j / per) * per;
+    si = rem / nt;
+    t = rem - si * nt;
+  };
+  int ntl = 0;
+  for (int g = g0; g < g1; ++g) ntl += ns * min(MG, nmt - g * MG);
+  const uint32_t tbase = *tseq;
+  int ji = 0;  // tiles issued so far (thread 0's count; ring holds tiles [jt, ji))
+  auto issue_tile = [&](int j) {  // lane 0 of warp 0 only
+    int g, si, t;
+    tile_of(j, g, si, t);
+    const uint32_t sq = tbase + (uint32_t)j;
+    const int slot = (int)(sq % (uint32_t)TR);
+    mbar_expect_tx(&S.tbar[slot], tbytes);
+    bulk_g2s(S.tiles + (size_t)slot * w * 8,
+             p.green + goff + ((size_t)(item.row * 4 + slot_of(si)) * nmt + g * MG + t) * w * 8, tbytes,
+             &S.tbar[slot]);
+  };
+  int negm = 0;  // bit si: slot panel si enters negated (exact)
+  for (int si = 0; si < ns; ++si) negm |= (item.flags >> slot_of(si) & 1) << si;
+  int twom = 0;  // bit si: two-term slot panel (d + p); its second term is staged in pan2
+  for (int si = 0; si < ns; ++si) twom |= (item.pan[slot_of(si)][1].vec >= 0) << si;
+  if (ns > 0) {
+    if (tid == 0)
+      for (int j = 0; j < min(TR, ntl); ++j) issue_tile(j);
+    ji = min(TR, ntl);
+    T.tick(13);  // tile issue
+    // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill).
+    // IN_THREADS % 8 == 0, so a thread's instance qq is fixed and its scratch base is computed once.
+    const int qq = tid & 7;
+    const bool okq = qq < nact;
+    const double2* ibase = p.scratch + (size_t)(job * p.R + (okq ? r0 + act[qq] : r0)) * p.inst_stride;
+    for (int si = 0, n2 = 0; si < ns; ++si) {
+      const Ref pr = item.pan[slot_of(si)][0], pr2 = item.pan[slot_of(si)][1];
+      const double2* src = ibase + (size_t)VM(pr.vec) * p.nmax + pr.seg * w;
+      double2* dst = S.pan + (size_t)si * w * 8 + qq;
+      for (int k = tid >> 3; k < w; k += IN_THREADS / 8) cp_async16(dst + k * 8, src + k, okq);
+      if (pr2.vec >= 0) {
+        const double2* src2 = ibase + (size_t)VM(pr2.vec) * p.nmax + pr2.seg * w;
+        double2* dst2 = S.pan2 + (size_t)n2++ * w * 8 + qq;
+        for (int k = tid >> 3; k < w; k += IN_THREADS / 8) cp_async16(dst2 + k * 8, src2 + k, okq);
+      }
+    }
+  }
+  T.tick(0);
+  int jt = 0;  // next local tile to consume
+  for (int g = g0; g < g1; ++g) {
+    const int mt0 = g * MG, nt = min(MG, nmt - mt0);
+    const int row0 = mt0 * 8, rows = min(w, row0 + nt * 8) - row0;
+    // this thread's output (row, instance) and its combine operands
+    const int oq = tid & 7, orow = tid >> 3;
+    const bool own = orow < rows && oq < nact;
+    const int rr = own ? r0 + act[oq] : r0;
+    const int gi = row0 + orow;
+    double2 addv = czero(), subv = czero(), revv = czero();
+    if (own) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (item.add[t].vec >= 0) addv = cadd(addv, ld_cg(vecp(p, job, rr, VM(item.add[t].vec)) + item.add[t].seg * w + gi));
+        if (item.sub[t].vec >= 0) subv = cadd(subv, ld_cg(vecp(p, job, rr, VM(item.sub[t].vec)) + item.sub[t].seg * w + gi));
+      }
+      if (item.rev.vec >= 0) revv = ld_cg(vecp(p, job, rr, VM(item.rev.vec)) + item.rev.seg * w + gi);
+    }
+    double2 y = czero();
+    if (ns > 0) {
+      if (g == g0) {
+        cp_async_wait_all();
+        __syncthreads();
+      }
+      T.tick(1);
+      // The group's P = ns x nt tiles are all in the ring at once (TR >= 4 MG); warp wp takes tile
+      // q = wp % P (slot si = q / nt, row tile t = q % nt) and k-part wp / P of KP = 8 / P parts, so every
+      // warp runs one long independent DMMA chain and the CTA synchronises once per group:
+      // Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br
+      const int P = ns * nt, KP = (IN_THREADS / 32) / P;
+      const int ar = lane >> 2, ak = lane & 3;
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+      if (wp < P * KP) {
+        const int q = wp % P, kp = wp / P;
+        const int si = q / nt;
+        const uint32_t sq = tbase + (uint32_t)(jt + q);
+        const int slot = (int)(sq % (uint32_t)TR);
+        const double sg = (negm >> si & 1) ? -1.0 : 1.0;
+        const bool two = twom >> si & 1;
+        const int i2 = __popc(twom & ((1 << si) - 1));
+        mbar_wait(&S.tbar[slot], (sq / (uint32_t)TR) & 1);
+        const double2* tl = S.tiles + (size_t)slot * w * 8;
+        const int kb = kp * kps / KP, ke = (kp + 1) * kps / KP;
+#pragma unroll 4
+        for (int ks = kb; ks < ke; ++ks) {
+          const int k = ks * 4 + ak;
+          const bool kin = k < w;
+          double2 bv = kin ? S.pan[((size_t)si * w + k) * 8 + ar] : czero();
+          if (two) bv = cadd(bv, kin ? S.pan2[((size_t)i2 * w + k) * 8 + ar] : czero());  // d + p
+          bv.x *= sg;
+          bv.y *= sg;
+          const double2 av = kin ? tl[(size_t)k * 8 + ar] : czero();
+          dmma_f64(c0, c1, av.x, bv.x);
+          dmma_f64(c2, c3, av.x, bv.y);
+          dmma_f64(c0, c1, -av.y, bv.y);
+          dmma_f64(c2, c3, av.y, bv.x);
+        }
+      }
+      T.tick(2);
+      S.red[((wp * IN_MG) * 8 + ar) * 8 + 2 * ak] = make_double2(c0, c2);
+      S.red[((wp * IN_MG) * 8 + ar) * 8 + 2 * ak + 1] = make_double2(c1, c3);
+      jt += P;
+      __syncthreads();  // the group's ring slots are free, its partial tiles visible
+      if (tid == 0)
+        for (; ji < min(ntl, jt + TR); ++ji) issue_tile(ji);
+      T.tick(3);
+      if (own) {  // fixed-order sum over the warps that worked on this row tile
+        const int t_o = orow >> 3, ro = orow & 7;
+        for (int w2 = 0; w2 < P * KP; ++w2)
+          if ((w2 % P) % nt == t_o) y = cadd(y, S.red[((w2 * IN_MG) * 8 + ro) * 8 + oq]);
+      }
+    }
+    // ---- combine: t = y + (add0 + add1) - (sub0 + sub1); out = t | rev - t | t - rev
+    if (own) {
+      if (item.add[0].vec >= 0) y = cadd(y, addv);
+      if (item.sub[0].vec >= 0) y = csub(y, subv);
+      const int mode = item.flags >> 8 & 3;
+      if (mode == 1) y = csub(revv, y);
+      else if (mode == 2) y = csub(y, revv);
+      vecp(p, job, rr, VM(item.dst.vec))[item.dst.seg * w + gi] = y;
+    }
+    __syncthreads();
+    T.tick(4);
+  }
+  *tseq += (uint32_t)ntl;
+}
+
 // Execute one program (list of phases) for the active instances of this cluster.
 // vmap: program vec ids {0:IN,1:OUT,2:AUX} -> scratch vector index.
 __device__ void run_program(const InnerParams& p, int job, int layer, int w, int r0, const int* ph, int nph,
                             const int vmap[3], int nact, const InSmem& S, int q, int CS, uint32_t* tseq,
                             Ticker& T) {
-  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   const int nmt = (w + 7) >> 3;
   const int MG = p.mg;  // 8-row tiles per group (shared-memory budget, from the widest layer)
   const int ngrp = (nmt + MG - 1) / MG;
-  const int kps = (w + 3) >> 2;  // k-steps per slot
-  const size_t tbuf = (size_t)4 * MG * w * 8;  // double2 per tile buffer
-  const uint32_t tbytes = (uint32_t)w * 8u * 16u;
-  auto VM = [&](int i) { return i == 0 ? vmap[0] : (i == 1 ? vmap[1] : vmap[2]); };
   for (int phz = 0; phz < nph; ++phz) {
     const int it0 = ph[phz], nit = ph[phz + 1] - it0;
     // Weighted split of the phase's (item, tile group) pairs over the cluster: a pair weighs its
@@ -107,153 +260,7 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
       if (g0 >= g1) continue;
       T.tick(12);  // phase/unit bookkeeping
       const IItem& item = S.items[it0 + ii];
-      int slotp = 0, ns = 0;  // packed slot list: slot of si in bits [2si, 2si+2)
-      if (item.cell >= 0)
-        for (int s = 0; s < 4; ++s)
-          if (item.pan[s][0].vec >= 0) slotp |= s << (2 * ns++);
-      auto slot_of = [&](int si) { return slotp >> (2 * si) & 3; };
-      const long long goff = S.goff[item.cell >= 0 ? item.cell : 0];
-      // The unit's Green tiles stream through a ring of p.tring single-tile slots (one 8-row tile of one slot
-      // block per copy, so the ring fits any w <= 128): local tile j = (group g0 + j / (ns MG), then slot-major
-      // (si, t) within the group).  tseq counts this CTA's tiles across units and programs (slot tseq % TR,
-      // mbarrier parity (tseq / TR) & 1).  Issued by lane 0 of warp 0; consumers release a slot at the
-      // __syncthreads that ends its tile.
-      const int TR = p.tring;
-      auto tile_of = [&](int j, int& g, int& si, int& t) {
-        const int per = ns * MG;
-        g = g0 + j / per;
-        const int mt0 = g * MG, nt = min(MG, nmt - mt0), rem = j - (j / per) * per;
-        si = rem / nt;
-        t = rem - si * nt;
-      };
-      int ntl = 0;
-      for (int g = g0; g < g1; ++g) ntl += ns * min(MG, nmt - g * MG);
-      const uint32_t tbase = *tseq;
-      auto issue_tile = [&](int j) {  // lane 0 of warp 0 only
-        int g, si, t;
-        tile_of(j, g, si, t);
-        const uint32_t sq = tbase + (uint32_t)j;
-        const int slot = (int)(sq % (uint32_t)TR);
-        mbar_expect_tx(&S.tbar[slot], tbytes);
-        bulk_g2s(S.tiles + (size_t)slot * w * 8,
-                 p.green + goff + ((size_t)(item.row * 4 + slot_of(si)) * nmt + g * MG + t) * w * 8, tbytes,
-                 &S.tbar[slot]);
-      };
-      int negm = 0;  // bit si: slot panel si enters negated (exact)
-      for (int si = 0; si < ns; ++si) negm |= (item.flags >> slot_of(si) & 1) << si;
-      int twom = 0;  // bit si: two-term slot panel (d + p); its second term is staged in pan2
-      for (int si = 0; si < ns; ++si) twom |= (item.pan[slot_of(si)][1].vec >= 0) << si;
-      if (ns > 0) {
-        if (tid == 0)
-          for (int j = 0; j < min(TR, ntl); ++j) issue_tile(j);
-        T.tick(13);  // tile issue
-        // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill).
-        // IN_THREADS % 8 == 0, so a thread's instance qq is fixed and its scratch base is computed once.
-        const int qq = tid & 7;
-        const bool okq = qq < nact;
-        const double2* ibase = p.scratch + (size_t)(job * p.R + (okq ? r0 + S.act[qq] : r0)) * p.inst_stride;
-        for (int si = 0, n2 = 0; si < ns; ++si) {
-          const Ref pr = item.pan[slot_of(si)][0], pr2 = item.pan[slot_of(si)][1];
-          const double2* src = ibase + (size_t)VM(pr.vec) * p.nmax + pr.seg * w;
-          double2* dst = S.pan + (size_t)si * w * 8 + qq;
-          for (int k = tid >> 3; k < w; k += IN_THREADS / 8) cp_async16(dst + k * 8, src + k, okq);
-          if (pr2.vec >= 0) {
-            const double2* src2 = ibase + (size_t)VM(pr2.vec) * p.nmax + pr2.seg * w;
-            double2* dst2 = S.pan2 + (size_t)n2++ * w * 8 + qq;
-            for (int k = tid >> 3; k < w; k += IN_THREADS / 8) cp_async16(dst2 + k * 8, src2 + k, okq);
-          }
-        }
-      }
-      T.tick(0);
-      int jt = 0;  // next local tile to consume
-      for (int g = g0; g < g1; ++g) {
-        const int mt0 = g * MG, nt = min(MG, nmt - mt0);
-        const int row0 = mt0 * 8, rows = min(w, row0 + nt * 8) - row0;
-        // this thread's output (row, instance) and its combine operands
-        const int oq = tid & 7, orow = tid >> 3;
-        const bool own = orow < rows && oq < nact;
-        const int rr = own ? r0 + S.act[oq] : r0;
-        const int gi = row0 + orow;
-        double2 addv = czero(), subv = czero(), revv = czero();
-        if (own) {
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            if (item.add[t].vec >= 0) addv = cadd(addv, ld_cg(vecp(p, job, rr, VM(item.add[t].vec)) + item.add[t].seg * w + gi));
-            if (item.sub[t].vec >= 0) subv = cadd(subv, ld_cg(vecp(p, job, rr, VM(item.sub[t].vec)) + item.sub[t].seg * w + gi));
-          }
-          if (item.rev.vec >= 0) revv = ld_cg(vecp(p, job, rr, VM(item.rev.vec)) + item.rev.seg * w + gi);
-        }
-        double2 y = czero();
-        if (ns > 0) {
-          if (g == g0) {
-            cp_async_wait_all();
-            __syncthreads();
-          }
-          T.tick(1);
-          // DMMA: per tile (slot si, row tile t) warp wp takes k-steps wp, wp + 8, ... of the slot:
-          // Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br
-          const int ar = lane >> 2, ak = lane & 3;
-          double c[IN_MG][4];
-#pragma unroll
-          for (int t = 0; t < IN_MG; ++t) c[t][0] = c[t][1] = c[t][2] = c[t][3] = 0.0;
-          for (int si = 0; si < ns; ++si) {
-            const double sg = (negm >> si & 1) ? -1.0 : 1.0;
-            const bool two = twom >> si & 1;
-            const int i2 = __popc(twom & ((1 << si) - 1));
-            for (int t = 0; t < nt; ++t, ++jt) {
-              const uint32_t sq = tbase + (uint32_t)jt;
-              const int slot = (int)(sq % (uint32_t)TR);
-              T.tick(1);
-              mbar_wait(&S.tbar[slot], (sq / (uint32_t)TR) & 1);
-              T.tick(2);
-              const double2* tl = S.tiles + (size_t)slot * w * 8;
-              for (int ks = wp; ks < kps; ks += IN_THREADS / 32) {
-                const int k = ks * 4 + ak;
-                const bool kin = k < w;
-                double2 bv = kin ? S.pan[((size_t)si * w + k) * 8 + ar] : czero();
-                if (two) bv = cadd(bv, kin ? S.pan2[((size_t)i2 * w + k) * 8 + ar] : czero());  // d + p
-                bv.x *= sg;
-                bv.y *= sg;
-                const double2 av = kin ? tl[(size_t)k * 8 + ar] : czero();
-#pragma unroll
-                for (int tt = 0; tt < IN_MG; ++tt)
-                  if (tt == t) {
-                    dmma_f64(c[tt][0], c[tt][1], av.x, bv.x);
-                    dmma_f64(c[tt][2], c[tt][3], av.x, bv.y);
-                    dmma_f64(c[tt][0], c[tt][1], -av.y, bv.y);
-                    dmma_f64(c[tt][2], c[tt][3], av.y, bv.x);
-                  }
-              }
-              __syncthreads();  // slot free
-              if (tid == 0 && jt + TR < ntl) issue_tile(jt + TR);
-            }
-          }
-#pragma unroll
-          for (int t = 0; t < IN_MG; ++t) {
-            S.red[((wp * IN_MG + t) * 8 + ar) * 8 + 2 * ak] = make_double2(c[t][0], c[t][2]);
-            S.red[((wp * IN_MG + t) * 8 + ar) * 8 + 2 * ak + 1] = make_double2(c[t][1], c[t][3]);
-          }
-          __syncthreads();
-          T.tick(3);
-          if (own) {
-            y = S.red[orow * 8 + oq];
-#pragma unroll
-            for (int g2 = 1; g2 < IN_THREADS / 32; ++g2) y = cadd(y, S.red[(g2 * IN_MG * 8 + orow) * 8 + oq]);
-          }
-        }
-        // ---- combine: t = y + (add0 + add1) - (sub0 + sub1); out = t | rev - t | t - rev
-        if (own) {
-          if (item.add[0].vec >= 0) y = cadd(y, addv);
-          if (item.sub[0].vec >= 0) y = csub(y, subv);
-          const int mode = item.flags >> 8 & 3;
-          if (mode == 1) y = csub(revv, y);
-          else if (mode == 2) y = csub(y, revv);
-          vecp(p, job, rr, VM(item.dst.vec))[item.dst.seg * w + gi] = y;
-        }
-        __syncthreads();
-        T.tick(4);
-      }
-      *tseq += (uint32_t)ntl;
+      item_unit(p, job, w, r0, S.act, nact, item, g0, g1, vmap, S, tseq, T, S.goff[item.cell >= 0 ? item.cell : 0]);
     }
     csync();
     T.tick(5);
@@ -1086,6 +1093,196 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Whole-GPU inner GMRES over the Green-block item programs (no dense operators; Lc > 8): the cluster
+// kernel's arithmetic (item_unit, instance_init / instance_arnoldi / instance_final) with every CTA of the
+// GPU sharing each program phase across all (job, <= 8 RHS) units of the stage, grid barriers between the
+// phases.  A sweep stage's single unit then streams its Green tiles with the whole GPU's bandwidth instead
+// of one 16-CTA cluster's.
+#define CI_STATIC_INTS 0
+__global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_items_kernel(const InnerParams p, int nunits) {
+  cg::grid_group grid = cg::this_grid();
+  Ticker T;
+  T.on = p.tprof && blockIdx.x == 0 && threadIdx.x == 0;
+  T.start();
+  auto gsync = [&]() {
+    T.tick(7);
+    grid.sync();
+    T.tick(5);
+  };
+  extern __shared__ __align__(128) unsigned char smem[];
+  InSmem S;
+  S.tiles = reinterpret_cast<double2*>(smem);
+  S.pan = S.tiles + (size_t)p.tring * p.wmax * 8;
+  S.pan2 = S.pan + (size_t)4 * p.wmax * 8;
+  S.red = S.pan2 + (size_t)2 * p.wmax * 8;
+  double* dred = reinterpret_cast<double*>(S.red + (IN_THREADS / 32) * IN_MG * 8 * 8);
+  S.tbar = reinterpret_cast<uint64_t*>(dred + 64);
+  S.dbar = S.tbar + IN_TRMAX;
+  int* uact = reinterpret_cast<int*>(S.dbar + 2 * DA_NS);  // [COOP_MAXU][8] active local ids per unit
+  int* unact = uact + COOP_MAXU * 8;                       // [COOP_MAXU] active count per unit
+  int* upre = unact + COOP_MAXU;                           // [COOP_MAXU + 1] prefix of active x ngrp
+  int* oph = upre + COOP_MAXU + 1;
+  int* pph = oph + 2 * PT_MAX_LC + 2;
+  S.items = reinterpret_cast<IItem*>(pph + 2 * PT_MAX_LC + 2);
+  S.act = nullptr;
+  S.goff = nullptr;
+  S.oph = oph;
+  S.pph = pph;
+  __shared__ int s_job[COOP_MAXU], s_w[COOP_MAXU], s_layer[COOP_MAXU];
+  const int tid = threadIdx.x, G = gridDim.x, b = blockIdx.x;
+  const int ngroups = (p.R + 7) >> 3;
+  const int nIc = p.Lc - 1;
+  const int VB = p.cap + 1, VY = p.cap + 2, VT = p.cap + 3, VA = p.cap + 4;
+  if (tid == 0) {
+    for (int i = 0; i < IN_TRMAX; ++i) mbar_init(&S.tbar[i], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < p.nitems; i += blockDim.x) S.items[i] = p.items[i];
+  for (int i = tid; i <= p.op_nph; i += blockDim.x) oph[i] = p.op_ph[i];
+  for (int i = tid; i <= p.pre_nph; i += blockDim.x) pph[i] = p.pre_ph[i];
+  const int njob_ = nunits / ngroups;
+  for (int jx = tid; jx < njob_; jx += blockDim.x) {
+    const int job = p.stage_jobs[jx];
+    const int layer = p.jobs[job].layer;
+    s_job[jx] = job;
+    s_layer[jx] = layer;
+    s_w[jx] = p.layers[layer].w;
+  }
+  __syncthreads();
+  auto ujob = [&](int u) { return s_job[u / ngroups]; };
+  auto ur0 = [&](int u) { return (u % ngroups) * 8; };
+  auto uni = [&](int u) { return min(8, p.R - (u % ngroups) * 8); };
+  auto uw = [&](int u) { return s_w[u / ngroups]; };
+  auto ungrp = [&](int u) { return (((uw(u) + 7) >> 3) + p.mg - 1) / p.mg; };
+  // active local instances of every unit, from the global states (all = every existing instance)
+  auto refresh = [&](bool all) {
+    for (int u = tid; u < nunits; u += blockDim.x) {
+      int na = 0;
+      const int r0 = ur0(u), ni = uni(u), job = ujob(u);
+      for (int l = 0; l < ni; ++l)
+        if (all || __ldcg(p.state + job * p.R + r0 + l) == 0) uact[u * 8 + na++] = l;
+      unact[u] = na;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int u = 0; u < nunits; ++u) {
+        upre[u] = acc;
+        if (unact[u] > 0) acc += ungrp(u);
+      }
+      upre[nunits] = acc;
+    }
+    __syncthreads();
+  };
+  uint32_t tseq = 0;
+  auto cdiv = [](long long a, long long bb) -> long long { return a <= 0 ? -((-a) / bb) : (a + bb - 1) / bb; };
+  // one program over every unit's active instances: CTA b takes the (unit, item, tile group) triples whose
+  // weight midpoints fall in its share; a grid barrier ends each phase
+  auto coop_program = [&](const int* ph, int nph, const int vmap[3]) {
+    for (int phz = 0; phz < nph; ++phz) {
+      const int it0 = ph[phz], nit = ph[phz + 1] - it0;
+      int witems = 0;
+      for (int ii = 0; ii < nit; ++ii) witems += S.items[it0 + ii].wgt;
+      const long long wtot = (long long)upre[nunits] * witems;
+      const long long wlo2 = 2 * ((long long)b * wtot / G), whi2 = 2 * ((long long)(b + 1) * wtot / G);
+      // first unit whose weight range reaches this CTA's share
+      int lo = 0, hi = nunits;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (2LL * upre[mid + 1] * witems <= wlo2) lo = mid + 1;
+        else hi = mid;
+      }
+      for (int u = lo; u < nunits && 2LL * upre[u] * witems < whi2; ++u) {
+        const int na = unact[u];
+        if (na == 0) continue;
+        const int ng = ungrp(u), job = ujob(u), w = uw(u), r0 = ur0(u), layer = s_layer[u / ngroups];
+        long long wcum = (long long)upre[u] * witems;
+        for (int ii = 0; ii < nit; ++ii) {
+          const IItem& item = S.items[it0 + ii];
+          const int wi = item.wgt;
+          const long long wa = wcum;
+          wcum += (long long)wi * ng;
+          const int g0 = (int)max(0LL, cdiv(wlo2 - 2 * wa - wi, 2LL * wi));
+          const int g1 = (int)min((long long)ng, cdiv(whi2 - 2 * wa - wi, 2LL * wi));
+          if (g0 >= g1) continue;
+          T.tick(12);
+          const long long goff = p.cells[layer * p.Lc + (item.cell >= 0 ? item.cell : 0)].green_off;
+          item_unit(p, job, w, r0, uact + u * 8, na, item, g0, g1, vmap, S, &tseq, T, goff);
+        }
+      }
+      gsync();
+    }
+  };
+  // ---- rhs_pol from the Newton tables (sie.py:230-242, negated)
+  for (int u = 0; u < nunits; ++u) {
+    const int job = ujob(u), r0 = ur0(u), ni = uni(u), w = uw(u), n = 4 * nIc * w;
+    for (long long t = (long long)b * blockDim.x + tid; t < (long long)ni * n; t += (long long)G * blockDim.x) {
+      const int l = (int)(t / n), e = (int)(t - (long long)l * n), r = r0 + l;
+      const int seg = e / w, j = e - seg * w;
+      const int half = seg / (2 * nIc);
+      const int I = (seg % (2 * nIc)) / 2, s_ = seg & 1;
+      const int c = half == 0 ? I : I + 1;
+      const int idx = half == 0 ? 2 + s_ : s_;
+      const double2 tv = __ldcg(p.tables + ((((size_t)job * p.Lc + c) * 4 + idx) * p.R + r) * p.wmax + j);
+      vecp(p, job, r, VB)[e] = make_double2(-tv.x, -tv.y);
+    }
+  }
+  refresh(true);
+  gsync();
+  T.tick(8);
+  // ---- b = pre(rhs), beta0 = ||b||, V_0 = b / beta0 (krylov.py:61-80)
+  {
+    const int vm[3] = {VB, VY, VA};
+    coop_program(pph, p.pre_nph, vm);
+  }
+  for (int t = b; t < nunits * 8; t += G) {
+    const int u = t >> 3, l = t & 7;
+    if (l < uni(u)) instance_init(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), VY, dred);
+  }
+  gsync();
+  for (int j = 0; j < p.max_iter; ++j) {
+    refresh(false);
+    if (upre[nunits] == 0) break;
+    if (j + 1 > p.cap) {  // basis capacity exhausted: the host retries with a larger capacity
+      for (int t = b; t < nunits * 8; t += G) {
+        const int u = t >> 3, l = t & 7;
+        if (tid == 0 && l < uni(u)) {
+          const int r = ur0(u) + l, job = ujob(u);
+          if (__ldcg(p.state + job * p.R + r) == 0) {
+            p.state[job * p.R + r] = 2;
+            p.iters[job * p.R + r] = -1;
+            atomicMax(p.err, 5);
+          }
+        }
+      }
+      gsync();
+      break;
+    }
+    T.tick(4);
+    {
+      const int vm1[3] = {j, VT, VA};
+      coop_program(oph, p.op_nph, vm1);
+      const int vm2[3] = {VT, j + 1, VA};
+      coop_program(pph, p.pre_nph, vm2);
+    }
+    T.tick(3);
+    for (int t = b; t < nunits * 8; t += G) {
+      const int u = t >> 3, l = t & 7;
+      if (l >= uni(u)) continue;
+      const int job = ujob(u), r = ur0(u) + l;
+      if (__ldcg(p.state + job * p.R + r) == 0) instance_arnoldi(p, job, r, j, 4 * nIc * uw(u), dred);
+    }
+    T.tick(6);
+    gsync();
+  }
+  for (int t = b; t < nunits * 8; t += G) {
+    const int u = t >> 3, l = t & 7;
+    if (l < uni(u)) instance_final(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), uw(u), S.pan);
+  }
+  T.tick(9);
+}
+
 int inner_coop_max_units() { return COOP_MAXU; }
 
 size_t inner_coop_smem(const InnerParams& p, size_t region) {
@@ -1093,8 +1290,45 @@ size_t inner_coop_smem(const InnerParams& p, size_t region) {
          (size_t)(p.cap + 2 + 24 + 300 + 24) * 16 + 128;
 }
 
+// extra shared memory of the cooperative item kernel over the cluster kernel's layout
+static size_t coop_items_extra() { return (size_t)COOP_MAXU * 8 * 4 + COOP_MAXU * 4 + (COOP_MAXU + 1) * 4; }
+
+static cudaError_t inner_coop_items_launch(const InnerParams& p0, int njobs, cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int nunits = njobs * ((p0.R + 7) / 8);
+  if (nunits > COOP_MAXU || p0.Lc < 2 || std::getenv("PT_NO_COOP_ITEMS")) return cudaErrorNotSupported;
+  InnerParams p = p0;
+  // the ring gives up what the unit tables take (static s_job/s_w/s_layer: 3 COOP_MAXU ints)
+  const int w = p.wmax < 8 ? 8 : p.wmax;
+  const long long tb = (long long)w * 8 * 16;
+  const long long shrink = ((long long)coop_items_extra() + 3LL * COOP_MAXU * 4 + tb - 1) / tb;
+  p.tring = (int)std::min((long long)IN_TRMAX, (long long)inner_tring(p.wmax, p.nitems) - shrink);
+  if (p.tring < 4 * p.mg) p.mg = 1;
+  if (p.tring < 4) return cudaErrorNotSupported;
+  const size_t sm = inner_smem_bytes(p.wmax, p.nitems, p.tring) + coop_items_extra();
+  set_smem_attr((const void*)inner_coop_items_kernel, sm);
+  static std::unordered_map<size_t, int> occ;
+  auto it = occ.find(sm);
+  if (it == occ.end()) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_coop_items_kernel, IN_THREADS, sm);
+    cudaGetLastError();
+    it = occ.emplace(sm, per_sm).first;
+  }
+  if (it->second < 1) return cudaErrorNotSupported;
+  int nu = nunits;
+  void* args[] = {(void*)&p, (void*)&nu};
+  return cudaLaunchCooperativeKernel((const void*)inner_coop_items_kernel, dim3(nsm), dim3(IN_THREADS), args, sm, st);
+}
+
 // returns cudaErrorNotSupported when the cooperative path does not apply (caller falls back)
 cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st) {
+  if (!p0.dense) return inner_coop_items_launch(p0, njobs, st);
   static int nsm = 0, maxsm = 0;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1162,7 +1396,7 @@ size_t inner_smem_bytes(int wmax, int nitems, int tring) {
 
 cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   if (njobs == 0 || p.Lc < 2) return cudaSuccess;
-  if (p.tring < 2) {  // program items do not fit in shared memory
+  if (p.tring < 4 * p.mg) {  // program items do not fit in shared memory
     fprintf(stderr, "inner_launch: %d program items leave no room for the Green-tile ring\n", p.nitems);
     return cudaErrorInvalidValue;
   }

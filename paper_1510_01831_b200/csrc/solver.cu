@@ -713,6 +713,7 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   ip.nitems = c->nitems;
   ip.mg = inner_mg(c->wmax);
   ip.tring = inner_tring(c->wmax, ip.nitems);
+  if (ip.tring < 4 * ip.mg) ip.mg = 1;  // a group's (slot, row tile) tiles must fit in the ring together
   return ip;
 }
 

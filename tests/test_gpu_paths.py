@@ -46,6 +46,7 @@ SWITCHES = {
     "k1-passes": {"PT_NO_Q0": "1", "PT_NO_GSMP": "1"},
     "item-programs": {"PT_NO_DENSE": "1"},
     "cluster-dense": {"PT_NO_COOP": "1"},
+    "cluster-items": {"PT_NO_DENSE": "1", "PT_NO_COOP": "1"},
     "fused-stage": {"PT_FUSE": "1"},
     "recon-k1": {"PT_NO_REUSE": "1"},
 }
