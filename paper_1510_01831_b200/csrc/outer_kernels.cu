@@ -80,14 +80,30 @@ __global__ void __launch_bounds__(GS2_KQ * GS2_TPC * 32) k_green_samples2(
   constexpr int NR = 8 * GS2_NG;
   const int r0 = blockIdx.y * NR, nr = min(NR, R - r0);
   const int s_lo = ci.has_top ? 0 : 2, s_hi = ci.has_bot ? 4 : 2;
-  for (int row = wp; row < 4 * NR; row += GS2_KQ * GS2_TPC) {  // (slot, rhs) rows of the trace panels
-    const int sl = row / NR, rr = row - sl * NR;
-    if (sl < s_lo || sl >= s_hi) continue;
-    const int I = sl < 2 ? c - 1 : c;
-    const bool okr = rr < nr && I >= 0 && I < nIc;
-    const double2* src = tr + (((size_t)(jid * R + r0 + (okr ? rr : 0)) * nIc + (okr ? I : 0)) * 2 + (sl & 1)) * wmax;
-    for (int j = lane; j < w4; j += 32)
-      trs[((size_t)sl * w4 + j) * NR + rr] = (okr && j < w) ? src[j] : make_double2(0.0, 0.0);
+  {
+    // trace panels of the used slots -> trs[sl][j][rr]: 8 independent loads in flight per thread, then the
+    // stores (a load-store loop would serialise one L2 round trip per element)
+    const int ne = (s_hi - s_lo) * NR * w4;
+    for (int e0 = tid; e0 < ne; e0 += 8 * GS2_KQ * GS2_TPC * 32) {
+      double2 v[8];
+      int dsti[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * GS2_KQ * GS2_TPC * 32;
+        v[u] = make_double2(0.0, 0.0);
+        dsti[u] = -1;
+        if (e < ne) {
+          const int j = e % w4, rest = e / w4, rr = rest % NR, sl = s_lo + rest / NR;
+          const int I = sl < 2 ? c - 1 : c;
+          const bool okr = rr < nr && I >= 0 && I < nIc && j < w;
+          if (okr) v[u] = __ldg(tr + (((size_t)(jid * R + r0 + rr) * nIc + I) * 2 + (sl & 1)) * wmax + j);
+          dsti[u] = (sl * w4 + j) * NR + rr;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (dsti[u] >= 0) trs[dsti[u]] = v[u];
+    }
   }
   __syncthreads();
   const int t = wp / GS2_KQ, kq = wp - t * GS2_KQ;

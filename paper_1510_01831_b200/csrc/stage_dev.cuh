@@ -98,7 +98,21 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
   double acc[2][4];
 #pragma unroll
   for (int gq = 0; gq < 2; ++gq) acc[gq][0] = acc[gq][1] = acc[gq][2] = acc[gq][3] = 0.0;
-  const int nks = K >> 2, kps = nk4 >> 2;  // k-steps in all / per slot
+  // only the slots some job of this layer group feeds (absent slot panels are zero): the K range runs over
+  // the used slots, packed (sweep stages use 1-2 of the 4)
+  int slist = 0, nsl = 0;
+  {
+    int used = 0;
+    for (int jj = 0; jj < nj; ++jj) {
+      const OJob& jo = jobs[ljobs[jb0 + jj]];
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) used |= (jo.pan[sl][0].vec >= 0) << sl;
+    }
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl)
+      if (used >> sl & 1) slist |= sl << (2 * nsl++);
+  }
+  const int kps = nk4 >> 2, nks = nsl * kps;  // k-steps per slot / over the used slots
   const int kb = wp * nks / P0_KQ, ke = (wp + 1) * nks / P0_KQ;
   for (int ks0 = kb; ks0 < ke; ks0 += 8) {
     double2 av[8], bv[8][2];
@@ -106,8 +120,9 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
     for (int u = 0; u < 8; ++u) {
       const int ks = ks0 + u;
       const bool kin = ks < ke;
-      const int sl = kin ? ks / kps : 0, kk = (ks - sl * kps) * 4;  // column within the slot block (+ ak)
-      av[u] = kin ? __ldg(arow + ks * 4) : make_double2(0.0, 0.0);
+      const int si = kin ? ks / kps : 0, sl = slist >> (2 * si) & 3;
+      const int kk = (ks - si * kps) * 4;  // column within the slot block (+ ak)
+      av[u] = kin ? __ldg(arow + (sl * kps + (ks - si * kps)) * 4) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int gq = 0; gq < 2; ++gq)
         bv[u][gq] = (kin && bok[gq] && kk + ak < nk) ? bload(gq, sl, kk) : make_double2(0.0, 0.0);
