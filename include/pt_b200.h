@@ -90,6 +90,7 @@ typedef struct {
   double inner_ktol;     /* NestedLayerSolver inner_ktol (1e-6) */
   int inner_max_iter;    /* NestedLayerSolver inner_max_iter (200) */
   int precond;           /* 0 = "gs", 1 = "jac" (sie.py:407) */
+  int method;            /* 0 = "gmres" (krylov.py:53-135), 1 = "bicgstab" (krylov.py:138-201) */
 } pt_krylov;
 
 typedef struct {

@@ -235,6 +235,64 @@ def gmres(op, rhs, precond, ktol, max_iter, restart=0):
     return x, float(total), hist, False
 
 
+def bicgstab(op, rhs, precond, ktol, max_iter):
+    """Left-preconditioned BiCGstab, half steps counted as 0.5 iterations, shadow residual = the
+    initial preconditioned residual, x0 = 0 (krylov.py:138-201).
+
+    Returns ``(x, iterations, residuals, converged)``; breakdowns raise ``KrylovBreakdown``.
+    """
+    b = precond(np.asarray(rhs, dtype=complex))
+    n = b.size
+    beta0 = np.linalg.norm(b)
+    if beta0 == 0.0:
+        return np.zeros(n, dtype=complex), 0.0, [0.0], True
+
+    def pa(v):
+        return precond(op(v))
+
+    x = np.zeros(n, dtype=complex)
+    r = b.copy()
+    r0 = r.copy()
+    rho = alpha = omega = 1.0 + 0.0j
+    v = np.zeros(n, dtype=complex)
+    p = np.zeros(n, dtype=complex)
+    hist = [np.linalg.norm(r) / beta0]
+    count = 0.0
+    for _ in range(int(np.ceil(max_iter))):
+        rho_new = np.vdot(r0, r)
+        if abs(rho_new) < 1e-300 * beta0**2:
+            raise KrylovBreakdown("BiCGstab breakdown (rho ~ 0)", count, hist)
+        beta = (rho_new / rho) * (alpha / omega) if count > 0 else 0.0
+        rho = rho_new
+        p = r + beta * (p - omega * v) if count > 0 else r.copy()
+        v = pa(p)
+        denom = np.vdot(r0, v)
+        if abs(denom) < 1e-300 * beta0**2:
+            raise KrylovBreakdown("BiCGstab breakdown (r0.v ~ 0)", count, hist)
+        alpha = rho / denom
+        s = r - alpha * v
+        count += 0.5
+        res = np.linalg.norm(s) / beta0
+        hist.append(res)
+        if res <= ktol:
+            return x + alpha * p, count, hist, True
+        t = pa(s)
+        tt = np.vdot(t, t)
+        if abs(tt) == 0.0:
+            raise KrylovBreakdown("BiCGstab breakdown (t = 0)", count, hist)
+        omega = np.vdot(t, s) / tt
+        x = x + alpha * p + omega * s
+        r = s - omega * t
+        count += 0.5
+        res = np.linalg.norm(r) / beta0
+        hist.append(res)
+        if res <= ktol:
+            return x, count, hist, True
+        if count >= max_iter:
+            break
+    return x, count, hist, False
+
+
 # --------------------------------------------------------------------------
 # trace machinery over a list of slabs (sie.py:112-346)
 
@@ -550,8 +608,9 @@ class OracleSolver:
     def touches(self):
         return int(sum(getattr(s, "counter", [0])[0] for s in self.outer.slabs))
 
-    def solve(self, f, ktol=1e-7, max_iter=200, restart=0, preconditioner="gs"):
-        """``PolarizedTracesSolver.solve`` (sie.py:392-439)."""
+    def solve(self, f, ktol=1e-7, max_iter=200, restart=0, preconditioner="gs", method="gmres"):
+        """``PolarizedTracesSolver.solve`` (sie.py:392-439); ``method`` as ``KrylovConfig.method``
+        (``krylov.py:204-214``)."""
         f = np.asarray(f, dtype=complex).reshape(self.shape)
         T = self.outer
         for s in T.slabs:
@@ -567,8 +626,11 @@ class OracleSolver:
             return OracleResult(u, 0.0, [r], True, r)
         d, p = T.newton_rhs(fl)
         op, pre, unpack = T.flat_ops(preconditioner)
-        x, its, hist, ok = gmres(op, np.concatenate([d.ravel(), p.ravel()]), pre, ktol,
-                                 max_iter, restart)
+        if method == "bicgstab":
+            x, its, hist, ok = bicgstab(op, np.concatenate([d.ravel(), p.ravel()]), pre, ktol, max_iter)
+        else:
+            x, its, hist, ok = gmres(op, np.concatenate([d.ravel(), p.ravel()]), pre, ktol,
+                                     max_iter, restart)
         if not ok:
             raise KrylovBreakdown(f"trace solve did not reach {ktol:g}", residuals=hist)
         a, b = unpack(x)

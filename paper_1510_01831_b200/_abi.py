@@ -61,6 +61,7 @@ class PtKrylov(C.Structure):
     _fields_ = [
         ("ktol", C.c_double), ("max_iter", C.c_int), ("restart", C.c_int),
         ("inner_ktol", C.c_double), ("inner_max_iter", C.c_int), ("precond", C.c_int),
+        ("method", C.c_int),
     ]
 
 

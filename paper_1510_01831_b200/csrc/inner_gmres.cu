@@ -491,7 +491,51 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
   }
   double ss = 0.0;
   constexpr int EPT = 8;  // register-resident w for n <= EPT * IN_THREADS
-  if (n <= EPT * IN_THREADS) {
+  constexpr int FE = 4, FV = 6;  // fast path: n <= FE * IN_THREADS, j < FV (every V_i prefetched)
+  double2 fw[FE];
+  const bool fast = p.arn_fast && gsm && n <= FE * IN_THREADS && j < FV;
+  if (fast) {
+    // W and every V_i (i <= j) issued before the first reduction: one L2 round trip instead of j + 3; the
+    // same per-thread element order and block sums as the path below (bitwise identical results)
+    double2 fv[FV][FE];
+#pragma unroll
+    for (int t = 0; t < FE; ++t) {
+      const int e = tid + t * IN_THREADS;
+      fw[t] = e < n ? ld_cg(W + e) : czero();
+      fw[t].x *= wscale;
+      fw[t].y *= wscale;
+    }
+#pragma unroll
+    for (int i = 0; i < FV; ++i)
+      if (i <= j) {
+        const double2* Vi = vecp(p, job, r, i);
+#pragma unroll
+        for (int t = 0; t < FE; ++t) {
+          const int e = tid + t * IN_THREADS;
+          fv[i][t] = e < n ? ld_cg(Vi + e) : czero();
+        }
+      }
+#pragma unroll
+    for (int i = 0; i < FV; ++i) {
+      if (i > j) break;
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int t = 0; t < FE; ++t) {
+        const double2 c = cconjmul(fv[i][t], fw[t]);
+        sr += c.x;
+        si += c.y;
+      }
+      const double2 h = block_sum2(sr, si, dred);
+      if (tid == 0) {
+        col[i] = h;
+        s_gv[i] = h;
+      }
+#pragma unroll
+      for (int t = 0; t < FE; ++t) fw[t] = csub(fw[t], cmul(h, fv[i][t]));
+    }
+#pragma unroll
+    for (int t = 0; t < FE; ++t) ss += fw[t].x * fw[t].x + fw[t].y * fw[t].y;
+  } else if (n <= EPT * IN_THREADS) {
     double2 wv[EPT];
 #pragma unroll
     for (int t = 0; t < EPT; ++t) {
@@ -647,11 +691,18 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
     if (st != 0) p.iters[job * p.R + r] = st == 1 ? j + 1 : -1;
   }
   __syncthreads();
-  if (s_st == 0)  // V_{j+1} = w / hn (krylov.py:125)
+  if (fast) {  // V_{j+1} = w / hn from registers (the orthogonalized w itself once the instance stops)
+#pragma unroll
+    for (int t = 0; t < FE; ++t) {
+      const int e = tid + t * IN_THREADS;
+      if (e < n) W[e] = s_st == 0 ? make_double2(fw[t].x / hn, fw[t].y / hn) : fw[t];
+    }
+  } else if (s_st == 0) {  // V_{j+1} = w / hn (krylov.py:125)
     for (int e = tid; e < n; e += blockDim.x) {
       const double2 x = W[e];
       W[e] = make_double2(x.x / hn, x.y / hn);
     }
+  }
   __syncthreads();
 }
 
@@ -1323,7 +1374,8 @@ static cudaError_t inner_coop_items_launch(const InnerParams& p0, int njobs, cud
   if (it->second < 1) return cudaErrorNotSupported;
   int nu = nunits;
   void* args[] = {(void*)&p, (void*)&nu};
-  return cudaLaunchCooperativeKernel((const void*)inner_coop_items_kernel, dim3(nsm), dim3(IN_THREADS), args, sm, st);
+  const int grid = p.coop_sms > 0 ? std::min(nsm, p.coop_sms) : nsm;
+  return cudaLaunchCooperativeKernel((const void*)inner_coop_items_kernel, dim3(grid), dim3(IN_THREADS), args, sm, st);
 }
 
 // returns cudaErrorNotSupported when the cooperative path does not apply (caller falls back)
@@ -1357,7 +1409,7 @@ cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st)
     it = occ.emplace(sm, per_sm).first;
   }
   if (it->second < 1) return cudaErrorNotSupported;
-  const int grid = nsm;  // one CTA per SM
+  const int grid = p.coop_sms > 0 ? std::min(nsm, p.coop_sms) : nsm;  // one CTA per SM (of the budget)
   void* args[] = {(void*)&p, (void*)&nunits};
   int nu = nunits;
   args[1] = (void*)&nu;

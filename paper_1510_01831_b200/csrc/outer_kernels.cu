@@ -216,6 +216,46 @@ __global__ void k_norm2(VecView v, long long len, const int* rmap, double* out) 
   if (threadIdx.x == 0) out[r] = s;
 }
 
+// complex dots per active RHS: out[r] = vdot(x, y) = sum conj(x) y (one CTA per RHS, fixed-order sums)
+__global__ void k_cdot(VecView x, VecView y, long long len, const int* rmap, double2* out) {
+  __shared__ double red[64];
+  const int r = rmap[blockIdx.x];
+  const double2* a = x.p + r * x.stride;
+  const double2* b = y.p + r * y.stride;
+  double sr = 0.0, si = 0.0;
+  for (long long i = threadIdx.x; i < len; i += blockDim.x) {
+    const double2 c = cconjmul(ld_cg(a + i), ld_cg(b + i));
+    sr += c.x;
+    si += c.y;
+  }
+  const double2 h = block_sum2(sr, si, red);
+  if (threadIdx.x == 0) out[r] = h;
+}
+
+// BiCGstab vector updates (krylov.py:164-196) per active RHS r with complex coefficients a[r], b[r]:
+//   mode 0: d = x + a y              (s = r - alpha v with a = -alpha; r = s - omega t; x + alpha p)
+//   mode 1: d = x + a (d - b y)      (p = r + beta (p - omega v))
+//   mode 2: d = (d + a y) + b z      (x = x + alpha p + omega s)
+__global__ void k_bicg_update(int mode, VecView d, VecView x, VecView y, VecView z, const double2* a,
+                              const double2* b, long long len, const int* rmap, int nq) {
+  const long long total = len * nq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / len);
+    const long long i = e - (long long)q * len;
+    const int r = rmap[q];
+    double2* dp = d.p + r * d.stride + i;
+    const double2 yv = ld_cg(y.p + r * y.stride + i);
+    if (mode == 0) {
+      *dp = cadd(ld_cg(x.p + r * x.stride + i), cmul(a[r], yv));
+    } else if (mode == 1) {
+      *dp = cadd(ld_cg(x.p + r * x.stride + i), cmul(a[r], csub(*dp, cmul(b[r], yv))));
+    } else {
+      *dp = cadd(cadd(*dp, cmul(a[r], yv)), cmul(b[r], ld_cg(z.p + r * z.stride + i)));
+    }
+  }
+}
+
 // dst = src / scale[r] (scale on device)
 __global__ void k_scale_div(VecView dst, VecView src, long long len, const int* rmap, int nq,
                             const double* scale) {

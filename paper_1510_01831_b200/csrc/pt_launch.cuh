@@ -99,6 +99,8 @@ struct InnerParams {
   int nitems;             // op + pre program items (staged in shared memory)
   int mg;                 // 8-row Green tiles per work group (inner_mg(wmax))
   int tring;              // Green-tile ring slots of the item-program path (inner_tring)
+  int coop_sms;           // SMs (CTAs) of the cooperative inner kernels; 0 = all
+  int arn_fast;           // Arnoldi steps of small instances with the basis prefetched (PT_ARN_SLOW = 0)
 };
 
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns);
@@ -145,6 +147,9 @@ __global__ void k_combine(const OJob* jobs, int njobs, VecTab t, const int* rmap
 __global__ void k_lincomb(VecView dst, long long doff, VecView xv, long long xoff, double a, VecView yv,
                           long long yoff, double b, int use_y, long long len, const int* rmap, int nq);
 __global__ void k_norm2(VecView v, long long len, const int* rmap, double* out);
+__global__ void k_cdot(VecView x, VecView y, long long len, const int* rmap, double2* out);
+__global__ void k_bicg_update(int mode, VecView d, VecView x, VecView y, VecView z, const double2* a,
+                              const double2* b, long long len, const int* rmap, int nq);
 __global__ void k_scale_div(VecView dst, VecView src, long long len, const int* rmap, int nq,
                             const double* scale);
 __global__ void k_arnoldi(double2* V, long long vstride, long long n, int j, const int* rmap, double2* hout,

@@ -73,6 +73,7 @@ int upload(T** dst, const T* src, size_t n) {
 
 }  // namespace
 
+#define PT_RMAP_SLOTS 32
 struct pt_ctx {
   int dev = 0;
   cudaStream_t st = nullptr;
@@ -151,6 +152,8 @@ struct pt_ctx {
   std::map<std::vector<long long>, GraphEnt> graphs;
   long long gen = 0;
   bool graphs_off = false;
+  int coop_sms = 0;  // SM budget of the cooperative inner kernels (PT_COOP_SMS; 0 = all)
+  unsigned rmap_slot = 0;
 };
 
 static cudaEvent_t pool_event(pt_ctx* c) {
@@ -566,7 +569,7 @@ static int ensure_scratch(pt_ctx* c, int R, int capO) {
   CK(cudaMalloc(&c->dscal, sizeof(double) * 2 * R));
   CK(cudaMalloc(&c->hout, sizeof(double2) * (size_t)R * (capO + 2)));
   CK(cudaMalloc(&c->ybuf, sizeof(double2) * (size_t)R * (capO + 1)));
-  CK(cudaMallocHost(&c->hrmap, sizeof(int) * R));
+  CK(cudaMallocHost(&c->hrmap, sizeof(int) * R * PT_RMAP_SLOTS));
   CK(cudaMallocHost(&c->hhout, sizeof(double2) * (size_t)R * (capO + 2)));
   CK(cudaMallocHost(&c->hdscal, sizeof(double) * 2 * R));
   CK(cudaMallocHost(&c->hy, sizeof(double2) * (size_t)R * (capO + 1)));
@@ -713,6 +716,9 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   ip.nitems = c->nitems;
   ip.mg = inner_mg(c->wmax);
   ip.tring = inner_tring(c->wmax, ip.nitems);
+  static const bool arn_slow = std::getenv("PT_ARN_SLOW") != nullptr;
+  ip.arn_fast = !arn_slow;
+  ip.coop_sms = c->coop_sms;
   if (ip.tring < 4 * ip.mg) ip.mg = 1;  // a group's (slot, row tile) tiles must fit in the ring together
   return ip;
 }
@@ -926,8 +932,11 @@ static int apply_op(pt_ctx* c, VecView in, VecView out, int Ract, const SolveIO&
 
 static int set_active(pt_ctx* c, const std::vector<int>& a) {
   c->act = a;
-  for (size_t i = 0; i < a.size(); ++i) c->hrmap[i] = a[i];
-  if (!a.empty()) CK(cudaMemcpyAsync(c->rmap_d, c->hrmap, sizeof(int) * a.size(), cudaMemcpyHostToDevice, c->st));
+  // the pinned staging rotates over PT_RMAP_SLOTS copies: an asynchronous copy still queued behind kernels
+  // never sees its source rewritten by a later set_active (a solve synchronises far more often than that)
+  int* h = c->hrmap + (size_t)(c->rmap_slot++ % PT_RMAP_SLOTS) * c->capR;
+  for (size_t i = 0; i < a.size(); ++i) h[i] = a[i];
+  if (!a.empty()) CK(cudaMemcpyAsync(c->rmap_d, h, sizeof(int) * a.size(), cudaMemcpyHostToDevice, c->st));
   return 0;
 }
 
@@ -1024,7 +1033,174 @@ struct RhsState {
   double beta0 = 0.0;
   int total = 0, k = 0;
   int status = 0;  // 0 running, 1 converged, 2 failed
+  double count = -1.0;  // BiCGstab: half steps (reported as the iteration count when >= 0)
 };
+
+// Outer BiCGstab (krylov.py:138-201, KrylovConfig.method == "bicgstab") on the device operators for the RHS
+// in `run` (beta0 > 0, b = P rhs in Bp, x = 0 in X).  All active RHS advance in lockstep half steps; an RHS
+// leaves the active set when it converges.  Vectors live in the outer basis slots: r, r0, p, v, s, t.
+// Scalars (vdot, norms) come to the host once per reduction, like the reference's numpy scalars.
+static int bicgstab_run(pt_ctx* c, std::vector<RhsState>& rs, std::vector<int>& run, const pt_krylov* cfg, int gs,
+                        const SolveIO& io, const long long kio[4]) {
+  const int R = c->capR;
+  if (grow_outer_basis(c, R, 6)) return PT_CUDA_ERROR;
+  const long long nO = c->nO, vs = (long long)(c->capO + 1) * nO;
+  VecView vr{c->V + 0 * nO, vs}, vr0{c->V + 1 * nO, vs}, vp{c->V + 2 * nO, vs}, vv{c->V + 3 * nO, vs},
+      vsv{c->V + 4 * nO, vs}, vt{c->V + 5 * nO, vs};
+  VecView vB{c->Bp, nO}, vX{c->X, nO}, vT{c->T1, nO}, vA{c->AX, nO};
+  // coefficients [a | b] and dot outputs [d0 | d1], R complex each, device + pinned host
+  double2 *cd = nullptr, *ch = nullptr;
+  CK(cudaMalloc(&cd, sizeof(double2) * 4 * R));
+  CK(cudaMallocHost(&ch, sizeof(double2) * 4 * R));
+  struct Free {
+    double2 *d, *h;
+    ~Free() {
+      cudaFree(d);
+      cudaFreeHost(h);
+    }
+  } fr{cd, ch};
+  double2 *ca = cd, *cb = cd + R, *d0 = cd + 2 * R, *d1 = cd + 3 * R;
+  auto cx = [](double2 v) { return cplx(v.x, v.y); };
+  auto pa = [&](VecView in, VecView out, int Ra, int which) -> int {  // P(A(in)) (krylov.py:151)
+    std::vector<long long> key = {5, which, Ra, gs};
+    key.insert(key.end(), kio, kio + 4);
+    return graphed(c, key, [&]() -> int {
+      int r1 = apply_op(c, in, vT, Ra, io);
+      if (r1) return r1;
+      return apply_pre(c, vT, out, vA, Ra, gs, io);
+    });
+  };
+  auto dots = [&](VecView x0, VecView y0, VecView x1, VecView y1, int two, int Ra) -> int {
+    { LaunchScope ls_(c, 2); }
+    k_cdot<<<Ra, 256, 0, c->st>>>(x0, y0, nO, c->rmap_d, d0);
+    if (two) {
+      LaunchScope ls_(c, 2);
+      k_cdot<<<Ra, 256, 0, c->st>>>(x1, y1, nO, c->rmap_d, d1);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ch + 2 * R, d0, sizeof(double2) * 2 * R, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+  };
+  auto norms = [&](VecView v, int Ra) -> int {
+    { LaunchScope ls_(c, 2); }
+    k_norm2<<<Ra, 256, 0, c->st>>>(v, nO, c->rmap_d, c->dscal);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * R, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+  };
+  auto update = [&](int mode, VecView d, VecView x, VecView y, VecView z, int Ra) -> int {
+    CK(cudaMemcpyAsync(cd, ch, sizeof(double2) * 2 * R, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));  // the host rewrites ch for the next update
+    LaunchScope ls_(c, 2);
+    k_bicg_update<<<grid_for(nO * Ra), 256, 0, c->st>>>(mode, d, x, y, z, ca, cb, nO, c->rmap_d, Ra);
+    CK(cudaGetLastError());
+    return 0;
+  };
+  int rc = 0;
+  if (run.empty()) return 0;
+  if ((rc = set_active(c, run))) return rc;
+  int Ra = (int)run.size();
+  // r = b, r0 = r (x0 = 0, krylov.py:155-157)
+  if ((rc = lincomb(c, vr, 0, vB, 0, 1.0, vB, 0, 0.0, 0, nO, Ra))) return rc;
+  if ((rc = lincomb(c, vr0, 0, vB, 0, 1.0, vB, 0, 0.0, 0, nO, Ra))) return rc;
+  std::vector<cplx> rho(R, cplx(1, 0)), alpha(R, cplx(1, 0)), omega(R, cplx(1, 0)), beta(R, cplx(0, 0));
+  for (int r : run) {
+    rs[r].hist.push_back(1.0);  // norm(r) / beta0 with r = b
+    rs[r].count = 0.0;
+  }
+  double count = 0.0;
+  const int nit = (int)std::ceil((double)cfg->max_iter);
+  for (int it = 0; it < nit && !run.empty(); ++it) {
+    if ((rc = set_active(c, run))) return rc;
+    Ra = (int)run.size();
+    // rho_new = vdot(r0, r) (krylov.py:163)
+    if ((rc = dots(vr0, vr, vr0, vr, 0, Ra))) return rc;
+    for (int r : run) {
+      const cplx rn = cx(ch[2 * R + r]);
+      if (std::abs(rn) < 1e-300 * rs[r].beta0 * rs[r].beta0) {
+        g_err = "BiCGstab breakdown (rho ~ 0)";
+        return PT_BREAKDOWN;
+      }
+      beta[r] = count > 0 ? (rn / rho[r]) * (alpha[r] / omega[r]) : cplx(0, 0);
+      rho[r] = rn;
+      ch[r] = make_double2(beta[r].real(), beta[r].imag());
+      ch[R + r] = make_double2(omega[r].real(), omega[r].imag());
+    }
+    // p = r + beta (p - omega v), or p = r on the first step
+    if (count > 0) {
+      if ((rc = update(1, vp, vr, vv, vv, Ra))) return rc;
+    } else if ((rc = lincomb(c, vp, 0, vr, 0, 1.0, vr, 0, 0.0, 0, nO, Ra))) {
+      return rc;
+    }
+    if ((rc = pa(vp, vv, Ra, 0))) return rc;  // v = P A p
+    if ((rc = dots(vr0, vv, vr0, vv, 0, Ra))) return rc;
+    for (int r : run) {
+      const cplx den = cx(ch[2 * R + r]);
+      if (std::abs(den) < 1e-300 * rs[r].beta0 * rs[r].beta0) {
+        g_err = "BiCGstab breakdown (r0.v ~ 0)";
+        return PT_BREAKDOWN;
+      }
+      alpha[r] = rho[r] / den;
+      ch[r] = make_double2(-alpha[r].real(), -alpha[r].imag());
+    }
+    if ((rc = update(0, vsv, vr, vv, vv, Ra))) return rc;  // s = r - alpha v
+    count += 0.5;
+    if ((rc = norms(vsv, Ra))) return rc;
+    std::vector<int> done, cont;
+    for (int r : run) {
+      const double res = std::sqrt(c->hdscal[r]) / rs[r].beta0;
+      rs[r].hist.push_back(res);
+      rs[r].count = count;
+      (res <= cfg->ktol ? done : cont).push_back(r);
+    }
+    if (!done.empty()) {  // x = x + alpha p (krylov.py:180-182)
+      if ((rc = set_active(c, done))) return rc;
+      for (int r : done) {
+        ch[r] = make_double2(alpha[r].real(), alpha[r].imag());
+        rs[r].status = 1;
+      }
+      if ((rc = update(0, vX, vX, vp, vp, (int)done.size()))) return rc;
+    }
+    run = cont;
+    if (run.empty()) break;
+    if ((rc = set_active(c, run))) return rc;
+    Ra = (int)run.size();
+    if ((rc = pa(vsv, vt, Ra, 1))) return rc;  // t = P A s
+    if ((rc = dots(vt, vt, vt, vsv, 1, Ra))) return rc;
+    for (int r : run) {
+      const cplx tt = cx(ch[2 * R + r]), ts = cx(ch[3 * R + r]);
+      if (std::abs(tt) == 0.0) {
+        g_err = "BiCGstab breakdown (t = 0)";
+        return PT_BREAKDOWN;
+      }
+      omega[r] = ts / tt;
+      ch[r] = make_double2(alpha[r].real(), alpha[r].imag());
+      ch[R + r] = make_double2(omega[r].real(), omega[r].imag());
+    }
+    if ((rc = update(2, vX, vX, vp, vsv, Ra))) return rc;  // x = x + alpha p + omega s
+    for (int r : run) ch[r] = make_double2(-omega[r].real(), -omega[r].imag());
+    if ((rc = update(0, vr, vsv, vt, vt, Ra))) return rc;  // r = s - omega t
+    count += 0.5;
+    if ((rc = norms(vr, Ra))) return rc;
+    cont.clear();
+    for (int r : run) {
+      const double res = std::sqrt(c->hdscal[r]) / rs[r].beta0;
+      rs[r].hist.push_back(res);
+      rs[r].count = count;
+      if (res <= cfg->ktol)
+        rs[r].status = 1;
+      else
+        cont.push_back(r);
+    }
+    run = cont;
+    if (count >= cfg->max_iter) break;
+  }
+  for (int r : run) rs[r].status = 2;
+  run.clear();
+  return 0;
+}
 
 static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg, double2* u, pt_stats* stats) {
   if (R <= 0) return PT_BAD_ARGUMENT;
@@ -1140,6 +1316,9 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
       }
     }
     int total = 0;
+    if (cfg->method == 1) {
+      if ((rc = bicgstab_run(c, rs, run, cfg, gs, io, kio))) return rc;
+    }
     while (total < max_iter && !run.empty()) {
       if ((rc = set_active(c, run))) return rc;
       int Ra = (int)run.size();
@@ -1334,7 +1513,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   if (stats) {
     for (int r = 0; r < R; ++r) {
       const RhsState& s = rs[r];
-      if (stats->iterations) stats->iterations[r] = (double)s.total;
+      if (stats->iterations) stats->iterations[r] = s.count >= 0.0 ? s.count : (double)s.total;
       if (stats->n_residuals) stats->n_residuals[r] = (int)s.hist.size();
       if (stats->residuals)
         for (size_t i = 0; i < s.hist.size() && (int)i < max_iter; ++i) stats->residuals[(size_t)r * max_iter + i] = s.hist[i];
@@ -1449,6 +1628,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   c->wz = pb->nz + 2 * pb->npml;
   c->nI = pb->L - 1;
   if (const char* e = std::getenv("PT_INNER_CAP")) c->inner_cap = std::max(2, atoi(e));
+  if (const char* e = std::getenv("PT_COOP_SMS")) c->coop_sms = std::max(0, atoi(e));
   const int npml = c->npml;
   // layers
   int off = 0;

@@ -203,13 +203,12 @@ class PolarizedTracesSolver:
 
     # -- one call into the C ABI for a batch of sources
     def _run(self, F, config, preconditioner, device_arrays=None, out=None):
-        if config.method != "gmres":
-            raise NotImplementedError("BiCGstab is not on the B200 path yet (SURVEY.md 8(f) rank 3)")
         if preconditioner not in ("gs", "jac"):
             raise ValueError(f"unknown preconditioner {preconditioner!r}")
         R = F.shape[0] if device_arrays is None else device_arrays[2]
         cfg = _abi.PtKrylov(config.ktol, config.max_iter, config.restart, self.layers.inner_ktol,
-                            self.layers.inner_max_iter, 0 if preconditioner == "gs" else 1)
+                            self.layers.inner_max_iter, 0 if preconditioner == "gs" else 1,
+                            0 if config.method == "gmres" else 1)
         wz, wx = self.grid.shape
         nO = 4 * self.nI * wx
         its = np.zeros(R)

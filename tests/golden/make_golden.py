@@ -60,8 +60,21 @@ def _outer_solve(*a, **kw):
         _STATE["in_solve"] = False
 
 
+_orig_bicgstab = ref_krylov.bicgstab
+
+
+def _outer_bicgstab(*a, **kw):
+    # the outer BiCGstab: inner gmres calls made under it are one level down
+    _STATE["depth"] += 1
+    try:
+        return _orig_bicgstab(*a, **kw)
+    finally:
+        _STATE["depth"] -= 1
+
+
 ref_krylov.gmres = _counting_gmres
 ref_krylov.solve = _outer_solve
+ref_krylov.bicgstab = _outer_bicgstab
 
 
 def ref_solver(prob, nested=True):
@@ -77,7 +90,7 @@ def ref_solver(prob, nested=True):
     return pt.PolarizedTracesSolver(grid, model, pml, part, layers=layers)
 
 
-def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1):
+def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1, method="gmres"):
     t0 = time.time()
     s = ref_solver(prob, nested)
     t1 = time.time()
@@ -86,7 +99,7 @@ def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1):
     for lay in s.layers:
         if hasattr(lay, "counter"):
             lay.counter.reset()
-    res = s.solve(f, pt.KrylovConfig(ktol=ktol, max_iter=200))
+    res = s.solve(f, pt.KrylovConfig(ktol=ktol, max_iter=200, method=method))
     t2 = time.time()
     touches = sum(lay.counter.total for lay in s.layers if hasattr(lay, "counter"))
     u = res.u if full_u else res.u[::decim, ::decim]
@@ -102,6 +115,7 @@ def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1):
         source=np.array(prob.sources[src_idx]),
         ktol=ktol,
         nested=nested,
+        method=method,
         offline_s=t1 - t0,
         online_s=t2 - t1,
     )
@@ -117,6 +131,13 @@ BIG = {"cfg1": 4, "cfg2": 8, "cfg3": 8, "cfg4": 8, "cfg5": 12}  # wavefield deci
 def main(argv):
     # ``make_golden.py cfg3 [cfg4 ...]`` regenerates only the named large configs
     # (cfg3 takes minutes, cfg4 tens of minutes, cfg5 hours on the reference)
+    if argv == ["bicgstab"]:  # the outer BiCGstab path (krylov.py:138-201)
+        for name, prob, decim in (("small_b", small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1),
+                                  ("cfg1", make_config("cfg1"), 4)):
+            out = run_case(prob, 1 if name == "small_b" else 0, full_u=decim == 1, decim=decim,
+                           method="bicgstab")
+            np.savez_compressed(os.path.join(HERE, f"{name}_bicgstab.npz"), **out)
+        return
     if argv:
         for name in argv:
             prob = make_config(name)

@@ -13,4 +13,7 @@ GOLDEN = {
     "cfg3": (lambda: make_config("cfg3"), 0, True),
     "cfg4": (lambda: make_config("cfg4"), 0, True),
     "cfg5": (lambda: make_config("cfg5"), 0, True),
+    # outer BiCGstab (KrylovConfig(method="bicgstab"), krylov.py:138-201); the fixture records "method"
+    "small_b_bicgstab": (lambda: small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, True),
+    "cfg1_bicgstab": (lambda: make_config("cfg1"), 0, True),
 }

@@ -74,7 +74,7 @@ def test_layer_solve_matches_nested_layer_solver(case):
 
 
 @pytest.mark.parametrize("name", ["small_a", "small_b", "small_c", "small_direct", "cfg1", "cfg2", "cfg3",
-                                  "cfg4", "cfg5"])
+                                  "cfg4", "cfg5", "small_b_bicgstab", "cfg1_bicgstab"])
 def test_solve_matches_reference_fixture(name):
     make, si, nested = GOLDEN[name]
     prob = make()
@@ -82,7 +82,8 @@ def test_solve_matches_reference_fixture(name):
         _SOLVERS.pop(key).close()  # the large configs hold tens of GB of factors each
     g = np.load(os.path.join(HERE, "golden", f"{name}.npz"))
     dev = device_solver(prob, nested)
-    res = dev.solve(prob.rhs([si])[0], KrylovConfig(ktol=float(g["ktol"]), max_iter=200))
+    method = str(g["method"]) if "method" in g.files else "gmres"
+    res = dev.solve(prob.rhs([si])[0], KrylovConfig(ktol=float(g["ktol"]), max_iter=200, method=method))
     d = int(g["decim"])
     err = rel(res.u[::d, ::d], g["u"])
     assert err <= 1e-8, err

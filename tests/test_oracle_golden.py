@@ -20,13 +20,15 @@ def load(name):
     return np.load(os.path.join(HERE, "golden", f"{name}.npz"))
 
 
-@pytest.mark.parametrize("name", ["small_a", "small_b", "small_c", "small_direct", "cfg1"])
+@pytest.mark.parametrize("name", ["small_a", "small_b", "small_c", "small_direct", "cfg1", "small_b_bicgstab",
+                                  "cfg1_bicgstab"])
 def test_oracle_matches_reference_fixture(name):
     make, si, nested = GOLDEN[name]
     prob = make()
     g = load(name)
     s = OracleSolver.from_problem(prob, nested=nested)
-    r = s.solve(prob.rhs([si])[0], ktol=float(g["ktol"]))
+    method = str(g["method"]) if "method" in g.files else "gmres"
+    r = s.solve(prob.rhs([si])[0], ktol=float(g["ktol"]), method=method)
     d = int(g["decim"])
     u = r.u[::d, ::d]
     assert np.array_equal(u, g["u"]), np.abs(u - g["u"]).max()
