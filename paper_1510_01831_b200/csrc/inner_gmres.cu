@@ -280,7 +280,7 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
 // the chunks this CTA has streamed so far (ring phases persist across calls).  Ends with a cluster barrier.
 #define DA_T 8
 #define DA_NS 8
-#define GV_MAX 128  // Arnoldi steps whose Givens state is staged in shared memory
+#define GV_MAX 32  // Arnoldi steps whose Givens state is staged in shared memory (beyond: global memory)
 // One streaming pass over row tiles [t0, t1) of M for the instances rr[0..nact): see dense_apply.
 // src < 0: x is rhs_pol gathered from the Newton tables (negated) instead of a scratch vector.
 // ring/region: the shared-memory ring; dbar: DA_NS full + DA_NS empty barriers; the partial tiles reuse the
@@ -1391,9 +1391,15 @@ cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st)
   const int nunits = njobs * ((p0.R + 7) / 8);
   if (!p0.dense || nunits > COOP_MAXU || p0.Lc < 2) return cudaErrorNotSupported;
   InnerParams p = p0;
-  // ring: as many DA_KC-chunk slots as fit next to the small arrays (>= 2), and >= the partial tiles
+  // ring: as many DA_KC-chunk slots as fit next to the small arrays and the kernel's static shared memory
+  // (>= 2), and >= the partial tiles
+  static size_t static_sm = (size_t)-1;
+  if (static_sm == (size_t)-1) {
+    cudaFuncAttributes fa;
+    static_sm = cudaFuncGetAttributes(&fa, inner_coop_kernel) == cudaSuccess ? fa.sharedSizeBytes : 16384;
+  }
   const size_t slot = (size_t)DA_T * DA_KC * 512 + 8 * (8 * DA_KC * 4 + 4) * 16;  // dense_slot_bytes(8)
-  const size_t fixed = inner_coop_smem(p, 0);
+  const size_t fixed = inner_coop_smem(p, 0) + static_sm;
   size_t region = std::min((size_t)DA_NS * slot, ((size_t)maxsm - fixed) / slot * slot);
   if (region < 2 * slot || region < (size_t)(IN_THREADS / 32) * DA_T * 4 * 32 * 8) return cudaErrorNotSupported;
   if (p.fused && (region < (size_t)4 * ((p.wmax + 3) & ~3) * 8 * 16 || region < 2 * (P0_KQ - 1) * 2 * 4 * 32 * 8))
