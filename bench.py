@@ -270,6 +270,7 @@ def _config(args, prob):
                         f"Lc={prob.Lc}, {R} point sources batched per step",
             "unknowns": g.nx * g.nz, "nrhs": R, "ktol": prob.ktol,
             "inner_ktol": prob.inner_ktol, "preconditioner": "gs",
+            "inner_backend": getattr(args, "backend", "pt"),
             "l2": "factor working set (Schur inverses) larger than the 126 MB L2; no explicit flush",
             "parallelism": f"rhs-replica x{args.gpus}"}
 
@@ -294,7 +295,7 @@ def run_ours(args):
     prob = make_config(args.config)
     t0 = time.time()
     layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=prob.Lc,
-                                 inner_ktol=prob.inner_ktol, device=f"cuda:{local}")
+                                 inner_ktol=prob.inner_ktol, device=f"cuda:{local}", backend=args.backend)
     solver = PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers,
                                    device=local)
     offline_s = time.time() - t0
@@ -370,7 +371,8 @@ def run_ours(args):
 
     # parity spot check of this run's wavefield against the committed reference fixture
     parity = None
-    gpath = os.path.join(REPO, "tests", "golden", f"{args.config}.npz")
+    gpath = os.path.join(REPO, "tests", "golden",
+                         f"{args.config}{'' if args.backend == 'pt' else '_' + args.backend}.npz")
     if os.path.exists(gpath):
         g = np.load(gpath)
         d = int(g["decim"])
@@ -461,6 +463,8 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nrhs", type=int, default=0, help="solve the config's first N sources (0 = all)")
+    ap.add_argument("--backend", default="pt", choices=["pt", "lu"],
+                    help="inner backend (build_nested_layers backend=; the benchmark line uses 'pt')")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

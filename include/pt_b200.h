@@ -81,6 +81,11 @@ typedef struct {
    * [L] -> [2][n][n] complex row-major, n = 4 (Lc-1) w: the layer's inner GS preconditioner
    * and preconditioned operator pre(op(.)) as dense matrices (sie.py:203-329) */
   const double* const* inner_dense;
+  /* optional (NULL: the inner solve is the polarized-traces GMRES of nested.py:125-153):
+   * [L] -> [m][m] complex row-major, m = 2 (Lc-1) w: the inverse of the assembled cell-interface
+   * system of the direct inner backend (backend="lu", nested.py:156-254); the inner solve of a layer
+   * solve is then x = A^-1 b with b = (row n of cell i, row 1 of cell i+1) of the Newton tables */
+  const double* const* inner_lu;
 } pt_problem;
 
 typedef struct {

@@ -485,6 +485,50 @@ class Cell(Local):
         return out
 
 
+class InnerLU:
+    """Unpivoted block-tridiagonal LU of the assembled cell-interface system (``nested.py:156-254``):
+    2w x 2w blocks per interface from the cells' Green blocks, pivot blocks inverted, both substitutions
+    as matrix-vector products; every matvec counts rows x cols touches (``nested.py:67-73``)."""
+
+    def __init__(self, cells, counter):
+        self.counter = counter
+        nI = len(cells) - 1
+        self.nI = nI
+        w = cells[0].width
+        self.w = w
+        eye = np.eye(w, dtype=complex)
+        zero = np.zeros((w, w), dtype=complex)
+        self.diag, self.lower, self.upper = [], [None], []
+        for i in range(nI):
+            gi, gp, n_i = cells[i].G, cells[i + 1].G, cells[i].n
+            self.diag.append(np.block([[eye - gi[(n_i, "vn")], -gi[(n_i, "vnp")]],
+                                       [-gp[(1, "v0")], eye - gp[(1, "v1")]]]))
+            if i >= 1:
+                self.lower.append(np.block([[-gi[(n_i, "v0")], -gi[(n_i, "v1")]], [zero, zero]]))
+            self.upper.append(np.block([[zero, zero], [-gp[(1, "vn")], -gp[(1, "vnp")]]])
+                              if i <= nI - 2 else None)
+        self.pivinv = []
+        for i in range(nI):
+            piv = self.diag[i].copy()
+            if i >= 1:
+                piv -= self.lower[i] @ (self.pivinv[i - 1] @ self.upper[i - 1])
+            self.pivinv.append(np.linalg.inv(piv))
+
+    def _mv(self, mat, v):
+        self.counter[0] += mat.shape[0] * mat.shape[1]
+        return mat @ v
+
+    def solve(self, b):
+        y = [b[0]]
+        for i in range(1, self.nI):
+            y.append(b[i] - self._mv(self.lower[i], self._mv(self.pivinv[i - 1], y[i - 1])))
+        x = [None] * self.nI
+        x[-1] = self._mv(self.pivinv[-1], y[-1])
+        for i in range(self.nI - 2, -1, -1):
+            x[i] = self._mv(self.pivinv[i], y[i] - self._mv(self.upper[i], x[i + 1]))
+        return x
+
+
 class NestedLayer:
     """One layer solved by the swapped cell decomposition (``nested.py:272-353``).
 
@@ -495,7 +539,7 @@ class NestedLayer:
     """
 
     def __init__(self, nx, n, h, npml, c_layer, C, omega, Lc, inner_ktol=1e-6,
-                 inner_max_iter=200):
+                 inner_max_iter=200, backend="pt"):
         self.nx, self.n, self.h, self.npml = nx, n, h, npml
         self.wx, self.wz = nx + 2 * npml, n + 2 * npml
         self.width = self.wx
@@ -515,6 +559,8 @@ class NestedLayer:
             ccell = cT[off : off + nxc + 2 * npml, :]
             self.cells.append(Cell(n, nxc, h, npml, ccell, C, omega, counter=self.counter))
         self.inner = Traces(self.cells, self.cell_offsets)
+        self.backend = backend
+        self.lu = InnerLU(self.cells, self.counter) if backend == "lu" and Lc > 1 else None
 
     row = Local.row
     block = Local.block
@@ -525,6 +571,14 @@ class NestedLayer:
         fc = self.inner.split(g)
         if self.inner.nI == 0:
             t = np.zeros((0, 2, self.inner.w), dtype=complex)
+        elif self.lu is not None:  # nested.py:322-342 with _InnerLU: rows n of cell i and 1 of cell i+1
+            d, p = self.inner.newton_rhs(fc)
+            x = self.lu.solve([np.concatenate([-d[i, 0], -p[i, 1]]) for i in range(self.inner.nI)])
+            w = self.inner.w
+            t = np.zeros((self.inner.nI, 2, w), dtype=complex)
+            for i in range(self.inner.nI):
+                t[i, 0] = x[i][:w]
+                t[i, 1] = x[i][w:]
         else:
             d, p = self.inner.newton_rhs(fc)
             op, pre, unpack = self.inner.flat_ops("gs")
@@ -572,7 +626,7 @@ class OracleSolver:
     """
 
     def __init__(self, nx, nz, h, npml, c, C, omega, extents, Lc=1, nested=True,
-                 inner_ktol=1e-6, inner_max_iter=200):
+                 inner_ktol=1e-6, inner_max_iter=200, backend="pt"):
         self.nx, self.nz, self.h, self.npml = nx, nz, h, npml
         self.shape = (nz + 2 * npml, nx + 2 * npml)
         self.c = np.asarray(c, dtype=float)
@@ -585,7 +639,7 @@ class OracleSolver:
             cl = self.c[off : off + n + 2 * npml, :]
             if nested:
                 layers.append(NestedLayer(nx, n, h, npml, cl, C, omega, Lc, inner_ktol,
-                                          inner_max_iter))
+                                          inner_max_iter, backend))
             else:
                 layers.append(Local(nx, n, h, npml, cl, C, omega))
         self.outer = Traces(layers, offs)
@@ -596,7 +650,7 @@ class OracleSolver:
         g = prob.grid
         return cls(g.nx, g.nz, g.h, g.npml, prob.model.c, prob.pml.C, prob.pml.omega,
                    prob.partition.extents, prob.Lc, nested=nested,
-                   inner_ktol=kw.get("inner_ktol", prob.inner_ktol),
+                   inner_ktol=kw.get("inner_ktol", prob.inner_ktol), backend=kw.get("backend", "pt"),
                    inner_max_iter=kw.get("inner_max_iter", 200))
 
     def global_operator(self):

@@ -54,6 +54,7 @@ class PtProblem(C.Structure):
         ("sinv", C.POINTER(_dp)), ("green", C.POINTER(_dp)), ("gsmp", C.POINTER(_dp)),
         ("q0", C.POINTER(_dp)),
         ("inner_dense", C.POINTER(_dp)),
+        ("inner_lu", C.POINTER(_dp)),
     ]
 
 
@@ -169,6 +170,17 @@ class Context:
                     P[i] = dptr(arr(v, np.complex128))
             ptr_arrays["inner_dense"] = P
             pb.inner_dense = C.cast(P, C.POINTER(_dp))
+        if F.Lc > 1 and all(getattr(lf, "lu_inv", None) is not None for lf in F.layers):
+            P = (_dp * F.L)()
+            for i, lf in enumerate(F.layers):
+                v = lf.lu_inv
+                if hasattr(v, "data_ptr"):
+                    keep.append(v)
+                    P[i] = C.cast(C.c_void_p(v.data_ptr()), _dp)
+                else:
+                    P[i] = dptr(arr(v, np.complex128))
+            ptr_arrays["inner_lu"] = P
+            pb.inner_lu = C.cast(P, C.POINTER(_dp))
         handle = C.c_void_p()
         rc = lib().pt_create(C.byref(pb), int(device), C.byref(handle))
         if rc != PT_OK:

@@ -187,6 +187,92 @@ __global__ void __launch_bounds__(GS2_KQ * GS2_TPC * 32) k_green_samples2(
     }
 }
 
+// Direct inner backend (nested.py:156-254, backend="lu"): traces x = A^-1 b per (job, RHS), A^-1 the layer's
+// inverted cell-interface system (m = 2 nI w, row-major), b_i = (Newton row n of cell i, row 1 of cell i+1)
+// from the tables, x_i -> traces (nI, 2, w).  CTA = (8-row tile, job, 16 RHS); P0_KQ warps split K, partial
+// tiles summed in a fixed order; DMMA m8n8k4 f64, complex as 4 real products.  Accounting as the reference's
+// substitutions: 4 w^2 (4 nI - 3) touches per instance (TouchCounter, nested.py:67-73).
+__global__ void __launch_bounds__(P0_KQ * 32) k_inner_lu(const int* __restrict__ stage_jobs, const OJob* __restrict__ jobs,
+                                                       const LayerInfo* __restrict__ layers,
+                                                       const double2* __restrict__ lu,
+                                                       const double2* __restrict__ tables, double2* __restrict__ trc,
+                                                       int R, int Lc, int wmax, unsigned long long* counters) {
+  __shared__ double part[(P0_KQ - 1) * 2 * 4 * 32];
+  const int job = stage_jobs[blockIdx.y];
+  const LayerInfo& lay = layers[jobs[job].layer];
+  const int w = lay.w, nI = Lc - 1, m = 2 * nI * w;
+  const int tile = blockIdx.x, n0 = blockIdx.z * 16;
+  if (tile * 8 >= m || n0 >= R) return;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int ar = lane >> 2, ak = lane & 3;
+  const double2* arow = lu + lay.lu_off + (size_t)min(tile * 8 + ar, m - 1) * m + ak;
+  const bool aok = tile * 8 + ar < m;
+  // b[k] for RHS column q: k = (i, h, j) -> tables[job][cell i + h][h ? r1 : rn][q][j]
+  auto bval = [&](int k, int q) -> double2 {
+    const int i = k / (2 * w), rem = k - i * 2 * w, h = rem / w, j = rem - h * w;
+    return __ldg(tables + ((((size_t)job * Lc + i + h) * 4 + (h ? 1 : 2)) * R + q) * wmax + j);
+  };
+  double acc[2][4];
+#pragma unroll
+  for (int g = 0; g < 2; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0;
+  const int nks = (m + 3) >> 2;
+  const int kb = wp * nks / P0_KQ, ke = (wp + 1) * nks / P0_KQ;
+  for (int ks0 = kb; ks0 < ke; ks0 += 8) {
+    double2 av[8], bv[8][2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = (ks0 + u) * 4 + ak;
+      const bool kin = ks0 + u < ke && k < m;
+      av[u] = kin && aok ? __ldg(arow + (size_t)(ks0 + u) * 4) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const int q = n0 + g * 8 + ar;
+        bv[u][g] = kin && q < R ? bval(k, q) : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        dmma_f64(acc[g][0], acc[g][1], av[u].x, bv[u][g].x);
+        dmma_f64(acc[g][2], acc[g][3], av[u].x, bv[u][g].y);
+        dmma_f64(acc[g][0], acc[g][1], -av[u].y, bv[u][g].y);
+        dmma_f64(acc[g][2], acc[g][3], av[u].y, bv[u][g].x);
+      }
+  }
+  if (wp > 0)
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) part[(((wp - 1) * 2 + g) * 4 + t) * 32 + lane] = acc[g][t];
+  __syncthreads();
+  if (wp > 0) return;
+#pragma unroll
+  for (int p2 = 0; p2 < P0_KQ - 1; ++p2)
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[g][t] += part[((p2 * 2 + g) * 4 + t) * 32 + lane];
+  const int row = tile * 8 + ar;
+  if (row < m) {
+    const int i = row / (2 * w), rem = row - i * 2 * w, h = rem / w, j = rem - h * w;
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int q = n0 + g * 8 + 2 * ak + hh;
+        if (q < R)
+          trc[(((size_t)job * R + q) * nI + i) * 2 * wmax + (size_t)h * wmax + j] =
+              make_double2(acc[g][hh], acc[g][2 + hh]);
+      }
+  }
+  if (tile == 0 && threadIdx.x == 0) {
+    const int nq = min(16, R - n0);
+    atomicAdd(&counters[1], (unsigned long long)nq * 4ULL * w * w * (4ULL * nI - 3ULL));
+    atomicAdd(&counters[2], (unsigned long long)nq);
+  }
+}
+
 // dst[seg..] = a*x[seg..] (+ b*y[seg..]) over len elements, for the active RHS
 __global__ void k_lincomb(VecView dst, long long doff, VecView xv, long long xoff, double a, VecView yv,
                           long long yoff, double b, int use_y, long long len, const int* rmap, int nq) {

@@ -24,6 +24,7 @@ struct LayerInfo {
   int prow[4];            // layer rows of slot sources v0,v1,vn,vnp: row(1), row(0), row(n+1), row(n)
   double2 coef[4];        // slot coefficients (subdomain.py:157-182)
   long long dense_off;    // double2 offset of the dense inner [pre; pre o op] pair (-1: none)
+  long long lu_off;       // double2 offset of the direct inner backend's A^-1 (-1: none)
 };
 
 // a[i & 3] without a dynamically indexed (local-memory) array

@@ -147,6 +147,10 @@ __global__ void k_combine(const OJob* jobs, int njobs, VecTab t, const int* rmap
 __global__ void k_lincomb(VecView dst, long long doff, VecView xv, long long xoff, double a, VecView yv,
                           long long yoff, double b, int use_y, long long len, const int* rmap, int nq);
 __global__ void k_norm2(VecView v, long long len, const int* rmap, double* out);
+__global__ void k_inner_lu(const int* __restrict__ stage_jobs, const OJob* __restrict__ jobs,
+                           const LayerInfo* __restrict__ layers, const double2* __restrict__ lu,
+                           const double2* __restrict__ tables, double2* __restrict__ trc, int R, int Lc, int wmax,
+                           unsigned long long* counters);
 __global__ void k_cdot(VecView x, VecView y, long long len, const int* rmap, double2* out);
 __global__ void k_bicg_update(int mode, VecView d, VecView x, VecView y, VecView z, const double2* a,
                               const double2* b, long long len, const int* rmap, int nq);

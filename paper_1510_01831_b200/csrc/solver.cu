@@ -19,6 +19,7 @@
 
 #include "../../include/pt_b200.h"
 #include "pt_launch.cuh"
+#include "stage_dev.cuh"  // P0_KQ (k_inner_lu launch shape)
 
 using cplx = std::complex<double>;
 
@@ -87,6 +88,7 @@ struct pt_ctx {
   double2* gsmp_d = nullptr;  // sampled trace responses (optional; enables the one-pass layer solve)
   double2* q0_d = nullptr;    // pass-0 operators (optional; layer solves without volume sources skip K1)
   double2* dense_d = nullptr; // dense inner operators (optional)
+  double2* lu_d = nullptr;    // direct inner backend: per-layer A^-1 (optional, backend="lu")
   double2* tables_f = nullptr;  // Newton tables of the volume sources alone (NEWTON stage), reused by RECON
   bool tables_f_ok = false;
   int tables_f_R = 0;
@@ -854,7 +856,13 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
       c->k1_bytes += T->bytes;
     }
     InnerParams ip = inner_params(c, S, Ract, io);
-    {
+    if (c->lu_d) {  // direct inner backend: one dense product per layer solve (nested.py:156-254)
+      LaunchScope ls(c, 1);
+      const int mmax = 2 * (c->Lc - 1) * c->wmax;
+      k_inner_lu<<<dim3((mmax + 7) / 8, J, (Ract + 15) / 16), P0_KQ * 32, 0, c->st>>>(
+          S.stage_jobs_d, S.jobs_d, c->lay_d, c->lu_d, c->tables, c->trc, Ract, c->Lc, c->wmax, c->cnt_d);
+      CK(cudaGetLastError());
+    } else {
       LaunchScope ls(c, 1);
       static const bool no_coop = std::getenv("PT_NO_COOP") != nullptr;
       cudaError_t e = no_coop ? cudaErrorNotSupported : inner_coop_launch(ip, J, c->st);
@@ -1649,6 +1657,7 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       li.coef[s] = make_double2(pb->layer_coefs[(l * 4 + s) * 2], pb->layer_coefs[(l * 4 + s) * 2 + 1]);
     }
     li.dense_off = -1;
+    li.lu_off = -1;
     if (li.w > 128) {
       g_err = "layer width n_l + 2 npml exceeds 128 (K1 holds <= 4 rows per lane)";
       return PT_BAD_ARGUMENT;
@@ -1778,6 +1787,20 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
     }
     cudaFree(tmp);
   }
+  // direct inner backend (optional): [L] x [m][m], m = 2 nI w, row-major
+  if (pb->inner_lu && c->Lc > 1) {
+    long long off = 0;
+    for (auto& li : c->lay) {
+      const long long m = 2LL * (c->Lc - 1) * li.w;
+      li.lu_off = off;
+      off += m * m;
+    }
+    CK(cudaMalloc(&c->lu_d, sizeof(double2) * (size_t)off));
+    for (int l = 0; l < c->L; ++l) {
+      const long long m = 2LL * (c->Lc - 1) * c->lay[l].w;
+      CK(cudaMemcpy(c->lu_d + c->lay[l].lu_off, pb->inner_lu[l], sizeof(double2) * (size_t)(m * m), cudaMemcpyDefault));
+    }
+  }
   if (upload(&c->lay_d, c->lay.data(), c->lay.size())) return PT_CUDA_ERROR;
   if (upload(&c->cel_d, c->cel.data(), c->cel.size())) return PT_CUDA_ERROR;
   if (upload(&c->tx_d, reinterpret_cast<const double2*>(pb->tx), 3 * (size_t)c->wx)) return PT_CUDA_ERROR;
@@ -1832,7 +1855,7 @@ int pt_destroy(pt_ctx* c) {
   cudaDeviceSynchronize();
   // the process-level allocations are released with the context
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
-  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->dense_d, (void*)c->lz_d,
+  for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->dense_d, (void*)c->lu_d, (void*)c->lz_d,
                   (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->items_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
                   (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->tables_f,

@@ -107,6 +107,9 @@ class LayerFactors:
     cells: list = field(default_factory=list)
     # (2, n, n) complex: the inner trace problem's dense preconditioner and pre o op (n = 4 (Lc-1) w)
     dense: torch.Tensor = None
+    # (m, m) complex, m = 2 (Lc-1) w: inverse of the assembled cell-interface system of the direct
+    # inner backend (backend="lu", nested.py:156-254)
+    lu_inv: torch.Tensor = None
 
 
 @dataclass
@@ -340,7 +343,46 @@ def inner_dense_operators(lf):
     return Pm, Bm
 
 
-def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=None, inner_dense=None):
+def inner_lu_inverse(lf):
+    """Direct inner backend (``_InnerLU``, ``nested.py:156-254``): the assembled cell-interface system
+    ``A x = b`` with 2w x 2w blocks per interface i (unknowns: rows n of cell i and 1 of cell i+1)
+
+    * diag  ``[[I - G_i(n,vn), -G_i(n,vnp)], [-G_i+1(1,v0), I - G_i+1(1,v1)]]``
+    * lower ``[[-G_i(n,v0), -G_i(n,v1)], [0, 0]]`` at block (i, i-1)
+    * upper ``[[0, 0], [-G_i+1(1,vn), -G_i+1(1,vnp)]]`` at block (i, i+1)
+
+    is inverted once (the reference factors it by unpivoted block LU and substitutes per solve; the
+    inverse applies the same linear map in one dense product, rounding order aside)."""
+    cells = lf.cells
+    nI = len(cells) - 1
+    if nI <= 0:
+        return None
+    w = lf.w
+    dev = cells[0].green.device
+    G = [cf.green.transpose(-1, -2) for cf in cells]  # row-major G[c][row][slot]
+    R1, RN = 1, 2
+    V0, V1, VN, VNP = 0, 1, 2, 3
+    m = 2 * nI * w
+    A = torch.zeros((m, m), dtype=torch.complex128, device=dev)
+    eye = torch.eye(w, dtype=torch.complex128, device=dev)
+    for i in range(nI):
+        gi, gp = G[i], G[i + 1]
+        a, b = 2 * i * w, 2 * i * w + w
+        A[a:b, a:b] = eye - gi[RN, VN]
+        A[a:b, b:b + w] = -gi[RN, VNP]
+        A[b:b + w, a:b] = -gp[R1, V0]
+        A[b:b + w, b:b + w] = eye - gp[R1, V1]
+        if i >= 1:
+            A[a:b, a - 2 * w:a - w] = -gi[RN, V0]
+            A[a:b, a - w:a] = -gi[RN, V1]
+        if i <= nI - 2:
+            A[b:b + w, b + w:b + 2 * w] = -gp[R1, VN]
+            A[b:b + w, b + 2 * w:b + 3 * w] = -gp[R1, VNP]
+    return torch.linalg.inv(A).contiguous()
+
+
+def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=None, inner_dense=None,
+                  backend="pt"):
     """Offline stage for a partitioned problem (all layers, all cells).
 
     ``grid``/``model``/``pml``/``partition`` follow the reference value types
@@ -443,7 +485,9 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
                     q0c[b],
                 )
         lf.cells = cells
-        if green and inner_dense:
+        if green and backend == "lu":
+            lf.lu_inv = inner_lu_inverse(lf)
+        elif green and inner_dense:
             ops = inner_dense_operators(lf)
             if ops is not None:
                 lf.dense = torch.stack(ops).contiguous()

@@ -148,8 +148,8 @@ def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), 
     ``inner_dense`` (None = by Lc) builds the dense inner operators that let
     the inner GMRES run as one dense product per step.
     """
-    if backend != "pt":
-        raise NotImplementedError("only the polarized-traces inner backend ('pt') has a B200 path")
+    if backend not in ("pt", "lu"):
+        raise ValueError(f"unknown inner backend {backend!r}")  # nested.py:283-284
     if disc.kind != "fd":
         raise NotImplementedError("only the finite-difference discretization has a B200 path")
     if plr_threshold is not None:
@@ -160,7 +160,8 @@ def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), 
         raise ValueError("need at least one cell")
     if Lc > 1 and grid.nx < 2 * Lc:
         raise ValueError(f"{Lc} cells need nx >= {2 * Lc}, got {grid.nx}")
-    F = build_factors(grid, model, pml, partition, Lc, device=device or "cpu", inner_dense=inner_dense)
+    F = build_factors(grid, model, pml, partition, Lc, device=device or "cpu", inner_dense=inner_dense,
+                      backend=backend)
     items = []
     for ell, (n, off) in enumerate(zip(partition.extents, partition.offsets)):
         lgrid = Grid(grid.nx, n, grid.h, grid.npml, origin=(grid.origin[0], grid.origin[1] + off))

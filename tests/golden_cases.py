@@ -16,4 +16,9 @@ GOLDEN = {
     # outer BiCGstab (KrylovConfig(method="bicgstab"), krylov.py:138-201); the fixture records "method"
     "small_b_bicgstab": (lambda: small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, True),
     "cfg1_bicgstab": (lambda: make_config("cfg1"), 0, True),
+    # direct inner backend (build_nested_layers(..., backend="lu"), nested.py:156-269); fixture key "backend"
+    "small_b_lu": (lambda: small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, True),
+    "small_c_lu": (lambda: small_problem(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7), 0, True),
+    "cfg1_lu": (lambda: make_config("cfg1"), 0, True),
+    "cfg2_lu": (lambda: make_config("cfg2"), 0, True),
 }

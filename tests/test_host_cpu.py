@@ -207,3 +207,26 @@ def test_dense_inner_operators_match_oracle():
         v = rng.standard_normal(Pm.shape[0]) + 1j * rng.standard_normal(Pm.shape[0])
         for got, want in ((Pm @ v, pre(v)), (Bm @ v, pre(op(v)))):
             assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_inner_lu_inverse_matches_block_lu():
+    """backend="lu": the offline inverse of the assembled cell-interface system applies the same linear map
+    as the reference's block-LU substitutions (nested.py:156-254, restated in the oracle's InnerLU)."""
+    import torch
+
+    from oracle.polartraces_oracle import OracleSolver
+    from paper_1510_01831_b200.configs import small_problem
+    from paper_1510_01831_b200.offline import build_factors
+
+    prob = small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3)
+    F = build_factors(prob.grid, prob.model, prob.pml, prob.partition, prob.Lc, backend="lu")
+    orc = OracleSolver.from_problem(prob, backend="lu")
+    rng = np.random.default_rng(2)
+    for ell, lay in enumerate(orc.outer.slabs):
+        Ainv = F.layers[ell].lu_inv.numpy()
+        w = lay.lu.w
+        b = [rng.standard_normal(2 * w) + 1j * rng.standard_normal(2 * w) for _ in range(lay.lu.nI)]
+        x = np.concatenate(lay.lu.solve(b))
+        y = Ainv @ np.concatenate(b)
+        assert np.linalg.norm(y - x) <= 1e-11 * np.linalg.norm(x)
+        assert F.layers[ell].dense is None

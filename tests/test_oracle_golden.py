@@ -21,12 +21,13 @@ def load(name):
 
 
 @pytest.mark.parametrize("name", ["small_a", "small_b", "small_c", "small_direct", "cfg1", "small_b_bicgstab",
-                                  "cfg1_bicgstab"])
+                                  "cfg1_bicgstab", "small_b_lu", "small_c_lu", "cfg1_lu"])
 def test_oracle_matches_reference_fixture(name):
     make, si, nested = GOLDEN[name]
     prob = make()
     g = load(name)
-    s = OracleSolver.from_problem(prob, nested=nested)
+    backend = str(g["backend"]) if "backend" in g.files else "pt"
+    s = OracleSolver.from_problem(prob, nested=nested, backend=backend)
     method = str(g["method"]) if "method" in g.files else "gmres"
     r = s.solve(prob.rhs([si])[0], ktol=float(g["ktol"]), method=method)
     d = int(g["decim"])
