@@ -86,6 +86,11 @@ typedef struct {
    * system of the direct inner backend (backend="lu", nested.py:156-254); the inner solve of a layer
    * solve is then x = A^-1 b with b = (row n of cell i, row 1 of cell i+1) of the Newton tables */
   const double* const* inner_lu;
+  /* 1: the reference's factored boundary pipeline (assembled_boundary=True, nested.py:355-486) is
+   * selected.  The sample-only layer solves run the same linear maps either way (pass-0 operator =
+   * M_f + direct part, sampled trace response = M_u); this selects its TouchCounter accounting:
+   * per boundary_samples call sum_c 16 w s_c + 16 s_c^2 + 4 nslot_c s_c w (s_c = kept rows of cell c) */
+  int assembled_boundary;
 } pt_problem;
 
 typedef struct {

@@ -55,6 +55,7 @@ class PtProblem(C.Structure):
         ("q0", C.POINTER(_dp)),
         ("inner_dense", C.POINTER(_dp)),
         ("inner_lu", C.POINTER(_dp)),
+        ("assembled_boundary", C.c_int),
     ]
 
 
@@ -181,6 +182,7 @@ class Context:
                     P[i] = dptr(arr(v, np.complex128))
             ptr_arrays["inner_lu"] = P
             pb.inner_lu = C.cast(P, C.POINTER(_dp))
+        pb.assembled_boundary = int(bool(getattr(F, "assembled_boundary", False)))
         handle = C.c_void_p()
         rc = lib().pt_create(C.byref(pb), int(device), C.byref(handle))
         if rc != PT_OK:

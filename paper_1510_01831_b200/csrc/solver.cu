@@ -148,13 +148,15 @@ struct pt_ctx {
   struct GraphEnt {
     int seen = 0;
     cudaGraphExec_t exec = nullptr;
-    long long d_layer_solves = 0, d_launches = 0, d_k1_launches = 0;
+    long long d_layer_solves = 0, d_launches = 0, d_k1_launches = 0, d_touch = 0;
     double d_k1_bytes = 0.0;
   };
   std::map<std::vector<long long>, GraphEnt> graphs;
   long long gen = 0;
   bool graphs_off = false;
   int coop_sms = 0;  // SM budget of the cooperative inner kernels (PT_COOP_SMS; 0 = all)
+  std::vector<long long> asm_touch;  // per layer: assembled-boundary touches per boundary_samples call
+  long long touch_extra = 0;         // host-side touches of this solve (assembled boundary accounting)
   unsigned rmap_slot = 0;
 };
 
@@ -770,6 +772,8 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
       if (e == cudaSuccess) {
         if (ip.tprof) inner_tprof_dump(S.name);
         c->layer_solves += (long long)J * Ract;
+        if (!c->asm_touch.empty())
+          for (const OJob& jb : S.jobs) c->touch_extra += c->asm_touch[jb.layer] * Ract;
         return 0;
       }
       if (e != cudaErrorNotSupported) CK(e);
@@ -892,6 +896,8 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     fprintf(stderr, "K1 tprof nc=%d ntasks=%d: prologue %lld preload %lld bar1 %lld matvec %lld bar2 %lld epi %lld\n",
             T->nc, T->n, tt[0], tt[1], tt[2], tt[3], tt[4], tt[5]);
   }
+  if (!c->asm_touch.empty() && S.samples_only && S.no_volume)  // boundary_samples calls (nested.py:356-359)
+    for (const OJob& jb : S.jobs) c->touch_extra += c->asm_touch[jb.layer] * Ract;
   if (S.any_sample && !fuse_comb) {
     LaunchScope ls(c, 2);
     k_combine<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract, c->wx,
@@ -997,13 +1003,14 @@ static int graphed(pt_ctx* c, std::vector<long long> key, Body&& body) {
   if (g.exec) {
     CK(cudaGraphLaunch(g.exec, c->st));
     c->layer_solves += g.d_layer_solves;
+    c->touch_extra += g.d_touch;
     c->launches += g.d_launches;
     c->k1_launches += g.d_k1_launches;
     c->k1_bytes += g.d_k1_bytes;
     return 0;
   }
   if (g.seen++ == 0) return body();
-  const long long ls0 = c->layer_solves, la0 = c->launches, k10 = c->k1_launches;
+  const long long ls0 = c->layer_solves, la0 = c->launches, k10 = c->k1_launches, tx0 = c->touch_extra;
   const double kb0 = c->k1_bytes;
   const long long gen0 = c->gen;
   CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
@@ -1022,9 +1029,11 @@ static int graphed(pt_ctx* c, std::vector<long long> key, Body&& body) {
     c->launches = la0;
     c->k1_launches = k10;
     c->k1_bytes = kb0;
+    c->touch_extra = tx0;
     return body();
   }
   g.d_layer_solves = c->layer_solves - ls0;
+  g.d_touch = c->touch_extra - tx0;
   g.d_launches = c->launches - la0;
   g.d_k1_launches = c->k1_launches - k10;
   g.d_k1_bytes = c->k1_bytes - kb0;
@@ -1225,6 +1234,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   CK(cudaMemsetAsync(c->cnt_d, 0, sizeof(unsigned long long) * 4, c->st));
   CK(cudaMemsetAsync(c->hist_d, 0, sizeof(int) * PT_HIST, c->st));
   c->layer_solves = 0;
+  c->touch_extra = 0;
   c->launches = c->k1_launches = 0;
   c->k1_bytes = 0.0;
   c->evs.clear();
@@ -1541,7 +1551,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     CK(cudaMemcpy(cnt, c->cnt_d, sizeof(cnt), cudaMemcpyDeviceToHost));
     if (stats->layer_solves) stats->layer_solves[0] = c->layer_solves;
     if (stats->inner_iters) stats->inner_iters[0] = (long long)cnt[0];
-    if (stats->touches) stats->touches[0] = (long long)cnt[1];
+    if (stats->touches) stats->touches[0] = (long long)cnt[1] + c->touch_extra;
     if (stats->inner_hist && stats->inner_hist_len > 0) {
       int hh[PT_HIST];
       CK(cudaMemcpy(hh, c->hist_d, sizeof(hh), cudaMemcpyDeviceToHost));
@@ -1829,6 +1839,13 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
       g_err = "cells need nx_c + 2 npml >= 3 block rows";
       return PT_BAD_ARGUMENT;
     }
+  if (pb->assembled_boundary && c->Lc > 1) {  // nested.py:447-484: M_f, direct and M_u matvecs per call
+    c->asm_touch.assign(c->L, 0);
+    for (const CellInfo& ci : c->cel) {
+      const long long s_ = ci.hi - ci.lo, w = ci.w, nsl = 2 * (ci.has_top + ci.has_bot);
+      c->asm_touch[ci.layer] += 16 * w * s_ + 16 * s_ * s_ + 4 * nsl * s_ * w;
+    }
+  }
   int rc = build_inner(c);
   if (!rc) rc = build_outer(c);
   if (rc) return rc;
@@ -2035,7 +2052,7 @@ int pt_layer_solve(pt_ctx* c, int layer, const double* rhs, int nrhs, double inn
     unsigned long long cnt[4] = {0, 0, 0, 0};
     CK(cudaMemcpy(cnt, c->cnt_d, sizeof(cnt), cudaMemcpyDeviceToHost));
     if (stats->inner_iters) stats->inner_iters[0] = (long long)cnt[0];
-    if (stats->touches) stats->touches[0] = (long long)cnt[1];
+    if (stats->touches) stats->touches[0] = (long long)cnt[1] + c->touch_extra;
     if (stats->inner_hist && stats->inner_hist_len > 0) {
       int hh[PT_HIST];
       CK(cudaMemcpy(hh, c->hist_d, sizeof(hh), cudaMemcpyDeviceToHost));

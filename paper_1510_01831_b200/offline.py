@@ -127,6 +127,9 @@ class Factors:
     tx: tuple  # global T_x diagonals (lower, main, upper), length wx
     tz: tuple  # global T_z diagonals, length wz
     m: np.ndarray  # (wz, wx) squared slowness
+    # the reference's factored boundary pipeline (nested.py:355-486) is selected: same linear maps (this
+    # path's pass-0 / sampled-response operators are M_f / direct / M_u), its touch accounting
+    assembled_boundary: bool = False
 
     @property
     def wx(self):

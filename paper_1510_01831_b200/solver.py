@@ -154,14 +154,16 @@ def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), 
         raise NotImplementedError("only the finite-difference discretization has a B200 path")
     if plr_threshold is not None:
         raise NotImplementedError("PLR compression is not part of the B200 path (off in every config)")
-    if assembled_boundary:
-        raise NotImplementedError("the factored boundary pipeline (Eq. 4.3) is not implemented yet")
     if Lc < 1:
         raise ValueError("need at least one cell")
     if Lc > 1 and grid.nx < 2 * Lc:
         raise ValueError(f"{Lc} cells need nx >= {2 * Lc}, got {grid.nx}")
     F = build_factors(grid, model, pml, partition, Lc, device=device or "cpu", inner_dense=inner_dense,
                       backend=backend)
+    # assembled_boundary (nested.py:355-486): boundary samples through M_f -> inner solve -> direct + M_u.
+    # This path's sample-only layer solves already are those linear maps (pass-0 operator = M_f and the
+    # direct part, sampled trace response = M_u); the flag selects the reference's touch accounting.
+    F.assembled_boundary = bool(assembled_boundary) and Lc > 1
     items = []
     for ell, (n, off) in enumerate(zip(partition.extents, partition.offsets)):
         lgrid = Grid(grid.nx, n, grid.h, grid.npml, origin=(grid.origin[0], grid.origin[1] + off))

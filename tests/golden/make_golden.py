@@ -77,7 +77,7 @@ ref_krylov.solve = _outer_solve
 ref_krylov.bicgstab = _outer_bicgstab
 
 
-def ref_solver(prob, nested=True, backend="pt"):
+def ref_solver(prob, nested=True, backend="pt", assembled=False):
     g = prob.grid
     grid = pt.Grid(g.nx, g.nz, g.h, g.npml)
     model = pt.VelocityModel(grid, prob.model.c)
@@ -86,13 +86,14 @@ def ref_solver(prob, nested=True, backend="pt"):
     layers = None
     if nested:
         layers = pt.build_nested_layers(grid, model, pml, part, Lc=prob.Lc, backend=backend,
-                                        inner_ktol=prob.inner_ktol)
+                                        inner_ktol=prob.inner_ktol, assembled_boundary=assembled)
     return pt.PolarizedTracesSolver(grid, model, pml, part, layers=layers)
 
 
-def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1, method="gmres", backend="pt"):
+def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1, method="gmres", backend="pt",
+             assembled=False):
     t0 = time.time()
-    s = ref_solver(prob, nested, backend)
+    s = ref_solver(prob, nested, backend, assembled)
     t1 = time.time()
     f = prob.rhs([src_idx])[0]
     _INNER.clear()
@@ -117,6 +118,7 @@ def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1, method
         nested=nested,
         method=method,
         backend=backend,
+        assembled=assembled,
         offline_s=t1 - t0,
         online_s=t2 - t1,
     )
@@ -132,6 +134,14 @@ BIG = {"cfg1": 4, "cfg2": 8, "cfg3": 8, "cfg4": 8, "cfg5": 12}  # wavefield deci
 def main(argv):
     # ``make_golden.py cfg3 [cfg4 ...]`` regenerates only the named large configs
     # (cfg3 takes minutes, cfg4 tens of minutes, cfg5 hours on the reference)
+    if argv == ["assembled"]:  # the factored boundary pipeline (nested.py:355-486, Eq. 4.3)
+        for name, prob, si, decim, backend in (
+                ("small_b", small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, 1, "pt"),
+                ("small_c", small_problem(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7), 0, 1, "lu"),
+                ("cfg1", make_config("cfg1"), 0, 4, "pt")):
+            out = run_case(prob, si, full_u=decim == 1, decim=decim, backend=backend, assembled=True)
+            np.savez_compressed(os.path.join(HERE, f"{name}_asm.npz"), **out)
+        return
     if argv == ["lu"]:  # the direct inner backend (nested.py:156-269)
         for name, prob, si, decim in (
                 ("small_b", small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, 1),

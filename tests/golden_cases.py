@@ -21,4 +21,8 @@ GOLDEN = {
     "small_c_lu": (lambda: small_problem(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7), 0, True),
     "cfg1_lu": (lambda: make_config("cfg1"), 0, True),
     "cfg2_lu": (lambda: make_config("cfg2"), 0, True),
+    # factored boundary pipeline (assembled_boundary=True, nested.py:355-486); fixture key "assembled"
+    "small_b_asm": (lambda: small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 1, True),
+    "small_c_asm": (lambda: small_problem(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7), 0, True),
+    "cfg1_asm": (lambda: make_config("cfg1"), 0, True),
 }

@@ -24,14 +24,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _SOLVERS = {}
 
 
-def device_solver(prob, nested=True, backend="pt"):
-    key = (prob.name, prob.Lc if nested else 1, id(prob) if prob.name.startswith("tmp") else 0, backend)
+def device_solver(prob, nested=True, backend="pt", assembled=False):
+    key = (prob.name, prob.Lc if nested else 1, id(prob) if prob.name.startswith("tmp") else 0, backend, assembled)
     if key not in _SOLVERS:
         Lc = prob.Lc if nested else 1
         # the large configs run their offline arithmetic on the GPU (torch), the small ones on the host
         dev = "cuda" if prob.name in ("cfg3", "cfg4", "cfg5") else "cpu"
         layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=Lc,
-                                     inner_ktol=prob.inner_ktol, device=dev, backend=backend)
+                                     inner_ktol=prob.inner_ktol, device=dev, backend=backend,
+                                     assembled_boundary=assembled)
         _SOLVERS[key] = PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition,
                                               layers=layers)
     return _SOLVERS[key]
@@ -75,14 +76,15 @@ def test_layer_solve_matches_nested_layer_solver(case):
 
 @pytest.mark.parametrize("name", ["small_a", "small_b", "small_c", "small_direct", "cfg1", "cfg2", "cfg3",
                                   "cfg4", "cfg5", "small_b_bicgstab", "cfg1_bicgstab", "small_b_lu", "small_c_lu",
-                                  "cfg1_lu", "cfg2_lu"])
+                                  "cfg1_lu", "cfg2_lu", "small_b_asm", "small_c_asm", "cfg1_asm"])
 def test_solve_matches_reference_fixture(name):
     make, si, nested = GOLDEN[name]
     prob = make()
     for key in [k for k in _SOLVERS if k[0] in ("cfg3", "cfg4", "cfg5") and k[0] != name]:
         _SOLVERS.pop(key).close()  # the large configs hold tens of GB of factors each
     g = np.load(os.path.join(HERE, "golden", f"{name}.npz"))
-    dev = device_solver(prob, nested, str(g["backend"]) if "backend" in g.files else "pt")
+    dev = device_solver(prob, nested, str(g["backend"]) if "backend" in g.files else "pt",
+                        bool(g["assembled"]) if "assembled" in g.files else False)
     method = str(g["method"]) if "method" in g.files else "gmres"
     res = dev.solve(prob.rhs([si])[0], KrylovConfig(ktol=float(g["ktol"]), max_iter=200, method=method))
     d = int(g["decim"])
