@@ -20,6 +20,7 @@ from .discretization import (
     partition_layers,
 )
 from .krylov import InnerSolveError, KrylovBreakdown, KrylovConfig, KrylovResult
+from .artifacts import cache_key, dump_offline, load_model, load_offline, save_model
 
 __version__ = "0.1.0"
 
@@ -35,6 +36,11 @@ def __getattr__(name):
 
 
 __all__ = [
+    "save_model",
+    "load_model",
+    "cache_key",
+    "dump_offline",
+    "load_offline",
     "Grid",
     "PmlProfile",
     "VelocityModel",
