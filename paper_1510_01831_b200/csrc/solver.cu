@@ -790,11 +790,13 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   static const bool no_reuse = std::getenv("PT_NO_REUSE") != nullptr;
   const bool rpath = &S == &c->recon && c->tables_f_ok && c->q0_d && S.any_panel && S.grp_d && !no_reuse &&
                      Ract == c->tables_f_R;
-  // opt-in (PT_FUSE_GLUE=1): gather and combine fused into the pass-0 product / sampled response where
-  // nothing else needs P or smp; measured slower on cfg2 (the panel refs are re-read in the inner loops)
+  // opt-in (PT_FUSE_GLUE=1): gather fused into the pass-0 product where nothing else needs P; measured
+  // slower on cfg2 (the panel refs are re-read in the inner loops)
   static const bool no_fuse_glue = std::getenv("PT_FUSE_GLUE") == nullptr;
   const bool direct_b = qpath && !no_fuse_glue;   // pass-0 reads the panels straight from the vectors
-  const bool fuse_comb = gpath && !no_fuse_glue;  // the sampled response writes the combined outputs
+  // the sampled response writes the combined outputs (k_combine folded in; PT_NO_FUSE_COMB keeps it apart)
+  static const bool no_fuse_comb = std::getenv("PT_NO_FUSE_COMB") != nullptr;
+  const bool fuse_comb = gpath && (!no_fuse_glue || !no_fuse_comb);
   if (S.any_panel && !direct_b) {
     LaunchScope ls(c, 2);
     k_gather_panels<<<grid_for((long long)J * 4 * Ract * c->wx), 256, 0, c->st>>>(S.jobs_d, J, tab, c->rmap_d, Ract,

@@ -47,6 +47,8 @@ SWITCHES = {
     "item-programs": {"PT_NO_DENSE": "1"},
     "cluster-dense": {"PT_NO_COOP": "1"},
     "cluster-items": {"PT_NO_DENSE": "1", "PT_NO_COOP": "1"},
+    "separate-combine": {"PT_NO_FUSE_COMB": "1"},
+    "fused-glue": {"PT_FUSE_GLUE": "1"},
     "fused-stage": {"PT_FUSE": "1"},
     "recon-k1": {"PT_NO_REUSE": "1"},
 }
