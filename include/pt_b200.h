@@ -78,8 +78,9 @@ typedef struct {
    * row (4 nk); M = roundup(4 w + 4 nk, 8) */
   const double* const* q0;
   /* optional (NULL: the inner GMRES applies its operator and preconditioner panel by panel):
-   * [L] -> [2][n][n] complex row-major, n = 4 (Lc-1) w: the layer's inner GS preconditioner
-   * and preconditioned operator pre(op(.)) as dense matrices (sie.py:203-329) */
+   * [L] -> [inner_dense_count][n][n] complex row-major, n = 4 (Lc-1) w: the layer's inner GS
+   * preconditioner and preconditioned operator pre(op(.)) as dense matrices (sie.py:203-329), then
+   * optionally E pre and E^2 pre (E = pre(op(.)) - I) for the s-step start of the inner GMRES */
   const double* const* inner_dense;
   /* optional (NULL: the inner solve is the polarized-traces GMRES of nested.py:125-153):
    * [L] -> [m][m] complex row-major, m = 2 (Lc-1) w: the inverse of the assembled cell-interface
@@ -91,6 +92,7 @@ typedef struct {
    * M_f + direct part, sampled trace response = M_u); this selects its TouchCounter accounting:
    * per boundary_samples call sum_c 16 w s_c + 16 s_c^2 + 4 nslot_c s_c w (s_c = kept rows of cell c) */
   int assembled_boundary;
+  int inner_dense_count;     /* matrices per layer in inner_dense: 2, or 4 with the s-step operators */
 } pt_problem;
 
 typedef struct {

@@ -56,6 +56,7 @@ class PtProblem(C.Structure):
         ("inner_dense", C.POINTER(_dp)),
         ("inner_lu", C.POINTER(_dp)),
         ("assembled_boundary", C.c_int),
+        ("inner_dense_count", C.c_int),
     ]
 
 
@@ -171,6 +172,7 @@ class Context:
                     P[i] = dptr(arr(v, np.complex128))
             ptr_arrays["inner_dense"] = P
             pb.inner_dense = C.cast(P, C.POINTER(_dp))
+            pb.inner_dense_count = int(F.layers[0].dense.shape[0])
         if F.Lc > 1 and all(getattr(lf, "lu_inv", None) is not None for lf in F.layers):
             P = (_dp * F.L)()
             for i, lf in enumerate(F.layers):

@@ -706,6 +706,182 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
   __syncthreads();
 }
 
+// One Givens step of krylov.py:97-127 on thread 0: column col[0..j+1] (col[j+1] = hn on entry) of instance
+// (job, r); applies the stored rotations, forms rotation j, updates g, writes the column, the rotation and the
+// state / iteration count exactly as instance_arnoldi does.  Returns the state (0 running, 1 converged, 2 failed).
+__device__ int givens_col(const InnerParams& p, int job, int r, int j, double2* col, double hn) {
+  const size_t hld = (size_t)p.cap + 1;
+  double2* H = p.hess + (size_t)(job * p.R + r) * p.hstride;
+  double2* g = H + hld * p.cap;
+  double2* cs = g + (p.cap + 1);
+  double2* sn = cs + p.cap;
+  for (int i = 0; i < j; ++i) {
+    const double2 t = cadd(cmul(cs[i], col[i]), cmul(sn[i], col[i + 1]));
+    const double2 nsc = make_double2(-sn[i].x, sn[i].y);  // -conj(sn)
+    const double2 csc = make_double2(cs[i].x, -cs[i].y);  // conj(cs)
+    col[i + 1] = cadd(cmul(nsc, col[i]), cmul(csc, col[i + 1]));
+    col[i] = t;
+  }
+  const double aa = hypot(col[j].x, col[j].y);
+  const double d = sqrt(aa * aa + hn * hn);
+  int st = 0;
+  if (d == 0.0) {
+    st = 2;
+    atomicMax(p.err, 3);
+  } else {
+    const double2 c = make_double2(col[j].x / d, -col[j].y / d);
+    const double2 sv = make_double2(hn / d, 0.0);
+    cs[j] = c;
+    sn[j] = sv;
+    col[j] = cadd(cmul(c, col[j]), make_double2(sv.x * hn, 0.0));
+    const double2 gj = g[j];
+    const double2 gj1 = cmul(make_double2(-sv.x, sv.y), gj);
+    g[j + 1] = gj1;
+    g[j] = cmul(c, gj);
+    const double res = hypot(gj1.x, gj1.y) / p.beta0[job * p.R + r];
+    if (hn == 0.0) {
+      st = res > p.ktol ? 2 : 1;  // happy breakdown (krylov.py:116-124)
+      if (st == 2) atomicMax(p.err, 3);
+    } else if (res <= p.ktol) {
+      st = 1;
+    } else if (j + 1 == p.max_iter) {
+      st = 2;
+      atomicMax(p.err, 2);  // InnerSolveError (nested.py:148-152)
+    }
+  }
+  double2* hc = H + (size_t)j * hld;
+  for (int i = 0; i <= j + 1; ++i) hc[i] = col[i];
+  p.state[job * p.R + r] = st;
+  if (st != 0) p.iters[job * p.R + r] = st == 1 ? j + 1 : -1;
+  return st;
+}
+
+// s-step start of the inner GMRES (krylov.py:61-127, steps j = 0 and 1) for one instance, from m0 = b = pre(rhs)
+// (VY), m1 = E b (VT) and m2 = E^2 b (VA), E = pre(op(.)) - I, all three produced by ONE dense pass: A V = E V + V
+// gives the two products of the Arnoldi steps without waiting for the GPU in between.  The MGS, norms, Givens
+// rotations and state are krylov.py's; only A V_j is formed from the shifted powers instead of a fresh product.
+// Leaves V_0..V_2 (as far as the instance runs), H columns 0-1 and the Givens state as instance_arnoldi would.
+// n <= SE * IN_THREADS.
+__device__ __noinline__ void instance_sstep(const InnerParams& p, int job, int r, int n, int VY, int VT, int VA,
+                                            double* dred) {
+  constexpr int SE = 4;
+  const int tid = threadIdx.x;
+  const double2* M0 = vecp(p, job, r, VY);
+  const double2* M1 = vecp(p, job, r, VT);
+  const double2* M2 = vecp(p, job, r, VA);
+  double2 m0[SE], m1[SE], m2[SE], w[SE], v1[SE];
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    const int e = tid + t * IN_THREADS;
+    m0[t] = e < n ? ld_cg(M0 + e) : czero();
+    m1[t] = e < n ? ld_cg(M1 + e) : czero();
+    m2[t] = e < n ? ld_cg(M2 + e) : czero();
+  }
+  __shared__ double2 s_col[4];
+  __shared__ int s_st;
+  __shared__ double s_hn;
+  // beta0 = ||b|| (instance_init)
+  double ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < SE; ++t) ss += m0[t].x * m0[t].x + m0[t].y * m0[t].y;
+  ss = block_sum(ss, dred);
+  const double b0 = sqrt(ss);
+  if (tid == 0) {
+    double2* g = p.hess + (size_t)(job * p.R + r) * p.hstride + ((size_t)p.cap + 1) * p.cap;
+    g[0] = make_double2(b0, 0.0);
+    p.beta0[job * p.R + r] = b0;
+    p.state[job * p.R + r] = b0 == 0.0 ? 1 : 0;
+    p.iters[job * p.R + r] = b0 == 0.0 ? 0 : -1;
+  }
+  if (b0 == 0.0) {  // converged with zero iterations (krylov.py:62-65)
+    __syncthreads();
+    return;
+  }
+  double2* V0 = vecp(p, job, r, 0);
+  // ---- j = 0: V_0 = b / beta0, w = A V_0 = E b / beta0 + V_0
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    const int e = tid + t * IN_THREADS;
+    const double2 v0 = make_double2(m0[t].x / b0, m0[t].y / b0);
+    m0[t] = v0;                                             // m0 holds V_0 from here
+    m1[t] = make_double2(m1[t].x / b0, m1[t].y / b0);       // E V_0
+    m2[t] = make_double2(m2[t].x / b0, m2[t].y / b0);       // E^2 V_0
+    if (e < n) V0[e] = v0;
+    w[t] = cadd(m1[t], v0);
+  }
+  double sr = 0.0, si = 0.0;
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    const double2 c = cconjmul(m0[t], w[t]);
+    sr += c.x;
+    si += c.y;
+  }
+  const double2 h00 = block_sum2(sr, si, dred);
+  ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    w[t] = csub(w[t], cmul(h00, m0[t]));
+    ss += w[t].x * w[t].x + w[t].y * w[t].y;
+  }
+  const double hn0 = sqrt(block_sum(ss, dred));
+  if (tid == 0) {
+    s_col[0] = h00;
+    s_col[1] = make_double2(hn0, 0.0);
+    s_st = givens_col(p, job, r, 0, s_col, hn0);
+  }
+  __syncthreads();
+  if (s_st != 0) return;
+  // ---- j = 1: V_1 = w / hn0, E V_1 = (E^2 V_0 + E V_0 - h00 E V_0) / hn0, w = E V_1 + V_1
+  double2* V1 = vecp(p, job, r, 1);
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    const int e = tid + t * IN_THREADS;
+    v1[t] = make_double2(w[t].x / hn0, w[t].y / hn0);
+    if (e < n) V1[e] = v1[t];
+    const double2 ev = csub(cadd(m2[t], m1[t]), cmul(h00, m1[t]));
+    w[t] = cadd(make_double2(ev.x / hn0, ev.y / hn0), v1[t]);
+  }
+  sr = si = 0.0;
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    const double2 c = cconjmul(m0[t], w[t]);
+    sr += c.x;
+    si += c.y;
+  }
+  const double2 h01 = block_sum2(sr, si, dred);
+  sr = si = 0.0;
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    w[t] = csub(w[t], cmul(h01, m0[t]));
+    const double2 c = cconjmul(v1[t], w[t]);
+    sr += c.x;
+    si += c.y;
+  }
+  const double2 h11 = block_sum2(sr, si, dred);
+  ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    w[t] = csub(w[t], cmul(h11, v1[t]));
+    ss += w[t].x * w[t].x + w[t].y * w[t].y;
+  }
+  const double hn1 = sqrt(block_sum(ss, dred));
+  if (tid == 0) {
+    s_col[0] = h01;
+    s_col[1] = h11;
+    s_col[2] = make_double2(hn1, 0.0);
+    s_st = givens_col(p, job, r, 1, s_col, hn1);
+  }
+  __syncthreads();
+  if (s_st != 0) return;
+  double2* V2 = vecp(p, job, r, 2);  // V_2 = w / hn1: the regular loop continues at j = 2
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    const int e = tid + t * IN_THREADS;
+    if (e < n) V2[e] = make_double2(w[t].x / hn1, w[t].y / hn1);
+  }
+  __syncthreads();
+}
+
 // b = Y = pre(rhs) and W = V_1 = pre(op(b)) (the product taken on the unnormalized b): beta0 = ||b||,
 // V_0 = b / beta0, then the Arnoldi step j = 0 on W / beta0 (= pre(op(V_0)) up to rounding)
 __device__ void instance_arnoldi0(const InnerParams& p, int job, int r, int n, int VY, double* dred) {
@@ -1074,12 +1250,25 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
     }
   }
   gsync();
-  // ---- b = pre(rhs) (krylov.py:61)
+  // ---- b = pre(rhs) (krylov.py:61); s-step start: E b and E^2 b in the same pass, then Arnoldi steps 0-1
   T.tick(8);
+  const int VT = p.cap + 3, VA = p.cap + 4;
   coop_apply(0, VB, VY, true);
+  if (p.sstep) {
+    coop_apply(2, VB, VT, true);
+    coop_apply(3, VB, VA, true);
+  }
   T.tick(3);
   gsync();
-  for (int j = 0; j < p.max_iter; ++j) {
+  if (p.sstep) {
+    for (int t = b; t < nunits * 8; t += G) {
+      const int u = t >> 3, l = t & 7;
+      if (l < uni(u)) instance_sstep(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), VY, VT, VA, dred);
+    }
+    T.tick(6);
+    gsync();
+  }
+  for (int j = p.sstep ? 2 : 0; j < p.max_iter; ++j) {
     if (j > 0) {  // at j = 0 every instance enters (its state is set by the first Arnoldi step)
       load_states(false);
       int any = 0;

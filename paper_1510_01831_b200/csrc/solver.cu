@@ -75,6 +75,7 @@ int upload(T** dst, const T* src, size_t n) {
 }  // namespace
 
 #define PT_RMAP_SLOTS 32
+#define IN_THREADS_HOST 256  // inner kernels' block size (IN_THREADS in inner_gmres.cu)
 struct pt_ctx {
   int dev = 0;
   cudaStream_t st = nullptr;
@@ -89,6 +90,7 @@ struct pt_ctx {
   double2* q0_d = nullptr;    // pass-0 operators (optional; layer solves without volume sources skip K1)
   double2* dense_d = nullptr; // dense inner operators (optional)
   double2* lu_d = nullptr;    // direct inner backend: per-layer A^-1 (optional, backend="lu")
+  int dense_cnt = 2;          // dense matrices per layer (4: with the s-step operators)
   double2* tables_f = nullptr;  // Newton tables of the volume sources alone (NEWTON stage), reused by RECON
   bool tables_f_ok = false;
   int tables_f_R = 0;
@@ -723,6 +725,8 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   static const bool arn_slow = std::getenv("PT_ARN_SLOW") != nullptr;
   ip.arn_fast = !arn_slow;
   ip.coop_sms = c->coop_sms;
+  static const bool no_sstep = std::getenv("PT_NO_SSTEP") != nullptr;
+  ip.sstep = !no_sstep && c->dense_cnt >= 4 && 4LL * (c->Lc - 1) * c->wmax <= 4 * IN_THREADS_HOST && c->dense_d;
   if (ip.tring < 4 * ip.mg) ip.mg = 1;  // a group's (slot, row tile) tiles must fit in the ring together
   return ip;
 }
@@ -1777,20 +1781,22 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   // dense inner operators (optional): [L] x [2][n][n], n = 4 nI w
   if (pb->inner_dense && c->Lc > 1) {
     // stored DMMA-fragment tile-major (k_dense_tiles), rows padded to whole 8-row tiles
+    const int cnt = pb->inner_dense_count >= 4 ? 4 : 2;
+    c->dense_cnt = cnt;
     long long doff = 0;
     for (auto& li : c->lay) {
       const long long n = 4LL * (c->Lc - 1) * li.w;
       li.dense_off = doff;
-      doff += 2 * dense_matrix_elems(n);
+      doff += cnt * dense_matrix_elems(n);
     }
     CK(cudaMalloc(&c->dense_d, sizeof(double2) * (size_t)doff));
     double2* tmp = nullptr;
     const long long nmx = 4LL * (c->Lc - 1) * c->wmax;
-    CK(cudaMalloc(&tmp, sizeof(double2) * (size_t)(2 * nmx * nmx)));
+    CK(cudaMalloc(&tmp, sizeof(double2) * (size_t)(cnt * nmx * nmx)));
     for (int l = 0; l < c->L; ++l) {
       const long long n = 4LL * (c->Lc - 1) * c->lay[l].w, me = dense_matrix_elems(n);
-      CK(cudaMemcpy(tmp, pb->inner_dense[l], sizeof(double2) * (size_t)(2 * n * n), cudaMemcpyDefault));
-      for (int m = 0; m < 2; ++m) {
+      CK(cudaMemcpy(tmp, pb->inner_dense[l], sizeof(double2) * (size_t)(cnt * n * n), cudaMemcpyDefault));
+      for (int m = 0; m < cnt; ++m) {
         k_dense_tiles<<<512, 256>>>(tmp + (size_t)m * n * n, c->dense_d + c->lay[l].dense_off + (size_t)m * me,
                                     (int)n, DA_KC);
         CK(cudaGetLastError());

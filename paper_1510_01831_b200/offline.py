@@ -105,7 +105,8 @@ class LayerFactors:
     coefs: np.ndarray  # (4,) layer-level slot coefficients
     prows: np.ndarray  # (4,) layer rows of the slot sources
     cells: list = field(default_factory=list)
-    # (2, n, n) complex: the inner trace problem's dense preconditioner and pre o op (n = 4 (Lc-1) w)
+    # (4, n, n) complex: the inner trace problem's dense preconditioner, pre o op, and the s-step operators
+    # E pre, E^2 pre with E = pre o op - I (n = 4 (Lc-1) w)
     dense: torch.Tensor = None
     # (m, m) complex, m = 2 (Lc-1) w: inverse of the assembled cell-interface system of the direct
     # inner backend (backend="lu", nested.py:156-254)
@@ -346,6 +347,19 @@ def inner_dense_operators(lf):
     return Pm, Bm
 
 
+def inner_sstep_operators(Pm, Bm):
+    """``(S1, S2) = (E Pm, E^2 Pm)`` with ``E = Bm - I`` (``Bm = pre o op``): applied to the inner rhs they
+    give ``E b`` and ``E^2 b`` for ``b = pre(rhs)`` in the same pass as ``b`` itself.  The shifted powers span
+    the Krylov spaces of the first two GMRES steps (``span{b, A b, A^2 b}``, ``A = E + I``) and, with
+    ``A V = E V + V``, let the device run those two Arnoldi steps without waiting for a product in between;
+    ``E`` is small where the preconditioner works, so no large vectors cancel."""
+    n = Pm.shape[0]
+    E = Bm - torch.eye(n, dtype=Bm.dtype, device=Bm.device)
+    S1 = E @ Pm
+    S2 = E @ S1
+    return S1, S2
+
+
 def inner_lu_inverse(lf):
     """Direct inner backend (``_InnerLU``, ``nested.py:156-254``): the assembled cell-interface system
     ``A x = b`` with 2w x 2w blocks per interface i (unknowns: rows n of cell i and 1 of cell i+1)
@@ -493,7 +507,8 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
         elif green and inner_dense:
             ops = inner_dense_operators(lf)
             if ops is not None:
-                lf.dense = torch.stack(ops).contiguous()
+                # [pre, pre o op, E pre, E^2 pre]: the last two drive the s-step start of the inner GMRES
+                lf.dense = torch.stack(list(ops) + list(inner_sstep_operators(*ops))).contiguous()
         layers.append(lf)
     tx = axis_tridiag(pml, grid.nx, h)
     tz = axis_tridiag(pml, grid.nz, h)

@@ -203,10 +203,16 @@ def test_dense_inner_operators_match_oracle():
     rng = np.random.default_rng(2)
     for l, lf in enumerate(F.layers):
         op, pre, _ = orc.outer.slabs[l].inner.flat_ops("gs")
-        Pm, Bm = (m.numpy() for m in lf.dense)
+        Pm, Bm, S1, S2 = (m.numpy() for m in lf.dense)
         v = rng.standard_normal(Pm.shape[0]) + 1j * rng.standard_normal(Pm.shape[0])
         for got, want in ((Pm @ v, pre(v)), (Bm @ v, pre(op(v)))):
             assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+        # s-step operators: E pre and E^2 pre with E = pre o op - I
+        b = pre(v)
+        e1 = pre(op(b)) - b
+        e2 = pre(op(e1)) - e1
+        assert np.abs(S1 @ v - e1).max() <= 1e-11 * np.abs(b).max()
+        assert np.abs(S2 @ v - e2).max() <= 1e-11 * np.abs(b).max()
 
 
 def test_inner_lu_inverse_matches_block_lu():
