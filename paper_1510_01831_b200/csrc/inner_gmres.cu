@@ -706,15 +706,17 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
   __syncthreads();
 }
 
-// One Givens step of krylov.py:97-127 on thread 0: column col[0..j+1] (col[j+1] = hn on entry) of instance
-// (job, r); applies the stored rotations, forms rotation j, updates g, writes the column, the rotation and the
-// state / iteration count exactly as instance_arnoldi does.  Returns the state (0 running, 1 converged, 2 failed).
-__device__ int givens_col(const InnerParams& p, int job, int r, int j, double2* col, double hn) {
+// One Givens step of krylov.py:97-127 on thread 0 with the rotation state in registers (no global read-back):
+// column col[0..j+1] (col[j+1] = hn on entry), rotations cs/sn[0..j), g[0..j] of instance (job, r) and its
+// beta0 b0.  Forms rotation j, updates g, writes the column, the rotation, g and the state / iteration count as
+// instance_arnoldi does.  Returns the state (0 running, 1 converged, 2 failed).
+__device__ int givens_col(const InnerParams& p, int job, int r, int j, double2* col, double hn, double2* cs,
+                          double2* sn, double2* g, double b0) {
   const size_t hld = (size_t)p.cap + 1;
   double2* H = p.hess + (size_t)(job * p.R + r) * p.hstride;
-  double2* g = H + hld * p.cap;
-  double2* cs = g + (p.cap + 1);
-  double2* sn = cs + p.cap;
+  double2* gG = H + hld * p.cap;
+  double2* csG = gG + (p.cap + 1);
+  double2* snG = csG + p.cap;
   for (int i = 0; i < j; ++i) {
     const double2 t = cadd(cmul(cs[i], col[i]), cmul(sn[i], col[i + 1]));
     const double2 nsc = make_double2(-sn[i].x, sn[i].y);  // -conj(sn)
@@ -733,12 +735,16 @@ __device__ int givens_col(const InnerParams& p, int job, int r, int j, double2* 
     const double2 sv = make_double2(hn / d, 0.0);
     cs[j] = c;
     sn[j] = sv;
+    csG[j] = c;
+    snG[j] = sv;
     col[j] = cadd(cmul(c, col[j]), make_double2(sv.x * hn, 0.0));
     const double2 gj = g[j];
     const double2 gj1 = cmul(make_double2(-sv.x, sv.y), gj);
     g[j + 1] = gj1;
     g[j] = cmul(c, gj);
-    const double res = hypot(gj1.x, gj1.y) / p.beta0[job * p.R + r];
+    gG[j + 1] = gj1;
+    gG[j] = g[j];
+    const double res = hypot(gj1.x, gj1.y) / b0;
     if (hn == 0.0) {
       st = res > p.ktol ? 2 : 1;  // happy breakdown (krylov.py:116-124)
       if (st == 2) atomicMax(p.err, 3);
@@ -762,7 +768,7 @@ __device__ int givens_col(const InnerParams& p, int job, int r, int j, double2* 
 // rotations and state are krylov.py's; only A V_j is formed from the shifted powers instead of a fresh product.
 // Leaves V_0..V_2 (as far as the instance runs), H columns 0-1 and the Givens state as instance_arnoldi would.
 // n <= SE * IN_THREADS.
-__device__ __noinline__ void instance_sstep(const InnerParams& p, int job, int r, int n, int VY, int VT, int VA,
+__device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int VY, int VT, int VA,
                                             double* dred) {
   constexpr int SE = 4;
   const int tid = threadIdx.x;
@@ -824,10 +830,12 @@ __device__ __noinline__ void instance_sstep(const InnerParams& p, int job, int r
     ss += w[t].x * w[t].x + w[t].y * w[t].y;
   }
   const double hn0 = sqrt(block_sum(ss, dred));
+  __shared__ double2 s_rot[7];  // cs[0..1], sn[0..1], g[0..2] of the Givens process (thread 0)
   if (tid == 0) {
+    s_rot[4] = make_double2(b0, 0.0);  // g[0] = beta0
     s_col[0] = h00;
     s_col[1] = make_double2(hn0, 0.0);
-    s_st = givens_col(p, job, r, 0, s_col, hn0);
+    s_st = givens_col(p, job, r, 0, s_col, hn0, s_rot, s_rot + 2, s_rot + 4, b0);
   }
   __syncthreads();
   if (s_st != 0) return;
@@ -869,7 +877,7 @@ __device__ __noinline__ void instance_sstep(const InnerParams& p, int job, int r
     s_col[0] = h01;
     s_col[1] = h11;
     s_col[2] = make_double2(hn1, 0.0);
-    s_st = givens_col(p, job, r, 1, s_col, hn1);
+    s_st = givens_col(p, job, r, 1, s_col, hn1, s_rot, s_rot + 2, s_rot + 4, b0);
   }
   __syncthreads();
   if (s_st != 0) return;
