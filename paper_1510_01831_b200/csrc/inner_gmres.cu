@@ -291,10 +291,12 @@ __device__ __forceinline__ uint32_t dense_slot_bytes(int scmax) {
 }
 __device__ void dense_pass(const InnerParams& p, const double2* __restrict__ Mt, int n, int job, const int* rr,
                            int nact, int src, int dst, int t0, int t1, unsigned char* ring, size_t region,
-                           uint64_t* dbar, unsigned& dch, int scmax) {
+                           uint64_t* dbar, unsigned& dch, int scmax, int nmat = 1) {
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   const int ar = lane >> 2, ak = lane & 3;
-  const int T8 = (n + 7) >> 3, nks = n >> 2;
+  // nmat stacked matrices (row tiles of matrix m at [m T8m, (m+1) T8m)) share the pass's x: T8 = stored row
+  // tiles per chunk, the output of stacked tile t goes to vector dst + t / T8m, row (t % T8m) * 8 + ar
+  const int T8m = (n + 7) >> 3, T8 = nmat * T8m, nks = n >> 2;
   const int XST = scmax * DA_KC * 4 + 4;                            // padded x row (double2) per instance
   const uint32_t abytes = (uint32_t)DA_T * DA_KC * 512u;            // A part of a slot
   const uint32_t slot_bytes = dense_slot_bytes(scmax);
@@ -404,12 +406,13 @@ __device__ void dense_pass(const InnerParams& p, const double2* __restrict__ Mt,
       for (int gw = 0; gw < IN_THREADS / 32; ++gw)
 #pragma unroll
         for (int v = 0; v < 4; ++v) c4[v] += part[((gw * DA_T + wp) * 4 + v) * 32 + lane];
-      const int row = (tc + wp) * 8 + ar;
+      const int ts = tc + wp, mi = ts / T8m;
+      const int row = (ts - mi * T8m) * 8 + ar;
       if (row < n) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int a = 2 * ak + h;  // instance slot
-          if (a < nact) vecp(p, job, rr[a], dst)[row] = make_double2(c4[h], c4[2 + h]);
+          if (a < nact) vecp(p, job, rr[a], dst + mi)[row] = make_double2(c4[h], c4[2 + h]);
         }
       }
     }
@@ -1210,7 +1213,8 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
   }
   unsigned dch = 0;
   // y = M_which x over the active instances of every unit; all = every instance (the first product)
-  auto coop_apply = [&](int which, int src, int dst, bool all) {
+  // nmat > 1: `which` is a stack of nmat matrices sharing x (row tiles stacked), outputs dst, dst + 1, ...
+  auto coop_apply = [&](int which, int src, int dst, bool all, int nmat = 1) {
     T.tick(7);
     load_states(all);
     if (tid == 0) {
@@ -1221,7 +1225,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
           if (sst[u * 8 + l] == 0) uact[u * 8 + na++] = (unsigned char)l;
         unact[u] = na;
         utile[u] = tot;
-        if (na > 0) tot += (4 * nIc * uw(u) + 7) >> 3;
+        if (na > 0) tot += nmat * ((4 * nIc * uw(u) + 7) >> 3);
       }
       utile[nunits] = tot;
     }
@@ -1239,7 +1243,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
       for (int i = 0; i < 8; ++i) rr[i] = i < na ? r0 + uact[u * 8 + i] : r0;
       const double2* Mt = p.dense + s_doff[u / ngroups] + (size_t)which * dense_matrix_elems(n);
       T.tick(12);
-      dense_pass(p, Mt, n, job, rr, na, src, dst, t0, t1, ring, region, dbar, dch, 8);
+      dense_pass(p, Mt, n, job, rr, na, src, dst, t0, t1, ring, region, dbar, dch, 8, nmat);
       T.tick(13);
     }
   };
@@ -1261,11 +1265,10 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
   // ---- b = pre(rhs) (krylov.py:61); s-step start: E b and E^2 b in the same pass, then Arnoldi steps 0-1
   T.tick(8);
   const int VT = p.cap + 3, VA = p.cap + 4;
-  coop_apply(0, VB, VY, true);
-  if (p.sstep) {
-    coop_apply(2, VB, VT, true);
-    coop_apply(3, VB, VA, true);
-  }
+  if (p.sstep)
+    coop_apply(2, VB, VY, true, 3);  // [pre; E pre; E^2 pre] stacked: b, E b, E^2 b -> VY, VT, VA in one pass
+  else
+    coop_apply(0, VB, VY, true);
   T.tick(3);
   gsync();
   if (p.sstep) {

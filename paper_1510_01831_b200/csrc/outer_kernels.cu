@@ -467,6 +467,25 @@ __global__ void k_green_tiles(const double2* src, double2* dst, int w) {
 // dense inner operator (row-major n x n) -> DMMA fragments, chunk-major: [chunk c of kc k-steps][8-row tile t]
 // [k-step kl < kc][32 lanes], lane = 4 r + col holding M[8 t + r][4 (c kc + kl) + col] (zero past n or past the
 // last k-step), so the tiles [t0, t1) of one chunk are one contiguous bulk copy
+// three n x n row-major matrices stacked by row tiles in the dense fragment layout: [chunk][3 T8][kc][32]
+__global__ void k_dense_tiles_stack3(const double2* s0, const double2* s1, const double2* s2, double2* dst, int n,
+                                     int kc) {
+  const int T8 = (n + 7) >> 3, nks = n >> 2, nch = (nks + kc - 1) / kc;
+  const long long total = (long long)nch * 3 * T8 * kc * 32;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(e & 31);
+    long long rest = e >> 5;
+    const int kl = (int)(rest % kc);
+    rest /= kc;
+    const int ts = (int)(rest % (3 * T8)), c = (int)(rest / (3 * T8));
+    const int m = ts / T8, t = ts - m * T8;
+    const double2* src = m == 0 ? s0 : (m == 1 ? s1 : s2);
+    const int row = t * 8 + (lane >> 2), ks = c * kc + kl, k = ks * 4 + (lane & 3);
+    dst[e] = (row < n && ks < nks) ? src[(size_t)row * n + k] : make_double2(0.0, 0.0);
+  }
+}
+
 __global__ void k_dense_tiles(const double2* src, double2* dst, int n, int kc) {
   const int T8 = (n + 7) >> 3, nks = n >> 2, nch = (nks + kc - 1) / kc;
   const long long total = (long long)nch * T8 * kc * 32;

@@ -124,6 +124,8 @@ cudaError_t inner_coop_launch(const InnerParams& p, int njobs, cudaStream_t st);
 int inner_coop_max_units();  // (job, 8-RHS group) units one cooperative inner launch holds
 void inner_tprof_dump(const char* tag);
 __global__ void k_dense_tiles(const double2* src, double2* dst, int n, int kc);
+__global__ void k_dense_tiles_stack3(const double2* s0, const double2* s1, const double2* s2, double2* dst, int n,
+                                     int kc);
 #define DA_KC 8  // k-steps per dense-apply chunk (inner_gmres.cu; the stored fragment layout depends on it)
 // double2 size of one stored dense inner matrix (k_dense_tiles layout)
 __host__ __device__ inline long long dense_matrix_elems(long long n) {

@@ -1781,13 +1781,15 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   // dense inner operators (optional): [L] x [2][n][n], n = 4 nI w
   if (pb->inner_dense && c->Lc > 1) {
     // stored DMMA-fragment tile-major (k_dense_tiles), rows padded to whole 8-row tiles
+    // per layer: [pre | pre o op] and, with the s-step operators, the stack [pre; E pre; E^2 pre] (row tiles of
+    // the three stacked in every k chunk, so one streaming pass serves all three)
     const int cnt = pb->inner_dense_count >= 4 ? 4 : 2;
     c->dense_cnt = cnt;
     long long doff = 0;
     for (auto& li : c->lay) {
       const long long n = 4LL * (c->Lc - 1) * li.w;
       li.dense_off = doff;
-      doff += cnt * dense_matrix_elems(n);
+      doff += (cnt == 4 ? 5 : 2) * dense_matrix_elems(n);
     }
     CK(cudaMalloc(&c->dense_d, sizeof(double2) * (size_t)doff));
     double2* tmp = nullptr;
@@ -1796,9 +1798,14 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
     for (int l = 0; l < c->L; ++l) {
       const long long n = 4LL * (c->Lc - 1) * c->lay[l].w, me = dense_matrix_elems(n);
       CK(cudaMemcpy(tmp, pb->inner_dense[l], sizeof(double2) * (size_t)(cnt * n * n), cudaMemcpyDefault));
-      for (int m = 0; m < cnt; ++m) {
+      for (int m = 0; m < 2; ++m) {
         k_dense_tiles<<<512, 256>>>(tmp + (size_t)m * n * n, c->dense_d + c->lay[l].dense_off + (size_t)m * me,
                                     (int)n, DA_KC);
+        CK(cudaGetLastError());
+      }
+      if (cnt == 4) {
+        k_dense_tiles_stack3<<<512, 256>>>(tmp, tmp + (size_t)2 * n * n, tmp + (size_t)3 * n * n,
+                                           c->dense_d + c->lay[l].dense_off + (size_t)2 * me, (int)n, DA_KC);
         CK(cudaGetLastError());
       }
       CK(cudaDeviceSynchronize());
