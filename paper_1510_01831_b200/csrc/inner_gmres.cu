@@ -1247,21 +1247,23 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
       T.tick(13);
     }
   };
-  // ---- rhs_pol from the Newton tables (sie.py:230-242, negated)
-  for (int u = 0; u < nunits; ++u) {
-    const int job = ujob(u), r0 = ur0(u), ni = uni(u), w = uw(u), n = 4 * nIc * w;
-    for (long long t = (long long)b * blockDim.x + tid; t < (long long)ni * n; t += (long long)G * blockDim.x) {
-      const int l = (int)(t / n), e = (int)(t - (long long)l * n), r = r0 + l;
-      const int seg = e / w, j = e - seg * w;
-      const int half = seg / (2 * nIc);  // 0 down, 1 up
-      const int I = (seg % (2 * nIc)) / 2, s_ = seg & 1;
-      const int c = half == 0 ? I : I + 1;
-      const int idx = half == 0 ? 2 + s_ : s_;
-      const double2 tv = __ldcg(p.tables + ((((size_t)job * p.Lc + c) * 4 + idx) * p.R + r) * p.wmax + j);
-      vecp(p, job, r, VB)[e] = make_double2(-tv.x, -tv.y);
+  // ---- rhs_pol from the Newton tables (sie.py:230-242, negated), unless the pass-0 product wrote it already
+  if (!p.rhs_ready || p.fused) {
+    for (int u = 0; u < nunits; ++u) {
+      const int job = ujob(u), r0 = ur0(u), ni = uni(u), w = uw(u), n = 4 * nIc * w;
+      for (long long t = (long long)b * blockDim.x + tid; t < (long long)ni * n; t += (long long)G * blockDim.x) {
+        const int l = (int)(t / n), e = (int)(t - (long long)l * n), r = r0 + l;
+        const int seg = e / w, j = e - seg * w;
+        const int half = seg / (2 * nIc);  // 0 down, 1 up
+        const int I = (seg % (2 * nIc)) / 2, s_ = seg & 1;
+        const int c = half == 0 ? I : I + 1;
+        const int idx = half == 0 ? 2 + s_ : s_;
+        const double2 tv = __ldcg(p.tables + ((((size_t)job * p.Lc + c) * 4 + idx) * p.R + r) * p.wmax + j);
+        vecp(p, job, r, VB)[e] = make_double2(-tv.x, -tv.y);
+      }
     }
+    gsync();
   }
-  gsync();
   // ---- b = pre(rhs) (krylov.py:61); s-step start: E b and E^2 b in the same pass, then Arnoldi steps 0-1
   T.tick(8);
   const int VT = p.cap + 3, VA = p.cap + 4;

@@ -39,11 +39,11 @@ __global__ void __launch_bounds__(P0_KQ * 32) k_pass0(const int* __restrict__ gr
                                                       const double2* __restrict__ q0, const double2* __restrict__ P,
                                                       double2* __restrict__ tables, double2* __restrict__ smp, int R,
                                                       int Lc, int wx, int wmax, int accum, VecTab tab,
-                                                      const int* rmap, int direct) {
+                                                      const int* rmap, int direct, RhsOut ro) {
   __shared__ double part[(P0_KQ - 1) * 2 * 4 * 32];
   pass0_item(grp, ljobs, jobs, cells, layers, q0, P, tables, smp, R, Lc, wx, wmax, blockIdx.x / Lc,
              blockIdx.x % Lc, blockIdx.y, blockIdx.z, threadIdx.x >> 5, part, 1, accum, direct ? &tab : nullptr,
-             rmap);
+             rmap, ro.base ? &ro : nullptr);
 }
 
 __global__ void __launch_bounds__(GS_WARPS * 32) k_green_samples(
@@ -547,12 +547,13 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
 cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
                          const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,
                          int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st,
-                         int accum, const VecTab* tab, const int* rmap) {
+                         int accum, const VecTab* tab, const int* rmap, const RhsOut* rhs_out) {
   if (ngroups == 0 || R == 0) return cudaSuccess;
   const VecTab tabv = tab ? *tab : VecTab{};
   const int mp = (4 * wmax + 4 * kmax + 7) / 8 * 8;
   const int gz = (max_jobs_per_layer * R + P0_COLS - 1) / P0_COLS;
+  const RhsOut ro = rhs_out ? *rhs_out : RhsOut{nullptr, 0, 0};
   k_pass0<<<dim3(ngroups * Lc, mp / 8, gz), P0_KQ * 32, 0, st>>>(grp, ljobs, jobs, cells, layers, q0, P, tables, smp,
-                                                                 R, Lc, wx, wmax, accum, tabv, rmap, tab != nullptr);
+                                                                 R, Lc, wx, wmax, accum, tabv, rmap, tab != nullptr, ro);
   return cudaGetLastError();
 }

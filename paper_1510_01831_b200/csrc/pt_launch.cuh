@@ -101,6 +101,7 @@ struct InnerParams {
   int tring;              // Green-tile ring slots of the item-program path (inner_tring)
   int coop_sms;           // SMs (CTAs) of the cooperative inner kernels; 0 = all
   int sstep;              // dense matrices 2, 3 = E pre, E^2 pre: s-step start of the inner GMRES (n <= 1024)
+  int rhs_ready;          // the stage's producer (pass-0 product) wrote rhs_pol into the VB scratch vectors
   int arn_fast;           // Arnoldi steps of small instances with the basis prefetched (PT_ARN_SLOW = 0)
 };
 
@@ -133,10 +134,19 @@ __host__ __device__ inline long long dense_matrix_elems(long long n) {
   return nch * T8 * DA_KC * 32;
 }
 // first layer-solve pass (no volume source) as a dense product with the offline pass-0 operators
+// Optional second output of the pass-0 product: the inner GMRES rhs_pol (sie.py:230-242, negated Newton rows
+// n, n+1 of cell I and 0, 1 of cell I+1) written straight into each instance's inner scratch vector, so the
+// inner kernel needs no gather pass: element e of instance (job, q) at base + (job R + q) stride + off + e.
+struct RhsOut {
+  double2* base;
+  long long stride, off;
+};
+
 cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
                          const LayerInfo* layers, const double2* q0, const double2* P, double2* tables, double2* smp,
                          int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st,
-                         int accum = 0, const VecTab* tab = nullptr, const int* rmap = nullptr);  // PT_INNER_TPROF: print and reset CTA 0's segment clocks
+                         int accum = 0, const VecTab* tab = nullptr, const int* rmap = nullptr,
+                         const RhsOut* rhs_out = nullptr);  // PT_INNER_TPROF: print and reset CTA 0's segment clocks
 // smp += trace-source response (sampled Green rows) for every (job, cell, output row, RHS)
 cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                  const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx,

@@ -844,12 +844,18 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   kp.s0 = gpath ? 1 : 0;
   if (c->Lc > 1) {
     kp.pass = 0;
+    // pass-0 products also write the inner rhs (rhs_pol) into the inner scratch: the inner kernel skips its
+    // gather pass and one grid barrier (dense cooperative path; PT_NO_RHS_OUT keeps the gather)
+    static const bool no_rhs_out = std::getenv("PT_NO_RHS_OUT") != nullptr;
+    const RhsOut ro{c->iscr, c->iscr_stride, (long long)(c->inner_cap + 1) * c->inmax};
+    const bool rhs_out = !no_rhs_out && c->dense_d && !c->lu_d && (rpath || qpath);
     if (rpath) {
       LaunchScope ls(c, 4);
       CK(cudaMemcpyAsync(c->tables, c->tables_f, sizeof(double2) * (size_t)J * c->Lc * 4 * Ract * c->wmax,
                          cudaMemcpyDeviceToDevice, c->st));
       CK(pass0_launch(S.grp_d, (int)S.lgrp.size(), S.ljobs_d, S.jobs_d, c->cel_d, c->lay_d, c->q0_d, c->P, c->tables,
-                      c->smp, Ract, c->Lc, c->wx, c->wmax, c->wzcmax, 1, c->st, 1));
+                      c->smp, Ract, c->Lc, c->wx, c->wmax, c->wzcmax, 1, c->st, 1, nullptr, nullptr,
+                      rhs_out ? &ro : nullptr));
     } else if (qpath) {  // first pass as one dense product with the offline pass-0 operators (no volume source)
       LaunchScope ls(c, 4);
       int maxj = 0;
@@ -859,13 +865,14 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
       }
       CK(pass0_launch(S.grp_d, (int)S.lgrp.size(), S.ljobs_d, S.jobs_d, c->cel_d, c->lay_d, c->q0_d, c->P, c->tables,
                       c->smp, Ract, c->Lc, c->wx, c->wmax, c->wzcmax, maxj, c->st, 0, direct_b ? &tab : nullptr,
-                      c->rmap_d));
+                      c->rmap_d, rhs_out ? &ro : nullptr));
     } else {
       LaunchScope ls(c, 0);
       CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
       c->k1_bytes += T->bytes;
     }
     InnerParams ip = inner_params(c, S, Ract, io);
+    ip.rhs_ready = rhs_out;
     if (c->lu_d) {  // direct inner backend: one dense product per layer solve (nested.py:156-254)
       LaunchScope ls(c, 1);
       const int mmax = 2 * (c->Lc - 1) * c->wmax;

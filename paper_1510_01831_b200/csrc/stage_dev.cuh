@@ -61,7 +61,8 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
                                            const double2* __restrict__ P, double2* __restrict__ tables,
                                            double2* __restrict__ smp, int R, int Lc, int wx, int wmax, int g, int c,
                                            int tile, int z, int wq, double* part, int barid, int accum = 0,
-                                           const VecTab* tabd = nullptr, const int* rmap = nullptr) {
+                                           const VecTab* tabd = nullptr, const int* rmap = nullptr,
+                                           const RhsOut* rhs_out = nullptr) {
   const int layer = grp[3 * g], jb0 = grp[3 * g + 1], nj = grp[3 * g + 2];
   const CellInfo& ci = cells[layer * Lc + c];
   const LayerInfo& lay = layers[layer];
@@ -169,7 +170,17 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
       if (m < 4 * w) {
         const int idx = m / w, j = m - (m / w) * w;
         double2* tp = tables + ((((size_t)jid * Lc + c) * 4 + idx) * R + q) * wmax + j;
-        *tp = accum ? cadd(*tp, v) : v;
+        const double2 tv = accum ? cadd(*tp, v) : v;
+        *tp = tv;
+        if (rhs_out) {  // rows n, n+1 of cell c < nI feed down[c]; rows 0, 1 of cell c >= 1 feed up[c - 1]
+          const int nIc = Lc - 1;
+          int seg = -1;
+          if (idx >= 2 && c < nIc) seg = 2 * c + (idx - 2);
+          else if (idx < 2 && c >= 1) seg = 2 * nIc + 2 * (c - 1) + idx;
+          if (seg >= 0)
+            rhs_out->base[((size_t)jid * R + q) * rhs_out->stride + rhs_out->off + (size_t)seg * w + j] =
+                make_double2(-tv.x, -tv.y);
+        }
       } else {
         const int mm = m - 4 * w, kk = mm >> 2, oi = mm & 3;
         const OJob& jb = jobs[jid];

@@ -48,6 +48,8 @@ SWITCHES = {
     "cluster-dense": {"PT_NO_COOP": "1"},
     "cluster-items": {"PT_NO_DENSE": "1", "PT_NO_COOP": "1"},
     "separate-combine": {"PT_NO_FUSE_COMB": "1"},
+    "inner-gather": {"PT_NO_RHS_OUT": "1"},
+    "no-sstep": {"PT_NO_SSTEP": "1"},
     "fused-glue": {"PT_FUSE_GLUE": "1"},
     "fused-stage": {"PT_FUSE": "1"},
     "recon-k1": {"PT_NO_REUSE": "1"},
