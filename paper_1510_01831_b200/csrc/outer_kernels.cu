@@ -121,19 +121,35 @@ __global__ void __launch_bounds__(GS2_KQ * GS2_TPC * 32) k_green_samples2(
 #pragma unroll
   for (int g = 0; g < GS2_NG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0;
   if (tile * 8 < nrows) {
+    // (slot, k-step within the slot) advanced incrementally (no divisions in the unrolled loops)
+    int sl_c = s_lo + kb / kps, r_c = kb - (kb / kps) * kps;
     for (int ks0 = kb; ks0 < ke; ks0 += 8) {
       double2 av[8];
+      int sls[8], js[8];
+      {
+        int sl = sl_c, r = r_c;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          sls[u] = sl;
+          js[u] = r * 4 + ak;
+          if (++r == kps) {
+            r = 0;
+            ++sl;
+          }
+        }
+        sl_c = sl;
+        r_c = r;
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int ks = ks0 + u;
-        const int sl = s_lo + ks / kps, j = (ks - (ks / kps) * kps) * 4 + ak;
-        av[u] = (ks < ke && mok && j < w) ? __ldg(grow + sl * w + j) : make_double2(0.0, 0.0);
+        const int sl = sls[u], j = js[u];
+        av[u] = (ks0 + u < ke && mok && j < w) ? __ldg(grow + sl * w + j) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int ks = ks0 + u;
         if (ks >= ke) break;
-        const int sl = s_lo + ks / kps, j = (ks - (ks / kps) * kps) * 4 + ak;
+        const int sl = sls[u], j = js[u];
         const double2* tb = trs + ((size_t)sl * w4 + j) * NR + ar;
 #pragma unroll
         for (int g = 0; g < GS2_NG; ++g) {

@@ -115,19 +115,27 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
   }
   const int kps = nk4 >> 2, nks = nsl * kps;  // k-steps per slot / over the used slots
   const int kb = wp * nks / P0_KQ, ke = (wp + 1) * nks / P0_KQ;
+  // (used-slot index, k-step within the slot) of the next k-step, advanced incrementally (no divisions)
+  int si_c = kps > 0 ? kb / kps : 0, r_c = kb - si_c * kps;
   for (int ks0 = kb; ks0 < ke; ks0 += 8) {
     double2 av[8], bv[8][2];
+    int si = si_c, r = r_c;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int ks = ks0 + u;
-      const bool kin = ks < ke;
-      const int si = kin ? ks / kps : 0, sl = slist >> (2 * si) & 3;
-      const int kk = (ks - si * kps) * 4;  // column within the slot block (+ ak)
-      av[u] = kin ? __ldg(arow + (sl * kps + (ks - si * kps)) * 4) : make_double2(0.0, 0.0);
+      const bool kin = ks0 + u < ke;
+      const int sl = slist >> (2 * (si & 3)) & 3;
+      const int kk = r * 4;  // column within the slot block (+ ak)
+      av[u] = kin ? __ldg(arow + (sl * kps + r) * 4) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int gq = 0; gq < 2; ++gq)
         bv[u][gq] = (kin && bok[gq] && kk + ak < nk) ? bload(gq, sl, kk) : make_double2(0.0, 0.0);
+      if (++r == kps) {
+        r = 0;
+        ++si;
+      }
     }
+    si_c = si;
+    r_c = r;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
 #pragma unroll
