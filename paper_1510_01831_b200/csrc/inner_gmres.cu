@@ -893,6 +893,115 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
   __syncthreads();
 }
 
+// instance_sstep for any n: the same quantities, every pass recomputed elementwise from m0, m1, m2 (read from
+// L2) instead of held in registers.  Element e belongs to thread e % IN_THREADS; each reduction sums a thread's
+// elements in increasing e, then block_sum in warp order (deterministic).
+__device__ void instance_sstep_loop(const InnerParams& p, int job, int r, int n, int VY, int VT, int VA,
+                                    double* dred) {
+  const int tid = threadIdx.x;
+  const double2* M0 = vecp(p, job, r, VY);
+  const double2* M1 = vecp(p, job, r, VT);
+  const double2* M2 = vecp(p, job, r, VA);
+  __shared__ double2 s_col[4];
+  __shared__ double2 s_rot[7];
+  __shared__ int s_st;
+  double ss = 0.0;
+  for (int e = tid; e < n; e += IN_THREADS) {
+    const double2 a = ld_cg(M0 + e);
+    ss += a.x * a.x + a.y * a.y;
+  }
+  const double b0 = sqrt(block_sum(ss, dred));
+  if (tid == 0) {
+    double2* g = p.hess + (size_t)(job * p.R + r) * p.hstride + ((size_t)p.cap + 1) * p.cap;
+    g[0] = make_double2(b0, 0.0);
+    p.beta0[job * p.R + r] = b0;
+    p.state[job * p.R + r] = b0 == 0.0 ? 1 : 0;
+    p.iters[job * p.R + r] = b0 == 0.0 ? 0 : -1;
+  }
+  if (b0 == 0.0) {
+    __syncthreads();
+    return;
+  }
+  double2* V0 = vecp(p, job, r, 0);
+  double2* V1 = vecp(p, job, r, 1);
+  double2* V2 = vecp(p, job, r, 2);
+  auto sc = [](double2 a, double d) { return make_double2(a.x / d, a.y / d); };
+  // ---- j = 0: V_0 = m0 / b0, w = E V_0 + V_0
+  double sr = 0.0, si = 0.0;
+  for (int e = tid; e < n; e += IN_THREADS) {
+    const double2 v0 = sc(ld_cg(M0 + e), b0);
+    V0[e] = v0;
+    const double2 c = cconjmul(v0, cadd(sc(ld_cg(M1 + e), b0), v0));
+    sr += c.x;
+    si += c.y;
+  }
+  const double2 h00 = block_sum2(sr, si, dred);
+  ss = 0.0;
+  for (int e = tid; e < n; e += IN_THREADS) {
+    const double2 v0 = sc(ld_cg(M0 + e), b0);
+    const double2 w = csub(cadd(sc(ld_cg(M1 + e), b0), v0), cmul(h00, v0));
+    ss += w.x * w.x + w.y * w.y;
+  }
+  const double hn0 = sqrt(block_sum(ss, dred));
+  if (tid == 0) {
+    s_rot[4] = make_double2(b0, 0.0);
+    s_col[0] = h00;
+    s_col[1] = make_double2(hn0, 0.0);
+    s_st = givens_col(p, job, r, 0, s_col, hn0, s_rot, s_rot + 2, s_rot + 4, b0);
+  }
+  __syncthreads();
+  if (s_st != 0) return;
+  // ---- j = 1: V_1 = w / hn0, E V_1 = (E^2 V_0 + E V_0 - h00 E V_0) / hn0, w = E V_1 + V_1
+  auto v1_of = [&](int e, double2& v0, double2& v1, double2& w1) {
+    v0 = sc(ld_cg(M0 + e), b0);
+    const double2 e0 = sc(ld_cg(M1 + e), b0);
+    v1 = sc(csub(cadd(e0, v0), cmul(h00, v0)), hn0);
+    const double2 ev = csub(cadd(sc(ld_cg(M2 + e), b0), e0), cmul(h00, e0));
+    w1 = cadd(sc(ev, hn0), v1);
+  };
+  sr = si = 0.0;
+  for (int e = tid; e < n; e += IN_THREADS) {
+    double2 v0, v1, w1;
+    v1_of(e, v0, v1, w1);
+    V1[e] = v1;
+    const double2 c = cconjmul(v0, w1);
+    sr += c.x;
+    si += c.y;
+  }
+  const double2 h01 = block_sum2(sr, si, dred);
+  sr = si = 0.0;
+  for (int e = tid; e < n; e += IN_THREADS) {
+    double2 v0, v1, w1;
+    v1_of(e, v0, v1, w1);
+    const double2 c = cconjmul(v1, csub(w1, cmul(h01, v0)));
+    sr += c.x;
+    si += c.y;
+  }
+  const double2 h11 = block_sum2(sr, si, dred);
+  ss = 0.0;
+  for (int e = tid; e < n; e += IN_THREADS) {
+    double2 v0, v1, w1;
+    v1_of(e, v0, v1, w1);
+    const double2 w = csub(csub(w1, cmul(h01, v0)), cmul(h11, v1));
+    ss += w.x * w.x + w.y * w.y;
+  }
+  const double hn1 = sqrt(block_sum(ss, dred));
+  if (tid == 0) {
+    s_col[0] = h01;
+    s_col[1] = h11;
+    s_col[2] = make_double2(hn1, 0.0);
+    s_st = givens_col(p, job, r, 1, s_col, hn1, s_rot, s_rot + 2, s_rot + 4, b0);
+  }
+  __syncthreads();
+  if (s_st != 0) return;
+  for (int e = tid; e < n; e += IN_THREADS) {
+    double2 v0, v1, w1;
+    v1_of(e, v0, v1, w1);
+    V2[e] = sc(csub(csub(w1, cmul(h01, v0)), cmul(h11, v1)), hn1);
+  }
+  __syncthreads();
+}
+
 // b = Y = pre(rhs) and W = V_1 = pre(op(b)) (the product taken on the unnormalized b): beta0 = ||b||,
 // V_0 = b / beta0, then the Arnoldi step j = 0 on W / beta0 (= pre(op(V_0)) up to rounding)
 __device__ void instance_arnoldi0(const InnerParams& p, int job, int r, int n, int VY, double* dred) {
@@ -1276,7 +1385,12 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
   if (p.sstep) {
     for (int t = b; t < nunits * 8; t += G) {
       const int u = t >> 3, l = t & 7;
-      if (l < uni(u)) instance_sstep(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), VY, VT, VA, dred);
+      if (l >= uni(u)) continue;
+      const int n_ = 4 * nIc * uw(u);
+      if (n_ <= 4 * IN_THREADS)
+        instance_sstep(p, ujob(u), ur0(u) + l, n_, VY, VT, VA, dred);
+      else
+        instance_sstep_loop(p, ujob(u), ur0(u) + l, n_, VY, VT, VA, dred);
     }
     T.tick(6);
     gsync();

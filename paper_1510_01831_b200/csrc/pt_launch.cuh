@@ -100,7 +100,7 @@ struct InnerParams {
   int mg;                 // 8-row Green tiles per work group (inner_mg(wmax))
   int tring;              // Green-tile ring slots of the item-program path (inner_tring)
   int coop_sms;           // SMs (CTAs) of the cooperative inner kernels; 0 = all
-  int sstep;              // dense matrices 2, 3 = E pre, E^2 pre: s-step start of the inner GMRES (n <= 1024)
+  int sstep;              // dense stack [pre; E pre; E^2 pre] present: s-step start of the inner GMRES
   int rhs_ready;          // the stage's producer (pass-0 product) wrote rhs_pol into the VB scratch vectors
   int arn_fast;           // Arnoldi steps of small instances with the basis prefetched (PT_ARN_SLOW = 0)
 };

@@ -75,7 +75,6 @@ int upload(T** dst, const T* src, size_t n) {
 }  // namespace
 
 #define PT_RMAP_SLOTS 32
-#define IN_THREADS_HOST 256  // inner kernels' block size (IN_THREADS in inner_gmres.cu)
 struct pt_ctx {
   int dev = 0;
   cudaStream_t st = nullptr;
@@ -726,7 +725,7 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   ip.arn_fast = !arn_slow;
   ip.coop_sms = c->coop_sms;
   static const bool no_sstep = std::getenv("PT_NO_SSTEP") != nullptr;
-  ip.sstep = !no_sstep && c->dense_cnt >= 4 && 4LL * (c->Lc - 1) * c->wmax <= 4 * IN_THREADS_HOST && c->dense_d;
+  ip.sstep = !no_sstep && c->dense_cnt >= 4 && c->dense_d;
   if (ip.tring < 4 * ip.mg) ip.mg = 1;  // a group's (slot, row tile) tiles must fit in the ring together
   return ip;
 }
