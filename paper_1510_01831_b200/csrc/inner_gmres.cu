@@ -284,8 +284,9 @@ __device__ void run_program(const InnerParams& p, int job, int layer, int w, int
 // One streaming pass over row tiles [t0, t1) of M for the instances rr[0..nact): see dense_apply.
 // src < 0: x is rhs_pol gathered from the Newton tables (negated) instead of a scratch vector.
 // ring/region: the shared-memory ring; dbar: DA_NS full + DA_NS empty barriers; the partial tiles reuse the
-// ring.  A ring slot holds SC stored chunks (SC = DA_T / nt, at most scmax) of the pass's tiles plus the
-// instances' x entries for those k-steps, so passes over few tiles still move large slots.
+// ring.  A ring slot (fixed capacity dense_slot_bytes(scmax)) holds as many stored chunks (<= 16) of the pass's
+// tiles as fit next to the instances' x entries for those k-steps, so passes over few tiles or few instances
+// still move large slots.
 __device__ __forceinline__ uint32_t dense_slot_bytes(int scmax) {
   return (uint32_t)DA_T * DA_KC * 512u + 8u * (uint32_t)(scmax * DA_KC * 4 + 4) * 16u;
 }
@@ -297,16 +298,23 @@ __device__ void dense_pass(const InnerParams& p, const double2* __restrict__ Mt,
   // nmat stacked matrices (row tiles of matrix m at [m T8m, (m+1) T8m)) share the pass's x: T8 = stored row
   // tiles per chunk, the output of stacked tile t goes to vector dst + t / T8m, row (t % T8m) * 8 + ar
   const int T8m = (n + 7) >> 3, T8 = nmat * T8m, nks = n >> 2;
-  const int XST = scmax * DA_KC * 4 + 4;                            // padded x row (double2) per instance
-  const uint32_t abytes = (uint32_t)DA_T * DA_KC * 512u;            // A part of a slot
-  const uint32_t slot_bytes = dense_slot_bytes(scmax);
+  const uint32_t slot_bytes = dense_slot_bytes(scmax);  // fixed slot capacity (ring phases)
   const int ns = (int)min((size_t)DA_NS, region / slot_bytes);
   uint64_t* full = dbar;
   uint64_t* empty = dbar + DA_NS;
   const int nchs = (nks + DA_KC - 1) / DA_KC;  // stored chunks
   for (int tc = t0; tc < t1; tc += DA_T) {
     const int nt = min(DA_T, t1 - tc);
-    const int sc = max(1, min(scmax, DA_T / nt));
+    // stored chunks per slot: as many as the slot holds next to the instances' x rows (few tiles or few
+    // instances -> more k per slot, more bytes in flight)
+    int sc = 1;
+    for (int cand = 16; cand > 1; --cand)
+      if ((uint32_t)(cand * nt * DA_KC * 512 + nact * (cand * DA_KC * 4 + 4) * 16) <= slot_bytes) {
+        sc = cand;
+        break;
+      }
+    const int XST = sc * DA_KC * 4 + 4;                   // padded x row (double2) per instance
+    const uint32_t abytes = (uint32_t)(sc * nt * DA_KC * 512);  // A part of this pass's slots
     const int kslot = sc * DA_KC;                  // k-steps per slot
     const int nsl = (nks + kslot - 1) / kslot;     // slots of this pass
     const unsigned base = dch;  // global index of this pass's slot 0
