@@ -803,6 +803,8 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
   for (int t = 0; t < SE; ++t) ss += m0[t].x * m0[t].x + m0[t].y * m0[t].y;
   ss = block_sum(ss, dred);
   const double b0 = sqrt(ss);
+  const bool tp_on = p.tprof && tid == 0 && blockIdx.x == 0;
+  long long tp0 = tp_on ? clock64() : 0;
   if (tid == 0) {
     double2* g = p.hess + (size_t)(job * p.R + r) * p.hstride + ((size_t)p.cap + 1) * p.cap;
     g[0] = make_double2(b0, 0.0);
@@ -815,14 +817,15 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
     return;
   }
   double2* V0 = vecp(p, job, r, 0);
-  // ---- j = 0: V_0 = b / beta0, w = A V_0 = E b / beta0 + V_0
+  // ---- j = 0: V_0 = b / beta0, w = A V_0 = E b / beta0 + V_0 (scalings as products with the reciprocal)
+  const double ib0 = 1.0 / b0;
 #pragma unroll
   for (int t = 0; t < SE; ++t) {
     const int e = tid + t * IN_THREADS;
-    const double2 v0 = make_double2(m0[t].x / b0, m0[t].y / b0);
+    const double2 v0 = make_double2(m0[t].x * ib0, m0[t].y * ib0);
     m0[t] = v0;                                             // m0 holds V_0 from here
-    m1[t] = make_double2(m1[t].x / b0, m1[t].y / b0);       // E V_0
-    m2[t] = make_double2(m2[t].x / b0, m2[t].y / b0);       // E^2 V_0
+    m1[t] = make_double2(m1[t].x * ib0, m1[t].y * ib0);     // E V_0
+    m2[t] = make_double2(m2[t].x * ib0, m2[t].y * ib0);     // E^2 V_0
     if (e < n) V0[e] = v0;
     w[t] = cadd(m1[t], v0);
   }
@@ -849,16 +852,22 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
     s_st = givens_col(p, job, r, 0, s_col, hn0, s_rot, s_rot + 2, s_rot + 4, b0);
   }
   __syncthreads();
+  if (tp_on) {
+    const long long t1 = clock64();
+    atomicAdd((unsigned long long*)&g_in_t[0], (unsigned long long)(t1 - tp0));
+    tp0 = t1;
+  }
   if (s_st != 0) return;
   // ---- j = 1: V_1 = w / hn0, E V_1 = (E^2 V_0 + E V_0 - h00 E V_0) / hn0, w = E V_1 + V_1
   double2* V1 = vecp(p, job, r, 1);
+  const double ihn0 = 1.0 / hn0;
 #pragma unroll
   for (int t = 0; t < SE; ++t) {
     const int e = tid + t * IN_THREADS;
-    v1[t] = make_double2(w[t].x / hn0, w[t].y / hn0);
+    v1[t] = make_double2(w[t].x * ihn0, w[t].y * ihn0);
     if (e < n) V1[e] = v1[t];
     const double2 ev = csub(cadd(m2[t], m1[t]), cmul(h00, m1[t]));
-    w[t] = cadd(make_double2(ev.x / hn0, ev.y / hn0), v1[t]);
+    w[t] = cadd(make_double2(ev.x * ihn0, ev.y * ihn0), v1[t]);
   }
   sr = si = 0.0;
 #pragma unroll
@@ -891,12 +900,14 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
     s_st = givens_col(p, job, r, 1, s_col, hn1, s_rot, s_rot + 2, s_rot + 4, b0);
   }
   __syncthreads();
+  if (tp_on) atomicAdd((unsigned long long*)&g_in_t[1], (unsigned long long)(clock64() - tp0));
   if (s_st != 0) return;
   double2* V2 = vecp(p, job, r, 2);  // V_2 = w / hn1: the regular loop continues at j = 2
+  const double ihn1 = 1.0 / hn1;
 #pragma unroll
   for (int t = 0; t < SE; ++t) {
     const int e = tid + t * IN_THREADS;
-    if (e < n) V2[e] = make_double2(w[t].x / hn1, w[t].y / hn1);
+    if (e < n) V2[e] = make_double2(w[t].x * ihn1, w[t].y * ihn1);
   }
   __syncthreads();
 }
@@ -933,21 +944,22 @@ __device__ void instance_sstep_loop(const InnerParams& p, int job, int r, int n,
   double2* V0 = vecp(p, job, r, 0);
   double2* V1 = vecp(p, job, r, 1);
   double2* V2 = vecp(p, job, r, 2);
-  auto sc = [](double2 a, double d) { return make_double2(a.x / d, a.y / d); };
+  const double ib0 = 1.0 / b0;
+  auto sc = [](double2 a, double d) { return make_double2(a.x * d, a.y * d); };  // d: a reciprocal
   // ---- j = 0: V_0 = m0 / b0, w = E V_0 + V_0
   double sr = 0.0, si = 0.0;
   for (int e = tid; e < n; e += IN_THREADS) {
-    const double2 v0 = sc(ld_cg(M0 + e), b0);
+    const double2 v0 = sc(ld_cg(M0 + e), ib0);
     V0[e] = v0;
-    const double2 c = cconjmul(v0, cadd(sc(ld_cg(M1 + e), b0), v0));
+    const double2 c = cconjmul(v0, cadd(sc(ld_cg(M1 + e), ib0), v0));
     sr += c.x;
     si += c.y;
   }
   const double2 h00 = block_sum2(sr, si, dred);
   ss = 0.0;
   for (int e = tid; e < n; e += IN_THREADS) {
-    const double2 v0 = sc(ld_cg(M0 + e), b0);
-    const double2 w = csub(cadd(sc(ld_cg(M1 + e), b0), v0), cmul(h00, v0));
+    const double2 v0 = sc(ld_cg(M0 + e), ib0);
+    const double2 w = csub(cadd(sc(ld_cg(M1 + e), ib0), v0), cmul(h00, v0));
     ss += w.x * w.x + w.y * w.y;
   }
   const double hn0 = sqrt(block_sum(ss, dred));
@@ -960,12 +972,13 @@ __device__ void instance_sstep_loop(const InnerParams& p, int job, int r, int n,
   __syncthreads();
   if (s_st != 0) return;
   // ---- j = 1: V_1 = w / hn0, E V_1 = (E^2 V_0 + E V_0 - h00 E V_0) / hn0, w = E V_1 + V_1
+  const double ihn0 = 1.0 / hn0;
   auto v1_of = [&](int e, double2& v0, double2& v1, double2& w1) {
-    v0 = sc(ld_cg(M0 + e), b0);
-    const double2 e0 = sc(ld_cg(M1 + e), b0);
-    v1 = sc(csub(cadd(e0, v0), cmul(h00, v0)), hn0);
-    const double2 ev = csub(cadd(sc(ld_cg(M2 + e), b0), e0), cmul(h00, e0));
-    w1 = cadd(sc(ev, hn0), v1);
+    v0 = sc(ld_cg(M0 + e), ib0);
+    const double2 e0 = sc(ld_cg(M1 + e), ib0);
+    v1 = sc(csub(cadd(e0, v0), cmul(h00, v0)), ihn0);
+    const double2 ev = csub(cadd(sc(ld_cg(M2 + e), ib0), e0), cmul(h00, e0));
+    w1 = cadd(sc(ev, ihn0), v1);
   };
   sr = si = 0.0;
   for (int e = tid; e < n; e += IN_THREADS) {
@@ -1002,10 +1015,11 @@ __device__ void instance_sstep_loop(const InnerParams& p, int job, int r, int n,
   }
   __syncthreads();
   if (s_st != 0) return;
+  const double ihn1 = 1.0 / hn1;
   for (int e = tid; e < n; e += IN_THREADS) {
     double2 v0, v1, w1;
     v1_of(e, v0, v1, w1);
-    V2[e] = sc(csub(csub(w1, cmul(h01, v0)), cmul(h11, v1)), hn1);
+    V2[e] = sc(csub(csub(w1, cmul(h01, v0)), cmul(h11, v1)), ihn1);
   }
   __syncthreads();
 }
