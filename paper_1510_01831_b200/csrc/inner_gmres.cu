@@ -457,11 +457,13 @@ __device__ void instance_init(const InnerParams& p, int job, int r, int n, int V
   ss = block_sum(ss, dred);
   const double b0 = sqrt(ss);
   double2* V0 = vecp(p, job, r, 0);
-  if (b0 != 0.0)
+  if (b0 != 0.0) {
+    const double ib0 = 1.0 / b0;
     for (int e = tid; e < n; e += blockDim.x) {
       const double2 y = ld_cg(Y + e);
-      V0[e] = make_double2(y.x / b0, y.y / b0);
+      V0[e] = make_double2(y.x * ib0, y.y * ib0);
     }
+  }
   if (tid == 0) {
     double2* g = p.hess + (size_t)(job * p.R + r) * p.hstride + hld * p.cap;
     g[0] = make_double2(b0, 0.0);
@@ -702,16 +704,17 @@ __device__ void instance_arnoldi(const InnerParams& p, int job, int r, int j, in
     if (st != 0) p.iters[job * p.R + r] = st == 1 ? j + 1 : -1;
   }
   __syncthreads();
+  const double ihn = 1.0 / hn;  // scalings as products with the reciprocal (FP64 division is slow)
   if (fast) {  // V_{j+1} = w / hn from registers (the orthogonalized w itself once the instance stops)
 #pragma unroll
     for (int t = 0; t < FE; ++t) {
       const int e = tid + t * IN_THREADS;
-      if (e < n) W[e] = s_st == 0 ? make_double2(fw[t].x / hn, fw[t].y / hn) : fw[t];
+      if (e < n) W[e] = s_st == 0 ? make_double2(fw[t].x * ihn, fw[t].y * ihn) : fw[t];
     }
   } else if (s_st == 0) {  // V_{j+1} = w / hn (krylov.py:125)
     for (int e = tid; e < n; e += blockDim.x) {
       const double2 x = W[e];
-      W[e] = make_double2(x.x / hn, x.y / hn);
+      W[e] = make_double2(x.x * ihn, x.y * ihn);
     }
   }
   __syncthreads();
@@ -773,6 +776,61 @@ __device__ int givens_col(const InnerParams& p, int job, int r, int j, double2* 
   return st;
 }
 
+// instance_final for an instance that stopped inside the register s-step (k = 1 or 2): the basis vectors are
+// still in registers (v0, v1), the triangle and g on thread 0's shared copies.  Same back substitution, x = V y
+// order and accounting as instance_final; the halves of x meet through the shared scratch xs (>= n double2).
+// Marks the instance finalized (state 3: stopped, traces written).
+template <int SE>
+__device__ void sstep_final(const InnerParams& p, int job, int r, int n, int k, const double2 (&v0)[SE],
+                            const double2 (&v1)[SE], const double2* rtri, const double2* gk, double2* xs) {
+  const int tid = threadIdx.x, nIc = p.Lc - 1, w = n / (4 * nIc);
+  __shared__ double2 s_y[2];
+  if (tid == 0) {  // rtri = (R00, R01, R11)
+    double2 y[2] = {czero(), czero()};
+    for (int i = k - 1; i >= 0; --i) {
+      double2 sacc = czero();
+      if (i == 0 && k == 2) cfma(sacc, rtri[1], y[1]);
+      const double2 num = csub(gk[i], sacc);
+      const double2 den = i == 0 ? rtri[0] : rtri[2];
+      const double dd = den.x * den.x + den.y * den.y;
+      y[i] = make_double2((num.x * den.x + num.y * den.y) / dd, (num.y * den.x - num.x * den.y) / dd);
+    }
+    s_y[0] = y[0];
+    s_y[1] = y[1];
+  }
+  __syncthreads();
+  const double2 y0 = s_y[0], y1 = s_y[1];
+#pragma unroll
+  for (int t = 0; t < SE; ++t) {
+    const int e = tid + t * IN_THREADS;
+    if (e < n) {
+      double2 x = czero();
+      cfma(x, v0[t], y0);
+      if (k == 2) cfma(x, v1[t], y1);
+      xs[e] = x;
+    }
+  }
+  __syncthreads();
+  const int half = n / 2;
+  double2* out = p.tr + (size_t)(job * p.R + r) * nIc * 2 * p.wmax;
+  for (int e = tid; e < half; e += IN_THREADS) {
+    const int seg = e / w, jj = e - seg * w;
+    out[(size_t)seg * p.wmax + jj] = cadd(xs[e], xs[e + half]);
+  }
+  if (tid == 0) {  // TouchCounter.total equivalent (nested.py:54-73), as instance_final
+    atomicAdd(&p.hist[min(k, PT_HIST - 1)], 1);
+    atomicAdd(&p.counters[0], (unsigned long long)k);
+    const unsigned long long t =
+        ((unsigned long long)(k + 1) * p.pre_blocks + (unsigned long long)k * p.op_blocks) * w * w;
+    atomicAdd(&p.counters[1], t);
+    atomicAdd(&p.counters[2], 1ULL);
+    p.state[job * p.R + r] = 3;
+  }
+  // xs is the dense ring: order these generic writes before later bulk copies into it
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+}
+
 // s-step start of the inner GMRES (krylov.py:61-127, steps j = 0 and 1) for one instance, from m0 = b = pre(rhs)
 // (VY), m1 = E b (VT) and m2 = E^2 b (VA), E = pre(op(.)) - I, all three produced by ONE dense pass: A V = E V + V
 // gives the two products of the Arnoldi steps without waiting for the GPU in between.  The MGS, norms, Givens
@@ -780,7 +838,7 @@ __device__ int givens_col(const InnerParams& p, int job, int r, int j, double2* 
 // Leaves V_0..V_2 (as far as the instance runs), H columns 0-1 and the Givens state as instance_arnoldi would.
 // n <= SE * IN_THREADS.
 __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int VY, int VT, int VA,
-                                            double* dred) {
+                               double* dred, double2* xs) {
   constexpr int SE = 4;
   const int tid = threadIdx.x;
   const double2* M0 = vecp(p, job, r, VY);
@@ -795,8 +853,8 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
     m2[t] = e < n ? ld_cg(M2 + e) : czero();
   }
   __shared__ double2 s_col[4];
+  __shared__ double2 s_tri[3];  // R00, R01, R11 of the triangularized Hessenberg (thread 0)
   __shared__ int s_st;
-  __shared__ double s_hn;
   // beta0 = ||b|| (instance_init)
   double ss = 0.0;
 #pragma unroll
@@ -850,6 +908,7 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
     s_col[0] = h00;
     s_col[1] = make_double2(hn0, 0.0);
     s_st = givens_col(p, job, r, 0, s_col, hn0, s_rot, s_rot + 2, s_rot + 4, b0);
+    s_tri[0] = s_col[0];  // R00
   }
   __syncthreads();
   if (tp_on) {
@@ -857,6 +916,7 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
     atomicAdd((unsigned long long*)&g_in_t[0], (unsigned long long)(t1 - tp0));
     tp0 = t1;
   }
+  if (s_st == 1 && xs) sstep_final<SE>(p, job, r, n, 1, m0, m0, s_tri, s_rot + 4, xs);
   if (s_st != 0) return;
   // ---- j = 1: V_1 = w / hn0, E V_1 = (E^2 V_0 + E V_0 - h00 E V_0) / hn0, w = E V_1 + V_1
   double2* V1 = vecp(p, job, r, 1);
@@ -898,9 +958,12 @@ __device__ void instance_sstep(const InnerParams& p, int job, int r, int n, int 
     s_col[1] = h11;
     s_col[2] = make_double2(hn1, 0.0);
     s_st = givens_col(p, job, r, 1, s_col, hn1, s_rot, s_rot + 2, s_rot + 4, b0);
+    s_tri[1] = s_col[0];  // R01
+    s_tri[2] = s_col[1];  // R11
   }
   __syncthreads();
   if (tp_on) atomicAdd((unsigned long long*)&g_in_t[1], (unsigned long long)(clock64() - tp0));
+  if (s_st == 1 && xs) sstep_final<SE>(p, job, r, n, 2, m0, v1, s_tri, s_rot + 4, xs);
   if (s_st != 0) return;
   double2* V2 = vecp(p, job, r, 2);  // V_2 = w / hn1: the regular loop continues at j = 2
   const double ihn1 = 1.0 / hn1;
@@ -1410,7 +1473,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
       if (l >= uni(u)) continue;
       const int n_ = 4 * nIc * uw(u);
       if (n_ <= 4 * IN_THREADS)
-        instance_sstep(p, ujob(u), ur0(u) + l, n_, VY, VT, VA, dred);
+        instance_sstep(p, ujob(u), ur0(u) + l, n_, VY, VT, VA, dred, reinterpret_cast<double2*>(ring));
       else
         instance_sstep_loop(p, ujob(u), ur0(u) + l, n_, VY, VT, VA, dred);
     }
@@ -1458,7 +1521,9 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
   }
   for (int t = b; t < nunits * 8; t += G) {
     const int u = t >> 3, l = t & 7;
-    if (l < uni(u)) instance_final(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), uw(u), yv);
+    // (instances the s-step already finalized, state 3, are skipped)
+    if (l < uni(u) && p.state[ujob(u) * p.R + ur0(u) + l] != 3)
+      instance_final(p, ujob(u), ur0(u) + l, 4 * nIc * uw(u), uw(u), yv);
   }
   T.tick(9);
   if (p.fused) {
