@@ -367,9 +367,9 @@ __global__ void k_scale_div(VecView dst, VecView src, long long len, const int* 
     const int q = (int)(e / len);
     const long long i = e - (long long)q * len;
     const int r = rmap[q];
-    const double s = scale[r];
+    const double s = 1.0 / scale[r];  // one division per element instead of two
     const double2 a = src.p[r * src.stride + i];
-    dst.p[r * dst.stride + i] = make_double2(a.x / s, a.y / s);
+    dst.p[r * dst.stride + i] = make_double2(a.x * s, a.y * s);
   }
 }
 
