@@ -1551,14 +1551,13 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
       if (stats->relres) stats->relres[r] = ff > 0 ? std::sqrt(c->hdscal[2 * r]) / std::sqrt(ff) : 0.0;
       if (stats->converged) stats->converged[r] = s.status == 1;
     }
+    // one strided copy for all RHS (the reassembled traces are the first half of each RHS's TR row)
     if (stats->traces && c->nI > 0)
-      for (int r = 0; r < R; ++r)
-        CK(cudaMemcpy(stats->traces + (size_t)r * nO, c->TR + (size_t)r * nO, sizeof(double2) * nO / 2,
-                      cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy2DAsync(stats->traces, sizeof(double2) * nO / 2, c->TR, sizeof(double2) * nO,
+                           sizeof(double2) * nO / 2, R, cudaMemcpyDeviceToHost, c->st));
     if (stats->polarized && c->nI > 0)
-      for (int r = 0; r < R; ++r)
-        CK(cudaMemcpy(stats->polarized + (size_t)r * 2 * nO, c->X + (size_t)r * nO, sizeof(double2) * nO,
-                      cudaMemcpyDeviceToHost));
+      CK(cudaMemcpyAsync(stats->polarized, c->X, sizeof(double2) * (size_t)R * nO, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
     unsigned long long cnt[4] = {0, 0, 0, 0};
     CK(cudaMemcpy(cnt, c->cnt_d, sizeof(cnt), cudaMemcpyDeviceToHost));
     if (stats->layer_solves) stats->layer_solves[0] = c->layer_solves;
