@@ -1408,6 +1408,9 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
   unsigned dch = 0;
   // y = M_which x over the active instances of every unit; all = every instance (the first product)
   // nmat > 1: `which` is a stack of nmat matrices sharing x (row tiles stacked), outputs dst, dst + 1, ...
+  // Work list: (tile, active unit) pairs, TILE-major within a job (f = job base + tile * nA + unit index), so a
+  // CTA streams the same operator tiles for every RHS group of a job back to back (the repeats hit L2).
+  __shared__ short s_ug[COOP_MAXU][2];  // per unit: active units of its job, its index among them
   auto coop_apply = [&](int which, int src, int dst, bool all, int nmat = 1) {
     T.tick(7);
     load_states(all);
@@ -1418,18 +1421,40 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
         for (int l = 0; l < 8; ++l)
           if (sst[u * 8 + l] == 0) uact[u * 8 + na++] = (unsigned char)l;
         unact[u] = na;
-        utile[u] = tot;
-        if (na > 0) tot += nmat * ((4 * nIc * uw(u) + 7) >> 3);
+      }
+      for (int u0 = 0; u0 < nunits; u0 += ngroups) {  // one job: units u0 .. u0 + ngroups - 1
+        int nA = 0;
+        for (int g = 0; g < ngroups; ++g)
+          if (unact[u0 + g] > 0) s_ug[u0 + g][1] = (short)nA++;
+        // unit-major order for jobs of <= 2 RHS groups (PT_UNIT_MAJOR forces it): there the tile-major split halves
+        // each pass and its staging overhead outweighs the L2 reuse (cfg2); from 3 groups on the reuse wins
+        // (cfg3, 8 groups: 536 -> 497 ms per 64-source step)
+        if (p.unit_major || ngroups <= 2) {  // each active unit its own contiguous range
+          for (int g = 0; g < ngroups; ++g) {
+            s_ug[u0 + g][0] = 1;
+            s_ug[u0 + g][1] = 0;
+            utile[u0 + g] = tot;
+            if (unact[u0 + g] > 0) tot += nmat * ((4 * nIc * uw(u0) + 7) >> 3);
+          }
+          continue;
+        }
+        for (int g = 0; g < ngroups; ++g) {
+          s_ug[u0 + g][0] = (short)nA;
+          utile[u0 + g] = tot;
+        }
+        tot += nA * nmat * ((4 * nIc * uw(u0) + 7) >> 3);
       }
       utile[nunits] = tot;
     }
     __syncthreads();
     const int tot = utile[nunits];
     const int lo = (int)((long long)b * tot / G), hi = (int)((long long)(b + 1) * tot / G);
+    auto cdivs = [](int a, int d) { return a <= 0 ? -((-a) / d) : (a + d - 1) / d; };
     for (int u = 0; u < nunits && lo < hi; ++u) {
       const int na = unact[u];
       if (na == 0) continue;
-      const int t0 = max(lo, utile[u]) - utile[u], t1 = min(hi, utile[u + 1]) - utile[u];  // unit u's tiles
+      const int nA = s_ug[u][0], gi = s_ug[u][1], T8u = nmat * ((4 * nIc * uw(u) + 7) >> 3);
+      const int t0 = max(0, cdivs(lo - utile[u] - gi, nA)), t1 = min(T8u, cdivs(hi - utile[u] - gi, nA));
       if (t0 >= t1) continue;
       const int job = ujob(u), r0 = ur0(u), w = uw(u), n = 4 * nIc * w;
       int rr[8];

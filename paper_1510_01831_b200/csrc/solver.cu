@@ -724,6 +724,8 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   static const bool arn_slow = std::getenv("PT_ARN_SLOW") != nullptr;
   ip.arn_fast = !arn_slow;
   ip.coop_sms = c->coop_sms;
+  static const bool unit_major = std::getenv("PT_UNIT_MAJOR") != nullptr;
+  ip.unit_major = unit_major;
   static const bool no_sstep = std::getenv("PT_NO_SSTEP") != nullptr;
   ip.sstep = !no_sstep && c->dense_cnt >= 4 && c->dense_d;
   if (ip.tring < 4 * ip.mg) ip.mg = 1;  // a group's (slot, row tile) tiles must fit in the ring together
