@@ -1609,6 +1609,8 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_items_kernel(const I
   S.oph = oph;
   S.pph = pph;
   __shared__ int s_job[COOP_MAXU], s_w[COOP_MAXU], s_layer[COOP_MAXU];
+  __shared__ short s_alist[COOP_MAXU];    // active units, job-major
+  __shared__ int s_jstart[COOP_MAXU + 1];  // per job: start of its active units in s_alist
   const int tid = threadIdx.x, G = gridDim.x, b = blockIdx.x;
   const int ngroups = (p.R + 7) >> 3;
   const int nIc = p.Lc - 1;
@@ -1645,49 +1647,68 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_items_kernel(const I
     }
     __syncthreads();
     if (tid == 0) {
-      int acc = 0;
-      for (int u = 0; u < nunits; ++u) {
-        upre[u] = acc;
-        if (unact[u] > 0) acc += ungrp(u);
+      // per job: prefix (upre, indexed by job) of active units x tile groups, and its active units in order
+      int acc = 0, na_tot = 0;
+      for (int jx = 0; jx < njob_; ++jx) {
+        upre[jx] = acc;
+        s_jstart[jx] = na_tot;
+        for (int g = 0; g < ngroups; ++g) {
+          const int u = jx * ngroups + g;
+          if (unact[u] > 0) {
+            s_alist[na_tot++] = (short)u;
+            acc += ungrp(u);
+          }
+        }
       }
-      upre[nunits] = acc;
+      upre[njob_] = acc;
+      s_jstart[njob_] = na_tot;
     }
     __syncthreads();
   };
   uint32_t tseq = 0;
   auto cdiv = [](long long a, long long bb) -> long long { return a <= 0 ? -((-a) / bb) : (a + bb - 1) / bb; };
-  // one program over every unit's active instances: CTA b takes the (unit, item, tile group) triples whose
-  // weight midpoints fall in its share; a grid barrier ends each phase
+  // one program over every unit's active instances: CTA b takes the (job, item, unit, tile group) work whose
+  // weight midpoints fall in its share, job-major then item-major, so the RHS groups of a job run an item's
+  // tile groups back to back on one CTA (their Green tiles repeat from L2); a grid barrier ends each phase
   auto coop_program = [&](const int* ph, int nph, const int vmap[3]) {
     for (int phz = 0; phz < nph; ++phz) {
       const int it0 = ph[phz], nit = ph[phz + 1] - it0;
       int witems = 0;
       for (int ii = 0; ii < nit; ++ii) witems += S.items[it0 + ii].wgt;
-      const long long wtot = (long long)upre[nunits] * witems;
+      const long long wtot = (long long)upre[njob_] * witems;
       const long long wlo2 = 2 * ((long long)b * wtot / G), whi2 = 2 * ((long long)(b + 1) * wtot / G);
-      // first unit whose weight range reaches this CTA's share
-      int lo = 0, hi = nunits;
+      // first job whose weight range reaches this CTA's share
+      int lo = 0, hi = njob_;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (2LL * upre[mid + 1] * witems <= wlo2) lo = mid + 1;
         else hi = mid;
       }
-      for (int u = lo; u < nunits && 2LL * upre[u] * witems < whi2; ++u) {
-        const int na = unact[u];
-        if (na == 0) continue;
-        const int ng = ungrp(u), job = ujob(u), w = uw(u), r0 = ur0(u), layer = s_layer[u / ngroups];
-        long long wcum = (long long)upre[u] * witems;
+      for (int jx = lo; jx < njob_ && 2LL * upre[jx] * witems < whi2; ++jx) {
+        const int nA = s_jstart[jx + 1] - s_jstart[jx];
+        if (nA == 0) continue;
+        const int u_first = s_alist[s_jstart[jx]];
+        const int ng = ungrp(u_first), job = ujob(u_first), w = uw(u_first), layer = s_layer[jx];
+        long long ib = (long long)upre[jx] * witems;  // item block start
         for (int ii = 0; ii < nit; ++ii) {
           const IItem& item = S.items[it0 + ii];
           const int wi = item.wgt;
-          const long long wa = wcum;
-          wcum += (long long)wi * ng;
-          const int g0 = (int)max(0LL, cdiv(wlo2 - 2 * wa - wi, 2LL * wi));
-          const int g1 = (int)min((long long)ng, cdiv(whi2 - 2 * wa - wi, 2LL * wi));
-          if (g0 >= g1) continue;
-          T.tick(12);
+          const long long iblock = (long long)wi * ng * nA;
+          if (2 * (ib + iblock) <= wlo2 || 2 * ib >= whi2) {
+            ib += iblock;
+            continue;
+          }
           const long long goff = p.cells[layer * p.Lc + (item.cell >= 0 ? item.cell : 0)].green_off;
-          item_unit(p, job, w, r0, uact + u * 8, na, item, g0, g1, vmap, S, &tseq, T, goff);
+          for (int gi = 0; gi < nA; ++gi) {
+            const long long wa = ib + (long long)gi * wi * ng;
+            const int g0 = (int)max(0LL, cdiv(wlo2 - 2 * wa - wi, 2LL * wi));
+            const int g1 = (int)min((long long)ng, cdiv(whi2 - 2 * wa - wi, 2LL * wi));
+            if (g0 >= g1) continue;
+            const int u = s_alist[s_jstart[jx] + gi];
+            T.tick(12);
+            item_unit(p, job, w, ur0(u), uact + u * 8, unact[u], item, g0, g1, vmap, S, &tseq, T, goff);
+          }
+          ib += iblock;
         }
       }
       gsync();
@@ -1722,7 +1743,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_items_kernel(const I
   gsync();
   for (int j = 0; j < p.max_iter; ++j) {
     refresh(false);
-    if (upre[nunits] == 0) break;
+    if (upre[njob_] == 0) break;
     if (j + 1 > p.cap) {  // basis capacity exhausted: the host retries with a larger capacity
       for (int t = b; t < nunits * 8; t += G) {
         const int u = t >> 3, l = t & 7;
@@ -1785,7 +1806,7 @@ static cudaError_t inner_coop_items_launch(const InnerParams& p0, int njobs, cud
   // the ring gives up what the unit tables take (static s_job/s_w/s_layer: 3 COOP_MAXU ints)
   const int w = p.wmax < 8 ? 8 : p.wmax;
   const long long tb = (long long)w * 8 * 16;
-  const long long shrink = ((long long)coop_items_extra() + 3LL * COOP_MAXU * 4 + tb - 1) / tb;
+  const long long shrink = ((long long)coop_items_extra() + 5LL * COOP_MAXU * 4 + tb - 1) / tb;
   p.tring = (int)std::min((long long)IN_TRMAX, (long long)inner_tring(p.wmax, p.nitems) - shrink);
   if (p.tring < 4 * p.mg) p.mg = 1;
   if (p.tring < 4) return cudaErrorNotSupported;
