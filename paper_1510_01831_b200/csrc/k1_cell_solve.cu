@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cstdio>
 
+#include <cstdlib>
 #include "pt_launch.cuh"
 
 #ifndef K1_FETCH_POS
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   uint64_t* xbar = cempty + K1_NS;
 
   const int w4 = (w + 3) & ~3;  // stored columns per block (zero padded)
-  const int jc = NC == 8 ? K1_JC8 : 7 * k1_jw(NC);  // columns per ring chunk
+  const int jc = NC == 8 ? p.jc8 : 7 * k1_jw(NC);  // columns per ring chunk
   const int wcols = NC == 8 ? w4 : w;                // streamed columns (DMMA: zero padded to w4)
   const int nch = (wcols + jc - 1) / jc;
   const int total = nst * nch;
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
         for (int t = 0; t < NMT; ++t) cm_[t][0] = cm_[t][1] = cm_[t][2] = cm_[t][3] = 0.0;
         for (int ch = 0; ch < nch; ++ch) {
           const int slot = rslot;
-          const int ks0 = ch * (K1_JC8 / 4), ks1 = min(w4, (ch + 1) * K1_JC8) >> 2;
+          const int ks0 = ch * (p.jc8 / 4), ks1 = min(w4, (ch + 1) * p.jc8) >> 2;
           int ks = ks0 + ((wp - ks0) % 7 + 7) % 7;  // first k-step of this warp in the chunk
           if (ks < ks1) {
             if (!(p.dbg & 1)) mbar_wait(&full[slot], rph);
@@ -569,12 +570,27 @@ cudaError_t k1_launch(const K1Params& p0, int ntasks, int nc, int wmax, cudaStre
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
-  // one ring slot holds one chunk (DMMA path K1_JC8 columns, DFMA path 7 * k1_jw(nc)); as many slots
+  // one ring slot holds one chunk (DMMA path p.jc8 columns, DFMA path 7 * k1_jw(nc)); as many slots
   // as the shared memory left next to this NC's vectors allows (<= K1_NS, a multiple of cm)
   K1Params p = p0;
-  const int jc = nc == 8 ? K1_JC8 : 7 * k1_jw(nc);
-  const long long slot = (16LL * wmax * jc + 127) / 128 * 128;
+  static const int jc8_env = std::getenv("PT_K1_JC8") ? atoi(std::getenv("PT_K1_JC8")) : 0;
   const long long fixed = (long long)k1_smem_bytes(wmax, nc, 0, 0);
+  // DMMA path: the widest chunk (28 / 20 / 12 columns = 7 / 5 / 3 k-steps) that still leaves >= 4 ring slots;
+  // 7 k-steps per chunk give every consumer warp one k-step of each chunk (cfg2: 9.9 -> 9.8 ms per step)
+  p.jc8 = K1_JC8;
+  if (jc8_env >= 4) {
+    p.jc8 = jc8_env & ~3;
+  } else {
+    for (int cand : {28, 20, 12}) {
+      const long long sl = (16LL * wmax * cand + 127) / 128 * 128;
+      if (((long long)maxsm - fixed) / sl >= 4) {
+        p.jc8 = cand;
+        break;
+      }
+    }
+  }
+  const int jc = nc == 8 ? p.jc8 : 7 * k1_jw(nc);
+  const long long slot = (16LL * wmax * jc + 127) / 128 * 128;
   int ns = (int)std::min<long long>(K1_NS, ((long long)maxsm - fixed) / slot);
   ns -= ns % p.cm;
   if (ns < 2) return cudaErrorInvalidValue;

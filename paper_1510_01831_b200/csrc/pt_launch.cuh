@@ -28,6 +28,7 @@ struct VecTab {
 };
 
 struct K1Params {
+  int jc8;                // DMMA path (NC = 8): columns per ring chunk (multiple of 4; K1_JC8 or PT_K1_JC8)
   const CellInfo* cells;
   const LayerInfo* layers;
   const OJob* jobs;
@@ -116,7 +117,7 @@ cudaError_t k1_launch(const K1Params& p, int ntasks, int nc, int wmax, cudaStrea
 #define K1_DMMA_ITEMS 3  // 8-row tiles per warp in the DMMA path: ceil(128/8) <= 3*7
 // DFMA path: columns per consumer warp per ring chunk (7 warps per chunk)
 __host__ __device__ constexpr int k1_jw(int nc) { return nc == 1 ? 5 : (nc == 2 ? 4 : 2); }
-#define K1_JC8 12        // ring chunk width (columns) of the DMMA path: 3 k-steps
+#define K1_JC8 12        // narrowest ring chunk width (columns) of the DMMA path: 3 k-steps (k1_launch widens it)
 size_t inner_smem_bytes(int wmax, int nitems, int tring);
 int inner_tring(int wmax, int nitems);
 int inner_mg(int wmax);
