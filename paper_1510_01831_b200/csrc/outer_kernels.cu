@@ -32,7 +32,7 @@ __global__ void k_combine(const OJob* jobs, int njobs, VecTab t, const int* rmap
     combine_elem(jobs, t, rmap, nq, wx, smp, e);
 }
 
-template <bool DIRECT>
+template <bool DIRECT, bool SEG>
 __global__ void __launch_bounds__(P0_KQ * 32) k_pass0(const int* __restrict__ grp, const int* __restrict__ ljobs,
                                                       const OJob* __restrict__ jobs,
                                                       const CellInfo* __restrict__ cells,
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(P0_KQ * 32) k_pass0(const int* __restrict__ gr
                                                       int Lc, int wx, int wmax, int accum, VecTab tab,
                                                       const int* rmap, int direct, RhsOut ro) {
   __shared__ double part[(P0_KQ - 1) * 2 * 4 * 32];
-  pass0_item<DIRECT>(grp, ljobs, jobs, cells, layers, q0, P, tables, smp, R, Lc, wx, wmax, blockIdx.x / Lc,
+  pass0_item<DIRECT, SEG>(grp, ljobs, jobs, cells, layers, q0, P, tables, smp, R, Lc, wx, wmax, blockIdx.x / Lc,
                      blockIdx.x % Lc, blockIdx.y, blockIdx.z, threadIdx.x >> 5, part, 1, accum,
                      DIRECT ? &tab : nullptr, rmap, ro.base ? &ro : nullptr);
 }
@@ -570,11 +570,19 @@ cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJ
   const int mp = (4 * wmax + 4 * kmax + 7) / 8 * 8;
   const int gz = (max_jobs_per_layer * R + P0_COLS - 1) / P0_COLS;
   const RhsOut ro = rhs_out ? *rhs_out : RhsOut{nullptr, 0, 0};
+  // k-loop variant: (slot, k) advanced incrementally across the used slots (default) or per-slot segments with
+  // contiguous addresses (PT_P0_SEG=1; measured 4 % slower on cfg2: 9.80-10.05 vs 9.39-9.51 ms per step)
+  static const bool no_seg = std::getenv("PT_P0_SEG") == nullptr;
   if (tab)
-    k_pass0<true><<<dim3(ngroups * Lc, mp / 8, gz), P0_KQ * 32, 0, st>>>(grp, ljobs, jobs, cells, layers, q0, P, tables,
+    k_pass0<true, true><<<dim3(ngroups * Lc, mp / 8, gz), P0_KQ * 32, 0, st>>>(grp, ljobs, jobs, cells, layers, q0, P, tables,
                                                                        smp, R, Lc, wx, wmax, accum, tabv, rmap, 1, ro);
+  else if (no_seg)
+    k_pass0<false, false><<<dim3(ngroups * Lc, mp / 8, gz), P0_KQ * 32, 0, st>>>(grp, ljobs, jobs, cells, layers, q0, P,
+                                                                               tables, smp, R, Lc, wx, wmax, accum, tabv,
+                                                                               rmap, 0, ro);
   else
-    k_pass0<false><<<dim3(ngroups * Lc, mp / 8, gz), P0_KQ * 32, 0, st>>>(grp, ljobs, jobs, cells, layers, q0, P, tables,
-                                                                        smp, R, Lc, wx, wmax, accum, tabv, rmap, 0, ro);
+    k_pass0<false, true><<<dim3(ngroups * Lc, mp / 8, gz), P0_KQ * 32, 0, st>>>(grp, ljobs, jobs, cells, layers, q0, P,
+                                                                              tables, smp, R, Lc, wx, wmax, accum, tabv,
+                                                                              rmap, 0, ro);
   return cudaGetLastError();
 }

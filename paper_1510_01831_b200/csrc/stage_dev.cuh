@@ -55,7 +55,7 @@ __device__ __forceinline__ void combine_elem(const OJob* jobs, const VecTab& t, 
 // One (layer group g, cell c, row tile, 16-column chunk z) item, executed by P0_KQ warps (wq = warp index in
 // the group); part: [P0_KQ-1][2][4][32] doubles of shared memory; barid: named barrier of the group;
 // accum: add to the Newton tables instead of overwriting them.
-template <bool DIRECT = false>
+template <bool DIRECT = false, bool SEG = true>
 __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const int* __restrict__ ljobs,
                                            const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells,
                                            const LayerInfo* __restrict__ layers, const double2* __restrict__ q0,
@@ -116,6 +116,7 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
   }
   const int kps = nk4 >> 2, nks = nsl * kps;  // k-steps per slot / over the used slots
   const int kb = wp * nks / P0_KQ, ke = (wp + 1) * nks / P0_KQ;
+  if constexpr (SEG) {
   // the warp's k-steps [kb, ke) as per-slot segments: contiguous A and B addresses inside a segment
   for (int si = kps > 0 ? kb / kps : nsl; si < nsl && si * kps < ke; ++si) {
     const int sl = slist >> (2 * si) & 3;
@@ -152,6 +153,42 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
         }
       }
     }
+  }
+  } else {
+  // (used-slot index, k-step within the slot) of the next k-step, advanced incrementally (no divisions)
+  int si_c = kps > 0 ? kb / kps : 0, r_c = kb - si_c * kps;
+  for (int ks0 = kb; ks0 < ke; ks0 += 8) {
+    double2 av[8], bv[8][2];
+    int si = si_c, r = r_c;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool kin = ks0 + u < ke;
+      const int sl = slist >> (2 * (si & 3)) & 3;
+      const int kk = r * 4;  // column within the slot block (+ ak)
+      av[u] = kin ? __ldg(arow + (sl * kps + r) * 4) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int gq = 0; gq < 2; ++gq)
+        bv[u][gq] = (kin && bok[gq] && kk + ak < nk) ? bload(gq, sl, kk) : make_double2(0.0, 0.0);
+      if (++r == kps) {
+        r = 0;
+        ++si;
+      }
+    }
+    si_c = si;
+    r_c = r;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int gq = 0; gq < 2; ++gq) {
+        if (gq < ngq) {
+          dmma_f64(acc[gq][0], acc[gq][1], av[u].x, bv[u][gq].x);
+          dmma_f64(acc[gq][2], acc[gq][3], av[u].x, bv[u][gq].y);
+          dmma_f64(acc[gq][0], acc[gq][1], -av[u].y, bv[u][gq].y);
+          dmma_f64(acc[gq][2], acc[gq][3], av[u].y, bv[u][gq].x);
+        }
+      }
+    }
+  }
   }
   if (wp > 0) {
 #pragma unroll

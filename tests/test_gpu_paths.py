@@ -50,6 +50,7 @@ SWITCHES = {
     "separate-combine": {"PT_NO_FUSE_COMB": "1"},
     "inner-gather": {"PT_NO_RHS_OUT": "1"},
     "no-sstep": {"PT_NO_SSTEP": "1"},
+    "pass0-segments": {"PT_P0_SEG": "1"},
     "fused-glue": {"PT_FUSE_GLUE": "1"},
     "fused-stage": {"PT_FUSE": "1"},
     "recon-k1": {"PT_NO_REUSE": "1"},
