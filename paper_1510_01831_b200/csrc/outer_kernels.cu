@@ -60,9 +60,15 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_green_samples(
 // each row tile's K = (slot, column) range is split over GS2_KQ warps (A loads of a warp issued 8 k-steps
 // at a time), every A fragment serves all GS2_NG RHS groups, and the partial tiles are summed in a fixed
 // order by the kq = 0 warp.  Same products as green_item; the sum over K is split in GS2_KQ parts.
+#ifndef GS2_KQ
 #define GS2_KQ 4
+#endif
+#ifndef GS2_TPC
 #define GS2_TPC 2
+#endif
+#ifndef GS2_NG
 #define GS2_NG 2
+#endif
 __global__ void __launch_bounds__(GS2_KQ * GS2_TPC * 32) k_green_samples2(
     const OJob* __restrict__ jobs, const CellInfo* __restrict__ cells, const LayerInfo* __restrict__ layers,
     const double2* __restrict__ gsmp, const double2* __restrict__ tr, double2* __restrict__ smp, int R, int Lc, int wx,

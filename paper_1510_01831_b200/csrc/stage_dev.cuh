@@ -51,7 +51,9 @@ __device__ __forceinline__ void combine_elem(const OJob* jobs, const VecTab& t, 
 }
 
 #define P0_COLS 16  // columns (job, RHS) per CTA: two DMMA column groups of 8
+#ifndef P0_KQ
 #define P0_KQ 4      // k parts per row tile (one warp each), summed in shared memory in a fixed order
+#endif
 // One (layer group g, cell c, row tile, 16-column chunk z) item, executed by P0_KQ warps (wq = warp index in
 // the group); part: [P0_KQ-1][2][4][32] doubles of shared memory; barid: named barrier of the group;
 // accum: add to the Newton tables instead of overwriting them.
