@@ -298,7 +298,8 @@ __device__ void dense_pass(const InnerParams& p, const double2* __restrict__ Mt,
   // nmat stacked matrices (row tiles of matrix m at [m T8m, (m+1) T8m)) share the pass's x: T8 = stored row
   // tiles per chunk, the output of stacked tile t goes to vector dst + t / T8m, row (t % T8m) * 8 + ar
   const int T8m = (n + 7) >> 3, T8 = nmat * T8m, nks = n >> 2;
-  const uint32_t slot_bytes = dense_slot_bytes(scmax);  // fixed slot capacity (ring phases)
+  // fixed slot capacity (ring phases): the launcher's choice for the cooperative kernel, else by scmax
+  const uint32_t slot_bytes = p.da_slot > 0 ? (uint32_t)p.da_slot : dense_slot_bytes(scmax);
   const int ns = (int)min((size_t)DA_NS, region / slot_bytes);
   uint64_t* full = dbar;
   uint64_t* empty = dbar + DA_NS;
@@ -1847,8 +1848,15 @@ cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st)
     cudaFuncAttributes fa;
     static_sm = cudaFuncGetAttributes(&fa, inner_coop_kernel) == cudaSuccess ? fa.sharedSizeBytes : 16384;
   }
-  const size_t slot = (size_t)DA_T * DA_KC * 512 + 8 * (8 * DA_KC * 4 + 4) * 16;  // dense_slot_bytes(8)
+  size_t slot = (size_t)DA_T * DA_KC * 512 + 8 * (8 * DA_KC * 4 + 4) * 16;  // dense_slot_bytes(8)
   const size_t fixed = inner_coop_smem(p, 0) + static_sm;
+  // PT_DA_NS = n: n equal slots filling the shared memory left (each >= one 8-tile chunk + 8 x rows)
+  static const int da_ns = std::getenv("PT_DA_NS") ? atoi(std::getenv("PT_DA_NS")) : 0;
+  if (da_ns >= 2 && da_ns <= DA_NS) {
+    const size_t s2 = ((size_t)maxsm - fixed) / da_ns / 128 * 128;
+    if (s2 >= (size_t)DA_T * DA_KC * 512 + 8 * (DA_KC * 4 + 4) * 16) slot = s2;
+  }
+  p.da_slot = (int)slot;
   size_t region = std::min((size_t)DA_NS * slot, ((size_t)maxsm - fixed) / slot * slot);
   if (region < 2 * slot || region < (size_t)(IN_THREADS / 32) * DA_T * 4 * 32 * 8) return cudaErrorNotSupported;
   if (p.fused && (region < (size_t)4 * ((p.wmax + 3) & ~3) * 8 * 16 || region < 2 * (P0_KQ - 1) * 2 * 4 * 32 * 8))

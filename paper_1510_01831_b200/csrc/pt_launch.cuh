@@ -104,6 +104,7 @@ struct InnerParams {
   int sstep;              // dense stack [pre; E pre; E^2 pre] present: s-step start of the inner GMRES
   int rhs_ready;          // the stage's producer (pass-0 product) wrote rhs_pol into the VB scratch vectors
   int unit_major;         // dense products: unit-major work split instead of tile-major (PT_UNIT_MAJOR)
+  int da_slot;            // cooperative dense passes: ring slot capacity in bytes (set by the launcher; 0 = default)
   int arn_fast;           // Arnoldi steps of small instances with the basis prefetched (PT_ARN_SLOW = 0)
 };
 
