@@ -120,6 +120,32 @@ def test_c_abi_library_exports_every_header_symbol():
     assert b"sm_100a" in _abi.lib().pt_version()
 
 
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """The ctypes mirrors of pt_problem / pt_krylov / pt_stats have the header's size and field offsets
+    (a C program compiled against include/pt_b200.h prints them)."""
+    import subprocess
+
+    from paper_1510_01831_b200 import _abi
+
+    structs = {"pt_problem": _abi.PtProblem, "pt_krylov": _abi.PtKrylov, "pt_stats": _abi.PtStats}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pt_b200.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(REPO, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                   check=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, (cname, fname)
+
+
 def test_solver_fails_loudly_without_gpu():
     """No CPU fallback: constructing the device solver without a GPU raises."""
     if torch.cuda.is_available():
