@@ -73,12 +73,43 @@ struct InSmem {
   size_t region;    // bytes from tiles to the end of red (the dense-apply ring lives there)
 };
 
+// Issue (thread 0) the first min(tring, tiles) Green tiles of a future item_unit call with the same tile order
+// and ring sequence numbers (from *tseq) that item_unit uses; returns how many were issued.  The tiles are
+// operator data, independent of the phase results, so they can be in flight across the grid barrier.
+__device__ int item_prefetch(const InnerParams& p, int w, const IItem& item, int g0, int g1, const InSmem& S,
+                             const uint32_t* tseq, long long goff) {
+  const int nmt = (w + 7) >> 3, MG = p.mg, TR = p.tring;
+  int slotp = 0, ns = 0;
+  if (item.cell >= 0)
+    for (int s_ = 0; s_ < 4; ++s_)
+      if (item.pan[s_][0].vec >= 0) slotp |= s_ << (2 * ns++);
+  if (ns == 0) return 0;
+  int ntl = 0;
+  for (int g = g0; g < g1; ++g) ntl += ns * min(MG, nmt - g * MG);
+  const int n = min(TR, ntl);
+  const uint32_t tbytes = (uint32_t)w * 8u * 16u;
+  for (int j = 0; j < n; ++j) {
+    const int per = ns * MG;
+    const int g = g0 + j / per;
+    const int nt = min(MG, nmt - g * MG), rem = j - (j / per) * per;
+    const int si = rem / nt, t = rem - si * nt;
+    const uint32_t sq = *tseq + (uint32_t)j;
+    const int slot = (int)(sq % (uint32_t)TR);
+    mbar_expect_tx(&S.tbar[slot], tbytes);
+    bulk_g2s(S.tiles + (size_t)slot * w * 8,
+             p.green + goff + ((size_t)(item.row * 4 + (slotp >> (2 * si) & 3)) * nmt + g * MG + t) * w * 8, tbytes,
+             &S.tbar[slot]);
+  }
+  return n;
+}
+
 // One unit of a program phase: item `item` over its tile groups [g0, g1), for the nact active instances
 // act[0..nact) (local ids from r0) of job `job` (layer width w, Green pool offset goff of the item's cell).
 // Gathers the item's panels, streams its Green tiles through the ring, runs the DMMA products and writes the
 // combined outputs.  Used by the cluster kernel (run_program) and the cooperative item kernel.
 __device__ void item_unit(const InnerParams& p, int job, int w, int r0, const int* act, int nact, const IItem& item,
-                          int g0, int g1, const int vmap[3], const InSmem& S, uint32_t* tseq, Ticker& T, long long goff) {
+                          int g0, int g1, const int vmap[3], const InSmem& S, uint32_t* tseq, Ticker& T, long long goff,
+                          int pre = 0) {
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   const int nmt = (w + 7) >> 3;
   const int MG = p.mg;
@@ -123,7 +154,7 @@ __device__ void item_unit(const InnerParams& p, int job, int w, int r0, const in
   for (int si = 0; si < ns; ++si) twom |= (item.pan[slot_of(si)][1].vec >= 0) << si;
   if (ns > 0) {
     if (tid == 0)
-      for (int j = 0; j < min(TR, ntl); ++j) issue_tile(j);
+      for (int j = pre; j < min(TR, ntl); ++j) issue_tile(j);  // [0, pre) came with a prefetch
     ji = min(TR, ntl);
     T.tick(13);  // tile issue
     // slot panels as B fragments pan[si][k][qq] (16-byte cp.async, inactive instances zero-fill).
@@ -1671,47 +1702,73 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_items_kernel(const I
   // one program over every unit's active instances: CTA b takes the (job, item, unit, tile group) work whose
   // weight midpoints fall in its share, job-major then item-major, so the RHS groups of a job run an item's
   // tile groups back to back on one CTA (their Green tiles repeat from L2); a grid barrier ends each phase
-  auto coop_program = [&](const int* ph, int nph, const int vmap[3]) {
-    for (int phz = 0; phz < nph; ++phz) {
-      const int it0 = ph[phz], nit = ph[phz + 1] - it0;
-      int witems = 0;
-      for (int ii = 0; ii < nit; ++ii) witems += S.items[it0 + ii].wgt;
-      const long long wtot = (long long)upre[njob_] * witems;
-      const long long wlo2 = 2 * ((long long)b * wtot / G), whi2 = 2 * ((long long)(b + 1) * wtot / G);
-      // first job whose weight range reaches this CTA's share
-      int lo = 0, hi = njob_;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (2LL * upre[mid + 1] * witems <= wlo2) lo = mid + 1;
-        else hi = mid;
-      }
-      for (int jx = lo; jx < njob_ && 2LL * upre[jx] * witems < whi2; ++jx) {
-        const int nA = s_jstart[jx + 1] - s_jstart[jx];
-        if (nA == 0) continue;
-        const int u_first = s_alist[s_jstart[jx]];
-        const int ng = ungrp(u_first), job = ujob(u_first), w = uw(u_first), layer = s_layer[jx];
-        long long ib = (long long)upre[jx] * witems;  // item block start
-        for (int ii = 0; ii < nit; ++ii) {
-          const IItem& item = S.items[it0 + ii];
-          const int wi = item.wgt;
-          const long long iblock = (long long)wi * ng * nA;
-          if (2 * (ib + iblock) <= wlo2 || 2 * ib >= whi2) {
-            ib += iblock;
-            continue;
-          }
-          const long long goff = p.cells[layer * p.Lc + (item.cell >= 0 ? item.cell : 0)].green_off;
-          for (int gi = 0; gi < nA; ++gi) {
-            const long long wa = ib + (long long)gi * wi * ng;
-            const int g0 = (int)max(0LL, cdiv(wlo2 - 2 * wa - wi, 2LL * wi));
-            const int g1 = (int)min((long long)ng, cdiv(whi2 - 2 * wa - wi, 2LL * wi));
-            if (g0 >= g1) continue;
-            const int u = s_alist[s_jstart[jx] + gi];
-            T.tick(12);
-            item_unit(p, job, w, ur0(u), uact + u * 8, unact[u], item, g0, g1, vmap, S, &tseq, T, goff);
-          }
+  // this CTA's work of phase phz in order, as cb(jx, ii, gi, u, g0, g1, item, goff) -> keep going?
+  auto for_work = [&](const int* ph, int phz, auto&& cb) {
+    const int it0 = ph[phz], nit = ph[phz + 1] - it0;
+    int witems = 0;
+    for (int ii = 0; ii < nit; ++ii) witems += S.items[it0 + ii].wgt;
+    const long long wtot = (long long)upre[njob_] * witems;
+    const long long wlo2 = 2 * ((long long)b * wtot / G), whi2 = 2 * ((long long)(b + 1) * wtot / G);
+    // first job whose weight range reaches this CTA's share
+    int lo = 0, hi = njob_;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (2LL * upre[mid + 1] * witems <= wlo2) lo = mid + 1;
+      else hi = mid;
+    }
+    for (int jx = lo; jx < njob_ && 2LL * upre[jx] * witems < whi2; ++jx) {
+      const int nA = s_jstart[jx + 1] - s_jstart[jx];
+      if (nA == 0) continue;
+      const int u_first = s_alist[s_jstart[jx]];
+      const int ng = ungrp(u_first), layer = s_layer[jx];
+      long long ib = (long long)upre[jx] * witems;  // item block start
+      for (int ii = 0; ii < nit; ++ii) {
+        const IItem& item = S.items[it0 + ii];
+        const int wi = item.wgt;
+        const long long iblock = (long long)wi * ng * nA;
+        if (2 * (ib + iblock) <= wlo2 || 2 * ib >= whi2) {
           ib += iblock;
+          continue;
         }
+        const long long goff = p.cells[layer * p.Lc + (item.cell >= 0 ? item.cell : 0)].green_off;
+        for (int gi = 0; gi < nA; ++gi) {
+          const long long wa = ib + (long long)gi * wi * ng;
+          const int g0 = (int)max(0LL, cdiv(wlo2 - 2 * wa - wi, 2LL * wi));
+          const int g1 = (int)min((long long)ng, cdiv(whi2 - 2 * wa - wi, 2LL * wi));
+          if (g0 >= g1) continue;
+          if (!cb(jx, ii, gi, s_alist[s_jstart[jx] + gi], g0, g1, item, goff)) return;
+        }
+        ib += iblock;
       }
+    }
+  };
+  // one program over every unit's active instances: CTA b takes the (job, item, unit, tile group) work whose
+  // weight midpoints fall in its share, job-major then item-major, so the RHS groups of a job run an item's
+  // tile groups back to back on one CTA (their Green tiles repeat from L2); a grid barrier ends each phase.
+  // With p.tprefetch (opt-in) a CTA issues, before the barrier, the first Green tiles of its first work item of
+  // the next phase (operator data, independent of the phase results).
+  auto coop_program = [&](const int* ph, int nph, const int vmap[3]) {
+    int pf_phz = -1, pf_jx = -1, pf_ii = -1, pf_gi = -1, pf_n = 0;
+    for (int phz = 0; phz < nph; ++phz) {
+      bool first = true;
+      for_work(ph, phz, [&](int jx, int ii, int gi, int u, int g0, int g1, const IItem& item, long long goff) {
+        const int pre = (first && pf_phz == phz && jx == pf_jx && ii == pf_ii && gi == pf_gi) ? pf_n : 0;
+        first = false;
+        T.tick(12);
+        item_unit(p, ujob(u), uw(u), ur0(u), uact + u * 8, unact[u], item, g0, g1, vmap, S, &tseq, T, goff, pre);
+        return true;
+      });
+      pf_phz = -1;
+      pf_n = 0;
+      if (p.tprefetch && phz + 1 < nph)
+        for_work(ph, phz + 1, [&](int jx, int ii, int gi, int u, int g0, int g1, const IItem& item, long long goff) {
+          if (tid == 0) pf_n = item_prefetch(p, uw(u), item, g0, g1, S, &tseq, goff);
+          pf_phz = phz + 1;
+          pf_jx = jx;
+          pf_ii = ii;
+          pf_gi = gi;
+          return false;  // the first work item only
+        });
       gsync();
     }
   };

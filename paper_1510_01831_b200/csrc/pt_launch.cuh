@@ -105,6 +105,7 @@ struct InnerParams {
   int rhs_ready;          // the stage's producer (pass-0 product) wrote rhs_pol into the VB scratch vectors
   int unit_major;         // dense products: unit-major work split instead of tile-major (PT_UNIT_MAJOR)
   int da_slot;            // cooperative dense passes: ring slot capacity in bytes (set by the launcher; 0 = default)
+  int tprefetch;          // item-program kernel: next phase's first Green tiles issued before the grid barrier
   int arn_fast;           // Arnoldi steps of small instances with the basis prefetched (PT_ARN_SLOW = 0)
 };
 

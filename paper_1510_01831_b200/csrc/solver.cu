@@ -726,6 +726,10 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   ip.coop_sms = c->coop_sms;
   static const bool unit_major = std::getenv("PT_UNIT_MAJOR") != nullptr;
   ip.unit_major = unit_major;
+  // opt-in (PT_TPREFETCH=1): measured slower (cfg5 1 source 1328 vs 1217 ms; the prefetch delays each CTA's
+  // arrival at the grid barrier more than it saves after it)
+  static const bool tprefetch = std::getenv("PT_TPREFETCH") != nullptr;
+  ip.tprefetch = tprefetch;
   static const bool no_sstep = std::getenv("PT_NO_SSTEP") != nullptr;
   ip.sstep = !no_sstep && c->dense_cnt >= 4 && c->dense_d;
   if (ip.tring < 4 * ip.mg) ip.mg = 1;  // a group's (slot, row tile) tiles must fit in the ring together

@@ -51,6 +51,7 @@ SWITCHES = {
     "inner-gather": {"PT_NO_RHS_OUT": "1"},
     "no-sstep": {"PT_NO_SSTEP": "1"},
     "pass0-segments": {"PT_P0_SEG": "1"},
+    "items-tile-prefetch": {"PT_NO_DENSE": "1", "PT_TPREFETCH": "1"},
     "fused-glue": {"PT_FUSE_GLUE": "1"},
     "fused-stage": {"PT_FUSE": "1"},
     "recon-k1": {"PT_NO_REUSE": "1"},
