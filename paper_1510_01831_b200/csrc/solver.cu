@@ -156,6 +156,11 @@ struct pt_ctx {
   long long gen = 0;
   bool graphs_off = false;
   int coop_sms = 0;  // SM budget of the cooperative inner kernels (PT_COOP_SMS; 0 = all)
+  // outputs copied to the host while the reconstruction runs: side stream, events, pinned staging
+  cudaStream_t side_st = nullptr;
+  cudaEvent_t ev_tr = nullptr, ev_cp = nullptr;
+  double2* hstage = nullptr;
+  size_t hstage_cap = 0;
   std::vector<long long> asm_touch;  // per layer: assembled-boundary touches per boundary_samples call
   long long touch_extra = 0;         // host-side touches of this solve (assembled boundary accounting)
   unsigned rmap_slot = 0;
@@ -1294,6 +1299,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   const long long vstride = (long long)(c->capO + 1) * nO;
   VecView vB{c->Bv, nO}, vBp{c->Bp, nO}, vT{c->T1, nO}, vA{c->AX, nO}, vX{c->X, nO}, vTR{c->TR, nO};
   int rc = 0;
+  bool staged = false;  // traces / polarized solution on their way to c->hstage
   // stage buffers index f/u by compact q: the stage kernels read f via rmap-free indexing, so
   // run the volumetric stages with f/u views offset per active list (contiguous when all live).
   std::vector<int> all(R);
@@ -1522,9 +1528,28 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     // traces = down + up (sie.py:426-427), then reconstruct (sie.py:428)
     if ((rc = set_active(c, all))) return rc;
     const long long half = nO / 2;
-    rc = graphed(c, gkey({4, R, c->tables_f_ok, c->tables_f_R}), [&]() -> int {
-      int r4 = lincomb(c, vTR, 0, vX, 0, 1.0, vX, half, 1.0, 1, half, R);
-      if (r4) return r4;
+    if ((rc = lincomb(c, vTR, 0, vX, 0, 1.0, vX, half, 1.0, 1, half, R))) return rc;
+    // the reassembled traces and the polarized solution are final here: they go to pinned staging on a side
+    // stream while the reconstruction runs, and reach the caller's arrays before the final synchronisation
+    if (stats && (stats->traces || stats->polarized)) {
+      const size_t need = (size_t)R * (nO / 2 + nO);
+      if (need > c->hstage_cap) {
+        if (c->hstage) cudaFreeHost(c->hstage);
+        c->hstage = nullptr;
+        c->hstage_cap = 0;
+        CK(cudaMallocHost(&c->hstage, sizeof(double2) * need));
+        c->hstage_cap = need;
+      }
+      CK(cudaEventRecord(c->ev_tr, c->st));
+      CK(cudaStreamWaitEvent(c->side_st, c->ev_tr, 0));
+      CK(cudaMemcpy2DAsync(c->hstage, sizeof(double2) * nO / 2, c->TR, sizeof(double2) * nO, sizeof(double2) * nO / 2,
+                           R, cudaMemcpyDeviceToHost, c->side_st));
+      CK(cudaMemcpyAsync(c->hstage + (size_t)R * nO / 2, c->X, sizeof(double2) * (size_t)R * nO,
+                         cudaMemcpyDeviceToHost, c->side_st));
+      CK(cudaEventRecord(c->ev_cp, c->side_st));
+      staged = true;
+    }
+    rc = graphed(c, gkey({6, R, c->tables_f_ok, c->tables_f_R}), [&]() -> int {
       return run_stage(c, c->recon, VecTab{{vTR, vTR, vTR}}, R, io);
     });
     if (rc) return rc;
@@ -1538,6 +1563,13 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   CK(cudaGetLastError());
   cudaEventRecord(e1, c->st);
   CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * 2 * R, cudaMemcpyDeviceToHost, c->st));
+  if (staged) {  // host copies from the staging overlap the reconstruction still running on the device
+    CK(cudaEventSynchronize(c->ev_cp));
+    if (stats->traces)
+      std::memcpy(stats->traces, c->hstage, sizeof(double2) * (size_t)R * nO / 2);
+    if (stats->polarized)
+      std::memcpy(stats->polarized, c->hstage + (size_t)R * nO / 2, sizeof(double2) * (size_t)R * nO);
+  }
   CK(cudaStreamSynchronize(c->st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -1557,13 +1589,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
       if (stats->relres) stats->relres[r] = ff > 0 ? std::sqrt(c->hdscal[2 * r]) / std::sqrt(ff) : 0.0;
       if (stats->converged) stats->converged[r] = s.status == 1;
     }
-    // one strided copy for all RHS (the reassembled traces are the first half of each RHS's TR row)
-    if (stats->traces && c->nI > 0)
-      CK(cudaMemcpy2DAsync(stats->traces, sizeof(double2) * nO / 2, c->TR, sizeof(double2) * nO,
-                           sizeof(double2) * nO / 2, R, cudaMemcpyDeviceToHost, c->st));
-    if (stats->polarized && c->nI > 0)
-      CK(cudaMemcpyAsync(stats->polarized, c->X, sizeof(double2) * (size_t)R * nO, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+
     unsigned long long cnt[4] = {0, 0, 0, 0};
     CK(cudaMemcpy(cnt, c->cnt_d, sizeof(cnt), cudaMemcpyDeviceToHost));
     if (stats->layer_solves) stats->layer_solves[0] = c->layer_solves;
@@ -1652,6 +1678,9 @@ int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   c->dev = device;
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->own_st = c->st;
+  CK(cudaStreamCreateWithFlags(&c->side_st, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_tr, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_cp, cudaEventDisableTiming));
   c->nx = pb->nx;
   c->nz = pb->nz;
   c->npml = pb->npml;
@@ -1921,6 +1950,10 @@ int pt_destroy(pt_ctx* c) {
   }
   for (auto& kv : c->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (c->hstage) cudaFreeHost(c->hstage);
+  if (c->ev_tr) cudaEventDestroy(c->ev_tr);
+  if (c->ev_cp) cudaEventDestroy(c->ev_cp);
+  if (c->side_st) cudaStreamDestroy(c->side_st);
   cudaStreamDestroy(c->own_st);
   delete c;
   return PT_OK;
