@@ -1569,6 +1569,9 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
       std::memcpy(stats->traces, c->hstage, sizeof(double2) * (size_t)R * nO / 2);
     if (stats->polarized)
       std::memcpy(stats->polarized, c->hstage + (size_t)R * nO / 2, sizeof(double2) * (size_t)R * nO);
+  } else if (stats && c->nI > 0) {  // nothing solved (monolayer / all sources zero): zero traces
+    if (stats->traces) std::memset(stats->traces, 0, sizeof(double2) * (size_t)R * nO / 2);
+    if (stats->polarized) std::memset(stats->polarized, 0, sizeof(double2) * (size_t)R * nO);
   }
   CK(cudaStreamSynchronize(c->st));
   float ms = 0.f;

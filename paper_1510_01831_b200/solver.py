@@ -219,8 +219,9 @@ class PolarizedTracesSolver:
         nh = np.zeros(R, dtype=np.int32)
         rel = np.zeros(R)
         conv = np.zeros(R, dtype=np.int32)
-        trac = np.zeros((R, max(nO // 2, 1)), dtype=np.complex128)
-        pol = np.zeros((R, max(nO, 1)), dtype=np.complex128)
+        # filled completely by pt_solve (zeros when there is nothing to copy): no zero-fill here
+        trac = np.empty((R, max(nO // 2, 1)), dtype=np.complex128)
+        pol = np.empty((R, max(nO, 1)), dtype=np.complex128)
         cnt = np.zeros(3, dtype=np.int64)
         ihist = np.zeros(64, dtype=np.int32)
         tms = np.zeros(1)
