@@ -72,6 +72,15 @@ def _peaks():
     return out
 
 
+def _inner_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_inner_traffic.json")) as fh:
+            return float(json.load(fh)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled every 10 ms during the timed region through NVML
     (in-process, so even a region of a few tens of ms gets samples); nvidia-smi -lms 200 if NVML is absent."""
@@ -411,7 +420,9 @@ def run_ours(args):
         "roofline": {
             "kernel": names[dom], "bound": "tensor", "unit": "TFLOP/s",
             "achieved": achieved_tf, "peak": peaks["fp64_tflops"],
-            "frac": achieved_tf / peaks["fp64_tflops"], "traffic": None,
+            "frac": achieved_tf / peaks["fp64_tflops"], "traffic": _inner_traffic(),
+            "traffic_src": "profiles/r01_inner_traffic.json: ncu dram__bytes_read+write per inner launch, averaged "
+                           "over the 57 inner launches of one solve (bytes per launch)",
             "peak_src": peaks["fp64_src"],
             "algorithmic": ("inner: 8 n^2 flops per instance per dense product (n = 4 (Lc-1) w), products = "
                             "inner iterations + inner solves; K1: 32*wz_c*w_c^2 B per cell solve per RHS "
