@@ -20,6 +20,7 @@
  *   pt_cell_solve   LayerWorkspace.solve on one cell (subdomain.py:214-221 -> SuperLU
  *                   solve): the K1 kernel alone (test hook).
  *   pt_set_stream / pt_set_profiling: run on a caller stream (e.g. torch's) / time every launch.
+ *   pt_residuals_stride: per-RHS length of the residual-history buffer for a Krylov config.
  *   pt_destroy / pt_last_error / pt_version.
  *
  * Return codes (errors map to the reference's exceptions, sie.py:420-425,
@@ -108,7 +109,7 @@ typedef struct {
 typedef struct {
   /* all optional (NULL = not requested); sized by the caller */
   double* iterations;    /* [nrhs] outer GMRES iterations (float, krylov.py:135) */
-  double* residuals;     /* [nrhs][max_iter] residual history (relative preconditioned) */
+  double* residuals;     /* [nrhs][pt_residuals_stride(cfg)] residual history (relative preconditioned) */
   int* n_residuals;      /* [nrhs] entries written per rhs */
   double* relres;        /* [nrhs] ||H u - f|| / ||f|| */
   int* converged;        /* [nrhs] */
@@ -147,6 +148,10 @@ int pt_layer_solve(pt_ctx* ctx, int layer, const double* rhs, int nrhs, double i
                    int inner_max_iter, double* out, pt_stats* stats);
 /* cell (layer, c): x = H_c^{-1} b for nrhs right-hand sides [nrhs][wz_c][w] (host) */
 int pt_cell_solve(pt_ctx* ctx, int layer, int cell, const double* b, int nrhs, double* x);
+
+/* entries per RHS of pt_stats.residuals: max_iter + 1 for GMRES (krylov.py:53-135), 2 max_iter + 1 for
+ * BiCGstab (krylov.py:138-201: the initial 1.0 plus two half steps per iteration) */
+int pt_residuals_stride(const pt_krylov* cfg);
 
 const char* pt_last_error(void);
 const char* pt_version(void);

@@ -34,6 +34,7 @@ EXPORTS = (
     "pt_solve_device",
     "pt_layer_solve",
     "pt_cell_solve",
+    "pt_residuals_stride",
     "pt_last_error",
     "pt_version",
 )
@@ -96,6 +97,8 @@ def load():
     lib.pt_layer_solve.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_double, C.c_int, _dp,
                                    C.POINTER(PtStats)]
     lib.pt_cell_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _dp]
+    lib.pt_residuals_stride.argtypes = [C.POINTER(PtKrylov)]
+    lib.pt_residuals_stride.restype = C.c_int
     lib.pt_last_error.restype = C.c_char_p
     lib.pt_version.restype = C.c_char_p
     for name in ("pt_create", "pt_destroy", "pt_solve", "pt_solve_device", "pt_layer_solve",

@@ -1887,7 +1887,12 @@ static cudaError_t inner_coop_items_launch(const InnerParams& p0, int njobs, cud
 
 // returns cudaErrorNotSupported when the cooperative path does not apply (caller falls back)
 cudaError_t inner_coop_launch(const InnerParams& p0, int njobs, cudaStream_t st) {
-  if (!p0.dense) return inner_coop_items_launch(p0, njobs, st);
+  if (!p0.dense) {
+    const cudaError_t e = inner_items_launch(p0, njobs, st);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+    return inner_coop_items_launch(p0, njobs, st);
+  }
   static int nsm = 0, maxsm = 0;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -2033,7 +2038,9 @@ cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st) {
   return e;
 }
 
+void inner_items_tprof_dump(const char* tag);
 void inner_tprof_dump(const char* tag) {
+  inner_items_tprof_dump(tag);
   long long t[16];
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(t, g_in_t, sizeof(t));

@@ -135,6 +135,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// expect_tx without release semantics: the producer thread does not wait for its earlier memory operations
+// (the bulk copies it has in flight) before arming the barrier
+__device__ __forceinline__ void mbar_expect_tx_relaxed(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
 // wait with a suspend-time hint: the thread sleeps in the barrier unit until the phase completes
 // (or the hint expires), so a waiting producer lane does not steal issue slots from its SMSP
 __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {

@@ -107,6 +107,12 @@ struct InnerParams {
   int da_slot;            // cooperative dense passes: ring slot capacity in bytes (set by the launcher; 0 = default)
   int tprefetch;          // item-program kernel: next phase's first Green tiles issued before the grid barrier
   int arn_fast;           // Arnoldi steps of small instances with the basis prefetched (PT_ARN_SLOW = 0)
+  // whole-GPU item-program kernel (inner_items.cu): RHS-minor scratch [job][vector][n-tile][nmax][8]
+  long long s2_vec, s2_job;  // double2 strides of one vector / one job (set by the launcher)
+  double2* part;             // vector-phase partials [3][part_items][cap + 2][8]
+  long long part_items;
+  int ii_dbg;                // PT_II_DBG timing switches of inner_items.cu (results invalid when set)
+  int ii_trace;              // PT_II_TRACE: event trace of CTA (ii_trace - 1), thread 0
 };
 
 size_t k1_smem_bytes(int wmax, int nc, int slot_bytes, int ns);
@@ -127,6 +133,10 @@ cudaError_t inner_launch(const InnerParams& p, int njobs, cudaStream_t st);
 // whole-GPU cooperative inner GMRES (dense operators); cudaErrorNotSupported: use inner_launch
 cudaError_t inner_coop_launch(const InnerParams& p, int njobs, cudaStream_t st);
 int inner_coop_max_units();  // (job, 8-RHS group) units one cooperative inner launch holds
+// whole-GPU inner GMRES over the item programs with all RHS of a job per tensor-core tile (inner_items.cu);
+// cudaErrorNotSupported: outside its limits (caller falls back)
+cudaError_t inner_items_launch(const InnerParams& p, int njobs, cudaStream_t st);
+long long inner_items_part_items(int num_sms, int jmax, int rmax);  // partial records the launcher needs
 void inner_tprof_dump(const char* tag);
 __global__ void k_dense_tiles(const double2* src, double2* dst, int n, int kc);
 __global__ void k_dense_tiles_stack3(const double2* s0, const double2* s1, const double2* s2, double2* dst, int n,

@@ -104,7 +104,7 @@ struct pt_ctx {
   Stage newton, op, refl, recon, layer_solve;
   std::vector<Stage> sdown, sup;  // sdown[I] for I=1..nI-1, sup[I] for I=0..nI-2
   // solve scratch
-  int capR = 0, capO = 0, inner_cap = 32;
+  int capR = 0, capO = 0, inner_cap = 12;  // inner Krylov basis; grown (up to inner_max_iter + 1) on demand
   long long nO = 0;
   double2 *V = nullptr, *Bv = nullptr, *Bp = nullptr, *T1 = nullptr, *AX = nullptr, *X = nullptr, *TR = nullptr;
   double2 *P = nullptr, *smp = nullptr, *tables = nullptr, *trc = nullptr, *Z = nullptr, *iscr = nullptr,
@@ -153,6 +153,9 @@ struct pt_ctx {
     double d_k1_bytes = 0.0;
   };
   std::map<std::vector<long long>, GraphEnt> graphs;
+  long long graphs_gen = -1;
+  double2* ipart = nullptr;  // vector-phase partials of the whole-GPU item-program inner kernel
+  long long ipart_items = 0;  // buffer generation the cached executables were captured against
   long long gen = 0;
   bool graphs_off = false;
   int coop_sms = 0;  // SM budget of the cooperative inner kernels (PT_COOP_SMS; 0 = all)
@@ -550,6 +553,7 @@ static int ensure_scratch(pt_ctx* c, int R, int capO) {
     if (p) cudaFree(p);
   };
   for (void* p : {(void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1, (void*)c->AX, (void*)c->X, (void*)c->TR,
+                  (void*)c->ipart,
                   (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->tables_f, (void*)c->trc, (void*)c->iscr,
                   (void*)c->hess, (void*)c->iters, (void*)c->istate, (void*)c->ibeta0, (void*)c->rmap_d, (void*)c->dscal,
                   (void*)c->hout, (void*)c->ybuf})
@@ -569,7 +573,11 @@ static int ensure_scratch(pt_ctx* c, int R, int capO) {
   CK(cudaMalloc(&c->trc, sizeof(double2) * (size_t)Jmax * R * std::max(c->Lc - 1, 1) * 2 * c->wmax));
   c->inmax = 4LL * std::max(c->Lc - 1, 1) * c->wmax;
   c->iscr_stride = (long long)(c->inner_cap + 5) * c->inmax;
-  CK(cudaMalloc(&c->iscr, sizeof(double2) * (size_t)Jmax * R * c->iscr_stride));
+  // instances padded to whole n-tiles of 8 (the item-program kernel's RHS-minor layout uses the same buffer)
+  const int Rp = (R + 7) / 8 * 8;
+  CK(cudaMalloc(&c->iscr, sizeof(double2) * (size_t)Jmax * Rp * c->iscr_stride));
+  c->ipart_items = inner_items_part_items(c->num_sms, Jmax, Rp);
+  CK(cudaMalloc(&c->ipart, sizeof(double2) * (size_t)3 * c->ipart_items * (c->inner_cap + 2) * 8));
   c->hstride = (long long)(c->inner_cap + 1) * c->inner_cap + (c->inner_cap + 1) + 2 * c->inner_cap;
   CK(cudaMalloc(&c->hess, sizeof(double2) * (size_t)Jmax * R * c->hstride));
   CK(cudaMalloc(&c->iters, sizeof(int) * (size_t)Jmax * R));
@@ -729,6 +737,10 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   static const bool arn_slow = std::getenv("PT_ARN_SLOW") != nullptr;
   ip.arn_fast = !arn_slow;
   ip.coop_sms = c->coop_sms;
+  ip.part = c->ipart;
+  ip.part_items = c->ipart_items;
+  ip.ii_dbg = std::getenv("PT_II_DBG") ? atoi(std::getenv("PT_II_DBG")) : 0;
+  ip.ii_trace = std::getenv("PT_II_TRACE") ? atoi(std::getenv("PT_II_TRACE")) : 0;
   static const bool unit_major = std::getenv("PT_UNIT_MAJOR") != nullptr;
   ip.unit_major = unit_major;
   // opt-in (PT_TPREFETCH=1): measured slower (cfg5 1 source 1328 vs 1217 ms; the prefetch delays each CTA's
@@ -1020,6 +1032,18 @@ static int graphed(pt_ctx* c, std::vector<long long> key, Body&& body) {
   static const bool no_graph = std::getenv("PT_NO_GRAPH") != nullptr || std::getenv("PT_INNER_TPROF") != nullptr ||
                                std::getenv("PT_K1_TPROF") != nullptr;
   if (no_graph || c->prof || c->graphs_off) return body();
+  // Executables captured against an older buffer generation can never match again (the key holds the
+  // generation), and callers passing fresh device buffers every call add keys: drop the stale ones when the
+  // generation moves, and everything when the cache grows past a bound (after the stream drains).
+  if (c->graphs_gen != c->gen || c->graphs.size() > 1024) {
+    if (!c->graphs.empty()) {
+      CK(cudaStreamSynchronize(c->st));
+      for (auto& kv : c->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      c->graphs.clear();
+    }
+    c->graphs_gen = c->gen;
+  }
   key.push_back(c->gen);
   key.push_back((long long)(uintptr_t)c->st);
   pt_ctx::GraphEnt& g = c->graphs[key];
@@ -1265,9 +1289,16 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   static const bool stage_prof = std::getenv("PT_STAGE_PROF") != nullptr;
   if (stage_prof) c->prof = true;
   c->cur_tag = "outer";
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  struct EvPair {  // released on every return path
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~EvPair() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } evp;
+  CK(cudaEventCreate(&evp.a));
+  CK(cudaEventCreate(&evp.b));
+  cudaEvent_t e0 = evp.a, e1 = evp.b;
   cudaEventRecord(e0, c->st);
 
   SolveIO io{f, N, u, N, cfg->inner_ktol, cfg->inner_max_iter};
@@ -1576,18 +1607,20 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   CK(cudaStreamSynchronize(c->st));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
-
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   int ecode = 0;
   if ((rc = check_err(c, &ecode))) return rc;
   if (stats) {
     for (int r = 0; r < R; ++r) {
       const RhsState& s = rs[r];
       if (stats->iterations) stats->iterations[r] = s.count >= 0.0 ? s.count : (double)s.total;
-      if (stats->n_residuals) stats->n_residuals[r] = (int)s.hist.size();
+      // the history buffer holds pt_residuals_stride(cfg) entries per RHS: GMRES writes at most max_iter + 1
+      // (krylov.py:76-78 appends a cycle-start check), BiCGstab 2 max_iter + 1 (the initial 1.0 and two half
+      // steps per iteration, krylov.py:159-199); n_residuals never exceeds what was stored
+      const int rstride = pt_residuals_stride(cfg);
+      const int nst = (int)std::min(s.hist.size(), (size_t)rstride);
+      if (stats->n_residuals) stats->n_residuals[r] = nst;
       if (stats->residuals)
-        for (size_t i = 0; i < s.hist.size() && (int)i < max_iter; ++i) stats->residuals[(size_t)r * max_iter + i] = s.hist[i];
+        for (int i = 0; i < nst; ++i) stats->residuals[(size_t)r * rstride + i] = s.hist[i];
       const double ff = c->hdscal[2 * r + 1];
       if (stats->relres) stats->relres[r] = ff > 0 ? std::sqrt(c->hdscal[2 * r]) / std::sqrt(ff) : 0.0;
       if (stats->converged) stats->converged[r] = s.status == 1;
@@ -1668,16 +1701,37 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
 extern "C" {
 
 const char* pt_last_error(void) { return g_err.c_str(); }
-const char* pt_version(void) { return "pt_b200 0.1 (sm_100a)"; }
+const char* pt_version(void) { return "pt_b200 0.2 (sm_100a)"; }
 
+int pt_residuals_stride(const pt_krylov* cfg) {
+  if (!cfg || cfg->max_iter < 1) return 0;
+  return cfg->method == 1 ? 2 * cfg->max_iter + 1 : cfg->max_iter + 1;
+}
+
+static int create_impl(pt_ctx* c, const pt_problem* pb, int device, pt_ctx** out);
+
+// Every failure after the context exists releases it (streams, events, device buffers) through
+// pt_destroy, which tolerates the members that were never created.
 int pt_create(const pt_problem* pb, int device, pt_ctx** out) {
   if (!pb || !out) return PT_BAD_ARGUMENT;
+  *out = nullptr;
   if (pb->L < 1 || pb->Lc < 1 || pb->Lc > PT_MAX_LC || pb->nx < 1 || pb->nz < 1) {
     g_err = "bad problem geometry";
     return PT_BAD_ARGUMENT;
   }
   CK(cudaSetDevice(device));
   pt_ctx* c = new pt_ctx();
+  const int rc = create_impl(c, pb, device, out);
+  if (rc != PT_OK) {
+    const std::string err = g_err;
+    *out = nullptr;
+    pt_destroy(c);
+    g_err = err;
+  }
+  return rc;
+}
+
+static int create_impl(pt_ctx* c, const pt_problem* pb, int device, pt_ctx** out) {
   c->dev = device;
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->own_st = c->st;
@@ -1937,7 +1991,7 @@ int pt_destroy(pt_ctx* c) {
                   (void*)c->trc, (void*)c->Z, (void*)c->iscr, (void*)c->hess, (void*)c->iters, (void*)c->istate,
                   (void*)c->ibeta0, (void*)c->err_d,
                   (void*)c->cnt_d, (void*)c->hist_d, (void*)c->rmap_d, (void*)c->dscal, (void*)c->hout,
-                  (void*)c->ybuf, (void*)c->io_f, (void*)c->io_u})
+                  (void*)c->ybuf, (void*)c->io_f, (void*)c->io_u, (void*)c->ipart})
     if (p) cudaFree(p);
   for (void* p : {(void*)c->hrmap, (void*)c->hhout, (void*)c->hdscal, (void*)c->hy})
     if (p) cudaFreeHost(p);
@@ -1957,18 +2011,23 @@ int pt_destroy(pt_ctx* c) {
   if (c->ev_tr) cudaEventDestroy(c->ev_tr);
   if (c->ev_cp) cudaEventDestroy(c->ev_cp);
   if (c->side_st) cudaStreamDestroy(c->side_st);
-  cudaStreamDestroy(c->own_st);
+  if (c->own_st) cudaStreamDestroy(c->own_st);
   delete c;
   return PT_OK;
 }
 
 static int solve_batch(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats) {
   int rc;
-  for (int attempt = 0; attempt < 4; ++attempt) {
+  const int need = std::max(2, cfg->inner_max_iter + 1);  // basis vectors of an inner solve at max_iter
+  while (true) {
     rc = solve_device(c, reinterpret_cast<const double2*>(f), nrhs, cfg, reinterpret_cast<double2*>(u), stats);
     if (rc != PT_CAPACITY) break;
-    // an inner Krylov basis outgrew its capacity: double it and redo the solve
-    c->inner_cap *= 2;
+    if (c->inner_cap >= need) {  // cannot happen: an inner solve stops at inner_max_iter (InnerSolveError)
+      g_err = "inner GMRES did not converge within inner_max_iter";
+      return PT_INNER_NOT_CONVERGED;
+    }
+    // an inner Krylov basis outgrew its capacity: grow it (up to inner_max_iter + 1) and redo the solve
+    c->inner_cap = std::min(2 * c->inner_cap, need);
     c->capR = 0;
     c->capO = 0;
   }
@@ -1981,6 +2040,9 @@ static int batch_rhs(const pt_ctx* c) {
   const int maxj = std::max(std::max((int)c->op.jobs.size(), (int)c->newton.jobs.size()),
                             std::max((int)c->recon.jobs.size(), (int)c->refl.jobs.size()));
   if (c->Lc < 2 || maxj == 0) return 1 << 30;
+  // item programs (no dense inner operators): the multi-job stages run the all-RHS item kernel
+  // (inner_items.cu, up to 256 RHS per job), the single-job sweep stages the per-8-RHS-unit kernel
+  if (!c->dense_d && !c->lu_d && maxj <= 64 && !std::getenv("PT_ITEMS_V1")) return 64;
   return 8 * std::max(1, inner_coop_max_units() / maxj);
 }
 
@@ -2006,7 +2068,7 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
     double btms = 0, bkms[3] = {0, 0, 0}, bk1b = 0, bcms[5] = {0, 0, 0, 0, 0}, bdfl = 0;
     std::vector<int> bh(hist.size(), 0);
     if (stats) {
-      const int mi = cfg->max_iter;
+      const int mi = pt_residuals_stride(cfg);
       sb.iterations = stats->iterations ? stats->iterations + r0 : nullptr;
       sb.residuals = stats->residuals ? stats->residuals + (size_t)r0 * mi : nullptr;
       sb.n_residuals = stats->n_residuals ? stats->n_residuals + r0 : nullptr;

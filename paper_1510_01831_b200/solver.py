@@ -212,10 +212,12 @@ class PolarizedTracesSolver:
         cfg = _abi.PtKrylov(config.ktol, config.max_iter, config.restart, self.layers.inner_ktol,
                             self.layers.inner_max_iter, 0 if preconditioner == "gs" else 1,
                             0 if config.method == "gmres" else 1)
+        L_ = _abi.lib()
         wz, wx = self.grid.shape
         nO = 4 * self.nI * wx
         its = np.zeros(R)
-        hist = np.zeros((R, config.max_iter))
+        hstride = L_.pt_residuals_stride(C.byref(cfg))  # max_iter + 1 (GMRES) / 2 max_iter + 1 (BiCGstab)
+        hist = np.zeros((R, hstride))
         nh = np.zeros(R, dtype=np.int32)
         rel = np.zeros(R)
         conv = np.zeros(R, dtype=np.int32)

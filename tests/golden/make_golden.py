@@ -91,9 +91,9 @@ def ref_solver(prob, nested=True, backend="pt", assembled=False):
 
 
 def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1, method="gmres", backend="pt",
-             assembled=False):
+             assembled=False, solver=None, traces=False, trace_decim=1):
     t0 = time.time()
-    s = ref_solver(prob, nested, backend, assembled)
+    s = solver if solver is not None else ref_solver(prob, nested, backend, assembled)
     t1 = time.time()
     f = prob.rhs([src_idx])[0]
     _INNER.clear()
@@ -121,7 +121,11 @@ def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1, method
         assembled=assembled,
         offline_s=t1 - t0,
         online_s=t2 - t1,
+        src_idx=src_idx,
     )
+    if traces and res.traces is not None:  # SolveResult.traces (sie.py:426-427), (nI, 2, wx)
+        out["traces"] = res.traces.data[:, :, ::trace_decim]
+        out["trace_decim"] = trace_decim
     print(f"{prob.name} src{src_idx} nested={nested}: its={res.iterations} "
           f"res={res.residuals} relres={res.relative_residual:.3e} touches={touches} "
           f"inner={len(_INNER)} offline={t1 - t0:.2f}s online={t2 - t1:.2f}s")
@@ -129,6 +133,33 @@ def run_case(prob, src_idx, nested=True, ktol=1e-9, full_u=True, decim=1, method
 
 
 BIG = {"cfg1": 4, "cfg2": 8, "cfg3": 8, "cfg4": 8, "cfg5": 12}  # wavefield decimation
+
+
+_FORK = {}
+
+
+def _fork_solve(job):
+    prob, s, name, decim, tdec = _FORK["prob"], _FORK["s"], _FORK["name"], _FORK["decim"], _FORK["tdec"]
+    out = run_case(prob, job, full_u=decim == 1, decim=decim, solver=s, traces=True, trace_decim=tdec)
+    out["offline_s"] = _FORK["offline_s"]
+    np.savez_compressed(os.path.join(HERE, f"{name}_s{job}.npz"), **out)
+    return job
+
+
+def sources(name, idx, decim=None, tdec=1):
+    """Per-source fixtures ``<name>_s<k>.npz`` of one config: the reference is built once (offline), then
+    the sources are solved in forked processes (the factors are shared copy-on-write and read-only)."""
+    import multiprocessing as mp
+
+    prob = make_config(name)
+    t0 = time.time()
+    s = ref_solver(prob)
+    _FORK.update(prob=prob, s=s, name=name, decim=BIG[name] if decim is None else decim, tdec=tdec,
+                 offline_s=time.time() - t0)
+    print(f"{name}: offline {time.time() - t0:.1f}s; solving sources {idx}", flush=True)
+    with mp.get_context("fork").Pool(len(idx)) as pool:
+        for k in pool.imap_unordered(_fork_solve, idx):
+            print(f"{name} source {k} done", flush=True)
 
 
 def main(argv):
@@ -156,6 +187,17 @@ def main(argv):
             out = run_case(prob, 1 if name == "small_b" else 0, full_u=decim == 1, decim=decim,
                            method="bicgstab")
             np.savez_compressed(os.path.join(HERE, f"{name}_bicgstab.npz"), **out)
+        return
+    if argv and argv[0] == "sources":
+        # ``make_golden.py sources cfg3 21 42 63 [--decim D] [--tdec T]``: per-source fixtures of the
+        # many-RHS source sets (sie.py:392-439 solves each source independently)
+        rest = argv[1:]
+        opts = {}
+        while "--decim" in rest or "--tdec" in rest:
+            i = rest.index("--decim") if "--decim" in rest else rest.index("--tdec")
+            opts[rest[i][2:]] = int(rest[i + 1])
+            del rest[i:i + 2]
+        sources(rest[0], [int(x) for x in rest[1:]], decim=opts.get("decim"), tdec=opts.get("tdec", 1))
         return
     if argv:
         for name in argv:

@@ -50,7 +50,8 @@ def test_dump_offline_reference_format_and_reload(tmp_path):
     prob = _prob()
     layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=prob.Lc)
     key = cache_key(prob.model, prob.grid, prob.pml.omega, prob.partition)
-    dump_offline(layers, tmp_path, key)
+    dump_offline(layers, tmp_path, key, model=prob.model, grid=prob.grid, omega=prob.pml.omega,
+                 partition=prob.partition)
     # the Green blocks in GreenBlockSet.dump's format equal the oracle's blocks (green.py:103-129)
     orc = OracleSolver.from_problem(prob)
     for ell, lay in enumerate(orc.outer.slabs):
@@ -74,6 +75,18 @@ def test_dump_offline_reference_format_and_reload(tmp_path):
     other = small_problem(nx=40, nz=36, npml=6, L=3, Lc=2, omega=14.0, seed=0)
     with pytest.raises(ValueError):
         load_offline(tmp_path, key, other.grid, other.partition)
+    # same grid and partition, another frequency or velocity model: rejected
+    with pytest.raises(ValueError, match="omega"):
+        load_offline(tmp_path, key, prob.grid, prob.partition, omega=prob.pml.omega * 1.5)
+    from paper_1510_01831_b200.discretization import VelocityModel
+
+    slower = VelocityModel(prob.grid, prob.model.c * 0.9)
+    with pytest.raises(ValueError, match="another model"):
+        load_offline(tmp_path, key, prob.grid, prob.partition, model=slower)
+    ok = load_offline(tmp_path, key, prob.grid, prob.partition, model=prob.model, omega=prob.pml.omega)
+    assert ok.factors.omega == prob.pml.omega
+    # the factor file holds tensors and plain values only: it loads without unpickling code
+    torch.load(tmp_path / f"factors_{key}.pt", weights_only=True)
 
 
 @pytest.mark.gpu

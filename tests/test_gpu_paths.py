@@ -45,13 +45,14 @@ SWITCHES = {
     "default": {},
     "k1-passes": {"PT_NO_Q0": "1", "PT_NO_GSMP": "1"},
     "item-programs": {"PT_NO_DENSE": "1"},
+    "item-programs-v1": {"PT_NO_DENSE": "1", "PT_ITEMS_V1": "1"},
     "cluster-dense": {"PT_NO_COOP": "1"},
     "cluster-items": {"PT_NO_DENSE": "1", "PT_NO_COOP": "1"},
     "separate-combine": {"PT_NO_FUSE_COMB": "1"},
     "inner-gather": {"PT_NO_RHS_OUT": "1"},
     "no-sstep": {"PT_NO_SSTEP": "1"},
     "pass0-segments": {"PT_P0_SEG": "1"},
-    "items-tile-prefetch": {"PT_NO_DENSE": "1", "PT_TPREFETCH": "1"},
+    "items-tile-prefetch": {"PT_NO_DENSE": "1", "PT_ITEMS_V1": "1", "PT_TPREFETCH": "1"},
     "fused-glue": {"PT_FUSE_GLUE": "1"},
     "fused-stage": {"PT_FUSE": "1"},
     "recon-k1": {"PT_NO_REUSE": "1"},
