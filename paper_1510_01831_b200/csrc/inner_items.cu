@@ -51,9 +51,16 @@ namespace cg = cooperative_groups;
 struct TileCfg {
   int mtc, ntc, wm, wn, kw;
 };
-// CTA tile shapes, largest first: MTC row tiles x NTC n-tiles; warps = (MTC/WM) x (NTC/WN) x KW = 8
-__device__ __constant__ TileCfg II_CFG[5] = {{8, 4, 2, 2, 1}, {4, 2, 1, 1, 1}, {2, 2, 1, 1, 2}, {2, 1, 1, 1, 4},
-                                             {1, 1, 1, 1, 8}};
+// CTA tile shapes: MTC row tiles x NTC n-tiles; warps = (MTC/WM) x (NTC/WN) x KW = 8.  2 x 2 warp blocks
+// wherever the tile allows (a warp product with one A and one B fragment per 4 DMMAs reaches only about half
+// of the DMMA rate: shared-memory fragment loads and DMMAs share the issue path; tools/chunk_mma_micro.cu).
+#define II_NCFG 7
+__device__ __constant__ TileCfg II_CFG[II_NCFG] = {{8, 4, 2, 2, 1}, {4, 4, 2, 2, 2}, {4, 2, 2, 2, 4}, {2, 2, 2, 2, 8},
+                                                   {4, 1, 2, 1, 4}, {2, 1, 2, 1, 8}, {1, 1, 1, 1, 8}};
+// relative DMMA issue rate of a warp block (measured: 2x2 0.23, 2x1 0.165, 1x1 0.12 DMMA/clk/SM)
+__device__ __forceinline__ float cfg_rate(const TileCfg& c) {
+  return c.wm * c.wn == 4 ? 0.23f : (c.wm * c.wn == 2 ? 0.165f : 0.12f);
+}
 
 // optional clock64 segment totals of CTA 0 (PT_INNER_TPROF): 0 phase setup, 1 chunk loop, 2 epilogue,
 // 3 program-phase grid barriers, 4 vector passes, 5 vector grid barriers, 6 init, 7 final, 8 phases, 9 tiles
@@ -98,8 +105,7 @@ struct IIShared {
   unsigned char act[II_MAXJ][II_MAXNT];     // active n-tile ids per job
   unsigned char amask[II_MAXJ][II_MAXNT];   // active instance bitmask per (job, n-tile)
   int jw[II_MAXJ], jlay[II_MAXJ], jjob[II_MAXJ];
-  long long jpre[II_MAXJ + 1];              // per-phase weight prefix over jobs
-  int tpre[5][II_MAXJ + 1];                 // per config: prefix over jobs of CTA tiles per item
+  int tpre[II_NCFG][II_MAXJ + 1];           // per config: prefix over jobs of CTA tiles per item
   unsigned char ins[II_MAXIT];              // slot count of every program item
   IItem items[II_MAXIT];                    // the op + pre programs (staged once)
   // vector-phase staging (aliases the program phases' reduction buffer): per instance of a (job, n-tile)
@@ -126,31 +132,17 @@ __device__ __forceinline__ void dmma4(double (&a)[8], double ar, double ai, doub
   dmma_f64(a[6], a[7], ai, br);
 }
 
-// ---------------------------------------------------------------------------------------- tile iterator
-// The CTA tiles of one phase, enumerated job-major, then item, then row-tile group, then n-tile group; tile
-// weight = the item's slot count (1 for a pure combination).  CTA b owns the tiles whose weight midpoints lie
-// in [b W / G, (b + 1) W / G).
-struct PhaseCtx {
-  int it0, nit;       // items of the phase
-  int cfg;            // TileCfg index
-  int witems;         // sum of item weights
-  long long lo2, hi2; // doubled weight range of this CTA
-};
-
-struct TileIt {
-  int jx, ii, t, tend;
-  long long bs;  // weight start of block (jx, ii)
-  int wi, ntile_blk;
-};
-
+// ---------------------------------------------------------------------------------------- tile enumeration
+// The CTA tiles of one phase are numbered item-major, then job, then row-tile group, then n-tile group, and dealt
+// round-robin to the CTAs (tile t -> CTA t mod G): every CTA gets a near-equal share of every item's tiles.
+// Decoding a number is a few 32-bit divisions and a binary search over the per-job prefix (no serial search
+// over the phase, no 64-bit division on the critical path after the grid barrier).
 __device__ __forceinline__ int item_ns_g(const IItem& it) {
   int ns = 0;
   if (it.cell >= 0)
     for (int s = 0; s < 4; ++s) ns += it.pan[s][0].vec >= 0;
   return ns;
 }
-
-__device__ __forceinline__ long long cdivll(long long a, long long b) { return a <= 0 ? -((-a) / b) : (a + b - 1) / b; }
 
 struct Geo {
   int nmtg, nntg;
@@ -160,55 +152,35 @@ __device__ __forceinline__ Geo job_geo(const IIShared& S, const TileCfg& c, int 
   return Geo{(nmt + c.mtc - 1) / c.mtc, (S.nact[jx] + c.ntc - 1) / c.ntc};
 }
 
-// position `it` on the first tile at or after block (jx, ii) whose midpoint lies in [lo2, hi2); false = done
-__device__ __noinline__ bool tile_seek(const InnerParams& p, const IIShared& S, const PhaseCtx& ph, const TileCfg& c, int J,
-                          TileIt& it) {
-  while (it.jx < J) {
-    const Geo g = job_geo(S, c, it.jx);
-    const int nb = g.nmtg * g.nntg;
-    if (2 * S.jpre[it.jx] >= ph.hi2) return false;
-    if (nb == 0 || 2 * S.jpre[it.jx + 1] <= ph.lo2) {
-      ++it.jx;
-      it.ii = 0;
-      it.bs = S.jpre[it.jx];
-      continue;
-    }
-    while (it.ii < ph.nit) {
-      const int ns = S.ins[ph.it0 + it.ii];
-      const int wi = ns > 0 ? ns : 1;
-      const long long blk = (long long)wi * nb;
-      const long long t0 = max(0LL, cdivll(ph.lo2 - 2 * it.bs - wi, 2LL * wi));
-      const long long t1 = min((long long)nb, cdivll(ph.hi2 - 2 * it.bs - wi, 2LL * wi));
-      if (t0 < t1) {
-        it.t = (int)t0;
-        it.tend = (int)t1;
-        it.wi = wi;
-        it.ntile_blk = nb;
-        return true;
-      }
-      if (2 * it.bs >= ph.hi2) return false;
-      it.bs += blk;
-      ++it.ii;
-    }
-    ++it.jx;
-    it.ii = 0;
-    it.bs = S.jpre[it.jx];
+struct TileRef {
+  int jx, ii, mtg, ntg;  // job, item (phase-local), row-tile group, n-tile group
+};
+__device__ __forceinline__ TileRef tile_decode(const IIShared& S, int cfg, int J, int t) {
+  const int tpi = S.tpre[cfg][J];
+  TileRef r;
+  r.ii = t / tpi;
+  int rem = t - r.ii * tpi;
+  int lo = 0, hi = J - 1;  // last job whose prefix <= rem
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (S.tpre[cfg][mid] <= rem) lo = mid;
+    else hi = mid - 1;
   }
-  return false;
-}
-
-__device__ __forceinline__ bool tile_next(const InnerParams& p, const IIShared& S, const PhaseCtx& ph,
-                                          const TileCfg& c, int J, TileIt& it) {
-  if (++it.t < it.tend) return true;
-  it.bs += (long long)it.wi * it.ntile_blk;
-  ++it.ii;
-  return tile_seek(p, S, ph, c, J, it);
+  r.jx = lo;
+  rem -= S.tpre[cfg][lo];
+  const int nntg = (S.nact[lo] + II_CFG[cfg].ntc - 1) / II_CFG[cfg].ntc;
+  r.mtg = rem / nntg;
+  r.ntg = rem - r.mtg * nntg;
+  return r;
 }
 
 // ---------------------------------------------------------------------------------------- tiles and chunks
 // K rows per chunk by config: narrow chunks for the big (throughput) tiles, whole slots for the small (latency)
 // tiles so a tile is a handful of chunks.  A ring slot holds A [MTC][KC][8] then B [NTC][2 terms][KC][8].
-__device__ __forceinline__ int cfg_kc(int cfg) { return cfg <= 1 ? 32 : (cfg == 2 ? 64 : 128); }
+__device__ __forceinline__ int cfg_kc(const TileCfg& c) {  // the widest chunk whose ring slot stays <= 48 KB
+  const int per = 128 * (c.mtc + 2 * c.ntc);              // bytes per K row
+  return per * 128 <= 48 * 1024 ? 128 : (per * 64 <= 48 * 1024 ? 64 : 32);
+}
 __device__ __forceinline__ uint32_t slot_elems(const TileCfg& c, int kc) { return (uint32_t)kc * 8u * (c.mtc + 2 * c.ntc); }
 
 // Everything a tile's chunks need, derived once per tile (warp-uniform values).
@@ -220,19 +192,17 @@ struct TileDesc {
 };
 
 __device__ __forceinline__ TileDesc tile_desc(const InnerParams& p, const IIShared& S, const TileCfg& c, int kc,
-                                              const TileIt& it, int it0) {
+                                              const TileRef& r, int it0) {
   TileDesc d;
-  d.jx = it.jx;
-  d.job = S.jjob[it.jx];
-  d.w = S.jw[it.jx];
+  d.jx = r.jx;
+  d.job = S.jjob[r.jx];
+  d.w = S.jw[r.jx];
   d.nmt = (d.w + 7) >> 3;
-  d.ii = it0 + it.ii;
-  const Geo g = job_geo(S, c, it.jx);
-  const int mtg = it.t / g.nntg, ntg = it.t - mtg * g.nntg;
-  d.mt0 = mtg * c.mtc;
-  d.nt0 = ntg * c.ntc;
+  d.ii = it0 + r.ii;
+  d.mt0 = r.mtg * c.mtc;
+  d.nt0 = r.ntg * c.ntc;
   d.mvalid = min(c.mtc, d.nmt - d.mt0);
-  d.nvalid = min(c.ntc, S.nact[it.jx] - d.nt0);
+  d.nvalid = min(c.ntc, S.nact[r.jx] - d.nt0);
   d.ns = S.ins[d.ii];
   d.nkc = (d.w + kc - 1) / kc;
   const IItem& item = S.items[d.ii];
@@ -339,45 +309,45 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
                                        IITrace& X) {
   const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, b = blockIdx.x;
-  // ---- config: the largest tile shape that still gives every CTA work (>= G tiles), else the smallest
-  int cfg = 4;
-  for (int ci = 0; ci < 5; ++ci)
-    if ((long long)S.tpre[ci][J] * nit >= G) {
-      cfg = ci;
-      break;
+  // ---- config: minimise (tile rounds) x (cycles of one tile at its warp block's DMMA rate + a fixed per-tile cost)
+  int cfg = II_NCFG - 1;
+  {
+    const float ksteps = (float)wphase / (float)max(nit, 1) * (float)((p.wmax + 3) >> 2);
+    float best = 3.4e38f;
+    for (int ci = 0; ci < II_NCFG; ++ci) {
+      const TileCfg cc = II_CFG[ci];
+      const int tiles = S.tpre[ci][J] * nit;
+      const int rounds = (tiles + G - 1) / G;
+      const float t = (float)rounds * ((float)(cc.mtc * cc.ntc) * ksteps * 4.0f / cfg_rate(cc) + 3000.0f);
+      if (tiles > 0 && t < best) {
+        best = t;
+        cfg = ci;
+      }
     }
+  }
+  X.ev(20, cfg);
   const TileCfg c = II_CFG[cfg];
-  const int kc = cfg_kc(cfg), ksn = kc / 4;
-  const int witems = wphase;
-  __syncthreads();
-  if (tid == 0)
-    for (int jx = 0; jx <= J; ++jx) S.jpre[jx] = (long long)S.tpre[cfg][jx] * witems;
-  __syncthreads();
-  const long long W = S.jpre[J];
-  PhaseCtx ph{it0, nit, cfg, witems, 2 * ((long long)b * W / G), 2 * ((long long)(b + 1) * W / G)};
+  const int kc = cfg_kc(c), ksn = kc / 4;
+  const int ntiles = S.tpre[cfg][J] * nit;
   const uint32_t se = slot_elems(c, kc);
   const int nslot = min(II_NSLOT, (int)(II_RING / (se * 16u)));
   // the B panels were written by other CTAs (generic proxy) before the grid barrier; order those writes
   // before this CTA's bulk (async-proxy) reads
   if (wp == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-  TileIt it{0, 0, 0, 0, 0, 0, 0};
-  bool live = tile_seek(p, S, ph, c, J, it);
-  // producer state (warp 0, warp-uniform): tile iterator, its descriptor, chunk position
-  TileIt pit = it;
-  bool plive = live;
-  int psi = 0, pkc = 0;
+  // producer state (warp 0, warp-uniform): its tile number, descriptor and chunk position
+  int pt = b, psi = 0, pkc = 0;
   TileDesc pd;
   if (wp == 0) {
-    while (plive && S.ins[it0 + pit.ii] == 0) plive = tile_next(p, S, ph, c, J, pit);
-    if (plive) pd = tile_desc(p, S, c, kc, pit, it0);
+    while (pt < ntiles && S.ins[it0 + tile_decode(S, cfg, J, pt).ii] == 0) pt += G;
+    if (pt < ntiles) pd = tile_desc(p, S, c, kc, tile_decode(S, cfg, J, pt), it0);
   }
   int issued = 0, done = 0;
   auto try_issue = [&](bool block) -> bool {  // warp 0: the next chunk, if its slot is free (or once it is)
-    if (!plive) return false;
+    if (pt >= ntiles) return false;
     const int slot = issued % nslot;
     bool ok = true;
     if (lane == 0) {
-      if (block) mbar_wait(&S.empty[slot], (rg.epar >> slot) & 1u);
+      if (block) mbar_wait_suspend(&S.empty[slot], (rg.epar >> slot) & 1u);
       else ok = mbar_test(&S.empty[slot], (rg.epar >> slot) & 1u);
     }
     ok = __shfl_sync(0xffffffffu, ok, 0);
@@ -391,9 +361,9 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
       if (++psi == pd.ns) {
         psi = 0;
         do {
-          plive = tile_next(p, S, ph, c, J, pit);
-        } while (plive && S.ins[it0 + pit.ii] == 0);
-        if (plive) pd = tile_desc(p, S, c, kc, pit, it0);
+          pt += G;
+        } while (pt < ntiles && S.ins[it0 + tile_decode(S, cfg, J, pt).ii] == 0);
+        if (pt < ntiles) pd = tile_desc(p, S, c, kc, tile_decode(S, cfg, J, pt), it0);
       }
     }
     return true;
@@ -407,12 +377,33 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
   const int kp = wp / wpk, wq = wp - kp * wpk;
   const int wmi = wq % (c.mtc / c.wm), wni = wq / (c.mtc / c.wm);
   const int ks0 = kp * ksn / c.kw, ks1 = (kp + 1) * ksn / c.kw;
-  while (live) {
-    X.ev(5, it.ii * 1000 + it.t);
+  for (int t = b; t < ntiles; t += G) {
+    X.ev(5, t);
     T.count(9);
     if (p.tprof && tid == 0 && b < 1024) atomicAdd(&g_ii_tiles[b], 1ULL);
-    const TileDesc d = tile_desc(p, S, c, kc, it, it0);
+    const TileDesc d = tile_desc(p, S, c, kc, tile_decode(S, cfg, J, t), it0);
     const IItem& item = S.items[d.ii];
+    const int npair = c.mtc * c.ntc;
+    // combine operands of this thread's first output, fetched before the products (one output per thread covers
+    // the small tiles of the latency-bound phases; larger tiles load theirs in the epilogue)
+    const int o0 = tid, pr0 = o0 >> 6, pos0 = o0 & 63;
+    const int ml0 = pr0 / c.ntc, nl0 = pr0 - ml0 * c.ntc, grow0 = (d.mt0 + ml0) * 8 + (pos0 >> 3);
+    const bool own0 = o0 < npair * 64 && ml0 < d.mvalid && nl0 < d.nvalid && grow0 < d.w;
+    const int mode = item.flags >> 8 & 3;
+    double2 pre_add = czero(), pre_sub = czero(), pre_rev = czero();
+    if (own0) {
+      const int nt = S.act[d.jx][d.nt0 + nl0], q = pos0 & 7;
+      auto opnd = [&](Ref r) { return ld_cg(v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + grow0) * 8 + q); };
+      if (item.add[0].vec >= 0) {
+        pre_add = opnd(item.add[0]);
+        if (item.add[1].vec >= 0) pre_add = cadd(pre_add, opnd(item.add[1]));
+      }
+      if (item.sub[0].vec >= 0) {
+        pre_sub = opnd(item.sub[0]);
+        if (item.sub[1].vec >= 0) pre_sub = cadd(pre_sub, opnd(item.sub[1]));
+      }
+      if (mode != 0) pre_rev = opnd(item.rev);
+    }
     double acc[2][2][8];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -427,7 +418,7 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
         if (wp == 0)
           while (issued <= done) try_issue(true);  // the chunk about to be consumed must be in flight
         const int slot = done % nslot;
-        mbar_wait(&S.full[slot], (rg.fpar >> slot) & 1u);
+        mbar_wait_suspend(&S.full[slot], (rg.fpar >> slot) & 1u);
         rg.fpar ^= 1u << slot;
         X.ev(3, done);
         const double2* A = ring + (size_t)slot * se;
@@ -446,7 +437,6 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
     }
     T.tick(1);
     // ---- partial tiles -> shared memory: red[kp][pair][row * 8 + col], pair = mtl * NTC + ntl
-    const int npair = c.mtc * c.ntc;
     if (d.ns > 0) {
       const int r8 = lane >> 2, cq = 2 * (lane & 3);
 #pragma unroll
@@ -463,7 +453,6 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
     }
     __syncthreads();
     // ---- combine: t = y + (add0 + add1) - (sub0 + sub1); dst = t | rev - t | t - rev
-    const int mode = item.flags >> 8 & 3;
     for (int o = tid; o < npair * 64; o += II_T) {
       const int pr = o >> 6, pos = o & 63, row = pos >> 3, q = pos & 7;
       const int ml = pr / c.ntc, nl = pr - ml * c.ntc;
@@ -473,25 +462,29 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
       double2 y = czero();
       if (d.ns > 0)
         for (int k = 0; k < c.kw; ++k) y = cadd(y, red[((size_t)k * npair + pr) * 64 + pos]);
-      auto opnd = [&](Ref r) { return ld_cg(v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + grow) * 8 + q); };
-      if (item.add[0].vec >= 0) {
-        double2 av = opnd(item.add[0]);
-        if (item.add[1].vec >= 0) av = cadd(av, opnd(item.add[1]));
-        y = cadd(y, av);
+      double2 av = pre_add, sv = pre_sub, rv = pre_rev;
+      if (o != o0) {
+        auto opnd = [&](Ref r) { return ld_cg(v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + grow) * 8 + q); };
+        av = sv = rv = czero();
+        if (item.add[0].vec >= 0) {
+          av = opnd(item.add[0]);
+          if (item.add[1].vec >= 0) av = cadd(av, opnd(item.add[1]));
+        }
+        if (item.sub[0].vec >= 0) {
+          sv = opnd(item.sub[0]);
+          if (item.sub[1].vec >= 0) sv = cadd(sv, opnd(item.sub[1]));
+        }
+        if (mode != 0) rv = opnd(item.rev);
       }
-      if (item.sub[0].vec >= 0) {
-        double2 sv = opnd(item.sub[0]);
-        if (item.sub[1].vec >= 0) sv = cadd(sv, opnd(item.sub[1]));
-        y = csub(y, sv);
-      }
-      if (mode == 1) y = csub(opnd(item.rev), y);
-      else if (mode == 2) y = csub(y, opnd(item.rev));
+      if (item.add[0].vec >= 0) y = cadd(y, av);
+      if (item.sub[0].vec >= 0) y = csub(y, sv);
+      if (mode == 1) y = csub(rv, y);
+      else if (mode == 2) y = csub(y, rv);
       v2p(p, d.job, vmap[item.dst.vec], nt)[((size_t)item.dst.seg * d.w + grow) * 8 + q] = y;
     }
     __syncthreads();  // red is reused by the next tile
     X.ev(6, 0);
     T.tick(2);
-    live = tile_next(p, S, ph, c, J, it);
   }
 }
 
@@ -797,7 +790,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
         any |= na;
       }
       S.any_active = any;
-      for (int ci = 0; ci < 5; ++ci) {
+      for (int ci = 0; ci < II_NCFG; ++ci) {
         int acc = 0;
         for (int jx = 0; jx < J; ++jx) {
           S.tpre[ci][jx] = acc;
@@ -1055,10 +1048,10 @@ cudaError_t inner_items_launch(const InnerParams& p0, int J, cudaStream_t st) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   static const bool v1 = std::getenv("PT_ITEMS_V1") != nullptr;  // the per-8-RHS-unit kernel instead
-  // stages with fewer jobs (the sequential sweep stages) keep the per-8-RHS-unit kernel by default: its
-  // per-phase latency is lower there (PT_ITEMS_MINJ=1 selects this kernel for every stage)
-  static const int minj = std::getenv("PT_ITEMS_MINJ") ? atoi(std::getenv("PT_ITEMS_MINJ")) : 2;
-  if (v1 || J < minj || p0.dense || !p0.part || J < 1 || J > II_MAXJ || p0.R > II_MAXNT * 8 || p0.cap > 32 || p0.Lc < 2 ||
+  // a single-job stage with one n-tile of RHS (a 1-RHS sweep stage) keeps the per-8-RHS-unit kernel by
+  // default: its per-phase latency is lower there (PT_ITEMS_ALL=1 selects this kernel for every stage)
+  static const bool all = std::getenv("PT_ITEMS_ALL") != nullptr;
+  if (v1 || (!all && J < 2 && p0.R <= 8) || p0.dense || !p0.part || J < 1 || J > II_MAXJ || p0.R > II_MAXNT * 8 || p0.cap > 32 || p0.Lc < 2 ||
       p0.nitems > II_MAXIT || p0.op_nph + p0.pre_nph > II_MAXPH ||
       p0.part_items < inner_items_part_items(nsm, J, p0.R))
     return cudaErrorNotSupported;
