@@ -1,26 +1,29 @@
 #!/usr/bin/env python
-"""Benchmark: online stage of the nested polarized-traces solver on one B200 per rank.
+"""Benchmark: the online stage of the nested polarized-traces solver on one B200 per rank.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg5] [--nrhs R]
 
-A step is one online solve of the config's whole source set (config 2 =
-BASELINE.json configs[1]: 400x400 Gaussian lens, L=8, Lc=4, 16 point sources),
-batched through ``pt_solve_device`` with sources and wavefields resident in HBM
-(``value``), and through the public API with pinned host buffers, H2D/D2H
-inside the timed region (``e2e``).  One process per GPU (torchrun for N>1);
-each rank solves its own copy of the source set (weak scaling, no collective
-on the data path); the step time is the max over ranks.
+Headline (default): BASELINE.json configs[4] ("cfg5"), the largest single-GPU config: 3000 x 3000 interior nodes
++ 16-point PML (9.2 M unknowns), L = 32 layers, Lc = 16 cells, its 64 surface point sources solved as ONE
+lockstep batch per step (the many-RHS, FP64-tensor regime of the north star).  ``value`` is solves/s with the
+sources and wavefields resident in HBM (``pt_solve_device`` on torch's stream, CUDA events); ``e2e`` is the
+same metric through the public ``solve_many`` with pinned host buffers, the 2 x 9.4 GB of host<->device copies
+inside the timed region.  Beside it: ``regimes.cfg5_1rhs`` (the HBM / latency regime, one source per solve)
+and ``regimes.cfg2_16rhs`` (round 1's line, kept for continuity).
 
-Roofline: the dominant kernel is K1 (cell solves).  Its algorithmic work is
-SURVEY.md 8(d)'s ``32 wz_c w_c^2`` bytes of Schur inverse per cell solve per
-RHS (flops = bytes/2).  With 16 RHS batched per stage the factor bytes are
-shared across RHS, so the bound is the FP64 pipe: achieved FLOP/s of K1 over
-its summed CUDA-event time in the timed region, against the measured FP64
-peak (profiles/fp64_peak.json, measured on the B200 by tools/fp64_peak.cu).
+Roofline: the kernel class with the largest share of the step (from a profiled pass with CUDA events around
+every launch) against its own executed work: flops = 8 per complex multiply-add the kernels perform (the inner
+GMRES: the reference's TouchCounter total x 8), over that class's device time, against the FP64 tensor peak
+(many RHS) -- or operator bytes streamed over time against the HBM peak (1 RHS).  ``reference_equivalent``
+is SURVEY.md 8(d)'s count of the reference's SuperLU + Green-block work, a throughput figure, NOT a hardware
+fraction (the device path does a restructured, smaller amount of work).
 
-``--impl reference`` times the CPU oracle port (oracle/, the reference's
-algorithm on SuperLU + BLAS) on the host cores: offline once, then each step
-solves a sample of the sources in forked worker processes (one per core).
+CPU legs (the oracle port: the reference's algorithm on SuperLU + BLAS; oracle/ is test infrastructure):
+cfg1/cfg2 solve whole sources.  For the large configs a whole source takes minutes to hours on the CPU, so the
+sample is a layer solve (NestedLayerSolver.solve, nested.py:344-353) on one middle layer built by the oracle,
+and the per-source time is that layer-solve time x the reference's layer-solve count per source
+(2L + (3L-5) + k(5L-7), k = the reference's outer iterations from the committed fixture).
+``--impl reference`` runs that sample in one forked worker per host core.
 """
 
 from __future__ import annotations
@@ -42,8 +45,9 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-METRIC = "online solves/s (complex128 nested polarized-traces solve, whole source set)"
+METRIC = "online solves/s (complex128 nested polarized-traces solve of the config's source set)"
 UNIT = "solves/s"
+SMALL = ("cfg1", "cfg2")  # configs whose whole sources fit the CPU legs' time budget
 
 
 def _env_rank():
@@ -52,33 +56,44 @@ def _env_rank():
 
 
 def _peaks():
-    out = {"hbm_gbs": 6536.4, "hbm_src": "fallback"}
+    out = {"hbm_gbs": 6536.4, "hbm_src": "fallback (B200_PROFILING.md)"}
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
             mp = json.load(fh)
         out["hbm_gbs"] = float(mp["hbm_gbs"])
         out["hbm_src"] = "measured (MEASURED_PEAKS.json)"
-        out["sm_max_mhz"] = float(mp.get("sm_max_mhz", 1965.0))
     except Exception:
         pass
     try:
         with open(os.path.join(REPO, "profiles", "fp64_peak.json")) as fh:
             fp = json.load(fh)
         out["fp64_tflops"] = float(max(fp["dfma_tflops"], fp["dmma_tflops"]))
-        out["fp64_src"] = "measured on B200 (profiles/fp64_peak.json)"
+        out["fp64_src"] = ("measured on a B200 by tools/fp64_peak.cu (profiles/fp64_peak.json); "
+                           "MEASURED_PEAKS.json has no FP64 figure")
     except Exception:
         out["fp64_tflops"] = 40.0
-        out["fp64_src"] = "nominal B200 FP64 (no measurement found)"
+        out["fp64_src"] = "nominal B200 FP64 tensor (no measurement found)"
     return out
 
 
-def _inner_traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture, or None."""
+def _traffic(name):
+    """DRAM bytes per launch of a kernel class from a committed ncu capture (profiles/r02_traffic.json)."""
     try:
-        with open(os.path.join(REPO, "profiles", "r01_inner_traffic.json")) as fh:
-            return float(json.load(fh)["dram_bytes_per_launch"])
+        with open(os.path.join(REPO, "profiles", "r02_traffic.json")) as fh:
+            return json.load(fh).get(name)
     except Exception:
         return None
+
+
+def layer_solves_per_source(L, k):
+    """2L (rhs + reconstruct) + (3L - 5) (initial preconditioner) + k (5L - 7)."""
+    return 2 * L + (3 * L - 5) + k * (5 * L - 7)
+
+
+def reference_iterations(cfg_name):
+    """The reference's own outer GMRES iterations for source 0 (committed live-reference fixture)."""
+    g = np.load(os.path.join(REPO, "tests", "golden", f"{cfg_name}.npz"))
+    return int(round(float(g["iterations"])))
 
 
 class ClockSampler:
@@ -184,38 +199,56 @@ class ClockSampler:
                 "source": "nvml (10 ms)" if self.nvml is not None else "nvidia-smi (200 ms)"}
 
 
-def _cpu_baseline_sample(cfg_name, n_src, threads):
-    """Run the oracle on a bounded sample in a subprocess with `threads` BLAS threads."""
-    code = f"""
+
+
+# ----------------------------------------------------------------------------- CPU legs (oracle port)
+
+_LAYER_CODE = r"""
 import sys, time, json
-sys.path.insert(0, {REPO!r})
-from oracle.polartraces_oracle import OracleSolver
+sys.path.insert(0, {repo!r})
+import numpy as np
+from oracle.polartraces_oracle import NestedLayer, OracleSolver, _offsets
 from paper_1510_01831_b200.configs import make_config
-prob = make_config({cfg_name!r})
-t0 = time.time(); s = OracleSolver.from_problem(prob); t1 = time.time()
-F = prob.rhs(list(range({n_src})))
-t2 = time.time()
-for f in F:
-    s.solve(f, ktol=prob.ktol, max_iter=prob.max_iter)
-t3 = time.time()
-print(json.dumps({{"offline_s": t1 - t0, "solve_s": t3 - t2}}))
+prob = make_config({cfg!r})
+g = prob.grid
+if {whole}:
+    t0 = time.time(); s = OracleSolver.from_problem(prob); t1 = time.time()
+    F = prob.rhs(list(range({n})))
+    t2 = time.time()
+    its = [s.solve(f, ktol=prob.ktol, max_iter=prob.max_iter).iterations for f in F]
+    print(json.dumps({{"offline_s": t1 - t0, "unit_s": (time.time() - t2) / len(F), "its": its}}))
+else:
+    ext = prob.partition.extents
+    ell = len(ext) // 2
+    n, off = ext[ell], _offsets(tuple(ext))[ell]
+    t0 = time.time()
+    lay = NestedLayer(g.nx, n, g.h, g.npml, prob.model.c[off: off + n + 2 * g.npml, :], prob.pml.C,
+                      prob.pml.omega, prob.Lc, prob.inner_ktol, 200, "pt")
+    t1 = time.time()
+    f = np.zeros((n + 2 * g.npml, g.wx), dtype=complex)
+    f[g.npml + n // 2, g.wx // 2] = 1.0 / g.h ** 2  # a point source inside the layer (NEWTON-type solve)
+    ts = []
+    for _ in range({n}):
+        t = time.time(); lay.solve(f); ts.append(time.time() - t)
+    print(json.dumps({{"offline_s": t1 - t0, "unit_s": float(np.mean(ts)), "layer": ell}}))
 """
+
+
+def _cpu_sample(cfg_name, n, threads=1):
+    """Oracle sample in a subprocess with `threads` BLAS threads: whole sources (small configs) or layer solves."""
+    code = _LAYER_CODE.format(repo=REPO, cfg=cfg_name, whole=cfg_name in SMALL, n=n)
     env = dict(os.environ, OPENBLAS_NUM_THREADS=str(threads), OMP_NUM_THREADS=str(threads),
                MKL_NUM_THREADS=str(threads))
-    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                         timeout=900)
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=1200)
     if res.returncode != 0:
         raise RuntimeError(res.stderr[-2000:])
     return json.loads(res.stdout.strip().splitlines()[-1])
 
 
-# ----------------------------------------------------------------------------- reference arm
-
 _REF = {}
 
 
 def _ref_init():
-    # one BLAS thread per worker process: numpy was initialised before the fork
     try:
         from threadpoolctl import threadpool_limits
 
@@ -224,70 +257,207 @@ def _ref_init():
         pass
 
 
-def _ref_worker(idx):
-    s, F, prob = _REF["s"], _REF["F"], _REF["prob"]
-    r = s.solve(F[idx], ktol=prob.ktol, max_iter=prob.max_iter)
-    return r.iterations
+def _ref_unit(idx):
+    """One unit of the reference arm: a whole source (small configs) or one layer solve (large configs)."""
+    if _REF["whole"]:
+        r = _REF["s"].solve(_REF["F"][idx % len(_REF["F"])], ktol=_REF["prob"].ktol, max_iter=_REF["prob"].max_iter)
+        return r.iterations
+    _REF["lay"].solve(_REF["f"])
+    return 0.0
 
 
 def run_reference(args):
+    """The reference's algorithm on the host cores (the oracle port, bitwise equal to the live reference on the
+    committed fixtures): every step runs one unit per core in forked workers."""
     rank, local, world = _env_rank()
     if rank != 0:
         return 0
     import multiprocessing as mp
 
-    from oracle.polartraces_oracle import OracleSolver
+    from oracle.polartraces_oracle import NestedLayer, OracleSolver, _offsets
     from paper_1510_01831_b200.configs import make_config
 
     prob = make_config(args.config)
+    g = prob.grid
+    whole = args.config in SMALL
     t0 = time.time()
-    s = OracleSolver.from_problem(prob)
+    if whole:
+        _REF.update(s=OracleSolver.from_problem(prob), F=prob.rhs(list(range(len(prob.sources)))))
+    else:
+        ext = prob.partition.extents
+        ell = len(ext) // 2
+        n, off = ext[ell], _offsets(tuple(ext))[ell]
+        lay = NestedLayer(g.nx, n, g.h, g.npml, prob.model.c[off: off + n + 2 * g.npml, :], prob.pml.C,
+                          prob.pml.omega, prob.Lc, prob.inner_ktol, 200, "pt")
+        f = np.zeros((n + 2 * g.npml, g.wx), dtype=complex)
+        f[g.npml + n // 2, g.wx // 2] = 1.0 / g.h ** 2
+        _REF.update(lay=lay, f=f)
+    _REF.update(whole=whole, prob=prob)
     offline = time.time() - t0
     cores = os.cpu_count() or 1
-    n_sample = min(len(prob.sources), cores)
-    _REF.update(s=s, F=prob.rhs(list(range(len(prob.sources)))), prob=prob)
+    n_units = min(len(prob.sources), cores) if whole else cores
     ctx = mp.get_context("fork")
     times = []
-    with ctx.Pool(n_sample, initializer=_ref_init) as pool:
+    with ctx.Pool(n_units, initializer=_ref_init) as pool:
         for step in range(args.warmup + args.steps):
             t = time.time()
-            its = pool.map(_ref_worker, [(step * n_sample + i) % len(prob.sources) for i in range(n_sample)])
+            pool.map(_ref_unit, [step * n_units + i for i in range(n_units)])
             dt = time.time() - t
             if step >= args.warmup:
                 times.append(dt)
-    ms = 1e3 * float(np.mean(times))
-    value = n_sample / (ms / 1e3)
+    step_s = float(np.mean(times))
+    if whole:
+        value = n_units / step_s
+        sample = (f"{n_units} of the {len(prob.sources)} {args.config} sources per step, one forked oracle process "
+                  f"per core (OPENBLAS_NUM_THREADS=1); offline {offline:.1f}s untimed")
+    else:
+        k = reference_iterations(args.config)
+        nls = layer_solves_per_source(prob.partition.L, k)
+        value = n_units / (step_s * nls)
+        sample = (f"{n_units} layer solves per step (NestedLayerSolver.solve on layer {len(prob.partition.extents) // 2} "
+                  f"of {args.config}, one forked oracle process per core, OPENBLAS_NUM_THREADS=1), "
+                  f"{step_s:.3f}s per step; solves/s = cores / (step time x {nls} layer solves per source: "
+                  f"2L + (3L-5) + k(5L-7) with the reference's k = {k} outer iterations, SURVEY 3 EP1); "
+                  f"one-layer offline {offline:.1f}s untimed")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step_s, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": _config(args, prob),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": n_sample, "kind": "port",
-                         "sample": f"{n_sample} of the {len(prob.sources)} {args.config} sources per step, "
-                                   f"one forked oracle process per core (OPENBLAS_NUM_THREADS=1); "
-                                   f"offline {offline:.1f}s untimed; outer its {sorted(set(its))}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": n_units, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def _config(args, prob):
+def _config(args, prob, R=None):
     g = prob.grid
-    R = len(prob.sources) if getattr(args, "nrhs", 0) <= 0 else min(args.nrhs, len(prob.sources))
+    R = R if R is not None else (len(prob.sources) if getattr(args, "nrhs", 0) <= 0
+                                 else min(args.nrhs, len(prob.sources)))
     return {"workload": f"{args.config}: {g.nx}x{g.nz} interior + {g.npml}-pt PML, L={prob.partition.L}, "
                         f"Lc={prob.Lc}, {R} point sources batched per step",
-            "unknowns": g.nx * g.nz, "nrhs": R, "ktol": prob.ktol,
-            "inner_ktol": prob.inner_ktol, "preconditioner": "gs",
-            "inner_backend": getattr(args, "backend", "pt"),
-            "l2": "factor working set (Schur inverses) larger than the 126 MB L2; no explicit flush",
+            "unknowns": g.nx * g.nz, "nrhs": R, "ktol": prob.ktol, "inner_ktol": prob.inner_ktol,
+            "preconditioner": "gs", "inner_backend": getattr(args, "backend", "pt"),
+            "l2": "operator working set (GBs of factors) far above the 126 MB L2; no explicit flush",
             "parallelism": f"rhs-replica x{args.gpus}"}
 
 
 # ----------------------------------------------------------------------------- our arm
 
+_CLS = ["k1_cell_solve", "inner_gmres", "glue", "green_samples", "pass0_product"]
+
+
+def _kernels(st, ms_step, peaks):
+    """Per launch-class device time share and executed-work rates from one profiled solve."""
+    out = {}
+    for i, nm in enumerate(_CLS):
+        t = float(st["class_ms"][i])
+        if t <= 0:
+            continue
+        fl, by = float(st["class_flops"][i]), float(st["class_bytes"][i])
+        out[nm] = {"ms": t, "share_of_step": t / ms_step,
+                   "tflops": fl / (t * 1e-3) / 1e12 if fl > 0 else None,
+                   "fp64_frac": fl / (t * 1e-3) / 1e12 / peaks["fp64_tflops"] if fl > 0 else None,
+                   "operator_gbs": by / (t * 1e-3) / 1e9 if by > 0 else None,
+                   "hbm_frac": by / (t * 1e-3) / 1e9 / peaks["hbm_gbs"] if by > 0 else None}
+    return out
+
+
+def _reference_equivalent(solver, st, R, ms):
+    """the reference's SuperLU + Green-block work for this batch (its layer solves and touches)."""
+    F_ = solver.layers.factors
+    per_layer = [sum(64.0 * cf.wzc * cf.w * cf.w for cf in lf.cells) for lf in F_.layers]
+    alg = st["layer_solves"] * float(np.mean(per_layer)) + 16.0 * st["touches"]
+    return {"formula": "SURVEY 8(d): sum_l N_l sum_c 2*32*wz_c*w_c^2 B + 16 B per inner touch; flops = bytes/2",
+            "note": "throughput in the reference's own work units, not a hardware fraction",
+            "bytes_per_rhs": alg / R, "equiv_tflops": alg / 2.0 / (ms * 1e-3) / 1e12,
+            "equiv_gbs": alg / (ms * 1e-3) / 1e9}
+
+
+def _parity(name, idx, U):
+    """Relative L2 error of this run's wavefields against every committed live-reference fixture in the batch."""
+    out = {}
+    gdir = os.path.join(REPO, "tests", "golden")
+    for fn in sorted(os.listdir(gdir)):
+        if not fn.endswith(".npz"):
+            continue
+        stem = fn[:-4]
+        if stem == name:
+            k = 0
+        elif stem.startswith(name + "_s") and stem[len(name) + 2:].isdigit():
+            k = int(stem[len(name) + 2:])
+        else:
+            continue
+        if k not in idx:
+            continue
+        g = np.load(os.path.join(gdir, fn))
+        d = int(g["decim"])
+        u = U[idx.index(k)].cpu().numpy()[::d, ::d]
+        out[f"source_{k}"] = float(np.linalg.norm(u - g["u"]) / np.linalg.norm(g["u"]))
+    return out
+
+
+def _solver(prob, local, backend="pt"):
+    from paper_1510_01831_b200 import PolarizedTracesSolver, build_nested_layers
+
+    layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=prob.Lc,
+                                 inner_ktol=prob.inner_ktol, device=f"cuda:{local}", backend=backend)
+    return PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers, device=local)
+
+
+def _time_device(solver, F, U, R, cfg, steps, warmup, clocks=None):
+    """Device time per step (CUDA events on torch's stream, synchronize on both sides)."""
+    import ctypes
+
+    import torch
+
+    from paper_1510_01831_b200 import _abi
+
+    # the library runs on torch's current stream, where the events are recorded
+    _abi.lib().pt_set_stream(solver.ctx.handle, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    for _ in range(warmup):
+        solver.solve_device(F.data_ptr(), U.data_ptr(), R, cfg)
+    torch.cuda.synchronize()
+    launches = 0
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    res = None
+    with (clocks if clocks is not None else _Null()):
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()  # `ncu --profile-from-start off` sees the timed region only
+        e0.record(stream)
+        for _ in range(steps):
+            res = solver.solve_device(F.data_ptr(), U.data_ptr(), R, cfg)
+            launches += solver.last_stats["launches"]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+    return e0.elapsed_time(e1) / steps, launches, res
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+
+def _profiled(solver, F, U, R, cfg):
+    from paper_1510_01831_b200 import _abi
+
+    L = _abi.lib()
+    L.pt_set_profiling(solver.ctx.handle, 1)
+    solver.solve_device(F.data_ptr(), U.data_ptr(), R, cfg)
+    L.pt_set_profiling(solver.ctx.handle, 0)
+    return dict(solver.last_stats)
+
 
 def run_ours(args):
+    import ctypes
+
     import torch
 
     rank, local, world = _env_rank()
@@ -297,69 +467,39 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1510_01831_b200 import KrylovConfig, PolarizedTracesSolver, build_nested_layers
-    from paper_1510_01831_b200 import _abi
+    from paper_1510_01831_b200 import KrylovConfig, _abi
     from paper_1510_01831_b200.configs import make_config
 
+    peaks = _peaks()
     prob = make_config(args.config)
     t0 = time.time()
-    layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=prob.Lc,
-                                 inner_ktol=prob.inner_ktol, device=f"cuda:{local}", backend=args.backend)
-    solver = PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers,
-                                   device=local)
+    solver = _solver(prob, local, args.backend)
+    torch.cuda.synchronize()
     offline_s = time.time() - t0
     R = len(prob.sources) if args.nrhs <= 0 else min(args.nrhs, len(prob.sources))
-    Fh = prob.rhs(list(range(R)))
+    # each rank solves the config's whole source set (weak scaling by RHS, no collective on the data path); the
+    # source order is rotated per rank
+    idx = [(i + rank * 7) % len(prob.sources) for i in range(R)]
+    Fh = prob.rhs(idx)
     F = torch.from_numpy(Fh).to(f"cuda:{local}")
     U = torch.empty_like(F)
     cfg = KrylovConfig(ktol=prob.ktol, max_iter=prob.max_iter)
-    stream = torch.cuda.current_stream()
     L = _abi.lib()
-    L.pt_set_stream(solver.ctx.handle, C_void(stream.cuda_stream))
-
-    def step():
-        return solver.solve_device(F.data_ptr(), U.data_ptr(), R, cfg)
-
-    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
-        res = step()
-    torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    launches = 0
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        torch.cuda.profiler.start()  # `ncu --profile-from-start off` sees the timed region only
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            res = step()
-            launches += solver.last_stats["launches"]
-        e1.record(stream)
-        torch.cuda.synchronize()
-        torch.cuda.profiler.stop()
-    ms = e0.elapsed_time(e1) / args.steps
+    clk = ClockSampler(local)
+    ms, launches, res = _time_device(solver, F, U, R, cfg, args.steps, max(args.warmup, 1), clk)
     if dist:
         t = torch.tensor([ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    # per-launch-class device time from a separate profiled pass (CUDA events around every launch add
-    # overhead, so they stay out of the timed region); drives the roofline and the shares
-    L.pt_set_profiling(solver.ctx.handle, 1)
-    prof_steps = 2
-    cls_ms = np.zeros(5)
-    k1_bytes = dense_flops = prof_ms = 0.0
-    for _ in range(prof_steps):
-        step()
-        st = solver.last_stats
-        cls_ms += st["class_ms"]
-        k1_bytes += st["k1_bytes"]
-        dense_flops += st["dense_flops"]
-        prof_ms += st["device_ms"]
-    L.pt_set_profiling(solver.ctx.handle, 0)
     value = R * world / (ms / 1e3)
+    st = _profiled(solver, F, U, R, cfg)
+    parity = _parity(args.config, idx, U)
+    its = sorted({r.iterations for r in res})
 
-    # end to end through the public API: pinned host f in, host u out, copies inside the timed region
+    # end to end through the public API: pinned host f in, host u out, the copies inside the timed region
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
     Fp = torch.from_numpy(Fh).pin_memory()
     Up = torch.empty_like(Fp).pin_memory()
     L.pt_set_stream(solver.ctx.handle, None)
@@ -368,88 +508,77 @@ def run_ours(args):
     if dist:
         dist.barrier()
     t = time.perf_counter()
-    for _ in range(args.steps):
-        out = solver.solve_many(Fp.numpy(), cfg, out=Up.numpy())
-    e2e_ms = 1e3 * (time.perf_counter() - t) / args.steps
+    for _ in range(e2e_steps):
+        solver.solve_many(Fp.numpy(), cfg, out=Up.numpy())
+    torch.cuda.synchronize()
+    e2e_ms = 1e3 * (time.perf_counter() - t) / e2e_steps
     if dist:
         tt = torch.tensor([e2e_ms], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     e2e = R * world / (e2e_ms / 1e3)
     nbytes = int(Fh.nbytes)
+    del Fp, Up
 
-    # parity spot check of this run's wavefield against the committed reference fixture
-    parity = None
-    gpath = os.path.join(REPO, "tests", "golden",
-                         f"{args.config}{'' if args.backend == 'pt' else '_' + args.backend}.npz")
-    if os.path.exists(gpath):
-        g = np.load(gpath)
-        d = int(g["decim"])
-        u0 = U[0].cpu().numpy()[::d, ::d]
-        parity = float(np.linalg.norm(u0 - g["u"]) / np.linalg.norm(g["u"]))
+    kern = _kernels(st, st["device_ms"], peaks)
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    dk = kern[dom]
+    tensor = R >= 8
+    roof = {"kernel": dom, "bound": "tensor" if tensor else "hbm",
+            "unit": "TFLOP/s" if tensor else "GB/s",
+            "achieved": dk["tflops"] if tensor else dk["operator_gbs"],
+            "peak": peaks["fp64_tflops"] if tensor else peaks["hbm_gbs"],
+            "peak_src": peaks["fp64_src"] if tensor else peaks["hbm_src"],
+            "traffic": _traffic(dom),
+            "traffic_src": "profiles/r02_traffic.json: ncu dram__bytes_read.sum + dram__bytes_write.sum per launch",
+            "algorithmic": ("executed work of the class in one profiled solve: 8 flops per complex multiply-add "
+                            "(inner GMRES = the reference's TouchCounter total x 8) / its CUDA-event time"),
+            "profiled_ms_per_step": st["device_ms"]}
+    roof["frac"] = roof["achieved"] / roof["peak"] if roof["achieved"] else None
 
+    extras = {}
+    if world == 1 and not args.no_extras:
+        extras = _regimes(args, prob, solver, peaks)
+    solver.close()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return 0
-    peaks = _peaks()
-    names = ["k1_cell_solve", "inner_gmres", "glue", "green_samples", "pass0_product"]
-    k1_tf = (k1_bytes / 2.0) / (cls_ms[0] * 1e-3) / 1e12 if cls_ms[0] > 0 else 0.0
-    inner_tf = dense_flops / (cls_ms[1] * 1e-3) / 1e12 if cls_ms[1] > 0 else 0.0
-    dom = int(np.argmax(cls_ms[:2]))
-    achieved_tf = inner_tf if dom == 1 else k1_tf
-    its = sorted({r.iterations for r in res})
-    # SURVEY 8(d) algorithmic work of the reference's online solve for this batch: every layer solve is
-    # 2 cell solves per cell, each reading its Schur factors twice (2 x 32 wz_c w_c^2 B), plus 16 B per
-    # inner Green-block touch; layer solves and touches are this step's own counts (identical to the
-    # reference's), per-layer bytes averaged over the layers (their heights differ by at most one row)
-    st_last = solver.last_stats
-    F_ = layers.factors
-    per_layer = [sum(64.0 * cf.wzc * cf.w * cf.w for cf in lf.cells) for lf in F_.layers]
-    alg_bytes = st_last["layer_solves"] * float(np.mean(per_layer)) + 16.0 * st_last["touches"]
-    alg_gbs = alg_bytes / (ms * 1e-3) / 1e9
-    alg_tf = alg_bytes / 2.0 / (ms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded config generator, SURVEY 8(d))",
-        "config": _config(args, prob),
+        "config": _config(args, prob, R),
         "munknowns_rhs_per_s": value * prob.grid.nx * prob.grid.nz / 1e6,
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "steps": e2e_steps, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
-        "roofline": {
-            "kernel": names[dom], "bound": "tensor", "unit": "TFLOP/s",
-            "achieved": achieved_tf, "peak": peaks["fp64_tflops"],
-            "frac": achieved_tf / peaks["fp64_tflops"], "traffic": _inner_traffic(),
-            "traffic_src": "profiles/r01_inner_traffic.json: ncu dram__bytes_read+write per inner launch, averaged "
-                           "over the 57 inner launches of one solve (bytes per launch)",
-            "peak_src": peaks["fp64_src"],
-            "algorithmic": ("inner: 8 n^2 flops per instance per dense product (n = 4 (Lc-1) w), products = "
-                            "inner iterations + inner solves; K1: 32*wz_c*w_c^2 B per cell solve per RHS "
-                            "(SURVEY 8(d)), flops = bytes/2"),
-            "class_share_of_step": {nm: float(c / prof_steps / ms) for nm, c in zip(names, cls_ms)},
-            "k1_tflops": k1_tf, "inner_dense_tflops": inner_tf,
-            "profiled_ms_per_step": prof_ms / prof_steps,
-        },
-        "solve_roofline": {
-            "formula": "SURVEY 8(d): sum_l N_l sum_c 2*32*wz_c*w_c^2 B + 16 B per inner touch; flops = bytes/2",
-            "bytes_per_rhs": alg_bytes / R, "achieved_gbs": alg_gbs, "hbm_peak_gbs": peaks["hbm_gbs"],
-            "hbm_frac": alg_gbs / peaks["hbm_gbs"], "achieved_tflops": alg_tf,
-            "fp64_peak_tflops": peaks["fp64_tflops"], "fp64_frac": alg_tf / peaks["fp64_tflops"],
-            "regime": "1 RHS: HBM bound" if R == 1 else f"{R} RHS per step: FP64 tensor bound",
-        },
+        "roofline": roof,
+        "kernels": kern,
+        "reference_equivalent": _reference_equivalent(solver, st, R, st["device_ms"]),
         "clocks": clk.summary(),
         "outer_iterations": its,
-        "parity_vs_reference_fixture": parity,
+        "parity_vs_reference_fixtures": parity,
         "offline_s": offline_s,
     }
+    line.update(extras)
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cb = _cpu_baseline_sample(args.config, 1, 1)
-            line["cpu_baseline"] = {"value": 1.0 / cb["solve_s"], "unit": UNIT, "cores": 1, "kind": "port",
-                                    "sample": f"1 {args.config} source solved by the oracle port "
-                                              f"(single process, OPENBLAS_NUM_THREADS=1, offline "
-                                              f"{cb['offline_s']:.1f}s untimed)"}
+            n = 2 if args.config not in SMALL else 1
+            cb = _cpu_sample(args.config, n, 1)
+            if args.config in SMALL:
+                v = 1.0 / cb["unit_s"]
+                sample = (f"1 {args.config} source solved by the oracle port (single process, OPENBLAS_NUM_THREADS=1, "
+                          f"offline {cb['offline_s']:.1f}s untimed)")
+            else:
+                k = reference_iterations(args.config)
+                nls = layer_solves_per_source(prob.partition.L, k)
+                v = 1.0 / (cb["unit_s"] * nls)
+                sample = (f"{n} layer solves (NestedLayerSolver.solve, layer {cb['layer']} of {args.config}) by the "
+                          f"oracle port on 1 core, {cb['unit_s']:.3f}s each, x {nls} layer solves per source "
+                          f"(2L + (3L-5) + k(5L-7), reference k = {k}); one-layer offline {cb['offline_s']:.1f}s "
+                          f"untimed")
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
         except Exception as exc:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
                                     "sample": f"failed: {exc!s:.200}"}
@@ -459,20 +588,54 @@ def run_ours(args):
     return 0
 
 
-def C_void(x):
-    import ctypes
+def _regimes(args, prob, solver, peaks):
+    """The other north-star regimes, measured beside the headline (not the bench line's value)."""
+    import torch
 
-    return ctypes.c_void_p(x)
+    from paper_1510_01831_b200 import KrylovConfig
+    from paper_1510_01831_b200.configs import make_config
+
+    out = {}
+    cfg = KrylovConfig(ktol=prob.ktol, max_iter=prob.max_iter)
+    if args.config == "cfg5":  # 1 RHS: the HBM / latency regime on the same factors
+        F = torch.from_numpy(prob.rhs([0])).cuda()
+        U = torch.empty_like(F)
+        ms, _, res = _time_device(solver, F, U, 1, cfg, 2, 1)
+        st = _profiled(solver, F, U, 1, cfg)
+        kern = _kernels(st, st["device_ms"], peaks)
+        tot_bytes = float(np.sum(st["class_bytes"]))
+        out["cfg5_1rhs"] = {
+            "ms_per_solve": ms, "solves_per_s": 1e3 / ms,
+            "operator_bytes_per_solve": tot_bytes, "operator_gbs": tot_bytes / (ms * 1e-3) / 1e9,
+            "hbm_frac": tot_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "kernels": kern, "parity_vs_reference_fixtures": _parity("cfg5", [0], U),
+            "outer_iterations": [r.iterations for r in res]}
+        del F, U
+    if args.config != "cfg2":  # round 1's line for continuity
+        p2 = make_config("cfg2")
+        s2 = _solver(p2, torch.cuda.current_device())
+        R2 = len(p2.sources)
+        F = torch.from_numpy(p2.rhs(list(range(R2)))).cuda()
+        U = torch.empty_like(F)
+        ms, _, res = _time_device(s2, F, U, R2, KrylovConfig(ktol=p2.ktol, max_iter=p2.max_iter), max(5, args.steps), 3)
+        out["cfg2_16rhs"] = {"ms_per_step": ms, "solves_per_s": R2 / (ms / 1e3),
+                             "parity_vs_reference_fixtures": _parity("cfg2", list(range(R2)), U)}
+        s2.close()
+        del F, U
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the 1-RHS and cfg2 regime keys")
+    ap.add_argument("--e2e-steps", type=int, default=3, help="end-to-end steps (at most --steps)")
     ap.add_argument("--nrhs", type=int, default=0, help="solve the config's first N sources (0 = all)")
     ap.add_argument("--backend", default="pt", choices=["pt", "lu"],
                     help="inner backend (build_nested_layers backend=; the benchmark line uses 'pt')")

@@ -129,6 +129,11 @@ typedef struct {
   double* class_ms;          /* [5] device time per launch class: K1, inner GMRES, glue, sampled trace
                                 response, pass-0 product (profiling only) */
   double* dense_flops;       /* [1] algorithmic flops of the dense inner products: 8 n^2 per instance per product */
+  /* executed work per launch class (same classes as class_ms): flops = 8 per complex multiply-add the kernels
+   * perform (inner GMRES: the TouchCounter total x 8, or the dense products), bytes = the operator data the
+   * launches stream (Schur inverses, Green blocks, pass-0 and sampled-response operators) */
+  double* class_flops;       /* [5] */
+  double* class_bytes;       /* [5] */
 } pt_stats;
 
 int pt_create(const pt_problem* prob, int device, pt_ctx** out);

@@ -76,7 +76,7 @@ class PtStats(C.Structure):
         ("layer_solves", _llp), ("inner_iters", _llp), ("touches", _llp),
         ("inner_hist", _ip), ("inner_hist_len", C.c_int), ("timing_ms", _dp),
         ("kernel_ms", _dp), ("k1_bytes", _dp), ("launches", _llp), ("k1_launches", _llp),
-        ("class_ms", _dp), ("dense_flops", _dp),
+        ("class_ms", _dp), ("dense_flops", _dp), ("class_flops", _dp), ("class_bytes", _dp),
     ]
 
 

@@ -57,7 +57,11 @@ struct Stage {
     long long zsize = 0;
     int cm = 1;
     double bytes = 0.0;  // algorithmic S^-1 bytes of one pass: 32 wz_c w^2 per (cell, column)
+    double hbytes = 0.0; // S^-1 bytes one pass streams: 16 wz_c w^2 per task (a task serves its nq columns)
   };
+  // executed work of one launch per active RHS (flops) and the operator bytes it streams, per kernel class
+  bool work_ok = false;
+  double p0_fpr = 0, p0_bytes = 0, gs_fpr = 0, gs_bytes = 0, in_bytes = 0;
   std::map<int, Tasks> tasks;
 };
 
@@ -151,9 +155,11 @@ struct pt_ctx {
     cudaGraphExec_t exec = nullptr;
     long long d_layer_solves = 0, d_launches = 0, d_k1_launches = 0, d_touch = 0;
     double d_k1_bytes = 0.0;
+    double d_cf[5] = {0, 0, 0, 0, 0}, d_cb[5] = {0, 0, 0, 0, 0};
   };
   std::map<std::vector<long long>, GraphEnt> graphs;
   long long graphs_gen = -1;
+  double cls_flops[5] = {0, 0, 0, 0, 0}, cls_bytes[5] = {0, 0, 0, 0, 0};  // executed work per kernel class
   double2* ipart = nullptr;  // vector-phase partials of the whole-GPU item-program inner kernel
   long long ipart_items = 0;  // buffer generation the cached executables were captured against
   long long gen = 0;
@@ -667,6 +673,7 @@ static Stage::Tasks* stage_tasks(pt_ctx* c, Stage& S, int Ract) {
         t.zoff = z;
         z += (long long)cm * ci.wzc * ci.w * nc;
         T.bytes += 32.0 * ci.wzc * (double)ci.w * ci.w * t.nq;
+        T.hbytes += 16.0 * ci.wzc * (double)ci.w * ci.w;
         v.push_back(t);
       }
   }
@@ -753,6 +760,42 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   return ip;
 }
 
+// Executed work per launch class of a stage (per active RHS) and the operator bytes it streams:
+// pass-0 product 8 Mp (used slots x nk4) per (job, cell); sampled response 8 (kept rows x outputs) (slots x w) per
+// (job, cell); inner GMRES: the Green blocks of the stage's layers (16 blocks of w^2 per cell) -- its flops are
+// the device's TouchCounter total x 8, added at the end of the solve.
+static void stage_work(pt_ctx* c, Stage& S) {
+  if (S.work_ok) return;
+  S.work_ok = true;
+  std::vector<char> seen(c->L, 0);
+  for (size_t g = 0; g < S.lgrp.size(); ++g) {
+    const int l = S.lgrp[g].first, b = S.lgrp[g].second;
+    const int e = g + 1 < S.lgrp.size() ? S.lgrp[g + 1].second : (int)S.ljobs.size();
+    int used = 0;
+    for (int jj = b; jj < e; ++jj)
+      for (int sl = 0; sl < 4; ++sl) used |= (S.jobs[S.ljobs[jj]].pan[sl][0].vec >= 0) << sl;
+    const int nsl = __builtin_popcount(used);
+    for (int cc = 0; cc < c->Lc; ++cc) {
+      const CellInfo& ci = c->cel[l * c->Lc + cc];
+      const int nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3, Mp = (4 * ci.w + 4 * nk + 7) & ~7;
+      S.p0_fpr += 8.0 * Mp * nsl * nk4 * (e - b);
+      S.p0_bytes += 16.0 * Mp * nsl * nk4;
+      if (!seen[l]) S.in_bytes += 16.0 * 16.0 * ci.w * ci.w;
+    }
+    seen[l] = 1;
+  }
+  for (const OJob& jb : S.jobs) {
+    if (jb.nout <= 0) continue;
+    for (int cc = 0; cc < c->Lc; ++cc) {
+      const CellInfo& ci = c->cel[jb.layer * c->Lc + cc];
+      const double rows = (double)(ci.hi - ci.lo) * jb.nout;
+      const double K = (double)((ci.has_bot ? 4 : 2) - (ci.has_top ? 0 : 2)) * ci.w;
+      S.gs_fpr += 8.0 * rows * K;
+      S.gs_bytes += 16.0 * rows * K;
+    }
+  }
+}
+
 static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& io) {
   c->cur_tag = S.name;
   const int J = (int)S.jobs.size();
@@ -760,6 +803,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
   Stage::Tasks* T = stage_tasks(c, S, Ract);
   if (!T) return PT_CUDA_ERROR;
   if (ensure_z(c, T->zsize)) return PT_CUDA_ERROR;
+  stage_work(c, S);
   // optionally one cooperative launch for a whole sample-only stage without volume source (gather, pass-0
   // product, inner GMRES, sampled response, combine); falls back to the launch sequence below
   {
@@ -871,6 +915,13 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     static const bool no_rhs_out = std::getenv("PT_NO_RHS_OUT") != nullptr;
     const RhsOut ro{c->iscr, c->iscr_stride, (long long)(c->inner_cap + 1) * c->inmax};
     const bool rhs_out = !no_rhs_out && c->dense_d && !c->lu_d && (rpath || qpath);
+    if (rpath || qpath) {
+      c->cls_flops[4] += S.p0_fpr * Ract;
+      c->cls_bytes[4] += S.p0_bytes;
+    } else {
+      c->cls_flops[0] += T->bytes / 4.0;  // one complex MAC (8 flops) per S^-1 element per column
+      c->cls_bytes[0] += T->hbytes;
+    }
     if (rpath) {
       LaunchScope ls(c, 4);
       CK(cudaMemcpyAsync(c->tables, c->tables_f, sizeof(double2) * (size_t)J * c->Lc * 4 * Ract * c->wmax,
@@ -895,6 +946,7 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     }
     InnerParams ip = inner_params(c, S, Ract, io);
     ip.rhs_ready = rhs_out;
+    c->cls_bytes[1] += S.in_bytes;
     if (c->lu_d) {  // direct inner backend: one dense product per layer solve (nested.py:156-254)
       LaunchScope ls(c, 1);
       const int mmax = 2 * (c->Lc - 1) * c->wmax;
@@ -914,12 +966,16 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
     if (ip.tprof) inner_tprof_dump(S.name);
   }
   if (gpath) {
+    c->cls_flops[3] += S.gs_fpr * Ract;
+    c->cls_bytes[3] += S.gs_bytes;
     LaunchScope ls(c, 3);
     CK(green_samples_launch(S.jobs_d, J, c->cel_d, c->lay_d, c->gsmp_d, c->trc, c->smp, Ract, c->Lc, c->wx,
                             c->wmax, c->wzcmax, c->num_sms, c->st, fuse_comb ? &tab : nullptr, c->rmap_d));
   } else {
     kp.pass = 1;
     kp.s0 = 0;
+    c->cls_flops[0] += T->bytes / 4.0;
+    c->cls_bytes[0] += T->hbytes;
     LaunchScope ls(c, 0);
     CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
     c->k1_bytes += T->bytes;
@@ -1054,11 +1110,20 @@ static int graphed(pt_ctx* c, std::vector<long long> key, Body&& body) {
     c->launches += g.d_launches;
     c->k1_launches += g.d_k1_launches;
     c->k1_bytes += g.d_k1_bytes;
+    for (int i = 0; i < 5; ++i) {
+      c->cls_flops[i] += g.d_cf[i];
+      c->cls_bytes[i] += g.d_cb[i];
+    }
     return 0;
   }
   if (g.seen++ == 0) return body();
   const long long ls0 = c->layer_solves, la0 = c->launches, k10 = c->k1_launches, tx0 = c->touch_extra;
   const double kb0 = c->k1_bytes;
+  double cf0[5], cb0[5];
+  for (int i = 0; i < 5; ++i) {
+    cf0[i] = c->cls_flops[i];
+    cb0[i] = c->cls_bytes[i];
+  }
   const long long gen0 = c->gen;
   CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
   const int rc = body();  // records the launches (and advances the host counters by what they will do)
@@ -1077,6 +1142,10 @@ static int graphed(pt_ctx* c, std::vector<long long> key, Body&& body) {
     c->k1_launches = k10;
     c->k1_bytes = kb0;
     c->touch_extra = tx0;
+    for (int i = 0; i < 5; ++i) {
+      c->cls_flops[i] = cf0[i];
+      c->cls_bytes[i] = cb0[i];
+    }
     return body();
   }
   g.d_layer_solves = c->layer_solves - ls0;
@@ -1084,6 +1153,10 @@ static int graphed(pt_ctx* c, std::vector<long long> key, Body&& body) {
   g.d_launches = c->launches - la0;
   g.d_k1_launches = c->k1_launches - k10;
   g.d_k1_bytes = c->k1_bytes - kb0;
+  for (int i = 0; i < 5; ++i) {
+    g.d_cf[i] = c->cls_flops[i] - cf0[i];
+    g.d_cb[i] = c->cls_bytes[i] - cb0[i];
+  }
   CK(cudaGraphLaunch(g.exec, c->st));
   return 0;
 }
@@ -1284,6 +1357,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   c->touch_extra = 0;
   c->launches = c->k1_launches = 0;
   c->k1_bytes = 0.0;
+  for (int i = 0; i < 5; ++i) c->cls_flops[i] = c->cls_bytes[i] = 0.0;
   c->evs.clear();
   c->ev_next = 0;
   static const bool stage_prof = std::getenv("PT_STAGE_PROF") != nullptr;
@@ -1686,6 +1760,18 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
     }
     if (stats->launches) stats->launches[0] = c->launches;
     if (stats->k1_launches) stats->k1_launches[0] = c->k1_launches;
+    if (stats->class_flops) {
+      for (int i = 0; i < 5; ++i) stats->class_flops[i] = c->cls_flops[i];
+      // inner GMRES: dense products (8 n^2 per instance and product) or the Green-block touches x 8
+      stats->class_flops[1] = c->dense_d ? (stats->dense_flops ? stats->dense_flops[0] : 0.0)
+                                         : 8.0 * (double)((long long)cnt[1] + c->touch_extra);
+      if (c->dense_d && !stats->dense_flops) {
+        const double n = 4.0 * (c->Lc - 1) * c->wmax;
+        stats->class_flops[1] = 8.0 * n * n * (double)(cnt[0] + (long long)c->layer_solves);
+      }
+    }
+    if (stats->class_bytes)
+      for (int i = 0; i < 5; ++i) stats->class_bytes[i] = c->cls_bytes[i];
   }
   if (ecode) return ecode;
   for (int r = 0; r < R; ++r)
@@ -2058,6 +2144,7 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
   std::memset(&acc, 0, sizeof(acc));
   long long ls = 0, ii = 0, to = 0, la = 0, k1l = 0;
   double tms = 0, kms[3] = {0, 0, 0}, k1b = 0, cms[5] = {0, 0, 0, 0, 0}, dfl = 0;
+  double cf[5] = {0, 0, 0, 0, 0}, cb[5] = {0, 0, 0, 0, 0};
   std::vector<int> hist(stats && stats->inner_hist_len > 0 ? stats->inner_hist_len : 0, 0);
   int worst = PT_OK;
   for (int r0 = 0; r0 < nrhs; r0 += B) {
@@ -2066,6 +2153,7 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
     std::memset(&sb, 0, sizeof(sb));
     long long bls = 0, bii = 0, bto = 0, bla = 0, bk1l = 0;
     double btms = 0, bkms[3] = {0, 0, 0}, bk1b = 0, bcms[5] = {0, 0, 0, 0, 0}, bdfl = 0;
+    double bcf[5] = {0, 0, 0, 0, 0}, bcb[5] = {0, 0, 0, 0, 0};
     std::vector<int> bh(hist.size(), 0);
     if (stats) {
       const int mi = pt_residuals_stride(cfg);
@@ -2088,13 +2176,19 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
       sb.k1_launches = &bk1l;
       sb.class_ms = bcms;
       sb.dense_flops = &bdfl;
+      sb.class_flops = bcf;
+      sb.class_bytes = bcb;
     }
     const int rc = solve_batch(c, f + (size_t)r0 * N, nb, cfg, u + (size_t)r0 * N, stats ? &sb : nullptr);
     if (rc != PT_OK && rc != PT_NOT_CONVERGED) return rc;
     if (rc == PT_NOT_CONVERGED) worst = rc;
     ls += bls, ii += bii, to += bto, la += bla, k1l += bk1l, tms += btms, k1b += bk1b, dfl += bdfl;
     for (int i = 0; i < 3; ++i) kms[i] += bkms[i];
-    for (int i = 0; i < 5; ++i) cms[i] += bcms[i];
+    for (int i = 0; i < 5; ++i) {
+      cms[i] += bcms[i];
+      cf[i] += bcf[i];
+      cb[i] += bcb[i];
+    }
     for (size_t i = 0; i < hist.size(); ++i) hist[i] += bh[i];
   }
   if (stats) {
@@ -2111,6 +2205,10 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
     if (stats->class_ms)
       for (int i = 0; i < 5; ++i) stats->class_ms[i] = cms[i];
     if (stats->dense_flops) stats->dense_flops[0] = dfl;
+    if (stats->class_flops)
+      for (int i = 0; i < 5; ++i) stats->class_flops[i] = cf[i];
+    if (stats->class_bytes)
+      for (int i = 0; i < 5; ++i) stats->class_bytes[i] = cb[i];
   }
   if (worst != PT_OK) g_err = "outer GMRES did not reach ktol within max_iter";
   return worst;

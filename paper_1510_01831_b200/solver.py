@@ -232,6 +232,8 @@ class PolarizedTracesSolver:
         lc = np.zeros(2, dtype=np.int64)
         cms = np.zeros(5)
         dfl = np.zeros(1)
+        cfl = np.zeros(5)
+        cby = np.zeros(5)
         st = _abi.PtStats(
             _abi.dptr(its), _abi.dptr(hist), nh.ctypes.data_as(_abi._ip), _abi.dptr(rel),
             conv.ctypes.data_as(_abi._ip), _abi.dptr(trac.view(np.float64)),
@@ -239,7 +241,7 @@ class PolarizedTracesSolver:
             cnt[0:].ctypes.data_as(_abi._llp), cnt[1:].ctypes.data_as(_abi._llp),
             cnt[2:].ctypes.data_as(_abi._llp), ihist.ctypes.data_as(_abi._ip), 64, _abi.dptr(tms),
             _abi.dptr(kms), _abi.dptr(kb), lc[0:].ctypes.data_as(_abi._llp),
-            lc[1:].ctypes.data_as(_abi._llp), _abi.dptr(cms), _abi.dptr(dfl))
+            lc[1:].ctypes.data_as(_abi._llp), _abi.dptr(cms), _abi.dptr(dfl), _abi.dptr(cfl), _abi.dptr(cby))
         L = _abi.lib()
         if device_arrays is None:
             F = np.ascontiguousarray(F, dtype=np.complex128)
@@ -260,7 +262,8 @@ class PolarizedTracesSolver:
                                touches=int(cnt[2]), inner_hist=ihist.copy(), device_ms=float(tms[0]),
                                k1_ms=float(kms[0]), inner_ms=float(kms[1]), other_ms=float(kms[2]),
                                k1_bytes=float(kb[0]), launches=int(lc[0]), k1_launches=int(lc[1]),
-                               class_ms=cms.copy(), dense_flops=float(dfl[0]))
+                               class_ms=cms.copy(), dense_flops=float(dfl[0]), class_flops=cfl.copy(),
+                               class_bytes=cby.copy())
         if rc == _abi.PT_NOT_CONVERGED:
             bad = int(np.argmin(conv))
             h = list(hist[bad, : nh[bad]])
