@@ -94,6 +94,10 @@ typedef struct {
    * per boundary_samples call sum_c 16 w s_c + 16 s_c^2 + 4 nslot_c s_c w (s_c = kept rows of cell c) */
   int assembled_boundary;
   int inner_dense_count;     /* matrices per layer in inner_dense: 2, or 4 with the s-step operators */
+  /* optional (NULL: Tx_main + Tz_main - omega^2 m): [wz][wx] complex diagonal of the global operator used by
+   * the true residual, for a caller-supplied global_operator (sie.py:381, 387-390); the neighbour couplings
+   * are tx / tz's lower and upper diagonals either way */
+  const double* hdiag;
 } pt_problem;
 
 typedef struct {

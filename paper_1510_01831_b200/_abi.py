@@ -58,6 +58,7 @@ class PtProblem(C.Structure):
         ("inner_lu", C.POINTER(_dp)),
         ("assembled_boundary", C.c_int),
         ("inner_dense_count", C.c_int),
+        ("hdiag", _dp),
     ]
 
 
@@ -188,6 +189,8 @@ class Context:
             ptr_arrays["inner_lu"] = P
             pb.inner_lu = C.cast(P, C.POINTER(_dp))
         pb.assembled_boundary = int(bool(getattr(F, "assembled_boundary", False)))
+        if getattr(F, "hdiag", None) is not None:  # residual of a caller-supplied global operator
+            pb.hdiag = dptr(arr(F.hdiag, np.complex128))
         handle = C.c_void_p()
         rc = lib().pt_create(C.byref(pb), int(device), C.byref(handle))
         if rc != PT_OK:

@@ -428,7 +428,8 @@ __global__ void k_accum_x(VecView x, const double2* V, long long vstride, long l
 
 // K5: ||H u - f||^2 and ||f||^2 per RHS (sie.py:441-445), 5-point PML stencil
 __global__ void k_residual(const double2* u, const double2* f, long long stride, int wz, int wx, const double2* tx,
-                           const double2* tz, const double* m, double omega2, const int* rmap, double* out) {
+                           const double2* tz, const double* m, double omega2, const int* rmap, double* out,
+                           const double2* hdiag) {
   __shared__ double red[32];
   const int r = rmap[blockIdx.y];
   const double2* ur = u + r * stride;
@@ -438,7 +439,7 @@ __global__ void k_residual(const double2* u, const double2* f, long long stride,
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x) {
     const int q = (int)(e / wx), pcol = (int)(e % wx);
     // diag = (Tx_main + Tz_main) - omega^2 m
-    const double2 dg = csub(cadd(tx[wx + pcol], tz[wz + q]), make_double2(omega2 * m[e], 0.0));
+    const double2 dg = hdiag ? hdiag[e] : csub(cadd(tx[wx + pcol], tz[wz + q]), make_double2(omega2 * m[e], 0.0));
     double2 a = cmul(dg, ur[e]);
     if (pcol > 0) a = cadd(a, cmul(tx[pcol], ur[e - 1]));
     if (pcol < wx - 1) a = cadd(a, cmul(tx[2 * wx + pcol], ur[e + 1]));

@@ -188,6 +188,7 @@ __global__ void k_arnoldi(double2* V, long long vstride, long long n, int j, con
 __global__ void k_accum_x(VecView x, const double2* V, long long vstride, long long n, const double2* y,
                           int yld, int k, const int* rmap, int nq);
 __global__ void k_residual(const double2* u, const double2* f, long long stride, int wz, int wx, const double2* tx,
-                           const double2* tz, const double* m, double omega2, const int* rmap, double* out);
+                           const double2* tz, const double* m, double omega2, const int* rmap, double* out,
+                           const double2* hdiag);
 __global__ void k_vol_norm2(const double2* f, long long stride, long long N, double* out);
 __global__ void k_green_tiles(const double2* src, double2* dst, int w);

@@ -99,6 +99,7 @@ struct pt_ctx {
   int tables_f_R = 0;
   double2 *tx_d = nullptr, *tz_d = nullptr;
   double* m_d = nullptr;
+  double2* hd_d = nullptr;  // optional global-operator diagonal for the residual
   // inner item programs
   IItem* items_d = nullptr;
   int *op_ph_d = nullptr, *pre_ph_d = nullptr;
@@ -1664,7 +1665,7 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
   CK(cudaMemsetAsync(c->dscal, 0, sizeof(double) * 2 * R, c->st));
   { LaunchScope ls_(c, 2); }
   k_residual<<<dim3(64, R), 256, 0, c->st>>>(u, f, N, c->wz, c->wx, c->tx_d, c->tz_d, c->m_d, c->omega * c->omega,
-                                             c->rmap_d, c->dscal);
+                                             c->rmap_d, c->dscal, c->hd_d);
   CK(cudaGetLastError());
   cudaEventRecord(e1, c->st);
   CK(cudaMemcpyAsync(c->hdscal, c->dscal, sizeof(double) * 2 * R, cudaMemcpyDeviceToHost, c->st));
@@ -2014,6 +2015,8 @@ static int create_impl(pt_ctx* c, const pt_problem* pb, int device, pt_ctx** out
   if (upload(&c->tx_d, reinterpret_cast<const double2*>(pb->tx), 3 * (size_t)c->wx)) return PT_CUDA_ERROR;
   if (upload(&c->tz_d, reinterpret_cast<const double2*>(pb->tz), 3 * (size_t)c->wz)) return PT_CUDA_ERROR;
   if (upload(&c->m_d, pb->m, (size_t)c->wz * c->wx)) return PT_CUDA_ERROR;
+  if (pb->hdiag && upload(&c->hd_d, reinterpret_cast<const double2*>(pb->hdiag), (size_t)c->wz * c->wx))
+    return PT_CUDA_ERROR;
   CK(cudaMalloc(&c->err_d, sizeof(int)));
   CK(cudaMalloc(&c->cnt_d, sizeof(unsigned long long) * 4));
   CK(cudaMalloc(&c->hist_d, sizeof(int) * PT_HIST));
@@ -2071,7 +2074,7 @@ int pt_destroy(pt_ctx* c) {
   // the process-level allocations are released with the context
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
   for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->dense_d, (void*)c->lu_d, (void*)c->lz_d,
-                  (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->items_d,
+                  (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->hd_d, (void*)c->items_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
                   (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->tables_f,
                   (void*)c->trc, (void*)c->Z, (void*)c->iscr, (void*)c->hess, (void*)c->iters, (void*)c->istate,

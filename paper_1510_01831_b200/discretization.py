@@ -275,6 +275,22 @@ def partition_cells(grid, Lc):
     return CellPartition(_split(nx, Lc))
 
 
+def assemble_fd(grid, model, pml):
+    """The global 5-point operator ``-Delta_PML - omega^2 m`` on the extended grid (``discretization.py:223-251``
+    of the reference): ``kron(I_z, T_x) + kron(T_z, I_x) - omega^2 diag(1/c^2)``, depth-major unknowns, as a
+    scipy CSR matrix.  The device path never forms it; this backs ``PolarizedTracesSolver.global_operator()``."""
+    import scipy.sparse as sp
+
+    def axis(n):
+        lower, main, upper = axis_tridiag(pml, n, grid.h)
+        return sp.diags([lower[1:], main, upper[:-1]], [-1, 0, 1], format="csr")
+
+    Tx, Tz = axis(grid.nx), axis(grid.nz)
+    m = 1.0 / np.asarray(model.c, dtype=float) ** 2
+    return (sp.kron(sp.eye(grid.wz), Tx) + sp.kron(Tz, sp.eye(grid.wx))
+            - pml.omega ** 2 * sp.diags(m.ravel())).tocsr().astype(np.complex128)
+
+
 def delta_source(grid, node, discretization="fd"):
     """Discrete point source ``1/h^2`` at lattice node (p, q) -- ``discretization.py:456-471``."""
     p, q = node

@@ -44,7 +44,7 @@ import torch
 
 from .discretization import axis_tridiag
 
-__all__ = ["CellFactors", "LayerFactors", "Factors", "build_factors", "cut_coefs"]
+__all__ = ["CellFactors", "LayerFactors", "Factors", "build_factors", "cut_coefs", "residual_from_operator"]
 
 ROWS = ("r0", "r1", "rn", "rnp")  # sampled rows j = 0, 1, n, n+1
 SLOTS = ("v0", "v1", "vn", "vnp")
@@ -131,6 +131,8 @@ class Factors:
     # the reference's factored boundary pipeline (nested.py:355-486) is selected: same linear maps (this
     # path's pass-0 / sampled-response operators are M_f / direct / M_u), its touch accounting
     assembled_boundary: bool = False
+    # optional (wz, wx) complex diagonal of a caller-supplied global operator (residual only)
+    hdiag: np.ndarray = None
 
     @property
     def wx(self):
@@ -398,12 +400,62 @@ def inner_lu_inverse(lf):
     return torch.linalg.inv(A).contiguous()
 
 
+def _scalar_blocks(H, nb, w, what):
+    """Split a block-tridiagonal operator with ``nb`` blocks of width ``w`` into the shared in-block tridiagonal
+    ``tw = (lower, 0, upper)``, the diagonal ``(nb, w)`` and the scalar block couplings ``lz``/``uz`` (blocks
+    ``l_k I`` / ``u_k I``): the structure of the reference's FD operators (``discretization.py:223-251``).
+    Raises ``ValueError`` when ``H`` is not of that form (e.g. the Q1 discretization)."""
+    import scipy.sparse as sp
+
+    H = sp.csr_matrix(H)
+    if H.shape != (nb * w, nb * w):
+        raise ValueError(f"{what}: operator of shape {H.shape}, expected {(nb * w, nb * w)}")
+    diag = np.asarray(H.diagonal(), dtype=np.complex128).reshape(nb, w)
+    i = np.arange(1, w)
+    lower = np.zeros(w, dtype=np.complex128)
+    upper = np.zeros(w, dtype=np.complex128)
+    lower[1:] = np.asarray(H[i, i - 1]).ravel()
+    upper[:-1] = np.asarray(H[i - 1, i]).ravel()
+    k = np.arange(1, nb)
+    lz = np.zeros(nb, dtype=np.complex128)
+    uz = np.zeros(nb, dtype=np.complex128)
+    lz[1:] = np.asarray(H[k * w, (k - 1) * w]).ravel()
+    uz[:-1] = np.asarray(H[(k - 1) * w, k * w]).ravel()
+    rebuilt = (sp.kron(sp.eye(nb), sp.diags([lower[1:], upper[:-1]], [-1, 1], shape=(w, w)))
+               + sp.diags(diag.ravel()) + sp.kron(sp.diags([lz[1:], uz[:-1]], [-1, 1], shape=(nb, nb)), sp.eye(w)))
+    err = abs(H - rebuilt).max()
+    if err > 1e-12 * abs(H).max():
+        raise ValueError(f"{what}: not a block-tridiagonal operator with scalar couplings (mismatch {err:.3e})")
+    return (lower, np.zeros(w, dtype=np.complex128), upper), diag, lz, uz
+
+
+def _reference_cells(ref, nxc_list, w, npml):
+    """Per-cell operators (cell frame: block rows = original x, width = layer depth) of one reference layer:
+    ``NestedLayerSolver.cells[c].H`` (``nested.py:297-302``) or, for a direct ``LayerWorkspace`` layer
+    (Lc = 1), its own operator with the x <-> z swap applied to the unknown ordering (``nested.py:45-47``)."""
+    if hasattr(ref, "cells"):
+        return [cell.H for cell in ref.cells]
+    wx = ref.grid.wx
+    wz = ref.grid.wz
+    perm = (np.arange(w)[None, :] * wx + np.arange(wx)[:, None]).ravel()  # cell (k=x, i=z) <- layer z*wx + x
+    assert wz == w and len(nxc_list) == 1
+    Hc = ref.H.tocsr()[perm][:, perm]
+    return [Hc]
+
+
 def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=None, inner_dense=None,
-                  backend="pt"):
+                  backend="pt", reference_layers=None):
     """Offline stage for a partitioned problem (all layers, all cells).
 
     ``grid``/``model``/``pml``/``partition`` follow the reference value types
     (``discretization.py:58-220``, ``subdomain.py:51-73``).
+
+    ``reference_layers``: the reference's own ``build_nested_layers`` output (``NestedLayerSolver`` objects,
+    ``nested.py:272-319``) or its direct ``LayerWorkspace`` layers (``subdomain.py:202-236``, Lc = 1).  The
+    couplings are then read from the layers' assembled operators (``LayerOperator.H``, the cells' ``H``) and
+    the interface Green blocks are the reference's own ``GreenBlockSet`` matrices (``green.py:90-153``),
+    uploaded as they are; only the device-side factorisation (Schur inverses) and the operators of the
+    online restructuring are computed here.
     """
     device = torch.device(device)
     if q0 is None:
@@ -421,10 +473,20 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
     for ell, (n, off) in enumerate(zip(partition.extents, partition.offsets)):
         w = n + 2 * npml
         # layer-level cut couplings: the layer's own depth axis (subdomain.py:157-182)
-        lzL, _, uzL = axis_tridiag(pml, n, h)
+        ref = reference_layers[ell] if reference_layers is not None else None
+        if ref is None:
+            lzL, _, uzL = axis_tridiag(pml, n, h)
+        else:  # the layer's depth-axis couplings H[(z, x), (z -/+ 1, x)] at x = 0 (discretization.py:251)
+            HL = ref.H.tocsr()
+            wxl = ref.grid.wx
+            z = np.arange(1, w)
+            lzL = np.zeros(w, dtype=np.complex128)
+            uzL = np.zeros(w, dtype=np.complex128)
+            lzL[1:] = np.asarray(HL[z * wxl, (z - 1) * wxl]).ravel()
+            uzL[:-1] = np.asarray(HL[(z - 1) * wxl, z * wxl]).ravel()
+            ref_ops = _reference_cells(ref, cext, w, npml)
         lcoefs, lrows = cut_coefs(lzL, uzL, npml, n)
         lf = LayerFactors(ell, n, off, w, lcoefs, lrows)
-        tw = axis_tridiag(pml, n, h)  # across the cell block: the layer depth
         c_layer = c[off : off + w, :]  # VelocityModel.restrict (subdomain.py:233-234)
         # group cells of equal nx_c for batched factorization
         groups = {}
@@ -433,14 +495,25 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
         cells = [None] * Lc
         for nxc, idxs in groups.items():
             wzc = nxc + 2 * npml
-            lz, tzm, uz = axis_tridiag(pml, nxc, h)  # along block rows (original x)
-            ccoefs, ckrows = cut_coefs(lz, uz, npml, nxc)
             diag = np.empty((len(idxs), wzc, w), dtype=np.complex128)
-            for b, ci in enumerate(idxs):
-                # cell model: transposed layer restricted to rows [off_c, off_c+wzc)
-                cc = c_layer[:, coffs[ci] : coffs[ci] + wzc].T  # (wzc, w)
-                diag[b] = tzm[:, None] - omega**2 * (1.0 / cc**2)
+            if ref is None:
+                lz, tzm, uz = axis_tridiag(pml, nxc, h)  # along block rows (original x)
+                for b, ci in enumerate(idxs):
+                    # cell model: transposed layer restricted to rows [off_c, off_c+wzc)
+                    cc = c_layer[:, coffs[ci] : coffs[ci] + wzc].T  # (wzc, w)
+                    diag[b] = tzm[:, None] - omega**2 * (1.0 / cc**2)
+            else:
+                parts = [_scalar_blocks(ref_ops[ci], wzc, w, f"layer {ell + 1} cell {ci + 1}") for ci in idxs]
+                tw, _, lz, uz = parts[0]
+                for b, (twb, db, lzb, uzb) in enumerate(parts):
+                    if not (np.allclose(twb[0], tw[0], rtol=0, atol=0) and np.array_equal(lzb, lz)
+                            and np.array_equal(uzb, uz)):
+                        raise ValueError("cells of equal width must share their couplings")
+                    diag[b] = db
+            ccoefs, ckrows = cut_coefs(lz, uz, npml, nxc)
             dg = torch.as_tensor(diag, device=device)
+            if ref is None:
+                tw = axis_tridiag(pml, n, h)  # across the cell block: the layer depth
             sinv = _schur_inverses(tw, dg, lz, uz, device)
             gblk = None
             gsmp = None
@@ -455,10 +528,19 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
                 X = _block_solve(sinv, lz, uz, rhs)
                 gblk = torch.empty((len(idxs), 4, 4, w, w), dtype=torch.complex128,
                                    device=device)
-                for jr, rr in enumerate(rows4):
-                    for s in range(4):
-                        # column-major storage == transpose of the row-major block
-                        gblk[:, jr, s] = X[:, rr, :, s * w : (s + 1) * w].transpose(-1, -2)
+                if ref is not None and hasattr(ref, "blocksets"):
+                    # the reference's own GreenBlockSet matrices (green.py:103-129), rows j = 0, 1, n, n+1
+                    for b, ci in enumerate(idxs):
+                        bs = ref.blocksets[ci]
+                        for jr, jrow in enumerate((0, 1, nxc, nxc + 1)):
+                            for s, slot in enumerate(SLOTS):
+                                gblk[b, jr, s] = torch.as_tensor(
+                                    np.asarray(bs.dense(jrow, slot)).T, dtype=torch.complex128, device=device)
+                else:
+                    for jr, rr in enumerate(rows4):
+                        for s in range(4):
+                            # column-major storage == transpose of the row-major block
+                            gblk[:, jr, s] = X[:, rr, :, s * w : (s + 1) * w].transpose(-1, -2)
                 # layer trace rows 0, 1, n, n+1 in the cell-local frame (offset npml - 1), every block row
                 jrows = [npml - 1, npml, n + npml - 1, n + npml]
                 gsmp = X[:, :, jrows, :].reshape(len(idxs), wzc, 4, 4, w).contiguous()
@@ -514,3 +596,36 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
     tz = axis_tridiag(pml, grid.nz, h)
     return Factors(grid.nx, grid.nz, h, npml, omega, partition.L, Lc, layers, cext, coffs,
                    tx, tz, 1.0 / c**2)
+
+
+def residual_from_operator(H, wz, wx):
+    """``(tx, tz, hdiag)`` of an assembled global 5-point operator (``PolarizedTracesSolver(global_operator=H)``,
+    ``sie.py:381, 387-390``) for the device residual ``||H u - f|| / ||f||`` (``sie.py:441-445``): the x / z
+    neighbour couplings (row-independent / column-independent in the FD operator, ``discretization.py:251``) and
+    the full complex diagonal.  Raises ``ValueError`` if ``H`` is not of that form."""
+    import scipy.sparse as sp
+
+    H = sp.csr_matrix(H)
+    n = wz * wx
+    if H.shape != (n, n):
+        raise ValueError(f"global_operator has shape {H.shape}, the grid needs {(n, n)}")
+    x = np.arange(1, wx)
+    txl = np.zeros(wx, dtype=np.complex128)
+    txu = np.zeros(wx, dtype=np.complex128)
+    txl[1:] = np.asarray(H[x, x - 1]).ravel()
+    txu[:-1] = np.asarray(H[x - 1, x]).ravel()
+    z = np.arange(1, wz)
+    tzl = np.zeros(wz, dtype=np.complex128)
+    tzu = np.zeros(wz, dtype=np.complex128)
+    tzl[1:] = np.asarray(H[z * wx, (z - 1) * wx]).ravel()
+    tzu[:-1] = np.asarray(H[(z - 1) * wx, z * wx]).ravel()
+    hdiag = np.asarray(H.diagonal(), dtype=np.complex128).reshape(wz, wx)
+    rebuilt = (sp.kron(sp.eye(wz), sp.diags([txl[1:], txu[:-1]], [-1, 1], shape=(wx, wx)))
+               + sp.kron(sp.diags([tzl[1:], tzu[:-1]], [-1, 1], shape=(wz, wz)), sp.eye(wx))
+               + sp.diags(hdiag.ravel()))
+    err = abs(H - rebuilt).max()
+    if err > 1e-12 * abs(H).max():
+        raise ValueError(f"global_operator is not a 5-point FD operator (mismatch {err:.3e})")
+    zeros_x = np.zeros(wx, dtype=np.complex128)
+    zeros_z = np.zeros(wz, dtype=np.complex128)
+    return (txl, zeros_x, txu), (tzl, zeros_z, tzu), hdiag

@@ -26,7 +26,7 @@ import numpy as np
 from . import _abi
 from .discretization import DiscretizationSpec, Grid
 from .krylov import InnerSolveError, KrylovBreakdown, KrylovConfig
-from .offline import build_factors
+from .offline import build_factors, residual_from_operator
 
 __all__ = [
     "TraceStack",
@@ -136,10 +136,44 @@ class LayerDescriptor:
     Lc: int
 
 
+def is_reference_layers(layers):
+    """The reference's own layer objects: ``NestedLayerSolver`` (``nested.py:272``, has ``cells`` and
+    ``blocksets``) or direct ``LayerWorkspace`` layers (``subdomain.py:202``, has ``lu`` and ``H``)."""
+    if isinstance(layers, NestedLayers) or not layers:
+        return False
+    first = layers[0]
+    return (hasattr(first, "cells") and hasattr(first, "blocksets")) or (hasattr(first, "lu") and hasattr(first, "H"))
+
+
+def from_reference_layers(layers, grid, model, pml, partition, device=None, inner_dense=None):
+    """``NestedLayers`` for this path from the reference's own offline objects: the list
+    ``build_nested_layers(...)`` of the reference returns (``nested.py:507-521``), or its direct layers
+    (``build_layer``, ``subdomain.py:227-236``).  The cell couplings are read from the reference's assembled
+    operators and its ``GreenBlockSet`` matrices are uploaded as they are (``offline.build_factors``,
+    ``reference_layers=``); the inner solver settings (backend, ``inner_ktol``, ``inner_max_iter``,
+    ``assembled_boundary``) are the layers' own."""
+    first = layers[0]
+    if hasattr(first, "cells"):
+        Lc = len(first.cells)
+        backend = first.backend
+        inner_ktol = first.inner_ktol
+        inner_max_iter = getattr(getattr(first, "inner", None), "max_iter", 200)
+        assembled = bool(getattr(first, "assembled_boundary", False))
+        if getattr(first, "_plr", {}).get("plr_threshold") is not None:
+            raise NotImplementedError("PLR-compressed Green blocks are not part of the B200 path")
+    else:
+        Lc, backend, inner_ktol, inner_max_iter, assembled = 1, "pt", 1e-6, 200, False
+    if len(layers) != partition.L:
+        raise ValueError(f"{len(layers)} layers for a partition of {partition.L}")
+    return build_nested_layers(grid, model, pml, partition, Lc=Lc, backend=backend, inner_ktol=inner_ktol,
+                               inner_max_iter=inner_max_iter, assembled_boundary=assembled, device=device,
+                               inner_dense=inner_dense, reference_layers=list(layers))
+
+
 def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), Lc=1, backend="pt",
                         inner_ktol=1e-6, inner_max_iter=200, plr_threshold=None, plr_eps=1e-8,
                         plr_max_rank=None, seed=0, assembled_boundary=False, device=None, inner_dense=None,
-                        **unused):
+                        reference_layers=None, **unused):
     """``nested.py:507-521`` (with ``NestedLayerSolver`` kwargs, ``nested.py:279-281``).
 
     Runs the offline stage (Schur factors + Green blocks) for every layer.
@@ -159,7 +193,7 @@ def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), 
     if Lc > 1 and grid.nx < 2 * Lc:
         raise ValueError(f"{Lc} cells need nx >= {2 * Lc}, got {grid.nx}")
     F = build_factors(grid, model, pml, partition, Lc, device=device or "cpu", inner_dense=inner_dense,
-                      backend=backend)
+                      backend=backend, reference_layers=reference_layers)
     # assembled_boundary (nested.py:355-486): boundary samples through M_f -> inner solve -> direct + M_u.
     # This path's sample-only layer solves already are those linear maps (pass-0 operator = M_f and the
     # direct part, sampled trace response = M_u); the flag selects the reference's touch accounting.
@@ -195,11 +229,25 @@ class PolarizedTracesSolver:
         self.disc = disc
         if layers is None:
             layers = build_nested_layers(grid, model, pml, partition, disc, Lc=1)
+        elif is_reference_layers(layers):  # the reference's own build_nested_layers / build_layer output
+            layers = from_reference_layers(layers, grid, model, pml, partition)
         if not isinstance(layers, NestedLayers):
-            raise TypeError("layers must come from paper_1510_01831_b200.build_nested_layers")
+            raise TypeError("layers must come from build_nested_layers (this package's or the reference's)")
         self.layers = layers
         self.nI = partition.L - 1
-        self.ctx = _abi.Context(layers.factors, device=device)
+        self._H = global_operator
+        F = layers.factors
+        if global_operator is not None:  # the true residual uses the caller's operator (sie.py:381, 441-445)
+            F.tx, F.tz, F.hdiag = residual_from_operator(global_operator, F.wz, F.wx)
+        self.ctx = _abi.Context(F, device=device)
+
+    def global_operator(self):
+        """``sie.py:387-390``: the caller's operator, or the FD operator of (grid, model, pml) assembled lazily."""
+        if self._H is None:
+            from .discretization import assemble_fd
+
+            self._H = assemble_fd(self.grid, self.model, self.pml)
+        return self._H
 
     def close(self):
         self.ctx.close()

@@ -26,3 +26,6 @@ GOLDEN = {
     "small_c_asm": (lambda: small_problem(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7), 0, True),
     "cfg1_asm": (lambda: make_config("cfg1"), 0, True),
 }
+
+# the problem whose offline artifacts tests/golden/make_refobj.py builds from the reference's own layer objects
+REFOBJ_CASE = dict(nx=24, nz=20, npml=4, L=2, Lc=2, omega=9.0, seed=2, n_sources=3)

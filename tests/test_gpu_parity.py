@@ -313,3 +313,27 @@ def test_batched_inner_histogram_is_sum_of_single_histograms(name):
         touch_s += dev.last_stats["touches"]
     assert np.array_equal(hist_b, hist_s)
     assert touch_b == touch_s
+
+
+def test_solve_with_factors_built_from_reference_objects():
+    """Drop-in construction (sie.py:368-390): the factors from the reference's own build_nested_layers objects
+    (couplings read from their operators, their GreenBlockSet matrices; tests/golden/make_refobj.py) solve like
+    the oracle on the device, and global_operator feeds the true residual."""
+    from paper_1510_01831_b200.artifacts import load_offline
+    from paper_1510_01831_b200.discretization import assemble_fd
+    from tests.golden_cases import REFOBJ_CASE
+
+    prob = small_problem(**REFOBJ_CASE)
+    layers = load_offline(os.path.join(HERE, "golden", "refobj"), "refobj", prob.grid, prob.partition,
+                          model=prob.model, omega=prob.pml.omega)
+    H = assemble_fd(prob.grid, prob.model, prob.pml)
+    dev = PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers, global_operator=H)
+    orc = OracleSolver.from_problem(prob)
+    for f in prob.rhs():
+        got = dev.solve(f, KrylovConfig(ktol=1e-9))
+        want = orc.solve(f, ktol=1e-9)
+        assert rel(got.u, want.u) < 1e-10
+        assert got.iterations == want.iterations
+        assert abs(got.relative_residual - want.relative_residual) <= 1e-6 * want.relative_residual + 1e-14
+    assert dev.global_operator() is H
+    dev.close()

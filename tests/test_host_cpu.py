@@ -262,3 +262,92 @@ def test_inner_lu_inverse_matches_block_lu():
         y = Ainv @ np.concatenate(b)
         assert np.linalg.norm(y - x) <= 1e-11 * np.linalg.norm(x)
         assert F.layers[ell].dense is None
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# Drop-in construction from the reference's own offline objects (sie.py:368-390, nested.py:272-319, 507-521).
+# Skipped where the reference package is absent (the GPU box).
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+def _reference_objects(prob, Lc=None, backend="pt"):
+    import sys
+
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import polartraces as rpt
+
+    g = prob.grid
+    grid = rpt.Grid(g.nx, g.nz, g.h, g.npml)
+    model = rpt.VelocityModel(grid, prob.model.c)
+    pml = rpt.PmlProfile(g.npml, g.h, prob.pml.C, prob.pml.omega)
+    part = rpt.LayerPartition(tuple(prob.partition.extents))
+    if Lc is None:  # direct LayerWorkspace layers (the reference's layers=None default)
+        layers = [rpt.build_layer(grid, model, pml, part, ell) for ell in range(1, part.L + 1)]
+    else:
+        layers = rpt.build_nested_layers(grid, model, pml, part, Lc=Lc, backend=backend,
+                                         inner_ktol=prob.inner_ktol)
+    return rpt, layers, rpt.discretization.assemble_fd(grid, model, pml)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference package not present")
+@pytest.mark.parametrize("case,Lc,backend", [
+    (dict(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), 3, "pt"),
+    (dict(nx=33, nz=30, npml=4, L=2, Lc=4, omega=11.0, seed=7), 4, "lu"),
+    (dict(nx=40, nz=36, npml=6, L=3, Lc=2, omega=14.0, seed=0), None, "pt"),
+])
+def test_factors_from_reference_objects_equal_own_offline(case, Lc, backend):
+    """The arrays uploaded for the reference's own layer objects (couplings read from their assembled
+    operators, Green blocks = their GreenBlockSet matrices) equal this package's offline stage to 1e-12."""
+    from paper_1510_01831_b200.solver import build_nested_layers, from_reference_layers, is_reference_layers
+
+    prob = small_problem(**case)
+    _, ref_layers, _ = _reference_objects(prob, Lc, backend)
+    assert is_reference_layers(ref_layers)
+    got = from_reference_layers(ref_layers, prob.grid, prob.model, prob.pml, prob.partition)
+    want = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=Lc or 1, backend=backend,
+                               inner_ktol=prob.inner_ktol)
+    assert got.backend == want.backend and got.Lc == want.Lc and got.inner_ktol == want.inner_ktol
+
+    def close(a, b):
+        a, b = np.asarray(a), np.asarray(b)
+        return np.linalg.norm(a - b) <= 1e-12 * max(np.linalg.norm(b), 1e-300)
+
+    for la, lb in zip(got.factors.layers, want.factors.layers):
+        assert close(la.coefs, lb.coefs) and np.array_equal(la.prows, lb.prows)
+        for ca, cb in zip(la.cells, lb.cells):
+            assert close(ca.lz, cb.lz) and close(ca.uz, cb.uz) and close(ca.coefs, cb.coefs)
+            assert np.array_equal(ca.krows, cb.krows)
+            assert close(ca.sinv.numpy(), cb.sinv.numpy())
+            for name in ("green", "gsmp", "q0"):
+                va, vb = getattr(ca, name), getattr(cb, name)
+                assert (va is None) == (vb is None)
+                if va is not None:
+                    assert close(va.numpy(), vb.numpy()), name
+        for name in ("dense", "lu_inv"):
+            va, vb = getattr(la, name), getattr(lb, name)
+            assert (va is None) == (vb is None)
+            if va is not None:
+                assert close(va.numpy(), vb.numpy()), name
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference package not present")
+def test_global_operator_residual_arrays():
+    """global_operator (sie.py:381): the device residual's couplings and diagonal reproduce the caller's H."""
+    import scipy.sparse as sp
+
+    from paper_1510_01831_b200.discretization import assemble_fd
+    from paper_1510_01831_b200.offline import residual_from_operator
+
+    prob = small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3)
+    _, _, Href = _reference_objects(prob, 3)
+    H = assemble_fd(prob.grid, prob.model, prob.pml)
+    assert abs(H - Href).max() == 0.0  # the restated assembly is the reference's, bit for bit
+    g = prob.grid
+    tx, tz, hd = residual_from_operator(Href, g.wz, g.wx)
+    rebuilt = (sp.kron(sp.eye(g.wz), sp.diags([tx[0][1:], tx[2][:-1]], [-1, 1]))
+               + sp.kron(sp.diags([tz[0][1:], tz[2][:-1]], [-1, 1]), sp.eye(g.wx)) + sp.diags(hd.ravel()))
+    assert abs(rebuilt - Href).max() == 0.0
+    with pytest.raises(ValueError):
+        residual_from_operator(Href + sp.eye(Href.shape[0], k=2 * g.wx), g.wz, g.wx)
