@@ -401,9 +401,15 @@ def _parity(name, idx, U):
 def _solver(prob, local, backend="pt"):
     from paper_1510_01831_b200 import PolarizedTracesSolver, build_nested_layers
 
+    import torch
+
     layers = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=prob.Lc,
                                  inner_ktol=prob.inner_ktol, device=f"cuda:{local}", backend=backend)
-    return PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers, device=local)
+    solver = PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers, device=local)
+    solver.release_offline_arrays()  # the context holds the device copy; drop torch's
+    del layers
+    torch.cuda.empty_cache()
+    return solver
 
 
 def _time_device(solver, F, U, R, cfg, steps, warmup, clocks=None):
@@ -536,10 +542,14 @@ def run_ours(args):
             "profiled_ms_per_step": st["device_ms"]}
     roof["frac"] = roof["achieved"] / roof["peak"] if roof["achieved"] else None
 
+    ref_eq = _reference_equivalent(solver, st, R, st["device_ms"])
+    del F, U
+    torch.cuda.empty_cache()
     extras = {}
     if world == 1 and not args.no_extras:
-        extras = _regimes(args, prob, solver, peaks)
-    solver.close()
+        extras = _regimes(args, prob, solver, peaks)  # closes the solver before it builds cfg2's
+    else:
+        solver.close()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -555,7 +565,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "roofline": roof,
         "kernels": kern,
-        "reference_equivalent": _reference_equivalent(solver, st, R, st["device_ms"]),
+        "reference_equivalent": ref_eq,
         "clocks": clk.summary(),
         "outer_iterations": its,
         "parity_vs_reference_fixtures": parity,
@@ -611,6 +621,8 @@ def _regimes(args, prob, solver, peaks):
             "kernels": kern, "parity_vs_reference_fixtures": _parity("cfg5", [0], U),
             "outer_iterations": [r.iterations for r in res]}
         del F, U
+    solver.close()
+    torch.cuda.empty_cache()
     if args.config != "cfg2":  # round 1's line for continuity
         p2 = make_config("cfg2")
         s2 = _solver(p2, torch.cuda.current_device())

@@ -252,6 +252,17 @@ class PolarizedTracesSolver:
     def close(self):
         self.ctx.close()
 
+    def release_offline_arrays(self):
+        """Drop this object's references to the offline arrays once ``pt_create`` has copied them to the device:
+        when the offline stage ran on the GPU (``build_nested_layers(device="cuda")``) this frees a full second
+        copy of the factors in HBM (tens of GB for cfg5).  Geometry and scalars stay available."""
+        F = self.layers.factors
+        for lf in F.layers:
+            lf.dense = lf.lu_inv = None
+            for cf in lf.cells:
+                cf.sinv = cf.green = cf.gsmp = cf.q0 = None
+        self.ctx.keep = None
+
     # -- one call into the C ABI for a batch of sources
     def _run(self, F, config, preconditioner, device_arrays=None, out=None):
         if preconditioner not in ("gs", "jac"):
