@@ -37,7 +37,8 @@
 
 namespace cg = cooperative_groups;
 
-#define II_T 256           // threads per CTA (8 warps)
+#define II_T 256           // consumer threads per CTA (8 warps)
+#define II_TB (II_T + 32)  // + one producer warp (warp 8) that only issues the ring's bulk copies
 #define II_RING (144 * 1024)
 #define II_NSLOT 16
 #define II_RED (32 * 1024)
@@ -112,6 +113,8 @@ struct IIShared {
   double2 (*gv)[3][34];                     // Givens: column, cs, sn / back substitution: g and triangle
   double2 (*yv)[34];                        // x = V y coefficients, [33] = k
   int phw[II_MAXPH];                        // per program phase (op phases first): sum of item weights
+  unsigned char phcfg[II_MAXPH];            // per program phase: tile shape for the current active sets
+  unsigned char phtwo[II_MAXPH];            // per program phase: some item has a two-term panel
   int any_active;
 };
 
@@ -124,6 +127,9 @@ __device__ __forceinline__ double2* partp(const InnerParams& p, int area, int v)
   const size_t rec = (size_t)(p.cap + 2) * 8;
   return p.part + ((size_t)area * p.part_items + v) * rec;
 }
+
+// barrier of the 8 consumer warps only (the producer warp never waits on the consumers' shared-memory work)
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 __device__ __forceinline__ void dmma4(double (&a)[8], double ar, double ai, double br, double bi) {
   dmma_f64(a[0], a[1], ar, br);
@@ -176,12 +182,18 @@ __device__ __forceinline__ TileRef tile_decode(const IIShared& S, int cfg, int J
 
 // ---------------------------------------------------------------------------------------- tiles and chunks
 // K rows per chunk by config: narrow chunks for the big (throughput) tiles, whole slots for the small (latency)
-// tiles so a tile is a handful of chunks.  A ring slot holds A [MTC][KC][8] then B [NTC][2 terms][KC][8].
-__device__ __forceinline__ int cfg_kc(const TileCfg& c) {  // the widest chunk whose ring slot stays <= 48 KB
-  const int per = 128 * (c.mtc + 2 * c.ntc);              // bytes per K row
-  return per * 128 <= 48 * 1024 ? 128 : (per * 64 <= 48 * 1024 ? 64 : 32);
+// tiles so a tile is a handful of chunks.  A ring slot holds A [MTC][KC][8] then B [NTC][terms][KC][8].
+// K rows per chunk: the widest chunk (so each warp's share of a chunk is a longer DMMA chain) whose ring still
+// holds two slots (KW > 1) or whose slot stays <= 48 KB (KW = 1: big tiles, deeper ring).  `terms` = 2 when a
+// phase has two-term panels (d + p, the op program), else 1.
+__device__ __forceinline__ int cfg_kc(const TileCfg& c, int terms) {
+  const int per = 128 * (c.mtc + terms * c.ntc);  // bytes per K row
+  const int cap = c.kw == 1 ? 48 * 1024 : II_RING / 2;
+  return per * 128 <= cap ? 128 : (per * 64 <= cap ? 64 : 32);
 }
-__device__ __forceinline__ uint32_t slot_elems(const TileCfg& c, int kc) { return (uint32_t)kc * 8u * (c.mtc + 2 * c.ntc); }
+__device__ __forceinline__ uint32_t slot_elems(const TileCfg& c, int kc, int terms) {
+  return (uint32_t)kc * 8u * (c.mtc + terms * c.ntc);
+}
 
 // Everything a tile's chunks need, derived once per tile (warp-uniform values).
 struct TileDesc {
@@ -222,8 +234,8 @@ __device__ __forceinline__ TileDesc tile_desc(const InnerParams& p, const IIShar
 // chunk's byte count (complete_tx may land before the arm: the phase cannot complete while the arm's arrival
 // is pending).  One round of independent bulk copies per chunk, no per-copy serial address work.
 __device__ __forceinline__ void issue_chunk_warp(const InnerParams& p, const IIShared& S, const TileCfg& c, int kc,
-                                                 const TileDesc& d, int si, int kcn, double2* slotp, uint64_t* bar,
-                                                 const int vmap[3]) {
+                                                 int terms, const TileDesc& d, int si, int kcn, double2* slotp,
+                                                 uint64_t* bar, const int vmap[3]) {
   const int lane = threadIdx.x & 31;
   const int s = d.slots >> (2 * si) & 3, two = d.twos >> si & 1;
   const int k0 = kcn * kc, kv = min(kc, d.w - k0);
@@ -239,7 +251,7 @@ __device__ __forceinline__ void issue_chunk_warp(const InnerParams& p, const IIS
     if (t <= two) {
       const Ref r = item.pan[s][t];
       const int nt = S.act[d.jx][d.nt0 + bq];
-      bulk_g2s(slotp + ((size_t)c.mtc + bq * 2 + t) * kc * 8,
+      bulk_g2s(slotp + ((size_t)c.mtc + bq * terms + t) * kc * 8,
                v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + k0) * 8, bytes, bar);
     }
   }
@@ -248,14 +260,15 @@ __device__ __forceinline__ void issue_chunk_warp(const InnerParams& p, const IIS
 // ---------------------------------------------------------------------------------------- warp product
 // One chunk of a tile for this warp: its (WM x WN <= 2 x 2) pairs over k-steps [ks0, ks1).  wm / wn are
 // warp-uniform runtime values (one code path keeps the hot loop small).
-__device__ __forceinline__ void chunk_mma(const double2* A, const double2* B, int kc, int wm, int wn, int wmi,
-                                          int wni, int ks0, int ks1, int kv, int two, double sg,
+__device__ __forceinline__ void chunk_mma(const double2* A, const double2* B, int kc, int terms, int wm, int wn,
+                                          int wmi, int wni, int ks0, int ks1, int kv, int two, double sg,
                                           double (&acc)[2][2][8], int mvalid, int nvalid) {
   const int lane = threadIdx.x & 31, r8 = lane >> 2, kl = lane & 3;
   const bool m1 = wm > 1 && wmi * wm + 1 < mvalid, n1 = wn > 1 && wni * wn + 1 < nvalid;
   const bool m0 = wmi * wm < mvalid, n0 = wni * wn < nvalid;
   const double2* A0 = A + (size_t)(wmi * wm) * kc * 8 + r8;
-  const double2* B0 = B + (size_t)(wni * wn) * 2 * kc * 8 + r8;
+  const double2* B0 = B + (size_t)(wni * wn) * terms * kc * 8 + r8;
+  const int bstride = terms * kc * 8;  // next n-tile's panel
 #pragma unroll 2
   for (int ks = ks0; ks < ks1; ++ks) {
     const int k = ks * 4 + kl;
@@ -269,8 +282,8 @@ __device__ __forceinline__ void chunk_mma(const double2* A, const double2* B, in
         if (two) b0 = cadd(b0, B0[(kc + k) * 8]);  // d + p (the gather's order)
       }
       if (n1) {
-        b1 = B0[(2 * kc + k) * 8];
-        if (two) b1 = cadd(b1, B0[(3 * kc + k) * 8]);
+        b1 = B0[bstride + k * 8];
+        if (two) b1 = cadd(b1, B0[bstride + (kc + k) * 8]);
       }
     }
     b0 = make_double2(b0.x * sg, b0.y * sg);
@@ -295,6 +308,25 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// The tile shape of a phase: minimise (tile rounds) x (cycles of one tile at its warp block's DMMA rate + a fixed
+// per-tile cost).  Evaluated for every program phase when the active n-tiles change (refresh), not per phase.
+__device__ __forceinline__ int phase_config(const IIShared& S, int J, int nit, int wphase, int wmax, int G) {
+  int cfg = II_NCFG - 1;
+  const float ksteps = (float)wphase / (float)max(nit, 1) * (float)((wmax + 3) >> 2);
+  float best = 3.4e38f;
+  for (int ci = 0; ci < II_NCFG; ++ci) {
+    const TileCfg cc = II_CFG[ci];
+    const int tiles = S.tpre[ci][J] * nit;
+    const int rounds = (tiles + G - 1) / G;
+    const float t = (float)rounds * ((float)(cc.mtc * cc.ntc) * ksteps * 4.0f / cfg_rate(cc) + 3000.0f);
+    if (tiles > 0 && t < best) {
+      best = t;
+      cfg = ci;
+    }
+  }
+  return cfg;
+}
+
 // Ring bookkeeping that persists across phases: consumers' full-barrier parities and the producer warp's
 // empty-barrier parities, one bit per physical slot.
 struct Ring {
@@ -305,78 +337,49 @@ struct Ring {
 // scratch vector index.  Warp 0 produces (a slot is refilled once its 8 consumer warps have arrived on its
 // empty barrier) and consumes like every other warp; there is no CTA-wide barrier per chunk.
 __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double2* ring, double2* red, int J,
-                                       int it0, int nit, int wphase, const int vmap[3], Ring& rg, IITick& T,
-                                       IITrace& X) {
+                                       int it0, int nit, int wphase, int pcfg, int phase_id, const int vmap[3],
+                                       Ring& rg, IITick& T, IITrace& X) {
   const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, b = blockIdx.x;
   // ---- config: minimise (tile rounds) x (cycles of one tile at its warp block's DMMA rate + a fixed per-tile cost)
-  int cfg = II_NCFG - 1;
-  {
-    const float ksteps = (float)wphase / (float)max(nit, 1) * (float)((p.wmax + 3) >> 2);
-    float best = 3.4e38f;
-    for (int ci = 0; ci < II_NCFG; ++ci) {
-      const TileCfg cc = II_CFG[ci];
-      const int tiles = S.tpre[ci][J] * nit;
-      const int rounds = (tiles + G - 1) / G;
-      const float t = (float)rounds * ((float)(cc.mtc * cc.ntc) * ksteps * 4.0f / cfg_rate(cc) + 3000.0f);
-      if (tiles > 0 && t < best) {
-        best = t;
-        cfg = ci;
-      }
-    }
-  }
+  const int cfg = pcfg;  // chosen per phase when the active sets change (phase_config)
   X.ev(20, cfg);
   const TileCfg c = II_CFG[cfg];
-  const int kc = cfg_kc(c), ksn = kc / 4;
+  const int terms = S.phtwo[phase_id] ? 2 : 1;  // two-term panels (d + p) in this phase
+  const int kc = cfg_kc(c, terms), ksn = kc / 4;
   const int ntiles = S.tpre[cfg][J] * nit;
-  const uint32_t se = slot_elems(c, kc);
+  const uint32_t se = slot_elems(c, kc, terms);
   const int nslot = min(II_NSLOT, (int)(II_RING / (se * 16u)));
   // the B panels were written by other CTAs (generic proxy) before the grid barrier; order those writes
   // before this CTA's bulk (async-proxy) reads
   if (wp == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-  // producer state (warp 0, warp-uniform): its tile number, descriptor and chunk position
-  int pt = b, psi = 0, pkc = 0;
-  TileDesc pd;
-  if (wp == 0) {
-    while (pt < ntiles && S.ins[it0 + tile_decode(S, cfg, J, pt).ii] == 0) pt += G;
-    if (pt < ntiles) pd = tile_desc(p, S, c, kc, tile_decode(S, cfg, J, pt), it0);
+  // ---- warp 8: the producer.  Walks this CTA's tiles and chunks in the consumers' order, waits for a slot's 8
+  // consumer warps to release it (empty barrier), then issues the chunk's bulk copies, one lane per copy.
+  if (wp == 8) {
+    int issued = 0;
+    for (int t = b; t < ntiles; t += G) {
+      const TileRef r = tile_decode(S, cfg, J, t);
+      if (S.ins[it0 + r.ii] == 0) continue;
+      const TileDesc d = tile_desc(p, S, c, kc, r, it0);
+      for (int si = 0; si < d.ns; ++si)
+        for (int kcn = 0; kcn < d.nkc; ++kcn) {
+          const int slot = issued % nslot;
+          if (lane == 0) mbar_wait_suspend(&S.empty[slot], (rg.epar >> slot) & 1u);
+          __syncwarp();
+          rg.epar ^= 1u << slot;
+          issue_chunk_warp(p, S, c, kc, terms, d, si, kcn, ring + (size_t)slot * se, &S.full[slot], vmap);
+          ++issued;
+        }
+    }
+    return;
   }
-  int issued = 0, done = 0;
-  auto try_issue = [&](bool block) -> bool {  // warp 0: the next chunk, if its slot is free (or once it is)
-    if (pt >= ntiles) return false;
-    const int slot = issued % nslot;
-    bool ok = true;
-    if (lane == 0) {
-      if (block) mbar_wait_suspend(&S.empty[slot], (rg.epar >> slot) & 1u);
-      else ok = mbar_test(&S.empty[slot], (rg.epar >> slot) & 1u);
-    }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (!ok) return false;
-    rg.epar ^= 1u << slot;
-    issue_chunk_warp(p, S, c, kc, pd, psi, pkc, ring + (size_t)slot * se, &S.full[slot], vmap);
-    X.ev(2, issued);
-    ++issued;
-    if (++pkc == pd.nkc) {
-      pkc = 0;
-      if (++psi == pd.ns) {
-        psi = 0;
-        do {
-          pt += G;
-        } while (pt < ntiles && S.ins[it0 + tile_decode(S, cfg, J, pt).ii] == 0);
-        if (pt < ntiles) pd = tile_desc(p, S, c, kc, tile_decode(S, cfg, J, pt), it0);
-      }
-    }
-    return true;
-  };
-  if (wp == 0)
-    while (issued < nslot && try_issue(false)) {
-    }
+  int done = 0;
   X.ev(1, cfg * 100 + nslot);
   T.tick(0);
   const int wpk = 8 / c.kw;  // warps per k part
   const int kp = wp / wpk, wq = wp - kp * wpk;
   const int wmi = wq % (c.mtc / c.wm), wni = wq / (c.mtc / c.wm);
-  const int ks0 = kp * ksn / c.kw, ks1 = (kp + 1) * ksn / c.kw;
+  const int ks0 = kp * ksn / c.kw, ks1 = (kp + 1) * ksn / c.kw;  // this warp's k-steps of every chunk
   for (int t = b; t < ntiles; t += G) {
     X.ev(5, t);
     T.count(9);
@@ -411,28 +414,23 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
       for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[a][bb][e] = 0.0;
-    for (int si = 0; si < d.ns; ++si) {
+    for (int si = 0, q = 0; si < d.ns; ++si) {
       const double sg = (d.negs >> si & 1) ? -1.0 : 1.0;
       const int two = d.twos >> si & 1;
-      for (int kcn = 0; kcn < d.nkc; ++kcn) {
-        if (wp == 0)
-          while (issued <= done) try_issue(true);  // the chunk about to be consumed must be in flight
+      for (int kcn = 0; kcn < d.nkc; ++kcn, ++q) {
         const int slot = done % nslot;
         mbar_wait_suspend(&S.full[slot], (rg.fpar >> slot) & 1u);
         rg.fpar ^= 1u << slot;
         X.ev(3, done);
         const double2* A = ring + (size_t)slot * se;
         const double2* B = A + (size_t)c.mtc * kc * 8;
-        chunk_mma(A, B, kc, c.wm, c.wn, wmi, wni, ks0, ks1, min(kc, d.w - kcn * kc), two, sg, acc, d.mvalid,
-                  d.nvalid);
+        chunk_mma(A, B, kc, terms, c.wm, c.wn, wmi, wni, ks0, ks1, min(kc, d.w - kcn * kc), two, sg, acc,
+                  d.mvalid, d.nvalid);
         __syncwarp();
         // relaxed: a release arrive would first wait for every outstanding memory operation of the thread
         if (lane == 0) mbar_arrive_relaxed(&S.empty[slot]);
         ++done;
         X.ev(4, done);
-        if (wp == 0)
-          while (issued < done + nslot && try_issue(false)) {
-          }
       }
     }
     T.tick(1);
@@ -451,7 +449,7 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
           dst[1] = make_double2(q[1] - q[3], q[5] + q[7]);
         }
     }
-    __syncthreads();
+    cbar();
     // ---- combine: t = y + (add0 + add1) - (sub0 + sub1); dst = t | rev - t | t - rev
     for (int o = tid; o < npair * 64; o += II_T) {
       const int pr = o >> 6, pos = o & 63, row = pos >> 3, q = pos & 7;
@@ -482,7 +480,7 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
       else if (mode == 2) y = csub(y, rv);
       v2p(p, d.job, vmap[item.dst.vec], nt)[((size_t)item.dst.seg * d.w + grow) * 8 + q] = y;
     }
-    __syncthreads();  // red is reused by the next tile
+    cbar();  // red is reused by the next tile
     X.ev(6, 0);
     T.tick(2);
   }
@@ -520,12 +518,12 @@ __device__ __forceinline__ double2 qsum(double2 v, double* dred) {
     v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
   }
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, q = threadIdx.x & 7;
-  __syncthreads();
+  cbar();
   if (lane < 8) {
     dred[(wp * 8 + lane) * 2] = v.x;
     dred[(wp * 8 + lane) * 2 + 1] = v.y;
   }
-  __syncthreads();
+  cbar();
   double2 s = czero();
   for (int k = 0; k < II_T / 32; ++k) s = cadd(s, make_double2(dred[(k * 8 + q) * 2], dred[(k * 8 + q) * 2 + 1]));
   return s;
@@ -639,7 +637,7 @@ __device__ __noinline__ void vec_item(const InnerParams& p, IIShared& S, int pas
       Wp[(size_t)e * 8 + q] = make_double2(x.x * ihn, x.y * ihn);
     }
   }
-  __syncthreads();  // every thread has read the instance state before the owner updates it
+  cbar();  // every thread has read the instance state before the owner updates it
   if (sl != 0) return;
   // owner of the (job, n-tile): stage the Hessenberg column h1 + h2 and the previous rotations of its 8
   // instances in shared memory (parallel loads), then each instance's serial rotation loop runs on thread q
@@ -660,7 +658,7 @@ __device__ __noinline__ void vec_item(const InnerParams& p, IIShared& S, int pas
       S.gv[q2][1][33] = ld_cg(g + j);  // g[j]
     }
   }
-  __syncthreads();
+  cbar();
   if (tid < 8 && act) {
     const int r = r_ + q;
     double2* H = p.hess + (size_t)(job * p.R + r) * p.hstride;
@@ -709,11 +707,11 @@ __device__ __noinline__ void vec_item(const InnerParams& p, IIShared& S, int pas
     p.state[job * p.R + r] = st;
     if (st != 0) p.iters[job * p.R + r] = st == 1 ? j + 1 : -1;
   }
-  __syncthreads();  // S.gv is reused by the next item
+  cbar();  // S.gv is reused by the next item
 }
 
 // ---------------------------------------------------------------------------------------- the kernel
-__global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams p, int J) {
+__global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams p, int J) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char smem[];
   double2* ring = reinterpret_cast<double2*>(smem);
@@ -732,7 +730,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
     fence_mbar_init();
   }
   __syncthreads();
-  if ((tid & 31) == 0)  // every slot starts free: complete phase 0 of its empty barrier
+  if ((tid & 31) == 0 && tid < II_T)  // every slot starts free: complete phase 0 of its empty barrier
     for (int i = 0; i < II_NSLOT; ++i) mbar_arrive(&S.empty[i]);
   IITick T;
   T.on = p.tprof && blockIdx.x == 0 && tid == 0;
@@ -748,7 +746,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
   IITrace X;
   X.on = p.ii_trace > 0 && (int)blockIdx.x == p.ii_trace - 1 && tid == 0;
   X.n = 0;
-  for (int jx = tid; jx < J; jx += II_T) {
+  for (int jx = tid; jx < J; jx += II_TB) {
     const int job = p.stage_jobs[jx];
     S.jlay[jx] = p.jobs[job].layer;
     S.jw[jx] = p.layers[S.jlay[jx]].w;
@@ -756,21 +754,25 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
   }
   S.gv = reinterpret_cast<double2(*)[3][34]>(red);
   S.yv = reinterpret_cast<double2(*)[34]>(red + 8 * 3 * 34);
-  for (int i = tid; i < p.nitems; i += II_T) {
+  for (int i = tid; i < p.nitems; i += II_TB) {
     S.items[i] = p.items[i];
     S.ins[i] = (unsigned char)item_ns_g(p.items[i]);
   }
   __syncthreads();
-  for (int ph = tid; ph < p.op_nph + p.pre_nph; ph += II_T) {
+  for (int ph = tid; ph < p.op_nph + p.pre_nph; ph += II_TB) {
     const int* phd = ph < p.op_nph ? p.op_ph + ph : p.pre_ph + (ph - p.op_nph);
-    int wsum = 0;
-    for (int i = phd[0]; i < phd[1]; ++i) wsum += S.ins[i] > 0 ? S.ins[i] : 1;
+    int wsum = 0, two = 0;
+    for (int i = phd[0]; i < phd[1]; ++i) {
+      wsum += S.ins[i] > 0 ? S.ins[i] : 1;
+      for (int s_ = 0; s_ < 4; ++s_) two |= S.items[i].cell >= 0 && S.items[i].pan[s_][1].vec >= 0;
+    }
     S.phw[ph] = wsum;
+    S.phtwo[ph] = (unsigned char)two;
   }
   // active n-tiles: all == every existing instance (before the states exist)
   auto refresh = [&](bool all) {
     __syncthreads();
-    for (int t = tid; t < J * NT; t += II_T) {
+    for (int t = tid; t < J * NT; t += II_TB) {
       const int jx = t / NT, nt = t - jx * NT, job = S.jjob[jx];
       unsigned m = 0;
       for (int q = 0; q < 8; ++q) {
@@ -801,11 +803,16 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
       }
     }
     __syncthreads();
+    for (int ph = tid; ph < p.op_nph + p.pre_nph; ph += II_TB) {
+      const int* phd = ph < p.op_nph ? p.op_ph + ph : p.pre_ph + (ph - p.op_nph);
+      S.phcfg[ph] = (unsigned char)phase_config(S, J, phd[1] - phd[0], S.phw[ph], p.wmax, G);
+    }
+    __syncthreads();
   };
   auto program = [&](const int* ph_d, int nph, int phw0, const int vm[3]) {
     for (int phz = 0; phz < nph; ++phz) {
       const int i0 = ph_d[phz], i1 = ph_d[phz + 1];
-      run_phase(p, S, ring, red, J, i0, i1 - i0, S.phw[phw0 + phz], vm, rg, T, X);
+      run_phase(p, S, ring, red, J, i0, i1 - i0, S.phw[phw0 + phz], S.phcfg[phw0 + phz], phw0 + phz, vm, rg, T, X);
       T.count(8);
       X.ev(7, phz);
       gsync();
@@ -819,7 +826,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
       const int job = S.jjob[jx], w = S.jw[jx], n = 4 * nIc * w;
       const long long tot = (long long)NT * n * 8;
       double2* vb = v2p(p, job, VB, 0);
-      for (long long t = (long long)b * II_T + tid; t < tot; t += (long long)G * II_T) {
+      for (long long t = (long long)b * II_T + tid; tid < II_T && t < tot; t += (long long)G * II_T) {
         const int q = (int)(t & 7);
         const long long rest = t >> 3;
         const int nt = (int)(rest / n), e = (int)(rest - (long long)nt * n);
@@ -850,7 +857,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
   // ---- beta0 = ||b||, V_0 = b / beta0, g[0] = beta0 (krylov.py:63-86)
   {
     const VSplit vs = vsplit(S, J, G, 4 * nIc * p.wmax);
-    for (int v = b; v < vs.nitem; v += G) {
+    for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
       const int job = S.jjob[jx], n = 4 * nIc * S.jw[jx];
@@ -867,7 +874,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
     T.tick(4);
     gsync();
     T.tick(5);
-    for (int v = b; v < vs.nitem; v += G) {
+    for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
       const int job = S.jjob[jx], n = 4 * nIc * S.jw[jx];
@@ -899,7 +906,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
     refresh(false);
     if (!S.any_active) break;
     if (j + 1 > p.cap) {  // basis capacity exhausted: the host retries with a larger capacity
-      for (int t = b * II_T + tid; t < J * p.R; t += G * II_T) {
+      for (int t = b * II_T + tid; tid < II_T && t < J * p.R; t += G * II_T) {
         const int jx = t / p.R, r = t - jx * p.R, job = S.jjob[jx];
         if (__ldcg(p.state + job * p.R + r) == 0) {
           p.state[job * p.R + r] = 2;
@@ -920,7 +927,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
     }
     const VSplit vs = vsplit(S, J, G, 4 * nIc * p.wmax);
     // pass 1: h1_i = vdot(V_i, w), i <= j -> area 0
-    for (int v = b; v < vs.nitem; v += G) {
+    for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
       vec_item(p, S, 1, j, S.jjob[jx], nt, v, sl, vs.S, 4 * nIc * S.jw[jx]);
@@ -929,7 +936,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
     gsync();
     T.tick(5);
     // pass 2: w' = w - V h1 (stored), h2_i = vdot(V_i, w') -> area 1
-    for (int v = b; v < vs.nitem; v += G) {
+    for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
       vec_item(p, S, 2, j, S.jjob[jx], nt, v, sl, vs.S, 4 * nIc * S.jw[jx]);
@@ -938,7 +945,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
     gsync();
     T.tick(5);
     // pass 3: w'' = w' - V h2 (stored), ||w''||^2 -> area 2
-    for (int v = b; v < vs.nitem; v += G) {
+    for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
       vec_item(p, S, 3, j, S.jjob[jx], nt, v, sl, vs.S, 4 * nIc * S.jw[jx]);
@@ -948,7 +955,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
     T.tick(5);
     // pass 4: hn = ||w''||, V_{j+1} = w'' / hn; the Hessenberg column h1 + h2, hn and the Givens step of
     // every active instance on the owner (slice 0) of its (job, n-tile)
-    for (int v = b; v < vs.nitem; v += G) {
+    for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
       vec_item(p, S, 4, j, S.jjob[jx], nt, v, sl, vs.S, 4 * nIc * S.jw[jx]);
@@ -961,16 +968,16 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
   refresh(true);
   {
     const VSplit vs = vsplit(S, J, G, 2 * nIc * p.wmax);
-    for (int v = b; v < vs.nitem; v += G) {
+    for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
       const int job = S.jjob[jx], w = S.jw[jx], half = 2 * nIc * w;
       const int q = tid & 7, r = nt * 8 + q;
-      __syncthreads();
+      cbar();
       // the triangle H[0..k)[0..k) and g[0..k) of the 8 instances staged in shared memory (k <= 12: packed
       // column-major after g in S.gv[q]), then the back substitution runs on thread q without L2 round trips
       if (tid < 8) S.yv[tid][33] = make_double2((double)(nt * 8 + tid < p.R ? max(0, __ldcg(p.iters + job * p.R + nt * 8 + tid)) : 0), 0.0);
-      __syncthreads();
+      cbar();
       for (int t = tid; t < 8 * 102; t += II_T) {
         const int q2 = t / 102, e = t - q2 * 102;
         const int k2 = (int)S.yv[q2][33].x;
@@ -986,7 +993,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
           *dst = ld_cg(H + (size_t)m * hld + (f - m * (m + 1) / 2));  // H[i][m], i = f - m(m+1)/2
         }
       }
-      __syncthreads();
+      cbar();
       if (tid < 8) {
         const int k = (int)S.yv[q][33].x;
         const bool sm = k <= 12;
@@ -1011,7 +1018,7 @@ __global__ void __launch_bounds__(II_T, 1) inner_items_kernel(const InnerParams 
           atomicAdd(&p.counters[2], 1ULL);
         }
       }
-      __syncthreads();
+      cbar();
       const int k = (int)S.yv[q][33].x;
       const int e0 = (int)((long long)sl * half / vs.S), e1 = (int)((long long)(sl + 1) * half / vs.S);
       double2* out = p.tr + (size_t)(job * p.R + (r < p.R ? r : 0)) * nIc * 2 * p.wmax;
@@ -1063,14 +1070,14 @@ cudaError_t inner_items_launch(const InnerParams& p0, int J, cudaStream_t st) {
   set_smem_attr((const void*)inner_items_kernel, sm);
   static int per_sm = -1;
   if (per_sm < 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_items_kernel, II_T, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inner_items_kernel, II_TB, sm);
     cudaGetLastError();
   }
   if (per_sm < 1) return cudaErrorNotSupported;
   int j_ = J;
   void* args[] = {(void*)&p, (void*)&j_};
   const int grid = p.coop_sms > 0 ? std::min(nsm, p.coop_sms) : nsm;
-  return cudaLaunchCooperativeKernel((const void*)inner_items_kernel, dim3(grid), dim3(II_T), args, sm, st);
+  return cudaLaunchCooperativeKernel((const void*)inner_items_kernel, dim3(grid), dim3(II_TB), args, sm, st);
 }
 
 void inner_items_trace_dump(const char* tag) {
