@@ -258,10 +258,20 @@ __device__ __forceinline__ void issue_chunk_warp(const InnerParams& p, const IIS
 }
 
 // ---------------------------------------------------------------------------------------- warp product
+__device__ __forceinline__ void flip_sign(double (&acc)[2][2][8]) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        acc[a][b][e] = __longlong_as_double(__double_as_longlong(acc[a][b][e]) ^ (long long)0x8000000000000000ULL);
+}
+
 // One chunk of a tile for this warp: its (WM x WN <= 2 x 2) pairs over k-steps [ks0, ks1).  wm / wn are
 // warp-uniform runtime values (one code path keeps the hot loop small).
 __device__ __forceinline__ void chunk_mma(const double2* A, const double2* B, int kc, int terms, int wm, int wn,
-                                          int wmi, int wni, int ks0, int ks1, int kv, int two, double sg,
+                                          int wmi, int wni, int ks0, int ks1, int kv, int two,
                                           double (&acc)[2][2][8], int mvalid, int nvalid) {
   const int lane = threadIdx.x & 31, r8 = lane >> 2, kl = lane & 3;
   const bool m1 = wm > 1 && wmi * wm + 1 < mvalid, n1 = wn > 1 && wni * wn + 1 < nvalid;
@@ -286,8 +296,6 @@ __device__ __forceinline__ void chunk_mma(const double2* A, const double2* B, in
         if (two) b1 = cadd(b1, B0[bstride + (kc + k) * 8]);
       }
     }
-    b0 = make_double2(b0.x * sg, b0.y * sg);
-    b1 = make_double2(b1.x * sg, b1.y * sg);
     dmma4(acc[0][0], a0.x, a0.y, b0.x, b0.y);
     if (wn > 1) dmma4(acc[0][1], a0.x, a0.y, b1.x, b1.y);
     if (wm > 1) {
@@ -415,7 +423,10 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[a][bb][e] = 0.0;
     for (int si = 0, q = 0; si < d.ns; ++si) {
-      const double sg = (d.negs >> si & 1) ? -1.0 : 1.0;
+      // a negated slot panel (exact): accumulate into -C, i.e. C - A B, by flipping the accumulators' sign bits
+      // before and after the slot (integer ops: the FP64 pipe is shared with DMMA)
+      const bool neg = d.negs >> si & 1;
+      if (neg) flip_sign(acc);
       const int two = d.twos >> si & 1;
       for (int kcn = 0; kcn < d.nkc; ++kcn, ++q) {
         const int slot = done % nslot;
@@ -424,7 +435,7 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
         X.ev(3, done);
         const double2* A = ring + (size_t)slot * se;
         const double2* B = A + (size_t)c.mtc * kc * 8;
-        chunk_mma(A, B, kc, terms, c.wm, c.wn, wmi, wni, ks0, ks1, min(kc, d.w - kcn * kc), two, sg, acc,
+        chunk_mma(A, B, kc, terms, c.wm, c.wn, wmi, wni, ks0, ks1, min(kc, d.w - kcn * kc), two, acc,
                   d.mvalid, d.nvalid);
         __syncwarp();
         // relaxed: a release arrive would first wait for every outstanding memory operation of the thread
@@ -432,6 +443,7 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
         ++done;
         X.ev(4, done);
       }
+      if (neg) flip_sign(acc);
     }
     T.tick(1);
     // ---- partial tiles -> shared memory: red[kp][pair][row * 8 + col], pair = mtl * NTC + ntl

@@ -60,11 +60,14 @@ __global__ void __launch_bounds__(GS_WARPS * 32) k_green_samples(
 // each row tile's K = (slot, column) range is split over GS2_KQ warps (A loads of a warp issued 8 k-steps
 // at a time), every A fragment serves all GS2_NG RHS groups, and the partial tiles are summed in a fixed
 // order by the kq = 0 warp.  Same products as green_item; the sum over K is split in GS2_KQ parts.
+// KQ = 1, TPC = 8 (one warp per row tile over the whole K, eight row tiles per CTA): the staged trace panels
+// serve 8 row tiles instead of 2 (cfg5 64 RHS: 263 -> 157 us per sweep-stage launch; KQ 4 / TPC 2 was tuned on
+// cfg2's 16 RHS in round 1)
 #ifndef GS2_KQ
-#define GS2_KQ 4
+#define GS2_KQ 1
 #endif
 #ifndef GS2_TPC
-#define GS2_TPC 2
+#define GS2_TPC 8
 #endif
 #ifndef GS2_NG
 #define GS2_NG 2
