@@ -233,20 +233,22 @@ __device__ __forceinline__ TileDesc tile_desc(const InnerParams& p, const IIShar
 // mt0 + a, lane 8 + 2 b + t the panel term t of n-tile nt0 + b; lane 0 arms the slot's barrier with the
 // chunk's byte count (complete_tx may land before the arm: the phase cannot complete while the arm's arrival
 // is pending).  One round of independent bulk copies per chunk, no per-copy serial address work.
+// parts: bit 0 = arm the barrier with the whole chunk's bytes and copy the Green rows (operator data, may be
+// issued before the grid barrier of the phase that produces the panels), bit 1 = copy the panels.
 __device__ __forceinline__ void issue_chunk_warp(const InnerParams& p, const IIShared& S, const TileCfg& c, int kc,
                                                  int terms, const TileDesc& d, int si, int kcn, double2* slotp,
-                                                 uint64_t* bar, const int vmap[3]) {
+                                                 uint64_t* bar, const int vmap[3], int parts = 3) {
   const int lane = threadIdx.x & 31;
   const int s = d.slots >> (2 * si) & 3, two = d.twos >> si & 1;
   const int k0 = kcn * kc, kv = min(kc, d.w - k0);
   const uint32_t bytes = (uint32_t)kv * 128u;
-  if (lane == 0) mbar_expect_tx_relaxed(bar, bytes * (uint32_t)(d.mvalid + d.nvalid * (1 + two)));
+  if ((parts & 1) && lane == 0) mbar_expect_tx_relaxed(bar, bytes * (uint32_t)(d.mvalid + d.nvalid * (1 + two)));
   const IItem& item = S.items[d.ii];
-  if (lane < d.mvalid) {
+  if ((parts & 1) && lane < d.mvalid) {
     const long long goff = __ldg(&p.cells[S.jlay[d.jx] * p.Lc + item.cell].green_off);
     bulk_g2s(slotp + (size_t)lane * kc * 8,
              p.green + goff + ((size_t)(item.row * 4 + s) * d.nmt + d.mt0 + lane) * d.w * 8 + (size_t)k0 * 8, bytes, bar);
-  } else if (lane >= 8 && lane < 8 + 2 * d.nvalid) {
+  } else if ((parts & 2) && lane >= 8 && lane < 8 + 2 * d.nvalid) {
     const int bq = (lane - 8) >> 1, t = (lane - 8) & 1;
     if (t <= two) {
       const Ref r = item.pan[s][t];
@@ -279,6 +281,19 @@ __device__ __forceinline__ void chunk_mma(const double2* A, const double2* B, in
   const double2* A0 = A + (size_t)(wmi * wm) * kc * 8 + r8;
   const double2* B0 = B + (size_t)(wni * wn) * terms * kc * 8 + r8;
   const int bstride = terms * kc * 8;  // next n-tile's panel
+  if (wm == 2 && wn == 2 && m1 && n1 && !two && ks1 * 4 <= kv) {
+    // the common full 2 x 2 block of single-term panels over whole k-steps: no predicates, deeper unroll
+#pragma unroll 4
+    for (int ks = ks0; ks < ks1; ++ks) {
+      const int k8 = (ks * 4 + kl) * 8;
+      const double2 a0 = A0[k8], a1 = A0[kc * 8 + k8], b0 = B0[k8], b1 = B0[bstride + k8];
+      dmma4(acc[0][0], a0.x, a0.y, b0.x, b0.y);
+      dmma4(acc[0][1], a0.x, a0.y, b1.x, b1.y);
+      dmma4(acc[1][0], a1.x, a1.y, b0.x, b0.y);
+      dmma4(acc[1][1], a1.x, a1.y, b1.x, b1.y);
+    }
+    return;
+  }
 #pragma unroll 2
   for (int ks = ks0; ks < ks1; ++ks) {
     const int k = ks * 4 + kl;
@@ -339,6 +354,23 @@ __device__ __forceinline__ int phase_config(const IIShared& S, int J, int nit, i
 // empty-barrier parities, one bit per physical slot.
 struct Ring {
   uint32_t fpar, epar;
+  uint32_t owed;  // producer: slots holding a chunk whose release it has not waited for yet
+  int pre;        // producer: chunks of the coming phase whose Green rows were issued before its grid barrier
+};
+
+// producer warp: make slot `slot` free (wait for the release of the chunk it holds, if any)
+__device__ __forceinline__ void slot_claim(IIShared& S, Ring& rg, int slot) {
+  if (rg.owed >> slot & 1u) {
+    if ((threadIdx.x & 31) == 0) mbar_wait_suspend(&S.empty[slot], (rg.epar >> slot) & 1u);
+    __syncwarp();
+    rg.epar ^= 1u << slot;
+  }
+  rg.owed |= 1u << slot;
+}
+
+// the next phase of the same iteration (its Green rows can be prefetched across the grid barrier)
+struct NextPhase {
+  int it0, nit, cfg, phase_id;  // nit < 0: none
 };
 
 // One program phase over every job's active n-tiles; vmap: program vector ids {0 IN, 1 OUT, 2 AUX} ->
@@ -346,7 +378,7 @@ struct Ring {
 // empty barrier) and consumes like every other warp; there is no CTA-wide barrier per chunk.
 __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double2* ring, double2* red, int J,
                                        int it0, int nit, int wphase, int pcfg, int phase_id, const int vmap[3],
-                                       Ring& rg, IITick& T, IITrace& X) {
+                                       NextPhase nx, Ring& rg, IITick& T, IITrace& X) {
   const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, b = blockIdx.x;
   // ---- config: minimise (tile rounds) x (cycles of one tile at its warp block's DMMA rate + a fixed per-tile cost)
@@ -360,10 +392,11 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
   const int nslot = min(II_NSLOT, (int)(II_RING / (se * 16u)));
   // the B panels were written by other CTAs (generic proxy) before the grid barrier; order those writes
   // before this CTA's bulk (async-proxy) reads
-  if (wp == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (wp == 8) asm volatile("fence.proxy.async.global;" ::: "memory");  // the producer issues the copies
   // ---- warp 8: the producer.  Walks this CTA's tiles and chunks in the consumers' order, waits for a slot's 8
   // consumer warps to release it (empty barrier), then issues the chunk's bulk copies, one lane per copy.
   if (wp == 8) {
+    // chunks [0, rg.pre) were armed and their Green rows issued during the previous phase: their panels now
     int issued = 0;
     for (int t = b; t < ntiles; t += G) {
       const TileRef r = tile_decode(S, cfg, J, t);
@@ -372,12 +405,44 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
       for (int si = 0; si < d.ns; ++si)
         for (int kcn = 0; kcn < d.nkc; ++kcn) {
           const int slot = issued % nslot;
-          if (lane == 0) mbar_wait_suspend(&S.empty[slot], (rg.epar >> slot) & 1u);
-          __syncwarp();
-          rg.epar ^= 1u << slot;
-          issue_chunk_warp(p, S, c, kc, terms, d, si, kcn, ring + (size_t)slot * se, &S.full[slot], vmap);
+          if (issued < rg.pre) {
+            issue_chunk_warp(p, S, c, kc, terms, d, si, kcn, ring + (size_t)slot * se, &S.full[slot], vmap, 2);
+          } else {
+            slot_claim(S, rg, slot);
+            issue_chunk_warp(p, S, c, kc, terms, d, si, kcn, ring + (size_t)slot * se, &S.full[slot], vmap);
+          }
           ++issued;
         }
+    }
+    rg.pre = 0;
+    if (nx.nit > 0) {
+      // every slot released (the next phase's ring layout may differ), then the next phase's first chunks: arm +
+      // Green rows; their panels follow after the grid barrier
+      for (int i = 0; i < II_NSLOT; ++i)
+        if (rg.owed >> i & 1u) {
+          if (lane == 0) mbar_wait_suspend(&S.empty[i], (rg.epar >> i) & 1u);
+          __syncwarp();
+          rg.epar ^= 1u << i;
+        }
+      rg.owed = 0;
+      const TileCfg c2 = II_CFG[nx.cfg];
+      const int terms2 = S.phtwo[nx.phase_id] ? 2 : 1;
+      const int kc2 = cfg_kc(c2, terms2);
+      const uint32_t se2 = slot_elems(c2, kc2, terms2);
+      const int nslot2 = min(II_NSLOT, (int)(II_RING / (se2 * 16u)));
+      const int ntiles2 = S.tpre[nx.cfg][J] * nx.nit;
+      int n = 0;
+      for (int t = b; t < ntiles2 && n < nslot2; t += G) {
+        const TileRef r = tile_decode(S, nx.cfg, J, t);
+        if (S.ins[nx.it0 + r.ii] == 0) continue;
+        const TileDesc d = tile_desc(p, S, c2, kc2, r, nx.it0);
+        for (int si = 0; si < d.ns && n < nslot2; ++si)
+          for (int kcn = 0; kcn < d.nkc && n < nslot2; ++kcn, ++n) {
+            rg.owed |= 1u << n;
+            issue_chunk_warp(p, S, c2, kc2, terms2, d, si, kcn, ring + (size_t)n * se2, &S.full[n], vmap, 1);
+          }
+      }
+      rg.pre = n;
     }
     return;
   }
@@ -742,8 +807,6 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
     fence_mbar_init();
   }
   __syncthreads();
-  if ((tid & 31) == 0 && tid < II_T)  // every slot starts free: complete phase 0 of its empty barrier
-    for (int i = 0; i < II_NSLOT; ++i) mbar_arrive(&S.empty[i]);
   IITick T;
   T.on = p.tprof && blockIdx.x == 0 && tid == 0;
   T.start();
@@ -754,7 +817,7 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
     grid.sync();
     t_wait += clock64() - t0;
   };
-  Ring rg{0u, 0u};
+  Ring rg{0u, 0u, 0u, 0};
   IITrace X;
   X.on = p.ii_trace > 0 && (int)blockIdx.x == p.ii_trace - 1 && tid == 0;
   X.n = 0;
@@ -821,10 +884,18 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
     }
     __syncthreads();
   };
-  auto program = [&](const int* ph_d, int nph, int phw0, const int vm[3]) {
+  // one program; `then_pre`: the preconditioner program follows in the same iteration (its first phase's Green
+  // rows are prefetched across the op program's last grid barrier)
+  auto program = [&](const int* ph_d, int nph, int phw0, const int vm[3], bool then_pre) {
     for (int phz = 0; phz < nph; ++phz) {
       const int i0 = ph_d[phz], i1 = ph_d[phz + 1];
-      run_phase(p, S, ring, red, J, i0, i1 - i0, S.phw[phw0 + phz], S.phcfg[phw0 + phz], phw0 + phz, vm, rg, T, X);
+      NextPhase nx{0, -1, 0, 0};
+      if (phz + 1 < nph) {
+        nx = NextPhase{ph_d[phz + 1], ph_d[phz + 2] - ph_d[phz + 1], S.phcfg[phw0 + phz + 1], phw0 + phz + 1};
+      } else if (then_pre) {
+        nx = NextPhase{p.pre_ph[0], p.pre_ph[1] - p.pre_ph[0], S.phcfg[p.op_nph], p.op_nph};
+      }
+      run_phase(p, S, ring, red, J, i0, i1 - i0, S.phw[phw0 + phz], S.phcfg[phw0 + phz], phw0 + phz, vm, nx, rg, T, X);
       T.count(8);
       X.ev(7, phz);
       gsync();
@@ -864,7 +935,7 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
   // ---- b = pre(rhs) (krylov.py:61)
   {
     const int vm[3] = {VB, VY, VA};
-    program(p.pre_ph, p.pre_nph, p.op_nph, vm);
+    program(p.pre_ph, p.pre_nph, p.op_nph, vm, false);
   }
   // ---- beta0 = ||b||, V_0 = b / beta0, g[0] = beta0 (krylov.py:63-86)
   {
@@ -933,9 +1004,9 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
     }
     {
       const int vm1[3] = {j, VT, VA};
-      program(p.op_ph, p.op_nph, 0, vm1);  // VT = op(V_j)
+      program(p.op_ph, p.op_nph, 0, vm1, true);  // VT = op(V_j)
       const int vm2[3] = {VT, j + 1, VA};
-      program(p.pre_ph, p.pre_nph, p.op_nph, vm2);  // V_{j+1} = w = pre(op(V_j))
+      program(p.pre_ph, p.pre_nph, p.op_nph, vm2, false);  // V_{j+1} = w = pre(op(V_j))
     }
     const VSplit vs = vsplit(S, J, G, 4 * nIc * p.wmax);
     // pass 1: h1_i = vdot(V_i, w), i <= j -> area 0
