@@ -18,7 +18,8 @@
  *   pt_layer_solve  NestedLayerSolver.solve (nested.py:344-353), one layer, nrhs volumes:
  *                   the "layer object" protocol of sie.py:112-118 (test/plugin hook).
  *   pt_cell_solve   LayerWorkspace.solve on one cell (subdomain.py:214-221 -> SuperLU
- *                   solve): the K1 kernel alone (test hook).
+ *                   solve): the K1 kernel alone (test hook); pt_cell_solve_device: the same on
+ *                   device buffers, the many-RHS solves of the offline stage (green.py:103-129).
  *   pt_set_stream / pt_set_profiling: run on a caller stream (e.g. torch's) / time every launch.
  *   pt_residuals_stride: per-RHS length of the residual-history buffer for a Krylov config.
  *   pt_destroy / pt_last_error / pt_version.
@@ -67,7 +68,8 @@ typedef struct {
   const double* const* lz;   /* [L*Lc] -> [wz_c] complex block sub-diagonal scalars  */
   const double* const* uz;   /* [L*Lc] -> [wz_c] complex block super-diagonal scalars */
   const double* const* sinv; /* [L*Lc] -> [wz_c][w][w] complex Schur inverses, column-major blocks */
-  const double* const* green;/* [L*Lc] -> [4 rows][4 slots][w][w] complex, column-major blocks */
+  const double* const* green;/* [L*Lc] -> [4 rows][4 slots][w][w] complex, column-major blocks; NULL = a
+                              * factor-only context for pt_cell_solve(_device) (the offline stage) */
   /* optional (NULL: sampled outputs come from a second cell-solve pass):
    * [L*Lc] -> [wz_c][4 layer trace rows 0,1,n,n+1][4 slots][w] complex, the trace-source
    * response H_c^{-1}(coef_s E_krow_s) sampled at every block row and the layer trace rows */
@@ -157,6 +159,10 @@ int pt_layer_solve(pt_ctx* ctx, int layer, const double* rhs, int nrhs, double i
                    int inner_max_iter, double* out, pt_stats* stats);
 /* cell (layer, c): x = H_c^{-1} b for nrhs right-hand sides [nrhs][wz_c][w] (host) */
 int pt_cell_solve(pt_ctx* ctx, int layer, int cell, const double* b, int nrhs, double* x);
+/* the same with device-resident b / x (K1 on the context's stream, synchronised on return).  The offline stage
+ * runs GreenBlockSet.build (green.py:103-129, nested.py:296-307: 4 w unit-source solves per cell) and the
+ * pass-0 / sampled-response operators through this entry on a factor-only context (pt_problem.green == NULL) */
+int pt_cell_solve_device(pt_ctx* ctx, int layer, int cell, const double* b_dev, int nrhs, double* x_dev);
 
 /* entries per RHS of pt_stats.residuals: max_iter + 1 for GMRES (krylov.py:53-135), 2 max_iter + 1 for
  * BiCGstab (krylov.py:138-201: the initial 1.0 plus two half steps per iteration) */

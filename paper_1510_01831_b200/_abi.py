@@ -34,6 +34,7 @@ EXPORTS = (
     "pt_solve_device",
     "pt_layer_solve",
     "pt_cell_solve",
+    "pt_cell_solve_device",
     "pt_residuals_stride",
     "pt_last_error",
     "pt_version",
@@ -98,12 +99,13 @@ def load():
     lib.pt_layer_solve.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_double, C.c_int, _dp,
                                    C.POINTER(PtStats)]
     lib.pt_cell_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _dp]
+    lib.pt_cell_solve_device.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
     lib.pt_residuals_stride.argtypes = [C.POINTER(PtKrylov)]
     lib.pt_residuals_stride.restype = C.c_int
     lib.pt_last_error.restype = C.c_char_p
     lib.pt_version.restype = C.c_char_p
     for name in ("pt_create", "pt_destroy", "pt_solve", "pt_solve_device", "pt_layer_solve",
-                 "pt_cell_solve", "pt_set_stream", "pt_set_profiling"):
+                 "pt_cell_solve", "pt_cell_solve_device", "pt_set_stream", "pt_set_profiling"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -153,8 +155,8 @@ class Context:
         pb.cell_coefs = dptr(arr(np.stack([cf.coefs for cf in cells]), np.complex128))
         ptr_arrays = {}
         for name in ("lz", "uz", "sinv", "green", "gsmp", "q0"):
-            if name in ("gsmp", "q0") and any(getattr(cf, name, None) is None for cf in cells):
-                continue  # optional: the cell-solve passes produce these outputs
+            if name in ("green", "gsmp", "q0") and any(getattr(cf, name, None) is None for cf in cells):
+                continue  # optional: the cell-solve passes produce these outputs (no green: factor-only context)
             P = (_dp * nid)()
             for i, cf in enumerate(cells):
                 v = getattr(cf, name)

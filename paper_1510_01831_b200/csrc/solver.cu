@@ -1942,7 +1942,9 @@ static int create_impl(pt_ctx* c, const pt_problem* pb, int device, pt_ctx** out
                       sizeof(double2) * (size_t)ci.w * ci.w, sizeof(double2) * (size_t)ci.w * ci.w, ci.wzc,
                       cudaMemcpyDefault));
     }
-    {
+    if (!pb->green) {  // factor-only context (the offline stage's own cell solves): no interface operators yet
+      CK(cudaMemset(c->green_d + ci.green_off, 0, sizeof(double2) * 16 * (size_t)((ci.w + 7) / 8) * 8 * ci.w));
+    } else {
       double2* tmp = nullptr;
       CK(cudaMalloc(&tmp, sizeof(double2) * 16 * (size_t)ci.w * ci.w));
       CK(cudaMemcpy(tmp, pb->green[id], sizeof(double2) * 16 * (size_t)ci.w * ci.w, cudaMemcpyDefault));
@@ -2294,15 +2296,16 @@ int pt_layer_solve(pt_ctx* c, int layer, const double* rhs, int nrhs, double inn
   return ecode;
 }
 
-int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, double* x) {
-  if (!c || layer < 0 || layer >= c->L || cell < 0 || cell >= c->Lc || nrhs <= 0) return PT_BAD_ARGUMENT;
+// K1 alone on device-resident volumes: x = H_c^{-1} b for nrhs right-hand sides [nrhs][wz_c][w], on the
+// context's stream (synchronised before returning).  The offline stage builds the Green blocks and the
+// operators of the online restructuring through this entry (offline.py, green.py:103-129 as many-RHS solves).
+int pt_cell_solve_device(pt_ctx* c, int layer, int cell, const double* b_dev, int nrhs, double* x_dev) {
+  if (!c || !b_dev || !x_dev || layer < 0 || layer >= c->L || cell < 0 || cell >= c->Lc || nrhs <= 0)
+    return PT_BAD_ARGUMENT;
   CK(cudaSetDevice(c->dev));
   const CellInfo& ci = c->cel[layer * c->Lc + cell];
-  const size_t bytes = sizeof(double2) * (size_t)nrhs * ci.wzc * ci.w;
-  double2 *bd = nullptr, *xd = nullptr;
-  CK(cudaMalloc(&bd, bytes));
-  CK(cudaMalloc(&xd, bytes));
-  CK(cudaMemcpy(bd, b, bytes, cudaMemcpyHostToDevice));
+  double2* bd = reinterpret_cast<double2*>(const_cast<double*>(b_dev));
+  double2* xd = reinterpret_cast<double2*>(x_dev);
   std::vector<K1Task> tasks;
   long long z = 0;
   const int nc = std::getenv("PT_K1_NC") ? atoi(std::getenv("PT_K1_NC")) : 8;
@@ -2366,11 +2369,29 @@ int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, dou
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  CK(cudaMemcpy(x, xd, bytes, cudaMemcpyDeviceToHost));
-  cudaFree(bd);
-  cudaFree(xd);
   cudaFree(td);
   return PT_OK;
+}
+
+int pt_cell_solve(pt_ctx* c, int layer, int cell, const double* b, int nrhs, double* x) {
+  if (!c || !b || !x || layer < 0 || layer >= c->L || cell < 0 || cell >= c->Lc || nrhs <= 0) return PT_BAD_ARGUMENT;
+  CK(cudaSetDevice(c->dev));
+  const CellInfo& ci = c->cel[layer * c->Lc + cell];
+  const size_t bytes = sizeof(double2) * (size_t)nrhs * ci.wzc * ci.w;
+  double2 *bd = nullptr, *xd = nullptr;
+  CK(cudaMalloc(&bd, bytes));
+  if (cudaMalloc(&xd, bytes) != cudaSuccess) {
+    cudaFree(bd);
+    g_err = "pt_cell_solve: out of device memory";
+    return PT_CUDA_ERROR;
+  }
+  int rc = cudaMemcpy(bd, b, bytes, cudaMemcpyHostToDevice) == cudaSuccess ? PT_OK : PT_CUDA_ERROR;
+  if (rc == PT_OK)
+    rc = pt_cell_solve_device(c, layer, cell, reinterpret_cast<const double*>(bd), nrhs, reinterpret_cast<double*>(xd));
+  if (rc == PT_OK && cudaMemcpy(x, xd, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) rc = PT_CUDA_ERROR;
+  cudaFree(bd);
+  cudaFree(xd);
+  return rc;
 }
 
 }  // extern "C"

@@ -443,12 +443,97 @@ def _reference_cells(ref, nxc_list, w, npml):
     return [Hc]
 
 
+def _k1_layer_operators(grid, lf, Lc, cext, coffs, device, green, q0, ref):
+    """Green blocks, sampled trace responses and pass-0 operators of one layer's cells as many-RHS solves with
+    the repo's own cell-solve kernel K1 (``csrc/k1_cell_solve.cu`` through ``pt_cell_solve_device``).
+
+    This is ``GreenBlockSet.build`` (``green.py:103-129``, called per cell at ``nested.py:303-307``): the
+    reference solves ``H_c x = coef_slot e_j`` at the slot row for the ``w`` unit vectors of each of the four
+    slots with the cell's SuperLU factors (``subdomain.py:205-221``); here the ``4 w`` unit sources of a cell are
+    one K1 launch on the twisted Schur factors already resident on the device (a one-layer, factor-only context:
+    ``pt_problem.green == NULL``), and the blocks are row samples of the solutions.  The operators of the online
+    restructuring come from the same solves (``gsmp``: every block row of those solutions at the layer trace
+    rows) and from a second launch (``q0``: the ``4 nk`` layer slot sources of the kept block rows).
+    """
+    import ctypes as C
+
+    from . import _abi
+
+    npml, w, n = grid.npml, lf.w, lf.n
+    wx = grid.nx + 2 * npml
+    zx = np.zeros(wx, dtype=np.complex128)
+    zz = np.zeros(w, dtype=np.complex128)
+    one = Factors(grid.nx, n, grid.h, npml, 0.0, 1, Lc, [lf], cext, coffs, (zx, zx, zx), (zz, zz, zz),
+                  np.zeros((w, wx)))
+    ctx = _abi.Context(one, device=device.index if device.index is not None else torch.cuda.current_device())
+    L_ = _abi.lib()
+    try:
+        jrows = [npml - 1, npml, n + npml - 1, n + npml]  # layer trace rows 0, 1, n, n+1 inside a block row
+        for ci, cf in enumerate(lf.cells):
+            wzc, nxc = cf.wzc, cf.nxc
+            rows4 = [int(r) for r in (cf.krows[1], cf.krows[0], cf.krows[3], cf.krows[2])]  # r0, r1, rn, rnp
+            ar = torch.arange(w, device=device)
+
+            def solve(B):
+                X = torch.empty_like(B)
+                rc = L_.pt_cell_solve_device(ctx.handle, 0, ci, C.c_void_p(B.data_ptr()), B.shape[0],
+                                             C.c_void_p(X.data_ptr()))
+                if rc != _abi.PT_OK:
+                    raise RuntimeError(f"pt_cell_solve_device failed ({rc}): {_abi.last_error()}")
+                return X
+
+            if green:
+                # right-hand side (slot s, column a): coef_s e_a at block row krow_s; K1 volumes are [rhs][wz_c][w]
+                B = torch.zeros((4, w, wzc, w), dtype=torch.complex128, device=device)
+                for s in range(4):
+                    B[s, ar, int(cf.krows[s]), ar] = complex(cf.coefs[s])
+                torch.cuda.synchronize(device)
+                X = solve(B.view(4 * w, wzc, w)).view(4, w, wzc, w)
+                del B
+                if ref is not None and hasattr(ref, "blocksets"):
+                    bs = ref.blocksets[ci]  # the reference's own GreenBlockSet matrices (green.py:103-129)
+                    cf.green = torch.stack([torch.stack([torch.as_tensor(
+                        np.asarray(bs.dense(jrow, slot)).T, dtype=torch.complex128, device=device)
+                        for slot in SLOTS]) for jrow in (0, 1, nxc, nxc + 1)]).contiguous()
+                else:
+                    # column-major block (row j, slot s): element (i, a) at a * w + i = X[s, a, row_j, i]
+                    cf.green = X[:, :, rows4, :].permute(2, 0, 1, 3).contiguous()
+                cf.gsmp = X[:, :, :, jrows].permute(2, 3, 0, 1).contiguous()  # (wzc, 4 trace rows, 4 slots, w)
+                del X
+            if q0:
+                lo = 0 if ci == 0 else npml
+                hi = wzc if ci == Lc - 1 else npml + nxc
+                nk = hi - lo
+                nk4 = (nk + 3) // 4 * 4
+                kk = torch.arange(nk, device=device)
+                B = torch.zeros((4, nk, wzc, w), dtype=torch.complex128, device=device)
+                for s in range(4):  # layer slot source s at kept block row lo + kk: coef_s at layer row prow_s
+                    B[s, kk, lo + kk, int(lf.prows[s])] = complex(lf.coefs[s])
+                torch.cuda.synchronize(device)
+                X = solve(B.view(4 * nk, wzc, w)).view(4, nk, wzc, w)
+                del B
+                qt = X[:, :, rows4, :].permute(2, 3, 0, 1).reshape(4 * w, 4, nk)
+                qs = X[:, :, lo:hi, :][:, :, :, jrows].permute(2, 3, 0, 1).reshape(4 * nk, 4, nk)
+                m = 4 * w + 4 * nk
+                mp = (m + 7) // 8 * 8
+                q = torch.zeros((mp, 4, nk4), dtype=torch.complex128, device=device)
+                q[:m, :, :nk] = torch.cat([qt, qs])
+                cf.q0 = q.reshape(mp, 4 * nk4)
+                del X
+    finally:
+        ctx.close()
+
+
 def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=None, inner_dense=None,
-                  backend="pt", reference_layers=None):
+                  backend="pt", reference_layers=None, cell_solver=None):
     """Offline stage for a partitioned problem (all layers, all cells).
 
     ``grid``/``model``/``pml``/``partition`` follow the reference value types
     (``discretization.py:58-220``, ``subdomain.py:51-73``).
+
+    ``cell_solver``: ``"k1"`` runs the unit-source cell solves of the Green blocks and of the pass-0 /
+    sampled-response operators on the device with the online stage's own K1 kernel (default on a CUDA device);
+    ``"torch"`` runs them as torch block substitutions (default on the CPU; the parity check of the K1 route).
 
     ``reference_layers``: the reference's own ``build_nested_layers`` output (``NestedLayerSolver`` objects,
     ``nested.py:272-319``) or its direct ``LayerWorkspace`` layers (``subdomain.py:202-236``, Lc = 1).  The
@@ -458,6 +543,13 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
     online restructuring are computed here.
     """
     device = torch.device(device)
+    if cell_solver is None:
+        cell_solver = "k1" if device.type == "cuda" else "torch"
+    if cell_solver not in ("k1", "torch"):
+        raise ValueError(f"unknown cell_solver {cell_solver!r}")
+    if cell_solver == "k1" and device.type != "cuda":
+        raise ValueError("cell_solver='k1' needs a CUDA device (the B200 kernels have no CPU fallback)")
+    use_k1 = cell_solver == "k1"
     if q0 is None:
         q0 = green
     if inner_dense is None:
@@ -517,7 +609,7 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
             sinv = _schur_inverses(tw, dg, lz, uz, device)
             gblk = None
             gsmp = None
-            if green:
+            if green and not use_k1:
                 # H_c^{-1} columns at the four slot rows, sampled at the four rows
                 rows4 = [int(r) for r in (ckrows[1], ckrows[0], ckrows[3], ckrows[2])]  # r0,r1,rn,rnp
                 eye = torch.eye(w, dtype=torch.complex128, device=device)
@@ -546,7 +638,7 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
                 gsmp = X[:, :, jrows, :].reshape(len(idxs), wzc, 4, 4, w).contiguous()
                 del X, rhs
             q0c = [None] * len(idxs)
-            if q0:
+            if q0 and not use_k1:
                 # responses to the layer slot sources at every block row: K_full = 4 wzc columns
                 rows4 = [int(r) for r in (ckrows[1], ckrows[0], ckrows[3], ckrows[2])]  # r0,r1,rn,rnp
                 jrows = [npml - 1, npml, n + npml - 1, n + npml]
@@ -584,6 +676,9 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
                     q0c[b],
                 )
         lf.cells = cells
+        if use_k1 and (green or q0):
+            del sinv, tinv, sinv_cm, dg
+            _k1_layer_operators(grid, lf, Lc, cext, coffs, device, green, q0, ref)
         if green and backend == "lu":
             lf.lu_inv = inner_lu_inverse(lf)
         elif green and inner_dense:

@@ -173,12 +173,14 @@ def from_reference_layers(layers, grid, model, pml, partition, device=None, inne
 def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), Lc=1, backend="pt",
                         inner_ktol=1e-6, inner_max_iter=200, plr_threshold=None, plr_eps=1e-8,
                         plr_max_rank=None, seed=0, assembled_boundary=False, device=None, inner_dense=None,
-                        reference_layers=None, **unused):
+                        reference_layers=None, cell_solver=None, **unused):
     """``nested.py:507-521`` (with ``NestedLayerSolver`` kwargs, ``nested.py:279-281``).
 
     Runs the offline stage (Schur factors + Green blocks) for every layer.
-    ``device`` selects where the offline arithmetic runs (``"cpu"`` or a CUDA
-    device for large configs); its output is uploaded by the solver.
+    ``device`` selects where the offline arithmetic runs: a CUDA device (the
+    default when one is present; the unit-source cell solves then run on the
+    K1 kernel, ``cell_solver="k1"``) or ``"cpu"`` (torch on the host, small
+    problems and CPU-only tests); its output is uploaded by the solver.
     ``inner_dense`` (None = by Lc) builds the dense inner operators that let
     the inner GMRES run as one dense product per step.
     """
@@ -192,8 +194,12 @@ def build_nested_layers(grid, model, pml, partition, disc=DiscretizationSpec(), 
         raise ValueError("need at least one cell")
     if Lc > 1 and grid.nx < 2 * Lc:
         raise ValueError(f"{Lc} cells need nx >= {2 * Lc}, got {grid.nx}")
-    F = build_factors(grid, model, pml, partition, Lc, device=device or "cpu", inner_dense=inner_dense,
-                      backend=backend, reference_layers=reference_layers)
+    if device is None:
+        import torch
+
+        device = f"cuda:{torch.cuda.current_device()}" if torch.cuda.is_available() else "cpu"
+    F = build_factors(grid, model, pml, partition, Lc, device=device, inner_dense=inner_dense,
+                      backend=backend, reference_layers=reference_layers, cell_solver=cell_solver)
     # assembled_boundary (nested.py:355-486): boundary samples through M_f -> inner solve -> direct + M_u.
     # This path's sample-only layer solves already are those linear maps (pass-0 operator = M_f and the
     # direct part, sampled trace response = M_u); the flag selects the reference's touch accounting.

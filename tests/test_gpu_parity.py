@@ -337,3 +337,30 @@ def test_solve_with_factors_built_from_reference_objects():
         assert abs(got.relative_residual - want.relative_residual) <= 1e-6 * want.relative_residual + 1e-14
     assert dev.global_operator() is H
     dev.close()
+
+
+@pytest.mark.parametrize("case", [dict(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3), "cfg1", "cfg2"])
+def test_offline_operators_by_k1_match_torch_block_substitution(case):
+    """the Green blocks (GreenBlockSet.build, green.py:103-129), sampled trace responses and
+    pass-0 operators built as many-RHS solves of the repo's own K1 kernel (cell_solver="k1", the default on a
+    CUDA device) equal the torch block substitution on the same device to 1e-12, and the reference construction
+    on the host."""
+    import torch
+
+    from paper_1510_01831_b200.offline import build_factors
+
+    prob = small_problem(**case) if isinstance(case, dict) else make_config(case)
+    args = (prob.grid, prob.model, prob.pml, prob.partition, prob.Lc)
+    Fk = build_factors(*args, device="cuda", cell_solver="k1")
+    Ft = build_factors(*args, device="cuda", cell_solver="torch")
+    Fh = build_factors(*args, device="cpu")
+    for lk, lt, lh in zip(Fk.layers, Ft.layers, Fh.layers):
+        for ck, ct, ch in zip(lk.cells, lt.cells, lh.cells):
+            for name in ("green", "gsmp", "q0"):
+                a, b, c = getattr(ck, name), getattr(ct, name), getattr(ch, name)
+                assert a.shape == b.shape and a.is_cuda
+                scale = float(torch.linalg.norm(b))
+                assert float(torch.linalg.norm(a - b)) <= 1e-12 * scale, (lk.index, ck.cell, name)
+                assert float(torch.linalg.norm(a.cpu() - c)) <= 1e-12 * scale, (lk.index, ck.cell, name)
+        if lt.dense is not None:
+            assert float(torch.linalg.norm(lk.dense - lt.dense)) <= 1e-11 * float(torch.linalg.norm(lt.dense))
