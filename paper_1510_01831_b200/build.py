@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpt_b200.so")
-SOURCES = ["k1_cell_solve.cu", "inner_gmres.cu", "inner_items.cu", "outer_kernels.cu", "solver.cu"]
+SOURCES = ["k1_cell_solve.cu", "inner_gmres.cu", "inner_items.cu", "outer_kernels.cu", "stage_gemm.cu", "solver.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

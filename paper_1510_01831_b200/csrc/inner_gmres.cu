@@ -1415,7 +1415,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) inner_coop_kernel(const InnerPa
     for (long long e = (long long)b * blockDim.x + tid; e < tot; e += (long long)G * blockDim.x)
       gather_elem(p.jobs, p.tab, p.rmap, p.R, p.wx, p.P, e);
     gsync();
-    const int mp8 = (4 * p.wmax + 4 * p.kmax + 7) / 8;
+    const int mp8 = q0_rows(p.wmax, p.kmax) / 8;
     const int gz0 = (p.maxj * p.R + P0_COLS - 1) / P0_COLS;
     const long long n0items = (long long)p.ngl * p.Lc * mp8 * gz0;
     const int half = wp_ >> 2;

@@ -45,7 +45,7 @@ namespace cg = cooperative_groups;
 #define II_MAXJ 64
 #define II_MAXNT 32
 #define II_SMAX 16     // element slices per (job, n-tile) in the vector phases
-#define II_MAXIT 160   // op + pre program items (staged in shared memory)
+#define II_MAXIT 320   // op + pre program items (staged in shared memory, compact form)
 #define II_MAXPH 256   // program phases
 #define II_JREG 4      // Arnoldi steps whose basis entries stay in registers (beyond: a slower loop)
 
@@ -98,6 +98,36 @@ struct IITick {  // fire-and-forget atomics: the timed thread never waits on the
   }
 };
 
+// program item as staged in shared memory: IItem with 16-bit references (vector id, segment)
+struct RefS {
+  short vec, seg;
+};
+struct IItemS {
+  short cell, row;
+  RefS pan[4][2];
+  RefS dst, add[2], sub[2], rev;
+  int flags;
+};
+__device__ __forceinline__ RefS refs(const Ref& r) { return RefS{(short)r.vec, (short)r.seg}; }
+__device__ __forceinline__ IItemS pack_item(const IItem& it) {
+  IItemS o;
+  o.cell = (short)it.cell;
+  o.row = (short)it.row;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    o.pan[s][0] = refs(it.pan[s][0]);
+    o.pan[s][1] = refs(it.pan[s][1]);
+  }
+  o.dst = refs(it.dst);
+  o.add[0] = refs(it.add[0]);
+  o.add[1] = refs(it.add[1]);
+  o.sub[0] = refs(it.sub[0]);
+  o.sub[1] = refs(it.sub[1]);
+  o.rev = refs(it.rev);
+  o.flags = it.flags;
+  return o;
+}
+
 struct IIShared {
   uint64_t full[II_NSLOT];
   uint64_t empty[II_NSLOT];  // one arrive per consumer warp
@@ -108,7 +138,7 @@ struct IIShared {
   int jw[II_MAXJ], jlay[II_MAXJ], jjob[II_MAXJ];
   int tpre[II_NCFG][II_MAXJ + 1];           // per config: prefix over jobs of CTA tiles per item
   unsigned char ins[II_MAXIT];              // slot count of every program item
-  IItem items[II_MAXIT];                    // the op + pre programs (staged once)
+  IItemS items[II_MAXIT];                   // the op + pre programs (staged once)
   // vector-phase staging (aliases the program phases' reduction buffer): per instance of a (job, n-tile)
   double2 (*gv)[3][34];                     // Givens: column, cs, sn / back substitution: g and triangle
   double2 (*yv)[34];                        // x = V y coefficients, [33] = k
@@ -217,7 +247,7 @@ __device__ __forceinline__ TileDesc tile_desc(const InnerParams& p, const IIShar
   d.nvalid = min(c.ntc, S.nact[r.jx] - d.nt0);
   d.ns = S.ins[d.ii];
   d.nkc = (d.w + kc - 1) / kc;
-  const IItem& item = S.items[d.ii];
+  const IItemS& item = S.items[d.ii];
   d.slots = d.twos = d.negs = 0;
   for (int s = 0, si = 0; s < 4; ++s)
     if (item.cell >= 0 && item.pan[s][0].vec >= 0) {
@@ -243,7 +273,7 @@ __device__ __forceinline__ void issue_chunk_warp(const InnerParams& p, const IIS
   const int k0 = kcn * kc, kv = min(kc, d.w - k0);
   const uint32_t bytes = (uint32_t)kv * 128u;
   if ((parts & 1) && lane == 0) mbar_expect_tx_relaxed(bar, bytes * (uint32_t)(d.mvalid + d.nvalid * (1 + two)));
-  const IItem& item = S.items[d.ii];
+  const IItemS& item = S.items[d.ii];
   if ((parts & 1) && lane < d.mvalid) {
     const long long goff = __ldg(&p.cells[S.jlay[d.jx] * p.Lc + item.cell].green_off);
     bulk_g2s(slotp + (size_t)lane * kc * 8,
@@ -251,7 +281,7 @@ __device__ __forceinline__ void issue_chunk_warp(const InnerParams& p, const IIS
   } else if ((parts & 2) && lane >= 8 && lane < 8 + 2 * d.nvalid) {
     const int bq = (lane - 8) >> 1, t = (lane - 8) & 1;
     if (t <= two) {
-      const Ref r = item.pan[s][t];
+      const RefS r = item.pan[s][t];
       const int nt = S.act[d.jx][d.nt0 + bq];
       bulk_g2s(slotp + ((size_t)c.mtc + bq * terms + t) * kc * 8,
                v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + k0) * 8, bytes, bar);
@@ -458,7 +488,7 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
     T.count(9);
     if (p.tprof && tid == 0 && b < 1024) atomicAdd(&g_ii_tiles[b], 1ULL);
     const TileDesc d = tile_desc(p, S, c, kc, tile_decode(S, cfg, J, t), it0);
-    const IItem& item = S.items[d.ii];
+    const IItemS& item = S.items[d.ii];
     const int npair = c.mtc * c.ntc;
     // combine operands of this thread's first output, fetched before the products (one output per thread covers
     // the small tiles of the latency-bound phases; larger tiles load theirs in the epilogue)
@@ -469,7 +499,7 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
     double2 pre_add = czero(), pre_sub = czero(), pre_rev = czero();
     if (own0) {
       const int nt = S.act[d.jx][d.nt0 + nl0], q = pos0 & 7;
-      auto opnd = [&](Ref r) { return ld_cg(v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + grow0) * 8 + q); };
+      auto opnd = [&](RefS r) { return ld_cg(v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + grow0) * 8 + q); };
       if (item.add[0].vec >= 0) {
         pre_add = opnd(item.add[0]);
         if (item.add[1].vec >= 0) pre_add = cadd(pre_add, opnd(item.add[1]));
@@ -539,7 +569,7 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
         for (int k = 0; k < c.kw; ++k) y = cadd(y, red[((size_t)k * npair + pr) * 64 + pos]);
       double2 av = pre_add, sv = pre_sub, rv = pre_rev;
       if (o != o0) {
-        auto opnd = [&](Ref r) { return ld_cg(v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + grow) * 8 + q); };
+        auto opnd = [&](RefS r) { return ld_cg(v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + grow) * 8 + q); };
         av = sv = rv = czero();
         if (item.add[0].vec >= 0) {
           av = opnd(item.add[0]);
@@ -830,7 +860,7 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
   S.gv = reinterpret_cast<double2(*)[3][34]>(red);
   S.yv = reinterpret_cast<double2(*)[34]>(red + 8 * 3 * 34);
   for (int i = tid; i < p.nitems; i += II_TB) {
-    S.items[i] = p.items[i];
+    S.items[i] = pack_item(p.items[i]);
     S.ins[i] = (unsigned char)item_ns_g(p.items[i]);
   }
   __syncthreads();
@@ -1146,6 +1176,15 @@ cudaError_t inner_items_launch(const InnerParams& p0, int J, cudaStream_t st) {
       p0.part_items < inner_items_part_items(nsm, J, p0.R))
     return cudaErrorNotSupported;
   InnerParams p = p0;
+  // single-job stages (the sequential outer sweeps): the scan form of the GS sweeps, 2 ceil(log2 nI) + 1
+  // phases per preconditioner application instead of 2 nI - 1 (PT_SCAN_MAXR: up to this many RHS, default all)
+  static const int scan_maxr = std::getenv("PT_SCAN_MAXR") ? atoi(std::getenv("PT_SCAN_MAXR")) : 1 << 30;
+  if (J == 1 && p.pre_nph_px > 0 && p.items_px && p.R <= scan_maxr && p.nitems_px <= II_MAXIT) {
+    p.items = p.items_px;
+    p.pre_ph = p.pre_ph_px;
+    p.pre_nph = p.pre_nph_px;
+    p.nitems = p.nitems_px;
+  }
   const int NT = (p.R + 7) / 8;
   p.s2_vec = (long long)NT * p.nmax * 8;
   p.s2_job = (long long)(p.cap + 5) * p.s2_vec;

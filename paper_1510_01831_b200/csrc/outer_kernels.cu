@@ -475,9 +475,51 @@ __global__ void k_vol_norm2(const double2* f, long long stride, long long N, dou
 
 // Green blocks, column-major [16 blocks][w cols][w rows] -> tile-major [16][ceil(w/8)][w][8]
 // (rows >= w zero-padded), the layout the inner kernel streams with one bulk copy per tile.
-__global__ void k_green_tiles(const double2* src, double2* dst, int w) {
+// pass-0 operator rows: ABI order (4 w table rows, then (k, o) k-major) -> device order (q0_rows, pt_device.cuh)
+__global__ void k_q0_rows(const double2* src, double2* dst, int w, int nk, int K) {
+  const int tab8 = q0_tab8(w), nk8 = q0_nk8(nk);
+  const long long tot = (long long)q0_rows(w, nk) * K;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(e / K), k = (int)(e - (long long)m * K);
+    long long srow = -1;
+    if (m < 4 * w) {
+      srow = m;
+    } else if (m >= tab8) {
+      const int mm = m - tab8, oi = mm / nk8, kk = mm - oi * nk8;
+      if (kk < nk) srow = 4LL * w + 4LL * kk + oi;
+    }
+    dst[e] = srow >= 0 ? src[srow * K + k] : make_double2(0.0, 0.0);
+  }
+}
+
+// C = A B for 2 x 2 block matrices of column-major w x w blocks ([s][k][w*w]; element (i, j) of a block at
+// j * w + i): C[s][k] = sum_m A[s][m] B[m][k].  Offline products of the scan-form inner sweeps (solver.cu).
+// grid (ceil(w/16), ceil(w/16), 4), block (16, 16).
+__global__ void k_block2_mm(const double2* A, const double2* B, double2* C, int w) {
+  __shared__ double2 as[16][17], bs[16][17];
+  const int sb = blockIdx.z >> 1, kb = blockIdx.z & 1;
+  const int i = blockIdx.x * 16 + threadIdx.x, j = blockIdx.y * 16 + threadIdx.y;
+  const size_t W = (size_t)w * w;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int m = 0; m < 2; ++m) {
+    const double2* Ab = A + (size_t)(sb * 2 + m) * W;
+    const double2* Bb = B + (size_t)(m * 2 + kb) * W;
+    for (int t0 = 0; t0 < w; t0 += 16) {
+      const int ta = t0 + threadIdx.y, tb = t0 + threadIdx.x;
+      as[threadIdx.y][threadIdx.x] = (i < w && ta < w) ? Ab[(size_t)ta * w + i] : make_double2(0.0, 0.0);
+      bs[threadIdx.y][threadIdx.x] = (tb < w && j < w) ? Bb[(size_t)j * w + tb] : make_double2(0.0, 0.0);
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < 16; ++t) cfma(acc, as[t][threadIdx.x], bs[threadIdx.y][t]);
+      __syncthreads();
+    }
+  }
+  if (i < w && j < w) C[(size_t)(sb * 2 + kb) * W + (size_t)j * w + i] = acc;
+}
+
+__global__ void k_green_tiles(const double2* src, double2* dst, int w, int nb) {
   const int nmt = (w + 7) >> 3;
-  const long long total = 16LL * nmt * w * 8;
+  const long long total = (long long)nb * nmt * w * 8;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(e & 7);
@@ -541,8 +583,9 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
                                  const int* rmap) {
   const int fuse_combine = tab != nullptr;
   const VecTab tabv = tab ? *tab : VecTab{};
-  (void)num_sms;
   if (J == 0 || R == 0) return cudaSuccess;
+  if (R >= stage_gemm_min_cols())  // many RHS: the streaming tensor-core GEMM (stage_gemm.cu)
+    return sample_gemm_launch(jobs, J, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax, kmax, num_sms, st, tab, rmap);
   const int gy = (R + 7) / 8;
   // rows per cell <= kmax kept block rows x 4 output rows; one 8-row tile per warp
   const int gz = (kmax * 4 + 8 * GS_WARPS - 1) / (8 * GS_WARPS);
@@ -576,8 +619,18 @@ cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJ
                          int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st,
                          int accum, const VecTab* tab, const int* rmap, const RhsOut* rhs_out) {
   if (ngroups == 0 || R == 0) return cudaSuccess;
+  if (!tab && max_jobs_per_layer * R >= stage_gemm_min_cols()) {  // many columns: stage_gemm.cu
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return pass0_gemm_launch(grp, ngroups, ljobs, jobs, cells, layers, q0, P, tables, smp, R, Lc, wx, wmax, kmax,
+                             max_jobs_per_layer, nsm, st, accum, rhs_out);
+  }
   const VecTab tabv = tab ? *tab : VecTab{};
-  const int mp = (4 * wmax + 4 * kmax + 7) / 8 * 8;
+  const int mp = q0_rows(wmax, kmax);
   const int gz = (max_jobs_per_layer * R + P0_COLS - 1) / P0_COLS;
   const RhsOut ro = rhs_out ? *rhs_out : RhsOut{nullptr, 0, 0};
   // k-loop variant: (slot, k) advanced incrementally across the used slots (default) or per-slot segments with

@@ -46,6 +46,14 @@ struct CellInfo {
   long long q0_off;       // double2 offset into the pass-0 operator pool (-1: none)
 };
 
+// Device row layout of a cell's pass-0 operator (pt_problem.q0 rows are (4 w table rows, then (kept row k, output
+// row o) k-major); the upload regroups the sample rows by output row so whole 8-row tiles of an output row that no
+// job samples are skipped): [4 w Newton-table rows | zero rows up to q0_tab8] then, for o = 0..3 (layer rows 0, 1,
+// n, n+1), q0_nk8 rows (o, k) of which the first nk are real.
+__host__ __device__ inline int q0_tab8(int w) { return (4 * w + 7) & ~7; }
+__host__ __device__ inline int q0_nk8(int nk) { return (nk + 7) & ~7; }
+__host__ __device__ inline int q0_rows(int w, int nk) { return q0_tab8(w) + 4 * q0_nk8(nk); }
+
 // A reference to one panel (segment) of a vector: vec < 0 = absent.
 struct Ref {
   int vec, seg;

@@ -111,6 +111,10 @@ struct InnerParams {
   long long s2_vec, s2_job;  // double2 strides of one vector / one job (set by the launcher)
   double2* part;             // vector-phase partials [3][part_items][cap + 2][8]
   long long part_items;
+  // scan form of the preconditioner program (single-job stages; solver.cu build_inner): op items + scan pre items
+  const IItem* items_px;
+  const int* pre_ph_px;
+  int pre_nph_px, nitems_px;
   int ii_dbg;                // PT_II_DBG timing switches of inner_items.cu (results invalid when set)
   int ii_trace;              // PT_II_TRACE: event trace of CTA (ii_trace - 1), thread 0
 };
@@ -167,6 +171,16 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
                                  int wmax, int kmax, int num_sms, cudaStream_t st, const VecTab* tab = nullptr,
                                  const int* rmap = nullptr);
 
+// many-RHS forms of the two products above as one streaming tensor-core GEMM kernel (stage_gemm.cu)
+int stage_gemm_min_cols();
+cudaError_t sample_gemm_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
+                               const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx, int wmax,
+                               int kmax, int num_sms, cudaStream_t st, const VecTab* tab, const int* rmap);
+cudaError_t pass0_gemm_launch(const int* grp, int ngroups, const int* ljobs, const OJob* jobs, const CellInfo* cells,
+                              const LayerInfo* layers, const double2* q0, const double2* P, double2* tables,
+                              double2* smp, int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer,
+                              int num_sms, cudaStream_t st, int accum, const RhsOut* rhs_out);
+
 __global__ void k_gather_panels(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
                                 double2* P);
 __global__ void k_combine(const OJob* jobs, int njobs, VecTab t, const int* rmap, int nq, int wx,
@@ -191,4 +205,6 @@ __global__ void k_residual(const double2* u, const double2* f, long long stride,
                            const double2* tz, const double* m, double omega2, const int* rmap, double* out,
                            const double2* hdiag);
 __global__ void k_vol_norm2(const double2* f, long long stride, long long N, double* out);
-__global__ void k_green_tiles(const double2* src, double2* dst, int w);
+__global__ void k_green_tiles(const double2* src, double2* dst, int w, int nb);
+__global__ void k_block2_mm(const double2* A, const double2* B, double2* C, int w);
+__global__ void k_q0_rows(const double2* src, double2* dst, int w, int nk, int K);

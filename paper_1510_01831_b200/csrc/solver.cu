@@ -105,6 +105,12 @@ struct pt_ctx {
   int *op_ph_d = nullptr, *pre_ph_d = nullptr;
   int op_nph = 0, pre_nph = 0, nitems = 0;
   long long op_blocks = 0, pre_blocks = 0;
+  // scan form of the inner GS sweeps (single-job stages; see build_inner): product blocks in the Green pool and a
+  // second preconditioner program
+  int scan_levels = 0;  // product levels stored per cell (strides 2, 4, ...); 0 = none
+  IItem* items_px_d = nullptr;
+  int* pre_ph_px_d = nullptr;
+  int pre_nph_px = 0, nitems_px = 0;
   // outer stages
   Stage newton, op, refl, recon, layer_solve;
   std::vector<Stage> sdown, sup;  // sdown[I] for I=1..nI-1, sup[I] for I=0..nI-2
@@ -546,6 +552,118 @@ static int build_inner(pt_ctx* c) {
   if (upload(&c->items_d, items.data(), items.size())) return PT_CUDA_ERROR;
   if (upload(&c->op_ph_d, oph.data(), oph.size())) return PT_CUDA_ERROR;
   if (upload(&c->pre_ph_d, pph.data(), pph.size())) return PT_CUDA_ERROR;
+  // ---- PRE, scan form.  The down sweep y_I = T_I y_{I-1} - v_I (sie.py:272-283 on the cells; T_I the 2 x 2 block
+  // matrix of cell I's Green blocks (rows n, n+1; slots v0, v1)) is a linear recurrence: with the products
+  // T^(2)_I = T_I T_{I-1}, T^(4)_I = T^(2)_I T^(2)_{I-2}, ... (create_impl) every y_I follows in ceil(log2 nI)
+  // data-parallel levels  d_I <- T^(st)_I d_{I-st} + d_I  (st = 1, 2, 4, ...; d_I starts as -v_I) instead of
+  // nI - 1 dependent phases; likewise the up sweep (sie.py:285-296) with U_I (rows 0, 1; slots vn, vnp of cell
+  // I + 1).  Same linear map as the sequential program (rounding order aside), 2 levels + 1 phases per
+  // application instead of 2 nI - 1: used where a stage is one job (the sequential outer sweeps), whose phases are
+  // latency-bound.  An index's value ping-pongs between its OUT segment and a spare AUX segment so that no level
+  // writes what another item of the level reads; the last update of every index lands in OUT.
+  if (c->scan_levels > 0 && nI >= 3) {
+    std::vector<IItem> px(items.begin(), items.begin() + oph.back());  // the op program, unchanged
+    std::vector<int> ph;
+    int nlev = 0;
+    while ((1 << nlev) < nI) ++nlev;  // strides 1 .. 2^(nlev-1)
+    if (nlev - 1 > c->scan_levels) return 0;
+    struct Cur {
+      Ref r[2];
+      bool neg;
+    };
+    auto nupd = [](int dist) {  // updates of an index at distance dist >= 1 from the chain start
+      int n = 0;
+      while ((1 << n) <= dist) ++n;
+      return n;
+    };
+    // one chain: down (dir 0: index I, predecessor I - st, start I = 0) or up (dir 1: predecessor I + st, start nI - 1)
+    auto chain = [&](int dir, std::vector<Cur>& cur) {
+      std::vector<int> done(nI, 0);
+      for (int lv = 0; lv < nlev; ++lv) {
+        const int st = 1 << lv;
+        std::vector<Cur> nxt = cur;
+        for (int I = 0; I < nI; ++I) {
+          const int dist = dir == 0 ? I : nI - 1 - I;
+          if (dist < st) continue;
+          const int Pd = dir == 0 ? I - st : I + st;
+          const int cell = dir == 0 ? I : I + 1;
+          const int n = nupd(dist), k = ++done[I];
+          for (int sb = 0; sb < 2; ++sb) {
+            IItem x = item(cell, lv == 0 ? (dir == 0 ? 2 + sb : sb) : 4 + (lv - 1) * 2 + sb);
+            for (int kk = 0; kk < 2; ++kk) {
+              const int slot = dir == 0 ? kk : 2 + kk;
+              x.pan[slot][0] = cur[Pd].r[kk];
+              if (cur[Pd].neg) x.flags |= 1 << slot;
+            }
+            if (cur[I].neg) x.sub[0] = cur[I].r[sb];
+            else x.add[0] = cur[I].r[sb];
+            const bool to_out = ((n - k) & 1) == 0;
+            x.dst = to_out ? Ref{1, dir == 0 ? D(I, sb) : U(I, sb)} : Ref{2, D(I, sb)};
+            nxt[I].r[sb] = x.dst;
+            px.push_back(x);
+          }
+          nxt[I].neg = false;
+        }
+        cur = nxt;
+        ph.push_back((int)px.size());
+      }
+    };
+    ph.push_back((int)px.size());
+    // phase 0 of the down chain also holds y_down[0] = -v_down[0]
+    for (int sb = 0; sb < 2; ++sb) {
+      IItem x = item(-1, 0);
+      x.dst = Ref{1, D(0, sb)};
+      x.sub[0] = Ref{0, D(0, sb)};
+      px.push_back(x);
+    }
+    {
+      std::vector<Cur> cur(nI);
+      for (int I = 0; I < nI; ++I) cur[I] = Cur{{Ref{0, D(I, 0)}, Ref{0, D(I, 1)}}, true};  // d_I = -v_I (IN)
+      chain(0, cur);
+    }
+    // reflections (sie.py:298-308) in one phase on the finished y_down; s = p - refl -> AUX, y_up[nI-1] -> OUT
+    for (int I = 0; I < nI; ++I)
+      for (int sb = 0; sb < 2; ++sb) {
+        IItem x = item(I + 1, sb);
+        x.pan[0][0] = Ref{1, D(I, 0)};
+        x.pan[1][0] = Ref{1, D(I, 1)};
+        if (I <= nI - 2) {
+          x.pan[2][0] = Ref{1, D(I + 1, 0)};
+          x.pan[3][0] = Ref{1, D(I + 1, 1)};
+        }
+        if (sb == 1) x.sub[0] = Ref{1, D(I, 1)};
+        x.rev = Ref{0, U(I, sb)};
+        if (I == nI - 1) {
+          x.dst = Ref{1, U(I, sb)};
+          x.flags |= 2 << 8;
+        } else {
+          x.dst = Ref{2, U(I, sb)};
+          x.flags |= 1 << 8;
+        }
+        px.push_back(x);
+      }
+    ph.push_back((int)px.size());
+    {
+      std::vector<Cur> cur(nI);
+      for (int I = 0; I < nI; ++I) cur[I] = Cur{{Ref{2, U(I, 0)}, Ref{2, U(I, 1)}}, true};  // e_I = -s_I (AUX)
+      cur[nI - 1] = Cur{{Ref{1, U(nI - 1, 0)}, Ref{1, U(nI - 1, 1)}}, false};               // y_up[nI-1] (OUT)
+      chain(1, cur);
+    }
+    for (IItem& x : px) {
+      int ns = 0;
+      if (x.cell >= 0)
+        for (int k = 0; k < 4; ++k) ns += x.pan[k][0].vec >= 0;
+      x.wgt = ns > 0 ? ns : 1;
+    }
+    // phase offsets: ph[0] = first pre item; the y_down[0] items belong to the first level's phase
+    std::vector<int> pph2;
+    pph2.push_back(ph[0]);
+    for (size_t i = 1; i < ph.size(); ++i) pph2.push_back(ph[i]);
+    c->pre_nph_px = (int)pph2.size() - 1;
+    c->nitems_px = (int)px.size();
+    if (upload(&c->items_px_d, px.data(), px.size())) return PT_CUDA_ERROR;
+    if (upload(&c->pre_ph_px_d, pph2.data(), pph2.size())) return PT_CUDA_ERROR;
+  }
   return 0;
 }
 
@@ -740,6 +858,10 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   ip.pre_blocks = c->pre_blocks;
   ip.tprof = std::getenv("PT_INNER_TPROF") != nullptr;
   ip.nitems = c->nitems;
+  ip.items_px = c->items_px_d;
+  ip.pre_ph_px = c->pre_ph_px_d;
+  ip.pre_nph_px = c->pre_nph_px;
+  ip.nitems_px = c->nitems_px;
   ip.mg = inner_mg(c->wmax);
   ip.tring = inner_tring(c->wmax, ip.nitems);
   static const bool arn_slow = std::getenv("PT_ARN_SLOW") != nullptr;
@@ -778,9 +900,21 @@ static void stage_work(pt_ctx* c, Stage& S) {
     const int nsl = __builtin_popcount(used);
     for (int cc = 0; cc < c->Lc; ++cc) {
       const CellInfo& ci = c->cel[l * c->Lc + cc];
-      const int nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3, Mp = (4 * ci.w + 4 * nk + 7) & ~7;
-      S.p0_fpr += 8.0 * Mp * nsl * nk4 * (e - b);
-      S.p0_bytes += 16.0 * Mp * nsl * nk4;
+      // executed rows: the Newton-table rows and, per job, the sample rows of the output rows it samples (whole
+      // tiles of the others are skipped); operator bytes: the rows some job of the group needs
+      const int nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3;
+      int oall = 0;
+      double rows_j = 0;
+      for (int jj = b; jj < e; ++jj) {
+        const OJob& jo = S.jobs[S.ljobs[jj]];
+        int om = 0;
+        for (int o = 0; o < jo.nout; ++o)
+          om |= 1 << (jo.orow[o] == 0 ? 0 : (jo.orow[o] == 1 ? 1 : (jo.orow[o] == c->lay[l].n ? 2 : 3)));
+        oall |= om;
+        rows_j += q0_tab8(ci.w) + (double)__builtin_popcount(om) * q0_nk8(nk);
+      }
+      S.p0_fpr += 8.0 * rows_j * nsl * nk4;
+      S.p0_bytes += 16.0 * (q0_tab8(ci.w) + (double)__builtin_popcount(oall) * q0_nk8(nk)) * nsl * nk4;
       if (!seen[l]) S.in_bytes += 16.0 * 16.0 * ci.w * ci.w;
     }
     seen[l] = 1;
@@ -1870,6 +2004,15 @@ static int create_impl(pt_ctx* c, const pt_problem* pb, int device, pt_ctx** out
     g_err = "layer extents do not sum to nz";
     return PT_BAD_ARGUMENT;
   }
+  // scan form of the inner GS sweeps (build_inner): product blocks T^(2), T^(4), ... of the cells' transfer
+  // matrices follow the 16 Green blocks of every cell (rows 4 + 2 (level - 1) + s, slots = [down k0, k1, up k0, k1]).
+  // Item-program layers only (no dense / direct inner operators); PT_NO_SCAN keeps the sequential sweeps.
+  c->scan_levels = 0;
+  if (pb->green && !pb->inner_dense && !pb->inner_lu && c->Lc >= 4 && !std::getenv("PT_NO_SCAN")) {
+    int nlev = 0;
+    while ((1 << nlev) < c->Lc - 1) ++nlev;
+    c->scan_levels = nlev - 1;
+  }
   // cells
   long long soff = 0, goff = 0, zoff = 0, gsoff = 0, q0off = 0;
   c->wzcmax = 0;
@@ -1916,12 +2059,12 @@ static int create_impl(pt_ctx* c, const pt_problem* pb, int device, pt_ctx** out
       gsoff += 16LL * ci.wzc * ci.w;
       {
         const int nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3;
-        const long long mp = (4LL * ci.w + 4LL * nk + 7) / 8 * 8;
+        const long long mp = q0_rows(ci.w, nk);  // device row layout
         ci.q0_off = pb->q0 ? q0off : -1;
         q0off += mp * 4 * nk4;
       }
       soff += (long long)ci.wzc * ci.w * ((ci.w + 3) & ~3);  // blocks padded to a multiple of 4 columns
-      goff += 16LL * ((ci.w + 7) / 8) * 8 * ci.w;  // tile-major, rows padded to 8
+      goff += (16LL + 8LL * c->scan_levels) * ((ci.w + 7) / 8) * 8 * ci.w;  // tile-major, rows padded to 8
       zoff += ci.wzc;
       c->wzcmax = std::max(c->wzcmax, ci.wzc);
       c->cel.push_back(ci);
@@ -1948,7 +2091,7 @@ static int create_impl(pt_ctx* c, const pt_problem* pb, int device, pt_ctx** out
       double2* tmp = nullptr;
       CK(cudaMalloc(&tmp, sizeof(double2) * 16 * (size_t)ci.w * ci.w));
       CK(cudaMemcpy(tmp, pb->green[id], sizeof(double2) * 16 * (size_t)ci.w * ci.w, cudaMemcpyDefault));
-      k_green_tiles<<<256, 256>>>(tmp, c->green_d + ci.green_off, ci.w);
+      k_green_tiles<<<256, 256>>>(tmp, c->green_d + ci.green_off, ci.w, 16);
       CK(cudaGetLastError());
       CK(cudaDeviceSynchronize());
       cudaFree(tmp);
@@ -1958,11 +2101,71 @@ static int create_impl(pt_ctx* c, const pt_problem* pb, int device, pt_ctx** out
                     cudaMemcpyDefault));
     if (pb->q0) {
       const int nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3;
-      const long long mp = (4LL * ci.w + 4LL * nk + 7) / 8 * 8;
-      CK(cudaMemcpy(c->q0_d + ci.q0_off, pb->q0[id], sizeof(double2) * (size_t)(mp * 4 * nk4), cudaMemcpyDefault));
+      const long long mp = (4LL * ci.w + 4LL * nk + 7) / 8 * 8;  // rows of the ABI array
+      double2* tmp = nullptr;
+      CK(cudaMalloc(&tmp, sizeof(double2) * (size_t)(mp * 4 * nk4)));
+      CK(cudaMemcpy(tmp, pb->q0[id], sizeof(double2) * (size_t)(mp * 4 * nk4), cudaMemcpyDefault));
+      k_q0_rows<<<512, 256>>>(tmp, c->q0_d + ci.q0_off, ci.w, nk, 4 * nk4);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+      cudaFree(tmp);
     }
     CK(cudaMemcpy(c->lz_d + ci.lz_off, pb->lz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
     CK(cudaMemcpy(c->uz_d + ci.lz_off, pb->uz[id], sizeof(double2) * ci.wzc, cudaMemcpyDefault));
+  }
+  if (c->scan_levels > 0) {
+    const int nI = c->Lc - 1;
+    for (int l = 0; l < c->L; ++l) {
+      const int w = c->lay[l].w;
+      const size_t W = (size_t)w * w, W4 = 4 * W;
+      // level matrices [dir][I][s][k][w*w], column-major blocks: dir 0 = T_I (cell I: rows n, n+1; slots v0, v1),
+      // dir 1 = U_I (cell I + 1: rows 0, 1; slots vn, vnp)
+      double2 *cur = nullptr, *nxt = nullptr, *tmp8 = nullptr;
+      CK(cudaMalloc(&cur, sizeof(double2) * 2 * nI * W4));
+      CK(cudaMalloc(&nxt, sizeof(double2) * 2 * nI * W4));
+      CK(cudaMalloc(&tmp8, sizeof(double2) * 8 * W));
+      CK(cudaMemset(cur, 0, sizeof(double2) * 2 * nI * W4));
+      for (int cc = 1; cc <= c->Lc - 2; ++cc) {
+        const double2* g = reinterpret_cast<const double2*>(pb->green[l * c->Lc + cc]);  // [4 rows][4 slots][w*w]
+        for (int sb = 0; sb < 2; ++sb) {
+          CK(cudaMemcpy(cur + (size_t)cc * W4 + (size_t)sb * 2 * W, g + (size_t)((2 + sb) * 4 + 0) * W,
+                        sizeof(double2) * 2 * W, cudaMemcpyDefault));
+          CK(cudaMemcpy(cur + (size_t)(nI + cc - 1) * W4 + (size_t)sb * 2 * W, g + (size_t)(sb * 4 + 2) * W,
+                        sizeof(double2) * 2 * W, cudaMemcpyDefault));
+        }
+      }
+      const dim3 mg((w + 15) / 16, (w + 15) / 16, 4), mb(16, 16);
+      for (int lv = 1; lv <= c->scan_levels; ++lv) {
+        const int st = 1 << (lv - 1);  // stride of the factors; the products have stride 2 st
+        CK(cudaMemset(nxt, 0, sizeof(double2) * 2 * nI * W4));
+        for (int I = 2 * st; I <= nI - 1; ++I)  // T^(2st)_I = T^(st)_I T^(st)_{I - st}
+          k_block2_mm<<<mg, mb>>>(cur + (size_t)I * W4, cur + (size_t)(I - st) * W4, nxt + (size_t)I * W4, w);
+        for (int I = 0; I <= nI - 1 - 2 * st; ++I)  // U^(2st)_I = U^(st)_I U^(st)_{I + st}
+          k_block2_mm<<<mg, mb>>>(cur + (size_t)(nI + I) * W4, cur + (size_t)(nI + I + st) * W4,
+                                  nxt + (size_t)(nI + I) * W4, w);
+        CK(cudaGetLastError());
+        for (int cc = 0; cc < c->Lc; ++cc) {
+          const CellInfo& ci = c->cel[l * c->Lc + cc];
+          CK(cudaMemsetAsync(tmp8, 0, sizeof(double2) * 8 * W));
+          for (int sb = 0; sb < 2; ++sb) {
+            if (cc >= 2 * st && cc <= nI - 1)
+              CK(cudaMemcpyAsync(tmp8 + (size_t)(sb * 4 + 0) * W, nxt + (size_t)cc * W4 + (size_t)sb * 2 * W,
+                                 sizeof(double2) * 2 * W, cudaMemcpyDeviceToDevice));
+            if (cc - 1 >= 0 && cc - 1 <= nI - 1 - 2 * st)
+              CK(cudaMemcpyAsync(tmp8 + (size_t)(sb * 4 + 2) * W, nxt + (size_t)(nI + cc - 1) * W4 + (size_t)sb * 2 * W,
+                                 sizeof(double2) * 2 * W, cudaMemcpyDeviceToDevice));
+          }
+          const size_t blk = (size_t)((ci.w + 7) / 8) * 8 * ci.w;  // one tile-major block
+          k_green_tiles<<<256, 256>>>(tmp8, c->green_d + ci.green_off + (16 + 8 * (size_t)(lv - 1)) * blk, ci.w, 8);
+          CK(cudaGetLastError());
+        }
+        std::swap(cur, nxt);
+      }
+      CK(cudaDeviceSynchronize());
+      cudaFree(cur);
+      cudaFree(nxt);
+      cudaFree(tmp8);
+    }
   }
   // dense inner operators (optional): [L] x [2][n][n], n = 4 nI w
   if (pb->inner_dense && c->Lc > 1) {
@@ -2076,7 +2279,7 @@ int pt_destroy(pt_ctx* c) {
   // the process-level allocations are released with the context
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
   for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->dense_d, (void*)c->lu_d, (void*)c->lz_d,
-                  (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->hd_d, (void*)c->items_d,
+                  (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->hd_d, (void*)c->items_d, (void*)c->items_px_d, (void*)c->pre_ph_px_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
                   (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->tables_f,
                   (void*)c->trc, (void*)c->Z, (void*)c->iscr, (void*)c->hess, (void*)c->iters, (void*)c->istate,
@@ -2308,7 +2511,8 @@ int pt_cell_solve_device(pt_ctx* c, int layer, int cell, const double* b_dev, in
   double2* xd = reinterpret_cast<double2*>(x_dev);
   std::vector<K1Task> tasks;
   long long z = 0;
-  const int nc = std::getenv("PT_K1_NC") ? atoi(std::getenv("PT_K1_NC")) : 8;
+  // 8 columns per cluster pair (the DMMA path) where K1's epilogue holds them (8 w <= 4 K1_CONSUMERS), else 4
+  const int nc = std::getenv("PT_K1_NC") ? atoi(std::getenv("PT_K1_NC")) : (8 * c->wmax <= 4 * K1_CONSUMERS ? 8 : 4);
   for (int q0 = 0; q0 < nrhs; q0 += nc) {  // one cluster pair per nc columns (cm = 1)
     K1Task t;
     t.cell = layer * c->Lc + cell;

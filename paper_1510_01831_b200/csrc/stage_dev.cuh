@@ -70,10 +70,22 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
   const CellInfo& ci = cells[layer * Lc + c];
   const LayerInfo& lay = layers[layer];
   const int w = ci.w, nk = ci.hi - ci.lo, nk4 = (nk + 3) & ~3, K = 4 * nk4;
-  const int M = 4 * w + 4 * nk, Mp = (M + 7) & ~7;
+  const int tab8 = q0_tab8(w), nk8 = q0_nk8(nk), Mp = tab8 + 4 * nk8;  // device row layout (pt_device.cuh)
   const int lane = threadIdx.x & 31, wp = wq;
   const int N = nj * R, n0 = z * P0_COLS;
   if (n0 >= N || tile * 8 >= Mp) return;
+  if (tile * 8 >= tab8) {  // a sample tile of output row oi: skipped when no job of these columns samples that row
+    const int oi_t = (tile * 8 - tab8) / nk8;
+    bool need = false;
+    for (int jj = n0 / R; jj < nj && jj * R < n0 + P0_COLS; ++jj) {
+      const OJob& jo = jobs[ljobs[jb0 + jj]];
+      for (int o = 0; o < jo.nout; ++o) {
+        const int orow = jo.orow[o];
+        need |= (orow == 0 ? 0 : (orow == 1 ? 1 : (orow == lay.n ? 2 : 3))) == oi_t;
+      }
+    }
+    if (!need) return;
+  }
   const int ngq = min(2, (N - n0 + 7) >> 3);
   const int ar = lane >> 2, ak = lane & 3;
   const double2* arow = q0 + ci.q0_off + (size_t)(tile * 8 + ar) * K + ak;
@@ -208,7 +220,7 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
       for (int t = 0; t < 4; ++t) acc[gq][t] += part[((p2 * 2 + gq) * 4 + t) * 32 + lane];
   // C fragment: row ar of the tile, columns 2 ak, 2 ak + 1 of each group
   const int m = tile * 8 + ar;
-  if (m >= M) return;
+  if (m >= 4 * w && (m < tab8 || (m - tab8) % nk8 >= nk)) return;  // padding rows
 #pragma unroll
   for (int gq = 0; gq < 2; ++gq) {
     if (gq >= ngq) continue;
@@ -233,7 +245,7 @@ __device__ __forceinline__ void pass0_item(const int* __restrict__ grp, const in
                 make_double2(-tv.x, -tv.y);
         }
       } else {
-        const int mm = m - 4 * w, kk = mm >> 2, oi = mm & 3;
+        const int mm = m - tab8, oi = mm / nk8, kk = mm - oi * nk8;
         const OJob& jb = jobs[jid];
         for (int o = 0; o < jb.nout; ++o) {
           const int orow = jb.orow[o];

@@ -56,6 +56,9 @@ SWITCHES = {
     "fused-glue": {"PT_FUSE_GLUE": "1"},
     "fused-stage": {"PT_FUSE": "1"},
     "recon-k1": {"PT_NO_REUSE": "1"},
+    # the many-RHS streaming GEMM of the pass-0 product and the sampled response for every column count
+    "stage-gemm": {"PT_SGEMM_MIN": "1"},
+    "stage-gemm-items": {"PT_SGEMM_MIN": "1", "PT_NO_DENSE": "1"},
 }
 
 
