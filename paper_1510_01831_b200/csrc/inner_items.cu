@@ -1168,10 +1168,13 @@ cudaError_t inner_items_launch(const InnerParams& p0, int J, cudaStream_t st) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   static const bool v1 = std::getenv("PT_ITEMS_V1") != nullptr;  // the per-8-RHS-unit kernel instead
-  // a single-job stage with one n-tile of RHS (a 1-RHS sweep stage) keeps the per-8-RHS-unit kernel by
-  // default: its per-phase latency is lower there (PT_ITEMS_ALL=1 selects this kernel for every stage)
+  // a single-job stage with one n-tile of RHS (a 1-RHS sweep stage) runs here with the scan form of the sweeps
+  // (cfg5 1 RHS: 998 ms per solve against 1180 ms on the per-8-RHS-unit kernel, 8 RHS 1071 against 1305 ms);
+  // without the scan program the per-8-RHS-unit kernel's per-phase latency is lower (1343 ms here):
+  // PT_ITEMS_ALL=1 selects this kernel for every stage regardless
   static const bool all = std::getenv("PT_ITEMS_ALL") != nullptr;
-  if (v1 || (!all && J < 2 && p0.R <= 8) || p0.dense || !p0.part || J < 1 || J > II_MAXJ || p0.R > II_MAXNT * 8 || p0.cap > 32 || p0.Lc < 2 ||
+  const bool scan = p0.pre_nph_px > 0 && p0.items_px && p0.nitems_px <= II_MAXIT;
+  if (v1 || (!all && !scan && J < 2 && p0.R <= 8) || p0.dense || !p0.part || J < 1 || J > II_MAXJ || p0.R > II_MAXNT * 8 || p0.cap > 32 || p0.Lc < 2 ||
       p0.nitems > II_MAXIT || p0.op_nph + p0.pre_nph > II_MAXPH ||
       p0.part_items < inner_items_part_items(nsm, J, p0.R))
     return cudaErrorNotSupported;

@@ -149,6 +149,37 @@ class Factors:
         return sum(cf.green.numel() * 16 for lf in self.layers for cf in lf.cells)
 
 
+class _Timer:
+    """Wall-clock totals of the offline phases (``PT_OFFLINE_TIMES=1`` prints them; device work is synchronised
+    at every mark, so the switch serialises the stage)."""
+
+    def __init__(self, device):
+        import os
+
+        self.on = bool(os.environ.get("PT_OFFLINE_TIMES"))
+        self.device = device
+        self.tot = {}
+        self.t = None
+
+    def mark(self, name=None):
+        if not self.on:
+            return
+        import time
+
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
+        now = time.perf_counter()
+        if name is not None and self.t is not None:
+            self.tot[name] = self.tot.get(name, 0.0) + now - self.t
+        self.t = now
+
+    def report(self):
+        if self.on:
+            import sys
+
+            sys.stderr.write("offline times: " + ", ".join(f"{k} {v:.2f}s" for k, v in self.tot.items()) + "\n")
+
+
 def _split(n, parts):
     base, rem = divmod(n, parts)
     return tuple(base + 1 if i < rem else base for i in range(parts))
@@ -524,6 +555,47 @@ def _k1_layer_operators(grid, lf, Lc, cext, coffs, device, green, q0, ref):
         ctx.close()
 
 
+def _batched_twisted_factors(grid, model, pml, partition, Lc, cext, coffs, device, tm, budget=24e9):
+    """Twisted Schur factors of every cell, the recursion batched over ALL cells of equal shape (layer depth n,
+    cell extent nx_c) across the layers: the block couplings depend only on (n, nx_c), so a config has a handful
+    of shapes (cfg5: 4) and the ``wz_c`` dependent inversion steps run on hundreds of cells at once instead of
+    once per layer.  Returns ``{(layer, cell): (wz_c, w, w) column-major twisted factors}``; ``budget`` bounds the
+    bytes of one batch's temporaries."""
+    npml, h, omega = grid.npml, grid.h, pml.omega
+    c = np.asarray(model.c, dtype=float)
+    shapes = {}
+    for ell, (n, off) in enumerate(zip(partition.extents, partition.offsets)):
+        for ci, nxc in enumerate(cext):
+            shapes.setdefault((n, nxc), []).append((ell, off, ci))
+    out = {}
+    for (n, nxc), lst in shapes.items():
+        w, wzc = n + 2 * npml, nxc + 2 * npml
+        if wzc < 3:
+            raise ValueError("cells need at least 3 block rows (nx_c + 2 npml >= 3)")
+        tw = axis_tridiag(pml, n, h)
+        lz, tzm, uz = axis_tridiag(pml, nxc, h)
+        per = 3.0 * wzc * w * w * 16
+        maxb = max(1, int(budget // per))
+        for b0 in range(0, len(lst), maxb):
+            part = lst[b0 : b0 + maxb]
+            diag = np.empty((len(part), wzc, w), dtype=np.complex128)
+            for b, (ell, off, ci) in enumerate(part):
+                cc = c[off : off + w, coffs[ci] : coffs[ci] + wzc].T  # (wzc, w): the transposed layer's cell
+                diag[b] = tzm[:, None] - omega**2 * (1.0 / cc**2)
+            dg = torch.as_tensor(diag, device=device)
+            tm.mark()
+            sinv = _schur_inverses(tw, dg, lz, uz, device)
+            tm.mark("schur")
+            tinv = _twisted_inverses(tw, dg, lz, uz, sinv, device)
+            del sinv
+            cm = tinv.transpose(-1, -2).contiguous()
+            del tinv
+            tm.mark("twisted")
+            for b, (ell, off, ci) in enumerate(part):
+                out[(ell, ci)] = cm[b]
+    return out
+
+
 def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=None, inner_dense=None,
                   backend="pt", reference_layers=None, cell_solver=None):
     """Offline stage for a partitioned problem (all layers, all cells).
@@ -558,9 +630,14 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
         # (2 (4 (Lc-1) w)^2 per layer) also grows with (Lc-1)^2
         inner_dense = green and Lc <= 8
     npml, h, omega = grid.npml, grid.h, pml.omega
+    tm = _Timer(device)
     cext = _split(grid.nx, Lc)  # partition_layers(sgrid, Lc), nested.py:294-296
     coffs = tuple(int(v) for v in np.concatenate([[0], np.cumsum(cext)[:-1]]))
     c = np.asarray(model.c, dtype=float)
+    # device route: every cell's factors first, batched by cell shape across the layers
+    pre = None
+    if use_k1 and reference_layers is None:
+        pre = _batched_twisted_factors(grid, model, pml, partition, Lc, cext, coffs, device, tm)
     layers = []
     for ell, (n, off) in enumerate(zip(partition.extents, partition.offsets)):
         w = n + 2 * npml
@@ -587,6 +664,13 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
         cells = [None] * Lc
         for nxc, idxs in groups.items():
             wzc = nxc + 2 * npml
+            if pre is not None:
+                lz, _, uz = axis_tridiag(pml, nxc, h)
+                ccoefs, ckrows = cut_coefs(lz, uz, npml, nxc)
+                for ci in idxs:
+                    cells[ci] = CellFactors(ell, ci, w, wzc, nxc, coffs[ci], pre.pop((ell, ci)), np.asarray(lz),
+                                            np.asarray(uz), None, ccoefs, ckrows, None, None)
+                continue
             diag = np.empty((len(idxs), wzc, w), dtype=np.complex128)
             if ref is None:
                 lz, tzm, uz = axis_tridiag(pml, nxc, h)  # along block rows (original x)
@@ -606,7 +690,9 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
             dg = torch.as_tensor(diag, device=device)
             if ref is None:
                 tw = axis_tridiag(pml, n, h)  # across the cell block: the layer depth
+            tm.mark()
             sinv = _schur_inverses(tw, dg, lz, uz, device)
+            tm.mark("schur")
             gblk = None
             gsmp = None
             if green and not use_k1:
@@ -664,7 +750,9 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
                 del X
             if wzc < 3:
                 raise ValueError("cells need at least 3 block rows (nx_c + 2 npml >= 3)")
+            tm.mark("torch-operators")
             tinv = _twisted_inverses(tw, dg, lz, uz, sinv, device)
+            tm.mark("twisted")
             sinv_cm = tinv.transpose(-1, -2).contiguous()
             for b, ci in enumerate(idxs):
                 cells[ci] = CellFactors(
@@ -677,8 +765,11 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
                 )
         lf.cells = cells
         if use_k1 and (green or q0):
-            del sinv, tinv, sinv_cm, dg
+            if pre is None:
+                del sinv, tinv, sinv_cm, dg
+            tm.mark()
             _k1_layer_operators(grid, lf, Lc, cext, coffs, device, green, q0, ref)
+            tm.mark("k1-operators")
         if green and backend == "lu":
             lf.lu_inv = inner_lu_inverse(lf)
         elif green and inner_dense:
@@ -687,6 +778,7 @@ def build_factors(grid, model, pml, partition, Lc, device="cpu", green=True, q0=
                 # [pre, pre o op, E pre, E^2 pre]: the last two drive the s-step start of the inner GMRES
                 lf.dense = torch.stack(list(ops) + list(inner_sstep_operators(*ops))).contiguous()
         layers.append(lf)
+    tm.report()
     tx = axis_tridiag(pml, grid.nx, h)
     tz = axis_tridiag(pml, grid.nz, h)
     return Factors(grid.nx, grid.nz, h, npml, omega, partition.L, Lc, layers, cext, coffs,
