@@ -15,9 +15,9 @@
 //
 // CTA = 8 consumer warps + 1 producer warp, one CTA per SM, persistent over (problem, row block, column block)
 // work items.  A CTA tile is MT x NT = 4 x 8 (32 rows x 64 columns) or 8 x 4 eight-wide tiles; K streams in
-// chunks of 32 through a 4-slot shared-memory ring: the producer warp issues one cp.async.bulk per operator row
-// and per panel column of the chunk (<= 96 copies of 512 B, completion on the slot's mbarrier), rows padded to
-// 36 double2 so the DMMA fragment loads (LDS.128, row = lane / 4, k = lane % 4) are conflict-free.  Every
+// chunks of 64 (2-slot ring) or 32 (4 slots) through shared memory: the producer warp issues one cp.async.bulk per operator row
+// and per panel column of the chunk (<= 96 copies of 1 KB / 512 B, completion on the slot.s mbarrier), rows padded by
+// 4 double2 so the DMMA fragment loads (LDS.128, row = lane / 4, k = lane % 4) are conflict-free.  Every
 // consumer warp owns a 2 x 2 block of (row tile, column tile) pairs over the whole K: four independent
 // accumulator chains per pair (Ar Br, Ai Bi, Ar Bi, Ai Br), 16 DMMAs per 4 fragment loads, no cross-warp
 // reduction; the sum over K runs in a fixed order (deterministic).  Epilogues as in stage_dev.cuh.
@@ -28,11 +28,14 @@
 
 #define SG_T 256
 #define SG_TB (SG_T + 32)
-#define SG_KC 32
-#define SG_LD 36
-#define SG_NSLOT 4
 #define SG_RC 96
+// K rows per chunk (template parameter KC): 32 with a 4-slot ring or 64 with a 2-slot ring (copies twice as
+// long: half the bulk-copy requests per flop); rows padded by 4 double2 (row stride = 4 mod 8 sixteen-byte
+// units: conflict-free LDS.128 fragment loads)
+#define SG_LD (KC + 4)
+#define SG_NSLOT (KC == 32 ? 4 : 2)
 #define SG_SLOT (SG_RC * SG_LD)  // double2 per ring slot
+#define SG_KC KC
 
 struct SgArgs {
   const OJob* jobs;
@@ -157,7 +160,7 @@ __device__ __forceinline__ void sg_dmma4(double (&q)[8], double ar, double ai, d
   dmma_f64(q[6], q[7], ai, br);
 }
 
-template <int MODE, int MT, int NT>
+template <int MODE, int MT, int NT, int KC>
 __global__ void __launch_bounds__(SG_TB, 1) k_stage_gemm(const SgArgs a, int nitems) {
   extern __shared__ __align__(128) unsigned char sg_smem[];
   double2* ring = reinterpret_cast<double2*>(sg_smem);
@@ -360,9 +363,11 @@ __global__ void __launch_bounds__(SG_TB, 1) k_stage_gemm(const SgArgs a, int nit
   }
 }
 
-static const size_t SG_SMEM = sizeof(double2) * SG_NSLOT * SG_SLOT + 2 * SG_NSLOT * sizeof(uint64_t);
-static_assert(sizeof(double2) * SG_NSLOT * SG_SLOT + 2 * SG_NSLOT * sizeof(uint64_t) <= 232448,
-              "k_stage_gemm exceeds 227 KB of shared memory");
+template <int KC>
+constexpr size_t sg_smem() {
+  return sizeof(double2) * SG_NSLOT * SG_SLOT + 2 * SG_NSLOT * sizeof(uint64_t);
+}
+static_assert(sg_smem<32>() <= 232448 && sg_smem<64>() <= 232448, "k_stage_gemm exceeds 227 KB of shared memory");
 
 // columns per product from which the streaming GEMM replaces the small-N kernels (PT_SGEMM_MIN; PT_NO_SGEMM)
 int stage_gemm_min_cols() {
@@ -387,13 +392,18 @@ static cudaError_t sg_launch(const SgArgs& a0, int M_max, int N_max, int num_sms
   if (nitems <= 0) return cudaSuccess;
   if (nitems > 0x7fffffffLL) return cudaErrorInvalidValue;
   const int grid = (int)std::min<long long>(nitems, num_sms);
-  if (wide) {
-    set_smem_attr((const void*)k_stage_gemm<MODE, 4, 8>, SG_SMEM);
-    k_stage_gemm<MODE, 4, 8><<<grid, SG_TB, SG_SMEM, st>>>(a, (int)nitems);
-  } else {
-    set_smem_attr((const void*)k_stage_gemm<MODE, 8, 4>, SG_SMEM);
-    k_stage_gemm<MODE, 8, 4><<<grid, SG_TB, SG_SMEM, st>>>(a, (int)nitems);
+  static const int kc = std::getenv("PT_SG_KC") ? atoi(std::getenv("PT_SG_KC")) : 64;
+#define SG_GO(MT_, NT_, KC_)                                                             \
+  {                                                                                      \
+    set_smem_attr((const void*)k_stage_gemm<MODE, MT_, NT_, KC_>, sg_smem<KC_>());       \
+    k_stage_gemm<MODE, MT_, NT_, KC_><<<grid, SG_TB, sg_smem<KC_>(), st>>>(a, (int)nitems); \
   }
+  if (wide) {
+    if (kc == 32) SG_GO(4, 8, 32) else SG_GO(4, 8, 64)
+  } else {
+    if (kc == 32) SG_GO(8, 4, 32) else SG_GO(8, 4, 64)
+  }
+#undef SG_GO
   return cudaGetLastError();
 }
 
