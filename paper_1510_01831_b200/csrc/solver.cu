@@ -175,6 +175,9 @@ struct pt_ctx {
   // outputs copied to the host while the reconstruction runs: side stream, events, pinned staging
   cudaStream_t side_st = nullptr;
   cudaEvent_t ev_tr = nullptr, ev_cp = nullptr;
+  // pt_solve on host buffers, several lockstep batches: the copies of batch b +- 1 run on io_st while batch b solves
+  cudaStream_t io_st = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_done = nullptr;
   double2* hstage = nullptr;
   size_t hstage_cap = 0;
   std::vector<long long> asm_touch;  // per layer: assembled-boundary touches per boundary_samples call
@@ -2305,6 +2308,9 @@ int pt_destroy(pt_ctx* c) {
   if (c->ev_tr) cudaEventDestroy(c->ev_tr);
   if (c->ev_cp) cudaEventDestroy(c->ev_cp);
   if (c->side_st) cudaStreamDestroy(c->side_st);
+  for (cudaEvent_t e : {c->ev_h2d[0], c->ev_h2d[1], c->ev_done})
+    if (e) cudaEventDestroy(e);
+  if (c->io_st) cudaStreamDestroy(c->io_st);
   if (c->own_st) cudaStreamDestroy(c->own_st);
   delete c;
   return PT_OK;
@@ -2340,11 +2346,26 @@ static int batch_rhs(const pt_ctx* c) {
   return 8 * std::max(1, inner_coop_max_units() / maxj);
 }
 
+// Host staging of a multi-batch solve (pt_solve): fh / uh are the caller's host arrays, f / u the device staging
+// buffers.  Batch b's sources are copied on io_st while batch b - 1 solves, its wavefields while batch b + 1 solves.
+struct HostIO {
+  const double* fh;
+  double* uh;
+};
+
+static int solve_batches(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats,
+                         const HostIO* hio);
+
 int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats) {
   if (!c || !f || !u || !cfg) return PT_BAD_ARGUMENT;
   CK(cudaSetDevice(c->dev));
+  return solve_batches(c, f, nrhs, cfg, u, stats, nullptr);
+}
+
+static int solve_batches(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double* u, pt_stats* stats,
+                         const HostIO* hio) {
   const int B = batch_rhs(c);
-  if (nrhs <= B) return solve_batch(c, f, nrhs, cfg, u, stats);
+  if (nrhs <= B && !hio) return solve_batch(c, f, nrhs, cfg, u, stats);
   // large source sets: consecutive lockstep batches; per-RHS outputs land at their offsets, totals add up
   const long long N = 2LL * c->wz * c->wx;  // doubles per wavefield
   const long long nO = 4LL * c->nI * c->wx;
@@ -2355,8 +2376,28 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
   double cf[5] = {0, 0, 0, 0, 0}, cb[5] = {0, 0, 0, 0, 0};
   std::vector<int> hist(stats && stats->inner_hist_len > 0 ? stats->inner_hist_len : 0, 0);
   int worst = PT_OK;
-  for (int r0 = 0; r0 < nrhs; r0 += B) {
+  if (hio) {
+    if (!c->io_st) {
+      CK(cudaStreamCreateWithFlags(&c->io_st, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+    }
+    const int n0 = std::min(B, nrhs);
+    CK(cudaMemcpyAsync(const_cast<double*>(f), hio->fh, sizeof(double) * (size_t)n0 * N, cudaMemcpyHostToDevice,
+                       c->io_st));
+    CK(cudaEventRecord(c->ev_h2d[0], c->io_st));
+  }
+  for (int r0 = 0, bi = 0; r0 < nrhs; r0 += B, ++bi) {
     const int nb = std::min(B, nrhs - r0);
+    if (hio) {
+      CK(cudaStreamWaitEvent(c->st, c->ev_h2d[bi & 1], 0));  // this batch's sources are on the device
+      if (r0 + B < nrhs) {  // the next batch's sources travel while this batch solves
+        const int nn = std::min(B, nrhs - r0 - B);
+        CK(cudaMemcpyAsync(const_cast<double*>(f) + (size_t)(r0 + B) * N, hio->fh + (size_t)(r0 + B) * N,
+                           sizeof(double) * (size_t)nn * N, cudaMemcpyHostToDevice, c->io_st));
+        CK(cudaEventRecord(c->ev_h2d[(bi + 1) & 1], c->io_st));
+      }
+    }
     pt_stats sb;
     std::memset(&sb, 0, sizeof(sb));
     long long bls = 0, bii = 0, bto = 0, bla = 0, bk1l = 0;
@@ -2388,8 +2429,17 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
       sb.class_bytes = bcb;
     }
     const int rc = solve_batch(c, f + (size_t)r0 * N, nb, cfg, u + (size_t)r0 * N, stats ? &sb : nullptr);
-    if (rc != PT_OK && rc != PT_NOT_CONVERGED) return rc;
+    if (rc != PT_OK && rc != PT_NOT_CONVERGED) {
+      if (hio) cudaStreamSynchronize(c->io_st);
+      return rc;
+    }
     if (rc == PT_NOT_CONVERGED) worst = rc;
+    if (hio) {  // this batch's wavefields travel while the next batch solves
+      CK(cudaEventRecord(c->ev_done, c->st));
+      CK(cudaStreamWaitEvent(c->io_st, c->ev_done, 0));
+      CK(cudaMemcpyAsync(hio->uh + (size_t)r0 * N, u + (size_t)r0 * N, sizeof(double) * (size_t)nb * N,
+                         cudaMemcpyDeviceToHost, c->io_st));
+    }
     ls += bls, ii += bii, to += bto, la += bla, k1l += bk1l, tms += btms, k1b += bk1b, dfl += bdfl;
     for (int i = 0; i < 3; ++i) kms[i] += bkms[i];
     for (int i = 0; i < 5; ++i) {
@@ -2418,6 +2468,7 @@ int pt_solve_device(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, 
     if (stats->class_bytes)
       for (int i = 0; i < 5; ++i) stats->class_bytes[i] = cb[i];
   }
+  if (hio) CK(cudaStreamSynchronize(c->io_st));
   if (worst != PT_OK) g_err = "outer GMRES did not reach ktol within max_iter";
   return worst;
 }
@@ -2435,6 +2486,10 @@ int pt_solve(pt_ctx* c, const double* f, int nrhs, const pt_krylov* cfg, double*
     c->io_bytes = bytes;
   }
   double2 *fd = c->io_f, *ud = c->io_u;
+  if (nrhs > batch_rhs(c)) {  // several lockstep batches: host copies of the neighbouring batches overlap each solve
+    const HostIO hio{f, u};
+    return solve_batches(c, reinterpret_cast<const double*>(fd), nrhs, cfg, reinterpret_cast<double*>(ud), stats, &hio);
+  }
   CK(cudaMemcpyAsync(fd, f, bytes, cudaMemcpyHostToDevice, c->st));
   int rc = pt_solve_device(c, reinterpret_cast<const double*>(fd), nrhs, cfg, reinterpret_cast<double*>(ud), stats);
   cudaError_t e = cudaMemcpyAsync(u, ud, bytes, cudaMemcpyDeviceToHost, c->st);

@@ -159,8 +159,10 @@ def from_reference_layers(layers, grid, model, pml, partition, device=None, inne
         inner_ktol = first.inner_ktol
         inner_max_iter = getattr(getattr(first, "inner", None), "max_iter", 200)
         assembled = bool(getattr(first, "assembled_boundary", False))
-        if getattr(first, "_plr", {}).get("plr_threshold") is not None:
-            raise NotImplementedError("PLR-compressed Green blocks are not part of the B200 path")
+        # PLR-compressed Green blocks (plr.py:96-219, green.py:124-126): the reference's GreenBlockSet.dense()
+        # expands them (as its own artifact dump does, green.py:156-163); the device applies the expanded block
+        # (U V) x where the reference applies U (V x) -- the same linear map.  TouchCounter totals then count
+        # dense touches, not the PLR leaves'.
     else:
         Lc, backend, inner_ktol, inner_max_iter, assembled = 1, "pt", 1e-6, 200, False
     if len(layers) != partition.L:

@@ -39,3 +39,27 @@ for fn in os.listdir(out):  # only the factor file and its manifest are needed b
     if fn.startswith("green_"):
         os.remove(os.path.join(out, fn))
 print(sorted(os.listdir(out)))
+
+# ---- the same from PLR-compressed reference layers (plr_threshold below the cell width, so every Green block is
+# a PlrMatrix): factors built from the reference objects (blocks expanded by GreenBlockSet.dense) plus the
+# reference's own solves with those compressed layers, which the device must reproduce
+import numpy as np  # noqa: E402
+
+from tests.golden_cases import REFOBJ_PLR  # noqa: E402
+
+plr_layers = rpt.build_nested_layers(grid, model, pml, part, Lc=prob.Lc, inner_ktol=prob.inner_ktol, **REFOBJ_PLR)
+assert all(isinstance(m, rpt.plr.PlrMatrix) for lay in plr_layers for bs in lay.blocksets for m in bs.blocks.values())
+layers = from_reference_layers(plr_layers, prob.grid, prob.model, prob.pml, prob.partition, inner_dense=False)
+out = os.path.join(HERE, "refobj_plr")
+shutil.rmtree(out, ignore_errors=True)
+dump_offline(layers, out, "refobj_plr", model=prob.model, grid=prob.grid, omega=prob.pml.omega,
+             partition=prob.partition)
+for fn in os.listdir(out):
+    if fn.startswith("green_"):
+        os.remove(os.path.join(out, fn))
+ref = rpt.PolarizedTracesSolver(grid, model, pml, part, layers=plr_layers)
+res = [ref.solve(f, rpt.KrylovConfig(ktol=1e-9)) for f in prob.rhs()]
+np.savez_compressed(os.path.join(HERE, "refobj_plr.npz"), u=np.stack([r.u for r in res]),
+                    iterations=np.array([r.iterations for r in res]),
+                    relres=np.array([r.relative_residual for r in res]))
+print(sorted(os.listdir(out)), [r.iterations for r in res])

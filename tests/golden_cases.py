@@ -29,3 +29,5 @@ GOLDEN = {
 
 # the problem whose offline artifacts tests/golden/make_refobj.py builds from the reference's own layer objects
 REFOBJ_CASE = dict(nx=24, nz=20, npml=4, L=2, Lc=2, omega=9.0, seed=2, n_sources=3)
+# PLR compression of the reference's Green blocks for the same problem (NestedLayerSolver kwargs, nested.py:279-281)
+REFOBJ_PLR = dict(plr_threshold=8, plr_eps=1e-10, seed=0)

@@ -364,3 +364,23 @@ def test_offline_operators_by_k1_match_torch_block_substitution(case):
                 assert float(torch.linalg.norm(a.cpu() - c)) <= 1e-12 * scale, (lk.index, ck.cell, name)
         if lt.dense is not None:
             assert float(torch.linalg.norm(lk.dense - lt.dense)) <= 1e-11 * float(torch.linalg.norm(lt.dense))
+
+
+def test_solve_with_plr_compressed_reference_layers():
+    """Reference layers built with PLR-compressed Green blocks (plr.py, nested.py:279-307): the factors built from
+    those objects (blocks expanded by GreenBlockSet.dense; tests/golden/make_refobj.py) reproduce the reference's
+    own solves WITH its compressed layers (it applies U (V x), the device (U V) x)."""
+    from paper_1510_01831_b200.artifacts import load_offline
+    from tests.golden_cases import REFOBJ_CASE
+
+    prob = small_problem(**REFOBJ_CASE)
+    layers = load_offline(os.path.join(HERE, "golden", "refobj_plr"), "refobj_plr", prob.grid, prob.partition,
+                          model=prob.model, omega=prob.pml.omega)
+    dev = PolarizedTracesSolver(prob.grid, prob.model, prob.pml, prob.partition, layers=layers)
+    g = np.load(os.path.join(HERE, "golden", "refobj_plr.npz"))
+    for k, f in enumerate(prob.rhs()):
+        got = dev.solve(f, KrylovConfig(ktol=1e-9))
+        assert rel(got.u, g["u"][k]) <= 1e-8
+        assert got.iterations == float(g["iterations"][k])
+        assert abs(got.relative_residual - float(g["relres"][k])) <= 1e-3 * float(g["relres"][k]) + 1e-13
+    dev.close()

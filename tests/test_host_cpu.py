@@ -351,3 +351,39 @@ def test_global_operator_residual_arrays():
     assert abs(rebuilt - Href).max() == 0.0
     with pytest.raises(ValueError):
         residual_from_operator(Href + sp.eye(Href.shape[0], k=2 * g.wx), g.wz, g.wx)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference package not present")
+def test_plr_compressed_reference_layers_are_accepted():
+    """Reference layers built with PLR compression (NestedLayerSolver(plr_threshold=...), nested.py:279-307;
+    plr.py:96-219): the uploaded Green blocks are the expansions GreenBlockSet.dense() returns (what the
+    reference's own artifact dump stores, green.py:156-163), within the PLR tolerance of the uncompressed ones."""
+    import sys
+
+    from paper_1510_01831_b200.solver import build_nested_layers, from_reference_layers
+    from tests.golden_cases import REFOBJ_CASE, REFOBJ_PLR
+
+    prob = small_problem(**REFOBJ_CASE)
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import polartraces as rpt
+
+    g = prob.grid
+    grid = rpt.Grid(g.nx, g.nz, g.h, g.npml)
+    model = rpt.VelocityModel(grid, prob.model.c)
+    pml = rpt.PmlProfile(g.npml, g.h, prob.pml.C, prob.pml.omega)
+    part = rpt.LayerPartition(tuple(prob.partition.extents))
+    ref_layers = rpt.build_nested_layers(grid, model, pml, part, Lc=prob.Lc, inner_ktol=prob.inner_ktol, **REFOBJ_PLR)
+    assert any(isinstance(m, rpt.plr.PlrMatrix) for lay in ref_layers for bs in lay.blocksets
+               for m in bs.blocks.values())
+    got = from_reference_layers(ref_layers, prob.grid, prob.model, prob.pml, prob.partition)
+    own = build_nested_layers(prob.grid, prob.model, prob.pml, prob.partition, Lc=prob.Lc, inner_ktol=prob.inner_ktol)
+    for lay, la, lo in zip(ref_layers, got.factors.layers, own.factors.layers):
+        for bs, ca, co in zip(lay.blocksets, la.cells, lo.cells):
+            for jr, jrow in enumerate((0, 1, ca.nxc, ca.nxc + 1)):
+                for s, slot in enumerate(("v0", "v1", "vn", "vnp")):
+                    dense = np.asarray(bs.dense(jrow, slot))
+                    assert np.array_equal(ca.green[jr, s].numpy().T, dense)  # column-major storage
+            scale = np.linalg.norm(co.green.numpy())
+            err = np.linalg.norm(ca.green.numpy() - co.green.numpy())
+            assert err <= 1e-8 * scale  # the compression tolerance (plr_eps = 1e-10 per block, certified)

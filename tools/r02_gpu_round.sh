@@ -8,7 +8,7 @@ DM="sm__inst_executed_pipe_tensor_subpipe_dmma.sum,sm__inst_executed_pipe_tensor
 for w in $what; do
 case $w in
 tests)
-  timeout 2400 python -m pytest tests -m gpu -x -q --durations=12 > gpurun_out/tests.log 2>&1
+  timeout 2400 python -m pytest tests -m gpu -q --durations=12 > gpurun_out/tests.log 2>&1
   echo "tests exit $?" >> gpurun_out/tests.log ;;
 bench)
   timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
@@ -24,7 +24,7 @@ launches)
   echo "launches exit $?" >> gpurun_out/launches.log ;;
 full)
   # cfg5 64 RHS: a few launches of each hot kernel from the middle of the timed solve
-  for k in inner_items_kernel k_pass0 k_green_samples2 k1_twisted; do
+  for k in inner_items_kernel k_stage_gemm k1_twisted; do
     skip=40; [ $k = k1_twisted ] && skip=0
     timeout 1200 ncu --set full --metrics $DM --clock-control none --import-source on --profile-from-start off \
         -k regex:$k --launch-skip $skip -c 3 -f -o gpurun_out/full_$k \
