@@ -48,7 +48,6 @@ namespace cg = cooperative_groups;
 #define II_MAXIT 320   // op + pre program items (staged in shared memory, compact form)
 #define II_MAXPH 256   // program phases
 #define II_JREG 4      // Arnoldi steps whose basis entries stay in registers (beyond: a slower loop)
-#define II_EB 4        // outputs per thread whose combine operands are loaded together
 
 struct TileCfg {
   int mtc, ntc, wm, wn, kw;
@@ -558,51 +557,35 @@ __device__ __noinline__ void run_phase(const InnerParams& p, IIShared& S, double
         }
     }
     cbar();
-    // ---- combine: t = y + (add0 + add1) - (sub0 + sub1); dst = t | rev - t | t - rev.  A thread's outputs are
-    // taken II_EB at a time: the operand loads of the whole batch are in flight together (big tiles have 8 outputs
-    // per thread; one L2 round trip per output was a fifth of a multi-job launch)
-    for (int ob = tid; ob < npair * 64; ob += II_T * II_EB) {
-      double2 av[II_EB], sv[II_EB], rv[II_EB];
-#pragma unroll
-      for (int u = 0; u < II_EB; ++u) {
-        const int o = ob + u * II_T;
-        av[u] = pre_add, sv[u] = pre_sub, rv[u] = pre_rev;
-        if (o >= npair * 64 || o == o0) continue;
-        const int pr = o >> 6, pos = o & 63, row = pos >> 3, q = pos & 7;
-        const int ml = pr / c.ntc, nl = pr - ml * c.ntc;
-        const int grow = (d.mt0 + ml) * 8 + row;
-        av[u] = sv[u] = rv[u] = czero();
-        if (ml >= d.mvalid || nl >= d.nvalid || grow >= d.w) continue;
-        const int nt = S.act[d.jx][d.nt0 + nl];
+    // ---- combine: t = y + (add0 + add1) - (sub0 + sub1); dst = t | rev - t | t - rev
+    for (int o = tid; o < npair * 64; o += II_T) {
+      const int pr = o >> 6, pos = o & 63, row = pos >> 3, q = pos & 7;
+      const int ml = pr / c.ntc, nl = pr - ml * c.ntc;
+      const int grow = (d.mt0 + ml) * 8 + row;
+      if (ml >= d.mvalid || nl >= d.nvalid || grow >= d.w) continue;
+      const int nt = S.act[d.jx][d.nt0 + nl];
+      double2 y = czero();
+      if (d.ns > 0)
+        for (int k = 0; k < c.kw; ++k) y = cadd(y, red[((size_t)k * npair + pr) * 64 + pos]);
+      double2 av = pre_add, sv = pre_sub, rv = pre_rev;
+      if (o != o0) {
         auto opnd = [&](RefS r) { return ld_cg(v2p(p, d.job, vmap[r.vec], nt) + ((size_t)r.seg * d.w + grow) * 8 + q); };
+        av = sv = rv = czero();
         if (item.add[0].vec >= 0) {
-          av[u] = opnd(item.add[0]);
-          if (item.add[1].vec >= 0) av[u] = cadd(av[u], opnd(item.add[1]));
+          av = opnd(item.add[0]);
+          if (item.add[1].vec >= 0) av = cadd(av, opnd(item.add[1]));
         }
         if (item.sub[0].vec >= 0) {
-          sv[u] = opnd(item.sub[0]);
-          if (item.sub[1].vec >= 0) sv[u] = cadd(sv[u], opnd(item.sub[1]));
+          sv = opnd(item.sub[0]);
+          if (item.sub[1].vec >= 0) sv = cadd(sv, opnd(item.sub[1]));
         }
-        if (mode != 0) rv[u] = opnd(item.rev);
+        if (mode != 0) rv = opnd(item.rev);
       }
-#pragma unroll
-      for (int u = 0; u < II_EB; ++u) {
-        const int o = ob + u * II_T;
-        if (o >= npair * 64) continue;
-        const int pr = o >> 6, pos = o & 63, row = pos >> 3, q = pos & 7;
-        const int ml = pr / c.ntc, nl = pr - ml * c.ntc;
-        const int grow = (d.mt0 + ml) * 8 + row;
-        if (ml >= d.mvalid || nl >= d.nvalid || grow >= d.w) continue;
-        const int nt = S.act[d.jx][d.nt0 + nl];
-        double2 y = czero();
-        if (d.ns > 0)
-          for (int k = 0; k < c.kw; ++k) y = cadd(y, red[((size_t)k * npair + pr) * 64 + pos]);
-        if (item.add[0].vec >= 0) y = cadd(y, av[u]);
-        if (item.sub[0].vec >= 0) y = csub(y, sv[u]);
-        if (mode == 1) y = csub(rv[u], y);
-        else if (mode == 2) y = csub(y, rv[u]);
-        v2p(p, d.job, vmap[item.dst.vec], nt)[((size_t)item.dst.seg * d.w + grow) * 8 + q] = y;
-      }
+      if (item.add[0].vec >= 0) y = cadd(y, av);
+      if (item.sub[0].vec >= 0) y = csub(y, sv);
+      if (mode == 1) y = csub(rv, y);
+      else if (mode == 2) y = csub(y, rv);
+      v2p(p, d.job, vmap[item.dst.vec], nt)[((size_t)item.dst.seg * d.w + grow) * 8 + q] = y;
     }
     cbar();  // red is reused by the next tile
     X.ev(6, 0);

@@ -76,6 +76,37 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_twisted(const K1Params p) {
   const int m = wzc >> 1, mb = wzc - 1 - m;
   const int nst = h == 0 ? 2 * m + 1 : 2 * mb + 1;
   const int tid = threadIdx.x;
+  if (p.pass == 0 && p.zflag) {
+    // every column of the task solves H_c x = 0 (zero split source, no panels): the outputs are zero
+    bool allzero = true;
+    for (int ql = 0; ql < task.nq && allzero; ++ql) {
+      const int q = task.q0 + ql;
+      const OJob& jb = p.jobs[p.ljobs[task.jb + q / p.R]];
+      bool pans = false;
+      for (int s = 0; s < 4; ++s) pans |= jb.pan[s][0].vec >= 0;
+      allzero = !pans && jb.vol && !jb.vfull && p.zflag[jb.layer * p.R + q % p.R] == 0;
+    }
+    if (allzero) {  // uniform over the cluster (same task, same flags): nobody reaches a cluster barrier
+      if (rank == 0) {
+        const int nk = cell.hi - cell.lo;
+        for (int ql = 0; ql < task.nq; ++ql) {
+          const int q = task.q0 + ql, jid = p.ljobs[task.jb + q / p.R], r = q % p.R;
+          const OJob& jb = p.jobs[jid];
+          for (int e = tid; e < 4 * w; e += blockDim.x) {
+            const int idx = e / w, j = e - idx * w;
+            if (idx < 2 ? cell.has_top : cell.has_bot)
+              p.tables[((size_t)(jid * p.Lc + cell.cell) * 4 + idx) * p.R * p.wmax + (size_t)r * p.wmax + j] = czero();
+          }
+          if (p.s0 && jb.nout > 0)
+            for (int e = tid; e < jb.nout * nk; e += blockDim.x) {
+              const int o = e / nk, k = e - o * nk;
+              p.smp[((size_t)(jid * 4 + o) * p.R + r) * p.wx + cell.off + cell.lo + k] = czero();
+            }
+        }
+      }
+      return;
+    }
+  }
   const int NS = p.ns;  // ring slots (<= K1_NS; a multiple of CM)
   // elements (row, column) per consumer thread: w*NC <= (NC == 8 ? 8*NMT : 32*NMT) * NC
   constexpr int TT = ((NC == 8 ? 8 * NMT : 32 * NMT) * NC + K1_CONSUMERS - 1) / K1_CONSUMERS;

@@ -461,6 +461,22 @@ __global__ void k_residual(const double2* u, const double2* f, long long stride,
 }
 
 // full-volume norms ||f||^2 per RHS (zero-source detection, sie.py:397-399)
+// flags[l * R + r] = 1 when the split source of RHS r (sie.py:134-151: rows [off + lo, off + hi) of layer l) has a
+// nonzero entry.  grid (L, R).
+__global__ void k_slab_flags(const double2* f, long long stride, const LayerInfo* layers, int wx, int R, int* flags) {
+  const LayerInfo& lay = layers[blockIdx.x];
+  const int r = blockIdx.y;
+  const double2* base = f + (size_t)r * stride + (size_t)(lay.off + lay.lo) * wx;
+  const long long n = (long long)(lay.hi - lay.lo) * wx;
+  int any = 0;
+  for (long long e = threadIdx.x; e < n && !any; e += blockDim.x) {
+    const double2 v = base[e];
+    any |= v.x != 0.0 || v.y != 0.0;
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) flags[blockIdx.x * R + r] = any;
+}
+
 __global__ void k_vol_norm2(const double2* f, long long stride, long long N, double* out) {
   __shared__ double red[32];
   const int r = blockIdx.y;

@@ -51,6 +51,10 @@ struct K1Params {
   double2* Z;
   const double2* bd;  // pass 2 (dense test mode): b [q][wzc][w]
   double2* xd;        // pass 2: x [q][wzc][w]
+  // pass 0 of a volume-source stage: [layer][R] 1 = the RHS's split source is nonzero somewhere in the layer
+  // (k_slab_flags); a task whose columns all have a zero source and no panels writes zero outputs and exits
+  // (point / surface sources touch one layer of L).  NULL: no shortcut.
+  const int* zflag;
   long long* tprof;   // optional per-phase clock64 totals of CTA 0 (debug instrumentation)
   int dbg;            // debug: 1 = no factor streaming (timing only), 2 = no matvec (timing only)
   int s0;             // pass 0 also writes the layer-row samples of its solution into smp
@@ -204,6 +208,7 @@ __global__ void k_accum_x(VecView x, const double2* V, long long vstride, long l
 __global__ void k_residual(const double2* u, const double2* f, long long stride, int wz, int wx, const double2* tx,
                            const double2* tz, const double* m, double omega2, const int* rmap, double* out,
                            const double2* hdiag);
+__global__ void k_slab_flags(const double2* f, long long stride, const LayerInfo* layers, int wx, int R, int* flags);
 __global__ void k_vol_norm2(const double2* f, long long stride, long long N, double* out);
 __global__ void k_green_tiles(const double2* src, double2* dst, int w, int nb);
 __global__ void k_block2_mm(const double2* A, const double2* B, double2* C, int w);

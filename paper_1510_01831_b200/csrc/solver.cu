@@ -175,6 +175,8 @@ struct pt_ctx {
   // outputs copied to the host while the reconstruction runs: side stream, events, pinned staging
   cudaStream_t side_st = nullptr;
   cudaEvent_t ev_tr = nullptr, ev_cp = nullptr;
+  int* zflag_d = nullptr;  // [L][R] nonzero-source flags of the NEWTON stage (k_slab_flags)
+  int zflag_cap = 0;
   // pt_solve on host buffers, several lockstep batches: the copies of batch b +- 1 run on io_st while batch b solves
   cudaStream_t io_st = nullptr;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_done = nullptr;
@@ -784,8 +786,13 @@ static Stage::Tasks* stage_tasks(pt_ctx* c, Stage& S, int Ract) {
   for (size_t g = 0; g < S.lgrp.size(); ++g) {
     const int l = S.lgrp[g].first, b = S.lgrp[g].second;
     const int n = ncols[g];
-    for (int q0 = 0; q0 < n; q0 += nc * cm)
-      for (int cc = 0; cc < c->Lc; ++cc) {
+    // cell-major: the column groups of one cell are neighbours in the launch order, so the CTA pairs that stream
+    // the same factor blocks run together and share them in L2 (PT_K1_COLMAJOR: column-group-major, round 1's order)
+    static const bool colmajor = std::getenv("PT_K1_COLMAJOR") != nullptr;
+    const int ngq = (n + nc * cm - 1) / (nc * cm);
+    for (int it = 0; it < ngq * c->Lc; ++it) {
+        const int cc = colmajor ? it % c->Lc : it / ngq;
+        const int q0 = (colmajor ? it / c->Lc : it % ngq) * nc * cm;
         const CellInfo& ci = c->cel[l * c->Lc + cc];
         K1Task t;
         t.cell = l * c->Lc + cc;
@@ -1079,6 +1086,22 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
                       c->rmap_d, rhs_out ? &ro : nullptr));
     } else {
       LaunchScope ls(c, 0);
+      // NEWTON (sie.py:175-188): a layer's solve of a source that is zero inside the layer is zero -- point and
+      // surface sources touch one layer of L.  Flag the (layer, RHS) slabs that hold a nonzero; K1 tasks whose
+      // columns are all unflagged write zero tables / samples and exit (PT_NO_ZSKIP solves them all).
+      static const bool no_zskip = std::getenv("PT_NO_ZSKIP") != nullptr;
+      if (&S == &c->newton && gpath && io.f && !no_zskip) {
+        if (c->L * Ract > c->zflag_cap) {
+          if (c->zflag_d) cudaFree(c->zflag_d);
+          c->zflag_d = nullptr;
+          CK(cudaMalloc(&c->zflag_d, sizeof(int) * (size_t)c->L * Ract));
+          c->zflag_cap = c->L * Ract;
+          c->gen++;  // graphs captured with the old buffer are stale
+        }
+        k_slab_flags<<<dim3(c->L, Ract), 256, 0, c->st>>>(io.f, io.f_stride, c->lay_d, c->wx, Ract, c->zflag_d);
+        CK(cudaGetLastError());
+        kp.zflag = c->zflag_d;
+      }
       CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
       c->k1_bytes += T->bytes;
     }
@@ -2282,7 +2305,7 @@ int pt_destroy(pt_ctx* c) {
   // the process-level allocations are released with the context
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
   for (void* p : {(void*)c->lay_d, (void*)c->cel_d, (void*)c->sinv_d, (void*)c->green_d, (void*)c->gsmp_d, (void*)c->q0_d, (void*)c->dense_d, (void*)c->lu_d, (void*)c->lz_d,
-                  (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->hd_d, (void*)c->items_d, (void*)c->items_px_d, (void*)c->pre_ph_px_d,
+                  (void*)c->uz_d, (void*)c->tx_d, (void*)c->tz_d, (void*)c->m_d, (void*)c->hd_d, (void*)c->items_d, (void*)c->items_px_d, (void*)c->pre_ph_px_d, (void*)c->zflag_d,
                   (void*)c->op_ph_d, (void*)c->pre_ph_d, (void*)c->V, (void*)c->Bv, (void*)c->Bp, (void*)c->T1,
                   (void*)c->AX, (void*)c->X, (void*)c->TR, (void*)c->P, (void*)c->smp, (void*)c->tables, (void*)c->tables_f,
                   (void*)c->trc, (void*)c->Z, (void*)c->iscr, (void*)c->hess, (void*)c->iters, (void*)c->istate,
