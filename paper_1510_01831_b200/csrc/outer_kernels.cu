@@ -5,6 +5,8 @@
 // V.p[r * V.stride + e]; panels (segments) are wx long.  Stage kernels run on
 // the compacted list of still-active RHS (rmap), so converged right-hand sides
 // cost nothing and never feed garbage into an inner solve.
+#include <cooperative_groups.h>
+
 #include "pt_device.cuh"
 
 #include <algorithm>
@@ -411,6 +413,49 @@ __global__ void k_arnoldi(double2* V, long long vstride, long long n, int j, con
   for (long long e = threadIdx.x; e < n; e += blockDim.x) s += w[e].x * w[e].x + w[e].y * w[e].y;
   s = block_sum(s, red);
   if (threadIdx.x == 0) hout[(size_t)r * hld + j + 1] = make_double2(sqrt(s), 0.0);
+}
+
+// The same MGS step on a cluster of two CTAs per RHS (each owns half of the vector; the partial dots meet through
+// distributed shared memory, summed rank 0 + rank 1 on both sides): the step is bound by per-SM bandwidth, and
+// one CTA per RHS leaves most SMs idle for <= 74 RHS.  grid = 2 * active RHS.
+__global__ void __cluster_dims__(2, 1, 1) k_arnoldi2(double2* V, long long vstride, long long n, int j,
+                                                     const int* rmap, double2* hout, int hld) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double red[32];
+  __shared__ double2 mine[2];  // this CTA's partial (re, im), double-buffered by step parity
+  const int rank = (int)cl.block_rank();
+  const int r = rmap[blockIdx.x >> 1];
+  double2* base = V + r * vstride;
+  double2* w = base + (long long)(j + 1) * n;
+  const long long e0 = rank * (n / 2), e1 = rank == 0 ? n / 2 : n;
+  const double2* peer = cl.map_shared_rank(mine, rank ^ 1);
+  for (int i = 0; i <= j + 1; ++i) {  // i == j + 1: the norm of the orthogonalised vector
+    const double2* vi = base + (long long)i * n;
+    double sr = 0.0, si = 0.0;
+    if (i <= j) {
+      for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const double2 c = cconjmul(vi[e], w[e]);
+        sr += c.x;
+        si += c.y;
+      }
+    } else {
+      for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) sr += w[e].x * w[e].x + w[e].y * w[e].y;
+    }
+    sr = block_sum(sr, red);
+    si = block_sum(si, red);
+    if (threadIdx.x == 0) mine[i & 1] = make_double2(sr, si);
+    cl.sync();  // both partials are written (and the peer has finished reading the buffer of step i - 2)
+    const double2 a = mine[i & 1], b = peer[i & 1];
+    const double2 h = rank == 0 ? cadd(a, b) : cadd(b, a);  // rank 0's partial first on both CTAs
+    if (i <= j) {
+      for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) w[e] = csub(w[e], cmul(h, vi[e]));
+      if (rank == 0 && threadIdx.x == 0) hout[(size_t)r * hld + i] = h;
+    } else if (rank == 0 && threadIdx.x == 0) {
+      hout[(size_t)r * hld + j + 1] = make_double2(sqrt(h.x), 0.0);
+    }
+  }
+  cl.sync();  // no CTA exits while its shared memory may still be read
 }
 
 // x[r] += sum_i y[r][i] V[r][i]   (krylov.py:128-131)

@@ -203,6 +203,8 @@ __global__ void k_scale_div(VecView dst, VecView src, long long len, const int* 
                             const double* scale);
 __global__ void k_arnoldi(double2* V, long long vstride, long long n, int j, const int* rmap, double2* hout,
                           int hld);
+__global__ void k_arnoldi2(double2* V, long long vstride, long long n, int j, const int* rmap, double2* hout,
+                           int hld);
 __global__ void k_accum_x(VecView x, const double2* V, long long vstride, long long n, const double2* y,
                           int yld, int k, const int* rmap, int nq);
 __global__ void k_residual(const double2* u, const double2* f, long long stride, int wz, int wx, const double2* tx,

@@ -1693,7 +1693,11 @@ static int solve_device(pt_ctx* c, const double2* f, int R, const pt_krylov* cfg
           if (r1) return r1;
           if ((r1 = apply_pre(c, vT, vj1, vA, Ra, gs, io))) return r1;
           { LaunchScope ls_(c, 2); }
-          k_arnoldi<<<Ra, 512, 0, c->st>>>(c->V, vs, nO, j, c->rmap_d, c->hout, hld);
+          static const bool arn1 = std::getenv("PT_ARNOLDI_1CTA") != nullptr;
+          if (arn1 || 2 * Ra > 2 * c->num_sms)
+            k_arnoldi<<<Ra, 512, 0, c->st>>>(c->V, vs, nO, j, c->rmap_d, c->hout, hld);
+          else  // two CTAs per RHS
+            k_arnoldi2<<<2 * Ra, 512, 0, c->st>>>(c->V, vs, nO, j, c->rmap_d, c->hout, hld);
           CK(cudaGetLastError());
           return 0;
         });

@@ -384,3 +384,30 @@ def test_solve_with_plr_compressed_reference_layers():
         assert got.iterations == float(g["iterations"][k])
         assert abs(got.relative_residual - float(g["relres"][k])) <= 1e-3 * float(g["relres"][k]) + 1e-13
     dev.close()
+
+
+def test_source_set_larger_than_the_lockstep_batch():
+    """More sources than one lockstep batch holds (pt_solve cuts the set into consecutive batches and moves the
+    neighbouring batches' host copies on a side stream while a batch solves): every sampled source -- first and
+    last of a batch, and the sources either side of a batch boundary -- equals its own single-source solve and the
+    oracle; the counters add up over the batches."""
+    prob = small_problem(nx=48, nz=41, npml=5, L=4, Lc=3, omega=20.0, seed=3, n_sources=700)
+    dev = device_solver(prob)
+    orc = OracleSolver.from_problem(prob)
+    cfg = KrylovConfig(ktol=1e-9)
+    F = prob.rhs()
+    out = np.empty_like(F)
+    many = dev.solve_many(F, cfg, out=out)
+    assert len(many) == 700 and all(r.converged for r in many)
+    assert dev.last_stats["layer_solves"] > 0 and dev.last_stats["inner_hist"].sum() > 0
+    # batch sizes of this path: 64 (item programs) or 8 * floor(256 / widest stage) = 336 (dense, L = 4)
+    for r in (0, 63, 64, 127, 128, 335, 336, 337, 671, 672, 699):
+        one = dev.solve(F[r], cfg)
+        assert rel(many[r].u, one.u) < 1e-13, r
+        assert many[r].u is not None and np.array_equal(many[r].u, out[r])
+        assert many[r].iterations == one.iterations
+        np.testing.assert_allclose(many[r].residuals, one.residuals, rtol=1e-6, atol=1e-12)
+    for r in (0, 336, 699):
+        want = orc.solve(F[r], ktol=1e-9)
+        assert rel(many[r].u, want.u) < 1e-10
+        assert many[r].iterations == want.iterations

@@ -37,6 +37,8 @@ full1)
       -k regex:inner_items_kernel --launch-skip 40 -c 3 -f -o gpurun_out/full1_inner_items_kernel \
       python bench.py --nrhs 1 --steps 1 --warmup 1 --no-extras --no-cpu-baseline --e2e-steps 1 > gpurun_out/full1.log 2>&1
   echo "full1 exit $?" >> gpurun_out/full1.log ;;
+traffic)
+  bash tools/r02_traffic.sh ;;
 esac
 done
 ls -la gpurun_out
