@@ -1101,6 +1101,26 @@ static int run_stage(pt_ctx* c, Stage& S, VecTab tab, int Ract, const SolveIO& i
         k_slab_flags<<<dim3(c->L, Ract), 256, 0, c->st>>>(io.f, io.f_stride, c->lay_d, c->wx, Ract, c->zflag_d);
         CK(cudaGetLastError());
         kp.zflag = c->zflag_d;
+        if (c->prof) {  // executed-work accounting (profiling runs eagerly): only the tasks that are not skipped
+          std::vector<int> fl((size_t)c->L * Ract);
+          CK(cudaMemcpyAsync(fl.data(), c->zflag_d, sizeof(int) * fl.size(), cudaMemcpyDeviceToHost, c->st));
+          CK(cudaStreamSynchronize(c->st));
+          const int gq = T->nc * T->cm;
+          long long live = 0, tot = 0;
+          for (size_t g = 0; g < S.lgrp.size(); ++g) {
+            const int l = S.lgrp[g].first, b = S.lgrp[g].second;
+            const int e = g + 1 < S.lgrp.size() ? S.lgrp[g + 1].second : (int)S.ljobs.size();
+            const int n = (e - b) * Ract;
+            for (int q0 = 0; q0 < n; q0 += gq, ++tot) {
+              bool any = false;
+              for (int q = q0; q < std::min(n, q0 + gq); ++q) any |= fl[(size_t)l * Ract + q % Ract] != 0;
+              live += any;
+            }
+          }
+          const double skipped = tot > 0 ? 1.0 - (double)live / (double)tot : 0.0;
+          c->cls_flops[0] -= skipped * T->bytes / 4.0;
+          c->cls_bytes[0] -= skipped * T->hbytes;
+        }
       }
       CK(k1_launch(kp, T->n, T->nc, c->wmax, c->st));
       c->k1_bytes += T->bytes;
