@@ -25,7 +25,10 @@
 // per-slice partials in a fixed order, so every CTA sees the same bits.  In exact arithmetic CGS2 and the
 // reference's MGS give the same Hessenberg column; both keep the basis orthonormal to working precision for
 // these short Krylov runs, so the iterate x_k and the per-instance iteration counts are the reference's
-// ("MGS vs CGS2 is harmless: x_k is the same minimiser over the same Krylov space").
+// ("MGS vs CGS2 is harmless: x_k is the same minimiser over the same Krylov space").  Three passes
+// and grid barriers per step: h1 = V^H w; w' = w - V h1 with h2 = V^H w' and ||w'||^2; then V_{j+1} = (w' - V h2) / hn
+// with hn^2 = ||w'||^2 - ||h2||^2 (w'' is orthogonal to V to rounding, so its norm is known before it is formed
+// and the vector is stored normalised without a fourth pass).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -363,7 +366,8 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 
 // The tile shape of a phase: minimise (tile rounds) x (cycles of one tile at its warp block's DMMA rate + a fixed
 // per-tile cost).  Evaluated for every program phase when the active n-tiles change (refresh), not per phase.
-__device__ __forceinline__ int phase_config(const IIShared& S, int J, int nit, int wphase, int wmax, int G) {
+__device__ __forceinline__ int phase_config(const IIShared& S, int J, int nit, int wphase, int wmax, int G,
+                                            float tile_cost) {
   int cfg = II_NCFG - 1;
   const float ksteps = (float)wphase / (float)max(nit, 1) * (float)((wmax + 3) >> 2);
   float best = 3.4e38f;
@@ -371,7 +375,7 @@ __device__ __forceinline__ int phase_config(const IIShared& S, int J, int nit, i
     const TileCfg cc = II_CFG[ci];
     const int tiles = S.tpre[ci][J] * nit;
     const int rounds = (tiles + G - 1) / G;
-    const float t = (float)rounds * ((float)(cc.mtc * cc.ntc) * ksteps * 4.0f / cfg_rate(cc) + 3000.0f);
+    const float t = (float)rounds * ((float)(cc.mtc * cc.ntc) * ksteps * 4.0f / cfg_rate(cc) + tile_cost);
     if (tiles > 0 && t < best) {
       best = t;
       cfg = ci;
@@ -656,9 +660,9 @@ __device__ __forceinline__ bool inst_active(const InnerParams& p, int job, int n
 
 // One (job, n-tile, element slice) item of an Arnoldi pass at step j (W = V_{j+1} holds pre(op(V_j))):
 //   pass 1: h1_i = vdot(V_i, W) partials -> area 0
-//   pass 2: W -= sum_i h1_i V_i (stored); h2_i = vdot(V_i, W) partials -> area 1
-//   pass 3: W -= sum_i h2_i V_i (stored); ||W||^2 partials -> area 2
-//   pass 4: hn = ||W||; W /= hn; owner (slice 0): column h1 + h2 | hn, Givens (krylov.py:96-127), state
+//   pass 2: W -= sum_i h1_i V_i (stored); h2_i = vdot(V_i, W) and ||W||^2 partials -> area 1
+//   pass 3: hn^2 = ||W||^2 - ||h2||^2; W = (W - sum_i h2_i V_i) / hn (stored); owner (slice 0): column h1 + h2 | hn,
+//           Givens (krylov.py:96-127), state
 // Thread (e = tid >> 3, q = tid & 7) walks elements e0 + e, e0 + e + 32, ... of instance q.
 __device__ __noinline__ void vec_item(const InnerParams& p, IIShared& S, int pass, int j, int job, int nt, int v, int sl, int nsl,
                          int n) {
@@ -670,6 +674,7 @@ __device__ __noinline__ void vec_item(const InnerParams& p, IIShared& S, int pas
   auto V = [&](int i, int e) { return ld_cg(v2p(p, job, i, nt) + (size_t)e * 8 + q); };
   if (pass == 1 || pass == 2) {
     double2* out = partp(p, pass - 1, v);
+    double nw2 = 0.0;
     for (int i0 = 0; i0 <= j; i0 += II_JREG) {
       const bool last = i0 + II_JREG > j;
       double2 h[II_JREG], acc[II_JREG];
@@ -694,6 +699,7 @@ __device__ __noinline__ void vec_item(const InnerParams& p, IIShared& S, int pas
 #pragma unroll
           for (int i = 0; i < II_JREG; ++i)
             if (i0 + i <= j) acc[i] = cadd(acc[i], cconjmul(vi[i], wv));
+        if (pass == 2 && last) nw2 += wv.x * wv.x + wv.y * wv.y;  // ||w'||^2 (w' is final in the last group)
       }
       if (pass == 1 || (last && i0 == 0)) {
 #pragma unroll
@@ -712,38 +718,39 @@ __device__ __noinline__ void vec_item(const InnerParams& p, IIShared& S, int pas
         if (tid < 8) out[i * 8 + tid] = s2;
       }
     }
-    return;
-  }
-  if (pass == 3) {
-    double ss = 0.0;
-    for (int i0 = 0; i0 <= j; i0 += II_JREG) {
-      const bool last = i0 + II_JREG > j;
-      double2 h[II_JREG];
-#pragma unroll
-      for (int i = 0; i < II_JREG; ++i) h[i] = i0 + i <= j ? psum(p, 1, vb, nsl, i0 + i, q) : czero();
-      for (int e = e0 + (tid >> 3); e < e1; e += II_T / 8) {
-        double2 wv = ld_cg(Wp + (size_t)e * 8 + q);
-#pragma unroll
-        for (int i = 0; i < II_JREG; ++i)
-          if (i0 + i <= j) wv = csub(wv, cmul(h[i], V(i0 + i, e)));
-        Wp[(size_t)e * 8 + q] = wv;
-        if (last) ss += wv.x * wv.x + wv.y * wv.y;
-      }
+    if (pass == 2) {
+      const double2 s2 = qsum(make_double2(nw2, 0.0), S.dred);
+      if (tid < 8) out[(j + 1) * 8 + tid] = s2;
     }
-    const double2 s2 = qsum(make_double2(ss, 0.0), S.dred);
-    if (tid < 8) partp(p, 2, v)[tid] = s2;
     return;
   }
-  // pass 4
-  const double hn = sqrt(psum(p, 2, vb, nsl, 0, q).x);
-  const bool act = inst_active(p, job, nt, q);
-  if (act && hn != 0.0) {
-    const double ihn = 1.0 / hn;  // scaling as a product with the reciprocal
+  // pass 3.  The new basis vector is orthogonal to V to rounding after the second projection, so
+  // ||w''||^2 = ||w'||^2 - ||h2||^2 (h2 = V^H w' is the reorthogonalisation correction, ~1e-16 ||w'||): the norm is
+  // known before w'' is formed and the vector is stored normalised in the same pass.
+  double hh = 0.0;
+  const double nw2 = psum(p, 1, vb, nsl, j + 1, q).x;
+  for (int i0 = 0; i0 <= j; i0 += II_JREG) {
+    const bool last = i0 + II_JREG > j;
+    double2 h[II_JREG];
+#pragma unroll
+    for (int i = 0; i < II_JREG; ++i) {
+      h[i] = i0 + i <= j ? psum(p, 1, vb, nsl, i0 + i, q) : czero();
+      hh += h[i].x * h[i].x + h[i].y * h[i].y;
+    }
+    const double hn2 = nw2 - hh;
+    const double hnl = hn2 > 0.0 ? sqrt(hn2) : 0.0;
+    const double ihn = (last && hnl > 0.0 && hnl < 1e300) ? 1.0 / hnl : 1.0;  // scaling by the reciprocal
     for (int e = e0 + (tid >> 3); e < e1; e += II_T / 8) {
-      const double2 x = ld_cg(Wp + (size_t)e * 8 + q);
-      Wp[(size_t)e * 8 + q] = make_double2(x.x * ihn, x.y * ihn);
+      double2 wv = ld_cg(Wp + (size_t)e * 8 + q);
+#pragma unroll
+      for (int i = 0; i < II_JREG; ++i)
+        if (i0 + i <= j) wv = csub(wv, cmul(h[i], V(i0 + i, e)));
+      Wp[(size_t)e * 8 + q] = make_double2(wv.x * ihn, wv.y * ihn);
     }
   }
+  const double hn2f = nw2 - hh;
+  const double hn = hn2f > 0.0 ? sqrt(hn2f) : 0.0;
+  const bool act = inst_active(p, job, nt, q);
   cbar();  // every thread has read the instance state before the owner updates it
   if (sl != 0) return;
   // owner of the (job, n-tile): stage the Hessenberg column h1 + h2 and the previous rotations of its 8
@@ -910,7 +917,8 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
     __syncthreads();
     for (int ph = tid; ph < p.op_nph + p.pre_nph; ph += II_TB) {
       const int* phd = ph < p.op_nph ? p.op_ph + ph : p.pre_ph + (ph - p.op_nph);
-      S.phcfg[ph] = (unsigned char)phase_config(S, J, phd[1] - phd[0], S.phw[ph], p.wmax, G);
+      S.phcfg[ph] = (unsigned char)phase_config(S, J, phd[1] - phd[0], S.phw[ph], p.wmax, G,
+                                                 p.ii_tilecost > 0 ? (float)p.ii_tilecost : 3000.0f);
     }
     __syncthreads();
   };
@@ -1048,7 +1056,7 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
     T.tick(4);
     gsync();
     T.tick(5);
-    // pass 2: w' = w - V h1 (stored), h2_i = vdot(V_i, w') -> area 1
+    // pass 2: w' = w - V h1 (stored), h2_i = vdot(V_i, w') and ||w'||^2 -> area 1
     for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
@@ -1057,21 +1065,12 @@ __global__ void __launch_bounds__(II_TB, 1) inner_items_kernel(const InnerParams
     T.tick(4);
     gsync();
     T.tick(5);
-    // pass 3: w'' = w' - V h2 (stored), ||w''||^2 -> area 2
+    // pass 3: V_{j+1} = (w' - V h2) / hn with hn^2 = ||w'||^2 - ||h2||^2; the Hessenberg column h1 + h2, hn and the
+    // Givens step of every active instance on the owner (slice 0) of its (job, n-tile)
     for (int v = b; tid < II_T && v < vs.nitem; v += G) {
       int jx, nt, sl;
       vitem(S, J, vs, v, jx, nt, sl);
       vec_item(p, S, 3, j, S.jjob[jx], nt, v, sl, vs.S, 4 * nIc * S.jw[jx]);
-    }
-    T.tick(4);
-    gsync();
-    T.tick(5);
-    // pass 4: hn = ||w''||, V_{j+1} = w'' / hn; the Hessenberg column h1 + h2, hn and the Givens step of
-    // every active instance on the owner (slice 0) of its (job, n-tile)
-    for (int v = b; tid < II_T && v < vs.nitem; v += G) {
-      int jx, nt, sl;
-      vitem(S, J, vs, v, jx, nt, sl);
-      vec_item(p, S, 4, j, S.jjob[jx], nt, v, sl, vs.S, 4 * nIc * S.jw[jx]);
     }
     T.tick(4);
     gsync();

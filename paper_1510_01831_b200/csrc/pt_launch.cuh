@@ -120,6 +120,7 @@ struct InnerParams {
   const int* pre_ph_px;
   int pre_nph_px, nitems_px;
   int ii_dbg;                // PT_II_DBG timing switches of inner_items.cu (results invalid when set)
+  int ii_tilecost;           // PT_II_TILECOST: fixed cycles per CTA tile in the tile-shape cost model (0 = 3000)
   int ii_trace;              // PT_II_TRACE: event trace of CTA (ii_trace - 1), thread 0
 };
 

@@ -880,6 +880,8 @@ static InnerParams inner_params(pt_ctx* c, Stage& S, int Ract, const SolveIO& io
   ip.part = c->ipart;
   ip.part_items = c->ipart_items;
   ip.ii_dbg = std::getenv("PT_II_DBG") ? atoi(std::getenv("PT_II_DBG")) : 0;
+  static const int tilecost = std::getenv("PT_II_TILECOST") ? atoi(std::getenv("PT_II_TILECOST")) : 0;
+  ip.ii_tilecost = tilecost;
   ip.ii_trace = std::getenv("PT_II_TRACE") ? atoi(std::getenv("PT_II_TRACE")) : 0;
   static const bool unit_major = std::getenv("PT_UNIT_MAJOR") != nullptr;
   ip.unit_major = unit_major;
