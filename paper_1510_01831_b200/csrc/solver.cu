@@ -175,6 +175,7 @@ struct pt_ctx {
   // outputs copied to the host while the reconstruction runs: side stream, events, pinned staging
   cudaStream_t side_st = nullptr;
   cudaEvent_t ev_tr = nullptr, ev_cp = nullptr;
+  int batch_cap = 0;       // RHS per lockstep batch on the item-program path (decided at the first solve)
   int* zflag_d = nullptr;  // [L][R] nonzero-source flags of the NEWTON stage (k_slab_flags)
   int zflag_cap = 0;
   // pt_solve on host buffers, several lockstep batches: the copies of batch b +- 1 run on io_st while batch b solves
@@ -2389,9 +2390,28 @@ static int batch_rhs(const pt_ctx* c) {
   const int maxj = std::max(std::max((int)c->op.jobs.size(), (int)c->newton.jobs.size()),
                             std::max((int)c->recon.jobs.size(), (int)c->refl.jobs.size()));
   if (c->Lc < 2 || maxj == 0) return 1 << 30;
-  // item programs (no dense inner operators): the multi-job stages run the all-RHS item kernel
-  // (inner_items.cu, up to 256 RHS per job), the single-job sweep stages the per-8-RHS-unit kernel
-  if (!c->dense_d && !c->lu_d && maxj <= 64 && !std::getenv("PT_ITEMS_V1")) return 64;
+  // item programs (no dense inner operators): every stage runs the all-RHS item kernel (inner_items.cu, up to
+  // 256 RHS per job).  The sweep stages are latency-bound, so a batch takes as many RHS as the kernel holds and
+  // the memory allows: 64 at least, then 128 / 192 / 256 while the per-RHS scratch (inner Krylov bases of the
+  // widest stage, stage panels and tables, staged wavefields) stays below 40 % of the free device memory seen at
+  // the first solve (PT_BATCH_RHS overrides).
+  if (!c->dense_d && !c->lu_d && maxj <= 64 && !std::getenv("PT_ITEMS_V1")) {
+    if (c->batch_cap <= 0) {
+      int b = 64;
+      if (const char* e = std::getenv("PT_BATCH_RHS")) {
+        b = std::max(8, std::min(256, atoi(e) / 8 * 8));
+      } else {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+          const double nmax = 4.0 * (c->Lc - 1) * c->wmax;
+          const double per = 1.25 * maxj * (c->inner_cap + 5) * nmax * 16.0 + 2.0 * 16.0 * c->wz * (double)c->wx;
+          while (b + 64 <= 256 && per * (b + 64) <= 0.4 * (double)free_b) b += 64;
+        }
+      }
+      const_cast<pt_ctx*>(c)->batch_cap = b;
+    }
+    return c->batch_cap;
+  }
   return 8 * std::max(1, inner_coop_max_units() / maxj);
 }
 

@@ -263,6 +263,8 @@ def test_single_source_matches_reference_fixture(fixture):
     ("cfg3", list(range(64))),
     # crosses the lockstep batch size and mixes far-apart sources
     ("cfg4", list(range(56)) + [63, 127, 255]),
+    # the whole 256-source set: one lockstep batch of 256 where the device memory allows (solver.cu batch_rhs)
+    ("cfg4", list(range(256))),
     ("cfg5", list(range(64))),
 ])
 def test_batched_sources_match_single_solves_and_fixtures(name, idx):
