@@ -2404,7 +2404,9 @@ static int batch_rhs(const pt_ctx* c) {
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
           const double nmax = 4.0 * (c->Lc - 1) * c->wmax;
-          const double per = 1.25 * maxj * (c->inner_cap + 5) * nmax * 16.0 + 2.0 * 16.0 * c->wz * (double)c->wx;
+          // inner Krylov bases sized for twice the default capacity (a capacity retry doubles them)
+          const double per = 1.25 * maxj * (std::max(c->inner_cap, 24) + 5) * nmax * 16.0 +
+                             2.0 * 16.0 * c->wz * (double)c->wx;
           while (b + 64 <= 256 && per * (b + 64) <= 0.4 * (double)free_b) b += 64;
         }
       }
