@@ -645,7 +645,7 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
   const int fuse_combine = tab != nullptr;
   const VecTab tabv = tab ? *tab : VecTab{};
   if (J == 0 || R == 0) return cudaSuccess;
-  if (R >= stage_gemm_min_cols())  // many RHS: the streaming tensor-core GEMM (stage_gemm.cu)
+  if (R >= stage_gemm_min_cols(0))  // the streaming tensor-core GEMM (stage_gemm.cu)
     return sample_gemm_launch(jobs, J, cells, layers, gsmp, tr, smp, R, Lc, wx, wmax, kmax, num_sms, st, tab, rmap);
   const int gy = (R + 7) / 8;
   // rows per cell <= kmax kept block rows x 4 output rows; one 8-row tile per warp
@@ -680,7 +680,7 @@ cudaError_t pass0_launch(const int* grp, int ngroups, const int* ljobs, const OJ
                          int R, int Lc, int wx, int wmax, int kmax, int max_jobs_per_layer, cudaStream_t st,
                          int accum, const VecTab* tab, const int* rmap, const RhsOut* rhs_out) {
   if (ngroups == 0 || R == 0) return cudaSuccess;
-  if (!tab && max_jobs_per_layer * R >= stage_gemm_min_cols()) {  // many columns: stage_gemm.cu
+  if (!tab && max_jobs_per_layer * R >= stage_gemm_min_cols(1)) {  // many columns: stage_gemm.cu
     static int nsm = 0;
     if (!nsm) {
       int dev = 0;

@@ -177,7 +177,7 @@ cudaError_t green_samples_launch(const OJob* jobs, int J, const CellInfo* cells,
                                  const int* rmap = nullptr);
 
 // many-RHS forms of the two products above as one streaming tensor-core GEMM kernel (stage_gemm.cu)
-int stage_gemm_min_cols();
+int stage_gemm_min_cols(int mode);  // mode 0: sampled response, 1: pass-0 product
 cudaError_t sample_gemm_launch(const OJob* jobs, int J, const CellInfo* cells, const LayerInfo* layers,
                                const double2* gsmp, const double2* tr, double2* smp, int R, int Lc, int wx, int wmax,
                                int kmax, int num_sms, cudaStream_t st, const VecTab* tab, const int* rmap);

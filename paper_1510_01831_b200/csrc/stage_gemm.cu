@@ -369,15 +369,19 @@ constexpr size_t sg_smem() {
 }
 static_assert(sg_smem<32>() <= 232448 && sg_smem<64>() <= 232448, "k_stage_gemm exceeds 227 KB of shared memory");
 
-// columns per product from which the streaming GEMM replaces the small-N kernels (PT_SGEMM_MIN; PT_NO_SGEMM)
-int stage_gemm_min_cols() {
-  static int v = -1;
-  if (v < 0) {
-    v = 32;
-    if (const char* e = std::getenv("PT_SGEMM_MIN")) v = std::max(1, atoi(e));
-    if (std::getenv("PT_NO_SGEMM")) v = 1 << 30;
+// columns per product from which the streaming GEMM replaces the small-N kernels: the sampled response from 1
+// (measured faster at every column count: cfg5 1 RHS 73 -> 51 ms per solve, 8 RHS 77 -> 58 ms; cfg3 1 RHS 11.2 ->
+// 9.7 ms), the pass-0 product from 32 (below, k_pass0's many small CTAs stream the operator faster: cfg5 1 RHS
+// 90 against 98 ms).  PT_SGEMM_MIN sets both; PT_NO_SGEMM keeps the small-N kernels everywhere.
+int stage_gemm_min_cols(int mode) {
+  static int v[2] = {-1, -1};
+  if (v[0] < 0) {
+    v[0] = 1;
+    v[1] = 32;
+    if (const char* e = std::getenv("PT_SGEMM_MIN")) v[0] = v[1] = std::max(1, atoi(e));
+    if (std::getenv("PT_NO_SGEMM")) v[0] = v[1] = 1 << 30;
   }
-  return v;
+  return v[mode ? 1 : 0];
 }
 
 template <int MODE>

@@ -59,6 +59,8 @@ SWITCHES = {
     # the many-RHS streaming GEMM of the pass-0 product and the sampled response for every column count
     "stage-gemm": {"PT_SGEMM_MIN": "1"},
     "stage-gemm-items": {"PT_SGEMM_MIN": "1", "PT_NO_DENSE": "1"},
+    # the round-1 small-N kernels of both products (the sampled response runs on the GEMM by default)
+    "small-n-kernels": {"PT_NO_SGEMM": "1"},
 }
 
 
