@@ -1180,8 +1180,10 @@ cudaError_t inner_items_launch(const InnerParams& p0, int J, cudaStream_t st) {
     return cudaErrorNotSupported;
   InnerParams p = p0;
   // single-job stages (the sequential outer sweeps): the scan form of the GS sweeps, 2 ceil(log2 nI) + 1
-  // phases per preconditioner application instead of 2 nI - 1 (PT_SCAN_MAXR: up to this many RHS, default all)
-  static const int scan_maxr = std::getenv("PT_SCAN_MAXR") ? atoi(std::getenv("PT_SCAN_MAXR")) : 1 << 30;
+  // phases per preconditioner application instead of 2 nI - 1, up to 128 RHS (PT_SCAN_MAXR): beyond, the phases of
+  // the sequential program are throughput-sized themselves and the scan's 1.7x flops cost more than its barriers
+  // save (cfg4, 256 RHS in one batch: 3449 ms sequential against 3548 ms; 128 RHS: 2022 against 1994 ms)
+  static const int scan_maxr = std::getenv("PT_SCAN_MAXR") ? atoi(std::getenv("PT_SCAN_MAXR")) : 128;
   if (J == 1 && p.pre_nph_px > 0 && p.items_px && p.R <= scan_maxr && p.nitems_px <= II_MAXIT) {
     p.items = p.items_px;
     p.pre_ph = p.pre_ph_px;
